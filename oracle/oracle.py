@@ -1,0 +1,192 @@
+"""CPU oracle for the Conv-LIF layer of arXiv 2603.13810 (TAC / TAC-TP / dense).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+module.  The product package ``paper_2603_13810_b200`` never imports it, and the
+two share no code: the arithmetic lives in ``oracle/tac_oracle.c`` (fp64, direct
+loops, see its header for the paper citations); this file is ctypes marshalling
+plus plain numpy reference implementations of the packed spike format (row a0 of
+SURVEY.md section 8, defined in include/tacsnn.h) and the OR-pool.
+
+Citations "P:n" are /root/reference/PAPER.md line n, "S:n" SPEC.md line n.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "tac_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+MODES = {"dense": 0, "tac": 1, "tactp": 2}
+RESETS = {"subtract": 0, "delayed": 1, "hard": 2}
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle/tac_oracle.c into oracle/liboracle.so (gcc, OpenMP)."""
+    if force or not os.path.exists(_LIB_PATH) or (
+            os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC)):
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared",
+                               "-std=c11", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            L = ctypes.CDLL(build())
+            P = ctypes.c_void_p
+            i, d = ctypes.c_int, ctypes.c_double
+            L.tac_oracle_forward.argtypes = [P, P, P] + [i] * 12 + [d, d, d, i] + \
+                [P, P, P, P, P, d, P, P]
+            L.tac_oracle_forward.restype = i
+            L.tac_oracle_conv2d.argtypes = [P, P, P] + [i] * 9 + [P]
+            L.tac_oracle_conv2d.restype = i
+            L.tac_oracle_or_pool2.argtypes = [P, i, i, i, i, P]
+            L.tac_oracle_or_pool2.restype = i
+            L.tac_oracle_threads.restype = i
+            _lib = L
+    return _lib
+
+
+def threads() -> int:
+    return int(lib().tac_oracle_threads())
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def out_hw(H, W, R=3, S=3, stride=1, pad=0):
+    return (H + 2 * pad - R) // stride + 1, (W + 2 * pad - S) // stride + 1
+
+
+def conv2d(X, Wt, bias=None, stride=1, pad=0):
+    """fp64 direct-loop cross-correlation.  X [B,Cin,H,W] -> [B,Cout,Ho,Wo]."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    Wt = np.ascontiguousarray(Wt, dtype=np.float32)
+    bias = None if bias is None else np.ascontiguousarray(bias, dtype=np.float32)
+    B, Cin, H, W = X.shape
+    Cout, _, R, S = Wt.shape
+    Ho, Wo = out_hw(H, W, R, S, stride, pad)
+    Y = np.empty((B, Cout, Ho, Wo), np.float64)
+    rc = lib().tac_oracle_conv2d(_ptr(X), _ptr(Wt), _ptr(bias), B, Cin, H, W, Cout,
+                                 R, S, stride, pad, _ptr(Y))
+    assert rc == 0
+    return Y
+
+
+def forward(S, Wt, bias=None, *, K=1, mode="tac", beta=0.9, v_th=1.0, v_reset=0.0,
+            reset="subtract", stride=1, pad=0, v_init=None, replay=None, band=1e-3):
+    """One Conv-LIF layer (Eq. 1 / Alg. 1 / Alg. 2) on u8 spikes S [T,B,Cin,H,W].
+
+    Returns dict(out u8 [T_out,B,Cout,Ho,Wo], v_final f64 [B,Cout,Ho,Wo],
+    counts i64 [B,Cout], mismatch, excused).  ``beta``/``v_th``/``v_reset`` are
+    rounded to fp32 first (the layer's parameters are fp32 in the ABI) and then
+    used in fp64.  With ``replay`` (device spikes, same layout as out) the
+    trajectory follows the replay protocol described in tac_oracle.c.
+    """
+    S = np.ascontiguousarray(S, dtype=np.uint8)
+    Wt = np.ascontiguousarray(Wt, dtype=np.float32)
+    bias = None if bias is None else np.ascontiguousarray(bias, dtype=np.float32)
+    T, B, Cin, H, W = S.shape
+    Cout, Cin2, R, Sk = Wt.shape
+    assert Cin2 == Cin
+    m = MODES[mode]
+    if m == 0:
+        K = 1
+    if T % K:
+        raise ValueError(f"K={K} does not divide T={T}")
+    Ho, Wo = out_hw(H, W, R, Sk, stride, pad)
+    T_out = T // K if m == 1 else T
+    out = np.empty((T_out, B, Cout, Ho, Wo), np.uint8)
+    v_final = np.empty((B, Cout, Ho, Wo), np.float64)
+    counts = np.empty((B, Cout), np.int64)
+    if v_init is not None:
+        v_init = np.ascontiguousarray(v_init, dtype=np.float64)
+        assert v_init.shape == (B, Cout, Ho, Wo)
+    if replay is not None:
+        replay = np.ascontiguousarray(replay, dtype=np.uint8)
+        assert replay.shape == out.shape, (replay.shape, out.shape)
+    mism = np.zeros(1, np.int64)
+    exc = np.zeros(1, np.int64)
+    f32 = lambda v: float(np.float32(v))
+    rc = lib().tac_oracle_forward(
+        _ptr(S), _ptr(Wt), _ptr(bias), T, B, Cin, H, W, Cout, R, Sk, stride, pad, K, m,
+        f32(beta), f32(v_th), f32(v_reset), RESETS[reset], _ptr(v_init), _ptr(out),
+        _ptr(v_final), _ptr(counts), _ptr(replay), float(band), _ptr(mism), _ptr(exc))
+    if rc != 0:
+        raise ValueError("tac_oracle_forward rejected its arguments")
+    return dict(out=out, v_final=v_final, counts=counts, mismatch=int(mism[0]),
+                excused=int(exc[0]))
+
+
+def or_pool2(x):
+    """2x2 OR-pool of binary maps (P:235 MaxPool(2) on {0,1}); x [..., C, H, W]."""
+    x = np.ascontiguousarray(x, dtype=np.uint8)
+    *lead, C, H, W = x.shape
+    N = int(np.prod(lead)) if lead else 1
+    y = np.empty((*lead, C, H // 2, W // 2), np.uint8)
+    rc = lib().tac_oracle_or_pool2(_ptr(x), N, C, H, W, _ptr(y))
+    if rc != 0:
+        raise ValueError("odd extent for 2x2 pool")
+    return y
+
+
+# ---------------------------------------------------------------------------
+# Packed spike format (include/tacsnn.h, "Packed spike layout"), numpy reference.
+# u32 [T][B][H][WPR], WPR = ceil(W*C/32); bit (t,b,c,y,x) lives at row offset
+# r = x*C + c: word r>>5, bit r&31 (LSB first); pad bits are zero.
+# ---------------------------------------------------------------------------
+def words_per_row(W, C):
+    return (W * C + 31) // 32
+
+
+def pack_spikes(dense):
+    """u8 {0,1} [T,B,C,H,W] -> u32 [T,B,H,WPR]."""
+    dense = np.asarray(dense, dtype=np.uint8)
+    T, B, C, H, W = dense.shape
+    wpr = words_per_row(W, C)
+    rows = dense.transpose(0, 1, 3, 4, 2).reshape(T, B, H, W * C)
+    padded = np.zeros((T, B, H, wpr * 32), np.uint8)
+    padded[..., :W * C] = rows
+    by = np.packbits(padded, axis=-1, bitorder="little")
+    return np.ascontiguousarray(by).view("<u4").reshape(T, B, H, wpr)
+
+
+def unpack_spikes(packed, C, W):
+    """u32 [T,B,H,WPR] -> u8 [T,B,C,H,W] (inverse of pack_spikes)."""
+    packed = np.ascontiguousarray(packed, dtype="<u4")
+    T, B, H, wpr = packed.shape
+    bits = np.unpackbits(packed.view(np.uint8).reshape(T, B, H, wpr * 4), axis=-1,
+                         bitorder="little")[..., :W * C]
+    return np.ascontiguousarray(bits.reshape(T, B, H, W, C).transpose(0, 1, 4, 2, 3))
+
+
+def group_count(T, K, mode):
+    """Conv calls of one layer: G = T/K (Alg. 1/2), T for dense (Eq. 1)."""
+    return T if mode == "dense" else T // K
+
+
+def temporal_extents(T, Ks, modes):
+    """Per-layer input extents and total conv calls of a stacked net (App. B,
+    P:470-483): TAC divides the running extent by K_l, TAC-TP / dense keep it."""
+    ext, calls, t = [], 0, T
+    for K, mode in zip(Ks, modes):
+        if mode != "dense" and t % K:
+            raise ValueError(f"extent {t} not divisible by K={K}")
+        ext.append(t)
+        calls += group_count(t, K, mode)
+        if mode == "tac":
+            t //= K
+    return ext, calls, t

@@ -1,0 +1,210 @@
+/*
+ * tac_oracle.c -- plain, slow, obviously-correct CPU oracle for the Conv-LIF
+ * layer of arXiv 2603.13810 (TAC / TAC-TP) and its per-timestep baseline.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * The product path (paper_2603_13810_b200/) never links, loads or calls it,
+ * and this file shares no code, header, table or constant with that path.
+ *
+ * Precision: every value is fp64 (inputs are the fp32 weights / beta / v_th the
+ * caller passes, promoted).  Layout is the paper's: spikes S in
+ * {0,1}^{T x B x C x H x W}, time outermost (Alg. 1 "Require").
+ *
+ * Citations "P:n" are /root/reference/PAPER.md line n, "S:n" SPEC.md line n.
+ *
+ *   conv      : Y[b,co,y,x] = bias[co] + sum_{ci,r,s} W[co,ci,r,s] *
+ *               X[b,ci,y*stride+r-pad, x*stride+s-pad]   (zero outside)
+ *               -- cross-correlation with zero padding, S:51-55 (conv2d post);
+ *               "W * S_t" of Eq. (1).
+ *   dense     : Eq. (1): for t<T: V <- beta V + conv(S_t); spike; reset
+ *   TAC       : Algorithm 1, P:135-150:
+ *               A_k = sum_{j<K} beta^{K-1-j} S_{kK+j}      (Def. TAC)
+ *               Y_k = Conv2d(A_k, W)                        (Alg.1 l.4)
+ *               V <- beta^K V + Y_k ; S_k = Theta(V - V_th) ; V <- V - S_k V_th
+ *   TAC-TP    : Algorithm 2: same A_k, Y_k; then K times
+ *               V <- beta V + Y_k ; S_{kK+j} = Theta(V - V_th) ; V <- V - S V_th
+ *
+ * Readings:
+ *   R1 reset: SUBTRACT is Alg.1/2 (immediate, then decayed); DELAYED is Eq. (1) /
+ *      App. A (V_t = beta V_{t-1} + I_t - V_th S_{t-1}); HARD sets V = v_reset.
+ *   R2 Theta(0) = 1: fire when V >= V_th ("fire at exact threshold").
+ *   R3 bias added once per conv call (folded BN).
+ *   R4 DELAYED at call start: s_prev = [v_init >= v_th] (0 when v_init = 0).
+ *   R5 v_final = V after the last step (post-reset for SUBTRACT/HARD).
+ *
+ * Replay (parity protocol): when `replay` (device spikes, same
+ * layout as `out`) is given, each threshold decision inside the band
+ * |V - v_th| <= band takes the device spike (excused); outside it the oracle's
+ * own decision is used and compared with the device spike (mismatch).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+enum { OR_MODE_DENSE = 0, OR_MODE_TAC = 1, OR_MODE_TACTP = 2 };
+enum { OR_RESET_SUBTRACT = 0, OR_RESET_DELAYED = 1, OR_RESET_HARD = 2 };
+
+int tac_oracle_abi(void) { return 1; }
+
+int tac_oracle_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+/* Direct-loop 2-D cross-correlation of ONE sample.
+ * X [Cin][H][W], Wt [Cout][Cin][R][S], bias [Cout] or NULL, Y [Cout][Ho][Wo]. */
+static void conv_one(const double *X, const float *Wt, const float *bias,
+                     int Cin, int H, int W, int Cout, int R, int S,
+                     int stride, int pad, int Ho, int Wo, double *Y) {
+  for (int co = 0; co < Cout; ++co)
+    for (int y = 0; y < Ho; ++y)
+      for (int x = 0; x < Wo; ++x) {
+        double acc = bias ? (double)bias[co] : 0.0;
+        for (int ci = 0; ci < Cin; ++ci)
+          for (int r = 0; r < R; ++r) {
+            int yi = y * stride + r - pad;
+            if (yi < 0 || yi >= H) continue;
+            for (int s = 0; s < S; ++s) {
+              int xi = x * stride + s - pad;
+              if (xi < 0 || xi >= W) continue;
+              acc += (double)Wt[((size_t)(co * Cin + ci) * R + r) * S + s] *
+                     X[((size_t)ci * H + yi) * W + xi];
+            }
+          }
+        Y[((size_t)co * Ho + y) * Wo + x] = acc;
+      }
+}
+
+/* Batched conv exposed for the linearity / library pins (P4, P5).
+ * X [B][Cin][H][W] fp64, Y [B][Cout][Ho][Wo] fp64. */
+int tac_oracle_conv2d(const double *X, const float *Wt, const float *bias,
+                      int B, int Cin, int H, int W, int Cout, int R, int S,
+                      int stride, int pad, double *Y) {
+  int Ho = (H + 2 * pad - R) / stride + 1, Wo = (W + 2 * pad - S) / stride + 1;
+  if (Ho < 1 || Wo < 1) return -1;
+  for (int b = 0; b < B; ++b)
+    conv_one(X + (size_t)b * Cin * H * W, Wt, bias, Cin, H, W, Cout, R, S,
+             stride, pad, Ho, Wo, Y + (size_t)b * Cout * Ho * Wo);
+  return 0;
+}
+
+/* One LIF step of one neuron.  decay = beta (dense, TAC-TP) or beta^K (TAC).
+ * Returns the spike; updates *V and *s_prev.  Replay semantics documented above. */
+static int lif_step(double *V, int *s_prev, double I, double decay, double v_th,
+                    double v_reset, int reset, const uint8_t *dev, double band,
+                    int64_t *mismatch, int64_t *excused) {
+  double v = decay * (*V) + I;                       /* Alg.1 l.5 / Alg.2 l.6 */
+  if (reset == OR_RESET_DELAYED) v -= v_th * (double)(*s_prev); /* Eq. (1) */
+  int s = (v >= v_th) ? 1 : 0;                       /* Theta, R2 */
+  if (dev) {
+    int d = *dev ? 1 : 0;
+    if (fabs(v - v_th) <= band) {
+      s = d;
+      ++*excused;
+    } else if (s != d) {
+      ++*mismatch;
+    }
+  }
+  if (reset == OR_RESET_SUBTRACT) v -= (double)s * v_th; /* Alg.1 l.7 */
+  else if (reset == OR_RESET_HARD) { if (s) v = v_reset; }
+  *s_prev = s;
+  *V = v;
+  return s;
+}
+
+/*
+ * Full layer forward.
+ *   S        : u8 [T][B][Cin][H][W] in {0,1}
+ *   Wt, bias : fp32 [Cout][Cin][R][S], [Cout] or NULL
+ *   v_init   : fp64 [B][Cout][Ho][Wo] or NULL (=> 0, "Initialize V <- 0", Alg.1 l.1)
+ *   out      : u8 [T_out][B][Cout][Ho][Wo], T_out = T/K (TAC) else T
+ *   v_final  : fp64 [B][Cout][Ho][Wo] or NULL
+ *   counts   : int64 [B][Cout] or NULL  (sum over t, y, x of out)
+ *   replay   : u8, same layout as out, or NULL
+ *   mismatch/excused : int64 scalars (may be NULL when replay is NULL)
+ * Returns 0, or -1 on a bad argument (K not dividing T, etc.).
+ */
+int tac_oracle_forward(const uint8_t *S, const float *Wt, const float *bias,
+                       int T, int B, int Cin, int H, int W, int Cout, int R,
+                       int Sk, int stride, int pad, int K, int mode,
+                       double beta, double v_th, double v_reset, int reset,
+                       const double *v_init, uint8_t *out, double *v_final,
+                       int64_t *counts, const uint8_t *replay, double band,
+                       int64_t *mismatch_out, int64_t *excused_out) {
+  if (mode == OR_MODE_DENSE) K = 1;
+  if (K < 1 || T < 1 || T % K != 0) return -1;
+  int Ho = (H + 2 * pad - R) / stride + 1, Wo = (W + 2 * pad - Sk) / stride + 1;
+  if (Ho < 1 || Wo < 1) return -1;
+  const int G = T / K;
+  const int T_out = (mode == OR_MODE_TAC) ? G : T;
+  const size_t nin = (size_t)Cin * H * W, nout = (size_t)Cout * Ho * Wo;
+  int64_t mism = 0, exc = 0;
+
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : mism, exc)
+  for (int b = 0; b < B; ++b) {
+    double *A = (double *)malloc(nin * sizeof(double));
+    double *Y = (double *)malloc(nout * sizeof(double));
+    double *V = (double *)malloc(nout * sizeof(double));
+    int *sp = (int *)malloc(nout * sizeof(int));
+    for (size_t n = 0; n < nout; ++n) {
+      V[n] = v_init ? v_init[(size_t)b * nout + n] : 0.0;
+      sp[n] = (reset == OR_RESET_DELAYED && V[n] >= v_th) ? 1 : 0; /* R4 */
+    }
+    if (counts) for (int co = 0; co < Cout; ++co) counts[(size_t)b * Cout + co] = 0;
+
+    for (int k = 0; k < G; ++k) {
+      /* A_k = sum_{j=0}^{K-1} beta^{K-1-j} S_{kK+j}.  Dense: A = S_t. */
+      for (size_t i = 0; i < nin; ++i) A[i] = 0.0;
+      for (int j = 0; j < K; ++j) {
+        double wj = pow(beta, (double)(K - 1 - j));
+        const uint8_t *St = S + ((size_t)(k * K + j) * B + b) * nin;
+        for (size_t i = 0; i < nin; ++i) A[i] += wj * (double)St[i];
+      }
+      /* Y_k = Conv2d(A_k, W): one conv call per group (Alg.1 l.4, Alg.2 l.4). */
+      conv_one(A, Wt, bias, Cin, H, W, Cout, R, Sk, stride, pad, Ho, Wo, Y);
+
+      int nsteps = (mode == OR_MODE_TACTP) ? K : 1;
+      double decay = (mode == OR_MODE_TAC) ? pow(beta, (double)K) : beta;
+      for (int j = 0; j < nsteps; ++j) {
+        int t_out = (mode == OR_MODE_TAC) ? k : k * K + j;
+        size_t ob = ((size_t)t_out * B + b) * nout;
+        for (size_t n = 0; n < nout; ++n) {
+          int s = lif_step(&V[n], &sp[n], Y[n], decay, v_th, v_reset, reset,
+                           replay ? replay + ob + n : NULL, band, &mism, &exc);
+          out[ob + n] = (uint8_t)s;
+          if (counts && s) counts[(size_t)b * Cout + n / ((size_t)Ho * Wo)] += 1;
+        }
+      }
+    }
+    if (v_final) memcpy(v_final + (size_t)b * nout, V, nout * sizeof(double));
+    free(A); free(Y); free(V); free(sp);
+  }
+  (void)T_out;
+  if (mismatch_out) *mismatch_out = mism;
+  if (excused_out) *excused_out = exc;
+  return 0;
+}
+
+/* 2x2 stride-2 OR pool of binary maps (= max-pool of {0,1}, "MaxPool(2)").
+ * in u8 [N][C][H][W] -> out u8 [N][C][H/2][W/2]; H, W even. */
+int tac_oracle_or_pool2(const uint8_t *in, int N, int C, int H, int W, uint8_t *out) {
+  if (H % 2 || W % 2) return -1;
+  int Hp = H / 2, Wp = W / 2;
+  for (int n = 0; n < N; ++n)
+    for (int c = 0; c < C; ++c)
+      for (int y = 0; y < Hp; ++y)
+        for (int x = 0; x < Wp; ++x) {
+          const uint8_t *p = in + (((size_t)n * C + c) * H + 2 * y) * W + 2 * x;
+          out[(((size_t)n * C + c) * Hp + y) * Wp + x] =
+              (uint8_t)((p[0] | p[1] | p[W] | p[W + 1]) ? 1 : 0);
+        }
+  return 0;
+}
