@@ -1,0 +1,396 @@
+#!/usr/bin/env python
+"""Benchmark of the Conv-LIF hot path (arXiv 2603.13810, TAC / TAC-TP / dense).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--mode tactp]
+                    [--K 4] [--impl ours|reference] [--no-cpu-baseline]
+    torchrun --nproc-per-node N bench.py --gpus N ...       (one rank per GPU)
+
+A step is one forward pass of the config's whole Conv-LIF stack (every row of
+SURVEY.md section 8(a): aggregation, per-group conv, LIF, packed/pool/counts
+outputs) over the rank's batch shard, followed by the NCCL all_gather of the
+final-layer spikes and spike counts (the only collective, north_star).
+Default workload: BASELINE config C5 (DVS128-shaped, 5 conv blocks, T=32, K=4,
+batch 2048 sharded across the ranks, TAC-TP).  Metric: spike-frames/s at the
+network input (B*T input frames per step), whole job.  Rank 0 prints ONE JSON
+line.  `--impl reference` times the CPU oracle (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Conv-LIF spike-frames/s (dense/TAC/TAC-TP) at 1/8 B200; % tensor-pipe peak"
+UNIT = "spike-frames/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--mode", default=None, help="dense | tac | tactp (default: config's)")
+    ap.add_argument("--K", type=int, default=None)
+    ap.add_argument("--B", type=int, default=None, help="global batch (default: config's)")
+    ap.add_argument("--engine", default="auto")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's global batch is sharded; weak: B per rank")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-T", type=int, default=8)
+    ap.add_argument("--layer-detail", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers --
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return dict(hbm=d["hbm_gbs"], bf16=d["bf16_tflops"],
+                    bf16_sustained=d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                    sm_max_mhz=d.get("sm_max_mhz", 1965.0), source="measured")
+    # fallback stated in /opt/skills/guides/B200_PROFILING.md
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sustained=1400.0, sm_max_mhz=1965.0,
+                source="fallback")
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clock and throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def useful_flops_per_sample(specs):
+    """Algorithmic conv FLOPs per sample of one forward: 2*Cout*H'W'*Cin*R*S per
+    conv call, G = T/K calls per layer."""
+    out = []
+    for s in specs:
+        hc, wc = s.conv_hw
+        G = s.T // (1 if s.mode == "dense" else s.K)
+        out.append(2.0 * s.C_out * hc * wc * s.C_in * s.R * s.S * G)
+    return out
+
+
+def algorithmic_bytes_per_sample(specs):
+    """Packed spike bytes in + out per sample of one forward (no v_final)."""
+    out = []
+    for s in specs:
+        T_out, Ho, Wo, wpr = s.out_shape()
+        out.append(4.0 * (s.T * s.H * s.in_words_per_row + T_out * Ho * wpr) + 4.0 * s.C_out)
+    return out
+
+
+# --------------------------------------------------------------- CPU oracle --
+def time_oracle(cfg, specs, weights, B, T_sample):
+    """Run the oracle over the stack on a bounded sample; returns (seconds, frames)."""
+    from oracle import oracle as O
+    from paper_2603_13810_b200 import configs
+    S = configs.make_inputs(cfg, B=B, T=T_sample).numpy()
+    t0 = time.perf_counter()
+    x = S
+    t = T_sample
+    for spec, (w, b) in zip(specs, weights):
+        K = 1 if spec.mode == "dense" else min(spec.K, t)
+        r = O.forward(x, w.numpy(), b.numpy(), K=K, mode=spec.mode, beta=spec.beta,
+                      v_th=spec.v_th, reset=spec.reset, pad=spec.pad)
+        x = O.or_pool2(r["out"]) if spec.out_pool == 2 else r["out"]
+        if spec.mode == "tac":
+            t //= K
+    return time.perf_counter() - t0, B * T_sample
+
+
+def cpu_baseline(cfg, specs, weights, T_sample):
+    from oracle import oracle as O
+    thr = O.threads()
+    B = max(1, min(thr, cfg.B))
+    K = specs[0].K if specs[0].mode != "dense" else 1
+    T_sample = max(K, (T_sample // K) * K)
+    dt, frames = time_oracle(cfg, specs, weights, B, T_sample)
+    return {"value": frames / dt, "unit": UNIT, "cores": thr, "kind": "oracle",
+            "sample": f"{cfg.name} stack, {B} samples x T={T_sample} (fp64 C oracle, OpenMP "
+                      f"over samples), {dt:.1f} s"}
+
+
+# --------------------------------------------------------------- reference --
+def run_reference(a, cfg, specs_fn, rank, world):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2603_13810_b200 import configs
+    specs = specs_fn(1)
+    weights = configs.layer_weights(cfg)
+    thr = O.threads()
+    B = max(1, min(thr, cfg.B))
+    K = specs[0].K if specs[0].mode != "dense" else 1
+    T_sample = K if specs[0].mode != "dense" else 1
+    for _ in range(a.warmup):
+        time_oracle(cfg, specs, weights, B, T_sample)
+    times = []
+    for _ in range(a.steps):
+        dt, frames = time_oracle(cfg, specs, weights, B, T_sample)
+        times.append(dt)
+    tot = sum(times)
+    value = frames * a.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True,
+            "scaling": a.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "description": cfg.description,
+                       "mode": specs[0].mode, "K": specs[0].K, "global_batch": cfg.B,
+                       "T": cfg.T, "sample_batch": B, "sample_T": T_sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle",
+                             "sample": f"{B} samples x T={T_sample} per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------------- ours --
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    from paper_2603_13810_b200 import configs
+    cfg = configs.CONFIGS[a.config]
+    B_global = a.B or cfg.B
+    if a.scaling == "weak":
+        B_global = B_global * world
+
+    def specs_fn(B):
+        return configs.layer_plan(cfg, mode=a.mode, K=a.K, B=B, engine=a.engine)
+
+    if a.impl == "reference":
+        return run_reference(a, cfg, specs_fn, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2603_13810_b200 import network, tacsnn
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    assert B_global % world == 0, "global batch must divide across ranks"
+    B = B_global // world
+    b0 = rank * B
+    specs = specs_fn(B)
+    weights = configs.layer_weights(cfg)
+    net = network.Network(specs, weights, device=dev)
+    engines = net.engines()
+
+    # inputs resident in HBM (larger than the 126 MB L2 for C5: no L2 flush needed)
+    x_u8 = configs.make_inputs(cfg, B=B, b0=b0, device=dev)
+    x = tacsnn.pack(x_u8)
+    del x_u8
+    T_out, Ho, Wo, wpr = specs[-1].out_shape()
+    gather_spk = torch.empty((world,) + (T_out, B, Ho, wpr), dtype=torch.int32, device=dev) \
+        if world > 1 else None
+    gather_cnt = torch.empty((world, B, specs[-1].C_out), dtype=torch.int32, device=dev) \
+        if world > 1 else None
+
+    def step(xin):
+        y, counts, _, _ = net.forward(xin)
+        if world > 1:
+            dist.all_gather_into_tensor(gather_spk.view(-1), y.contiguous().view(-1))
+            dist.all_gather_into_tensor(gather_cnt.view(-1), counts[-1].contiguous().view(-1))
+        return y, counts
+
+    launches_per_step = net.count_launches(x)
+    for _ in range(a.warmup):
+        step(x)
+    torch.cuda.synchronize()
+
+    # per-layer event timing inside the timed region (events on the launch stream)
+    stream = torch.cuda.current_stream(dev)
+    nL = len(specs)
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(nL)] for _ in range(a.steps)]
+
+    def step_timed(i, xin):
+        B_ = xin.shape[1]
+        cnt = None
+        for li, (spec, prep) in enumerate(zip(net.specs, net.prepared)):
+            s = spec if spec.B == B_ else spec.replace(B=B_)
+            ev[i][li][0].record(stream)
+            xin, _, cnt = tacsnn.conv_lif(s, prep, xin)
+            ev[i][li][1].record(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gather_spk.view(-1), xin.contiguous().view(-1))
+            dist.all_gather_into_tensor(gather_cnt.view(-1), cnt.contiguous().view(-1))
+        return xin
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(a.steps):
+        step_timed(i, x)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms_local = t_start.elapsed_time(t_end)
+    ms_t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_total = float(ms_t.item())
+    ms_per_step = ms_total / a.steps
+    layer_ms = [statistics.mean(ev[i][li][0].elapsed_time(ev[i][li][1]) for i in range(a.steps))
+                for li in range(nL)]
+
+    frames_per_step = B_global * cfg.T
+    value = frames_per_step / (ms_per_step / 1e3)
+
+    # ---------------- end to end: pinned host input -> device -> counts back
+    e2e = None
+    if not a.no_e2e:
+        host_x = torch.empty(x.shape, dtype=torch.int32, pin_memory=True)
+        host_x.copy_(x)
+        dev_x = torch.empty_like(x)
+        host_cnt = torch.empty((B, specs[-1].C_out), dtype=torch.int32, pin_memory=True)
+        for _ in range(2):
+            dev_x.copy_(host_x, non_blocking=True)
+            _, c = step(dev_x)
+            host_cnt.copy_(c[-1], non_blocking=True)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.steps):
+            dev_x.copy_(host_x, non_blocking=True)
+            _, c = step(dev_x)
+            host_cnt.copy_(c[-1], non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": frames_per_step / (float(e_ms.item()) / a.steps / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(host_x.numel() * 4 * world),
+               "d2h_bytes_per_step": int(host_cnt.numel() * 4 * world)}
+        del host_x, dev_x
+
+    # ---------------- roofline of the dominant kernel (per-layer launch)
+    peaks = load_peaks()
+    flops = useful_flops_per_sample(specs)
+    bytes_ = algorithmic_bytes_per_sample(specs)
+    dom = max(range(nL), key=lambda li: layer_ms[li])
+    dspec = specs[dom]
+    dur_s = layer_ms[dom] / 1e3
+    if engines[dom] == "tcgen05":
+        # int8 MMA (kind::i8): peak = measured bf16 x nominal int8:bf16 ratio (4.5/2.25)
+        peak = (peaks["bf16_sustained"] if a.steps * ms_per_step > 2000 else peaks["bf16"]) * 2.0
+        roof = {"bound": "tensor", "achieved": flops[dom] * B / dur_s / 1e12, "peak": peak,
+                "unit": "TFLOP/s"}
+        roof["peak_note"] = (f"int8 tcgen05 peak = {peaks['source']} bf16 x 2 (nominal "
+                             f"4.5/2.25); achieved counts useful conv FLOPs only")
+    else:
+        # SIMT fp32 FFMA: 148 SMs x 128 lanes x 2 FLOP x sm clock
+        sm_mhz = (clk or {}).get("sm_mhz") or peaks["sm_max_mhz"]
+        peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+        roof = {"bound": "alu", "achieved": flops[dom] * B / dur_s / 1e12, "peak": peak,
+                "unit": "TFLOP/s", "peak_note": "fp32 FFMA: 148 SM x 128 lanes x 2 x SM clock"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel"] = f"layer {dom} ({dspec.C_in}->{dspec.C_out} @{dspec.H}x{dspec.W}, {engines[dom]})"
+    roof["hbm_achieved_gbs"] = bytes_[dom] * B / dur_s / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, specs, weights, a.cpu_sample_T)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None,
+            "dtype": "u8xi8->i32 (tcgen05) / f32 (LIF)" if "tcgen05" in engines else "f32",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "description": cfg.description,
+                       "mode": specs[0].mode, "K": specs[0].K, "global_batch": B_global,
+                       "per_rank_batch": B, "T": cfg.T, "parallelism": f"dp{world}",
+                       "layers": len(specs), "engines": engines,
+                       "l2": "inputs+activations > 126 MB L2 (no flush needed)"},
+            "clocks": clk,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * a.steps,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "layers": [{"layer": li, "engine": engines[li], "ms": layer_ms[li],
+                        "useful_tflops": flops[li] * B / (layer_ms[li] / 1e3) / 1e12,
+                        "packed_gbs": bytes_[li] * B / (layer_ms[li] / 1e3) / 1e9,
+                        "frames_per_s": B * specs[li].T / (layer_ms[li] / 1e3)}
+                       for li in range(nL)],
+            "peaks": peaks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,172 @@
+/*
+ * tacsnn.h -- C ABI of libtacsnn: the Conv-LIF layer of arXiv 2603.13810
+ * ("TAC: Temporal Aggregated Convolution") on NVIDIA B200 (sm_100a).
+ *
+ * One call runs ONE spiking convolutional layer over a whole spike sequence:
+ *
+ *   dense  (mode 0)  Eq. (1), PAPER.md:101-105 -- T conv calls:
+ *            V_t = beta V_{t-1} + W*S_t + b ; s_t = [V_t >= v_th] ; reset
+ *   TAC    (mode 1)  Algorithm 1, PAPER.md:135-150 -- T/K conv calls, T/K outputs:
+ *            A_k = sum_{j<K} beta^{K-1-j} S_{kK+j}         (Definition)
+ *            Y_k = W*A_k + b ; V = beta^K V + Y_k ; s_k = [V >= v_th] ; reset
+ *   TAC-TP (mode 2)  Algorithm 2, PAPER.md:170-187 -- T/K conv calls, T outputs:
+ *            same A_k, Y_k ; then K times: V = beta V + Y_k ; s = [V >= v_th] ; reset
+ *
+ * "W*X" is the 2-D cross-correlation with zero padding,
+ * W [C_out][C_in][R][S], stride `stride`, padding `pad`; the bias b is added once
+ * per conv call (folded inference BatchNorm; R3).
+ * Reset forms (R1): SUBTRACT V -= s v_th right after spiking
+ * (Alg. 1 l.7 / Alg. 2 l.8, the default); SUBTRACT_DELAYED subtracts
+ * v_th s_{t-1} at the next update (Eq. (1), App. A);
+ * HARD sets V = v_reset on a spike.  Threshold ties fire.
+ *
+ * ---------------------------------------------------------------------------
+ * Packed spike layout (inputs and outputs), "tac-packed-v1":
+ *   u32 words [T][B][H][WPR], WPR = ceil(W*C/32).  The bit of spike
+ *   (t, b, c, y, x) is at row offset r = x*C + c: word r>>5, bit r&31 (LSB
+ *   first).  Bits past W*C in the last word of a row are zero.  Rows are packed
+ *   (row stride WPR); the t and b strides are explicit (in words) so batch
+ *   shards are zero-copy views; 0 means the packed default (B*H*WPR, H*WPR).
+ *   tac_pack_spikes / tac_unpack_spikes convert from/to u8 {0,1} [T][B][C][H][W]
+ *   (the paper's layout, Alg. 1 "Require").
+ * Output spikes use the same layout with C = C_out, (H, W) = the layer output
+ *   extent -- after the optional fused 2x2 OR-pool (= MaxPool(2) of binary
+ *   spikes) when out_pool = 2.  T_out = T/K for TAC, else T.
+ * v_init / v_final: fp32 [B][H'][W'][C_out] (channels last, PRE-pool extent
+ *   H' = (H+2 pad-R)/stride+1), contiguous.  v_final is V after the last step
+ *   (post-reset for SUBTRACT / HARD; R5).  NULL v_init means V=0
+ *   (Alg. 1 l.1); with SUBTRACT_DELAYED the pending reset at call start is
+ *   [v_init >= v_th] (R4), so chained calls equal one long call.
+ * counts: u32 [B][C_out] = sum over output steps and PRE-pool pixels of the
+ *   spikes (the spike-count readout).
+ *
+ * ---------------------------------------------------------------------------
+ * Conventions for every function:
+ *  - Ownership: the caller allocates every buffer (device memory unless a
+ *    parameter says host); the library never allocates device memory and keeps
+ *    no reference to any buffer after the call returns.
+ *  - Ordering: device work is enqueued on `stream` (a cudaStream_t passed as
+ *    void*; NULL = legacy default stream) and is asynchronous; results are valid
+ *    when the stream reaches the call.  No implicit device synchronisation,
+ *    except tac_prepare_weights which copies host data synchronously.
+ *  - Errors: all argument checks run on the host before anything is launched
+ *    and return a status; on error nothing is launched and outputs are
+ *    untouched.  A failed launch returns TAC_ERR_CUDA.  tac_last_error_detail()
+ *    (thread-local) names the offending argument.  No C++ exception crosses
+ *    this ABI.  Asynchronous device faults surface at the caller's next sync.
+ *  - Thread safety: no global mutable state besides the thread-local detail
+ *    string and launch counter; distinct calls may run concurrently.
+ */
+#ifndef TACSNN_H_
+#define TACSNN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TACSNN_ABI_VERSION 1
+
+typedef enum { TAC_MODE_DENSE = 0, TAC_MODE_TAC = 1, TAC_MODE_TACTP = 2 } tac_mode;
+
+typedef enum {
+  TAC_RESET_SUBTRACT = 0,         /* Alg. 1 l.7 / Alg. 2 l.8 (default)            */
+  TAC_RESET_SUBTRACT_DELAYED = 1, /* Eq. (1): V_t = bV_{t-1} + I_t - v_th s_{t-1} */
+  TAC_RESET_HARD = 2              /* V = v_reset on spike                         */
+} tac_reset;
+
+typedef enum {
+  TAC_ENGINE_AUTO = 0,    /* TCGEN05 when the layer qualifies, else SIMT        */
+  TAC_ENGINE_SIMT = 1,    /* fp32 FFMA direct conv + LIF; any R/S/stride/pad/K  */
+  TAC_ENGINE_TCGEN05 = 2  /* fused tcgen05/TMEM implicit GEMM   */
+} tac_engine;
+
+typedef enum {
+  TAC_OK = 0,
+  TAC_ERR_NULL = 1,             /* a required pointer is NULL                   */
+  TAC_ERR_SHAPE = 2,            /* non-positive extent, H' < 1, odd pooled extent */
+  TAC_ERR_K_NOT_DIVIDING_T = 3, /* K < 1 or T % K != 0 */
+  TAC_ERR_PARAM = 4,            /* beta not in (0,1), v_th <= 0, bad enum        */
+  TAC_ERR_NONFINITE = 5,        /* non-finite weight, bias, beta, v_th, v_reset  */
+  TAC_ERR_ALIGN = 6,            /* pointer / stride alignment                    */
+  TAC_ERR_UNSUPPORTED = 7,      /* layer outside the requested engine's envelope */
+  TAC_ERR_WORKSPACE = 8,        /* buffer smaller than required                  */
+  TAC_ERR_CUDA = 9              /* CUDA runtime error (detail has the text)      */
+} tac_status;
+
+/* Layer descriptor (host struct, passed by pointer to every call). */
+typedef struct tac_conv_lif_desc {
+  int32_t T, B, C_in, H, W;         /* logical input spikes [T][B][C_in][H][W]      */
+  int32_t C_out, R, S, stride, pad; /* kernel [C_out][C_in][R][S]                   */
+  int32_t K;                        /* group size; ignored (=1) for DENSE           */
+  int32_t mode;                     /* tac_mode                                     */
+  float beta;                       /* membrane decay, 0 < beta < 1  */
+  float v_th;                       /* threshold > 0                                */
+  float v_reset;                    /* HARD reset value                             */
+  int32_t reset;                    /* tac_reset                                    */
+  int32_t out_pool;                 /* 1 = none, 2 = fused 2x2 OR-pool (even H', W') */
+  int32_t engine;                   /* tac_engine                                   */
+  int64_t in_stride_t, in_stride_b; /* u32 words; 0 = packed default               */
+  int64_t out_stride_t, out_stride_b;
+} tac_conv_lif_desc;
+
+/* Validate a descriptor (no device access).  TAC_OK or the first violation. */
+tac_status tac_desc_check(const tac_conv_lif_desc *desc);
+
+/* Output geometry: T_out, output (pooled) H_o, W_o and words per output row. */
+tac_status tac_out_shape(const tac_conv_lif_desc *desc, int32_t *T_out,
+                         int32_t *H_out, int32_t *W_out, int32_t *out_words_per_row);
+
+/* Engine a call with this descriptor runs on (resolves AUTO); -1 if invalid or
+ * if an explicitly requested engine cannot run the layer. */
+int32_t tac_select_engine(const tac_conv_lif_desc *desc);
+
+/* Size in bytes of the prepared-weights device buffer for this descriptor. */
+tac_status tac_weights_bytes(const tac_conv_lif_desc *desc, size_t *bytes);
+
+/* Prepare weights once per (desc, W, b): validates finiteness,
+ * builds every engine's device format and copies it into `prepared` (device,
+ * >= tac_weights_bytes, 256-B aligned).  weight: HOST fp32 [C_out][C_in][R][S];
+ * bias: HOST fp32 [C_out] or NULL (= 0).  Synchronous host->device copy. */
+tac_status tac_prepare_weights(const tac_conv_lif_desc *desc, const float *weight,
+                               const float *bias, void *prepared, size_t bytes,
+                               void *stream);
+
+/* Workspace bytes tac_conv_lif_forward needs (may be 0). */
+tac_status tac_workspace_bytes(const tac_conv_lif_desc *desc, size_t *bytes);
+
+/* The layer (one call = whole sequence, all groups).
+ *   prepared   device, from tac_prepare_weights with an identical desc
+ *   spikes_in  device u32, packed layout above (16-B aligned for TCGEN05)
+ *   v_init     device fp32 [B][H'][W'][C_out] or NULL (= 0)
+ *   spikes_out device u32, packed, T_out x B x H_o x WPR_out (with strides)
+ *   v_final    device fp32 [B][H'][W'][C_out] or NULL (not written)
+ *   counts     device u32 [B][C_out] or NULL (overwritten, not accumulated)
+ *   ws         device workspace of ws_bytes >= tac_workspace_bytes (or NULL if 0)
+ * spikes_out must not alias spikes_in. */
+tac_status tac_conv_lif_forward(const tac_conv_lif_desc *desc, const void *prepared,
+                                const uint32_t *spikes_in, const float *v_init,
+                                uint32_t *spikes_out, float *v_final,
+                                uint32_t *counts, void *ws, size_t ws_bytes,
+                                void *stream);
+
+/* u8 {0,1} [T][B][C][H][W] (device) <-> packed [T][B][H][WPR] (device).
+ * pack treats any non-zero byte as a spike. */
+tac_status tac_pack_spikes(const uint8_t *dense01, uint32_t *packed, int32_t T,
+                           int32_t B, int32_t C, int32_t H, int32_t W, void *stream);
+tac_status tac_unpack_spikes(const uint32_t *packed, uint8_t *dense01, int32_t T,
+                             int32_t B, int32_t C, int32_t H, int32_t W, void *stream);
+
+const char *tac_status_string(tac_status status);
+const char *tac_last_error_detail(void); /* thread-local; "" when none */
+int32_t tac_abi_version(void);           /* TACSNN_ABI_VERSION */
+/* Device kernels launched by this thread's most recent successful
+ * tac_conv_lif_forward / tac_pack_spikes / tac_unpack_spikes call. */
+int32_t tac_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TACSNN_H_ */

@@ -1,0 +1,325 @@
+// abi.cu -- host side of libtacsnn: the C ABI declared in include/tacsnn.h.
+// Validation, weight preparation, engine selection and launch on the caller's
+// stream.  No device allocation; no exception crosses the ABI.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tacsnn.h"
+#include "layer.cuh"
+#include "tc.cuh"
+
+namespace {
+
+thread_local std::string g_detail;
+thread_local int g_launches = 0;
+
+tac_status fail(tac_status st, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+tac_status fail(tac_status st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_detail = buf;
+  return st;
+}
+
+struct Geo {
+  int Ho, Wo, Hq, Wq, G, T_out, nsteps, wpr_in, wpr_out, K;
+  long long in_st, in_sb, out_st, out_sb;
+};
+
+tac_status check(const tac_conv_lif_desc *d, Geo *g) {
+  if (!d) return fail(TAC_ERR_NULL, "desc is NULL");
+  if (d->T < 1) return fail(TAC_ERR_SHAPE, "T=%d < 1", d->T);
+  if (d->B < 1) return fail(TAC_ERR_SHAPE, "B=%d < 1", d->B);
+  if (d->C_in < 1) return fail(TAC_ERR_SHAPE, "C_in=%d < 1", d->C_in);
+  if (d->H < 1 || d->W < 1) return fail(TAC_ERR_SHAPE, "H=%d, W=%d must be >= 1", d->H, d->W);
+  if (d->C_out < 1) return fail(TAC_ERR_SHAPE, "C_out=%d < 1", d->C_out);
+  if (d->R < 1 || d->S < 1) return fail(TAC_ERR_SHAPE, "R=%d, S=%d must be >= 1", d->R, d->S);
+  if (d->stride < 1) return fail(TAC_ERR_SHAPE, "stride=%d < 1", d->stride);
+  if (d->pad < 0) return fail(TAC_ERR_SHAPE, "pad=%d < 0", d->pad);
+  if (d->mode < 0 || d->mode > 2) return fail(TAC_ERR_PARAM, "mode=%d not in {0,1,2}", d->mode);
+  if (d->reset < 0 || d->reset > 2) return fail(TAC_ERR_PARAM, "reset=%d not in {0,1,2}", d->reset);
+  if (d->engine < 0 || d->engine > 2) return fail(TAC_ERR_PARAM, "engine=%d not in {0,1,2}", d->engine);
+  if (d->out_pool != 1 && d->out_pool != 2)
+    return fail(TAC_ERR_PARAM, "out_pool=%d not in {1,2}", d->out_pool);
+  if (!std::isfinite(d->beta)) return fail(TAC_ERR_NONFINITE, "beta is not finite");
+  if (!std::isfinite(d->v_th)) return fail(TAC_ERR_NONFINITE, "v_th is not finite");
+  if (!std::isfinite(d->v_reset)) return fail(TAC_ERR_NONFINITE, "v_reset is not finite");
+  if (!(d->beta > 0.f && d->beta < 1.f))
+    return fail(TAC_ERR_PARAM, "beta=%g not in (0,1) (PAPER.md:105)", (double)d->beta);
+  if (!(d->v_th > 0.f)) return fail(TAC_ERR_PARAM, "v_th=%g must be > 0", (double)d->v_th);
+  const int K = d->mode == TAC_MODE_DENSE ? 1 : d->K;
+  if (K < 1 || d->T % K != 0)
+    return fail(TAC_ERR_K_NOT_DIVIDING_T, "K=%d must be >= 1 and divide T=%d (PAPER.md:444)",
+                d->K, d->T);
+  if (K > tacsnn::kMaxK) return fail(TAC_ERR_UNSUPPORTED, "K=%d > %d", K, tacsnn::kMaxK);
+  const int Ho = (d->H + 2 * d->pad - d->R) / d->stride + 1;
+  const int Wo = (d->W + 2 * d->pad - d->S) / d->stride + 1;
+  if (d->H + 2 * d->pad < d->R || Ho < 1)
+    return fail(TAC_ERR_SHAPE, "output height H'=(H+2pad-R)/stride+1 < 1");
+  if (d->W + 2 * d->pad < d->S || Wo < 1)
+    return fail(TAC_ERR_SHAPE, "output width W'=(W+2pad-S)/stride+1 < 1");
+  if (d->out_pool == 2 && (Ho % 2 || Wo % 2))
+    return fail(TAC_ERR_SHAPE, "out_pool=2 needs even H'=%d, W'=%d", Ho, Wo);
+  if ((long long)d->W * d->C_in > (1LL << 30) || (long long)Wo * d->C_out > (1LL << 30))
+    return fail(TAC_ERR_SHAPE, "row too wide");
+  if (d->in_stride_t < 0 || d->in_stride_b < 0 || d->out_stride_t < 0 || d->out_stride_b < 0)
+    return fail(TAC_ERR_SHAPE, "negative stride");
+  g->K = K;
+  g->Ho = Ho;
+  g->Wo = Wo;
+  g->Hq = d->out_pool == 2 ? Ho / 2 : Ho;
+  g->Wq = d->out_pool == 2 ? Wo / 2 : Wo;
+  g->G = d->T / K;
+  g->T_out = d->mode == TAC_MODE_TAC ? g->G : d->T;
+  g->nsteps = d->mode == TAC_MODE_TACTP ? K : 1;
+  g->wpr_in = (d->W * d->C_in + 31) / 32;
+  g->wpr_out = (g->Wq * d->C_out + 31) / 32;
+  const long long in_plane = (long long)d->H * g->wpr_in;
+  const long long out_plane = (long long)g->Hq * g->wpr_out;
+  g->in_sb = d->in_stride_b ? d->in_stride_b : in_plane;
+  g->in_st = d->in_stride_t ? d->in_stride_t : in_plane * d->B;
+  g->out_sb = d->out_stride_b ? d->out_stride_b : out_plane;
+  g->out_st = d->out_stride_t ? d->out_stride_t : out_plane * d->B;
+  if (g->in_sb < in_plane) return fail(TAC_ERR_SHAPE, "in_stride_b < H*WPR");
+  if (g->out_sb < out_plane) return fail(TAC_ERR_SHAPE, "out_stride_b < H_o*WPR_out");
+  return TAC_OK;
+}
+
+// Prepared-weights buffer layout (device):
+//   [0, simt_bytes)             SIMT fp32 weights [Cin][R][S][Cout]
+//   [bias_off, +4*Cout)         fp32 bias
+//   [tc_off, +tc bytes)         tcgen05 image (tc.cuh), when the shape qualifies
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct PrepLayout {
+  size_t simt_off, bias_off, tc_off, tc_bytes, total;
+};
+
+PrepLayout prep_layout(const tac_conv_lif_desc *d) {
+  PrepLayout L{};
+  L.simt_off = 0;
+  L.bias_off = align256((size_t)d->C_in * d->R * d->S * d->C_out * 4);
+  L.tc_off = align256(L.bias_off + (size_t)d->C_out * 4);
+  L.tc_bytes = tacsnn::tc_shape_ok(d) ? tacsnn::tc_weights_bytes(d) : 0;
+  L.total = align256(L.tc_off + L.tc_bytes);
+  return L;
+}
+
+bool is_device_ptr(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int resolve_engine(const tac_conv_lif_desc *d) {
+  const bool tc = tacsnn::tc_supported(d);
+  if (d->engine == TAC_ENGINE_SIMT) return TAC_ENGINE_SIMT;
+  if (d->engine == TAC_ENGINE_TCGEN05) return tc ? TAC_ENGINE_TCGEN05 : -1;
+  return tc ? TAC_ENGINE_TCGEN05 : TAC_ENGINE_SIMT;
+}
+
+}  // namespace
+
+extern "C" {
+
+tac_status tac_desc_check(const tac_conv_lif_desc *desc) {
+  g_detail.clear();
+  Geo g;
+  return check(desc, &g);
+}
+
+tac_status tac_out_shape(const tac_conv_lif_desc *desc, int32_t *T_out, int32_t *H_out,
+                         int32_t *W_out, int32_t *wpr) {
+  g_detail.clear();
+  Geo g;
+  tac_status st = check(desc, &g);
+  if (st != TAC_OK) return st;
+  if (T_out) *T_out = g.T_out;
+  if (H_out) *H_out = g.Hq;
+  if (W_out) *W_out = g.Wq;
+  if (wpr) *wpr = g.wpr_out;
+  return TAC_OK;
+}
+
+int32_t tac_select_engine(const tac_conv_lif_desc *desc) {
+  g_detail.clear();
+  Geo g;
+  if (check(desc, &g) != TAC_OK) return -1;
+  return resolve_engine(desc);
+}
+
+tac_status tac_weights_bytes(const tac_conv_lif_desc *desc, size_t *bytes) {
+  g_detail.clear();
+  Geo g;
+  tac_status st = check(desc, &g);
+  if (st != TAC_OK) return st;
+  if (!bytes) return fail(TAC_ERR_NULL, "bytes is NULL");
+  *bytes = prep_layout(desc).total;
+  return TAC_OK;
+}
+
+tac_status tac_workspace_bytes(const tac_conv_lif_desc *desc, size_t *bytes) {
+  g_detail.clear();
+  Geo g;
+  tac_status st = check(desc, &g);
+  if (st != TAC_OK) return st;
+  if (!bytes) return fail(TAC_ERR_NULL, "bytes is NULL");
+  *bytes = 0;
+  return TAC_OK;
+}
+
+tac_status tac_prepare_weights(const tac_conv_lif_desc *desc, const float *weight,
+                               const float *bias, void *prepared, size_t bytes,
+                               void *stream) {
+  g_detail.clear();
+  Geo g;
+  tac_status st = check(desc, &g);
+  if (st != TAC_OK) return st;
+  if (!weight) return fail(TAC_ERR_NULL, "weight is NULL");
+  if (!prepared) return fail(TAC_ERR_NULL, "prepared is NULL");
+  const PrepLayout L = prep_layout(desc);
+  if (bytes < L.total) return fail(TAC_ERR_WORKSPACE, "prepared buffer %zu < %zu bytes", bytes, L.total);
+  if ((uintptr_t)prepared % 256) return fail(TAC_ERR_ALIGN, "prepared must be 256-B aligned");
+  if (!is_device_ptr(prepared)) return fail(TAC_ERR_PARAM, "prepared is not device memory");
+  const int Co = desc->C_out, Ci = desc->C_in, R = desc->R, S = desc->S;
+  const size_t nw = (size_t)Co * Ci * R * S;
+  for (size_t i = 0; i < nw; ++i)
+    if (!std::isfinite(weight[i])) return fail(TAC_ERR_NONFINITE, "weight[%zu] is not finite", i);
+  if (bias)
+    for (int i = 0; i < Co; ++i)
+      if (!std::isfinite(bias[i])) return fail(TAC_ERR_NONFINITE, "bias[%d] is not finite", i);
+  std::vector<unsigned char> img(L.total, 0);
+  float *ws = reinterpret_cast<float *>(img.data() + L.simt_off);
+  for (int co = 0; co < Co; ++co)
+    for (int ci = 0; ci < Ci; ++ci)
+      for (int r = 0; r < R; ++r)
+        for (int s = 0; s < S; ++s)
+          ws[((size_t)(ci * R + r) * S + s) * Co + co] = weight[((size_t)(co * Ci + ci) * R + r) * S + s];
+  float *bs = reinterpret_cast<float *>(img.data() + L.bias_off);
+  for (int co = 0; co < Co; ++co) bs[co] = bias ? bias[co] : 0.f;
+  if (L.tc_bytes) tacsnn::tc_prepare(desc, weight, bias, img.data() + L.tc_off);
+  cudaError_t e = cudaMemcpyAsync(prepared, img.data(), L.total, cudaMemcpyHostToDevice,
+                                  (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(TAC_ERR_CUDA, "prepare copy: %s", cudaGetErrorString(e));
+  return TAC_OK;
+}
+
+tac_status tac_conv_lif_forward(const tac_conv_lif_desc *desc, const void *prepared,
+                                const uint32_t *spikes_in, const float *v_init,
+                                uint32_t *spikes_out, float *v_final, uint32_t *counts,
+                                void *ws, size_t ws_bytes, void *stream) {
+  g_detail.clear();
+  Geo g;
+  tac_status st = check(desc, &g);
+  if (st != TAC_OK) return st;
+  if (!prepared) return fail(TAC_ERR_NULL, "prepared is NULL");
+  if (!spikes_in) return fail(TAC_ERR_NULL, "spikes_in is NULL");
+  if (!spikes_out) return fail(TAC_ERR_NULL, "spikes_out is NULL");
+  (void)ws;
+  (void)ws_bytes;
+  const int engine = resolve_engine(desc);
+  if (engine < 0)
+    return fail(TAC_ERR_UNSUPPORTED, "engine TCGEN05 cannot run this layer: %s",
+                tacsnn::tc_unsupported_reason(desc));
+  if ((uintptr_t)spikes_in % 4 || (uintptr_t)spikes_out % 4 || (uintptr_t)prepared % 256)
+    return fail(TAC_ERR_ALIGN, "misaligned pointer");
+  if (engine == TAC_ENGINE_TCGEN05 && ((uintptr_t)spikes_in % 16 || (uintptr_t)spikes_out % 16 ||
+                                       g.in_sb % 4 || g.in_st % 4 || g.out_sb % 4 || g.out_st % 4))
+    return fail(TAC_ERR_ALIGN, "TCGEN05 needs 16-B aligned spike buffers and strides");
+  if (v_init && (uintptr_t)v_init % 16) return fail(TAC_ERR_ALIGN, "v_init must be 16-B aligned");
+  if (v_final && (uintptr_t)v_final % 16) return fail(TAC_ERR_ALIGN, "v_final must be 16-B aligned");
+  if (counts && (uintptr_t)counts % 4) return fail(TAC_ERR_ALIGN, "counts misaligned");
+  const void *dev_ptrs[] = {prepared, spikes_in, spikes_out, v_init, v_final, counts};
+  const char *names[] = {"prepared", "spikes_in", "spikes_out", "v_init", "v_final", "counts"};
+  for (int i = 0; i < 6; ++i)
+    if (dev_ptrs[i] && !is_device_ptr(dev_ptrs[i]))
+      return fail(TAC_ERR_PARAM, "%s is not device memory", names[i]);
+
+  tacsnn::LayerParams p{};
+  p.T = desc->T; p.B = desc->B; p.Cin = desc->C_in; p.H = desc->H; p.W = desc->W;
+  p.Cout = desc->C_out; p.R = desc->R; p.S = desc->S; p.stride = desc->stride; p.pad = desc->pad;
+  p.K = g.K; p.mode = desc->mode; p.reset = desc->reset; p.pool = desc->out_pool;
+  p.Ho = g.Ho; p.Wo = g.Wo; p.Hq = g.Hq; p.Wq = g.Wq; p.G = g.G; p.nsteps = g.nsteps;
+  p.T_out = g.T_out; p.wpr_in = g.wpr_in; p.wpr_out = g.wpr_out;
+  p.in_st = g.in_st; p.in_sb = g.in_sb; p.out_st = g.out_st; p.out_sb = g.out_sb;
+  p.v_th = desc->v_th; p.v_reset = desc->v_reset;
+  const double beta = (double)desc->beta;
+  p.decay = (float)(desc->mode == TAC_MODE_TAC ? std::pow(beta, (double)g.K) : beta);
+  for (int j = 0; j < g.K; ++j) p.coef[j] = (float)std::pow(beta, (double)(g.K - 1 - j));
+  p.in = spikes_in; p.out = spikes_out; p.v_init = v_init; p.v_final = v_final; p.counts = counts;
+  const PrepLayout L = prep_layout(desc);
+  const unsigned char *base = static_cast<const unsigned char *>(prepared);
+  p.w = reinterpret_cast<const float *>(base + L.simt_off);
+  p.bias = reinterpret_cast<const float *>(base + L.bias_off);
+
+  int launches = 0;
+  int err = 0;
+  if (engine == TAC_ENGINE_TCGEN05) {
+    err = tacsnn::tc_launch(desc, p, base + L.tc_off, stream, &launches);
+  } else {
+    err = tacsnn::launch_zero_outputs(p, stream, &launches);
+    if (!err) err = tacsnn::launch_simt_conv_lif(p, stream, &launches);
+  }
+  if (err) return fail(TAC_ERR_CUDA, "launch failed: %s", cudaGetErrorString((cudaError_t)err));
+  g_launches = launches;
+  return TAC_OK;
+}
+
+tac_status tac_pack_spikes(const uint8_t *dense01, uint32_t *packed, int32_t T, int32_t B,
+                           int32_t C, int32_t H, int32_t W, void *stream) {
+  g_detail.clear();
+  if (!dense01 || !packed) return fail(TAC_ERR_NULL, "NULL buffer");
+  if (T < 1 || B < 1 || C < 1 || H < 1 || W < 1) return fail(TAC_ERR_SHAPE, "extent < 1");
+  if ((uintptr_t)packed % 4) return fail(TAC_ERR_ALIGN, "packed misaligned");
+  int e = tacsnn::launch_pack(dense01, packed, T, B, C, H, W, stream);
+  if (e) return fail(TAC_ERR_CUDA, "pack: %s", cudaGetErrorString((cudaError_t)e));
+  g_launches = 1;
+  return TAC_OK;
+}
+
+tac_status tac_unpack_spikes(const uint32_t *packed, uint8_t *dense01, int32_t T, int32_t B,
+                             int32_t C, int32_t H, int32_t W, void *stream) {
+  g_detail.clear();
+  if (!dense01 || !packed) return fail(TAC_ERR_NULL, "NULL buffer");
+  if (T < 1 || B < 1 || C < 1 || H < 1 || W < 1) return fail(TAC_ERR_SHAPE, "extent < 1");
+  if ((uintptr_t)packed % 4) return fail(TAC_ERR_ALIGN, "packed misaligned");
+  int e = tacsnn::launch_unpack(packed, dense01, T, B, C, H, W, stream);
+  if (e) return fail(TAC_ERR_CUDA, "unpack: %s", cudaGetErrorString((cudaError_t)e));
+  g_launches = 1;
+  return TAC_OK;
+}
+
+const char *tac_status_string(tac_status s) {
+  switch (s) {
+    case TAC_OK: return "TAC_OK";
+    case TAC_ERR_NULL: return "TAC_ERR_NULL";
+    case TAC_ERR_SHAPE: return "TAC_ERR_SHAPE";
+    case TAC_ERR_K_NOT_DIVIDING_T: return "TAC_ERR_K_NOT_DIVIDING_T";
+    case TAC_ERR_PARAM: return "TAC_ERR_PARAM";
+    case TAC_ERR_NONFINITE: return "TAC_ERR_NONFINITE";
+    case TAC_ERR_ALIGN: return "TAC_ERR_ALIGN";
+    case TAC_ERR_UNSUPPORTED: return "TAC_ERR_UNSUPPORTED";
+    case TAC_ERR_WORKSPACE: return "TAC_ERR_WORKSPACE";
+    case TAC_ERR_CUDA: return "TAC_ERR_CUDA";
+  }
+  return "TAC_ERR_UNKNOWN";
+}
+
+const char *tac_last_error_detail(void) { return g_detail.c_str(); }
+int32_t tac_abi_version(void) { return TACSNN_ABI_VERSION; }
+int32_t tac_last_launch_count(void) { return g_launches; }
+
+}  // extern "C"

@@ -1,0 +1,22 @@
+// tc.cuh -- the tcgen05 engine of libtacsnn (fused aggregation + tcgen05/TMEM
+// implicit-GEMM conv + LIF epilogue).  See tc.cu and DESIGN.md.
+#pragma once
+#include <cstddef>
+
+#include "../../include/tacsnn.h"
+#include "layer.cuh"
+
+namespace tacsnn {
+
+// Shape envelope of the tcgen05 kernel (independent of beta / K / mode).
+bool tc_shape_ok(const tac_conv_lif_desc *d);
+// Full envelope (shape + exactness of the integer aggregate for beta, K, mode).
+bool tc_supported(const tac_conv_lif_desc *d);
+const char *tc_unsupported_reason(const tac_conv_lif_desc *d);
+size_t tc_weights_bytes(const tac_conv_lif_desc *d);
+void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bias,
+                unsigned char *dst);
+int tc_launch(const tac_conv_lif_desc *d, const LayerParams &p, const unsigned char *tc_prep,
+              void *stream, int *launches);
+
+}  // namespace tacsnn

@@ -1,0 +1,55 @@
+"""A stack of Conv-LIF layers run through libtacsnn, one ABI call per layer.
+
+The spike tensors stay packed and resident in HBM between layers; each layer's
+fused 2x2 OR-pool output is the next layer's input.  Batch shards are plain
+views (the ABI takes the T and B strides), so the multi-GPU driver just hands
+each rank its slice.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import tacsnn
+from .tacsnn import LayerSpec
+
+
+class Network:
+    def __init__(self, specs: list[LayerSpec], weights, device="cuda"):
+        assert len(specs) == len(weights)
+        self.specs = list(specs)
+        self.device = torch.device(device)
+        self.prepared = [tacsnn.prepare_weights(s, w, b, device=self.device)
+                         for s, (w, b) in zip(self.specs, weights)]
+
+    def engines(self):
+        return [s.engine_used() for s in self.specs]
+
+    def forward(self, x: torch.Tensor, keep: bool = False, want_v_final: bool = False,
+                want_counts: bool = True):
+        """x: packed int32 [T, B, H, WPR] on the device.  Returns (final spikes,
+        per-layer counts, per-layer outputs if keep, per-layer v_final if asked)."""
+        B = x.shape[1]
+        counts, outs, vfs = [], [], []
+        for spec, prep in zip(self.specs, self.prepared):
+            s = spec if spec.B == B else spec.replace(B=B)
+            x, vf, cnt = tacsnn.conv_lif(s, prep, x, want_v_final=want_v_final,
+                                         want_counts=want_counts)
+            counts.append(cnt)
+            vfs.append(vf)
+            if keep:
+                outs.append(x)
+        return x, counts, outs, vfs
+
+    def launches_per_forward(self) -> int:
+        """Kernels one forward launches (measured from the library's counter)."""
+        return self._launches
+
+    def count_launches(self, x):
+        n = 0
+        B = x.shape[1]
+        for spec, prep in zip(self.specs, self.prepared):
+            s = spec if spec.B == B else spec.replace(B=B)
+            x, _, _ = tacsnn.conv_lif(s, prep, x)
+            n += tacsnn.last_launch_count()
+        self._launches = n
+        return n

@@ -1,0 +1,225 @@
+"""Python binding of libtacsnn (include/tacsnn.h) -- argument marshalling only.
+
+Every step of the Conv-LIF path runs in the library's CUDA kernels; this module
+turns torch tensors into device pointers / strides and the current CUDA stream
+into the ``stream`` argument.  There is no fallback: if ``libtacsnn.so`` is
+missing or a call returns a non-OK status, a RuntimeError is raised.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+import threading
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libtacsnn.so")
+
+MODES = {"dense": 0, "tac": 1, "tactp": 2}
+RESETS = {"subtract": 0, "delayed": 1, "hard": 2}
+ENGINES = {"auto": 0, "simt": 1, "tcgen05": 2}
+ENGINE_NAMES = {v: k for k, v in ENGINES.items()}
+
+EXPORTS = ("tac_desc_check", "tac_out_shape", "tac_select_engine", "tac_weights_bytes",
+           "tac_prepare_weights", "tac_workspace_bytes", "tac_conv_lif_forward",
+           "tac_pack_spikes", "tac_unpack_spikes", "tac_status_string",
+           "tac_last_error_detail", "tac_abi_version", "tac_last_launch_count")
+
+
+class Desc(ctypes.Structure):
+    """Mirror of tac_conv_lif_desc."""
+    _fields_ = [(n, ctypes.c_int32) for n in ("T", "B", "C_in", "H", "W", "C_out", "R", "S",
+                                               "stride", "pad", "K", "mode")] + \
+               [("beta", ctypes.c_float), ("v_th", ctypes.c_float), ("v_reset", ctypes.c_float),
+                ("reset", ctypes.c_int32), ("out_pool", ctypes.c_int32), ("engine", ctypes.c_int32),
+                ("in_stride_t", ctypes.c_int64), ("in_stride_b", ctypes.c_int64),
+                ("out_stride_t", ctypes.c_int64), ("out_stride_b", ctypes.c_int64)]
+
+
+_lock = threading.Lock()
+_L = None
+
+
+def lib():
+    """Load libtacsnn.so (built by ``python -m paper_2603_13810_b200.build``)."""
+    global _L
+    with _lock:
+        if _L is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(f"libtacsnn.so not found at {LIB_PATH}; build it with "
+                                   "`python -m paper_2603_13810_b200.build` (no CPU fallback)")
+            L = ctypes.CDLL(LIB_PATH)
+            P, i32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t
+            D = ctypes.POINTER(Desc)
+            sig = {
+                "tac_desc_check": ([D], i32),
+                "tac_out_shape": ([D, P, P, P, P], i32),
+                "tac_select_engine": ([D], i32),
+                "tac_weights_bytes": ([D, ctypes.POINTER(sz)], i32),
+                "tac_prepare_weights": ([D, P, P, P, sz, P], i32),
+                "tac_workspace_bytes": ([D, ctypes.POINTER(sz)], i32),
+                "tac_conv_lif_forward": ([D, P, P, P, P, P, P, P, sz, P], i32),
+                "tac_pack_spikes": ([P, P, i32, i32, i32, i32, i32, P], i32),
+                "tac_unpack_spikes": ([P, P, i32, i32, i32, i32, i32, P], i32),
+                "tac_status_string": ([i32], ctypes.c_char_p),
+                "tac_last_error_detail": ([], ctypes.c_char_p),
+                "tac_abi_version": ([], i32),
+                "tac_last_launch_count": ([], i32),
+            }
+            for name, (args, res) in sig.items():
+                f = getattr(L, name)
+                f.argtypes, f.restype = args, res
+            _L = L
+    return _L
+
+
+def _check(status):
+    if status != 0:
+        L = lib()
+        raise RuntimeError(f"{L.tac_status_string(status).decode()}: "
+                           f"{L.tac_last_error_detail().decode()}")
+
+
+@dataclasses.dataclass(frozen=True)
+class LayerSpec:
+    """One Conv-LIF layer (include/tacsnn.h tac_conv_lif_desc)."""
+    T: int
+    B: int
+    C_in: int
+    H: int
+    W: int
+    C_out: int
+    R: int = 3
+    S: int = 3
+    stride: int = 1
+    pad: int = 0
+    K: int = 1
+    mode: str = "tac"
+    beta: float = 0.9
+    v_th: float = 1.0
+    v_reset: float = 0.0
+    reset: str = "subtract"
+    out_pool: int = 1
+    engine: str = "auto"
+
+    def replace(self, **kw) -> "LayerSpec":
+        return dataclasses.replace(self, **kw)
+
+    def desc(self, in_strides=(0, 0), out_strides=(0, 0)) -> Desc:
+        return Desc(self.T, self.B, self.C_in, self.H, self.W, self.C_out, self.R, self.S,
+                    self.stride, self.pad, 1 if self.mode == "dense" else self.K,
+                    MODES[self.mode], self.beta, self.v_th, self.v_reset, RESETS[self.reset],
+                    self.out_pool, ENGINES[self.engine], in_strides[0], in_strides[1],
+                    out_strides[0], out_strides[1])
+
+    @property
+    def conv_hw(self):
+        return ((self.H + 2 * self.pad - self.R) // self.stride + 1,
+                (self.W + 2 * self.pad - self.S) // self.stride + 1)
+
+    @property
+    def in_words_per_row(self):
+        return (self.W * self.C_in + 31) // 32
+
+    def out_shape(self):
+        """(T_out, H_o, W_o, words_per_row) of the packed output."""
+        vals = [ctypes.c_int32() for _ in range(4)]
+        d = self.desc()
+        _check(lib().tac_out_shape(ctypes.byref(d), *[ctypes.byref(v) for v in vals]))
+        return tuple(v.value for v in vals)
+
+    def engine_used(self) -> str:
+        d = self.desc()
+        e = lib().tac_select_engine(ctypes.byref(d))
+        if e < 0:
+            _check(lib().tac_desc_check(ctypes.byref(d)))
+            raise RuntimeError("requested engine cannot run this layer")
+        return ENGINE_NAMES[e]
+
+    def check(self):
+        d = self.desc()
+        _check(lib().tac_desc_check(ctypes.byref(d)))
+
+
+def _stream(device=None):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def prepare_weights(spec: LayerSpec, weight: torch.Tensor, bias: torch.Tensor | None = None,
+                    device="cuda") -> torch.Tensor:
+    """Build the device prepared-weights buffer (tac_prepare_weights)."""
+    d = spec.desc()
+    nbytes = ctypes.c_size_t()
+    _check(lib().tac_weights_bytes(ctypes.byref(d), ctypes.byref(nbytes)))
+    w = weight.detach().to("cpu", torch.float32).contiguous()
+    assert tuple(w.shape) == (spec.C_out, spec.C_in, spec.R, spec.S), w.shape
+    b = None if bias is None else bias.detach().to("cpu", torch.float32).contiguous()
+    buf = torch.empty(nbytes.value + 256, dtype=torch.uint8, device=device)
+    off = (-buf.data_ptr()) % 256
+    prep = buf[off:off + nbytes.value]
+    _check(lib().tac_prepare_weights(ctypes.byref(d), _ptr(w), _ptr(b), _ptr(prep),
+                                     nbytes.value, _stream(prep.device)))
+    return prep
+
+
+def conv_lif(spec: LayerSpec, prepared: torch.Tensor, x: torch.Tensor, *, v_init=None,
+             want_v_final=False, want_counts=True, out: torch.Tensor | None = None):
+    """Run one layer (tac_conv_lif_forward) on the current stream.
+
+    x: int32/uint32-bit packed spikes [T, B, H, WPR] (rows contiguous; T and B
+    strides taken from the tensor).  Returns (spikes_out [T_out,B,H_o,WPR_out]
+    int32, v_final [B,H',W',C_out] fp32 or None, counts [B,C_out] int32 or None).
+    """
+    assert x.is_cuda and x.dtype == torch.int32 and x.dim() == 4
+    assert x.stride(3) == 1 and x.stride(2) == spec.in_words_per_row, "rows must be packed"
+    T_out, Ho, Wo, wpr = spec.out_shape()
+    if out is None:
+        out = torch.empty((T_out, spec.B, Ho, wpr), dtype=torch.int32, device=x.device)
+    assert tuple(out.shape) == (T_out, spec.B, Ho, wpr) and out.stride(3) == 1 and out.stride(2) == wpr
+    hc, wc = spec.conv_hw
+    v_final = torch.empty((spec.B, hc, wc, spec.C_out), dtype=torch.float32,
+                          device=x.device) if want_v_final else None
+    counts = torch.empty((spec.B, spec.C_out), dtype=torch.int32,
+                         device=x.device) if want_counts else None
+    if v_init is not None:
+        assert v_init.is_cuda and v_init.dtype == torch.float32 and v_init.is_contiguous()
+        assert tuple(v_init.shape) == (spec.B, hc, wc, spec.C_out)
+    d = spec.desc((x.stride(0), x.stride(1)), (out.stride(0), out.stride(1)))
+    _check(lib().tac_conv_lif_forward(ctypes.byref(d), _ptr(prepared), _ptr(x), _ptr(v_init),
+                                      _ptr(out), _ptr(v_final), _ptr(counts), None, 0,
+                                      _stream(x.device)))
+    return out, v_final, counts
+
+
+def pack(dense: torch.Tensor) -> torch.Tensor:
+    """u8 {0,1} [T,B,C,H,W] (cuda) -> packed int32 [T,B,H,WPR] (tac_pack_spikes)."""
+    assert dense.is_cuda and dense.dtype == torch.uint8 and dense.is_contiguous()
+    T, B, C, H, W = dense.shape
+    out = torch.empty((T, B, H, (W * C + 31) // 32), dtype=torch.int32, device=dense.device)
+    _check(lib().tac_pack_spikes(_ptr(dense), _ptr(out), T, B, C, H, W, _stream(dense.device)))
+    return out
+
+
+def unpack(packed: torch.Tensor, C: int, W: int) -> torch.Tensor:
+    """packed int32 [T,B,H,WPR] (cuda, contiguous) -> u8 [T,B,C,H,W] (tac_unpack_spikes)."""
+    assert packed.is_cuda and packed.dtype == torch.int32 and packed.is_contiguous()
+    T, B, H, wpr = packed.shape
+    assert wpr == (W * C + 31) // 32
+    out = torch.empty((T, B, C, H, W), dtype=torch.uint8, device=packed.device)
+    _check(lib().tac_unpack_spikes(_ptr(packed), _ptr(out), T, B, C, H, W,
+                                   _stream(packed.device)))
+    return out
+
+
+def last_launch_count() -> int:
+    return int(lib().tac_last_launch_count())
+
+
+def abi_version() -> int:
+    return int(lib().tac_abi_version())

@@ -1,0 +1,62 @@
+"""Calibrate per-layer weight gains with the ORACLE (run once; results frozen in
+paper_2603_13810_b200/configs.py GAINS).  Uses only oracle/ and the seeded input
+generators -- no CUDA path.
+
+For each layer in order, bisect (in log space) the gain g of
+synth.weights(..., gain=g) so that the layer's output firing rate in the
+config's primary mode is ~target; the layer's (pooled) oracle output is the next
+layer's input.
+
+    python scripts/calibrate_gains.py C4 --B 2 --target 0.1
+"""
+import argparse
+import math
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import oracle as O  # noqa: E402
+from paper_2603_13810_b200 import configs, synth  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config")
+    ap.add_argument("--B", type=int, default=2)
+    ap.add_argument("--target", type=float, default=0.1)
+    ap.add_argument("--iters", type=int, default=8)
+    a = ap.parse_args()
+    cfg = configs.CONFIGS[a.config]
+    x = configs.make_inputs(cfg, B=a.B).numpy()
+    t = cfg.T
+    gains = []
+    for i, L in enumerate(cfg.layers):
+        K = 1 if cfg.mode == "dense" else min(cfg.K, t)
+        lo, hi = 0.25, 16.0
+        best = None
+        for _ in range(a.iters):
+            g = math.sqrt(lo * hi)
+            w, b = synth.weights(cfg.seeds[0] * 1000 + i, L.C_out, L.C_in, 3, 3, gain=g)
+            r = O.forward(x, w.numpy(), b.numpy(), K=K, mode=cfg.mode, beta=cfg.beta, pad=L.pad)
+            rate = float(r["out"].mean())
+            best = (g, rate, r["out"])
+            print(f"  layer {i} gain {g:.3f} rate {rate:.4f}", flush=True)
+            if rate < a.target:
+                lo = g
+            else:
+                hi = g
+        g, rate, out = best
+        gains.append(round(g, 2))
+        print(f"layer {i}: gain {g:.3f} -> rate {rate:.4f}", flush=True)
+        x = O.or_pool2(out) if L.pool == 2 else out
+        if cfg.mode == "tac":
+            t //= K
+    print("GAINS", gains)
+
+
+if __name__ == "__main__":
+    main()

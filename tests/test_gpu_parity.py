@@ -1,0 +1,228 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+All inputs come from the seeded generators (paper_2603_13810_b200.synth); the
+oracle and the device see identical spikes.  See tests/_parity.py for the
+replay protocol and tolerances (north_star: bit-exact spikes outside a 1e-3
+band around v_th, membranes within 1e-3 relative).
+"""
+import itertools
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+import _parity as P
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def T():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2603_13810_b200 import build, tacsnn
+    build.build()
+    return tacsnn
+
+
+@pytest.fixture(scope="module")
+def O():
+    from oracle import oracle
+    oracle.build()
+    return oracle
+
+
+def _w(seed, cout, cin, gain, r=3, s=3):
+    from paper_2603_13810_b200 import synth
+    return synth.weights(seed, cout, cin, r, s, gain=gain)
+
+
+def _spikes(seed, shape, rho):
+    g = torch.Generator().manual_seed(seed)
+    return (torch.rand(shape, generator=g) < rho).to(torch.uint8).numpy()
+
+
+ENGINES = ["simt", "tcgen05"]
+
+
+def _engine_or_skip(spec, engine):
+    s = spec.replace(engine=engine)
+    try:
+        assert s.engine_used() == engine
+    except RuntimeError:
+        pytest.skip(f"{engine} does not take this layer")
+    return s
+
+
+# ---------------------------------------------------------------- formats ----
+@pytest.mark.parametrize("C,H,W", [(1, 28, 28), (2, 128, 128), (32, 13, 13), (128, 8, 8),
+                                   (3, 5, 7), (8, 26, 26)])
+def test_pack_unpack_match_oracle_format(T, O, C, H, W):
+    d = _spikes(C * 100 + W, (3, 2, C, H, W), 0.3)
+    p = T.pack(torch.from_numpy(d).cuda())
+    assert np.array_equal(P.to_u32(p), O.pack_spikes(d))
+    assert np.array_equal(T.unpack(p, C, W).cpu().numpy(), d)
+    assert T.last_launch_count() == 1
+
+
+# ------------------------------------------------------- single layers ------
+LAYER_CASES = [
+    # name, (T,B,Cin,H,W,Cout,pad,pool), gain, rho
+    ("C1", (8, 4, 1, 28, 28, 8, 0, 1), 1.42, 0.1),
+    ("mnistL1", (8, 3, 1, 28, 28, 32, 0, 2), 0.9, 0.15),
+    ("mnistL2", (8, 3, 32, 13, 13, 64, 0, 1), 0.6, 0.15),
+    ("dvsL1", (4, 2, 2, 128, 128, 128, 1, 2), 7.1, 0.03),
+    ("dvsL2", (4, 2, 128, 64, 64, 128, 1, 2), 1.1, 0.1),
+    ("dvsL5", (8, 5, 128, 8, 8, 128, 1, 2), 0.9, 0.1),
+    ("ragged", (8, 3, 3, 13, 11, 24, 1, 1), 2.0, 0.3),
+    ("wide_cin", (4, 2, 96, 10, 9, 48, 1, 2), 1.5, 0.2),
+]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("mode,K,beta", [("tac", 2, 0.5), ("tactp", 2, 0.5), ("dense", 1, 0.5),
+                                         ("tac", 4, 0.9), ("tactp", 4, 0.5)])
+@pytest.mark.parametrize("case", LAYER_CASES, ids=[c[0] for c in LAYER_CASES])
+def test_layer_parity(T, O, case, mode, K, beta, engine):
+    name, (Tn, B, Cin, H, W, Cout, pad, pool), gain, rho = case
+    spec = T.LayerSpec(T=Tn, B=B, C_in=Cin, H=H, W=W, C_out=Cout, pad=pad, K=K, mode=mode,
+                       beta=beta, out_pool=pool)
+    spec = _engine_or_skip(spec, engine)
+    S = _spikes(zlib.crc32(name.encode()) % 1000, (Tn, B, Cin, H, W), rho)
+    w, b = _w(7, Cout, Cin, gain * (0.5 if mode == "tactp" else 1.0))
+    _, _, st = P.check_layer(T, O, spec, S, w, b, label=f"{name}/{mode}/K{K}/{engine}")
+    assert 0.0 < st["rate"] < 0.9, st
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("reset", ["delayed", "hard"])
+@pytest.mark.parametrize("mode", ["dense", "tac", "tactp"])
+def test_reset_variants(T, O, mode, reset, engine):
+    spec = T.LayerSpec(T=8, B=3, C_in=32, H=12, W=12, C_out=32, pad=1, K=2, mode=mode,
+                       beta=0.5, v_reset=-0.25, reset=reset, out_pool=2)
+    spec = _engine_or_skip(spec, engine)
+    S = _spikes(11, (8, 3, 32, 12, 12), 0.2)
+    w, b = _w(3, 32, 32, 1.5)
+    P.check_layer(T, O, spec, S, w, b, label=f"{mode}/{reset}/{engine}")
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("reset", ["subtract", "delayed", "hard"])
+def test_v_init_chaining(T, O, reset, engine):
+    """P12 on the device: forward(T) == forward(T1) -> forward(T-T1, v_init=v_final)."""
+    spec = T.LayerSpec(T=8, B=2, C_in=32, H=10, W=10, C_out=32, pad=1, K=2, mode="tactp",
+                       beta=0.5, reset=reset, out_pool=1)
+    spec = _engine_or_skip(spec, engine)
+    S = _spikes(12, (8, 2, 32, 10, 10), 0.25)
+    w, b = _w(4, 32, 32, 1.2)
+    prep = T.prepare_weights(spec, w, b)
+    x = T.pack(torch.from_numpy(S).cuda())
+    full, vf, _ = T.conv_lif(spec, prep, x, want_v_final=True)
+    h = spec.replace(T=4)
+    a, va, _ = T.conv_lif(h, prep, x[:4], want_v_final=True)
+    c, vc, _ = T.conv_lif(h, prep, x[4:], v_init=va, want_v_final=True)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat([a, c]), full)
+    assert torch.equal(vc, vf)
+    # and the chained second half against the oracle with v_init
+    P.check_layer(T, O, h, S[4:], w, b, v_init=va.cpu().numpy().transpose(0, 3, 1, 2),
+                  label=f"chain/{reset}/{engine}")
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_exhaustive_tiny_batch(T, O, engine):
+    """P9: every binary input of a 1-channel 2x2 image over T=4 steps (2^16
+    samples in one batch), pad 1, K=2, all three modes."""
+    bits = np.array(list(itertools.product([0, 1], repeat=16)), np.uint8)   # [65536, 16]
+    S = np.ascontiguousarray(bits.reshape(-1, 4, 1, 2, 2).transpose(1, 0, 2, 3, 4))
+    w, b = _w(5, 16, 1, 3.0)
+    for mode in ("dense", "tac", "tactp"):
+        spec = T.LayerSpec(T=4, B=S.shape[1], C_in=1, H=2, W=2, C_out=16, pad=1, K=2,
+                           mode=mode, beta=0.5, out_pool=1)
+        spec = _engine_or_skip(spec, engine)
+        P.check_layer(T, O, spec, S, w, b, label=f"exhaustive/{mode}/{engine}")
+
+
+def test_shard_invariance(T):
+    """P13: a batch-shard view gives bitwise the same per-sample outputs."""
+    spec = T.LayerSpec(T=8, B=6, C_in=128, H=16, W=16, C_out=128, pad=1, K=4, mode="tactp",
+                       beta=0.5, out_pool=2)
+    S = _spikes(13, (8, 6, 128, 16, 16), 0.1)
+    w, b = _w(6, 128, 128, 1.0)
+    prep = T.prepare_weights(spec, w, b)
+    x = T.pack(torch.from_numpy(S).cuda())
+    full, vf, cf = T.conv_lif(spec, prep, x, want_v_final=True)
+    parts = [T.conv_lif(spec.replace(B=3), prep, x[:, i:i + 3], want_v_final=True)
+             for i in (0, 3)]
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat([p[0] for p in parts], 1), full)
+    assert torch.equal(torch.cat([p[1] for p in parts], 0), vf)
+    assert torch.equal(torch.cat([p[2] for p in parts], 0), cf)
+
+
+def test_errors_launch_nothing(T):
+    spec = T.LayerSpec(T=8, B=2, C_in=2, H=8, W=8, C_out=16, pad=1, K=4, mode="tac", beta=0.5)
+    prep = T.prepare_weights(spec, *_w(1, 16, 2, 1.0))
+    x = T.pack(torch.zeros((8, 2, 2, 8, 8), dtype=torch.uint8, device="cuda"))
+    with pytest.raises(RuntimeError, match="K_NOT_DIVIDING"):
+        T.conv_lif(spec.replace(K=3), prep, x)
+    with pytest.raises(RuntimeError, match="NONFINITE"):
+        w, b = _w(1, 16, 2, 1.0)
+        w[0, 0, 0, 0] = float("nan")
+        T.prepare_weights(spec, w, b)
+    xc = x.cpu()
+    import ctypes
+    d = spec.desc()
+    out = torch.empty((2, 2, 8, 4), dtype=torch.int32, device="cuda")
+    st = T.lib().tac_conv_lif_forward(ctypes.byref(d), ctypes.c_void_p(prep.data_ptr()),
+                                      ctypes.c_void_p(xc.data_ptr()), None,
+                                      ctypes.c_void_p(out.data_ptr()), None, None, None, 0, None)
+    assert st == 4 and b"not device memory" in T.lib().tac_last_error_detail()
+
+
+# ------------------------------------------------------------- stacks -------
+@pytest.mark.parametrize("cfg_name,B,mode", [("C1", 4, "tac"), ("C1", 4, "dense"),
+                                             ("C2", 6, "tac"), ("C3", 4, "tac"),
+                                             ("C3", 2, "dense"), ("C4", 2, "tactp"),
+                                             ("C4", 1, "tac"), ("C4", 1, "dense")])
+def test_config_stack_parity(T, O, cfg_name, B, mode):
+    from paper_2603_13810_b200 import configs
+    cfg = configs.CONFIGS[cfg_name]
+    specs = configs.layer_plan(cfg, mode=mode, B=B)
+    if mode == "tac" and cfg.inputs == "dvs":
+        specs = configs.layer_plan(cfg, mode=mode, K=2, B=B)[:4]   # 16/2^4 = 1 step left
+    weights = configs.layer_weights(cfg)[:len(specs)]
+    S = configs.make_inputs(cfg, B=B).numpy()
+    stats = P.check_stack(T, O, specs, weights, S, label=f"{cfg_name}/{mode}")
+    for st in stats:
+        assert st["rate"] > 0.0
+
+
+@pytest.mark.slow
+def test_c5_full_size_sampled(T, O):
+    """C5 at its full batch (2048) in the bench launch configuration; sampled
+    samples are re-checked layer by layer through the oracle replay, and the
+    full-batch pooled outputs for those samples must equal the oracle's."""
+    from paper_2603_13810_b200 import configs, network
+    cfg = configs.CONFIGS["C5"]
+    specs = configs.layer_plan(cfg)
+    weights = configs.layer_weights(cfg)
+    net = network.Network(specs, weights)
+    x = T.pack(configs.make_inputs(cfg, device="cuda"))
+    _, counts, outs, _ = net.forward(x, keep=True)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(0)
+    samples = [0, cfg.B - 1] + sorted(rng.choice(np.arange(1, cfg.B - 1), 2, replace=False).tolist())
+    for bsel in samples:
+        S = configs.make_inputs(cfg, B=1, b0=bsel).numpy()
+        x_dev = None
+        for i, (spec, (w, b)) in enumerate(zip(specs, weights)):
+            s1 = spec.replace(B=1)
+            ref_out, dev_out, st = P.check_layer(T, O, s1, S, w, b, x_packed=x_dev,
+                                                 label=f"C5 sample {bsel} layer {i}")
+            full_b = P.to_u32(outs[i][:, bsel:bsel + 1])
+            assert np.array_equal(full_b, O.pack_spikes(ref_out)), f"layer {i} sample {bsel}"
+            assert np.array_equal(counts[i][bsel].cpu().numpy().astype(np.int64),
+                                  st["counts"][0]), f"counts layer {i} sample {bsel}"
+            S, x_dev = ref_out, dev_out
