@@ -69,14 +69,14 @@ def test_pack_unpack_match_oracle_format(T, O, C, H, W):
 # ------------------------------------------------------- single layers ------
 LAYER_CASES = [
     # name, (T,B,Cin,H,W,Cout,pad,pool), gain, rho
-    ("C1", (8, 4, 1, 28, 28, 8, 0, 1), 1.42, 0.1),
-    ("mnistL1", (8, 3, 1, 28, 28, 32, 0, 2), 0.9, 0.15),
-    ("mnistL2", (8, 3, 32, 13, 13, 64, 0, 1), 0.6, 0.15),
+    ("C1", (8, 4, 1, 28, 28, 8, 0, 1), 2.5, 0.1),
+    ("mnistL1", (8, 3, 1, 28, 28, 32, 0, 2), 2.5, 0.15),
+    ("mnistL2", (8, 3, 32, 13, 13, 64, 0, 1), 3.5, 0.15),
     ("dvsL1", (4, 2, 2, 128, 128, 128, 1, 2), 7.1, 0.03),
-    ("dvsL2", (4, 2, 128, 64, 64, 128, 1, 2), 1.1, 0.1),
-    ("dvsL5", (8, 5, 128, 8, 8, 128, 1, 2), 0.9, 0.1),
+    ("dvsL2", (4, 2, 128, 64, 64, 128, 1, 2), 3.5, 0.1),
+    ("dvsL5", (8, 5, 128, 8, 8, 128, 1, 2), 3.5, 0.1),
     ("ragged", (8, 3, 3, 13, 11, 24, 1, 1), 2.0, 0.3),
-    ("wide_cin", (4, 2, 96, 10, 9, 48, 1, 2), 1.5, 0.2),
+    ("wide_cin", (4, 2, 96, 10, 9, 48, 1, 2), 2.5, 0.2),
 ]
 
 
@@ -90,7 +90,7 @@ def test_layer_parity(T, O, case, mode, K, beta, engine):
                        beta=beta, out_pool=pool)
     spec = _engine_or_skip(spec, engine)
     S = _spikes(zlib.crc32(name.encode()) % 1000, (Tn, B, Cin, H, W), rho)
-    w, b = _w(7, Cout, Cin, gain * (0.5 if mode == "tactp" else 1.0))
+    w, b = _w(7, Cout, Cin, gain)
     _, _, st = P.check_layer(T, O, spec, S, w, b, label=f"{name}/{mode}/K{K}/{engine}")
     assert 0.0 < st["rate"] < 0.9, st
 
