@@ -1,13 +1,825 @@
-// tc.cu -- tcgen05 engine (placeholder until the fused kernel lands).
+// tc.cu -- the tcgen05 engine of libtacsnn: ONE fused kernel per layer call that
+// aggregates the K spike frames of a group (A_k = sum_j beta^{K-1-j} S_{kK+j},
+// Definition TAC), convolves A_k once on the 5th-generation tensor
+// cores (Alg. 1 l.4 / Alg. 2 l.4), and runs the LIF steps (Alg. 1 l.5-7, Alg. 2
+// l.5-9, Eq. (1) for dense) with the membrane resident in registers across all
+// T/K groups, writing packed (optionally 2x2 OR-pooled) spikes and spike counts.
+//
+// Exactness of the tensor-core operands:
+//   * beta = 2^-m (DVS beta = 0.5) => A_k * 2^{m(K-1)} =
+//     sum_j S_{kK+j} 2^{m j} is an exact unsigned integer <= 255 (u8 operand);
+//     dense mode (K = 1) has A = S in {0,1} for any beta.
+//   * W [C_out][C_in][3][3] fp32 is split per output channel into two int8
+//     slices, w ~= s1 q1 + s2 q2 (s2 = s1/254), |w - w~| <= max|w| * 1.55e-5;
+//     both slices ride in ONE MMA with N = 2 C_out (hi rows on CTA 0, lo rows on
+//     CTA 1 of the pair), accumulated exactly in s32 in TMEM.
+//   * the epilogue forms Y = 2^{-m(K-1)} (s1 D_hi + s2 D_lo) + b in fp32.
+//
+// Implicit GEMM layout ("padded linear space"): output position L =
+// (b*S_h + y)*S_w + x with S_h = H + pad, S_w = W + pad.  The aggregated input
+// halo of a 128-position tile is stored K-major, no swizzle, one 16-byte row per
+// position, so the 3x3 tap (r, s) is just a start-address offset of
+// (r*S_w + s)*16 bytes of the tensor-core smem descriptor -- no im2col copies.
+// Positions with y >= H' or x >= W' are computed and discarded.  Layers with
+// C_in <= 2 (first layers) use an explicit 32-byte im2col row per position
+// instead (K_red = 9 C_in <= 18 padded to 32).
+//
+// CTA pair (cluster of 2, tcgen05 cta_group::2, M = 256): each CTA owns 128
+// output positions and half of the B operand (one int8 slice of all 9 taps,
+// resident in smem for the whole kernel).  Warp roles per CTA (384 threads):
+//   warp 0      : TMEM alloc; in CTA 0 one lane issues all MMAs of the pair
+//   warps 1..3  : producers -- load packed spikes, build the u8 aggregate A_k
+//   warps 4..11 : epilogue  -- TMEM -> registers, LIF over K steps, spikes to
+//                 smem staging, pooled/packed stores, counts, v_init/v_final
+// Pipelines: A stages (2) producer -> MMA, TMEM accumulators (2) MMA -> epilogue.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "ptx.cuh"
 #include "tc.cuh"
 
 namespace tacsnn {
-bool tc_shape_ok(const tac_conv_lif_desc *) { return false; }
-bool tc_supported(const tac_conv_lif_desc *) { return false; }
-const char *tc_unsupported_reason(const tac_conv_lif_desc *) { return "tcgen05 engine not built"; }
-size_t tc_weights_bytes(const tac_conv_lif_desc *) { return 0; }
-void tc_prepare(const tac_conv_lif_desc *, const float *, const float *, unsigned char *) {}
-int tc_launch(const tac_conv_lif_desc *, const LayerParams &, const unsigned char *, void *, int *) {
-  return 1;
+
+namespace {
+
+constexpr int kProdWarps = 3;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 32 * (1 + kProdWarps + kEpiWarps);
+constexpr int kStages = 2;
+constexpr int kAccs = 2;
+constexpr int kMaxSteps = 8;
+constexpr int kPlanes = 6;  // bit-sliced spike counters (<= 63 steps per flush)
+constexpr uint32_t kSmemLimit = 232448;
+
+enum { PATH_HALO = 0, PATH_IM2COL = 1 };
+
+struct TcParams {
+  int B, H, W, Cin, Cout, Cout_pad, pad, Ho, Wo, Hq, Wq, pool;
+  int K, G, nsteps, mode, reset;
+  int Sh, Sw;
+  long long M_total;
+  int num_tiles, num_pairs;
+  int halo_rows, nkc, ntaps, m_shift;
+  int wpr_in, wpr_out, nwo, out_atomic;
+  long long in_st, in_sb, out_st, out_sb;
+  float decay, v_th, v_reset, agg_scale;
+  uint32_t off_w, off_a, a_stage_bytes, off_stage, off_scale, off_bar, smem_bytes;
+  uint32_t w_bytes_cta, tmem_cols, n_total, lbo_a, lbo_b;
+  int tap_off[9];
+  const uint32_t *in;
+  uint32_t *out;
+  const float *v_init;
+  float *v_final;
+  uint32_t *counts;
+  const unsigned char *w_img;
+  const float *scale_bias;
+};
+
+// ------------------------------------------------------------ host helpers --
+int beta_shift(float beta) {  // m with beta == 2^-m exactly, else 0
+  int e;
+  const double mant = std::frexp((double)beta, &e);
+  if (mant != 0.5) return 0;
+  const int m = 1 - e;
+  return m >= 1 ? m : 0;
 }
+
+int cout_pad_of(int Cout) {
+  if (Cout <= 16) return 16;
+  if (Cout <= 32) return 32;
+  if (Cout <= 64) return 64;
+  return 128;
+}
+
+int path_of(const tac_conv_lif_desc *d) {
+  return (d->C_in % 32 == 0) ? PATH_HALO : PATH_IM2COL;
+}
+
+struct Geometry {
+  int path, Sh, Sw, halo_rows, nkc, ntaps, cout_pad, nsteps;
+  uint32_t w_bytes_cta, a_stage_bytes, stage_bytes, off_w, off_a, off_stage, off_scale, off_bar,
+      smem_bytes;
+};
+
+uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
+
+Geometry geometry(const tac_conv_lif_desc *d) {
+  Geometry g{};
+  g.path = path_of(d);
+  g.cout_pad = cout_pad_of(d->C_out);
+  const int K = d->mode == TAC_MODE_DENSE ? 1 : d->K;
+  g.nsteps = d->mode == TAC_MODE_TACTP ? K : 1;
+  if (g.path == PATH_HALO) {
+    g.Sh = d->H + d->pad;
+    g.Sw = d->W + d->pad;
+    g.halo_rows = (int)align_up(128 + 2 * g.Sw + 2, 8);
+    g.nkc = d->C_in / 16;
+    g.ntaps = 9;
+    g.w_bytes_cta = 9u * d->C_in * g.cout_pad;
+    g.a_stage_bytes = align_up((uint32_t)g.halo_rows * d->C_in, 128);
+  } else {
+    g.Sh = d->H;
+    g.Sw = d->W;
+    g.halo_rows = 128;
+    g.nkc = 2;
+    g.ntaps = 1;
+    g.w_bytes_cta = 32u * g.cout_pad;
+    g.a_stage_bytes = 128u * 32u;
+  }
+  const int nwt2 = std::max(2, g.cout_pad / 32);  // stage words per position
+  g.stage_bytes = (uint32_t)g.nsteps * 128u * nwt2 * 4u;
+  g.off_w = 0;
+  g.off_a = align_up(g.w_bytes_cta, 1024);
+  g.off_stage = align_up(g.off_a + kStages * g.a_stage_bytes, 128);
+  g.off_scale = align_up(g.off_stage + g.stage_bytes, 128);
+  g.off_bar = align_up(g.off_scale + 3u * g.cout_pad * 4u, 64);
+  g.smem_bytes = g.off_bar + 8u * (2 * kStages + 2 * kAccs + 1) + 16u;
+  return g;
+}
+
+const char *shape_reason(const tac_conv_lif_desc *d) {
+  if (d->R != 3 || d->S != 3) return "needs a 3x3 kernel";
+  if (d->stride != 1) return "needs stride 1";
+  if (d->pad < 0 || d->pad > 1) return "needs pad 0 or 1";
+  if (!((d->C_in % 32 == 0 && d->C_in <= 128) || d->C_in <= 2))
+    return "needs C_in in {1,2} or a multiple of 32 up to 128";
+  if (d->C_out > 128 || !(d->C_out % 32 == 0 || d->C_out == 8 || d->C_out == 16))
+    return "needs C_out in {8,16} or a multiple of 32 up to 128";
+  const int K = d->mode == TAC_MODE_DENSE ? 1 : d->K;
+  if (d->mode == TAC_MODE_TACTP && K > kMaxSteps) return "TAC-TP needs K <= 8";
+  if (geometry(d).smem_bytes > kSmemLimit) return "shared-memory footprint exceeds 227 KB";
+  return nullptr;
+}
+
+const char *reason(const tac_conv_lif_desc *d) {
+  const char *r = shape_reason(d);
+  if (r) return r;
+  if (d->mode != TAC_MODE_DENSE) {
+    const int m = beta_shift(d->beta);
+    if (!m) return "TAC/TAC-TP on tensor cores needs beta = 2^-m (exact u8 aggregate)";
+    if (m * (d->K - 1) > 7) return "u8 aggregate overflow: needs m*(K-1) <= 7";
+  }
+  return nullptr;
+}
+
+// ------------------------------------------------------------ device code ---
+template <int PATH>
+struct PosDecode {
+  // output position L -> (b, y, x) and validity
+  __device__ __forceinline__ static void out(const TcParams &p, long long L, int &b, int &y,
+                                             int &x, bool &valid) {
+    if (PATH == PATH_HALO) {
+      const long long per = (long long)p.Sh * p.Sw;
+      const long long bb = L / per;
+      const int rem = (int)(L - bb * per);
+      y = rem / p.Sw;
+      x = rem - y * p.Sw;
+      b = (int)bb;
+      valid = bb < p.B && y < p.Ho && x < p.Wo;
+    } else if (p.pool == 2) {  // quad-major: the 4 members of a 2x2 pool window adjacent
+      const long long q = L >> 2;
+      const int mem = (int)(L & 3);
+      const long long per = (long long)p.Hq * p.Wq;
+      const long long bb = q / per;
+      const int rq = (int)(q - bb * per);
+      const int py = rq / p.Wq, px = rq - (rq / p.Wq) * p.Wq;
+      y = 2 * py + (mem >> 1);
+      x = 2 * px + (mem & 1);
+      b = (int)bb;
+      valid = bb < p.B;
+    } else {
+      const long long per = (long long)p.Ho * p.Wo;
+      const long long bb = L / per;
+      const int rem = (int)(L - bb * per);
+      y = rem / p.Wo;
+      x = rem - y * p.Wo;
+      b = (int)bb;
+      valid = bb < p.B;
+    }
+  }
+};
+
+// --- producers: build the u8 aggregate A_k * 2^{m(K-1)} in the MMA layout ---
+__device__ __forceinline__ void agg_word(uint32_t (&o)[8], const uint32_t (&xj)[kMaxSteps],
+                                         int K, int m) {
+  // byte b of output word o <- input channel (o + 8b) of the 32-channel word;
+  // bit e_j = m*j of that byte <- frame j  (weights 2^{m j}, oldest frame = 1)
+#pragma unroll
+  for (int j = 0; j < kMaxSteps; ++j) {
+    if (j < K) {
+      const uint32_t x = xj[j];
+      const int e = m * j;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) o[q] |= ((x >> q) & 0x01010101u) << e;
+    }
+  }
+}
+
+__device__ __forceinline__ void produce_halo(const TcParams &p, int tile, int k, uint32_t a_stage,
+                                             int ptid) {
+  const int nwin = p.Cin >> 5;
+  const int ntask = p.halo_rows * nwin;
+  const long long L0 = (long long)tile * 128;
+  const long long per = (long long)p.Sh * p.Sw;
+  const uint32_t *frame0 = p.in + (long long)(k * p.K) * p.in_st;
+  for (int task = ptid; task < ntask; task += kProdWarps * 32) {
+    const int row = task / nwin, w = task - (task / nwin) * nwin;
+    const long long L = L0 + row;
+    const long long bb = L / per;
+    const int rem = (int)(L - bb * per);
+    const int yy = rem / p.Sw, xx = rem - (rem / p.Sw) * p.Sw;
+    const int yi = yy - p.pad, xi = xx - p.pad;
+    uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (bb < p.B && yi >= 0 && yi < p.H && xi >= 0 && xi < p.W) {
+      const uint32_t *src = frame0 + bb * p.in_sb + (long long)yi * p.wpr_in + xi * nwin + w;
+      uint32_t xj[kMaxSteps];
+#pragma unroll
+      for (int j = 0; j < kMaxSteps; ++j) xj[j] = (j < p.K) ? __ldg(src + j * p.in_st) : 0u;
+      agg_word(o, xj, p.K, p.m_shift);
+    }
+    const uint32_t dst = a_stage + (uint32_t)(2 * w) * p.lbo_a + (uint32_t)row * 16u;
+    ptx::st_shared_v4(dst, o[0], o[1], o[2], o[3]);
+    ptx::st_shared_v4(dst + p.lbo_a, o[4], o[5], o[6], o[7]);
+  }
+}
+
+__device__ __forceinline__ void produce_im2col(const TcParams &p, int tile, int k,
+                                               uint32_t a_stage, int ptid) {
+  const long long L0 = (long long)tile * 128;
+  const uint32_t wmask = (1u << (3 * p.Cin)) - 1u;
+  for (int pos = ptid; pos < 128; pos += kProdWarps * 32) {
+    int b, y, x;
+    bool valid;
+    PosDecode<PATH_IM2COL>::out(p, L0 + pos, b, y, x, valid);
+    uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (valid) {
+      const int bit0 = (x - p.pad) * p.Cin;
+      const int w0 = bit0 >= 0 ? (bit0 >> 5) : -1;  // bit0 >= -2
+      const int sh = bit0 - w0 * 32;
+#pragma unroll
+      for (int j = 0; j < kMaxSteps; ++j) {
+        if (j < p.K) {
+          const uint32_t *fr = p.in + (long long)(k * p.K + j) * p.in_st + (long long)b * p.in_sb;
+          uint32_t z = 0;
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+            const int yi = y + r - p.pad;
+            if (yi < 0 || yi >= p.H) continue;
+            const uint32_t *row = fr + (long long)yi * p.wpr_in;
+            const uint32_t lo = (w0 >= 0 && w0 < p.wpr_in) ? __ldg(row + w0) : 0u;
+            const uint32_t hi = (w0 + 1 < p.wpr_in) ? __ldg(row + w0 + 1) : 0u;
+            z |= (__funnelshift_r(lo, hi, sh) & wmask) << (8 * r);
+          }
+          const int e = p.m_shift * j;
+          // word q, byte r <- (row r, window bit q): K-index 4q + r
+#pragma unroll
+          for (int q = 0; q < 6; ++q) o[q] |= ((z >> q) & 0x00010101u) << e;
+        }
+      }
+    }
+    const uint32_t dst = a_stage + (uint32_t)pos * 16u;
+    ptx::st_shared_v4(dst, o[0], o[1], o[2], o[3]);
+    ptx::st_shared_v4(dst + p.lbo_a, o[4], o[5], o[6], o[7]);
+  }
+}
+
+// --- epilogue helpers ---------------------------------------------------------
+// column popcount of a 32x32 bit matrix held one row per lane (32x32 transpose)
+__device__ __forceinline__ uint32_t warp_col_popc(uint32_t x, uint32_t lane) {
+  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const int s = 16 >> i;
+    const uint32_t m = masks[i];
+    const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, s);
+    if (lane & s)
+      x = (x & ~m) | ((y >> s) & m);
+    else
+      x = (x & m) | ((y << s) & ~m);
+  }
+  return __popc(x);
+}
+
+template <int NWT>
+__device__ __forceinline__ void flush_counts(const TcParams &p, uint32_t (&planes)[kPlanes][NWT],
+                                             bool valid, int b, int co_base, int nch,
+                                             uint32_t lane) {
+  uint32_t rem = __ballot_sync(0xFFFFFFFFu, valid);
+  while (rem) {
+    const int leader = __ffs(rem) - 1;
+    const int bsel = __shfl_sync(0xFFFFFFFFu, b, leader);
+    const bool mine = valid && b == bsel;
+    rem &= ~__ballot_sync(0xFFFFFFFFu, mine);
+#pragma unroll
+    for (int w = 0; w < NWT; ++w) {
+      uint32_t total = 0;
+#pragma unroll
+      for (int pl = 0; pl < kPlanes; ++pl)
+        total += warp_col_popc(mine ? planes[pl][w] : 0u, lane) << pl;
+      const int c = w * 32 + (int)lane;
+      const int co = co_base + c;
+      if (total && c < nch && co < p.Cout) atomicAdd(p.counts + (long long)bsel * p.Cout + co, total);
+    }
+  }
+#pragma unroll
+  for (int pl = 0; pl < kPlanes; ++pl)
+#pragma unroll
+    for (int w = 0; w < NWT; ++w) planes[pl][w] = 0u;
+}
+
+template <int RESET>
+__device__ __forceinline__ void lif_step(float &v, float y, float decay, float vth, float vres,
+                                         uint32_t &inv_bits, uint32_t bitmask, uint32_t &prev) {
+  // one LIF step; inv_bits collects NOT(spike) at `bitmask`
+  v = fmaf(decay, v, y);                                    // Alg.1 l.5 / Alg.2 l.6 / Eq.(1)
+  if (RESET == 1) v -= (prev & bitmask) ? vth : 0.f;        // delayed: - v_th s_{t-1}
+  const float v2 = v - vth;
+  const int msk = __float_as_int(v2) >> 31;                 // -1: v < v_th (no spike)
+  if (RESET == 0)                                           // subtract: v - v_th on spike
+    v = __int_as_float((__float_as_int(v2) & ~msk) | (__float_as_int(v) & msk));
+  else if (RESET == 2)                                      // hard: v_reset on spike
+    v = __int_as_float((__float_as_int(vres) & ~msk) | (__float_as_int(v) & msk));
+  inv_bits |= (uint32_t)msk & bitmask;
+  if (RESET == 1) prev = (prev & ~bitmask) | (~(uint32_t)msk & bitmask);
+}
+
+template <int NCH, int PATH>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    tc_conv_lif_kernel(const __grid_constant__ TcParams p) {
+  constexpr int NWT = NCH >= 32 ? NCH / 32 : 1;  // spike words per epilogue thread
+  constexpr int SROW = NCH >= 32 ? 2 * NWT : 2;  // stage words per position
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const uint32_t sbase = ptx::smem_u32(smem);
+  const uint32_t bar_a_full = sbase + p.off_bar;
+  const uint32_t bar_a_empty = bar_a_full + 8 * kStages;
+  const uint32_t bar_t_full = bar_a_empty + 8 * kStages;
+  const uint32_t bar_t_empty = bar_t_full + 8 * kAccs;
+  const uint32_t bar_w = bar_t_empty + 8 * kAccs;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + p.off_bar + 8 * (2 * kStages + 2 * kAccs + 1));
+  float *sc = reinterpret_cast<float *>(smem + p.off_scale);  // [S1*agg | S2*agg | bias]
+  uint32_t *stage = reinterpret_cast<uint32_t *>(smem + p.off_stage);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(bar_a_full + 8 * s, 2 * kProdWarps);
+      ptx::mbar_init(bar_a_empty + 8 * s, 1);
+    }
+    for (int a = 0; a < kAccs; ++a) {
+      ptx::mbar_init(bar_t_full + 8 * a, 1);
+      ptx::mbar_init(bar_t_empty + 8 * a, 2 * kEpiWarps);
+    }
+    ptx::mbar_init(bar_w, 1);
+    ptx::fence_mbar_init();
+    // resident weights: this CTA's int8 slice of every tap
+    ptx::mbar_arrive_expect_tx(bar_w, p.w_bytes_cta);
+    const unsigned char *src = p.w_img + (size_t)rank * p.w_bytes_cta;
+    for (uint32_t off = 0; off < p.w_bytes_cta; off += 16384u)
+      ptx::bulk_g2s(sbase + p.off_w + off, src + off, min(16384u, p.w_bytes_cta - off), bar_w);
+  }
+  if (warp == 0) {
+    ptx::tmem_alloc_cg2(ptx::smem_u32(tmem_slot), p.tmem_cols);
+    ptx::tmem_relinquish_cg2();
+  }
+  for (int i = threadIdx.x; i < 3 * p.Cout_pad; i += kThreads)
+    sc[i] = p.scale_bias[i] * (i < 2 * p.Cout_pad ? p.agg_scale : 1.f);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  ptx::mbar_wait(bar_w, 0);
+  ptx::cluster_sync();  // both CTAs' weight slices resident before the first MMA
+
+  const int ncl = (int)ptx::nclusters_x();
+  const int cid = (int)ptx::cluster_id_x();
+
+  if (warp == 0) {
+    // ================================ MMA issuer (CTA 0 of the pair) =========
+    if (rank == 0 && lane == 0) {
+      const uint32_t idesc = ptx::idesc_i8(256, p.n_total);
+      const uint32_t n_half_bytes = (uint32_t)p.Cout_pad * 16u;
+      uint32_t it = 0;
+      for (int pair = cid; pair < p.num_pairs; pair += ncl) {
+        for (int k = 0; k < p.G; ++k, ++it) {
+          const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
+          const uint32_t acc = it % kAccs, aph = (it / kAccs) & 1u;
+          ptx::mbar_wait_cluster(bar_t_empty + 8 * acc, aph ^ 1u);
+          ptx::mbar_wait_cluster(bar_a_full + 8 * s, ph);
+          ptx::tc_fence_after();
+          const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
+          const uint32_t d_tmem = tmem_base + acc * p.n_total;
+          for (int tap = 0; tap < p.ntaps; ++tap) {
+            for (int kc2 = 0; kc2 < (p.nkc >> 1); ++kc2) {
+              const uint64_t ad = ptx::smem_desc(
+                  a_stage + (uint32_t)(2 * kc2) * p.lbo_a + (uint32_t)p.tap_off[tap] * 16u,
+                  p.lbo_a, 128u);
+              const uint64_t bd = ptx::smem_desc(
+                  sbase + p.off_w + (uint32_t)(tap * p.nkc + 2 * kc2) * n_half_bytes, p.lbo_b,
+                  128u);
+              ptx::mma_i8_cg2(d_tmem, ad, bd, idesc, (tap | kc2) ? 1u : 0u);
+            }
+          }
+          ptx::mma_commit_cg2_multicast(bar_a_empty + 8 * s);
+          ptx::mma_commit_cg2_multicast(bar_t_full + 8 * acc);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp <= kProdWarps) {
+    // ================================ producers ================================
+    const int ptid = (int)threadIdx.x - 32;
+    uint32_t it = 0;
+    for (int pair = cid; pair < p.num_pairs; pair += ncl) {
+      const int tile = 2 * pair + (int)rank;
+      for (int k = 0; k < p.G; ++k, ++it) {
+        const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
+        ptx::mbar_wait(bar_a_empty + 8 * s, ph ^ 1u);
+        const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
+        if (PATH == PATH_HALO)
+          produce_halo(p, tile, k, a_stage, ptid);
+        else
+          produce_im2col(p, tile, k, a_stage, ptid);
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(bar_a_full + 8 * s, 0);
+      }
+    }
+  } else {
+    // ================================ epilogue =================================
+    const int e = (int)warp - 1 - kProdWarps;         // 0..7
+    const int quad = (int)(warp & 3);                  // TMEM lane quadrant of this warp
+    const int half = e >> 2;                           // channel half
+    const int m = quad * 32 + (int)lane;               // position within the CTA tile
+    const int tid_e = e * 32 + (int)lane;              // 0..255
+    const int co_base = half * NCH;
+    const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+    const float decay = p.decay, vth = p.v_th, vres = p.v_reset;
+    uint32_t it = 0;
+    for (int pair = cid; pair < p.num_pairs; pair += ncl) {
+      const int tile = 2 * pair + (int)rank;
+      const long long L0 = (long long)tile * 128;
+      int b, y, x;
+      bool valid;
+      PosDecode<PATH>::out(p, L0 + m, b, y, x, valid);
+      const long long vbase = (((long long)b * p.Ho + y) * p.Wo + x) * p.Cout + co_base;
+      float V[NCH];
+      uint32_t prev[NWT];
+      uint32_t planes[kPlanes][NWT];
+      int steps_acc = 0;
+#pragma unroll
+      for (int w = 0; w < NWT; ++w) {
+        prev[w] = 0u;
+#pragma unroll
+        for (int pl = 0; pl < kPlanes; ++pl) planes[pl][w] = 0u;
+      }
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        V[c] = (p.v_init && valid && co_base + c < p.Cout) ? __ldg(p.v_init + vbase + c) : 0.f;
+        if (p.reset == 1 && V[c] >= vth) prev[c / 32] |= 1u << (c % 32);  // reading R4
+      }
+      for (int k = 0; k < p.G; ++k, ++it) {
+        const uint32_t acc = it % kAccs, aph = (it / kAccs) & 1u;
+        ptx::mbar_wait(bar_t_full + 8 * acc, aph);
+        ptx::tc_fence_after();
+        uint32_t inv[kMaxSteps][NWT];
+#pragma unroll
+        for (int j = 0; j < kMaxSteps; ++j)
+#pragma unroll
+          for (int w = 0; w < NWT; ++w) inv[j][w] = 0u;
+        const uint32_t tcol = tmem_base + lane_addr + acc * p.n_total + (uint32_t)co_base;
+#pragma unroll
+        for (int ch = 0; ch < NCH / 8; ++ch) {
+          uint32_t d1[8], d2[8];
+          ptx::tmem_ld8(tcol + ch * 8, d1);
+          ptx::tmem_ld8(tcol + p.Cout_pad + ch * 8, d2);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int c = ch * 8 + i;
+            const int co = co_base + c;
+            const float yv = fmaf((float)(int)d1[i], sc[co],
+                                  fmaf((float)(int)d2[i], sc[p.Cout_pad + co], sc[2 * p.Cout_pad + co]));
+            const uint32_t bm = 1u << (c % 32);
+            float v = V[c];
+            if (p.reset == 0) {
+#pragma unroll
+              for (int j = 0; j < kMaxSteps; ++j)
+                if (j < p.nsteps) lif_step<0>(v, yv, decay, vth, vres, inv[j][c / 32], bm, prev[c / 32]);
+            } else if (p.reset == 1) {
+#pragma unroll
+              for (int j = 0; j < kMaxSteps; ++j)
+                if (j < p.nsteps) lif_step<1>(v, yv, decay, vth, vres, inv[j][c / 32], bm, prev[c / 32]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < kMaxSteps; ++j)
+                if (j < p.nsteps) lif_step<2>(v, yv, decay, vth, vres, inv[j][c / 32], bm, prev[c / 32]);
+            }
+            V[c] = v;
+          }
+        }
+        // accumulator consumed: hand TMEM back to the MMA issuer
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(bar_t_empty + 8 * acc, 0);
+
+        // spikes -> staging smem, bit-sliced counters
+        const uint32_t chmask = NCH >= 32 ? 0xFFFFFFFFu : ((1u << NCH) - 1u);
+#pragma unroll
+        for (int j = 0; j < kMaxSteps; ++j) {
+          if (j < p.nsteps) {
+#pragma unroll
+            for (int w = 0; w < NWT; ++w) {
+              const uint32_t s = valid ? (~inv[j][w] & chmask) : 0u;
+              stage[(j * 128 + m) * SROW + half * NWT + w] = s;
+              uint32_t c = s;
+#pragma unroll
+              for (int pl = 0; pl < kPlanes; ++pl) {
+                const uint32_t t = planes[pl][w] & c;
+                planes[pl][w] ^= c;
+                c = t;
+              }
+            }
+          }
+        }
+        steps_acc += p.nsteps;
+        if (p.counts && (steps_acc + p.nsteps > (1 << kPlanes) - 1 || k == p.G - 1)) {
+          flush_counts<NWT>(p, planes, valid, b, co_base, NCH, lane);
+          steps_acc = 0;
+        }
+        ptx::named_bar_sync(1, kEpiWarps * 32);
+
+        // staged spikes -> global packed output
+        const int nwo = p.nwo;
+        if (PATH == PATH_IM2COL && p.pool == 2) {
+          const int ntask = p.nsteps * 32 * nwo;
+          for (int task = tid_e; task < ntask; task += kEpiWarps * 32) {
+            const int wd = task % nwo;
+            const int qi = (task / nwo) % 32;
+            const int j = task / (32 * nwo);
+            int qb, qy, qx;
+            bool qv;
+            PosDecode<PATH>::out(p, L0 + 4 * qi, qb, qy, qx, qv);
+            if (!qv) continue;
+            uint32_t wv = 0;
+#pragma unroll
+            for (int mm = 0; mm < 4; ++mm) {
+              const uint32_t *sr = stage + (j * 128 + 4 * qi + mm) * SROW;
+              wv |= NCH >= 32 ? sr[wd] : (sr[0] | (sr[1] << NCH));
+            }
+            const int t_out = p.mode == 1 ? k : k * p.K + j;
+            uint32_t *row = p.out + (long long)t_out * p.out_st + (long long)qb * p.out_sb +
+                            (long long)(qy >> 1) * p.wpr_out;
+            if (p.Cout % 32 == 0) {
+              row[(qx >> 1) * nwo + wd] = wv;
+            } else {
+              const long long bit = (long long)(qx >> 1) * p.Cout;
+              if (wv) atomicOr(row + (bit >> 5), wv << (bit & 31));
+            }
+          }
+        } else {
+          const int ntask = p.nsteps * 128 * nwo;
+          for (int task = tid_e; task < ntask; task += kEpiWarps * 32) {
+            const int wd = task % nwo;
+            const int mm = (task / nwo) % 128;
+            const int j = task / (128 * nwo);
+            int pb, py, px;
+            bool pv;
+            PosDecode<PATH>::out(p, L0 + mm, pb, py, px, pv);
+            if (!pv) continue;
+            const int t_out = p.mode == 1 ? k : k * p.K + j;
+            uint32_t *base = p.out + (long long)t_out * p.out_st + (long long)pb * p.out_sb;
+            if (p.pool == 2) {
+              // halo path: the 2x2 window may straddle tiles -> leader-in-tile ORs
+              const int y0 = py & ~1, x0 = px & ~1;
+              const long long Lq = ((long long)pb * p.Sh + y0) * p.Sw + x0;
+              const long long mem[4] = {Lq - L0, Lq + 1 - L0, Lq + p.Sw - L0, Lq + p.Sw + 1 - L0};
+              int leader = -1;
+              bool full = true;
+              uint32_t wv = 0;
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                if (mem[t] >= 0 && mem[t] < 128) {
+                  if (leader < 0) leader = (int)mem[t];
+                  const uint32_t *sr = stage + (j * 128 + (int)mem[t]) * SROW;
+                  wv |= NCH >= 32 ? sr[wd] : (sr[0] | (sr[1] << NCH));
+                } else {
+                  full = false;
+                }
+              }
+              if (leader != mm) continue;
+              uint32_t *row = base + (long long)(y0 >> 1) * p.wpr_out;
+              if (p.Cout % 32 == 0) {
+                if (full)
+                  row[(x0 >> 1) * nwo + wd] = wv;
+                else if (wv)
+                  atomicOr(row + (x0 >> 1) * nwo + wd, wv);
+              } else {
+                const long long bit = (long long)(x0 >> 1) * p.Cout;
+                if (wv) atomicOr(row + (bit >> 5), wv << (bit & 31));
+              }
+            } else {
+              const uint32_t *sr = stage + (j * 128 + mm) * SROW;
+              const uint32_t wv = NCH >= 32 ? sr[wd] : (sr[0] | (sr[1] << NCH));
+              uint32_t *row = base + (long long)py * p.wpr_out;
+              if (p.Cout % 32 == 0) {
+                row[px * nwo + wd] = wv;
+              } else {
+                const long long bit = (long long)px * p.Cout;
+                if (wv) atomicOr(row + (bit >> 5), wv << (bit & 31));
+              }
+            }
+          }
+        }
+        ptx::named_bar_sync(1, kEpiWarps * 32);
+      }
+      if (p.v_final && valid) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+          if (co_base + c < p.Cout) p.v_final[vbase + c] = V[c];
+      }
+    }
+  }
+
+  // teardown: every role done in both CTAs before TMEM is released
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 0) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_cg2(tmem_base, p.tmem_cols);
+  }
+}
+
+template <int NCH, int PATH>
+cudaError_t launch_kernel(const TcParams &p, int nclusters, cudaStream_t stream) {
+  auto kern = tc_conv_lif_kernel<NCH, PATH>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)p.smem_bytes);
+  if (e != cudaSuccess) return e;
+  kern<<<dim3(2 * nclusters), dim3(kThreads), p.smem_bytes, stream>>>(p);
+  return cudaGetLastError();
+}
+
+__global__ void tc_zero_kernel(uint32_t *out, int T_out, int B, long long plane, long long st,
+                               long long sb, uint32_t *counts, long long ncounts) {
+  const long long total = (long long)T_out * B * plane;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += stride) {
+    const long long tb = i / plane, o = i - tb * plane;
+    const long long t = tb / B, b = tb - t * B;
+    out[t * st + b * sb + o] = 0u;
+  }
+  if (counts)
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ncounts; i += stride)
+      counts[i] = 0u;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host API --
+bool tc_shape_ok(const tac_conv_lif_desc *d) { return shape_reason(d) == nullptr; }
+bool tc_supported(const tac_conv_lif_desc *d) { return reason(d) == nullptr; }
+const char *tc_unsupported_reason(const tac_conv_lif_desc *d) {
+  const char *r = reason(d);
+  return r ? r : "supported";
+}
+
+size_t tc_weights_bytes(const tac_conv_lif_desc *d) {
+  const Geometry g = geometry(d);
+  return 2 * (size_t)g.w_bytes_cta + 3 * (size_t)g.cout_pad * 4;
+}
+
+// Two int8 slices per output channel, laid out as the smem image of each CTA:
+// halo  : [tap][kc16][n][16 B], K index 32w + 4o + b <-> channel 32w + o + 8b
+// im2col: [kc16 (2)][n][16 B],  K index 4o + r       <-> (r, s = o / C_in, c = o % C_in)
+// followed by fp32 [s1 | s2 | bias] per padded output channel.
+void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bias,
+                unsigned char *dst) {
+  const Geometry g = geometry(d);
+  const int Co = d->C_out, Ci = d->C_in, Cp = g.cout_pad;
+  std::vector<signed char> q1((size_t)Cp * Ci * 9, 0), q2((size_t)Cp * Ci * 9, 0);
+  std::vector<float> s1(Cp, 0.f), s2(Cp, 0.f), bs(Cp, 0.f);
+  for (int co = 0; co < Co; ++co) {
+    double amax = 0.0;
+    for (int i = 0; i < Ci * 9; ++i) amax = std::max(amax, std::fabs((double)weight[(size_t)co * Ci * 9 + i]));
+    if (amax == 0.0) continue;
+    const double sc1 = amax / 127.0, sc2 = sc1 / 254.0;
+    s1[co] = (float)sc1;
+    s2[co] = (float)sc2;
+    for (int i = 0; i < Ci * 9; ++i) {
+      const double w = weight[(size_t)co * Ci * 9 + i];
+      const double a = std::max(-127.0, std::min(127.0, std::nearbyint(w / sc1)));
+      const double r = w - a * (double)s1[co];
+      const double b = std::max(-127.0, std::min(127.0, std::nearbyint(r / (double)s2[co])));
+      q1[(size_t)co * Ci * 9 + i] = (signed char)a;
+      q2[(size_t)co * Ci * 9 + i] = (signed char)b;
+    }
+    bs[co] = bias ? bias[co] : 0.f;
+  }
+  auto q_at = [&](int half, int co, int ci, int r, int s) -> signed char {
+    const std::vector<signed char> &q = half ? q2 : q1;
+    return q[(((size_t)co * Ci + ci) * 3 + r) * 3 + s];
+  };
+  for (int half = 0; half < 2; ++half) {
+    unsigned char *img = dst + (size_t)half * g.w_bytes_cta;
+    std::memset(img, 0, g.w_bytes_cta);
+    if (g.path == PATH_HALO) {
+      for (int tap = 0; tap < 9; ++tap)
+        for (int kidx = 0; kidx < Ci; ++kidx) {
+          const int w32 = kidx / 32, o = (kidx % 32) / 4, b = kidx % 4;
+          const int ci = 32 * w32 + o + 8 * b;
+          const int kc = kidx / 16, byte = kidx % 16;
+          for (int n = 0; n < Cp; ++n)
+            img[(((size_t)tap * g.nkc + kc) * Cp + n) * 16 + byte] =
+                (unsigned char)(n < Co ? q_at(half, n, ci, tap / 3, tap % 3) : 0);
+        }
+    } else {
+      for (int kidx = 0; kidx < 32; ++kidx) {
+        const int o = kidx / 4, r = kidx % 4;
+        if (r >= 3 || o >= 3 * Ci) continue;
+        const int s = o / Ci, c = o % Ci;
+        const int kc = kidx / 16, byte = kidx % 16;
+        for (int n = 0; n < Co; ++n)
+          img[((size_t)kc * Cp + n) * 16 + byte] = (unsigned char)q_at(half, n, c, r, s);
+      }
+    }
+  }
+  float *sb = reinterpret_cast<float *>(dst + 2 * (size_t)g.w_bytes_cta);
+  for (int i = 0; i < Cp; ++i) {
+    sb[i] = s1[i];
+    sb[Cp + i] = s2[i];
+    sb[2 * Cp + i] = bs[i];
+  }
+}
+
+int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned char *tc_prep,
+              void *stream, int *launches) {
+  const Geometry g = geometry(d);
+  TcParams p{};
+  p.B = lp.B; p.H = lp.H; p.W = lp.W; p.Cin = lp.Cin; p.Cout = lp.Cout; p.Cout_pad = g.cout_pad;
+  p.pad = lp.pad; p.Ho = lp.Ho; p.Wo = lp.Wo; p.Hq = lp.Hq; p.Wq = lp.Wq; p.pool = lp.pool;
+  p.K = lp.K; p.G = lp.G; p.nsteps = lp.nsteps; p.mode = lp.mode; p.reset = lp.reset;
+  p.Sh = g.Sh; p.Sw = g.Sw;
+  p.M_total = g.path == PATH_HALO ? (long long)lp.B * g.Sh * g.Sw : (long long)lp.B * lp.Ho * lp.Wo;
+  p.num_tiles = (int)((p.M_total + 127) / 128);
+  p.num_pairs = (p.num_tiles + 1) / 2;
+  p.halo_rows = g.halo_rows; p.nkc = g.nkc; p.ntaps = g.ntaps;
+  p.m_shift = d->mode == TAC_MODE_DENSE ? 0 : beta_shift(d->beta);
+  p.wpr_in = lp.wpr_in; p.wpr_out = lp.wpr_out;
+  p.nwo = lp.Cout % 32 == 0 ? lp.Cout / 32 : 1;
+  p.out_atomic = ((g.path == PATH_HALO && lp.pool == 2) || lp.Cout % 32 != 0) ? 1 : 0;
+  p.in_st = lp.in_st; p.in_sb = lp.in_sb; p.out_st = lp.out_st; p.out_sb = lp.out_sb;
+  p.decay = lp.decay; p.v_th = lp.v_th; p.v_reset = lp.v_reset;
+  p.agg_scale = (float)std::ldexp(1.0, -p.m_shift * (lp.K - 1));
+  p.off_w = g.off_w; p.off_a = g.off_a; p.a_stage_bytes = g.a_stage_bytes;
+  p.off_stage = g.off_stage; p.off_scale = g.off_scale; p.off_bar = g.off_bar;
+  p.smem_bytes = g.smem_bytes; p.w_bytes_cta = g.w_bytes_cta;
+  p.n_total = 2u * g.cout_pad;
+  uint32_t cols = 32;
+  while (cols < 2u * p.n_total) cols <<= 1;
+  p.tmem_cols = cols;
+  p.lbo_a = g.path == PATH_HALO ? (uint32_t)g.halo_rows * 16u : 128u * 16u;
+  p.lbo_b = (uint32_t)g.cout_pad * 16u;
+  for (int t = 0; t < 9; ++t) p.tap_off[t] = g.path == PATH_HALO ? (t / 3) * g.Sw + (t % 3) : 0;
+  p.in = lp.in; p.out = lp.out; p.v_init = lp.v_init; p.v_final = lp.v_final; p.counts = lp.counts;
+  p.w_img = tc_prep;
+  p.scale_bias = reinterpret_cast<const float *>(tc_prep + 2 * (size_t)g.w_bytes_cta);
+
+  cudaStream_t st = (cudaStream_t)stream;
+  if (p.out_atomic || p.counts) {
+    const long long plane = p.out_atomic ? (long long)lp.Hq * lp.wpr_out : 0;
+    const long long total = std::max((long long)lp.T_out * lp.B * plane, (long long)lp.B * lp.Cout);
+    const int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+    tc_zero_kernel<<<std::max(grid, 1), 256, 0, st>>>(p.out, lp.T_out, lp.B, plane, lp.out_st,
+                                                       lp.out_sb, p.counts, (long long)lp.B * lp.Cout);
+    ++*launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return (int)e;
+  }
+  const int nclusters = std::max(1, std::min(p.num_pairs, 74));
+  cudaError_t e = cudaSuccess;
+  const int nch = g.cout_pad / 2;
+  if (g.path == PATH_HALO) {
+    switch (nch) {
+      case 8: e = launch_kernel<8, PATH_HALO>(p, nclusters, st); break;
+      case 16: e = launch_kernel<16, PATH_HALO>(p, nclusters, st); break;
+      case 32: e = launch_kernel<32, PATH_HALO>(p, nclusters, st); break;
+      default: e = launch_kernel<64, PATH_HALO>(p, nclusters, st); break;
+    }
+  } else {
+    switch (nch) {
+      case 8: e = launch_kernel<8, PATH_IM2COL>(p, nclusters, st); break;
+      case 16: e = launch_kernel<16, PATH_IM2COL>(p, nclusters, st); break;
+      case 32: e = launch_kernel<32, PATH_IM2COL>(p, nclusters, st); break;
+      default: e = launch_kernel<64, PATH_IM2COL>(p, nclusters, st); break;
+    }
+  }
+  ++*launches;
+  return (int)e;
+}
+
 }  // namespace tacsnn
