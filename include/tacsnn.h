@@ -139,7 +139,7 @@ tac_status tac_workspace_bytes(const tac_conv_lif_desc *desc, size_t *bytes);
 
 /* The layer (one call = whole sequence, all groups).
  *   prepared   device, from tac_prepare_weights with an identical desc
- *   spikes_in  device u32, packed layout above (16-B aligned for TCGEN05)
+ *   spikes_in  device u32, packed layout above (4-B aligned)
  *   v_init     device fp32 [B][H'][W'][C_out] or NULL (= 0)
  *   spikes_out device u32, packed, T_out x B x H_o x WPR_out (with strides)
  *   v_final    device fp32 [B][H'][W'][C_out] or NULL (not written)

@@ -236,9 +236,6 @@ tac_status tac_conv_lif_forward(const tac_conv_lif_desc *desc, const void *prepa
                 tacsnn::tc_unsupported_reason(desc));
   if ((uintptr_t)spikes_in % 4 || (uintptr_t)spikes_out % 4 || (uintptr_t)prepared % 256)
     return fail(TAC_ERR_ALIGN, "misaligned pointer");
-  if (engine == TAC_ENGINE_TCGEN05 && ((uintptr_t)spikes_in % 16 || (uintptr_t)spikes_out % 16 ||
-                                       g.in_sb % 4 || g.in_st % 4 || g.out_sb % 4 || g.out_st % 4))
-    return fail(TAC_ERR_ALIGN, "TCGEN05 needs 16-B aligned spike buffers and strides");
   if (v_init && (uintptr_t)v_init % 16) return fail(TAC_ERR_ALIGN, "v_init must be 16-B aligned");
   if (v_final && (uintptr_t)v_final % 16) return fail(TAC_ERR_ALIGN, "v_final must be 16-B aligned");
   if (counts && (uintptr_t)counts % 4) return fail(TAC_ERR_ALIGN, "counts misaligned");
