@@ -64,10 +64,10 @@ struct TcParams {
   long long M_total;
   int num_tiles, num_pairs;
   int halo_rows, nkc, ntaps, m_shift;
-  int wpr_in, wpr_out, nwo, out_atomic;
+  int wpr_in, wpr_out, nwo, out_atomic, int_combine;
   long long in_st, in_sb, out_st, out_sb;
   float decay, v_th, v_reset, agg_scale;
-  uint32_t off_w, off_a, a_stage_bytes, off_stage, off_scale, off_bar, smem_bytes;
+  uint32_t off_w, off_a, a_stage_bytes, off_stage, off_pinfo, off_scale, off_bar, smem_bytes;
   uint32_t w_bytes_cta, tmem_cols, n_total, lbo_a, lbo_b;
   int tap_off[9];
   const uint32_t *in;
@@ -101,8 +101,8 @@ int path_of(const tac_conv_lif_desc *d) {
 
 struct Geometry {
   int path, Sh, Sw, halo_rows, nkc, ntaps, cout_pad, nsteps;
-  uint32_t w_bytes_cta, a_stage_bytes, stage_bytes, off_w, off_a, off_stage, off_scale, off_bar,
-      smem_bytes;
+  uint32_t w_bytes_cta, a_stage_bytes, stage_bytes, off_w, off_a, off_stage, off_pinfo, off_scale,
+      off_bar, smem_bytes;
 };
 
 uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
@@ -135,8 +135,9 @@ Geometry geometry(const tac_conv_lif_desc *d) {
   g.off_w = 0;
   g.off_a = align_up(g.w_bytes_cta, 1024);
   g.off_stage = align_up(g.off_a + kStages * g.a_stage_bytes, 128);
-  g.off_scale = align_up(g.off_stage + g.stage_bytes, 128);
-  g.off_bar = align_up(g.off_scale + 3u * g.cout_pad * 4u, 64);
+  g.off_pinfo = align_up(g.off_stage + g.stage_bytes, 128);
+  g.off_scale = align_up(g.off_pinfo + 128u * 16u, 128);
+  g.off_bar = align_up(g.off_scale + 4u * g.cout_pad * 4u, 64);
   g.smem_bytes = g.off_bar + 8u * (2 * kStages + 2 * kAccs + 1) + 16u;
   return g;
 }
@@ -167,46 +168,51 @@ const char *reason(const tac_conv_lif_desc *d) {
 }
 
 // ------------------------------------------------------------ device code ---
-template <int PATH>
-struct PosDecode {
-  // output position L -> (b, y, x) and validity
-  __device__ __forceinline__ static void out(const TcParams &p, long long L, int &b, int &y,
-                                             int &x, bool &valid) {
-    if (PATH == PATH_HALO) {
-      const long long per = (long long)p.Sh * p.Sw;
-      const long long bb = L / per;
-      const int rem = (int)(L - bb * per);
-      y = rem / p.Sw;
-      x = rem - y * p.Sw;
-      b = (int)bb;
-      valid = bb < p.B && y < p.Ho && x < p.Wo;
-    } else if (p.pool == 2) {  // quad-major: the 4 members of a 2x2 pool window adjacent
-      const long long q = L >> 2;
-      const int mem = (int)(L & 3);
-      const long long per = (long long)p.Hq * p.Wq;
-      const long long bb = q / per;
-      const int rq = (int)(q - bb * per);
-      const int py = rq / p.Wq, px = rq - (rq / p.Wq) * p.Wq;
-      y = 2 * py + (mem >> 1);
-      x = 2 * px + (mem & 1);
-      b = (int)bb;
-      valid = bb < p.B;
-    } else {
-      const long long per = (long long)p.Ho * p.Wo;
-      const long long bb = L / per;
-      const int rem = (int)(L - bb * per);
-      y = rem / p.Wo;
-      x = rem - y * p.Wo;
-      b = (int)bb;
-      valid = bb < p.B;
-    }
-  }
+// Per-position output descriptor, rebuilt at the start of every tile by the
+// epilogue (replaces per-task 64-bit divisions in the store pass).
+struct __align__(16) PInfo {
+  long long off;  // word offset of this position's output in a (t) plane; -1: no store
+  int org;        // pooled halo path: tile-local index of the 2x2 window origin
+  int aux;        // bits 0-3: in-tile member mask (pooled halo), bits 8-12: bit shift
 };
+
+template <int PATH>
+__device__ __forceinline__ void decode_out(const TcParams &p, long long L, int &b, int &y, int &x,
+                                           bool &valid) {
+  if (PATH == PATH_HALO) {
+    const long long per = (long long)p.Sh * p.Sw;
+    const long long bb = L / per;
+    const int rem = (int)(L - bb * per);
+    y = rem / p.Sw;
+    x = rem - y * p.Sw;
+    b = (int)bb;
+    valid = bb < p.B && y < p.Ho && x < p.Wo;
+  } else if (p.pool == 2) {  // quad-major: the 4 members of a 2x2 pool window adjacent
+    const long long q = L >> 2;
+    const int mem = (int)(L & 3);
+    const long long per = (long long)p.Hq * p.Wq;
+    const long long bb = q / per;
+    const int rq = (int)(q - bb * per);
+    const int py = rq / p.Wq, px = rq - (rq / p.Wq) * p.Wq;
+    y = 2 * py + (mem >> 1);
+    x = 2 * px + (mem & 1);
+    b = (int)bb;
+    valid = bb < p.B;
+  } else {
+    const long long per = (long long)p.Ho * p.Wo;
+    const long long bb = L / per;
+    const int rem = (int)(L - bb * per);
+    y = rem / p.Wo;
+    x = rem - y * p.Wo;
+    b = (int)bb;
+    valid = bb < p.B;
+  }
+}
 
 // --- producers: build the u8 aggregate A_k * 2^{m(K-1)} in the MMA layout ---
 __device__ __forceinline__ void agg_word(uint32_t (&o)[8], const uint32_t (&xj)[kMaxSteps],
                                          int K, int m) {
-  // byte b of output word o <- input channel (o + 8b) of the 32-channel word;
+  // byte b of output word q <- input channel (q + 8b) of the 32-channel word;
   // bit e_j = m*j of that byte <- frame j  (weights 2^{m j}, oldest frame = 1)
 #pragma unroll
   for (int j = 0; j < kMaxSteps; ++j) {
@@ -221,29 +227,38 @@ __device__ __forceinline__ void agg_word(uint32_t (&o)[8], const uint32_t (&xj)[
 
 __device__ __forceinline__ void produce_halo(const TcParams &p, int tile, int k, uint32_t a_stage,
                                              int ptid) {
+  // thread owns 32-channel word w of halo rows row0, row0 + rstep, ... (96 % nwin == 0)
   const int nwin = p.Cin >> 5;
-  const int ntask = p.halo_rows * nwin;
-  const long long L0 = (long long)tile * 128;
+  const int w = ptid % nwin, row0 = ptid / nwin, rstep = (kProdWarps * 32) / nwin;
+  const long long L = (long long)tile * 128 + row0;
   const long long per = (long long)p.Sh * p.Sw;
-  const uint32_t *frame0 = p.in + (long long)(k * p.K) * p.in_st;
-  for (int task = ptid; task < ntask; task += kProdWarps * 32) {
-    const int row = task / nwin, w = task - (task / nwin) * nwin;
-    const long long L = L0 + row;
-    const long long bb = L / per;
-    const int rem = (int)(L - bb * per);
-    const int yy = rem / p.Sw, xx = rem - (rem / p.Sw) * p.Sw;
+  long long bb = L / per;
+  int rem = (int)(L - bb * per);
+  int yy = rem / p.Sw, xx = rem - (rem / p.Sw) * p.Sw;
+  const uint32_t *frame0 = p.in + (long long)(k * p.K) * p.in_st + w;
+  const int K = p.K, mshift = p.m_shift;
+  const long long in_st = p.in_st;
+  for (int row = row0; row < p.halo_rows; row += rstep) {
     const int yi = yy - p.pad, xi = xx - p.pad;
     uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (bb < p.B && yi >= 0 && yi < p.H && xi >= 0 && xi < p.W) {
-      const uint32_t *src = frame0 + bb * p.in_sb + (long long)yi * p.wpr_in + xi * nwin + w;
+      const uint32_t *src = frame0 + bb * p.in_sb + (long long)yi * p.wpr_in + xi * nwin;
       uint32_t xj[kMaxSteps];
 #pragma unroll
-      for (int j = 0; j < kMaxSteps; ++j) xj[j] = (j < p.K) ? __ldg(src + j * p.in_st) : 0u;
-      agg_word(o, xj, p.K, p.m_shift);
+      for (int j = 0; j < kMaxSteps; ++j) xj[j] = (j < K) ? __ldg(src + j * in_st) : 0u;
+      agg_word(o, xj, K, mshift);
     }
     const uint32_t dst = a_stage + (uint32_t)(2 * w) * p.lbo_a + (uint32_t)row * 16u;
     ptx::st_shared_v4(dst, o[0], o[1], o[2], o[3]);
     ptx::st_shared_v4(dst + p.lbo_a, o[4], o[5], o[6], o[7]);
+    xx += rstep;  // advance the padded-linear position by rstep rows
+    while (xx >= p.Sw) {
+      xx -= p.Sw;
+      if (++yy == p.Sh) {
+        yy = 0;
+        ++bb;
+      }
+    }
   }
 }
 
@@ -254,7 +269,7 @@ __device__ __forceinline__ void produce_im2col(const TcParams &p, int tile, int 
   for (int pos = ptid; pos < 128; pos += kProdWarps * 32) {
     int b, y, x;
     bool valid;
-    PosDecode<PATH_IM2COL>::out(p, L0 + pos, b, y, x, valid);
+    decode_out<PATH_IM2COL>(p, L0 + pos, b, y, x, valid);
     uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (valid) {
       const int bit0 = (x - p.pad) * p.Cin;
@@ -322,7 +337,8 @@ __device__ __forceinline__ void flush_counts(const TcParams &p, uint32_t (&plane
         total += warp_col_popc(mine ? planes[pl][w] : 0u, lane) << pl;
       const int c = w * 32 + (int)lane;
       const int co = co_base + c;
-      if (total && c < nch && co < p.Cout) atomicAdd(p.counts + (long long)bsel * p.Cout + co, total);
+      if (total && c < nch && co < p.Cout)
+        atomicAdd(p.counts + (long long)bsel * p.Cout + co, total);
     }
   }
 #pragma unroll
@@ -331,10 +347,10 @@ __device__ __forceinline__ void flush_counts(const TcParams &p, uint32_t (&plane
     for (int w = 0; w < NWT; ++w) planes[pl][w] = 0u;
 }
 
+// generic (runtime reset mode) LIF step; inv_bits collects NOT(spike) at `bitmask`
 template <int RESET>
 __device__ __forceinline__ void lif_step(float &v, float y, float decay, float vth, float vres,
                                          uint32_t &inv_bits, uint32_t bitmask, uint32_t &prev) {
-  // one LIF step; inv_bits collects NOT(spike) at `bitmask`
   v = fmaf(decay, v, y);                                    // Alg.1 l.5 / Alg.2 l.6 / Eq.(1)
   if (RESET == 1) v -= (prev & bitmask) ? vth : 0.f;        // delayed: - v_th s_{t-1}
   const float v2 = v - vth;
@@ -347,11 +363,288 @@ __device__ __forceinline__ void lif_step(float &v, float y, float decay, float v
   if (RESET == 1) prev = (prev & ~bitmask) | (~(uint32_t)msk & bitmask);
 }
 
+// two neurons, NS steps sharing one drive (TAC-TP) or NS = 1 (TAC / dense), subtract
+// reset, packed fp32x2 arithmetic (identical rounding to the scalar form)
+template <int NS>
+__device__ __forceinline__ void lif_pair_sub(float2 &v, float2 y, float2 dec2, float2 nth2,
+                                             uint32_t (&inv)[NS], uint32_t b0, uint32_t b1) {
+#pragma unroll
+  for (int j = 0; j < NS; ++j) {
+    v = __ffma2_rn(dec2, v, y);
+    const float2 v2 = __fadd2_rn(v, nth2);
+    const int m0 = __float_as_int(v2.x) >> 31, m1 = __float_as_int(v2.y) >> 31;
+    v.x = __int_as_float((__float_as_int(v2.x) & ~m0) | (__float_as_int(v.x) & m0));
+    v.y = __int_as_float((__float_as_int(v2.y) & ~m1) | (__float_as_int(v.y) & m1));
+    inv[j] |= ((uint32_t)m0 & b0) | ((uint32_t)m1 & b1);
+  }
+}
+
+// Y for 8 channels from the two s32 accumulator slices (see file header)
+__device__ __forceinline__ void combine8(const TcParams &p, const float *sc, int co,
+                                         const uint32_t (&d1)[8], const uint32_t (&d2)[8],
+                                         float (&y)[8]) {
+  const int Cp = p.Cout_pad;
+  if (p.int_combine) {
+    // X = 254 D_hi + D_lo exactly in s32;  Y = X * (s1 agg / 254) + b
+    const float4 sa = *reinterpret_cast<const float4 *>(sc + co);
+    const float4 sb = *reinterpret_cast<const float4 *>(sc + co + 4);
+    const float4 ba = *reinterpret_cast<const float4 *>(sc + Cp + co);
+    const float4 bb = *reinterpret_cast<const float4 *>(sc + Cp + co + 4);
+    const float s8[8] = {sa.x, sa.y, sa.z, sa.w, sb.x, sb.y, sb.z, sb.w};
+    const float b8[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int X = (int)d1[i] * 254 + (int)d2[i];
+      y[i] = fmaf((float)X, s8[i], b8[i]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float s1 = sc[2 * Cp + co + i], s2 = sc[3 * Cp + co + i], b = sc[Cp + co + i];
+      y[i] = fmaf((float)(int)d1[i], s1, fmaf((float)(int)d2[i], s2, b));
+    }
+  }
+}
+
+// NS > 0: subtract reset with NS LIF steps per group (specialised hot path);
+// NS == 0: any reset, runtime step count.
+template <int NCH, int PATH, int NS>
+__device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, uint32_t tmem_base,
+                                              uint32_t bar_t_full, uint32_t bar_t_empty, int cid,
+                                              int ncl, uint32_t rank, uint32_t warp,
+                                              uint32_t lane) {
+  constexpr int NWT = NCH >= 32 ? NCH / 32 : 1;  // spike words per epilogue thread
+  constexpr int SROW = NCH >= 32 ? 2 * NWT : 2;  // stage words per position
+  constexpr int NSM = NS ? NS : kMaxSteps;
+  const float *sc = reinterpret_cast<const float *>(smem + p.off_scale);
+  uint32_t *stage = reinterpret_cast<uint32_t *>(smem + p.off_stage);
+  PInfo *pinfo = reinterpret_cast<PInfo *>(smem + p.off_pinfo);
+  const int e = (int)warp - 1 - kProdWarps;  // 0..7
+  const int quad = (int)(warp & 3);           // TMEM lane quadrant of this warp
+  const int half = e >> 2;                    // channel half
+  const int m = quad * 32 + (int)lane;        // position within the CTA tile
+  const int tid_e = e * 32 + (int)lane;       // 0..255
+  const int co_base = half * NCH;
+  const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+  const float decay = p.decay, vth = p.v_th, vres = p.v_reset;
+  const float2 dec2 = make_float2(decay, decay), nth2 = make_float2(-vth, -vth);
+  const int nsteps = NS ? NS : p.nsteps;
+  const int G = p.G, K = p.K, mode = p.mode, nwo = p.nwo, Cout = p.Cout, Cp = p.Cout_pad;
+  const uint32_t chmask = NCH >= 32 ? 0xFFFFFFFFu : ((1u << NCH) - 1u);
+  uint32_t it = 0;
+  for (int pair = cid; pair < p.num_pairs; pair += ncl) {
+    const int tile = 2 * pair + (int)rank;
+    const long long L0 = (long long)tile * 128;
+    int b, y, x;
+    bool valid;
+    decode_out<PATH>(p, L0 + m, b, y, x, valid);
+    if (half == 0) {  // per-tile output descriptors (read by the store pass)
+      PInfo pi;
+      pi.off = -1;
+      pi.org = 0;
+      pi.aux = 0;
+      if (valid) {
+        int yo = y, xo = x;
+        bool store = true;
+        if (p.pool == 2) {
+          yo = y >> 1;
+          xo = x >> 1;
+          if (PATH == PATH_IM2COL) {
+            store = (m & 3) == 0;
+          } else {
+            const int y0 = y & ~1, x0 = x & ~1;
+            const long long Lq = ((long long)b * p.Sh + y0) * p.Sw + x0;
+            const long long org = Lq - L0;
+            const long long mem[4] = {org, org + 1, org + p.Sw, org + p.Sw + 1};
+            int mask = 0, leader = -1;
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              if (mem[t] >= 0 && mem[t] < 128) {
+                mask |= 1 << t;
+                if (leader < 0) leader = (int)mem[t];
+              }
+            store = leader == m;
+            pi.org = (int)org;
+            pi.aux = mask;
+          }
+        }
+        if (store) {
+          const long long rowoff = (long long)b * p.out_sb + (long long)yo * p.wpr_out;
+          if (Cout % 32 == 0) {
+            pi.off = rowoff + (long long)xo * nwo;
+          } else {
+            const long long bit = (long long)xo * Cout;
+            pi.off = rowoff + (bit >> 5);
+            pi.aux |= (int)(bit & 31) << 8;
+          }
+        }
+      }
+      pinfo[m] = pi;
+    }
+    const long long vbase = (((long long)b * p.Ho + y) * p.Wo + x) * Cout + co_base;
+    float2 V[NCH / 2];
+    uint32_t prev[NWT];
+    uint32_t planes[kPlanes][NWT];
+    int steps_acc = 0;
+#pragma unroll
+    for (int w = 0; w < NWT; ++w) {
+      prev[w] = 0u;
+#pragma unroll
+      for (int pl = 0; pl < kPlanes; ++pl) planes[pl][w] = 0u;
+    }
+#pragma unroll
+    for (int c = 0; c < NCH; c += 2) {
+      float v0 = 0.f, v1 = 0.f;
+      if (p.v_init && valid) {
+        if (co_base + c < Cout) v0 = __ldg(p.v_init + vbase + c);
+        if (co_base + c + 1 < Cout) v1 = __ldg(p.v_init + vbase + c + 1);
+      }
+      V[c / 2] = make_float2(v0, v1);
+      if (NS == 0 && p.reset == 1) {  // reading R4
+        if (v0 >= vth) prev[c / 32] |= 1u << (c % 32);
+        if (v1 >= vth) prev[(c + 1) / 32] |= 1u << ((c + 1) % 32);
+      }
+    }
+    for (int k = 0; k < G; ++k, ++it) {
+      const uint32_t acc = it % kAccs, aph = (it / kAccs) & 1u;
+      ptx::mbar_wait(bar_t_full + 8 * acc, aph);
+      ptx::tc_fence_after();
+      uint32_t inv[NSM][NWT];
+#pragma unroll
+      for (int j = 0; j < NSM; ++j)
+#pragma unroll
+        for (int w = 0; w < NWT; ++w) inv[j][w] = 0u;
+      const uint32_t tcol = tmem_base + lane_addr + acc * p.n_total + (uint32_t)co_base;
+      uint32_t d[2][2][8];  // [buffer][hi/lo][col]
+      ptx::tmem_ld8(tcol, d[0][0]);
+      ptx::tmem_ld8(tcol + Cp, d[0][1]);
+      ptx::tmem_wait_ld_dep(d[0][0], d[0][1]);
+#pragma unroll
+      for (int ch = 0; ch < NCH / 8; ++ch) {
+        const int cur = ch & 1, nxt = cur ^ 1;
+        if (ch + 1 < NCH / 8) {  // prefetch the next 8 columns while this chunk computes
+          ptx::tmem_ld8(tcol + (ch + 1) * 8, d[nxt][0]);
+          ptx::tmem_ld8(tcol + Cp + (ch + 1) * 8, d[nxt][1]);
+        }
+        float yv[8];
+        combine8(p, sc, co_base + ch * 8, d[cur][0], d[cur][1], yv);
+        if (NS > 0) {
+#pragma unroll
+          for (int i = 0; i < 8; i += 2) {
+            const int c = ch * 8 + i;
+            constexpr int NSP = (NS > 0) ? NS : 1;
+            uint32_t invp[NSP];
+#pragma unroll
+            for (int j = 0; j < NSP; ++j) invp[j] = 0u;
+            lif_pair_sub<NSP>(V[c / 2], make_float2(yv[i], yv[i + 1]), dec2, nth2, invp,
+                              1u << (c % 32), 1u << ((c + 1) % 32));
+#pragma unroll
+            for (int j = 0; j < NSP; ++j) inv[j][c / 32] |= invp[j];
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int c = ch * 8 + i;
+            const uint32_t bm = 1u << (c % 32);
+            float v = (i & 1) ? V[c / 2].y : V[c / 2].x;
+            const int rs = p.reset;
+#pragma unroll
+            for (int j = 0; j < kMaxSteps; ++j) {
+              if (j < nsteps) {
+                if (rs == 0) lif_step<0>(v, yv[i], decay, vth, vres, inv[j][c / 32], bm, prev[c / 32]);
+                else if (rs == 1) lif_step<1>(v, yv[i], decay, vth, vres, inv[j][c / 32], bm, prev[c / 32]);
+                else lif_step<2>(v, yv[i], decay, vth, vres, inv[j][c / 32], bm, prev[c / 32]);
+              }
+            }
+            if (i & 1) V[c / 2].y = v; else V[c / 2].x = v;
+          }
+        }
+        if (ch + 1 < NCH / 8) ptx::tmem_wait_ld_dep(d[nxt][0], d[nxt][1]);
+      }
+      // accumulator consumed: hand TMEM back to the MMA issuer
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(bar_t_empty + 8 * acc, 0);
+
+      // spikes -> staging smem, bit-sliced counters
+#pragma unroll
+      for (int j = 0; j < NSM; ++j) {
+        if (NS > 0 || j < nsteps) {
+#pragma unroll
+          for (int w = 0; w < NWT; ++w) {
+            const uint32_t s = valid ? (~inv[j][w] & chmask) : 0u;
+            stage[(j * 128 + m) * SROW + half * NWT + w] = s;
+            uint32_t c = s;
+#pragma unroll
+            for (int pl = 0; pl < kPlanes; ++pl) {
+              const uint32_t t = planes[pl][w] & c;
+              planes[pl][w] ^= c;
+              c = t;
+            }
+          }
+        }
+      }
+      steps_acc += nsteps;
+      if (p.counts && (steps_acc + nsteps > (1 << kPlanes) - 1 || k == G - 1)) {
+        flush_counts<NWT>(p, planes, valid, b, co_base, NCH, lane);
+        steps_acc = 0;
+      }
+      ptx::named_bar_sync(1, kEpiWarps * 32);
+
+      // staged spikes -> global packed output
+      const int ntask = nsteps * 128 * nwo;
+      for (int task = tid_e; task < ntask; task += kEpiWarps * 32) {
+        const int wd = task % nwo;
+        const int mm = (task / nwo) & 127;
+        const int j = task / (nwo * 128);
+        const PInfo pi = pinfo[mm];
+        if (pi.off < 0) continue;
+        const uint32_t *st = stage + j * 128 * SROW;
+        auto pix = [&](int q) -> uint32_t {
+          const uint32_t *sr = st + q * SROW;
+          return NCH >= 32 ? sr[wd] : (sr[0] | (sr[1] << NCH));
+        };
+        uint32_t wv;
+        bool full = true;
+        if (p.pool == 2 && PATH == PATH_IM2COL) {
+          wv = pix(mm) | pix(mm + 1) | pix(mm + 2) | pix(mm + 3);
+        } else if (p.pool == 2) {
+          const int mask = pi.aux & 15;
+          wv = 0;
+          if (mask & 1) wv |= pix(pi.org);
+          if (mask & 2) wv |= pix(pi.org + 1);
+          if (mask & 4) wv |= pix(pi.org + p.Sw);
+          if (mask & 8) wv |= pix(pi.org + p.Sw + 1);
+          full = mask == 15;
+        } else {
+          wv = pix(mm);
+        }
+        const int t_out = mode == 1 ? k : k * K + j;
+        uint32_t *dst = p.out + (long long)t_out * p.out_st + pi.off;
+        if (Cout % 32 == 0) {
+          if (full)
+            dst[wd] = wv;
+          else if (wv)
+            atomicOr(dst + wd, wv);
+        } else if (wv) {
+          atomicOr(dst, wv << ((pi.aux >> 8) & 31));
+        }
+      }
+      ptx::named_bar_sync(1, kEpiWarps * 32);
+    }
+    if (p.v_final && valid) {
+#pragma unroll
+      for (int c = 0; c < NCH; c += 2) {
+        if (co_base + c < Cout) p.v_final[vbase + c] = V[c / 2].x;
+        if (co_base + c + 1 < Cout) p.v_final[vbase + c + 1] = V[c / 2].y;
+      }
+    }
+  }
+}
+
 template <int NCH, int PATH>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_conv_lif_kernel(const __grid_constant__ TcParams p) {
-  constexpr int NWT = NCH >= 32 ? NCH / 32 : 1;  // spike words per epilogue thread
-  constexpr int SROW = NCH >= 32 ? 2 * NWT : 2;  // stage words per position
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = ptx::cluster_ctarank();
@@ -361,9 +654,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t bar_t_full = bar_a_empty + 8 * kStages;
   const uint32_t bar_t_empty = bar_t_full + 8 * kAccs;
   const uint32_t bar_w = bar_t_empty + 8 * kAccs;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + p.off_bar + 8 * (2 * kStages + 2 * kAccs + 1));
-  float *sc = reinterpret_cast<float *>(smem + p.off_scale);  // [S1*agg | S2*agg | bias]
-  uint32_t *stage = reinterpret_cast<uint32_t *>(smem + p.off_stage);
+  uint32_t *tmem_slot =
+      reinterpret_cast<uint32_t *>(smem + p.off_bar + 8 * (2 * kStages + 2 * kAccs + 1));
+  float *sc = reinterpret_cast<float *>(smem + p.off_scale);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -386,8 +679,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     ptx::tmem_alloc_cg2(ptx::smem_u32(tmem_slot), p.tmem_cols);
     ptx::tmem_relinquish_cg2();
   }
-  for (int i = threadIdx.x; i < 3 * p.Cout_pad; i += kThreads)
-    sc[i] = p.scale_bias[i] * (i < 2 * p.Cout_pad ? p.agg_scale : 1.f);
+  for (int i = threadIdx.x; i < 4 * p.Cout_pad; i += kThreads) {
+    const float f = p.scale_bias[i];
+    sc[i] = (i / p.Cout_pad == 1) ? f : f * p.agg_scale;  // [s1/254 | bias | s1 | s2]
+  }
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
@@ -398,29 +693,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int ncl = (int)ptx::nclusters_x();
   const int cid = (int)ptx::cluster_id_x();
 
+  // register rebalance: MMA + producer warpgroup gives registers to the epilogue
+  if (warp < 4)
+    ptx::setmaxnreg_dec<88>();
+  else
+    ptx::setmaxnreg_inc<208>();
+
   if (warp == 0) {
     // ================================ MMA issuer (CTA 0 of the pair) =========
     if (rank == 0 && lane == 0) {
       const uint32_t idesc = ptx::idesc_i8(256, p.n_total);
       const uint32_t n_half_bytes = (uint32_t)p.Cout_pad * 16u;
+      const uint32_t w_base = sbase + p.off_w;
+      const int ntaps = p.ntaps, nkc2 = p.nkc >> 1;
       uint32_t it = 0;
       for (int pair = cid; pair < p.num_pairs; pair += ncl) {
         for (int k = 0; k < p.G; ++k, ++it) {
           const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
           const uint32_t acc = it % kAccs, aph = (it / kAccs) & 1u;
-          ptx::mbar_wait_cluster(bar_t_empty + 8 * acc, aph ^ 1u);
-          ptx::mbar_wait_cluster(bar_a_full + 8 * s, ph);
+          ptx::mbar_wait(bar_t_empty + 8 * acc, aph ^ 1u);
+          ptx::mbar_wait(bar_a_full + 8 * s, ph);
           ptx::tc_fence_after();
           const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
           const uint32_t d_tmem = tmem_base + acc * p.n_total;
-          for (int tap = 0; tap < p.ntaps; ++tap) {
-            for (int kc2 = 0; kc2 < (p.nkc >> 1); ++kc2) {
+          for (int tap = 0; tap < ntaps; ++tap) {
+            for (int kc2 = 0; kc2 < nkc2; ++kc2) {
               const uint64_t ad = ptx::smem_desc(
                   a_stage + (uint32_t)(2 * kc2) * p.lbo_a + (uint32_t)p.tap_off[tap] * 16u,
                   p.lbo_a, 128u);
               const uint64_t bd = ptx::smem_desc(
-                  sbase + p.off_w + (uint32_t)(tap * p.nkc + 2 * kc2) * n_half_bytes, p.lbo_b,
-                  128u);
+                  w_base + (uint32_t)(tap * p.nkc + 2 * kc2) * n_half_bytes, p.lbo_b, 128u);
               ptx::mma_i8_cg2(d_tmem, ad, bd, idesc, (tap | kc2) ? 1u : 0u);
             }
           }
@@ -451,197 +753,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else {
     // ================================ epilogue =================================
-    const int e = (int)warp - 1 - kProdWarps;         // 0..7
-    const int quad = (int)(warp & 3);                  // TMEM lane quadrant of this warp
-    const int half = e >> 2;                           // channel half
-    const int m = quad * 32 + (int)lane;               // position within the CTA tile
-    const int tid_e = e * 32 + (int)lane;              // 0..255
-    const int co_base = half * NCH;
-    const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-    const float decay = p.decay, vth = p.v_th, vres = p.v_reset;
-    uint32_t it = 0;
-    for (int pair = cid; pair < p.num_pairs; pair += ncl) {
-      const int tile = 2 * pair + (int)rank;
-      const long long L0 = (long long)tile * 128;
-      int b, y, x;
-      bool valid;
-      PosDecode<PATH>::out(p, L0 + m, b, y, x, valid);
-      const long long vbase = (((long long)b * p.Ho + y) * p.Wo + x) * p.Cout + co_base;
-      float V[NCH];
-      uint32_t prev[NWT];
-      uint32_t planes[kPlanes][NWT];
-      int steps_acc = 0;
-#pragma unroll
-      for (int w = 0; w < NWT; ++w) {
-        prev[w] = 0u;
-#pragma unroll
-        for (int pl = 0; pl < kPlanes; ++pl) planes[pl][w] = 0u;
-      }
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        V[c] = (p.v_init && valid && co_base + c < p.Cout) ? __ldg(p.v_init + vbase + c) : 0.f;
-        if (p.reset == 1 && V[c] >= vth) prev[c / 32] |= 1u << (c % 32);  // reading R4
-      }
-      for (int k = 0; k < p.G; ++k, ++it) {
-        const uint32_t acc = it % kAccs, aph = (it / kAccs) & 1u;
-        ptx::mbar_wait(bar_t_full + 8 * acc, aph);
-        ptx::tc_fence_after();
-        uint32_t inv[kMaxSteps][NWT];
-#pragma unroll
-        for (int j = 0; j < kMaxSteps; ++j)
-#pragma unroll
-          for (int w = 0; w < NWT; ++w) inv[j][w] = 0u;
-        const uint32_t tcol = tmem_base + lane_addr + acc * p.n_total + (uint32_t)co_base;
-#pragma unroll
-        for (int ch = 0; ch < NCH / 8; ++ch) {
-          uint32_t d1[8], d2[8];
-          ptx::tmem_ld8(tcol + ch * 8, d1);
-          ptx::tmem_ld8(tcol + p.Cout_pad + ch * 8, d2);
-          ptx::tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int c = ch * 8 + i;
-            const int co = co_base + c;
-            const float yv = fmaf((float)(int)d1[i], sc[co],
-                                  fmaf((float)(int)d2[i], sc[p.Cout_pad + co], sc[2 * p.Cout_pad + co]));
-            const uint32_t bm = 1u << (c % 32);
-            float v = V[c];
-            if (p.reset == 0) {
-#pragma unroll
-              for (int j = 0; j < kMaxSteps; ++j)
-                if (j < p.nsteps) lif_step<0>(v, yv, decay, vth, vres, inv[j][c / 32], bm, prev[c / 32]);
-            } else if (p.reset == 1) {
-#pragma unroll
-              for (int j = 0; j < kMaxSteps; ++j)
-                if (j < p.nsteps) lif_step<1>(v, yv, decay, vth, vres, inv[j][c / 32], bm, prev[c / 32]);
-            } else {
-#pragma unroll
-              for (int j = 0; j < kMaxSteps; ++j)
-                if (j < p.nsteps) lif_step<2>(v, yv, decay, vth, vres, inv[j][c / 32], bm, prev[c / 32]);
-            }
-            V[c] = v;
-          }
-        }
-        // accumulator consumed: hand TMEM back to the MMA issuer
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(bar_t_empty + 8 * acc, 0);
-
-        // spikes -> staging smem, bit-sliced counters
-        const uint32_t chmask = NCH >= 32 ? 0xFFFFFFFFu : ((1u << NCH) - 1u);
-#pragma unroll
-        for (int j = 0; j < kMaxSteps; ++j) {
-          if (j < p.nsteps) {
-#pragma unroll
-            for (int w = 0; w < NWT; ++w) {
-              const uint32_t s = valid ? (~inv[j][w] & chmask) : 0u;
-              stage[(j * 128 + m) * SROW + half * NWT + w] = s;
-              uint32_t c = s;
-#pragma unroll
-              for (int pl = 0; pl < kPlanes; ++pl) {
-                const uint32_t t = planes[pl][w] & c;
-                planes[pl][w] ^= c;
-                c = t;
-              }
-            }
-          }
-        }
-        steps_acc += p.nsteps;
-        if (p.counts && (steps_acc + p.nsteps > (1 << kPlanes) - 1 || k == p.G - 1)) {
-          flush_counts<NWT>(p, planes, valid, b, co_base, NCH, lane);
-          steps_acc = 0;
-        }
-        ptx::named_bar_sync(1, kEpiWarps * 32);
-
-        // staged spikes -> global packed output
-        const int nwo = p.nwo;
-        if (PATH == PATH_IM2COL && p.pool == 2) {
-          const int ntask = p.nsteps * 32 * nwo;
-          for (int task = tid_e; task < ntask; task += kEpiWarps * 32) {
-            const int wd = task % nwo;
-            const int qi = (task / nwo) % 32;
-            const int j = task / (32 * nwo);
-            int qb, qy, qx;
-            bool qv;
-            PosDecode<PATH>::out(p, L0 + 4 * qi, qb, qy, qx, qv);
-            if (!qv) continue;
-            uint32_t wv = 0;
-#pragma unroll
-            for (int mm = 0; mm < 4; ++mm) {
-              const uint32_t *sr = stage + (j * 128 + 4 * qi + mm) * SROW;
-              wv |= NCH >= 32 ? sr[wd] : (sr[0] | (sr[1] << NCH));
-            }
-            const int t_out = p.mode == 1 ? k : k * p.K + j;
-            uint32_t *row = p.out + (long long)t_out * p.out_st + (long long)qb * p.out_sb +
-                            (long long)(qy >> 1) * p.wpr_out;
-            if (p.Cout % 32 == 0) {
-              row[(qx >> 1) * nwo + wd] = wv;
-            } else {
-              const long long bit = (long long)(qx >> 1) * p.Cout;
-              if (wv) atomicOr(row + (bit >> 5), wv << (bit & 31));
-            }
-          }
-        } else {
-          const int ntask = p.nsteps * 128 * nwo;
-          for (int task = tid_e; task < ntask; task += kEpiWarps * 32) {
-            const int wd = task % nwo;
-            const int mm = (task / nwo) % 128;
-            const int j = task / (128 * nwo);
-            int pb, py, px;
-            bool pv;
-            PosDecode<PATH>::out(p, L0 + mm, pb, py, px, pv);
-            if (!pv) continue;
-            const int t_out = p.mode == 1 ? k : k * p.K + j;
-            uint32_t *base = p.out + (long long)t_out * p.out_st + (long long)pb * p.out_sb;
-            if (p.pool == 2) {
-              // halo path: the 2x2 window may straddle tiles -> leader-in-tile ORs
-              const int y0 = py & ~1, x0 = px & ~1;
-              const long long Lq = ((long long)pb * p.Sh + y0) * p.Sw + x0;
-              const long long mem[4] = {Lq - L0, Lq + 1 - L0, Lq + p.Sw - L0, Lq + p.Sw + 1 - L0};
-              int leader = -1;
-              bool full = true;
-              uint32_t wv = 0;
-#pragma unroll
-              for (int t = 0; t < 4; ++t) {
-                if (mem[t] >= 0 && mem[t] < 128) {
-                  if (leader < 0) leader = (int)mem[t];
-                  const uint32_t *sr = stage + (j * 128 + (int)mem[t]) * SROW;
-                  wv |= NCH >= 32 ? sr[wd] : (sr[0] | (sr[1] << NCH));
-                } else {
-                  full = false;
-                }
-              }
-              if (leader != mm) continue;
-              uint32_t *row = base + (long long)(y0 >> 1) * p.wpr_out;
-              if (p.Cout % 32 == 0) {
-                if (full)
-                  row[(x0 >> 1) * nwo + wd] = wv;
-                else if (wv)
-                  atomicOr(row + (x0 >> 1) * nwo + wd, wv);
-              } else {
-                const long long bit = (long long)(x0 >> 1) * p.Cout;
-                if (wv) atomicOr(row + (bit >> 5), wv << (bit & 31));
-              }
-            } else {
-              const uint32_t *sr = stage + (j * 128 + mm) * SROW;
-              const uint32_t wv = NCH >= 32 ? sr[wd] : (sr[0] | (sr[1] << NCH));
-              uint32_t *row = base + (long long)py * p.wpr_out;
-              if (p.Cout % 32 == 0) {
-                row[px * nwo + wd] = wv;
-              } else {
-                const long long bit = (long long)px * p.Cout;
-                if (wv) atomicOr(row + (bit >> 5), wv << (bit & 31));
-              }
-            }
-          }
-        }
-        ptx::named_bar_sync(1, kEpiWarps * 32);
-      }
-      if (p.v_final && valid) {
-#pragma unroll
-        for (int c = 0; c < NCH; ++c)
-          if (co_base + c < p.Cout) p.v_final[vbase + c] = V[c];
-      }
+    const int ns = p.reset == 0 ? p.nsteps : 0;
+    switch (ns) {
+      case 1: epilogue_role<NCH, PATH, 1>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 2: epilogue_role<NCH, PATH, 2>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 4: epilogue_role<NCH, PATH, 4>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 8: epilogue_role<NCH, PATH, 8>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      default: epilogue_role<NCH, PATH, 0>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
     }
   }
 
@@ -690,7 +808,7 @@ const char *tc_unsupported_reason(const tac_conv_lif_desc *d) {
 
 size_t tc_weights_bytes(const tac_conv_lif_desc *d) {
   const Geometry g = geometry(d);
-  return 2 * (size_t)g.w_bytes_cta + 3 * (size_t)g.cout_pad * 4;
+  return 2 * (size_t)g.w_bytes_cta + 4 * (size_t)g.cout_pad * 4;
 }
 
 // Two int8 slices per output channel, laid out as the smem image of each CTA:
@@ -707,14 +825,14 @@ void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bi
     double amax = 0.0;
     for (int i = 0; i < Ci * 9; ++i) amax = std::max(amax, std::fabs((double)weight[(size_t)co * Ci * 9 + i]));
     if (amax == 0.0) continue;
-    const double sc1 = amax / 127.0, sc2 = sc1 / 254.0;
-    s1[co] = (float)sc1;
+    s1[co] = (float)(amax / 127.0);
+    const double sc1 = (double)s1[co], sc2 = sc1 / 254.0;  // lo slice step = s1 / 254
     s2[co] = (float)sc2;
     for (int i = 0; i < Ci * 9; ++i) {
       const double w = weight[(size_t)co * Ci * 9 + i];
       const double a = std::max(-127.0, std::min(127.0, std::nearbyint(w / sc1)));
-      const double r = w - a * (double)s1[co];
-      const double b = std::max(-127.0, std::min(127.0, std::nearbyint(r / (double)s2[co])));
+      const double r = w - a * sc1;
+      const double b = std::max(-127.0, std::min(127.0, std::nearbyint(r / sc2)));
       q1[(size_t)co * Ci * 9 + i] = (signed char)a;
       q2[(size_t)co * Ci * 9 + i] = (signed char)b;
     }
@@ -748,11 +866,13 @@ void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bi
       }
     }
   }
+  // [s1/254 | bias | s1 | s2] (the kernel multiplies all but bias by 2^{-m(K-1)})
   float *sb = reinterpret_cast<float *>(dst + 2 * (size_t)g.w_bytes_cta);
   for (int i = 0; i < Cp; ++i) {
-    sb[i] = s1[i];
-    sb[Cp + i] = s2[i];
-    sb[2 * Cp + i] = bs[i];
+    sb[i] = (float)((double)s1[i] / 254.0);
+    sb[Cp + i] = bs[i];
+    sb[2 * Cp + i] = s1[i];
+    sb[3 * Cp + i] = s2[i];
   }
 }
 
@@ -772,11 +892,18 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   p.wpr_in = lp.wpr_in; p.wpr_out = lp.wpr_out;
   p.nwo = lp.Cout % 32 == 0 ? lp.Cout / 32 : 1;
   p.out_atomic = ((g.path == PATH_HALO && lp.pool == 2) || lp.Cout % 32 != 0) ? 1 : 0;
+  {  // exact s32 combine 254 D_hi + D_lo possible? |A| <= A_max, |q| <= 127, K_red terms
+    const int K = lp.K;
+    double a_max = 0;
+    for (int j = 0; j < K; ++j) a_max += std::ldexp(1.0, p.m_shift * j);
+    const double kred = g.path == PATH_HALO ? 9.0 * lp.Cin : 32.0;
+    p.int_combine = (a_max * 127.0 * kred * 255.0 < 2147483647.0) ? 1 : 0;
+  }
   p.in_st = lp.in_st; p.in_sb = lp.in_sb; p.out_st = lp.out_st; p.out_sb = lp.out_sb;
   p.decay = lp.decay; p.v_th = lp.v_th; p.v_reset = lp.v_reset;
   p.agg_scale = (float)std::ldexp(1.0, -p.m_shift * (lp.K - 1));
   p.off_w = g.off_w; p.off_a = g.off_a; p.a_stage_bytes = g.a_stage_bytes;
-  p.off_stage = g.off_stage; p.off_scale = g.off_scale; p.off_bar = g.off_bar;
+  p.off_stage = g.off_stage; p.off_pinfo = g.off_pinfo; p.off_scale = g.off_scale; p.off_bar = g.off_bar;
   p.smem_bytes = g.smem_bytes; p.w_bytes_cta = g.w_bytes_cta;
   p.n_total = 2u * g.cout_pad;
   uint32_t cols = 32;
