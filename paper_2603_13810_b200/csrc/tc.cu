@@ -210,24 +210,26 @@ __device__ __forceinline__ void decode_out(const TcParams &p, long long L, int &
 }
 
 // --- producers: build the u8 aggregate A_k * 2^{m(K-1)} in the MMA layout ---
-__device__ __forceinline__ void agg_word(uint32_t (&o)[8], const uint32_t (&xj)[kMaxSteps],
-                                         int K, int m) {
-  // byte b of output word q <- input channel (q + 8b) of the 32-channel word;
-  // bit e_j = m*j of that byte <- frame j  (weights 2^{m j}, oldest frame = 1)
+// byte b of output word q <- input channel (q + 8b) of a 32-channel word; bit
+// e_j = m*j of that byte <- frame j (weights 2^{m j}, oldest frame = 1)
+template <int K>
+__device__ __forceinline__ void agg_word_k(uint32_t (&o)[8], const uint32_t *xj, int m) {
 #pragma unroll
-  for (int j = 0; j < kMaxSteps; ++j) {
-    if (j < K) {
-      const uint32_t x = xj[j];
-      const int e = m * j;
+  for (int j = 0; j < K; ++j) {
+    const uint32_t x = xj[j];
+    const int e = m * j;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) o[q] |= ((x >> q) & 0x01010101u) << e;
-    }
+    for (int q = 0; q < 8; ++q) o[q] |= ((x >> q) & 0x01010101u) << e;
   }
 }
 
+// Halo producer.  The thread owns 32-channel word w of halo rows row0, row0 +
+// rstep, ... (96 % nwin == 0).  Loads are issued in batches of RB rows x K
+// frames before any is consumed, so one memory round trip covers RB rows.
+template <int K>
 __device__ __forceinline__ void produce_halo(const TcParams &p, int tile, int k, uint32_t a_stage,
                                              int ptid) {
-  // thread owns 32-channel word w of halo rows row0, row0 + rstep, ... (96 % nwin == 0)
+  constexpr int RB = K >= 8 ? 2 : (K >= 4 ? 6 : 12);
   const int nwin = p.Cin >> 5;
   const int w = ptid % nwin, row0 = ptid / nwin, rstep = (kProdWarps * 32) / nwin;
   const long long L = (long long)tile * 128 + row0;
@@ -235,33 +237,47 @@ __device__ __forceinline__ void produce_halo(const TcParams &p, int tile, int k,
   long long bb = L / per;
   int rem = (int)(L - bb * per);
   int yy = rem / p.Sw, xx = rem - (rem / p.Sw) * p.Sw;
-  const uint32_t *frame0 = p.in + (long long)(k * p.K) * p.in_st + w;
-  const int K = p.K, mshift = p.m_shift;
+  const uint32_t *frame0 = p.in + (long long)(k * K) * p.in_st + w;
   const long long in_st = p.in_st;
-  for (int row = row0; row < p.halo_rows; row += rstep) {
-    const int yi = yy - p.pad, xi = xx - p.pad;
-    uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (bb < p.B && yi >= 0 && yi < p.H && xi >= 0 && xi < p.W) {
-      const uint32_t *src = frame0 + bb * p.in_sb + (long long)yi * p.wpr_in + xi * nwin;
-      uint32_t xj[kMaxSteps];
+  const int mshift = p.m_shift;
+  const int nrows = row0 < p.halo_rows ? (p.halo_rows - row0 + rstep - 1) / rstep : 0;
+  for (int ib = 0; ib < nrows; ib += RB) {
+    uint32_t xs[RB][K];
+    bool ok[RB];
 #pragma unroll
-      for (int j = 0; j < kMaxSteps; ++j) xj[j] = (j < K) ? __ldg(src + j * in_st) : 0u;
-      agg_word(o, xj, K, mshift);
+    for (int r = 0; r < RB; ++r) {
+      ok[r] = false;
+      if (ib + r < nrows) {
+        const int yi = yy - p.pad, xi = xx - p.pad;
+        ok[r] = bb < p.B && yi >= 0 && yi < p.H && xi >= 0 && xi < p.W;
+        const uint32_t *src = frame0 + bb * p.in_sb + (long long)yi * p.wpr_in + xi * nwin;
+#pragma unroll
+        for (int j = 0; j < K; ++j) xs[r][j] = ok[r] ? __ldg(src + j * in_st) : 0u;
+        xx += rstep;  // advance the padded-linear position by rstep rows
+        while (xx >= p.Sw) {
+          xx -= p.Sw;
+          if (++yy == p.Sh) {
+            yy = 0;
+            ++bb;
+          }
+        }
+      }
     }
-    const uint32_t dst = a_stage + (uint32_t)(2 * w) * p.lbo_a + (uint32_t)row * 16u;
-    ptx::st_shared_v4(dst, o[0], o[1], o[2], o[3]);
-    ptx::st_shared_v4(dst + p.lbo_a, o[4], o[5], o[6], o[7]);
-    xx += rstep;  // advance the padded-linear position by rstep rows
-    while (xx >= p.Sw) {
-      xx -= p.Sw;
-      if (++yy == p.Sh) {
-        yy = 0;
-        ++bb;
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      if (ib + r < nrows) {
+        uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        agg_word_k<K>(o, xs[r], mshift);
+        const int row = row0 + (ib + r) * rstep;
+        const uint32_t dst = a_stage + (uint32_t)(2 * w) * p.lbo_a + (uint32_t)row * 16u;
+        ptx::st_shared_v4(dst, o[0], o[1], o[2], o[3]);
+        ptx::st_shared_v4(dst + p.lbo_a, o[4], o[5], o[6], o[7]);
       }
     }
   }
 }
 
+template <int K>
 __device__ __forceinline__ void produce_im2col(const TcParams &p, int tile, int k,
                                                uint32_t a_stage, int ptid) {
   const long long L0 = (long long)tile * 128;
@@ -270,35 +286,65 @@ __device__ __forceinline__ void produce_im2col(const TcParams &p, int tile, int 
     int b, y, x;
     bool valid;
     decode_out<PATH_IM2COL>(p, L0 + pos, b, y, x, valid);
+    const int bit0 = (x - p.pad) * p.Cin;
+    const int w0 = bit0 >= 0 ? (bit0 >> 5) : -1;  // bit0 >= -2
+    const int sh = bit0 - w0 * 32;
+    const bool lo_ok = w0 >= 0 && w0 < p.wpr_in, hi_ok = w0 + 1 < p.wpr_in;
+    constexpr int KB = K > 2 ? 2 : K;  // frames per load batch
     uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (valid) {
-      const int bit0 = (x - p.pad) * p.Cin;
-      const int w0 = bit0 >= 0 ? (bit0 >> 5) : -1;  // bit0 >= -2
-      const int sh = bit0 - w0 * 32;
 #pragma unroll
-      for (int j = 0; j < kMaxSteps; ++j) {
-        if (j < p.K) {
-          const uint32_t *fr = p.in + (long long)(k * p.K + j) * p.in_st + (long long)b * p.in_sb;
-          uint32_t z = 0;
+    for (int j0 = 0; j0 < K; j0 += KB) {
+      uint32_t lo[KB][3], hi[KB][3];
 #pragma unroll
-          for (int r = 0; r < 3; ++r) {
-            const int yi = y + r - p.pad;
-            if (yi < 0 || yi >= p.H) continue;
-            const uint32_t *row = fr + (long long)yi * p.wpr_in;
-            const uint32_t lo = (w0 >= 0 && w0 < p.wpr_in) ? __ldg(row + w0) : 0u;
-            const uint32_t hi = (w0 + 1 < p.wpr_in) ? __ldg(row + w0 + 1) : 0u;
-            z |= (__funnelshift_r(lo, hi, sh) & wmask) << (8 * r);
-          }
-          const int e = p.m_shift * j;
-          // word q, byte r <- (row r, window bit q): K-index 4q + r
+      for (int r = 0; r < 3; ++r) {
+        const int yi = y + r - p.pad;
+        const bool rok = valid && yi >= 0 && yi < p.H;
+        const uint32_t *row = p.in + (long long)(k * K + j0) * p.in_st + (long long)b * p.in_sb +
+                              (long long)yi * p.wpr_in;
 #pragma unroll
-          for (int q = 0; q < 6; ++q) o[q] |= ((z >> q) & 0x00010101u) << e;
+        for (int j = 0; j < KB; ++j) {
+          lo[j][r] = (rok && lo_ok) ? __ldg(row + j * p.in_st + w0) : 0u;
+          hi[j][r] = (rok && hi_ok) ? __ldg(row + j * p.in_st + w0 + 1) : 0u;
         }
+      }
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        uint32_t z = 0;
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+          z |= (__funnelshift_r(lo[j][r], hi[j][r], sh) & wmask) << (8 * r);
+        const int e = p.m_shift * (j0 + j);
+        // word q, byte r <- (row r, window bit q): K-index 4q + r
+#pragma unroll
+        for (int q = 0; q < 6; ++q) o[q] |= ((z >> q) & 0x00010101u) << e;
       }
     }
     const uint32_t dst = a_stage + (uint32_t)pos * 16u;
     ptx::st_shared_v4(dst, o[0], o[1], o[2], o[3]);
     ptx::st_shared_v4(dst + p.lbo_a, o[4], o[5], o[6], o[7]);
+  }
+}
+
+template <int PATH, int K>
+__device__ __forceinline__ void producer_role(const TcParams &p, uint32_t sbase,
+                                              uint32_t bar_a_full, uint32_t bar_a_empty, int cid,
+                                              int ncl, uint32_t rank, uint32_t lane) {
+  const int ptid = (int)threadIdx.x - 32;
+  uint32_t it = 0;
+  for (int pair = cid; pair < p.num_pairs; pair += ncl) {
+    const int tile = 2 * pair + (int)rank;
+    for (int k = 0; k < p.G; ++k, ++it) {
+      const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
+      ptx::mbar_wait(bar_a_empty + 8 * s, ph ^ 1u);
+      const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
+      if (PATH == PATH_HALO)
+        produce_halo<K>(p, tile, k, a_stage, ptid);
+      else
+        produce_im2col<K>(p, tile, k, a_stage, ptid);
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(bar_a_full + 8 * s, 0);
+    }
   }
 }
 
@@ -363,19 +409,29 @@ __device__ __forceinline__ void lif_step(float &v, float y, float decay, float v
   if (RESET == 1) prev = (prev & ~bitmask) | (~(uint32_t)msk & bitmask);
 }
 
-// two neurons, NS steps sharing one drive (TAC-TP) or NS = 1 (TAC / dense), subtract
-// reset, packed fp32x2 arithmetic (identical rounding to the scalar form)
+__device__ __forceinline__ uint32_t lop3_select(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;  // (a & ~c) | (b & c)
+  asm("lop3.b32 %0, %1, %2, %3, 0xD8;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// two neurons, NS steps sharing one drive (TAC-TP) or NS = 1 (TAC / dense),
+// subtract reset, packed fp32x2 arithmetic (identical rounding to the scalar
+// form).  inv[j] collects the sign bit of V - v_th (1 = no spike) by funnel
+// shift: the first channel shifted in ends up in the highest bit.
 template <int NS>
 __device__ __forceinline__ void lif_pair_sub(float2 &v, float2 y, float2 dec2, float2 nth2,
-                                             uint32_t (&inv)[NS], uint32_t b0, uint32_t b1) {
+                                             uint32_t (&inv)[NS]) {
 #pragma unroll
   for (int j = 0; j < NS; ++j) {
-    v = __ffma2_rn(dec2, v, y);
-    const float2 v2 = __fadd2_rn(v, nth2);
-    const int m0 = __float_as_int(v2.x) >> 31, m1 = __float_as_int(v2.y) >> 31;
-    v.x = __int_as_float((__float_as_int(v2.x) & ~m0) | (__float_as_int(v.x) & m0));
-    v.y = __int_as_float((__float_as_int(v2.y) & ~m1) | (__float_as_int(v.y) & m1));
-    inv[j] |= ((uint32_t)m0 & b0) | ((uint32_t)m1 & b1);
+    v = __ffma2_rn(dec2, v, y);                       // V <- beta V + Y
+    const float2 v2 = __fadd2_rn(v, nth2);            // V - v_th
+    const uint32_t a0 = __float_as_uint(v2.x), a1 = __float_as_uint(v2.y);
+    const uint32_t m0 = (uint32_t)((int)a0 >> 31), m1 = (uint32_t)((int)a1 >> 31);
+    v.x = __uint_as_float(lop3_select(a0, __float_as_uint(v.x), m0));  // spike: V - v_th
+    v.y = __uint_as_float(lop3_select(a1, __float_as_uint(v.y), m1));
+    inv[j] = __funnelshift_l(a0, inv[j], 1);
+    inv[j] = __funnelshift_l(a1, inv[j], 1);
   }
 }
 
@@ -535,11 +591,10 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
             constexpr int NSP = (NS > 0) ? NS : 1;
             uint32_t invp[NSP];
 #pragma unroll
-            for (int j = 0; j < NSP; ++j) invp[j] = 0u;
-            lif_pair_sub<NSP>(V[c / 2], make_float2(yv[i], yv[i + 1]), dec2, nth2, invp,
-                              1u << (c % 32), 1u << ((c + 1) % 32));
+            for (int j = 0; j < NSP; ++j) invp[j] = inv[j][c / 32];
+            lif_pair_sub<NSP>(V[c / 2], make_float2(yv[i], yv[i + 1]), dec2, nth2, invp);
 #pragma unroll
-            for (int j = 0; j < NSP; ++j) inv[j][c / 32] |= invp[j];
+            for (int j = 0; j < NSP; ++j) inv[j][c / 32] = invp[j];
           }
         } else {
 #pragma unroll
@@ -572,7 +627,9 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
         if (NS > 0 || j < nsteps) {
 #pragma unroll
           for (int w = 0; w < NWT; ++w) {
-            const uint32_t s = valid ? (~inv[j][w] & chmask) : 0u;
+            uint32_t iv = inv[j][w];
+            if (NS > 0) iv = __brev(iv) >> (NCH >= 32 ? 0 : 32 - NCH);  // funnel order -> bit c
+            const uint32_t s = valid ? (~iv & chmask) : 0u;
             stage[(j * 128 + m) * SROW + half * NWT + w] = s;
             uint32_t c = s;
 #pragma unroll
@@ -695,7 +752,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   // register rebalance: MMA + producer warpgroup gives registers to the epilogue
   if (warp < 4)
-    ptx::setmaxnreg_dec<88>();
+    ptx::setmaxnreg_dec<96>();
   else
     ptx::setmaxnreg_inc<208>();
 
@@ -734,22 +791,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp <= kProdWarps) {
     // ================================ producers ================================
-    const int ptid = (int)threadIdx.x - 32;
-    uint32_t it = 0;
-    for (int pair = cid; pair < p.num_pairs; pair += ncl) {
-      const int tile = 2 * pair + (int)rank;
-      for (int k = 0; k < p.G; ++k, ++it) {
-        const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
-        ptx::mbar_wait(bar_a_empty + 8 * s, ph ^ 1u);
-        const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
-        if (PATH == PATH_HALO)
-          produce_halo(p, tile, k, a_stage, ptid);
-        else
-          produce_im2col(p, tile, k, a_stage, ptid);
-        ptx::fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(bar_a_full + 8 * s, 0);
-      }
+    switch (p.K) {
+      case 1: producer_role<PATH, 1>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane); break;
+      case 2: producer_role<PATH, 2>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane); break;
+      case 4: producer_role<PATH, 4>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane); break;
+      default: producer_role<PATH, 8>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane); break;
     }
   } else {
     // ================================ epilogue =================================
