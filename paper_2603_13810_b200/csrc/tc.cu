@@ -750,11 +750,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int ncl = (int)ptx::nclusters_x();
   const int cid = (int)ptx::cluster_id_x();
 
-  // register rebalance: MMA + producer warpgroup gives registers to the epilogue
+  // register rebalance: MMA + producer warpgroup gives registers to the epilogue.
+  // The sum must not exceed what the launch allocated (384 x 168), or the
+  // increase blocks forever.
+  constexpr uint32_t kRegsLow = 96, kRegsHigh = 200;
+  static_assert(128 * kRegsLow + 256 * kRegsHigh <= kThreads * 168, "register budget");
   if (warp < 4)
-    ptx::setmaxnreg_dec<96>();
+    ptx::setmaxnreg_dec<kRegsLow>();
   else
-    ptx::setmaxnreg_inc<208>();
+    ptx::setmaxnreg_inc<kRegsHigh>();
 
   if (warp == 0) {
     // ================================ MMA issuer (CTA 0 of the pair) =========
