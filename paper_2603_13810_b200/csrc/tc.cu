@@ -619,7 +619,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
       // accumulator consumed: hand TMEM back to the MMA issuer
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(bar_t_empty + 8 * acc, 0);
+      if (lane == 0) ptx::mbar_arrive_cluster_relaxed(bar_t_empty + 8 * acc, 0);
 
       // spikes -> staging smem, bit-sliced counters
 #pragma unroll
@@ -648,43 +648,67 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
       }
       ptx::named_bar_sync(1, kEpiWarps * 32);
 
-      // staged spikes -> global packed output
-      const int ntask = nsteps * 128 * nwo;
-      for (int task = tid_e; task < ntask; task += kEpiWarps * 32) {
-        const int wd = task % nwo;
-        const int mm = (task / nwo) & 127;
-        const int j = task / (nwo * 128);
-        const PInfo pi = pinfo[mm];
-        if (pi.off < 0) continue;
-        const uint32_t *st = stage + j * 128 * SROW;
-        auto pix = [&](int q) -> uint32_t {
+      // staged spikes -> global packed output.  Tasks (step j, position, word)
+      // decompose with shifts (NWOP words per position is a compile-time power of 2).
+      {
+        constexpr int NWOP = NCH >= 32 ? 2 * NWT : 1;
+        constexpr int LG = NWOP == 4 ? 2 : (NWOP == 2 ? 1 : 0);
+        const bool pooled = p.pool == 2;
+        auto pix = [&](const uint32_t *st, int q, int wd) -> uint32_t {
           const uint32_t *sr = st + q * SROW;
           return NCH >= 32 ? sr[wd] : (sr[0] | (sr[1] << NCH));
         };
-        uint32_t wv;
-        bool full = true;
-        if (p.pool == 2 && PATH == PATH_IM2COL) {
-          wv = pix(mm) | pix(mm + 1) | pix(mm + 2) | pix(mm + 3);
-        } else if (p.pool == 2) {
-          const int mask = pi.aux & 15;
-          wv = 0;
-          if (mask & 1) wv |= pix(pi.org);
-          if (mask & 2) wv |= pix(pi.org + 1);
-          if (mask & 4) wv |= pix(pi.org + p.Sw);
-          if (mask & 8) wv |= pix(pi.org + p.Sw + 1);
-          full = mask == 15;
+        if (PATH == PATH_IM2COL && pooled) {
+          // quad-major positions: window q = positions 4q .. 4q+3, all in this tile
+          const int ntask = nsteps << (5 + LG);
+          for (int t = tid_e; t < ntask; t += kEpiWarps * 32) {
+            const int wd = t & (NWOP - 1), q = (t >> LG) & 31, j = t >> (5 + LG);
+            if (wd >= nwo) continue;
+            const PInfo pi = pinfo[4 * q];
+            if (pi.off < 0) continue;
+            const uint32_t *st = stage + j * 128 * SROW;
+            const uint32_t wv = pix(st, 4 * q, wd) | pix(st, 4 * q + 1, wd) |
+                                pix(st, 4 * q + 2, wd) | pix(st, 4 * q + 3, wd);
+            const int t_out = mode == 1 ? k : k * K + j;
+            uint32_t *dst = p.out + (long long)t_out * p.out_st + pi.off;
+            if (Cout % 32 == 0)
+              dst[wd] = wv;
+            else if (wv)
+              atomicOr(dst, wv << ((pi.aux >> 8) & 31));
+          }
         } else {
-          wv = pix(mm);
-        }
-        const int t_out = mode == 1 ? k : k * K + j;
-        uint32_t *dst = p.out + (long long)t_out * p.out_st + pi.off;
-        if (Cout % 32 == 0) {
-          if (full)
-            dst[wd] = wv;
-          else if (wv)
-            atomicOr(dst + wd, wv);
-        } else if (wv) {
-          atomicOr(dst, wv << ((pi.aux >> 8) & 31));
+          const int ntask = nsteps << (7 + LG);
+          const int sw = p.Sw;
+          for (int t = tid_e; t < ntask; t += kEpiWarps * 32) {
+            const int wd = t & (NWOP - 1), mm = (t >> LG) & 127, j = t >> (7 + LG);
+            if (wd >= nwo) continue;
+            const PInfo pi = pinfo[mm];
+            if (pi.off < 0) continue;
+            const uint32_t *st = stage + j * 128 * SROW;
+            uint32_t wv;
+            bool full = true;
+            if (pooled) {  // halo path: the 2x2 window may straddle tiles
+              const int mask = pi.aux & 15, o = pi.org;
+              wv = 0;
+              if (mask & 1) wv |= pix(st, o, wd);
+              if (mask & 2) wv |= pix(st, o + 1, wd);
+              if (mask & 4) wv |= pix(st, o + sw, wd);
+              if (mask & 8) wv |= pix(st, o + sw + 1, wd);
+              full = mask == 15;
+            } else {
+              wv = pix(st, mm, wd);
+            }
+            const int t_out = mode == 1 ? k : k * K + j;
+            uint32_t *dst = p.out + (long long)t_out * p.out_st + pi.off;
+            if (Cout % 32 == 0) {
+              if (full)
+                dst[wd] = wv;
+              else if (wv)
+                atomicOr(dst + wd, wv);
+            } else if (wv) {
+              atomicOr(dst, wv << ((pi.aux >> 8) & 31));
+            }
+          }
         }
       }
       ptx::named_bar_sync(1, kEpiWarps * 32);
