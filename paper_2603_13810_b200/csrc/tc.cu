@@ -415,11 +415,20 @@ __device__ __forceinline__ uint32_t lop3_select(uint32_t a, uint32_t b, uint32_t
   return d;
 }
 
-// two neurons, NS steps sharing one drive (TAC-TP) or NS = 1 (TAC / dense),
-// subtract reset, packed fp32x2 arithmetic (identical rounding to the scalar
-// form).  inv[j] collects the sign bit of V - v_th (1 = no spike) by funnel
-// shift: the first channel shifted in ends up in the highest bit.
-template <int NS>
+// inv += m * (-bit) on the FMA pipe (m in {0,-1}): sets `bit` when m = -1
+template <uint32_t BIT>
+__device__ __forceinline__ uint32_t mad_bit(uint32_t m, uint32_t inv) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(m), "n"(0u - BIT), "r"(inv));
+  return d;
+}
+
+// two neurons (channels C0, C0+1 of a 32-bit word), NS steps sharing one drive
+// (TAC-TP) or NS = 1 (TAC / dense), subtract reset, packed fp32x2 arithmetic
+// (identical rounding to the scalar form).  Per neuron-step: half an FFMA2 and
+// an FADD2, one SHF + one LOP3 (ALU pipe), one IMAD (FMA pipe) -- balanced pipes.
+// inv[j] bit c is set when channel c did NOT spike.
+template <int NS, int C0>
 __device__ __forceinline__ void lif_pair_sub(float2 &v, float2 y, float2 dec2, float2 nth2,
                                              uint32_t (&inv)[NS]) {
 #pragma unroll
@@ -430,8 +439,8 @@ __device__ __forceinline__ void lif_pair_sub(float2 &v, float2 y, float2 dec2, f
     const uint32_t m0 = (uint32_t)((int)a0 >> 31), m1 = (uint32_t)((int)a1 >> 31);
     v.x = __uint_as_float(lop3_select(a0, __float_as_uint(v.x), m0));  // spike: V - v_th
     v.y = __uint_as_float(lop3_select(a1, __float_as_uint(v.y), m1));
-    inv[j] = __funnelshift_l(a0, inv[j], 1);
-    inv[j] = __funnelshift_l(a1, inv[j], 1);
+    inv[j] = mad_bit<1u << C0>(m0, inv[j]);
+    inv[j] = mad_bit<1u << (C0 + 1)>(m1, inv[j]);
   }
 }
 
@@ -585,17 +594,40 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
         float yv[8];
         combine8(p, sc, co_base + ch * 8, d[cur][0], d[cur][1], yv);
         if (NS > 0) {
+          constexpr int NSP = (NS > 0) ? NS : 1;
+          const int w = (ch * 8) / 32;
+          uint32_t invp[NSP];
 #pragma unroll
-          for (int i = 0; i < 8; i += 2) {
-            const int c = ch * 8 + i;
-            constexpr int NSP = (NS > 0) ? NS : 1;
-            uint32_t invp[NSP];
-#pragma unroll
-            for (int j = 0; j < NSP; ++j) invp[j] = inv[j][c / 32];
-            lif_pair_sub<NSP>(V[c / 2], make_float2(yv[i], yv[i + 1]), dec2, nth2, invp);
-#pragma unroll
-            for (int j = 0; j < NSP; ++j) inv[j][c / 32] = invp[j];
+          for (int j = 0; j < NSP; ++j) invp[j] = inv[j][w];
+          // channel offsets within the word are compile-time: (ch*8) % 32 + i
+          switch ((ch * 8) % 32) {
+            case 0:
+              lif_pair_sub<NSP, 0>(V[ch * 4 + 0], make_float2(yv[0], yv[1]), dec2, nth2, invp);
+              lif_pair_sub<NSP, 2>(V[ch * 4 + 1], make_float2(yv[2], yv[3]), dec2, nth2, invp);
+              lif_pair_sub<NSP, 4>(V[ch * 4 + 2], make_float2(yv[4], yv[5]), dec2, nth2, invp);
+              lif_pair_sub<NSP, 6>(V[ch * 4 + 3], make_float2(yv[6], yv[7]), dec2, nth2, invp);
+              break;
+            case 8:
+              lif_pair_sub<NSP, 8>(V[ch * 4 + 0], make_float2(yv[0], yv[1]), dec2, nth2, invp);
+              lif_pair_sub<NSP, 10>(V[ch * 4 + 1], make_float2(yv[2], yv[3]), dec2, nth2, invp);
+              lif_pair_sub<NSP, 12>(V[ch * 4 + 2], make_float2(yv[4], yv[5]), dec2, nth2, invp);
+              lif_pair_sub<NSP, 14>(V[ch * 4 + 3], make_float2(yv[6], yv[7]), dec2, nth2, invp);
+              break;
+            case 16:
+              lif_pair_sub<NSP, 16>(V[ch * 4 + 0], make_float2(yv[0], yv[1]), dec2, nth2, invp);
+              lif_pair_sub<NSP, 18>(V[ch * 4 + 1], make_float2(yv[2], yv[3]), dec2, nth2, invp);
+              lif_pair_sub<NSP, 20>(V[ch * 4 + 2], make_float2(yv[4], yv[5]), dec2, nth2, invp);
+              lif_pair_sub<NSP, 22>(V[ch * 4 + 3], make_float2(yv[6], yv[7]), dec2, nth2, invp);
+              break;
+            default:
+              lif_pair_sub<NSP, 24>(V[ch * 4 + 0], make_float2(yv[0], yv[1]), dec2, nth2, invp);
+              lif_pair_sub<NSP, 26>(V[ch * 4 + 1], make_float2(yv[2], yv[3]), dec2, nth2, invp);
+              lif_pair_sub<NSP, 28>(V[ch * 4 + 2], make_float2(yv[4], yv[5]), dec2, nth2, invp);
+              lif_pair_sub<NSP, 30>(V[ch * 4 + 3], make_float2(yv[6], yv[7]), dec2, nth2, invp);
+              break;
           }
+#pragma unroll
+          for (int j = 0; j < NSP; ++j) inv[j][w] = invp[j];
         } else {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -627,9 +659,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
         if (NS > 0 || j < nsteps) {
 #pragma unroll
           for (int w = 0; w < NWT; ++w) {
-            uint32_t iv = inv[j][w];
-            if (NS > 0) iv = __brev(iv) >> (NCH >= 32 ? 0 : 32 - NCH);  // funnel order -> bit c
-            const uint32_t s = valid ? (~iv & chmask) : 0u;
+            const uint32_t s = valid ? (~inv[j][w] & chmask) : 0u;
             stage[(j * 128 + m) * SROW + half * NWT + w] = s;
             uint32_t c = s;
 #pragma unroll
