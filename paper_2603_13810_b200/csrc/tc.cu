@@ -10,28 +10,31 @@
 //     sum_j S_{kK+j} 2^{m j} is an exact unsigned integer <= 255 (u8 operand);
 //     dense mode (K = 1) has A = S in {0,1} for any beta.
 //   * W [C_out][C_in][3][3] fp32 is split per output channel into two int8
-//     slices, w ~= s1 q1 + s2 q2 (s2 = s1/254), |w - w~| <= max|w| * 1.55e-5;
-//     both slices ride in ONE MMA with N = 2 C_out (hi rows on CTA 0, lo rows on
-//     CTA 1 of the pair), accumulated exactly in s32 in TMEM.
-//   * the epilogue forms Y = 2^{-m(K-1)} (s1 D_hi + s2 D_lo) + b in fp32.
+//     slices, w ~= s1 q1 + (s1/254) q2, |w - w~| <= max|w| * 1.55e-5; both
+//     slices ride in ONE MMA with N = 2 C_out (hi rows on CTA 0, lo rows on CTA
+//     1 of the pair), accumulated exactly in s32 in TMEM.
+//   * the epilogue forms Y = 2^{-m(K-1)} s1 (D_hi + D_lo/254) + b in fp32.
 //
-// Implicit GEMM layout ("padded linear space"): output position L =
-// (b*S_h + y)*S_w + x with S_h = H + pad, S_w = W + pad.  The aggregated input
-// halo of a 128-position tile is stored K-major, no swizzle, one 16-byte row per
-// position, so the 3x3 tap (r, s) is just a start-address offset of
-// (r*S_w + s)*16 bytes of the tensor-core smem descriptor -- no im2col copies.
-// Positions with y >= H' or x >= W' are computed and discarded.  Layers with
-// C_in <= 2 (first layers) use an explicit 32-byte im2col row per position
-// instead (K_red = 9 C_in <= 18 padded to 32).
+// Tile = 16 output rows x 8 output columns of one sample per CTA (M = 128).
+// Halo path (C_in a multiple of 32): the u8 aggregate of the 18 x 10 input halo
+// is stored K-major without swizzle, one 16-byte row per halo pixel, halo rows
+// 10 pixels apart.  A-operand row i = (g, c) = (i / 8, i % 8) of the tile is read
+// at halo pixel (g + r, c + s) for tap (r, s): the 8 rows of a core matrix are
+// 16 B apart and core-matrix groups (tile rows) SBO = 160 B apart, so a tap is
+// a start-address offset of (10 r + s) * 16 B -- no im2col copies, no junk rows.
+// Layers with C_in <= 2 (first layers) use an explicit 32-byte im2col row.
+// TMEM lane i = tile pixel (g, c): epilogue warp q holds tile rows 4q..4q+3, so
+// every 2x2 pooling window lies inside one warp (lanes l, l^1, l^8, l^9) and
+// spikes are OR-pooled with two shuffles and stored straight from registers.
 //
-// CTA pair (cluster of 2, tcgen05 cta_group::2, M = 256): each CTA owns 128
-// output positions and half of the B operand (one int8 slice of all 9 taps,
-// resident in smem for the whole kernel).  Warp roles per CTA (384 threads):
+// CTA pair (cluster of 2, tcgen05 cta_group::2, M = 256): each CTA owns one tile
+// and half of the B operand (one int8 slice of all 9 taps, resident in smem for
+// the whole kernel).  Warp roles per CTA (384 threads):
 //   warp 0      : TMEM alloc; in CTA 0 one lane issues all MMAs of the pair
 //   warps 1..3  : producers -- load packed spikes, build the u8 aggregate A_k
-//   warps 4..11 : epilogue  -- TMEM -> registers, LIF over K steps, spikes to
-//                 smem staging, pooled/packed stores, counts, v_init/v_final
-// Pipelines: A stages (2) producer -> MMA, TMEM accumulators (2) MMA -> epilogue.
+//   warps 4..11 : epilogue  -- TMEM -> registers, LIF over K steps, pooled /
+//                 packed stores, bit-sliced spike counts, v_init / v_final
+// Pipelines: A stages (2-3) producer -> MMA, TMEM accumulators (2) MMA -> epilogue.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -49,26 +52,27 @@ namespace {
 constexpr int kProdWarps = 3;
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 32 * (1 + kProdWarps + kEpiWarps);
-constexpr int kStages = 2;
+constexpr int kMaxStages = 3;
 constexpr int kAccs = 2;
 constexpr int kMaxSteps = 8;
 constexpr int kPlanes = 6;  // bit-sliced spike counters (<= 63 steps per flush)
+constexpr int kTileH = 16, kTileW = 8;                 // output pixels per CTA tile
+constexpr int kHaloH = kTileH + 2, kHaloW = kTileW + 2;  // 3x3 halo
+constexpr int kHaloRows = kHaloH * kHaloW;              // 180 halo pixels
 constexpr uint32_t kSmemLimit = 232448;
 
 enum { PATH_HALO = 0, PATH_IM2COL = 1 };
 
 struct TcParams {
-  int B, H, W, Cin, Cout, Cout_pad, pad, Ho, Wo, Hq, Wq, pool;
+  int B, H, W, Cin, Cout, Cout_pad, pad, Ho, Wo, pool;
   int K, G, nsteps, mode, reset;
-  int Sh, Sw;
-  long long M_total;
-  int num_tiles, num_pairs;
-  int halo_rows, nkc, ntaps, m_shift;
-  int wpr_in, wpr_out, nwo, out_atomic, int_combine;
+  int tiles_x, tiles_y, num_tiles, num_pairs, nstages;
+  int nkc, ntaps, m_shift;
+  int wpr_in, wpr_out, nwo, int_combine;
   long long in_st, in_sb, out_st, out_sb;
   float decay, v_th, v_reset, agg_scale;
-  uint32_t off_w, off_a, a_stage_bytes, off_stage, off_pinfo, off_scale, off_bar, smem_bytes;
-  uint32_t w_bytes_cta, tmem_cols, n_total, lbo_a, lbo_b;
+  uint32_t off_w, off_a, a_stage_bytes, off_scale, off_bar, smem_bytes;
+  uint32_t w_bytes_cta, tmem_cols, n_total, lbo_a, sbo_a, lbo_b;
   int tap_off[9];
   const uint32_t *in;
   uint32_t *out;
@@ -100,9 +104,8 @@ int path_of(const tac_conv_lif_desc *d) {
 }
 
 struct Geometry {
-  int path, Sh, Sw, halo_rows, nkc, ntaps, cout_pad, nsteps;
-  uint32_t w_bytes_cta, a_stage_bytes, stage_bytes, off_w, off_a, off_stage, off_pinfo, off_scale,
-      off_bar, smem_bytes;
+  int path, nkc, ntaps, cout_pad, nsteps, nstages;
+  uint32_t w_bytes_cta, a_stage_bytes, off_w, off_a, off_scale, off_bar, smem_bytes;
 };
 
 uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
@@ -114,31 +117,25 @@ Geometry geometry(const tac_conv_lif_desc *d) {
   const int K = d->mode == TAC_MODE_DENSE ? 1 : d->K;
   g.nsteps = d->mode == TAC_MODE_TACTP ? K : 1;
   if (g.path == PATH_HALO) {
-    g.Sh = d->H + d->pad;
-    g.Sw = d->W + d->pad;
-    g.halo_rows = (int)align_up(128 + 2 * g.Sw + 2, 8);
     g.nkc = d->C_in / 16;
     g.ntaps = 9;
     g.w_bytes_cta = 9u * d->C_in * g.cout_pad;
-    g.a_stage_bytes = align_up((uint32_t)g.halo_rows * d->C_in, 128);
+    g.a_stage_bytes = align_up((uint32_t)kHaloRows * d->C_in, 128);
   } else {
-    g.Sh = d->H;
-    g.Sw = d->W;
-    g.halo_rows = 128;
     g.nkc = 2;
     g.ntaps = 1;
     g.w_bytes_cta = 32u * g.cout_pad;
     g.a_stage_bytes = 128u * 32u;
   }
-  const int nwt2 = std::max(2, g.cout_pad / 32);  // stage words per position
-  g.stage_bytes = (uint32_t)g.nsteps * 128u * nwt2 * 4u;
-  g.off_w = 0;
-  g.off_a = align_up(g.w_bytes_cta, 1024);
-  g.off_stage = align_up(g.off_a + kStages * g.a_stage_bytes, 128);
-  g.off_pinfo = align_up(g.off_stage + g.stage_bytes, 128);
-  g.off_scale = align_up(g.off_pinfo + 128u * 16u, 128);
-  g.off_bar = align_up(g.off_scale + 4u * g.cout_pad * 4u, 64);
-  g.smem_bytes = g.off_bar + 8u * (2 * kStages + 2 * kAccs + 1) + 16u;
+  for (g.nstages = kMaxStages; g.nstages >= 2; --g.nstages) {
+    g.off_w = 0;
+    g.off_a = align_up(g.w_bytes_cta, 1024);
+    g.off_scale = align_up(g.off_a + g.nstages * g.a_stage_bytes, 128);
+    g.off_bar = align_up(g.off_scale + 4u * g.cout_pad * 4u, 64);
+    g.smem_bytes = g.off_bar + 8u * (2 * kMaxStages + 2 * kAccs + 1) + 16u;
+    if (g.smem_bytes <= kSmemLimit) break;
+  }
+  if (g.nstages < 2) g.nstages = 2;
   return g;
 }
 
@@ -168,45 +165,15 @@ const char *reason(const tac_conv_lif_desc *d) {
 }
 
 // ------------------------------------------------------------ device code ---
-// Per-position output descriptor, rebuilt at the start of every tile by the
-// epilogue (replaces per-task 64-bit divisions in the store pass).
-struct __align__(16) PInfo {
-  long long off;  // word offset of this position's output in a (t) plane; -1: no store
-  int org;        // pooled halo path: tile-local index of the 2x2 window origin
-  int aux;        // bits 0-3: in-tile member mask (pooled halo), bits 8-12: bit shift
-};
-
-template <int PATH>
-__device__ __forceinline__ void decode_out(const TcParams &p, long long L, int &b, int &y, int &x,
-                                           bool &valid) {
-  if (PATH == PATH_HALO) {
-    const long long per = (long long)p.Sh * p.Sw;
-    const long long bb = L / per;
-    const int rem = (int)(L - bb * per);
-    y = rem / p.Sw;
-    x = rem - y * p.Sw;
-    b = (int)bb;
-    valid = bb < p.B && y < p.Ho && x < p.Wo;
-  } else if (p.pool == 2) {  // quad-major: the 4 members of a 2x2 pool window adjacent
-    const long long q = L >> 2;
-    const int mem = (int)(L & 3);
-    const long long per = (long long)p.Hq * p.Wq;
-    const long long bb = q / per;
-    const int rq = (int)(q - bb * per);
-    const int py = rq / p.Wq, px = rq - (rq / p.Wq) * p.Wq;
-    y = 2 * py + (mem >> 1);
-    x = 2 * px + (mem & 1);
-    b = (int)bb;
-    valid = bb < p.B;
-  } else {
-    const long long per = (long long)p.Ho * p.Wo;
-    const long long bb = L / per;
-    const int rem = (int)(L - bb * per);
-    y = rem / p.Wo;
-    x = rem - y * p.Wo;
-    b = (int)bb;
-    valid = bb < p.B;
-  }
+__device__ __forceinline__ void tile_origin(const TcParams &p, int tile, int &b, int &y0, int &x0,
+                                            bool &ok) {
+  const int per = p.tiles_y * p.tiles_x;
+  b = tile / per;
+  const int rem = tile - b * per;
+  const int ty = rem / p.tiles_x;
+  y0 = ty * kTileH;
+  x0 = (rem - ty * p.tiles_x) * kTileW;
+  ok = tile < p.num_tiles;
 }
 
 // --- producers: build the u8 aggregate A_k * 2^{m(K-1)} in the MMA layout ---
@@ -223,45 +190,33 @@ __device__ __forceinline__ void agg_word_k(uint32_t (&o)[8], const uint32_t *xj,
   }
 }
 
-// Halo producer.  The thread owns 32-channel word w of halo rows row0, row0 +
-// rstep, ... (96 % nwin == 0).  Loads are issued in batches of RB rows x K
-// frames before any is consumed, so one memory round trip covers RB rows.
+// Halo producer: the thread owns 32-channel word w of halo pixels row0, row0 +
+// rstep, ... (96 % nwin == 0).  Loads are issued in batches of RB pixels x K
+// frames before any is consumed, so one memory round trip covers RB pixels.
 template <int K>
 __device__ __forceinline__ void produce_halo(const TcParams &p, int tile, int k, uint32_t a_stage,
                                              int ptid) {
-  constexpr int RB = K >= 8 ? 2 : (K >= 4 ? 6 : 12);
+  constexpr int RB = K >= 8 ? 2 : (K >= 4 ? 8 : 12);
   const int nwin = p.Cin >> 5;
   const int w = ptid % nwin, row0 = ptid / nwin, rstep = (kProdWarps * 32) / nwin;
-  const long long L = (long long)tile * 128 + row0;
-  const long long per = (long long)p.Sh * p.Sw;
-  long long bb = L / per;
-  int rem = (int)(L - bb * per);
-  int yy = rem / p.Sw, xx = rem - (rem / p.Sw) * p.Sw;
-  const uint32_t *frame0 = p.in + (long long)(k * K) * p.in_st + w;
+  int b, y0, x0;
+  bool tok;
+  tile_origin(p, tile, b, y0, x0, tok);
+  const uint32_t *frame0 = p.in + (long long)(k * K) * p.in_st + (long long)b * p.in_sb + w;
   const long long in_st = p.in_st;
   const int mshift = p.m_shift;
-  const int nrows = row0 < p.halo_rows ? (p.halo_rows - row0 + rstep - 1) / rstep : 0;
+  const int nrows = row0 < kHaloRows ? (kHaloRows - row0 + rstep - 1) / rstep : 0;
   for (int ib = 0; ib < nrows; ib += RB) {
     uint32_t xs[RB][K];
-    bool ok[RB];
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
-      ok[r] = false;
-      if (ib + r < nrows) {
-        const int yi = yy - p.pad, xi = xx - p.pad;
-        ok[r] = bb < p.B && yi >= 0 && yi < p.H && xi >= 0 && xi < p.W;
-        const uint32_t *src = frame0 + bb * p.in_sb + (long long)yi * p.wpr_in + xi * nwin;
+      const int row = row0 + (ib + r) * rstep;
+      const int hy = row / kHaloW, hx = row - (row / kHaloW) * kHaloW;
+      const int yi = y0 + hy - p.pad, xi = x0 + hx - p.pad;
+      const bool ok = tok && ib + r < nrows && yi >= 0 && yi < p.H && xi >= 0 && xi < p.W;
+      const uint32_t *src = frame0 + (long long)yi * p.wpr_in + xi * nwin;
 #pragma unroll
-        for (int j = 0; j < K; ++j) xs[r][j] = ok[r] ? __ldg(src + j * in_st) : 0u;
-        xx += rstep;  // advance the padded-linear position by rstep rows
-        while (xx >= p.Sw) {
-          xx -= p.Sw;
-          if (++yy == p.Sh) {
-            yy = 0;
-            ++bb;
-          }
-        }
-      }
+      for (int j = 0; j < K; ++j) xs[r][j] = ok ? __ldg(src + j * in_st) : 0u;
     }
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
@@ -277,15 +232,18 @@ __device__ __forceinline__ void produce_halo(const TcParams &p, int tile, int k,
   }
 }
 
+// im2col producer (C_in <= 2): one 32-byte A row per tile pixel; byte r of word
+// q = (window row r, window bit q) with window bit q = s * C_in + c.
 template <int K>
 __device__ __forceinline__ void produce_im2col(const TcParams &p, int tile, int k,
                                                uint32_t a_stage, int ptid) {
-  const long long L0 = (long long)tile * 128;
+  int b, y0, x0;
+  bool tok;
+  tile_origin(p, tile, b, y0, x0, tok);
   const uint32_t wmask = (1u << (3 * p.Cin)) - 1u;
   for (int pos = ptid; pos < 128; pos += kProdWarps * 32) {
-    int b, y, x;
-    bool valid;
-    decode_out<PATH_IM2COL>(p, L0 + pos, b, y, x, valid);
+    const int y = y0 + (pos >> 3), x = x0 + (pos & 7);
+    const bool valid = tok && y < p.Ho && x < p.Wo;
     const int bit0 = (x - p.pad) * p.Cin;
     const int w0 = bit0 >= 0 ? (bit0 >> 5) : -1;  // bit0 >= -2
     const int sh = bit0 - w0 * 32;
@@ -314,7 +272,6 @@ __device__ __forceinline__ void produce_im2col(const TcParams &p, int tile, int 
         for (int r = 0; r < 3; ++r)
           z |= (__funnelshift_r(lo[j][r], hi[j][r], sh) & wmask) << (8 * r);
         const int e = p.m_shift * (j0 + j);
-        // word q, byte r <- (row r, window bit q): K-index 4q + r
 #pragma unroll
         for (int q = 0; q < 6; ++q) o[q] |= ((z >> q) & 0x00010101u) << e;
       }
@@ -330,11 +287,12 @@ __device__ __forceinline__ void producer_role(const TcParams &p, uint32_t sbase,
                                               uint32_t bar_a_full, uint32_t bar_a_empty, int cid,
                                               int ncl, uint32_t rank, uint32_t lane) {
   const int ptid = (int)threadIdx.x - 32;
+  const uint32_t ns = (uint32_t)p.nstages;
   uint32_t it = 0;
   for (int pair = cid; pair < p.num_pairs; pair += ncl) {
     const int tile = 2 * pair + (int)rank;
     for (int k = 0; k < p.G; ++k, ++it) {
-      const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
+      const uint32_t s = it % ns, ph = (it / ns) & 1u;
       ptx::mbar_wait(bar_a_empty + 8 * s, ph ^ 1u);
       const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
       if (PATH == PATH_HALO)
@@ -365,27 +323,19 @@ __device__ __forceinline__ uint32_t warp_col_popc(uint32_t x, uint32_t lane) {
   return __popc(x);
 }
 
+// counts[b][co] += column sums of the bit-sliced per-lane counters (one sample
+// per warp: a tile never spans samples); clears the counters
 template <int NWT>
 __device__ __forceinline__ void flush_counts(const TcParams &p, uint32_t (&planes)[kPlanes][NWT],
-                                             bool valid, int b, int co_base, int nch,
-                                             uint32_t lane) {
-  uint32_t rem = __ballot_sync(0xFFFFFFFFu, valid);
-  while (rem) {
-    const int leader = __ffs(rem) - 1;
-    const int bsel = __shfl_sync(0xFFFFFFFFu, b, leader);
-    const bool mine = valid && b == bsel;
-    rem &= ~__ballot_sync(0xFFFFFFFFu, mine);
+                                             int b, int co_base, int nch, uint32_t lane) {
 #pragma unroll
-    for (int w = 0; w < NWT; ++w) {
-      uint32_t total = 0;
+  for (int w = 0; w < NWT; ++w) {
+    uint32_t total = 0;
 #pragma unroll
-      for (int pl = 0; pl < kPlanes; ++pl)
-        total += warp_col_popc(mine ? planes[pl][w] : 0u, lane) << pl;
-      const int c = w * 32 + (int)lane;
-      const int co = co_base + c;
-      if (total && c < nch && co < p.Cout)
-        atomicAdd(p.counts + (long long)bsel * p.Cout + co, total);
-    }
+    for (int pl = 0; pl < kPlanes; ++pl) total += warp_col_popc(planes[pl][w], lane) << pl;
+    const int c = w * 32 + (int)lane;
+    const int co = co_base + c;
+    if (total && c < nch && co < p.Cout) atomicAdd(p.counts + (long long)b * p.Cout + co, total);
   }
 #pragma unroll
   for (int pl = 0; pl < kPlanes; ++pl)
@@ -444,6 +394,15 @@ __device__ __forceinline__ void lif_pair_sub(float2 &v, float2 y, float2 dec2, f
   }
 }
 
+template <int NSP, int CB>
+__device__ __forceinline__ void lif_chunk8(float2 *V, const float (&yv)[8], float2 dec2,
+                                           float2 nth2, uint32_t (&invp)[NSP]) {
+  lif_pair_sub<NSP, CB + 0>(V[0], make_float2(yv[0], yv[1]), dec2, nth2, invp);
+  lif_pair_sub<NSP, CB + 2>(V[1], make_float2(yv[2], yv[3]), dec2, nth2, invp);
+  lif_pair_sub<NSP, CB + 4>(V[2], make_float2(yv[4], yv[5]), dec2, nth2, invp);
+  lif_pair_sub<NSP, CB + 6>(V[3], make_float2(yv[6], yv[7]), dec2, nth2, invp);
+}
+
 // Y for 8 channels from the two s32 accumulator slices (see file header)
 __device__ __forceinline__ void combine8(const TcParams &p, const float *sc, int co,
                                          const uint32_t (&d1)[8], const uint32_t (&d2)[8],
@@ -473,22 +432,19 @@ __device__ __forceinline__ void combine8(const TcParams &p, const float *sc, int
 
 // NS > 0: subtract reset with NS LIF steps per group (specialised hot path);
 // NS == 0: any reset, runtime step count.
-template <int NCH, int PATH, int NS>
+template <int NCH, int NS>
 __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, uint32_t tmem_base,
                                               uint32_t bar_t_full, uint32_t bar_t_empty, int cid,
                                               int ncl, uint32_t rank, uint32_t warp,
                                               uint32_t lane) {
   constexpr int NWT = NCH >= 32 ? NCH / 32 : 1;  // spike words per epilogue thread
-  constexpr int SROW = NCH >= 32 ? 2 * NWT : 2;  // stage words per position
   constexpr int NSM = NS ? NS : kMaxSteps;
   const float *sc = reinterpret_cast<const float *>(smem + p.off_scale);
-  uint32_t *stage = reinterpret_cast<uint32_t *>(smem + p.off_stage);
-  PInfo *pinfo = reinterpret_cast<PInfo *>(smem + p.off_pinfo);
   const int e = (int)warp - 1 - kProdWarps;  // 0..7
   const int quad = (int)(warp & 3);           // TMEM lane quadrant of this warp
   const int half = e >> 2;                    // channel half
-  const int m = quad * 32 + (int)lane;        // position within the CTA tile
-  const int tid_e = e * 32 + (int)lane;       // 0..255
+  const int g = quad * 4 + (int)(lane >> 3);  // tile row of this lane's pixel
+  const int c = (int)(lane & 7);              // tile column
   const int co_base = half * NCH;
   const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
   const float decay = p.decay, vth = p.v_th, vres = p.v_reset;
@@ -496,57 +452,23 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
   const int nsteps = NS ? NS : p.nsteps;
   const int G = p.G, K = p.K, mode = p.mode, nwo = p.nwo, Cout = p.Cout, Cp = p.Cout_pad;
   const uint32_t chmask = NCH >= 32 ? 0xFFFFFFFFu : ((1u << NCH) - 1u);
+  const bool pooled = p.pool == 2;
+  const bool active_half = co_base < Cout;
   uint32_t it = 0;
   for (int pair = cid; pair < p.num_pairs; pair += ncl) {
     const int tile = 2 * pair + (int)rank;
-    const long long L0 = (long long)tile * 128;
-    int b, y, x;
-    bool valid;
-    decode_out<PATH>(p, L0 + m, b, y, x, valid);
-    if (half == 0) {  // per-tile output descriptors (read by the store pass)
-      PInfo pi;
-      pi.off = -1;
-      pi.org = 0;
-      pi.aux = 0;
-      if (valid) {
-        int yo = y, xo = x;
-        bool store = true;
-        if (p.pool == 2) {
-          yo = y >> 1;
-          xo = x >> 1;
-          if (PATH == PATH_IM2COL) {
-            store = (m & 3) == 0;
-          } else {
-            const int y0 = y & ~1, x0 = x & ~1;
-            const long long Lq = ((long long)b * p.Sh + y0) * p.Sw + x0;
-            const long long org = Lq - L0;
-            const long long mem[4] = {org, org + 1, org + p.Sw, org + p.Sw + 1};
-            int mask = 0, leader = -1;
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-              if (mem[t] >= 0 && mem[t] < 128) {
-                mask |= 1 << t;
-                if (leader < 0) leader = (int)mem[t];
-              }
-            store = leader == m;
-            pi.org = (int)org;
-            pi.aux = mask;
-          }
-        }
-        if (store) {
-          const long long rowoff = (long long)b * p.out_sb + (long long)yo * p.wpr_out;
-          if (Cout % 32 == 0) {
-            pi.off = rowoff + (long long)xo * nwo;
-          } else {
-            const long long bit = (long long)xo * Cout;
-            pi.off = rowoff + (bit >> 5);
-            pi.aux |= (int)(bit & 31) << 8;
-          }
-        }
-      }
-      pinfo[m] = pi;
-    }
+    int b, y0, x0;
+    bool tok;
+    tile_origin(p, tile, b, y0, x0, tok);
+    const int y = y0 + g, x = x0 + c;
+    const bool valid = tok && y < p.Ho && x < p.Wo;
     const long long vbase = (((long long)b * p.Ho + y) * p.Wo + x) * Cout + co_base;
+    // output word address of this lane (pooled: of its 2x2 window; only lanes with
+    // (lane & 9) == 0 store, after the in-warp OR)
+    const int yo = pooled ? (y >> 1) : y, xo = pooled ? (x >> 1) : x;
+    uint32_t *orow = p.out + (long long)b * p.out_sb + (long long)yo * p.wpr_out;
+    const bool store_lane = valid && active_half && (!pooled || (lane & 9) == 0);
+    long long obit = (long long)xo * Cout + co_base;  // NCH < 32: bit offset of the field
     float2 V[NCH / 2];
     uint32_t prev[NWT];
     uint32_t planes[kPlanes][NWT];
@@ -558,16 +480,16 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
       for (int pl = 0; pl < kPlanes; ++pl) planes[pl][w] = 0u;
     }
 #pragma unroll
-    for (int c = 0; c < NCH; c += 2) {
+    for (int cc = 0; cc < NCH; cc += 2) {
       float v0 = 0.f, v1 = 0.f;
       if (p.v_init && valid) {
-        if (co_base + c < Cout) v0 = __ldg(p.v_init + vbase + c);
-        if (co_base + c + 1 < Cout) v1 = __ldg(p.v_init + vbase + c + 1);
+        if (co_base + cc < Cout) v0 = __ldg(p.v_init + vbase + cc);
+        if (co_base + cc + 1 < Cout) v1 = __ldg(p.v_init + vbase + cc + 1);
       }
-      V[c / 2] = make_float2(v0, v1);
+      V[cc / 2] = make_float2(v0, v1);
       if (NS == 0 && p.reset == 1) {  // reading R4
-        if (v0 >= vth) prev[c / 32] |= 1u << (c % 32);
-        if (v1 >= vth) prev[(c + 1) / 32] |= 1u << ((c + 1) % 32);
+        if (v0 >= vth) prev[cc / 32] |= 1u << (cc % 32);
+        if (v1 >= vth) prev[(cc + 1) / 32] |= 1u << ((cc + 1) % 32);
       }
     }
     for (int k = 0; k < G; ++k, ++it) {
@@ -599,51 +521,30 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
           uint32_t invp[NSP];
 #pragma unroll
           for (int j = 0; j < NSP; ++j) invp[j] = inv[j][w];
-          // channel offsets within the word are compile-time: (ch*8) % 32 + i
-          switch ((ch * 8) % 32) {
-            case 0:
-              lif_pair_sub<NSP, 0>(V[ch * 4 + 0], make_float2(yv[0], yv[1]), dec2, nth2, invp);
-              lif_pair_sub<NSP, 2>(V[ch * 4 + 1], make_float2(yv[2], yv[3]), dec2, nth2, invp);
-              lif_pair_sub<NSP, 4>(V[ch * 4 + 2], make_float2(yv[4], yv[5]), dec2, nth2, invp);
-              lif_pair_sub<NSP, 6>(V[ch * 4 + 3], make_float2(yv[6], yv[7]), dec2, nth2, invp);
-              break;
-            case 8:
-              lif_pair_sub<NSP, 8>(V[ch * 4 + 0], make_float2(yv[0], yv[1]), dec2, nth2, invp);
-              lif_pair_sub<NSP, 10>(V[ch * 4 + 1], make_float2(yv[2], yv[3]), dec2, nth2, invp);
-              lif_pair_sub<NSP, 12>(V[ch * 4 + 2], make_float2(yv[4], yv[5]), dec2, nth2, invp);
-              lif_pair_sub<NSP, 14>(V[ch * 4 + 3], make_float2(yv[6], yv[7]), dec2, nth2, invp);
-              break;
-            case 16:
-              lif_pair_sub<NSP, 16>(V[ch * 4 + 0], make_float2(yv[0], yv[1]), dec2, nth2, invp);
-              lif_pair_sub<NSP, 18>(V[ch * 4 + 1], make_float2(yv[2], yv[3]), dec2, nth2, invp);
-              lif_pair_sub<NSP, 20>(V[ch * 4 + 2], make_float2(yv[4], yv[5]), dec2, nth2, invp);
-              lif_pair_sub<NSP, 22>(V[ch * 4 + 3], make_float2(yv[6], yv[7]), dec2, nth2, invp);
-              break;
-            default:
-              lif_pair_sub<NSP, 24>(V[ch * 4 + 0], make_float2(yv[0], yv[1]), dec2, nth2, invp);
-              lif_pair_sub<NSP, 26>(V[ch * 4 + 1], make_float2(yv[2], yv[3]), dec2, nth2, invp);
-              lif_pair_sub<NSP, 28>(V[ch * 4 + 2], make_float2(yv[4], yv[5]), dec2, nth2, invp);
-              lif_pair_sub<NSP, 30>(V[ch * 4 + 3], make_float2(yv[6], yv[7]), dec2, nth2, invp);
-              break;
+          switch ((ch * 8) % 32) {  // compile-time after unrolling
+            case 0: lif_chunk8<NSP, 0>(V + ch * 4, yv, dec2, nth2, invp); break;
+            case 8: lif_chunk8<NSP, 8>(V + ch * 4, yv, dec2, nth2, invp); break;
+            case 16: lif_chunk8<NSP, 16>(V + ch * 4, yv, dec2, nth2, invp); break;
+            default: lif_chunk8<NSP, 24>(V + ch * 4, yv, dec2, nth2, invp); break;
           }
 #pragma unroll
           for (int j = 0; j < NSP; ++j) inv[j][w] = invp[j];
         } else {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const int c = ch * 8 + i;
-            const uint32_t bm = 1u << (c % 32);
-            float v = (i & 1) ? V[c / 2].y : V[c / 2].x;
+            const int cc = ch * 8 + i;
+            const uint32_t bm = 1u << (cc % 32);
+            float v = (i & 1) ? V[cc / 2].y : V[cc / 2].x;
             const int rs = p.reset;
 #pragma unroll
             for (int j = 0; j < kMaxSteps; ++j) {
               if (j < nsteps) {
-                if (rs == 0) lif_step<0>(v, yv[i], decay, vth, vres, inv[j][c / 32], bm, prev[c / 32]);
-                else if (rs == 1) lif_step<1>(v, yv[i], decay, vth, vres, inv[j][c / 32], bm, prev[c / 32]);
-                else lif_step<2>(v, yv[i], decay, vth, vres, inv[j][c / 32], bm, prev[c / 32]);
+                if (rs == 0) lif_step<0>(v, yv[i], decay, vth, vres, inv[j][cc / 32], bm, prev[cc / 32]);
+                else if (rs == 1) lif_step<1>(v, yv[i], decay, vth, vres, inv[j][cc / 32], bm, prev[cc / 32]);
+                else lif_step<2>(v, yv[i], decay, vth, vres, inv[j][cc / 32], bm, prev[cc / 32]);
               }
             }
-            if (i & 1) V[c / 2].y = v; else V[c / 2].x = v;
+            if (i & 1) V[cc / 2].y = v; else V[cc / 2].x = v;
           }
         }
         if (ch + 1 < NCH / 8) ptx::tmem_wait_ld_dep(d[nxt][0], d[nxt][1]);
@@ -653,101 +554,48 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_cluster_relaxed(bar_t_empty + 8 * acc, 0);
 
-      // spikes -> staging smem, bit-sliced counters
+      // spikes: bit-sliced counters, in-warp 2x2 OR-pool, direct packed stores
 #pragma unroll
       for (int j = 0; j < NSM; ++j) {
         if (NS > 0 || j < nsteps) {
+          const int t_out = mode == 1 ? k : k * K + j;
+          uint32_t *orow_t = orow + (long long)t_out * p.out_st;
 #pragma unroll
           for (int w = 0; w < NWT; ++w) {
-            const uint32_t s = valid ? (~inv[j][w] & chmask) : 0u;
-            stage[(j * 128 + m) * SROW + half * NWT + w] = s;
-            uint32_t c = s;
+            uint32_t s = valid ? (~inv[j][w] & chmask) : 0u;
+            uint32_t cy = s;
 #pragma unroll
             for (int pl = 0; pl < kPlanes; ++pl) {
-              const uint32_t t = planes[pl][w] & c;
-              planes[pl][w] ^= c;
-              c = t;
+              const uint32_t t = planes[pl][w] & cy;
+              planes[pl][w] ^= cy;
+              cy = t;
+            }
+            if (pooled) {
+              s |= __shfl_xor_sync(0xFFFFFFFFu, s, 1);
+              s |= __shfl_xor_sync(0xFFFFFFFFu, s, 8);
+            }
+            if (store_lane) {
+              if (NCH >= 32) {
+                const int wd = half * NWT + w;
+                if (wd < nwo) orow_t[(long long)xo * nwo + wd] = s;
+              } else if (s) {
+                atomicOr(orow_t + (obit >> 5), s << (obit & 31));
+              }
             }
           }
         }
       }
       steps_acc += nsteps;
       if (p.counts && (steps_acc + nsteps > (1 << kPlanes) - 1 || k == G - 1)) {
-        flush_counts<NWT>(p, planes, valid, b, co_base, NCH, lane);
+        if (tok) flush_counts<NWT>(p, planes, b, co_base, NCH, lane);
         steps_acc = 0;
       }
-      ptx::named_bar_sync(1, kEpiWarps * 32);
-
-      // staged spikes -> global packed output.  Tasks (step j, position, word)
-      // decompose with shifts (NWOP words per position is a compile-time power of 2).
-      {
-        constexpr int NWOP = NCH >= 32 ? 2 * NWT : 1;
-        constexpr int LG = NWOP == 4 ? 2 : (NWOP == 2 ? 1 : 0);
-        const bool pooled = p.pool == 2;
-        auto pix = [&](const uint32_t *st, int q, int wd) -> uint32_t {
-          const uint32_t *sr = st + q * SROW;
-          return NCH >= 32 ? sr[wd] : (sr[0] | (sr[1] << NCH));
-        };
-        if (PATH == PATH_IM2COL && pooled) {
-          // quad-major positions: window q = positions 4q .. 4q+3, all in this tile
-          const int ntask = nsteps << (5 + LG);
-          for (int t = tid_e; t < ntask; t += kEpiWarps * 32) {
-            const int wd = t & (NWOP - 1), q = (t >> LG) & 31, j = t >> (5 + LG);
-            if (wd >= nwo) continue;
-            const PInfo pi = pinfo[4 * q];
-            if (pi.off < 0) continue;
-            const uint32_t *st = stage + j * 128 * SROW;
-            const uint32_t wv = pix(st, 4 * q, wd) | pix(st, 4 * q + 1, wd) |
-                                pix(st, 4 * q + 2, wd) | pix(st, 4 * q + 3, wd);
-            const int t_out = mode == 1 ? k : k * K + j;
-            uint32_t *dst = p.out + (long long)t_out * p.out_st + pi.off;
-            if (Cout % 32 == 0)
-              dst[wd] = wv;
-            else if (wv)
-              atomicOr(dst, wv << ((pi.aux >> 8) & 31));
-          }
-        } else {
-          const int ntask = nsteps << (7 + LG);
-          const int sw = p.Sw;
-          for (int t = tid_e; t < ntask; t += kEpiWarps * 32) {
-            const int wd = t & (NWOP - 1), mm = (t >> LG) & 127, j = t >> (7 + LG);
-            if (wd >= nwo) continue;
-            const PInfo pi = pinfo[mm];
-            if (pi.off < 0) continue;
-            const uint32_t *st = stage + j * 128 * SROW;
-            uint32_t wv;
-            bool full = true;
-            if (pooled) {  // halo path: the 2x2 window may straddle tiles
-              const int mask = pi.aux & 15, o = pi.org;
-              wv = 0;
-              if (mask & 1) wv |= pix(st, o, wd);
-              if (mask & 2) wv |= pix(st, o + 1, wd);
-              if (mask & 4) wv |= pix(st, o + sw, wd);
-              if (mask & 8) wv |= pix(st, o + sw + 1, wd);
-              full = mask == 15;
-            } else {
-              wv = pix(st, mm, wd);
-            }
-            const int t_out = mode == 1 ? k : k * K + j;
-            uint32_t *dst = p.out + (long long)t_out * p.out_st + pi.off;
-            if (Cout % 32 == 0) {
-              if (full)
-                dst[wd] = wv;
-              else if (wv)
-                atomicOr(dst + wd, wv);
-            } else if (wv) {
-              atomicOr(dst, wv << ((pi.aux >> 8) & 31));
-            }
-          }
-        }
-      }
-      ptx::named_bar_sync(1, kEpiWarps * 32);
     }
     if (p.v_final && valid) {
 #pragma unroll
-      for (int c = 0; c < NCH; c += 2) {
-        if (co_base + c < Cout) p.v_final[vbase + c] = V[c / 2].x;
-        if (co_base + c + 1 < Cout) p.v_final[vbase + c + 1] = V[c / 2].y;
+      for (int cc = 0; cc < NCH; cc += 2) {
+        if (co_base + cc < Cout) p.v_final[vbase + cc] = V[cc / 2].x;
+        if (co_base + cc + 1 < Cout) p.v_final[vbase + cc + 1] = V[cc / 2].y;
       }
     }
   }
@@ -761,16 +609,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t rank = ptx::cluster_ctarank();
   const uint32_t sbase = ptx::smem_u32(smem);
   const uint32_t bar_a_full = sbase + p.off_bar;
-  const uint32_t bar_a_empty = bar_a_full + 8 * kStages;
-  const uint32_t bar_t_full = bar_a_empty + 8 * kStages;
+  const uint32_t bar_a_empty = bar_a_full + 8 * kMaxStages;
+  const uint32_t bar_t_full = bar_a_empty + 8 * kMaxStages;
   const uint32_t bar_t_empty = bar_t_full + 8 * kAccs;
   const uint32_t bar_w = bar_t_empty + 8 * kAccs;
   uint32_t *tmem_slot =
-      reinterpret_cast<uint32_t *>(smem + p.off_bar + 8 * (2 * kStages + 2 * kAccs + 1));
+      reinterpret_cast<uint32_t *>(smem + p.off_bar + 8 * (2 * kMaxStages + 2 * kAccs + 1));
   float *sc = reinterpret_cast<float *>(smem + p.off_scale);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kMaxStages; ++s) {
       ptx::mbar_init(bar_a_full + 8 * s, 2 * kProdWarps);
       ptx::mbar_init(bar_a_empty + 8 * s, 1);
     }
@@ -821,10 +669,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t n_half_bytes = (uint32_t)p.Cout_pad * 16u;
       const uint32_t w_base = sbase + p.off_w;
       const int ntaps = p.ntaps, nkc2 = p.nkc >> 1;
+      const uint32_t ns = (uint32_t)p.nstages;
       uint32_t it = 0;
       for (int pair = cid; pair < p.num_pairs; pair += ncl) {
         for (int k = 0; k < p.G; ++k, ++it) {
-          const uint32_t s = it % kStages, ph = (it / kStages) & 1u;
+          const uint32_t s = it % ns, ph = (it / ns) & 1u;
           const uint32_t acc = it % kAccs, aph = (it / kAccs) & 1u;
           ptx::mbar_wait(bar_t_empty + 8 * acc, aph ^ 1u);
           ptx::mbar_wait(bar_a_full + 8 * s, ph);
@@ -835,7 +684,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int kc2 = 0; kc2 < nkc2; ++kc2) {
               const uint64_t ad = ptx::smem_desc(
                   a_stage + (uint32_t)(2 * kc2) * p.lbo_a + (uint32_t)p.tap_off[tap] * 16u,
-                  p.lbo_a, 128u);
+                  p.lbo_a, p.sbo_a);
               const uint64_t bd = ptx::smem_desc(
                   w_base + (uint32_t)(tap * p.nkc + 2 * kc2) * n_half_bytes, p.lbo_b, 128u);
               ptx::mma_i8_cg2(d_tmem, ad, bd, idesc, (tap | kc2) ? 1u : 0u);
@@ -859,11 +708,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ================================ epilogue =================================
     const int ns = p.reset == 0 ? p.nsteps : 0;
     switch (ns) {
-      case 1: epilogue_role<NCH, PATH, 1>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      case 2: epilogue_role<NCH, PATH, 2>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      case 4: epilogue_role<NCH, PATH, 4>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      case 8: epilogue_role<NCH, PATH, 8>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      default: epilogue_role<NCH, PATH, 0>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 1: epilogue_role<NCH, 1>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 2: epilogue_role<NCH, 2>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 4: epilogue_role<NCH, 4>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 8: epilogue_role<NCH, 8>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      default: epilogue_role<NCH, 0>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
     }
   }
 
@@ -918,7 +767,7 @@ size_t tc_weights_bytes(const tac_conv_lif_desc *d) {
 // Two int8 slices per output channel, laid out as the smem image of each CTA:
 // halo  : [tap][kc16][n][16 B], K index 32w + 4o + b <-> channel 32w + o + 8b
 // im2col: [kc16 (2)][n][16 B],  K index 4o + r       <-> (r, s = o / C_in, c = o % C_in)
-// followed by fp32 [s1 | s2 | bias] per padded output channel.
+// followed by fp32 [s1/254 | bias | s1 | s2] per padded output channel.
 void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bias,
                 unsigned char *dst) {
   const Geometry g = geometry(d);
@@ -985,21 +834,21 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   const Geometry g = geometry(d);
   TcParams p{};
   p.B = lp.B; p.H = lp.H; p.W = lp.W; p.Cin = lp.Cin; p.Cout = lp.Cout; p.Cout_pad = g.cout_pad;
-  p.pad = lp.pad; p.Ho = lp.Ho; p.Wo = lp.Wo; p.Hq = lp.Hq; p.Wq = lp.Wq; p.pool = lp.pool;
+  p.pad = lp.pad; p.Ho = lp.Ho; p.Wo = lp.Wo; p.pool = lp.pool;
   p.K = lp.K; p.G = lp.G; p.nsteps = lp.nsteps; p.mode = lp.mode; p.reset = lp.reset;
-  p.Sh = g.Sh; p.Sw = g.Sw;
-  p.M_total = g.path == PATH_HALO ? (long long)lp.B * g.Sh * g.Sw : (long long)lp.B * lp.Ho * lp.Wo;
-  p.num_tiles = (int)((p.M_total + 127) / 128);
+  p.tiles_x = (lp.Wo + kTileW - 1) / kTileW;
+  p.tiles_y = (lp.Ho + kTileH - 1) / kTileH;
+  p.num_tiles = lp.B * p.tiles_x * p.tiles_y;
   p.num_pairs = (p.num_tiles + 1) / 2;
-  p.halo_rows = g.halo_rows; p.nkc = g.nkc; p.ntaps = g.ntaps;
+  p.nstages = g.nstages;
+  p.nkc = g.nkc; p.ntaps = g.ntaps;
   p.m_shift = d->mode == TAC_MODE_DENSE ? 0 : beta_shift(d->beta);
   p.wpr_in = lp.wpr_in; p.wpr_out = lp.wpr_out;
   p.nwo = lp.Cout % 32 == 0 ? lp.Cout / 32 : 1;
-  p.out_atomic = ((g.path == PATH_HALO && lp.pool == 2) || lp.Cout % 32 != 0) ? 1 : 0;
+  const bool out_atomic = g.cout_pad < 64;  // sub-word or shared-word output fields
   {  // exact s32 combine 254 D_hi + D_lo possible? |A| <= A_max, |q| <= 127, K_red terms
-    const int K = lp.K;
     double a_max = 0;
-    for (int j = 0; j < K; ++j) a_max += std::ldexp(1.0, p.m_shift * j);
+    for (int j = 0; j < lp.K; ++j) a_max += std::ldexp(1.0, p.m_shift * j);
     const double kred = g.path == PATH_HALO ? 9.0 * lp.Cin : 32.0;
     p.int_combine = (a_max * 127.0 * kred * 255.0 < 2147483647.0) ? 1 : 0;
   }
@@ -1007,22 +856,29 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   p.decay = lp.decay; p.v_th = lp.v_th; p.v_reset = lp.v_reset;
   p.agg_scale = (float)std::ldexp(1.0, -p.m_shift * (lp.K - 1));
   p.off_w = g.off_w; p.off_a = g.off_a; p.a_stage_bytes = g.a_stage_bytes;
-  p.off_stage = g.off_stage; p.off_pinfo = g.off_pinfo; p.off_scale = g.off_scale; p.off_bar = g.off_bar;
+  p.off_scale = g.off_scale; p.off_bar = g.off_bar;
   p.smem_bytes = g.smem_bytes; p.w_bytes_cta = g.w_bytes_cta;
   p.n_total = 2u * g.cout_pad;
   uint32_t cols = 32;
   while (cols < 2u * p.n_total) cols <<= 1;
   p.tmem_cols = cols;
-  p.lbo_a = g.path == PATH_HALO ? (uint32_t)g.halo_rows * 16u : 128u * 16u;
+  if (g.path == PATH_HALO) {
+    p.lbo_a = (uint32_t)kHaloRows * 16u;  // between 16-byte K chunks
+    p.sbo_a = (uint32_t)kHaloW * 16u;     // between tile rows (8-row core-matrix groups)
+    for (int t = 0; t < 9; ++t) p.tap_off[t] = (t / 3) * kHaloW + (t % 3);
+  } else {
+    p.lbo_a = 128u * 16u;
+    p.sbo_a = 128u;
+    for (int t = 0; t < 9; ++t) p.tap_off[t] = 0;
+  }
   p.lbo_b = (uint32_t)g.cout_pad * 16u;
-  for (int t = 0; t < 9; ++t) p.tap_off[t] = g.path == PATH_HALO ? (t / 3) * g.Sw + (t % 3) : 0;
   p.in = lp.in; p.out = lp.out; p.v_init = lp.v_init; p.v_final = lp.v_final; p.counts = lp.counts;
   p.w_img = tc_prep;
   p.scale_bias = reinterpret_cast<const float *>(tc_prep + 2 * (size_t)g.w_bytes_cta);
 
   cudaStream_t st = (cudaStream_t)stream;
-  if (p.out_atomic || p.counts) {
-    const long long plane = p.out_atomic ? (long long)lp.Hq * lp.wpr_out : 0;
+  if (out_atomic || p.counts) {
+    const long long plane = out_atomic ? (long long)lp.Hq * lp.wpr_out : 0;
     const long long total = std::max((long long)lp.T_out * lp.B * plane, (long long)lp.B * lp.Cout);
     const int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
     tc_zero_kernel<<<std::max(grid, 1), 256, 0, st>>>(p.out, lp.T_out, lp.B, plane, lp.out_st,
