@@ -50,8 +50,9 @@ namespace tacsnn {
 namespace {
 
 constexpr int kProdWarps = 3;
-constexpr int kEpiWarps = 8;
-constexpr int kThreads = 32 * (1 + kProdWarps + kEpiWarps);
+// epilogue: NPART channel parts x 4 TMEM lane quadrants warps
+constexpr int epi_warps(int npart) { return 4 * npart; }
+constexpr int kernel_threads(int npart) { return 32 * (1 + kProdWarps + epi_warps(npart)); }
 constexpr int kMaxStages = 3;
 constexpr int kAccs = 2;
 constexpr int kMaxSteps = 8;
@@ -196,7 +197,7 @@ __device__ __forceinline__ void agg_word_k(uint32_t (&o)[8], const uint32_t *xj,
 template <int K>
 __device__ __forceinline__ void produce_halo(const TcParams &p, int tile, int k, uint32_t a_stage,
                                              int ptid) {
-  constexpr int RB = K >= 8 ? 2 : (K >= 4 ? 8 : 12);
+  constexpr int RB = K >= 8 ? 2 : (K >= 4 ? 4 : 8);
   const int nwin = p.Cin >> 5;
   const int w = ptid % nwin, row0 = ptid / nwin, rstep = (kProdWarps * 32) / nwin;
   int b, y0, x0;
@@ -432,7 +433,7 @@ __device__ __forceinline__ void combine8(const TcParams &p, const float *sc, int
 
 // NS > 0: subtract reset with NS LIF steps per group (specialised hot path);
 // NS == 0: any reset, runtime step count.
-template <int NCH, int NS>
+template <int NCH, int NPART, int NS>
 __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, uint32_t tmem_base,
                                               uint32_t bar_t_full, uint32_t bar_t_empty, int cid,
                                               int ncl, uint32_t rank, uint32_t warp,
@@ -440,9 +441,9 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
   constexpr int NWT = NCH >= 32 ? NCH / 32 : 1;  // spike words per epilogue thread
   constexpr int NSM = NS ? NS : kMaxSteps;
   const float *sc = reinterpret_cast<const float *>(smem + p.off_scale);
-  const int e = (int)warp - 1 - kProdWarps;  // 0..7
+  const int e = (int)warp - 1 - kProdWarps;  // 0 .. 4 NPART - 1
   const int quad = (int)(warp & 3);           // TMEM lane quadrant of this warp
-  const int half = e >> 2;                    // channel half
+  const int half = e >> 2;                    // channel part
   const int g = quad * 4 + (int)(lane >> 3);  // tile row of this lane's pixel
   const int c = (int)(lane & 7);              // tile column
   const int co_base = half * NCH;
@@ -502,14 +503,15 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
 #pragma unroll
         for (int w = 0; w < NWT; ++w) inv[j][w] = 0u;
       const uint32_t tcol = tmem_base + lane_addr + acc * p.n_total + (uint32_t)co_base;
-      uint32_t d[2][2][8];  // [buffer][hi/lo][col]
+      constexpr int NBUF = NPART == 2 ? 2 : 1;  // TMEM prefetch depth (registers)
+      uint32_t d[NBUF][2][8];                    // [buffer][hi/lo][col]
       ptx::tmem_ld8(tcol, d[0][0]);
       ptx::tmem_ld8(tcol + Cp, d[0][1]);
       ptx::tmem_wait_ld_dep(d[0][0], d[0][1]);
 #pragma unroll
       for (int ch = 0; ch < NCH / 8; ++ch) {
-        const int cur = ch & 1, nxt = cur ^ 1;
-        if (ch + 1 < NCH / 8) {  // prefetch the next 8 columns while this chunk computes
+        const int cur = NBUF == 2 ? (ch & 1) : 0, nxt = NBUF == 2 ? (cur ^ 1) : 0;
+        if (NBUF == 2 && ch + 1 < NCH / 8) {  // prefetch the next 8 columns
           ptx::tmem_ld8(tcol + (ch + 1) * 8, d[nxt][0]);
           ptx::tmem_ld8(tcol + Cp + (ch + 1) * 8, d[nxt][1]);
         }
@@ -547,7 +549,13 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
             if (i & 1) V[cc / 2].y = v; else V[cc / 2].x = v;
           }
         }
-        if (ch + 1 < NCH / 8) ptx::tmem_wait_ld_dep(d[nxt][0], d[nxt][1]);
+        if (ch + 1 < NCH / 8) {
+          if (NBUF == 1) {
+            ptx::tmem_ld8(tcol + (ch + 1) * 8, d[0][0]);
+            ptx::tmem_ld8(tcol + Cp + (ch + 1) * 8, d[0][1]);
+          }
+          ptx::tmem_wait_ld_dep(d[nxt][0], d[nxt][1]);
+        }
       }
       // accumulator consumed: hand TMEM back to the MMA issuer
       ptx::tc_fence_before();
@@ -601,9 +609,11 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
   }
 }
 
-template <int NCH, int PATH>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+template <int NCH, int PATH, int NPART>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART), 1)
     tc_conv_lif_kernel(const __grid_constant__ TcParams p) {
+  constexpr int kThreads = kernel_threads(NPART);
+  constexpr int kEpiWarps = epi_warps(NPART);
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = ptx::cluster_ctarank();
@@ -652,15 +662,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int ncl = (int)ptx::nclusters_x();
   const int cid = (int)ptx::cluster_id_x();
 
-  // register rebalance: MMA + producer warpgroup gives registers to the epilogue.
-  // The sum must not exceed what the launch allocated (384 x 168), or the
-  // increase blocks forever.
-  constexpr uint32_t kRegsLow = 96, kRegsHigh = 200;
-  static_assert(128 * kRegsLow + 256 * kRegsHigh <= kThreads * 168, "register budget");
-  if (warp < 4)
-    ptx::setmaxnreg_dec<kRegsLow>();
-  else
-    ptx::setmaxnreg_inc<kRegsHigh>();
+  // register rebalance (8 epilogue warps): the MMA + producer warpgroup gives
+  // registers to the epilogue.  The sum must not exceed what the launch
+  // allocated (384 x 168), or the increase blocks forever.
+  {
+    constexpr uint32_t kLaunchRegs = NPART == 2 ? 168 : 96;  // ptxas allocation at launch
+    constexpr uint32_t kRegsLow = NPART == 2 ? 96 : 64, kRegsHigh = NPART == 2 ? 200 : 104;
+    static_assert(128 * kRegsLow + 32 * epi_warps(NPART) * kRegsHigh <=
+                      kernel_threads(NPART) * kLaunchRegs, "register budget");
+    if (warp < 4)
+      ptx::setmaxnreg_dec<kRegsLow>();
+    else
+      ptx::setmaxnreg_inc<kRegsHigh>();
+  }
 
   if (warp == 0) {
     // ================================ MMA issuer (CTA 0 of the pair) =========
@@ -708,11 +722,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ================================ epilogue =================================
     const int ns = p.reset == 0 ? p.nsteps : 0;
     switch (ns) {
-      case 1: epilogue_role<NCH, 1>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      case 2: epilogue_role<NCH, 2>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      case 4: epilogue_role<NCH, 4>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      case 8: epilogue_role<NCH, 8>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      default: epilogue_role<NCH, 0>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 1: epilogue_role<NCH, NPART, 1>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 2: epilogue_role<NCH, NPART, 2>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 4: epilogue_role<NCH, NPART, 4>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 8: epilogue_role<NCH, NPART, 8>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      default: epilogue_role<NCH, NPART, 0>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
     }
   }
 
@@ -725,13 +739,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int NCH, int PATH>
+template <int NCH, int PATH, int NPART>
 cudaError_t launch_kernel(const TcParams &p, int nclusters, cudaStream_t stream) {
-  auto kern = tc_conv_lif_kernel<NCH, PATH>;
+  auto kern = tc_conv_lif_kernel<NCH, PATH, NPART>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
-  kern<<<dim3(2 * nclusters), dim3(kThreads), p.smem_bytes, stream>>>(p);
+  kern<<<dim3(2 * nclusters), dim3(kernel_threads(NPART)), p.smem_bytes, stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -889,20 +903,20 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   }
   const int nclusters = std::max(1, std::min(p.num_pairs, 74));
   cudaError_t e = cudaSuccess;
-  const int nch = g.cout_pad / 2;
+  // C_out 128: 16 epilogue warps x 32 channels; smaller C_out: 8 warps x C_out/2
   if (g.path == PATH_HALO) {
-    switch (nch) {
-      case 8: e = launch_kernel<8, PATH_HALO>(p, nclusters, st); break;
-      case 16: e = launch_kernel<16, PATH_HALO>(p, nclusters, st); break;
-      case 32: e = launch_kernel<32, PATH_HALO>(p, nclusters, st); break;
-      default: e = launch_kernel<64, PATH_HALO>(p, nclusters, st); break;
+    switch (g.cout_pad) {
+      case 16: e = launch_kernel<8, PATH_HALO, 2>(p, nclusters, st); break;
+      case 32: e = launch_kernel<16, PATH_HALO, 2>(p, nclusters, st); break;
+      case 64: e = launch_kernel<32, PATH_HALO, 2>(p, nclusters, st); break;
+      default: e = launch_kernel<32, PATH_HALO, 4>(p, nclusters, st); break;
     }
   } else {
-    switch (nch) {
-      case 8: e = launch_kernel<8, PATH_IM2COL>(p, nclusters, st); break;
-      case 16: e = launch_kernel<16, PATH_IM2COL>(p, nclusters, st); break;
-      case 32: e = launch_kernel<32, PATH_IM2COL>(p, nclusters, st); break;
-      default: e = launch_kernel<64, PATH_IM2COL>(p, nclusters, st); break;
+    switch (g.cout_pad) {
+      case 16: e = launch_kernel<8, PATH_IM2COL, 2>(p, nclusters, st); break;
+      case 32: e = launch_kernel<16, PATH_IM2COL, 2>(p, nclusters, st); break;
+      case 64: e = launch_kernel<32, PATH_IM2COL, 2>(p, nclusters, st); break;
+      default: e = launch_kernel<32, PATH_IM2COL, 4>(p, nclusters, st); break;
     }
   }
   ++*launches;
