@@ -35,6 +35,8 @@
 //   warps 4..11 : epilogue  -- TMEM -> registers, LIF over K steps, pooled /
 //                 packed stores, bit-sliced spike counts, v_init / v_final
 // Pipelines: A stages (2-3) producer -> MMA, TMEM accumulators (2) MMA -> epilogue.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -65,6 +67,9 @@ constexpr uint32_t kSmemLimit = 232448;
 enum { PATH_HALO = 0, PATH_IM2COL = 1 };
 
 struct TcParams {
+  CUtensorMap tmap;  // 4-D [T][B][H][WPR] u32 view of the input spikes (TMA producer)
+  int use_tma, raw_bw, nraw;
+  uint32_t off_raw, raw_stage_bytes, raw_box_bytes;
   int B, H, W, Cin, Cout, Cout_pad, pad, Ho, Wo, pool;
   int K, G, nsteps, mode, reset;
   int tiles_x, tiles_y, num_tiles, num_pairs, nstages;
@@ -105,13 +110,18 @@ int path_of(const tac_conv_lif_desc *d) {
 }
 
 struct Geometry {
-  int path, nkc, ntaps, cout_pad, nsteps, nstages;
-  uint32_t w_bytes_cta, a_stage_bytes, off_w, off_a, off_scale, off_bar, smem_bytes;
+  int path, nkc, ntaps, cout_pad, nsteps, nstages, use_tma, nraw, raw_bw;
+  uint32_t w_bytes_cta, a_stage_bytes, raw_stage_bytes, raw_box_bytes, off_w, off_a, off_raw,
+      off_scale, off_bar, smem_bytes;
 };
+constexpr int kMaxRaw = 2;
+constexpr int kNumBars = 2 * kMaxStages + 2 * kAccs + 1 + kMaxRaw;
 
 uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
-Geometry geometry(const tac_conv_lif_desc *d) {
+// Shared-memory plan.  With use_tma the producers aggregate from a TMA-loaded
+// raw halo ([K][18][raw_bw] u32 per stage) instead of loading from global.
+Geometry geometry(const tac_conv_lif_desc *d, bool use_tma = false) {
   Geometry g{};
   g.path = path_of(d);
   g.cout_pad = cout_pad_of(d->C_out);
@@ -122,21 +132,29 @@ Geometry geometry(const tac_conv_lif_desc *d) {
     g.ntaps = 9;
     g.w_bytes_cta = 9u * d->C_in * g.cout_pad;
     g.a_stage_bytes = align_up((uint32_t)kHaloRows * d->C_in, 128);
+    g.raw_bw = (int)align_up(kHaloW * (d->C_in / 32), 4);
   } else {
     g.nkc = 2;
     g.ntaps = 1;
     g.w_bytes_cta = 32u * g.cout_pad;
     g.a_stage_bytes = 128u * 32u;
+    g.raw_bw = 4;
   }
-  for (g.nstages = kMaxStages; g.nstages >= 2; --g.nstages) {
+  g.raw_box_bytes = (uint32_t)K * kHaloH * g.raw_bw * 4u;
+  g.raw_stage_bytes = align_up(g.raw_box_bytes, 128);
+  const int combos[4][2] = {{3, 2}, {2, 2}, {3, 1}, {2, 1}};
+  for (int ci = 0; ci < (use_tma ? 4 : 2); ++ci) {
+    g.nstages = use_tma ? combos[ci][0] : (ci == 0 ? 3 : 2);
+    g.nraw = use_tma ? combos[ci][1] : 0;
     g.off_w = 0;
     g.off_a = align_up(g.w_bytes_cta, 1024);
-    g.off_scale = align_up(g.off_a + g.nstages * g.a_stage_bytes, 128);
+    g.off_raw = align_up(g.off_a + g.nstages * g.a_stage_bytes, 128);
+    g.off_scale = align_up(g.off_raw + g.nraw * g.raw_stage_bytes, 128);
     g.off_bar = align_up(g.off_scale + 4u * g.cout_pad * 4u, 64);
-    g.smem_bytes = g.off_bar + 8u * (2 * kMaxStages + 2 * kAccs + 1) + 16u;
+    g.smem_bytes = g.off_bar + 8u * kNumBars + 16u;
     if (g.smem_bytes <= kSmemLimit) break;
   }
-  if (g.nstages < 2) g.nstages = 2;
+  g.use_tma = use_tma && g.smem_bytes <= kSmemLimit;
   return g;
 }
 
@@ -280,6 +298,113 @@ __device__ __forceinline__ void produce_im2col(const TcParams &p, int tile, int 
     const uint32_t dst = a_stage + (uint32_t)pos * 16u;
     ptx::st_shared_v4(dst, o[0], o[1], o[2], o[3]);
     ptx::st_shared_v4(dst + p.lbo_a, o[4], o[5], o[6], o[7]);
+  }
+}
+
+// --- TMA producers: aggregate from the raw halo in smem (compact loops) --------
+template <int K>
+__device__ __forceinline__ void produce_halo_tma(const TcParams &p, const uint32_t *raw,
+                                                 uint32_t a_stage, int ptid) {
+  const int nwin = p.Cin >> 5, bw = p.raw_bw, fstride = kHaloH * p.raw_bw;
+  const int w = ptid % nwin, row0 = ptid / nwin, rstep = (kProdWarps * 32) / nwin;
+  const int mshift = p.m_shift;
+#pragma unroll 1
+  for (int row = row0; row < kHaloRows; row += rstep) {
+    const int hy = row / kHaloW, hx = row - (row / kHaloW) * kHaloW;
+    const uint32_t *src = raw + hy * bw + hx * nwin + w;
+    uint32_t xj[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) xj[j] = src[j * fstride];
+    uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    agg_word_k<K>(o, xj, mshift);
+    const uint32_t dst = a_stage + (uint32_t)(2 * w) * p.lbo_a + (uint32_t)row * 16u;
+    ptx::st_shared_v4(dst, o[0], o[1], o[2], o[3]);
+    ptx::st_shared_v4(dst + p.lbo_a, o[4], o[5], o[6], o[7]);
+  }
+}
+
+__device__ __forceinline__ int floor_div32(int v) { return v >= 0 ? (v >> 5) : -((31 - v) >> 5); }
+
+template <int K>
+__device__ __forceinline__ void produce_im2col_tma(const TcParams &p, const uint32_t *raw,
+                                                   uint32_t a_stage, int ptid, int x0) {
+  const int Cin = p.Cin, pad = p.pad;
+  const uint32_t wmask = (1u << (3 * Cin)) - 1u;
+  const int fstride = kHaloH * 4;
+  const int c0w = floor_div32((x0 - pad) * Cin);
+#pragma unroll 1
+  for (int pos = ptid; pos < 128; pos += kProdWarps * 32) {
+    const int g = pos >> 3, c = pos & 7;
+    const int bitoff = (x0 + c - pad) * Cin - c0w * 32;
+    const int w0 = bitoff >> 5, sh = bitoff & 31;
+    uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      uint32_t z = 0;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const uint32_t *rr = raw + j * fstride + (g + r) * 4 + w0;
+        z |= (__funnelshift_r(rr[0], rr[1], sh) & wmask) << (8 * r);
+      }
+      const int e = p.m_shift * j;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) o[q] |= ((z >> q) & 0x00010101u) << e;
+    }
+    const uint32_t dst = a_stage + (uint32_t)pos * 16u;
+    ptx::st_shared_v4(dst, o[0], o[1], o[2], o[3]);
+    ptx::st_shared_v4(dst + p.lbo_a, o[4], o[5], o[6], o[7]);
+  }
+}
+
+// TMA producer pipeline: producer thread 0 keeps nraw raw-halo loads in flight;
+// all 96 producer threads aggregate stage `it % nraw` into A stage `it % nstages`.
+template <int PATH, int K>
+__device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sbase,
+                                                  const uint8_t *smem, uint32_t bar_a_full,
+                                                  uint32_t bar_a_empty, uint32_t bar_raw, int cid,
+                                                  int ncl, uint32_t rank, uint32_t lane) {
+  const int ptid = (int)threadIdx.x - 32;
+  const uint32_t ns = (uint32_t)p.nstages, nr = (uint32_t)p.nraw;
+  const int nwin = p.Cin >> 5;
+  int ipair = cid, ik = 0;  // next (pair, group) whose raw halo is to be loaded
+  auto issue = [&](uint32_t slot) {
+    int b, y0, x0;
+    bool tok;
+    tile_origin(p, 2 * ipair + (int)rank, b, y0, x0, tok);
+    const int c0 = PATH == PATH_HALO ? (x0 - p.pad) * nwin : floor_div32((x0 - p.pad) * p.Cin);
+    const uint32_t bar = bar_raw + 8 * slot;
+    ptx::mbar_arrive_expect_tx(bar, p.raw_box_bytes);
+    ptx::tma_load_4d(sbase + p.off_raw + slot * p.raw_stage_bytes, &p.tmap, c0, y0 - p.pad, b,
+                     ik * K, bar);
+    if (++ik == p.G) {
+      ik = 0;
+      ipair += ncl;
+    }
+  };
+  if (ptid == 0)
+    for (uint32_t r = 0; r < nr && ipair < p.num_pairs; ++r) issue(r);
+  uint32_t it = 0;
+  for (int pair = cid; pair < p.num_pairs; pair += ncl) {
+    int b, y0, x0;
+    bool tok;
+    tile_origin(p, 2 * pair + (int)rank, b, y0, x0, tok);
+    for (int k = 0; k < p.G; ++k, ++it) {
+      const uint32_t s = it % ns, ph = (it / ns) & 1u;
+      const uint32_t r = it % nr, rph = (it / nr) & 1u;
+      ptx::mbar_wait(bar_raw + 8 * r, rph);
+      ptx::mbar_wait(bar_a_empty + 8 * s, ph ^ 1u);
+      const uint32_t *raw = reinterpret_cast<const uint32_t *>(smem + p.off_raw + r * p.raw_stage_bytes);
+      const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
+      if (PATH == PATH_HALO)
+        produce_halo_tma<K>(p, raw, a_stage, ptid);
+      else
+        produce_im2col_tma<K>(p, raw, a_stage, ptid, x0);
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(bar_a_full + 8 * s, 0);
+      ptx::named_bar_sync(2, kProdWarps * 32);  // every producer is done with raw stage r
+      if (ptid == 0 && ipair < p.num_pairs) issue(r);
+    }
   }
 }
 
@@ -623,8 +748,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
   const uint32_t bar_t_full = bar_a_empty + 8 * kMaxStages;
   const uint32_t bar_t_empty = bar_t_full + 8 * kAccs;
   const uint32_t bar_w = bar_t_empty + 8 * kAccs;
-  uint32_t *tmem_slot =
-      reinterpret_cast<uint32_t *>(smem + p.off_bar + 8 * (2 * kMaxStages + 2 * kAccs + 1));
+  const uint32_t bar_raw = bar_w + 8;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + p.off_bar + 8 * kNumBars);
   float *sc = reinterpret_cast<float *>(smem + p.off_scale);
 
   if (threadIdx.x == 0) {
@@ -637,7 +762,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
       ptx::mbar_init(bar_t_empty + 8 * a, 2 * kEpiWarps);
     }
     ptx::mbar_init(bar_w, 1);
+    for (int r = 0; r < kMaxRaw; ++r) ptx::mbar_init(bar_raw + 8 * r, 1);
     ptx::fence_mbar_init();
+    if (p.use_tma) ptx::prefetch_tmap(&p.tmap);
     // resident weights: this CTA's int8 slice of every tap
     ptx::mbar_arrive_expect_tx(bar_w, p.w_bytes_cta);
     const unsigned char *src = p.w_img + (size_t)rank * p.w_bytes_cta;
@@ -712,11 +839,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
     __syncwarp();
   } else if (warp <= kProdWarps) {
     // ================================ producers ================================
-    switch (p.K) {
-      case 1: producer_role<PATH, 1>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane); break;
-      case 2: producer_role<PATH, 2>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane); break;
-      case 4: producer_role<PATH, 4>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane); break;
-      default: producer_role<PATH, 8>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane); break;
+    if (p.use_tma) {
+      switch (p.K) {
+        case 1: producer_role_tma<PATH, 1>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, cid, ncl, rank, lane); break;
+        case 2: producer_role_tma<PATH, 2>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, cid, ncl, rank, lane); break;
+        case 4: producer_role_tma<PATH, 4>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, cid, ncl, rank, lane); break;
+        default: producer_role_tma<PATH, 8>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, cid, ncl, rank, lane); break;
+      }
+    } else {
+      switch (p.K) {
+        case 1: producer_role<PATH, 1>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane); break;
+        case 2: producer_role<PATH, 2>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane); break;
+        case 4: producer_role<PATH, 4>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane); break;
+        default: producer_role<PATH, 8>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane); break;
+      }
     }
   } else {
     // ================================ epilogue =================================
@@ -843,10 +979,51 @@ void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bi
   }
 }
 
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+}  // namespace
+
 int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned char *tc_prep,
               void *stream, int *launches) {
-  const Geometry g = geometry(d);
+  // TMA raw-halo producer when the packed input is a legal 4-D tensor-map view
+  // (16-B aligned base and strides) and the plan fits in shared memory
+  const bool tma_layout = (lp.wpr_in * 4) % 16 == 0 && (lp.in_sb * 4) % 16 == 0 &&
+                          (lp.in_st * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(lp.in) % 16) == 0;
+  Geometry g = geometry(d, tma_layout);
+  PFN_cuTensorMapEncodeTiled_v12000 encode = g.use_tma ? tensor_map_encoder() : nullptr;
+  if (!encode) g = geometry(d, false);
   TcParams p{};
+  if (g.use_tma) {
+    const int K = lp.K;
+    const cuuint64_t dims[4] = {(cuuint64_t)lp.wpr_in, (cuuint64_t)lp.H, (cuuint64_t)lp.B,
+                                (cuuint64_t)lp.T};
+    const cuuint64_t strides[3] = {(cuuint64_t)lp.wpr_in * 4, (cuuint64_t)lp.in_sb * 4,
+                                   (cuuint64_t)lp.in_st * 4};
+    const cuuint32_t box[4] = {(cuuint32_t)g.raw_bw, (cuuint32_t)kHaloH, 1u, (cuuint32_t)K};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = encode(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, (void *)lp.in, dims, strides,
+                              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) g = geometry(d, false);
+  }
+  p.use_tma = g.use_tma;
+  p.raw_bw = g.raw_bw;
+  p.nraw = g.nraw;
+  p.off_raw = g.off_raw;
+  p.raw_stage_bytes = g.raw_stage_bytes;
+  p.raw_box_bytes = g.raw_box_bytes;
   p.B = lp.B; p.H = lp.H; p.W = lp.W; p.Cin = lp.Cin; p.Cout = lp.Cout; p.Cout_pad = g.cout_pad;
   p.pad = lp.pad; p.Ho = lp.Ho; p.Wo = lp.Wo; p.pool = lp.pool;
   p.K = lp.K; p.G = lp.G; p.nsteps = lp.nsteps; p.mode = lp.mode; p.reset = lp.reset;
