@@ -132,13 +132,15 @@ Geometry geometry(const tac_conv_lif_desc *d, bool use_tma = false) {
     g.ntaps = 9;
     g.w_bytes_cta = 9u * d->C_in * g.cout_pad;
     g.a_stage_bytes = align_up((uint32_t)kHaloRows * d->C_in, 128);
-    g.raw_bw = (int)align_up(kHaloW * (d->C_in / 32), 4);
+    // TMA box start is aligned down to 16 B (4 words): up to 3 extra words in front
+    const int nwin = d->C_in / 32;
+    g.raw_bw = nwin == 4 ? kHaloW * 4 : (int)align_up(kHaloW * nwin + 3, 4);
   } else {
     g.nkc = 2;
     g.ntaps = 1;
     g.w_bytes_cta = 32u * g.cout_pad;
     g.a_stage_bytes = 128u * 32u;
-    g.raw_bw = 4;
+    g.raw_bw = 8;  // 16-B aligned start word + the <= 2 words holding the window bits
   }
   g.raw_box_bytes = (uint32_t)K * kHaloH * g.raw_bw * 4u;
   g.raw_stage_bytes = align_up(g.raw_box_bytes, 128);
@@ -302,10 +304,19 @@ __device__ __forceinline__ void produce_im2col(const TcParams &p, int tile, int 
 }
 
 // --- TMA producers: aggregate from the raw halo in smem (compact loops) --------
+// raw-halo start word of a tile: the TMA box starts 16-B aligned (word c0 & ~3)
+__device__ __forceinline__ int halo_c0(const TcParams &p, int x0) {
+  return p.Cin >= 32 ? (x0 - p.pad) * (p.Cin >> 5)
+                     : ((x0 - p.pad) * p.Cin >= 0 ? ((x0 - p.pad) * p.Cin) >> 5
+                                                  : -((31 - (x0 - p.pad) * p.Cin) >> 5));
+}
+
 template <int K>
 __device__ __forceinline__ void produce_halo_tma(const TcParams &p, const uint32_t *raw,
-                                                 uint32_t a_stage, int ptid) {
+                                                 uint32_t a_stage, int ptid, int x0) {
   const int nwin = p.Cin >> 5, bw = p.raw_bw, fstride = kHaloH * p.raw_bw;
+  const int c0 = halo_c0(p, x0);
+  raw += c0 - (c0 & ~3);
   const int w = ptid % nwin, row0 = ptid / nwin, rstep = (kProdWarps * 32) / nwin;
   const int mshift = p.m_shift;
 #pragma unroll 1
@@ -330,8 +341,8 @@ __device__ __forceinline__ void produce_im2col_tma(const TcParams &p, const uint
                                                    uint32_t a_stage, int ptid, int x0) {
   const int Cin = p.Cin, pad = p.pad;
   const uint32_t wmask = (1u << (3 * Cin)) - 1u;
-  const int fstride = kHaloH * 4;
-  const int c0w = floor_div32((x0 - pad) * Cin);
+  const int fstride = kHaloH * p.raw_bw;
+  const int c0w = halo_c0(p, x0) & ~3;
 #pragma unroll 1
   for (int pos = ptid; pos < 128; pos += kProdWarps * 32) {
     const int g = pos >> 3, c = pos & 7;
@@ -343,7 +354,7 @@ __device__ __forceinline__ void produce_im2col_tma(const TcParams &p, const uint
       uint32_t z = 0;
 #pragma unroll
       for (int r = 0; r < 3; ++r) {
-        const uint32_t *rr = raw + j * fstride + (g + r) * 4 + w0;
+        const uint32_t *rr = raw + j * fstride + (g + r) * p.raw_bw + w0;
         z |= (__funnelshift_r(rr[0], rr[1], sh) & wmask) << (8 * r);
       }
       const int e = p.m_shift * j;
@@ -365,13 +376,12 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
                                                   int ncl, uint32_t rank, uint32_t lane) {
   const int ptid = (int)threadIdx.x - 32;
   const uint32_t ns = (uint32_t)p.nstages, nr = (uint32_t)p.nraw;
-  const int nwin = p.Cin >> 5;
   int ipair = cid, ik = 0;  // next (pair, group) whose raw halo is to be loaded
   auto issue = [&](uint32_t slot) {
     int b, y0, x0;
     bool tok;
     tile_origin(p, 2 * ipair + (int)rank, b, y0, x0, tok);
-    const int c0 = PATH == PATH_HALO ? (x0 - p.pad) * nwin : floor_div32((x0 - p.pad) * p.Cin);
+    const int c0 = halo_c0(p, x0) & ~3;  // 16-B aligned box start
     const uint32_t bar = bar_raw + 8 * slot;
     ptx::mbar_arrive_expect_tx(bar, p.raw_box_bytes);
     ptx::tma_load_4d(sbase + p.off_raw + slot * p.raw_stage_bytes, &p.tmap, c0, y0 - p.pad, b,
@@ -396,7 +406,7 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
       const uint32_t *raw = reinterpret_cast<const uint32_t *>(smem + p.off_raw + r * p.raw_stage_bytes);
       const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
       if (PATH == PATH_HALO)
-        produce_halo_tma<K>(p, raw, a_stage, ptid);
+        produce_halo_tma<K>(p, raw, a_stage, ptid, x0);
       else
         produce_im2col_tma<K>(p, raw, a_stage, ptid, x0);
       ptx::fence_proxy_async_smem();
