@@ -522,7 +522,10 @@ __device__ __forceinline__ void lif_pair_sub(float2 &v, float2 y, float2 dec2, f
     v = __ffma2_rn(dec2, v, y);                       // V <- beta V + Y
     const float2 v2 = __fadd2_rn(v, nth2);            // V - v_th
     const uint32_t a0 = __float_as_uint(v2.x), a1 = __float_as_uint(v2.y);
-    const uint32_t m0 = (uint32_t)((int)a0 >> 31), m1 = (uint32_t)((int)a1 >> 31);
+    // sign masks: one on the ALU pipe (SHF), one on the FMA pipe (IMAD.HI) for balance
+    const uint32_t m0 = (uint32_t)((int)a0 >> 31);
+    uint32_t m1;
+    asm("mul.hi.s32 %0, %1, 1;" : "=r"(m1) : "r"(a1));
     v.x = __uint_as_float(lop3_select(a0, __float_as_uint(v.x), m0));  // spike: V - v_th
     v.y = __uint_as_float(lop3_select(a1, __float_as_uint(v.y), m1));
     inv[j] = mad_bit<1u << C0>(m0, inv[j]);
@@ -564,6 +567,37 @@ __device__ __forceinline__ void combine8(const TcParams &p, const float *sc, int
       y[i] = fmaf((float)(int)d1[i], s1, fmaf((float)(int)d2[i], s2, b));
     }
   }
+}
+
+#define TAC_LOP3(d, a, b, c, lut) asm("lop3.b32 %0, %1, %2, %3, " #lut ";" : "=r"(d) : "r"(a), "r"(b), "r"(c))
+
+// Add a small count (bit-planes v0 + 2 v1 + 4 v2, any of them may be absent) into
+// the 6 bit-sliced per-lane counters P (one bit per channel).
+__device__ __forceinline__ void planes_add3(uint32_t *P, uint32_t v0, uint32_t v1, uint32_t v2) {
+  uint32_t c0, c1, c2, x;
+  c0 = P[0] & v0;
+  P[0] ^= v0;
+  TAC_LOP3(x, P[1], v1, c0, 0x96);   // sum
+  TAC_LOP3(c1, P[1], v1, c0, 0xE8);  // majority (carry)
+  P[1] = x;
+  TAC_LOP3(x, P[2], v2, c1, 0x96);
+  TAC_LOP3(c2, P[2], v2, c1, 0xE8);
+  P[2] = x;
+  const uint32_t c3 = P[3] & c2;
+  P[3] ^= c2;
+  const uint32_t c4 = P[4] & c3;
+  P[4] ^= c3;
+  P[5] ^= c4;
+}
+
+// carry-save count of 4 spike words -> planes (u + 2 t1 + 4 t2)
+__device__ __forceinline__ void planes_add4(uint32_t *P, uint32_t s0, uint32_t s1, uint32_t s2,
+                                            uint32_t s3) {
+  uint32_t u, v;
+  TAC_LOP3(u, s0, s1, s2, 0x96);
+  TAC_LOP3(v, s0, s1, s2, 0xE8);
+  const uint32_t u2 = u ^ s3, c = u & s3;
+  planes_add3(P, u2, v ^ c, v & c);
 }
 
 // NS > 0: subtract reset with NS LIF steps per group (specialised hot path);
@@ -706,12 +740,14 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
 #pragma unroll
           for (int w = 0; w < NWT; ++w) {
             uint32_t s = valid ? (~inv[j][w] & chmask) : 0u;
-            uint32_t cy = s;
+            if (NS == 0 || NS == 1) {  // ripple add of one word into the counters
+              uint32_t cy = s;
 #pragma unroll
-            for (int pl = 0; pl < kPlanes; ++pl) {
-              const uint32_t t = planes[pl][w] & cy;
-              planes[pl][w] ^= cy;
-              cy = t;
+              for (int pl = 0; pl < kPlanes; ++pl) {
+                const uint32_t t = planes[pl][w] & cy;
+                planes[pl][w] ^= cy;
+                cy = t;
+              }
             }
             if (pooled) {
               s |= __shfl_xor_sync(0xFFFFFFFFu, s, 1);
@@ -726,6 +762,25 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
               }
             }
           }
+        }
+      }
+      if (NS >= 2) {  // carry-save counting of this group's NS spike words
+#pragma unroll
+        for (int w = 0; w < NWT; ++w) {
+          uint32_t sw[NSM];
+#pragma unroll
+          for (int j = 0; j < NSM; ++j) sw[j] = valid ? (~inv[j][w] & chmask) : 0u;
+          uint32_t P[kPlanes];
+#pragma unroll
+          for (int pl = 0; pl < kPlanes; ++pl) P[pl] = planes[pl][w];
+          if (NS == 2) {
+            planes_add3(P, sw[0] ^ sw[1], sw[0] & sw[1], 0u);
+          } else {
+#pragma unroll
+            for (int j = 0; j < NSM; j += 4) planes_add4(P, sw[j], sw[j + 1], sw[j + 2], sw[j + 3]);
+          }
+#pragma unroll
+          for (int pl = 0; pl < kPlanes; ++pl) planes[pl][w] = P[pl];
         }
       }
       steps_acc += nsteps;
