@@ -125,6 +125,27 @@ def useful_flops_per_sample(specs):
     return out
 
 
+def neuron_steps_per_sample(specs):
+    """LIF neuron-steps per sample of one forward: C_out * H' * W' * (LIF steps)."""
+    out = []
+    for s in specs:
+        hc, wc = s.conv_hw
+        steps = s.T // s.K if s.mode == "tac" else s.T
+        out.append(float(s.C_out * hc * wc * steps))
+    return out
+
+
+LIF_ALG_OPS = 3.0  # per neuron-step: V <- beta V + Y (one FMA), threshold compare, reset subtract
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
 def algorithmic_bytes_per_sample(specs):
     """Packed spike bytes in + out per sample of one forward (no v_final)."""
     out = []
@@ -219,15 +240,13 @@ def main():
 
     import torch
     import torch.distributed as dist
-    from paper_2603_13810_b200 import network, tacsnn
+    from paper_2603_13810_b200 import dist as D, network, tacsnn
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    assert B_global % world == 0, "global batch must divide across ranks"
-    B = B_global // world
-    b0 = rank * B
+    b0, B = D.shard_range(B_global, world, rank)
     specs = specs_fn(B)
     weights = configs.layer_weights(cfg)
     net = network.Network(specs, weights, device=dev)
@@ -237,17 +256,15 @@ def main():
     x_u8 = configs.make_inputs(cfg, B=B, b0=b0, device=dev)
     x = tacsnn.pack(x_u8)
     del x_u8
-    T_out, Ho, Wo, wpr = specs[-1].out_shape()
-    gather_spk = torch.empty((world,) + (T_out, B, Ho, wpr), dtype=torch.int32, device=dev) \
-        if world > 1 else None
-    gather_cnt = torch.empty((world, B, specs[-1].C_out), dtype=torch.int32, device=dev) \
-        if world > 1 else None
+    def gather(y, cnt):
+        """The path's only collective: final-layer packed spikes and counts."""
+        if world > 1:
+            D.gather_batch(y, dim=1)
+            D.gather_batch(cnt, dim=0)
 
     def step(xin):
         y, counts, _, _ = net.forward(xin)
-        if world > 1:
-            dist.all_gather_into_tensor(gather_spk.view(-1), y.contiguous().view(-1))
-            dist.all_gather_into_tensor(gather_cnt.view(-1), counts[-1].contiguous().view(-1))
+        gather(y, counts[-1])
         return y, counts
 
     launches_per_step = net.count_launches(x)
@@ -269,9 +286,7 @@ def main():
             ev[i][li][0].record(stream)
             xin, _, cnt = tacsnn.conv_lif(s, prep, xin)
             ev[i][li][1].record(stream)
-        if world > 1:
-            dist.all_gather_into_tensor(gather_spk.view(-1), xin.contiguous().view(-1))
-            dist.all_gather_into_tensor(gather_cnt.view(-1), cnt.contiguous().view(-1))
+        gather(xin, cnt)
         return xin
 
     clocks = ClockSampler(local)
@@ -336,27 +351,42 @@ def main():
     # ---------------- roofline of the dominant kernel (per-layer launch)
     peaks = load_peaks()
     flops = useful_flops_per_sample(specs)
+    nsteps_ps = neuron_steps_per_sample(specs)
     bytes_ = algorithmic_bytes_per_sample(specs)
+    long_run = a.steps * ms_per_step > 2000
+    tensor_peak = (peaks["bf16_sustained"] if long_run else peaks["bf16"]) * 2.0  # int8 = bf16 x 2
+    alu_peak = 148 * 128 * peaks["sm_max_mhz"] * 1e6 / 1e12  # T lane-ops/s
+    traffic = load_traffic()
+    layer_rows = []
+    for li in range(nL):
+        dur = layer_ms[li] / 1e3
+        t_ach = flops[li] * B / dur / 1e12
+        a_ach = LIF_ALG_OPS * nsteps_ps[li] * B / dur / 1e12
+        row = {"layer": li, "engine": engines[li], "ms": layer_ms[li],
+               "useful_tflops": t_ach,
+               "tensor_frac": t_ach / tensor_peak if engines[li] == "tcgen05" else None,
+               "tensor_issued_frac": 2.0 * t_ach / tensor_peak if engines[li] == "tcgen05" else None,
+               "lif_tops": a_ach, "alu_frac": a_ach / alu_peak,
+               "packed_gbs": bytes_[li] * B / dur / 1e9,
+               "frames_per_s": B * specs[li].T / dur}
+        layer_rows.append(row)
     dom = max(range(nL), key=lambda li: layer_ms[li])
-    dspec = specs[dom]
-    dur_s = layer_ms[dom] / 1e3
-    if engines[dom] == "tcgen05":
-        # int8 MMA (kind::i8): peak = measured bf16 x nominal int8:bf16 ratio (4.5/2.25)
-        peak = (peaks["bf16_sustained"] if a.steps * ms_per_step > 2000 else peaks["bf16"]) * 2.0
-        roof = {"bound": "tensor", "achieved": flops[dom] * B / dur_s / 1e12, "peak": peak,
-                "unit": "TFLOP/s"}
-        roof["peak_note"] = (f"int8 tcgen05 peak = {peaks['source']} bf16 x 2 (nominal "
-                             f"4.5/2.25); achieved counts useful conv FLOPs only")
+    dspec, drow = specs[dom], layer_rows[dom]
+    tkey = f"{cfg.name}/{specs[0].mode}/K{specs[0].K}/B{B}/layer{dom}"
+    if engines[dom] == "tcgen05" and (drow["tensor_frac"] or 0) >= drow["alu_frac"]:
+        roof = {"bound": "tensor", "achieved": drow["useful_tflops"], "peak": tensor_peak,
+                "unit": "TFLOP/s", "frac": drow["tensor_frac"],
+                "peak_note": f"int8 tcgen05 peak = {peaks['source']} bf16 x 2 (nominal 4.5/2.25); "
+                             f"achieved = useful conv FLOPs (2 int8 weight slices issue 2x)"}
     else:
-        # SIMT fp32 FFMA: 148 SMs x 128 lanes x 2 FLOP x sm clock
-        sm_mhz = (clk or {}).get("sm_mhz") or peaks["sm_max_mhz"]
-        peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
-        roof = {"bound": "alu", "achieved": flops[dom] * B / dur_s / 1e12, "peak": peak,
-                "unit": "TFLOP/s", "peak_note": "fp32 FFMA: 148 SM x 128 lanes x 2 x SM clock"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+        roof = {"bound": "alu", "achieved": drow["lif_tops"], "peak": alu_peak,
+                "unit": "Tops/s", "frac": drow["alu_frac"],
+                "peak_note": "148 SM x 128 lanes x SM clock (one 32-lane warp instr/cycle/SMSP); "
+                             f"achieved = {LIF_ALG_OPS:.0f} algorithmic LIF ops per neuron-step "
+                             "(FMA, compare, reset subtract)"}
+    roof["traffic"] = traffic.get(tkey)
     roof["kernel"] = f"layer {dom} ({dspec.C_in}->{dspec.C_out} @{dspec.H}x{dspec.W}, {engines[dom]})"
-    roof["hbm_achieved_gbs"] = bytes_[dom] * B / dur_s / 1e9
+    roof["hbm_achieved_gbs"] = drow["packed_gbs"]
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -367,7 +397,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None,
-            "dtype": "u8xi8->i32 (tcgen05) / f32 (LIF)" if "tcgen05" in engines else "f32",
+            "dtype": "u8 x i8 -> s32 (tcgen05 conv), f32 (LIF)" if "tcgen05" in engines else "f32",
             "data": "synthetic",
             "config": {"workload": cfg.name, "description": cfg.description,
                        "mode": specs[0].mode, "K": specs[0].K, "global_batch": B_global,
@@ -379,11 +409,7 @@ def main():
             "gpu_launches": launches_per_step * a.steps,
             "roofline": roof,
             "cpu_baseline": cpu,
-            "layers": [{"layer": li, "engine": engines[li], "ms": layer_ms[li],
-                        "useful_tflops": flops[li] * B / (layer_ms[li] / 1e3) / 1e12,
-                        "packed_gbs": bytes_[li] * B / (layer_ms[li] / 1e3) / 1e9,
-                        "frames_per_s": B * specs[li].T / (layer_ms[li] / 1e3)}
-                       for li in range(nL)],
+            "layers": layer_rows,
             "peaks": peaks,
         }
         print(json.dumps(line), flush=True)
