@@ -870,11 +870,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
 
   if (warp == 0) {
     // ================================ MMA issuer (CTA 0 of the pair) =========
-    if (rank == 0 && lane == 0) {
+    // The whole warp runs the loop converged (warp-uniform descriptors, no
+    // waterfall); one elected lane issues.  Descriptors are built once and only
+    // their 14-bit start-address field (addr >> 4, always < 2^14) is advanced.
+    if (rank == 0) {
       const uint32_t idesc = ptx::idesc_i8(256, p.n_total);
-      const uint32_t n_half_bytes = (uint32_t)p.Cout_pad * 16u;
-      const uint32_t w_base = sbase + p.off_w;
-      const int ntaps = p.ntaps, nkc2 = p.nkc >> 1;
+      const uint32_t nhb16 = (uint32_t)p.Cout_pad;                // n_half_bytes >> 4
+      const uint64_t a_desc0 = ptx::smem_desc(sbase + p.off_a, p.lbo_a, p.sbo_a);
+      const uint64_t b_desc0 = ptx::smem_desc(sbase + p.off_w, p.lbo_b, 128u);
+      const uint32_t lbo16 = p.lbo_a >> 4, stage16 = p.a_stage_bytes >> 4;
+      const int nkc = p.nkc, nkc2 = p.nkc >> 1;
       const uint32_t ns = (uint32_t)p.nstages;
       uint32_t it = 0;
       for (int pair = cid; pair < p.num_pairs; pair += ncl) {
@@ -884,20 +889,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
           ptx::mbar_wait(bar_t_empty + 8 * acc, aph ^ 1u);
           ptx::mbar_wait(bar_a_full + 8 * s, ph);
           ptx::tc_fence_after();
-          const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
+          const uint64_t a_base = a_desc0 + (uint64_t)(s * stage16);
           const uint32_t d_tmem = tmem_base + acc * p.n_total;
-          for (int tap = 0; tap < ntaps; ++tap) {
-            for (int kc2 = 0; kc2 < nkc2; ++kc2) {
-              const uint64_t ad = ptx::smem_desc(
-                  a_stage + (uint32_t)(2 * kc2) * p.lbo_a + (uint32_t)p.tap_off[tap] * 16u,
-                  p.lbo_a, p.sbo_a);
-              const uint64_t bd = ptx::smem_desc(
-                  w_base + (uint32_t)(tap * p.nkc + 2 * kc2) * n_half_bytes, p.lbo_b, 128u);
-              ptx::mma_i8_cg2(d_tmem, ad, bd, idesc, (tap | kc2) ? 1u : 0u);
+          if (ptx::elect_one()) {
+            if (PATH == PATH_HALO) {
+#pragma unroll
+              for (int tap = 0; tap < 9; ++tap) {
+                const uint32_t toff = (uint32_t)((tap / 3) * kHaloW + (tap % 3));  // 16-B rows
+                for (int kc2 = 0; kc2 < nkc2; ++kc2) {
+                  const uint64_t ad = a_base + (uint64_t)(2u * kc2 * lbo16 + toff);
+                  const uint64_t bd = b_desc0 + (uint64_t)((tap * nkc + 2 * kc2) * nhb16);
+                  ptx::mma_i8_cg2(d_tmem, ad, bd, idesc, (tap | kc2) ? 1u : 0u);
+                }
+              }
+            } else {
+              ptx::mma_i8_cg2(d_tmem, a_base, b_desc0, idesc, 0u);
             }
+            ptx::mma_commit_cg2_multicast(bar_a_empty + 8 * s);
+            ptx::mma_commit_cg2_multicast(bar_t_full + 8 * acc);
           }
-          ptx::mma_commit_cg2_multicast(bar_a_empty + 8 * s);
-          ptx::mma_commit_cg2_multicast(bar_t_full + 8 * acc);
+          __syncwarp();
         }
       }
     }
