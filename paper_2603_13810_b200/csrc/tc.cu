@@ -22,7 +22,11 @@
 // at halo pixel (g + r, c + s) for tap (r, s): the 8 rows of a core matrix are
 // 16 B apart and core-matrix groups (tile rows) SBO = 160 B apart, so a tap is
 // a start-address offset of (10 r + s) * 16 B -- no im2col copies, no junk rows.
-// Layers with C_in <= 2 (first layers) use an explicit 32-byte im2col row.
+// Layers with C_in <= 2 (first layers) use an explicit im2col row in fp16 and
+// kind::f16 MMAs: the u8 aggregate (exact in fp16), the two fp16 slices of the
+// weights (hi + lo, |error| <= 2^-22 |w|) accumulated into ONE fp32 accumulator
+// by two MMAs, and the bias as a constant-1 A column -- so the epilogue reads Y
+// straight from TMEM (no combine).
 // TMEM lane i = tile pixel (g, c): epilogue warp q holds tile rows 4q..4q+3, so
 // every 2x2 pooling window lies inside one warp (lanes l, l^1, l^8, l^9) and
 // spikes are OR-pooled with two shuffles and stored straight from registers.
@@ -37,6 +41,7 @@
 // Pipelines: A stages (2-3) producer -> MMA, TMEM accumulators (2) MMA -> epilogue.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -136,10 +141,10 @@ Geometry geometry(const tac_conv_lif_desc *d, bool use_tma = false) {
     const int nwin = d->C_in / 32;
     g.raw_bw = nwin == 4 ? kHaloW * 4 : (int)align_up(kHaloW * nwin + 3, 4);
   } else {
-    g.nkc = 2;
+    g.nkc = 4;                              // 32 fp16 = 64 B = four 16-B K chunks
     g.ntaps = 1;
-    g.w_bytes_cta = 32u * g.cout_pad;
-    g.a_stage_bytes = 128u * 32u;
+    g.w_bytes_cta = 64u * g.cout_pad;       // [hi/lo][4 chunks][C_out_pad/2 rows][16 B]
+    g.a_stage_bytes = 128u * 64u;
     g.raw_bw = 8;  // 16-B aligned start word + the <= 2 words holding the window bits
   }
   g.raw_box_bytes = (uint32_t)K * kHaloH * g.raw_bw * 4u;
@@ -297,9 +302,21 @@ __device__ __forceinline__ void produce_im2col(const TcParams &p, int tile, int 
         for (int q = 0; q < 6; ++q) o[q] |= ((z >> q) & 0x00010101u) << e;
       }
     }
-    const uint32_t dst = a_stage + (uint32_t)pos * 16u;
-    ptx::st_shared_v4(dst, o[0], o[1], o[2], o[3]);
-    ptx::st_shared_v4(dst + p.lbo_a, o[4], o[5], o[6], o[7]);
+    // fp16 row: slot 4q + r <- byte r of word q (the u8 aggregate), slot 3 = 1.0
+    // (the bias column), slots 24..31 = 0
+    uint32_t h[16];
+    #pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t b0 = o[q] & 0xFFu, b1 = (o[q] >> 8) & 0xFFu, b2 = (o[q] >> 16) & 0xFFu;
+      const uint32_t b3 = q == 0 ? 0x3C00u : 0u;  // fp16 1.0
+      h[2 * q] = (uint32_t)__half_as_ushort(__uint2half_rn(b0)) |
+                 ((uint32_t)__half_as_ushort(__uint2half_rn(b1)) << 16);
+      h[2 * q + 1] = (uint32_t)__half_as_ushort(__uint2half_rn(b2)) | (b3 << 16);
+    }
+    #pragma unroll
+    for (int ck = 0; ck < 4; ++ck)
+      ptx::st_shared_v4(a_stage + (uint32_t)ck * p.lbo_a + (uint32_t)pos * 16u, h[4 * ck],
+                        h[4 * ck + 1], h[4 * ck + 2], h[4 * ck + 3]);
   }
 }
 
@@ -361,9 +378,21 @@ __device__ __forceinline__ void produce_im2col_tma(const TcParams &p, const uint
 #pragma unroll
       for (int q = 0; q < 6; ++q) o[q] |= ((z >> q) & 0x00010101u) << e;
     }
-    const uint32_t dst = a_stage + (uint32_t)pos * 16u;
-    ptx::st_shared_v4(dst, o[0], o[1], o[2], o[3]);
-    ptx::st_shared_v4(dst + p.lbo_a, o[4], o[5], o[6], o[7]);
+    // fp16 row: slot 4q + r <- byte r of word q (the u8 aggregate), slot 3 = 1.0
+    // (the bias column), slots 24..31 = 0
+    uint32_t h[16];
+    #pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t b0 = o[q] & 0xFFu, b1 = (o[q] >> 8) & 0xFFu, b2 = (o[q] >> 16) & 0xFFu;
+      const uint32_t b3 = q == 0 ? 0x3C00u : 0u;  // fp16 1.0
+      h[2 * q] = (uint32_t)__half_as_ushort(__uint2half_rn(b0)) |
+                 ((uint32_t)__half_as_ushort(__uint2half_rn(b1)) << 16);
+      h[2 * q + 1] = (uint32_t)__half_as_ushort(__uint2half_rn(b2)) | (b3 << 16);
+    }
+    #pragma unroll
+    for (int ck = 0; ck < 4; ++ck)
+      ptx::st_shared_v4(a_stage + (uint32_t)ck * p.lbo_a + (uint32_t)pos * 16u, h[4 * ck],
+                        h[4 * ck + 1], h[4 * ck + 2], h[4 * ck + 3]);
   }
 }
 
@@ -602,7 +631,7 @@ __device__ __forceinline__ void planes_add4(uint32_t *P, uint32_t s0, uint32_t s
 
 // NS > 0: subtract reset with NS LIF steps per group (specialised hot path);
 // NS == 0: any reset, runtime step count.
-template <int NCH, int NPART, int NS>
+template <int NCH, int PATH, int NPART, int NS>
 __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, uint32_t tmem_base,
                                               uint32_t bar_t_full, uint32_t bar_t_empty, int cid,
                                               int ncl, uint32_t rank, uint32_t warp,
@@ -672,20 +701,26 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
 #pragma unroll
         for (int w = 0; w < NWT; ++w) inv[j][w] = 0u;
       const uint32_t tcol = tmem_base + lane_addr + acc * p.n_total + (uint32_t)co_base;
-      constexpr int NBUF = NPART == 2 ? 2 : 1;  // TMEM prefetch depth (registers)
+      constexpr bool F16 = PATH == PATH_IM2COL;  // fp32 Y straight from TMEM
+      constexpr int NBUF = (NPART == 2 || F16) ? 2 : 1;  // TMEM prefetch depth (registers)
       uint32_t d[NBUF][2][8];                    // [buffer][hi/lo][col]
       ptx::tmem_ld8(tcol, d[0][0]);
-      ptx::tmem_ld8(tcol + Cp, d[0][1]);
+      if (!F16) ptx::tmem_ld8(tcol + Cp, d[0][1]);
       ptx::tmem_wait_ld_dep(d[0][0], d[0][1]);
 #pragma unroll
       for (int ch = 0; ch < NCH / 8; ++ch) {
         const int cur = NBUF == 2 ? (ch & 1) : 0, nxt = NBUF == 2 ? (cur ^ 1) : 0;
         if (NBUF == 2 && ch + 1 < NCH / 8) {  // prefetch the next 8 columns
           ptx::tmem_ld8(tcol + (ch + 1) * 8, d[nxt][0]);
-          ptx::tmem_ld8(tcol + Cp + (ch + 1) * 8, d[nxt][1]);
+          if (!F16) ptx::tmem_ld8(tcol + Cp + (ch + 1) * 8, d[nxt][1]);
         }
         float yv[8];
-        combine8(p, sc, co_base + ch * 8, d[cur][0], d[cur][1], yv);
+        if (F16) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) yv[i] = __uint_as_float(d[cur][0][i]);
+        } else {
+          combine8(p, sc, co_base + ch * 8, d[cur][0], d[cur][1], yv);
+        }
         if (NS > 0) {
           constexpr int NSP = (NS > 0) ? NS : 1;
           const int w = (ch * 8) / 32;
@@ -721,7 +756,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
         if (ch + 1 < NCH / 8) {
           if (NBUF == 1) {
             ptx::tmem_ld8(tcol + (ch + 1) * 8, d[0][0]);
-            ptx::tmem_ld8(tcol + Cp + (ch + 1) * 8, d[0][1]);
+            if (!F16) ptx::tmem_ld8(tcol + Cp + (ch + 1) * 8, d[0][1]);
           }
           ptx::tmem_wait_ld_dep(d[nxt][0], d[nxt][1]);
         }
@@ -875,7 +910,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
     // their 14-bit start-address field (addr >> 4, always < 2^14) is advanced.
     if (rank == 0) {
       const uint32_t idesc = ptx::idesc_i8(256, p.n_total);
-      const uint32_t nhb16 = (uint32_t)p.Cout_pad;                // n_half_bytes >> 4
+      const uint32_t nhb16 = p.lbo_b >> 4;                        // B rows of this CTA x 16 B
       const uint64_t a_desc0 = ptx::smem_desc(sbase + p.off_a, p.lbo_a, p.sbo_a);
       const uint64_t b_desc0 = ptx::smem_desc(sbase + p.off_w, p.lbo_b, 128u);
       const uint32_t lbo16 = p.lbo_a >> 4, stage16 = p.a_stage_bytes >> 4;
@@ -903,7 +938,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
                 }
               }
             } else {
-              ptx::mma_i8_cg2(d_tmem, a_base, b_desc0, idesc, 0u);
+              // D = A W_hi + A W_lo (+ bias via the constant column): 2 slices x 2 K=16 steps
+              const uint32_t idf = ptx::idesc_f16(256, p.n_total);
+#pragma unroll
+              for (int sl = 0; sl < 2; ++sl)
+#pragma unroll
+                for (int kc2 = 0; kc2 < 2; ++kc2)
+                  ptx::mma_f16_cg2(d_tmem, a_base + (uint64_t)(2u * kc2 * lbo16),
+                                   b_desc0 + (uint64_t)((sl * 4 + 2 * kc2) * nhb16), idf,
+                                   (sl | kc2) ? 1u : 0u);
             }
             ptx::mma_commit_cg2_multicast(bar_a_empty + 8 * s);
             ptx::mma_commit_cg2_multicast(bar_t_full + 8 * acc);
@@ -934,11 +977,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
     // ================================ epilogue =================================
     const int ns = p.reset == 0 ? p.nsteps : 0;
     switch (ns) {
-      case 1: epilogue_role<NCH, NPART, 1>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      case 2: epilogue_role<NCH, NPART, 2>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      case 4: epilogue_role<NCH, NPART, 4>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      case 8: epilogue_role<NCH, NPART, 8>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      default: epilogue_role<NCH, NPART, 0>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 1: epilogue_role<NCH, PATH, NPART, 1>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 2: epilogue_role<NCH, PATH, NPART, 2>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 4: epilogue_role<NCH, PATH, NPART, 4>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 8: epilogue_role<NCH, PATH, NPART, 8>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      default: epilogue_role<NCH, PATH, NPART, 0>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
     }
   }
 
@@ -992,7 +1035,7 @@ size_t tc_weights_bytes(const tac_conv_lif_desc *d) {
 
 // Two int8 slices per output channel, laid out as the smem image of each CTA:
 // halo  : [tap][kc16][n][16 B], K index 32w + 4o + b <-> channel 32w + o + 8b
-// im2col: [kc16 (2)][n][16 B],  K index 4o + r       <-> (r, s = o / C_in, c = o % C_in)
+// im2col: fp16 hi/lo slices, see below (K index 4o + r <-> (r, s = o / C_in, c = o % C_in))
 // followed by fp32 [s1/254 | bias | s1 | s2] per padded output channel.
 void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bias,
                 unsigned char *dst) {
@@ -1035,13 +1078,30 @@ void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bi
                 (unsigned char)(n < Co ? q_at(half, n, ci, tap / 3, tap % 3) : 0);
         }
     } else {
-      for (int kidx = 0; kidx < 32; ++kidx) {
-        const int o = kidx / 4, r = kidx % 4;
-        if (r >= 3 || o >= 3 * Ci) continue;
-        const int s = o / Ci, c = o % Ci;
-        const int kc = kidx / 16, byte = kidx % 16;
-        for (int n = 0; n < Co; ++n)
-          img[((size_t)kc * Cp + n) * 16 + byte] = (unsigned char)q_at(half, n, c, r, s);
+      // fp16 image, CTA `half` holds output channels [half*Cp/2, (half+1)*Cp/2) of BOTH
+      // slices: [slice][16-B chunk (4)][row (Cp/2)][8 fp16].  K index k = 4o + r holds
+      // W[n][c][r][s] (o = s*C_in + c), k = 3 the bias; the aggregate scale
+      // 2^{-m(K-1)} (exact) is folded into the weights, not the bias.
+      const int m = d->mode == TAC_MODE_DENSE ? 0 : beta_shift(d->beta);
+      const int Kg = d->mode == TAC_MODE_DENSE ? 1 : d->K;
+      const double agg = std::ldexp(1.0, -m * (Kg - 1));
+      const int nh = Cp / 2;
+      uint16_t *img16 = reinterpret_cast<uint16_t *>(img);
+      for (int nl = 0; nl < nh; ++nl) {
+        const int n = half * nh + nl;
+        for (int kidx = 0; kidx < 32; ++kidx) {
+          const int o = kidx / 4, r = kidx % 4;
+          double wv = 0.0;
+          if (n < Co) {
+            if (kidx == 3) wv = bias ? (double)bias[n] : 0.0;
+            else if (r < 3 && o < 3 * Ci) wv = (double)weight[(((size_t)n * Ci + o % Ci) * 3 + r) * 3 + o / Ci] * agg;
+          }
+          const __half hi = __double2half(wv);
+          const __half lo = __double2half(wv - (double)__half2float(hi));
+          const int ck = kidx / 8, e = kidx % 8;
+          img16[((size_t)(0 * 4 + ck) * nh + nl) * 8 + e] = __half_as_ushort(hi);
+          img16[((size_t)(1 * 4 + ck) * nh + nl) * 8 + e] = __half_as_ushort(lo);
+        }
       }
     }
   }
@@ -1125,7 +1185,7 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   p.off_w = g.off_w; p.off_a = g.off_a; p.a_stage_bytes = g.a_stage_bytes;
   p.off_scale = g.off_scale; p.off_bar = g.off_bar;
   p.smem_bytes = g.smem_bytes; p.w_bytes_cta = g.w_bytes_cta;
-  p.n_total = 2u * g.cout_pad;
+  p.n_total = g.path == PATH_HALO ? 2u * g.cout_pad : (uint32_t)g.cout_pad;  // TMEM columns / acc
   uint32_t cols = 32;
   while (cols < 2u * p.n_total) cols <<= 1;
   p.tmem_cols = cols;
@@ -1138,7 +1198,8 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
     p.sbo_a = 128u;
     for (int t = 0; t < 9; ++t) p.tap_off[t] = 0;
   }
-  p.lbo_b = (uint32_t)g.cout_pad * 16u;
+  // B: rows held by one CTA x 16 B between 16-byte K chunks
+  p.lbo_b = g.path == PATH_HALO ? (uint32_t)g.cout_pad * 16u : (uint32_t)(g.cout_pad / 2) * 16u;
   p.in = lp.in; p.out = lp.out; p.v_init = lp.v_init; p.v_final = lp.v_final; p.counts = lp.counts;
   p.w_img = tc_prep;
   p.scale_bias = reinterpret_cast<const float *>(tc_prep + 2 * (size_t)g.w_bytes_cta);
