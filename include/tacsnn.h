@@ -166,6 +166,12 @@ int32_t tac_abi_version(void);           /* TACSNN_ABI_VERSION */
  * tac_conv_lif_forward / tac_pack_spikes / tac_unpack_spikes call. */
 int32_t tac_last_launch_count(void);
 
+/* Diagnostics (not needed for computation): route a per-group role timeline of
+ * CTA 0 of every tcgen05 launch into `dev_buffer` (device, >= 4096 x 8 u64,
+ * %globaltimer ns; slots: producer start/done, MMA ready/issued, epilogue
+ * full/released/done), or stop with NULL.  Process-global; not thread-safe. */
+void tac_debug_set_trace(void *dev_buffer);
+
 #ifdef __cplusplus
 }
 #endif

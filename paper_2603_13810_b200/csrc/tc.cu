@@ -92,7 +92,19 @@ struct TcParams {
   uint32_t *counts;
   const unsigned char *w_img;
   const float *scale_bias;
+  unsigned long long *trace;  // optional: per-(group) role timestamps of CTA 0 (debug)
 };
+
+// trace slots per group iteration (CTA 0 only; TACSNN_TRACE env var)
+enum { TR_PROD_START = 0, TR_PROD_DONE, TR_MMA_READY, TR_MMA_ISSUED, TR_EPI_FULL, TR_EPI_RELEASED,
+       TR_EPI_DONE, TR_SLOTS = 8 };
+__device__ __forceinline__ void trace_mark(const TcParams &p, uint32_t it, int slot) {
+  if (p.trace && blockIdx.x == 0 && it < 4096) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[it * TR_SLOTS + slot] = t;
+  }
+}
 
 // ------------------------------------------------------------ host helpers --
 int beta_shift(float beta) {  // m with beta == 2^-m exactly, else 0
@@ -432,6 +444,7 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
       const uint32_t r = it % nr, rph = (it / nr) & 1u;
       ptx::mbar_wait(bar_raw + 8 * r, rph);
       ptx::mbar_wait(bar_a_empty + 8 * s, ph ^ 1u);
+      if (ptid == 0) trace_mark(p, it, TR_PROD_START);
       const uint32_t *raw = reinterpret_cast<const uint32_t *>(smem + p.off_raw + r * p.raw_stage_bytes);
       const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
       if (PATH == PATH_HALO)
@@ -442,6 +455,7 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_cluster(bar_a_full + 8 * s, 0);
       ptx::named_bar_sync(2, kProdWarps * 32);  // every producer is done with raw stage r
+      if (ptid == 0) trace_mark(p, it, TR_PROD_DONE);
       if (ptid == 0 && ipair < p.num_pairs) issue(r);
     }
   }
@@ -695,6 +709,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
       const uint32_t acc = it % kAccs, aph = (it / kAccs) & 1u;
       ptx::mbar_wait(bar_t_full + 8 * acc, aph);
       ptx::tc_fence_after();
+      if (e == 0 && lane == 0) trace_mark(p, it, TR_EPI_FULL);
       uint32_t inv[NSM][NWT];
 #pragma unroll
       for (int j = 0; j < NSM; ++j)
@@ -765,6 +780,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_cluster_relaxed(bar_t_empty + 8 * acc, 0);
+      if (e == 0 && lane == 0) trace_mark(p, it, TR_EPI_RELEASED);
 
       // spikes: bit-sliced counters, in-warp 2x2 OR-pool, direct packed stores
 #pragma unroll
@@ -823,6 +839,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
         if (tok) flush_counts<NWT>(p, planes, b, co_base, NCH, lane);
         steps_acc = 0;
       }
+      if (e == 0 && lane == 0) trace_mark(p, it, TR_EPI_DONE);
     }
     if (p.v_final && valid) {
 #pragma unroll
@@ -924,6 +941,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
           ptx::mbar_wait(bar_t_empty + 8 * acc, aph ^ 1u);
           ptx::mbar_wait(bar_a_full + 8 * s, ph);
           ptx::tc_fence_after();
+          if (lane == 0) trace_mark(p, it, TR_MMA_READY);
           const uint64_t a_base = a_desc0 + (uint64_t)(s * stage16);
           const uint32_t d_tmem = tmem_base + acc * p.n_total;
           if (ptx::elect_one()) {
@@ -952,6 +970,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
             ptx::mma_commit_cg2_multicast(bar_t_full + 8 * acc);
           }
           __syncwarp();
+          if (lane == 0) trace_mark(p, it, TR_MMA_ISSUED);
         }
       }
     }
@@ -1131,6 +1150,15 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 }  // namespace
 
+// Debug timeline (not part of the ABI contract): when tac_debug_set_trace() was
+// given a device buffer of >= 4096 * 8 u64, CTA 0 of every tcgen05 launch records
+// %globaltimer per group iteration and role event (see TR_* slots).
+static unsigned long long *g_trace = nullptr;
+unsigned long long *tacsnn_trace_buffer() { return g_trace; }
+extern "C" void tac_debug_set_trace(void *dev) {
+  g_trace = reinterpret_cast<unsigned long long *>(dev);
+}
+
 int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned char *tc_prep,
               void *stream, int *launches) {
   // TMA raw-halo producer when the packed input is a legal 4-D tensor-map view
@@ -1201,6 +1229,7 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   // B: rows held by one CTA x 16 B between 16-byte K chunks
   p.lbo_b = g.path == PATH_HALO ? (uint32_t)g.cout_pad * 16u : (uint32_t)(g.cout_pad / 2) * 16u;
   p.in = lp.in; p.out = lp.out; p.v_init = lp.v_init; p.v_final = lp.v_final; p.counts = lp.counts;
+  p.trace = tacsnn_trace_buffer();
   p.w_img = tc_prep;
   p.scale_bias = reinterpret_cast<const float *>(tc_prep + 2 * (size_t)g.w_bytes_cta);
 

@@ -25,7 +25,8 @@ ENGINE_NAMES = {v: k for k, v in ENGINES.items()}
 EXPORTS = ("tac_desc_check", "tac_out_shape", "tac_select_engine", "tac_weights_bytes",
            "tac_prepare_weights", "tac_workspace_bytes", "tac_conv_lif_forward",
            "tac_pack_spikes", "tac_unpack_spikes", "tac_status_string",
-           "tac_last_error_detail", "tac_abi_version", "tac_last_launch_count")
+           "tac_last_error_detail", "tac_abi_version", "tac_last_launch_count",
+           "tac_debug_set_trace")
 
 
 class Desc(ctypes.Structure):
@@ -67,6 +68,7 @@ def lib():
                 "tac_last_error_detail": ([], ctypes.c_char_p),
                 "tac_abi_version": ([], i32),
                 "tac_last_launch_count": ([], i32),
+                "tac_debug_set_trace": ([P], None),
             }
             for name, (args, res) in sig.items():
                 f = getattr(L, name)
