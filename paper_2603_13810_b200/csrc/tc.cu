@@ -57,7 +57,10 @@ namespace tacsnn {
 namespace {
 
 constexpr int kProdWarps = 3;
-// epilogue: NPART channel parts x 4 TMEM lane quadrants warps
+// Warp layout: epilogue warps first (NPART channel parts x 4 TMEM lane quadrants),
+// then the MMA warp, then the producer warps.  The SM warp schedulers favour
+// higher warp ids, so the warps feeding the tensor pipe (MMA, producers) win
+// issue slots over the 16 compute-heavy epilogue warps.
 constexpr int epi_warps(int npart) { return 4 * npart; }
 constexpr int kernel_threads(int npart) { return 32 * (1 + kProdWarps + epi_warps(npart)); }
 constexpr int kMaxStages = 3;
@@ -131,7 +134,7 @@ struct Geometry {
   uint32_t w_bytes_cta, a_stage_bytes, raw_stage_bytes, raw_box_bytes, off_w, off_a, off_raw,
       off_scale, off_bar, smem_bytes;
 };
-constexpr int kMaxRaw = 2;
+constexpr int kMaxRaw = 4;
 constexpr int kNumBars = 2 * kMaxStages + 2 * kAccs + 1 + kMaxRaw;
 
 uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
@@ -161,8 +164,8 @@ Geometry geometry(const tac_conv_lif_desc *d, bool use_tma = false) {
   }
   g.raw_box_bytes = (uint32_t)K * kHaloH * g.raw_bw * 4u;
   g.raw_stage_bytes = align_up(g.raw_box_bytes, 128);
-  const int combos[4][2] = {{3, 2}, {2, 2}, {3, 1}, {2, 1}};
-  for (int ci = 0; ci < (use_tma ? 4 : 2); ++ci) {
+  const int combos[6][2] = {{3, 4}, {3, 3}, {3, 2}, {2, 2}, {3, 1}, {2, 1}};
+  for (int ci = 0; ci < (use_tma ? 6 : 2); ++ci) {
     g.nstages = use_tma ? combos[ci][0] : (ci == 0 ? 3 : 2);
     g.nraw = use_tma ? combos[ci][1] : 0;
     g.off_w = 0;
@@ -414,8 +417,8 @@ template <int PATH, int K>
 __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sbase,
                                                   const uint8_t *smem, uint32_t bar_a_full,
                                                   uint32_t bar_a_empty, uint32_t bar_raw, int cid,
-                                                  int ncl, uint32_t rank, uint32_t lane) {
-  const int ptid = (int)threadIdx.x - 32;
+                                                  int ncl, uint32_t rank, uint32_t lane,
+                                                  int ptid) {
   const uint32_t ns = (uint32_t)p.nstages, nr = (uint32_t)p.nraw;
   int ipair = cid, ik = 0;  // next (pair, group) whose raw halo is to be loaded
   auto issue = [&](uint32_t slot) {
@@ -464,8 +467,7 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
 template <int PATH, int K>
 __device__ __forceinline__ void producer_role(const TcParams &p, uint32_t sbase,
                                               uint32_t bar_a_full, uint32_t bar_a_empty, int cid,
-                                              int ncl, uint32_t rank, uint32_t lane) {
-  const int ptid = (int)threadIdx.x - 32;
+                                              int ncl, uint32_t rank, uint32_t lane, int ptid) {
   const uint32_t ns = (uint32_t)p.nstages;
   uint32_t it = 0;
   for (int pair = cid; pair < p.num_pairs; pair += ncl) {
@@ -653,7 +655,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
   constexpr int NWT = NCH >= 32 ? NCH / 32 : 1;  // spike words per epilogue thread
   constexpr int NSM = NS ? NS : kMaxSteps;
   const float *sc = reinterpret_cast<const float *>(smem + p.off_scale);
-  const int e = (int)warp - 1 - kProdWarps;  // 0 .. 4 NPART - 1
+  const int e = (int)warp;                   // epilogue warps are 0 .. 4 NPART - 1
   const int quad = (int)(warp & 3);           // TMEM lane quadrant of this warp
   const int half = e >> 2;                    // channel part
   const int g = quad * 4 + (int)(lane >> 3);  // tile row of this lane's pixel
@@ -906,93 +908,93 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
   const int ncl = (int)ptx::nclusters_x();
   const int cid = (int)ptx::cluster_id_x();
 
-  // register rebalance (8 epilogue warps): the MMA + producer warpgroup gives
-  // registers to the epilogue.  The sum must not exceed what the launch
-  // allocated (384 x 168), or the increase blocks forever.
-  {
-    constexpr uint32_t kLaunchRegs = NPART == 2 ? 168 : 96;  // ptxas allocation at launch
-    constexpr uint32_t kRegsLow = NPART == 2 ? 96 : 64, kRegsHigh = NPART == 2 ? 200 : 104;
-    static_assert(128 * kRegsLow + 32 * epi_warps(NPART) * kRegsHigh <=
-                      kernel_threads(NPART) * kLaunchRegs, "register budget");
-    if (warp < 4)
-      ptx::setmaxnreg_dec<kRegsLow>();
-    else
-      ptx::setmaxnreg_inc<kRegsHigh>();
-  }
-
-  if (warp == 0) {
-    // ================================ MMA issuer (CTA 0 of the pair) =========
-    // The whole warp runs the loop converged (warp-uniform descriptors, no
-    // waterfall); one elected lane issues.  Descriptors are built once and only
-    // their 14-bit start-address field (addr >> 4, always < 2^14) is advanced.
-    if (rank == 0) {
-      const uint32_t idesc = ptx::idesc_i8(256, p.n_total);
-      const uint32_t nhb16 = p.lbo_b >> 4;                        // B rows of this CTA x 16 B
-      const uint64_t a_desc0 = ptx::smem_desc(sbase + p.off_a, p.lbo_a, p.sbo_a);
-      const uint64_t b_desc0 = ptx::smem_desc(sbase + p.off_w, p.lbo_b, 128u);
-      const uint32_t lbo16 = p.lbo_a >> 4, stage16 = p.a_stage_bytes >> 4;
-      const int nkc = p.nkc, nkc2 = p.nkc >> 1;
-      const uint32_t ns = (uint32_t)p.nstages;
-      uint32_t it = 0;
-      for (int pair = cid; pair < p.num_pairs; pair += ncl) {
-        for (int k = 0; k < p.G; ++k, ++it) {
-          const uint32_t s = it % ns, ph = (it / ns) & 1u;
-          const uint32_t acc = it % kAccs, aph = (it / kAccs) & 1u;
-          ptx::mbar_wait(bar_t_empty + 8 * acc, aph ^ 1u);
-          ptx::mbar_wait(bar_a_full + 8 * s, ph);
-          ptx::tc_fence_after();
-          if (lane == 0) trace_mark(p, it, TR_MMA_READY);
-          const uint64_t a_base = a_desc0 + (uint64_t)(s * stage16);
-          const uint32_t d_tmem = tmem_base + acc * p.n_total;
-          if (ptx::elect_one()) {
-            if (PATH == PATH_HALO) {
-#pragma unroll
-              for (int tap = 0; tap < 9; ++tap) {
-                const uint32_t toff = (uint32_t)((tap / 3) * kHaloW + (tap % 3));  // 16-B rows
-                for (int kc2 = 0; kc2 < nkc2; ++kc2) {
-                  const uint64_t ad = a_base + (uint64_t)(2u * kc2 * lbo16 + toff);
-                  const uint64_t bd = b_desc0 + (uint64_t)((tap * nkc + 2 * kc2) * nhb16);
-                  ptx::mma_i8_cg2(d_tmem, ad, bd, idesc, (tap | kc2) ? 1u : 0u);
+  // Register rebalance: the MMA + producer warpgroup gives registers to the
+  // epilogue warpgroups.  The sum must not exceed what the launch allocated
+  // (threads x kLaunchRegs), or the increase blocks forever.  Each setmaxnreg
+  // sits at the top of its role branch so ptxas sees the register regions.
+  constexpr uint32_t kLaunchRegs = NPART == 2 ? 168 : 96;  // ptxas allocation at launch
+  constexpr uint32_t kRegsLow = NPART == 2 ? 96 : 64, kRegsHigh = NPART == 2 ? 200 : 104;
+  static_assert(128 * kRegsLow + 32 * epi_warps(NPART) * kRegsHigh <=
+                    kernel_threads(NPART) * kLaunchRegs, "register budget");
+  const uint32_t kMmaWarp = (uint32_t)kEpiWarps;
+  if (warp >= kMmaWarp) {
+    ptx::setmaxnreg_dec<kRegsLow>();
+    if (warp == kMmaWarp) {
+      // ================================ MMA issuer (CTA 0 of the pair) =========
+      // The whole warp runs the loop converged (warp-uniform descriptors, no
+      // waterfall); one elected lane issues.  Descriptors are built once and only
+      // their 14-bit start-address field (addr >> 4, always < 2^14) is advanced.
+      if (rank == 0) {
+        const uint32_t idesc = ptx::idesc_i8(256, p.n_total);
+        const uint32_t nhb16 = p.lbo_b >> 4;                        // B rows of this CTA x 16 B
+        const uint64_t a_desc0 = ptx::smem_desc(sbase + p.off_a, p.lbo_a, p.sbo_a);
+        const uint64_t b_desc0 = ptx::smem_desc(sbase + p.off_w, p.lbo_b, 128u);
+        const uint32_t lbo16 = p.lbo_a >> 4, stage16 = p.a_stage_bytes >> 4;
+        const int nkc = p.nkc, nkc2 = p.nkc >> 1;
+        const uint32_t ns = (uint32_t)p.nstages;
+        uint32_t it = 0;
+        for (int pair = cid; pair < p.num_pairs; pair += ncl) {
+          for (int k = 0; k < p.G; ++k, ++it) {
+            const uint32_t s = it % ns, ph = (it / ns) & 1u;
+            const uint32_t acc = it % kAccs, aph = (it / kAccs) & 1u;
+            ptx::mbar_wait(bar_t_empty + 8 * acc, aph ^ 1u);
+            ptx::mbar_wait(bar_a_full + 8 * s, ph);
+            ptx::tc_fence_after();
+            if (lane == 0) trace_mark(p, it, TR_MMA_READY);
+            const uint64_t a_base = a_desc0 + (uint64_t)(s * stage16);
+            const uint32_t d_tmem = tmem_base + acc * p.n_total;
+            if (ptx::elect_one()) {
+              if (PATH == PATH_HALO) {
+  #pragma unroll
+                for (int tap = 0; tap < 9; ++tap) {
+                  const uint32_t toff = (uint32_t)((tap / 3) * kHaloW + (tap % 3));  // 16-B rows
+                  for (int kc2 = 0; kc2 < nkc2; ++kc2) {
+                    const uint64_t ad = a_base + (uint64_t)(2u * kc2 * lbo16 + toff);
+                    const uint64_t bd = b_desc0 + (uint64_t)((tap * nkc + 2 * kc2) * nhb16);
+                    ptx::mma_i8_cg2(d_tmem, ad, bd, idesc, (tap | kc2) ? 1u : 0u);
+                  }
                 }
+              } else {
+                // D = A W_hi + A W_lo (+ bias via the constant column): 2 slices x 2 K=16 steps
+                const uint32_t idf = ptx::idesc_f16(256, p.n_total);
+  #pragma unroll
+                for (int sl = 0; sl < 2; ++sl)
+  #pragma unroll
+                  for (int kc2 = 0; kc2 < 2; ++kc2)
+                    ptx::mma_f16_cg2(d_tmem, a_base + (uint64_t)(2u * kc2 * lbo16),
+                                     b_desc0 + (uint64_t)((sl * 4 + 2 * kc2) * nhb16), idf,
+                                     (sl | kc2) ? 1u : 0u);
               }
-            } else {
-              // D = A W_hi + A W_lo (+ bias via the constant column): 2 slices x 2 K=16 steps
-              const uint32_t idf = ptx::idesc_f16(256, p.n_total);
-#pragma unroll
-              for (int sl = 0; sl < 2; ++sl)
-#pragma unroll
-                for (int kc2 = 0; kc2 < 2; ++kc2)
-                  ptx::mma_f16_cg2(d_tmem, a_base + (uint64_t)(2u * kc2 * lbo16),
-                                   b_desc0 + (uint64_t)((sl * 4 + 2 * kc2) * nhb16), idf,
-                                   (sl | kc2) ? 1u : 0u);
+              ptx::mma_commit_cg2_multicast(bar_a_empty + 8 * s);
+              ptx::mma_commit_cg2_multicast(bar_t_full + 8 * acc);
             }
-            ptx::mma_commit_cg2_multicast(bar_a_empty + 8 * s);
-            ptx::mma_commit_cg2_multicast(bar_t_full + 8 * acc);
+            __syncwarp();
+            if (lane == 0) trace_mark(p, it, TR_MMA_ISSUED);
           }
-          __syncwarp();
-          if (lane == 0) trace_mark(p, it, TR_MMA_ISSUED);
+        }
+      }
+      __syncwarp();
+    } else {
+      // ================================ producers ================================
+      const int ptid = (int)(threadIdx.x - 32 * (kMmaWarp + 1));
+      if (p.use_tma) {
+        switch (p.K) {
+          case 1: producer_role_tma<PATH, 1>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, cid, ncl, rank, lane, ptid); break;
+          case 2: producer_role_tma<PATH, 2>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, cid, ncl, rank, lane, ptid); break;
+          case 4: producer_role_tma<PATH, 4>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, cid, ncl, rank, lane, ptid); break;
+          default: producer_role_tma<PATH, 8>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, cid, ncl, rank, lane, ptid); break;
+        }
+      } else {
+        switch (p.K) {
+          case 1: producer_role<PATH, 1>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
+          case 2: producer_role<PATH, 2>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
+          case 4: producer_role<PATH, 4>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
+          default: producer_role<PATH, 8>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
         }
       }
     }
-    __syncwarp();
-  } else if (warp <= kProdWarps) {
-    // ================================ producers ================================
-    if (p.use_tma) {
-      switch (p.K) {
-        case 1: producer_role_tma<PATH, 1>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, cid, ncl, rank, lane); break;
-        case 2: producer_role_tma<PATH, 2>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, cid, ncl, rank, lane); break;
-        case 4: producer_role_tma<PATH, 4>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, cid, ncl, rank, lane); break;
-        default: producer_role_tma<PATH, 8>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, cid, ncl, rank, lane); break;
-      }
-    } else {
-      switch (p.K) {
-        case 1: producer_role<PATH, 1>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane); break;
-        case 2: producer_role<PATH, 2>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane); break;
-        case 4: producer_role<PATH, 4>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane); break;
-        default: producer_role<PATH, 8>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane); break;
-      }
-    }
   } else {
+    ptx::setmaxnreg_inc<kRegsHigh>();
     // ================================ epilogue =================================
     const int ns = p.reset == 0 ? p.nsteps : 0;
     switch (ns) {
@@ -1002,7 +1004,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
       case 8: epilogue_role<NCH, PATH, NPART, 8>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
       default: epilogue_role<NCH, PATH, NPART, 0>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
     }
-  }
+    }
 
   // teardown: every role done in both CTAs before TMEM is released
   ptx::tc_fence_before();
