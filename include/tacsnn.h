@@ -167,7 +167,7 @@ int32_t tac_abi_version(void);           /* TACSNN_ABI_VERSION */
 int32_t tac_last_launch_count(void);
 
 /* Diagnostics (not needed for computation): route a per-group role timeline of
- * CTA 0 of every tcgen05 launch into `dev_buffer` (device, >= 4096 x 8 u64,
+ * CTA 0 of every tcgen05 launch into `dev_buffer` (device, >= 4096 x 16 u64,
  * %globaltimer ns; slots: producer start/done, MMA ready/issued, epilogue
  * full/released/done), or stop with NULL.  Process-global; not thread-safe. */
 void tac_debug_set_trace(void *dev_buffer);

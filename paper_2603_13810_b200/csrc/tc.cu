@@ -22,11 +22,11 @@
 // at halo pixel (g + r, c + s) for tap (r, s): the 8 rows of a core matrix are
 // 16 B apart and core-matrix groups (tile rows) SBO = 160 B apart, so a tap is
 // a start-address offset of (10 r + s) * 16 B -- no im2col copies, no junk rows.
-// Layers with C_in <= 2 (first layers) use an explicit im2col row in fp16 and
-// kind::f16 MMAs: the u8 aggregate (exact in fp16), the two fp16 slices of the
-// weights (hi + lo, |error| <= 2^-22 |w|) accumulated into ONE fp32 accumulator
-// by two MMAs, and the bias as a constant-1 A column -- so the epilogue reads Y
-// straight from TMEM (no combine).
+// Layers with C_in <= 8 (first layers) use the same halo scheme with 16 fp16
+// channels per halo pixel and kind::f16 MMAs: the u8 aggregate (exact in fp16),
+// the two fp16 slices of the weights (hi + lo, |error| <= 2^-22 |w|) accumulated
+// into ONE fp32 accumulator, and the bias through a constant-1 channel that only
+// the centre tap's weights read -- so the epilogue reads Y straight from TMEM.
 // TMEM lane i = tile pixel (g, c): epilogue warp q holds tile rows 4q..4q+3, so
 // every 2x2 pooling window lies inside one warp (lanes l, l^1, l^8, l^9) and
 // spikes are OR-pooled with two shuffles and stored straight from registers.
@@ -72,7 +72,7 @@ constexpr int kHaloH = kTileH + 2, kHaloW = kTileW + 2;  // 3x3 halo
 constexpr int kHaloRows = kHaloH * kHaloW;              // 180 halo pixels
 constexpr uint32_t kSmemLimit = 232448;
 
-enum { PATH_HALO = 0, PATH_IM2COL = 1 };
+enum { PATH_HALO = 0, PATH_H16 = 1 };  // int8 halo (C_in % 32 == 0) | fp16 halo (C_in <= 8)
 
 struct TcParams {
   CUtensorMap tmap;  // 4-D [T][B][H][WPR] u32 view of the input spikes (TMA producer)
@@ -100,7 +100,7 @@ struct TcParams {
 
 // trace slots per group iteration (CTA 0 only; TACSNN_TRACE env var)
 enum { TR_PROD_START = 0, TR_PROD_DONE, TR_MMA_READY, TR_MMA_ISSUED, TR_EPI_FULL, TR_EPI_RELEASED,
-       TR_EPI_DONE, TR_SLOTS = 8 };
+       TR_EPI_DONE, TR_PROD_RAW, TR_PROD_ISSUED, TR_SLOTS = 16 };
 __device__ __forceinline__ void trace_mark(const TcParams &p, uint32_t it, int slot) {
   if (p.trace && blockIdx.x == 0 && it < 4096) {
     unsigned long long t;
@@ -126,7 +126,7 @@ int cout_pad_of(int Cout) {
 }
 
 int path_of(const tac_conv_lif_desc *d) {
-  return (d->C_in % 32 == 0) ? PATH_HALO : PATH_IM2COL;
+  return (d->C_in % 32 == 0) ? PATH_HALO : PATH_H16;
 }
 
 struct Geometry {
@@ -156,11 +156,11 @@ Geometry geometry(const tac_conv_lif_desc *d, bool use_tma = false) {
     const int nwin = d->C_in / 32;
     g.raw_bw = nwin == 4 ? kHaloW * 4 : (int)align_up(kHaloW * nwin + 3, 4);
   } else {
-    g.nkc = 4;                              // 32 fp16 = 64 B = four 16-B K chunks
-    g.ntaps = 1;
-    g.w_bytes_cta = 64u * g.cout_pad;       // [hi/lo][4 chunks][C_out_pad/2 rows][16 B]
-    g.a_stage_bytes = 128u * 64u;
-    g.raw_bw = 8;  // 16-B aligned start word + the <= 2 words holding the window bits
+    g.nkc = 2;                              // 16 fp16 channels = two 16-B K chunks
+    g.ntaps = 9;
+    g.w_bytes_cta = 288u * g.cout_pad;      // [hi/lo][tap][2 chunks][C_out_pad/2 rows][16 B]
+    g.a_stage_bytes = align_up((uint32_t)kHaloRows * 32u, 128);
+    g.raw_bw = 8;  // 16-B aligned start word + the <= 3 words holding 10 px x C_in bits
   }
   g.raw_box_bytes = (uint32_t)K * kHaloH * g.raw_bw * 4u;
   g.raw_stage_bytes = align_up(g.raw_box_bytes, 128);
@@ -184,8 +184,8 @@ const char *shape_reason(const tac_conv_lif_desc *d) {
   if (d->R != 3 || d->S != 3) return "needs a 3x3 kernel";
   if (d->stride != 1) return "needs stride 1";
   if (d->pad < 0 || d->pad > 1) return "needs pad 0 or 1";
-  if (!((d->C_in % 32 == 0 && d->C_in <= 128) || d->C_in <= 2))
-    return "needs C_in in {1,2} or a multiple of 32 up to 128";
+  if (!((d->C_in % 32 == 0 && d->C_in <= 128) || d->C_in <= 8))
+    return "needs C_in <= 8 or a multiple of 32 up to 128";
   if (d->C_out > 128 || !(d->C_out % 32 == 0 || d->C_out == 8 || d->C_out == 16))
     return "needs C_out in {8,16} or a multiple of 32 up to 128";
   const int K = d->mode == TAC_MODE_DENSE ? 1 : d->K;
@@ -273,65 +273,66 @@ __device__ __forceinline__ void produce_halo(const TcParams &p, int tile, int k,
   }
 }
 
-// im2col producer (C_in <= 2): one 32-byte A row per tile pixel; byte r of word
-// q = (window row r, window bit q) with window bit q = s * C_in + c.
+// --- fp16 halo (C_in <= 8) ---------------------------------------------------
+// A halo pixel is a 32-byte K-major row of 16 fp16 channels: the u8 aggregate of
+// channels 0..C_in-1, 1.0 at channel C_in (read only by the centre tap's bias
+// weights), zeros above.  Bytes are built first (channel c <- byte c of lo/hi)
+// and converted exactly: fp16 bits 0x64nn = 1024 + n, minus 1024.
+__device__ __forceinline__ void h16_bias_slot(int Cin, uint32_t &lo, uint32_t &hi, uint32_t &c8) {
+  lo = Cin < 4 ? 1u << (8 * Cin) : 0u;
+  hi = (Cin >= 4 && Cin < 8) ? 1u << (8 * (Cin - 4)) : 0u;
+  c8 = Cin == 8 ? 0x3C00u : 0u;  // fp16 1.0 in channel 8 (chunk 1)
+}
+
+// spike bits (channel c = bit c, c < 8) of frame weight 2^e -> bytes of lo / hi
+__device__ __forceinline__ void h16_acc(uint32_t &lo, uint32_t &hi, uint32_t bits, int e) {
+  lo |= (((bits & 0xFu) * 0x204081u) & 0x01010101u) << e;  // bit i -> byte i
+  hi |= ((((bits >> 4) & 0xFu) * 0x204081u) & 0x01010101u) << e;
+}
+
+__device__ __forceinline__ uint32_t u8x2_to_f16x2(uint32_t bytes, uint32_t sel) {
+  uint32_t h = __byte_perm(bytes, 0x64646464u, sel), r;
+  asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(h), "r"(0x64006400u));
+  return r;
+}
+
+__device__ __forceinline__ void store_h16_row(uint32_t dst, uint32_t lbo, uint32_t lo, uint32_t hi,
+                                              uint32_t c8) {
+  ptx::st_shared_v4(dst, u8x2_to_f16x2(lo, 0x5140u), u8x2_to_f16x2(lo, 0x7362u),
+                    u8x2_to_f16x2(hi, 0x5140u), u8x2_to_f16x2(hi, 0x7362u));
+  ptx::st_shared_v4(dst + lbo, c8, 0u, 0u, 0u);
+}
+
+// LDG fallback: one halo pixel per thread and pass; the C_in <= 8 bits of pixel
+// xi start at row bit xi * C_in and straddle at most two words.
 template <int K>
-__device__ __forceinline__ void produce_im2col(const TcParams &p, int tile, int k,
-                                               uint32_t a_stage, int ptid) {
+__device__ __forceinline__ void produce_h16(const TcParams &p, int tile, int k, uint32_t a_stage,
+                                            int ptid) {
   int b, y0, x0;
   bool tok;
   tile_origin(p, tile, b, y0, x0, tok);
-  const uint32_t wmask = (1u << (3 * p.Cin)) - 1u;
-  for (int pos = ptid; pos < 128; pos += kProdWarps * 32) {
-    const int y = y0 + (pos >> 3), x = x0 + (pos & 7);
-    const bool valid = tok && y < p.Ho && x < p.Wo;
-    const int bit0 = (x - p.pad) * p.Cin;
-    const int w0 = bit0 >= 0 ? (bit0 >> 5) : -1;  // bit0 >= -2
-    const int sh = bit0 - w0 * 32;
-    const bool lo_ok = w0 >= 0 && w0 < p.wpr_in, hi_ok = w0 + 1 < p.wpr_in;
-    constexpr int KB = K > 2 ? 2 : K;  // frames per load batch
-    uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int Cin = p.Cin;
+  const uint32_t cmask = (1u << Cin) - 1u;
+  uint32_t one_lo, one_hi, c8;
+  h16_bias_slot(Cin, one_lo, one_hi, c8);
+  const uint32_t *frame0 = p.in + (long long)(k * K) * p.in_st + (long long)b * p.in_sb;
+  for (int row = ptid; row < kHaloRows; row += kProdWarps * 32) {
+    const int hy = row / kHaloW, hx = row - (row / kHaloW) * kHaloW;
+    const int yi = y0 + hy - p.pad, xi = x0 + hx - p.pad;
+    const bool ok = tok && yi >= 0 && yi < p.H && xi >= 0 && xi < p.W;
+    const int bit = ok ? xi * Cin : 0, sh = bit & 31;
+    const bool two = ok && sh + Cin > 32;
+    const uint32_t *src = frame0 + (long long)(ok ? yi : 0) * p.wpr_in + (bit >> 5);
+    uint32_t w0[K], w1[K];
 #pragma unroll
-    for (int j0 = 0; j0 < K; j0 += KB) {
-      uint32_t lo[KB][3], hi[KB][3];
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        const int yi = y + r - p.pad;
-        const bool rok = valid && yi >= 0 && yi < p.H;
-        const uint32_t *row = p.in + (long long)(k * K + j0) * p.in_st + (long long)b * p.in_sb +
-                              (long long)yi * p.wpr_in;
-#pragma unroll
-        for (int j = 0; j < KB; ++j) {
-          lo[j][r] = (rok && lo_ok) ? __ldg(row + j * p.in_st + w0) : 0u;
-          hi[j][r] = (rok && hi_ok) ? __ldg(row + j * p.in_st + w0 + 1) : 0u;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < KB; ++j) {
-        uint32_t z = 0;
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-          z |= (__funnelshift_r(lo[j][r], hi[j][r], sh) & wmask) << (8 * r);
-        const int e = p.m_shift * (j0 + j);
-#pragma unroll
-        for (int q = 0; q < 6; ++q) o[q] |= ((z >> q) & 0x00010101u) << e;
-      }
+    for (int j = 0; j < K; ++j) {
+      w0[j] = ok ? __ldg(src + (long long)j * p.in_st) : 0u;
+      w1[j] = two ? __ldg(src + (long long)j * p.in_st + 1) : 0u;
     }
-    // fp16 row: slot 4q + r <- byte r of word q (the u8 aggregate), slot 3 = 1.0
-    // (the bias column), slots 24..31 = 0
-    uint32_t h[16];
-    #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const uint32_t b0 = o[q] & 0xFFu, b1 = (o[q] >> 8) & 0xFFu, b2 = (o[q] >> 16) & 0xFFu;
-      const uint32_t b3 = q == 0 ? 0x3C00u : 0u;  // fp16 1.0
-      h[2 * q] = (uint32_t)__half_as_ushort(__uint2half_rn(b0)) |
-                 ((uint32_t)__half_as_ushort(__uint2half_rn(b1)) << 16);
-      h[2 * q + 1] = (uint32_t)__half_as_ushort(__uint2half_rn(b2)) | (b3 << 16);
-    }
-    #pragma unroll
-    for (int ck = 0; ck < 4; ++ck)
-      ptx::st_shared_v4(a_stage + (uint32_t)ck * p.lbo_a + (uint32_t)pos * 16u, h[4 * ck],
-                        h[4 * ck + 1], h[4 * ck + 2], h[4 * ck + 3]);
+    uint32_t lo = one_lo, hi = one_hi;
+#pragma unroll
+    for (int j = 0; j < K; ++j) h16_acc(lo, hi, __funnelshift_r(w0[j], w1[j], sh) & cmask, p.m_shift * j);
+    store_h16_row(a_stage + (uint32_t)row * 16u, p.lbo_a, lo, hi, c8);
   }
 }
 
@@ -368,46 +369,29 @@ __device__ __forceinline__ void produce_halo_tma(const TcParams &p, const uint32
 
 __device__ __forceinline__ int floor_div32(int v) { return v >= 0 ? (v >> 5) : -((31 - v) >> 5); }
 
+// The raw box holds words [c0w, c0w + 8) of each halo row (OOB words are zero, and
+// so are the bits past W*C_in of a row), so pixel xi sits at box bit
+// (xi * C_in - 32 c0w) >= 0 and never straddles past word 7.
 template <int K>
-__device__ __forceinline__ void produce_im2col_tma(const TcParams &p, const uint32_t *raw,
-                                                   uint32_t a_stage, int ptid, int x0) {
-  const int Cin = p.Cin, pad = p.pad;
-  const uint32_t wmask = (1u << (3 * Cin)) - 1u;
-  const int fstride = kHaloH * p.raw_bw;
+__device__ __forceinline__ void produce_h16_tma(const TcParams &p, const uint32_t *raw,
+                                                uint32_t a_stage, int ptid, int x0) {
+  const int Cin = p.Cin, bw = p.raw_bw, fstride = kHaloH * p.raw_bw;
+  const uint32_t cmask = (1u << Cin) - 1u;
   const int c0w = halo_c0(p, x0) & ~3;
+  uint32_t one_lo, one_hi, c8;
+  h16_bias_slot(Cin, one_lo, one_hi, c8);
+  const int mshift = p.m_shift;
 #pragma unroll 1
-  for (int pos = ptid; pos < 128; pos += kProdWarps * 32) {
-    const int g = pos >> 3, c = pos & 7;
-    const int bitoff = (x0 + c - pad) * Cin - c0w * 32;
-    const int w0 = bitoff >> 5, sh = bitoff & 31;
-    uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int row = ptid; row < kHaloRows; row += kProdWarps * 32) {
+    const int hy = row / kHaloW, hx = row - (row / kHaloW) * kHaloW;
+    const int bitoff = (x0 + hx - p.pad) * Cin - c0w * 32;
+    const uint32_t *src = raw + hy * bw + (bitoff >> 5);
+    const int sh = bitoff & 31;
+    uint32_t lo = one_lo, hi = one_hi;
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      uint32_t z = 0;
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        const uint32_t *rr = raw + j * fstride + (g + r) * p.raw_bw + w0;
-        z |= (__funnelshift_r(rr[0], rr[1], sh) & wmask) << (8 * r);
-      }
-      const int e = p.m_shift * j;
-#pragma unroll
-      for (int q = 0; q < 6; ++q) o[q] |= ((z >> q) & 0x00010101u) << e;
-    }
-    // fp16 row: slot 4q + r <- byte r of word q (the u8 aggregate), slot 3 = 1.0
-    // (the bias column), slots 24..31 = 0
-    uint32_t h[16];
-    #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const uint32_t b0 = o[q] & 0xFFu, b1 = (o[q] >> 8) & 0xFFu, b2 = (o[q] >> 16) & 0xFFu;
-      const uint32_t b3 = q == 0 ? 0x3C00u : 0u;  // fp16 1.0
-      h[2 * q] = (uint32_t)__half_as_ushort(__uint2half_rn(b0)) |
-                 ((uint32_t)__half_as_ushort(__uint2half_rn(b1)) << 16);
-      h[2 * q + 1] = (uint32_t)__half_as_ushort(__uint2half_rn(b2)) | (b3 << 16);
-    }
-    #pragma unroll
-    for (int ck = 0; ck < 4; ++ck)
-      ptx::st_shared_v4(a_stage + (uint32_t)ck * p.lbo_a + (uint32_t)pos * 16u, h[4 * ck],
-                        h[4 * ck + 1], h[4 * ck + 2], h[4 * ck + 3]);
+    for (int j = 0; j < K; ++j)
+      h16_acc(lo, hi, __funnelshift_r(src[j * fstride], src[j * fstride + 1], sh) & cmask, mshift * j);
+    store_h16_row(a_stage + (uint32_t)row * 16u, p.lbo_a, lo, hi, c8);
   }
 }
 
@@ -446,6 +430,7 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
       const uint32_t s = it % ns, ph = (it / ns) & 1u;
       const uint32_t r = it % nr, rph = (it / nr) & 1u;
       ptx::mbar_wait(bar_raw + 8 * r, rph);
+      if (ptid == 0) trace_mark(p, it, TR_PROD_RAW);
       ptx::mbar_wait(bar_a_empty + 8 * s, ph ^ 1u);
       if (ptid == 0) trace_mark(p, it, TR_PROD_START);
       const uint32_t *raw = reinterpret_cast<const uint32_t *>(smem + p.off_raw + r * p.raw_stage_bytes);
@@ -453,13 +438,14 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
       if (PATH == PATH_HALO)
         produce_halo_tma<K>(p, raw, a_stage, ptid, x0);
       else
-        produce_im2col_tma<K>(p, raw, a_stage, ptid, x0);
+        produce_h16_tma<K>(p, raw, a_stage, ptid, x0);
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_cluster(bar_a_full + 8 * s, 0);
       ptx::named_bar_sync(2, kProdWarps * 32);  // every producer is done with raw stage r
       if (ptid == 0) trace_mark(p, it, TR_PROD_DONE);
       if (ptid == 0 && ipair < p.num_pairs) issue(r);
+      if (ptid == 0) trace_mark(p, it, TR_PROD_ISSUED);
     }
   }
 }
@@ -479,7 +465,7 @@ __device__ __forceinline__ void producer_role(const TcParams &p, uint32_t sbase,
       if (PATH == PATH_HALO)
         produce_halo<K>(p, tile, k, a_stage, ptid);
       else
-        produce_im2col<K>(p, tile, k, a_stage, ptid);
+        produce_h16<K>(p, tile, k, a_stage, ptid);
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_cluster(bar_a_full + 8 * s, 0);
@@ -718,7 +704,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
 #pragma unroll
         for (int w = 0; w < NWT; ++w) inv[j][w] = 0u;
       const uint32_t tcol = tmem_base + lane_addr + acc * p.n_total + (uint32_t)co_base;
-      constexpr bool F16 = PATH == PATH_IM2COL;  // fp32 Y straight from TMEM
+      constexpr bool F16 = PATH == PATH_H16;  // fp32 Y straight from TMEM
       constexpr int NBUF = (NPART == 2 || F16) ? 2 : 1;  // TMEM prefetch depth (registers)
       uint32_t d[NBUF][2][8];                    // [buffer][hi/lo][col]
       ptx::tmem_ld8(tcol, d[0][0]);
@@ -955,15 +941,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
                   }
                 }
               } else {
-                // D = A W_hi + A W_lo (+ bias via the constant column): 2 slices x 2 K=16 steps
+                // D = sum_taps A_tap (W_hi + W_lo) (+ bias via the constant channel of the
+                // centre tap): 9 taps x 2 fp16 slices, K = 16 each, into one accumulator
                 const uint32_t idf = ptx::idesc_f16(256, p.n_total);
-  #pragma unroll
-                for (int sl = 0; sl < 2; ++sl)
-  #pragma unroll
-                  for (int kc2 = 0; kc2 < 2; ++kc2)
-                    ptx::mma_f16_cg2(d_tmem, a_base + (uint64_t)(2u * kc2 * lbo16),
-                                     b_desc0 + (uint64_t)((sl * 4 + 2 * kc2) * nhb16), idf,
-                                     (sl | kc2) ? 1u : 0u);
+#pragma unroll
+                for (int tap = 0; tap < 9; ++tap) {
+                  const uint32_t toff = (uint32_t)((tap / 3) * kHaloW + (tap % 3));
+#pragma unroll
+                  for (int sl = 0; sl < 2; ++sl)
+                    ptx::mma_f16_cg2(d_tmem, a_base + (uint64_t)toff,
+                                     b_desc0 + (uint64_t)((sl * 9 + tap) * 2 * nhb16), idf,
+                                     (tap | sl) ? 1u : 0u);
+                }
               }
               ptx::mma_commit_cg2_multicast(bar_a_empty + 8 * s);
               ptx::mma_commit_cg2_multicast(bar_t_full + 8 * acc);
@@ -1056,7 +1045,7 @@ size_t tc_weights_bytes(const tac_conv_lif_desc *d) {
 
 // Two int8 slices per output channel, laid out as the smem image of each CTA:
 // halo  : [tap][kc16][n][16 B], K index 32w + 4o + b <-> channel 32w + o + 8b
-// im2col: fp16 hi/lo slices, see below (K index 4o + r <-> (r, s = o / C_in, c = o % C_in))
+// h16   : fp16 hi/lo slices over a 16-channel halo pixel, see below
 // followed by fp32 [s1/254 | bias | s1 | s2] per padded output channel.
 void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bias,
                 unsigned char *dst) {
@@ -1100,9 +1089,10 @@ void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bi
         }
     } else {
       // fp16 image, CTA `half` holds output channels [half*Cp/2, (half+1)*Cp/2) of BOTH
-      // slices: [slice][16-B chunk (4)][row (Cp/2)][8 fp16].  K index k = 4o + r holds
-      // W[n][c][r][s] (o = s*C_in + c), k = 3 the bias; the aggregate scale
-      // 2^{-m(K-1)} (exact) is folded into the weights, not the bias.
+      // slices: [slice][tap][16-B chunk (2)][row (Cp/2)][8 fp16].  Halo channel k < C_in
+      // holds W[n][k][r][s] (tap = 3r + s), channel C_in of the centre tap the bias
+      // (the producers store 1.0 there); the aggregate scale 2^{-m(K-1)} (exact) is
+      // folded into the weights, not the bias.
       const int m = d->mode == TAC_MODE_DENSE ? 0 : beta_shift(d->beta);
       const int Kg = d->mode == TAC_MODE_DENSE ? 1 : d->K;
       const double agg = std::ldexp(1.0, -m * (Kg - 1));
@@ -1110,19 +1100,19 @@ void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bi
       uint16_t *img16 = reinterpret_cast<uint16_t *>(img);
       for (int nl = 0; nl < nh; ++nl) {
         const int n = half * nh + nl;
-        for (int kidx = 0; kidx < 32; ++kidx) {
-          const int o = kidx / 4, r = kidx % 4;
-          double wv = 0.0;
-          if (n < Co) {
-            if (kidx == 3) wv = bias ? (double)bias[n] : 0.0;
-            else if (r < 3 && o < 3 * Ci) wv = (double)weight[(((size_t)n * Ci + o % Ci) * 3 + r) * 3 + o / Ci] * agg;
+        for (int tap = 0; tap < 9; ++tap)
+          for (int k = 0; k < 16; ++k) {
+            double wv = 0.0;
+            if (n < Co) {
+              if (k < Ci) wv = (double)weight[(((size_t)n * Ci + k) * 3 + tap / 3) * 3 + tap % 3] * agg;
+              else if (k == Ci && tap == 4) wv = bias ? (double)bias[n] : 0.0;
+            }
+            const __half hi = __double2half(wv);
+            const __half lo = __double2half(wv - (double)__half2float(hi));
+            const int ck = k / 8, e = k % 8;
+            img16[((((size_t)0 * 9 + tap) * 2 + ck) * nh + nl) * 8 + e] = __half_as_ushort(hi);
+            img16[((((size_t)1 * 9 + tap) * 2 + ck) * nh + nl) * 8 + e] = __half_as_ushort(lo);
           }
-          const __half hi = __double2half(wv);
-          const __half lo = __double2half(wv - (double)__half2float(hi));
-          const int ck = kidx / 8, e = kidx % 8;
-          img16[((size_t)(0 * 4 + ck) * nh + nl) * 8 + e] = __half_as_ushort(hi);
-          img16[((size_t)(1 * 4 + ck) * nh + nl) * 8 + e] = __half_as_ushort(lo);
-        }
       }
     }
   }
@@ -1219,15 +1209,9 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   uint32_t cols = 32;
   while (cols < 2u * p.n_total) cols <<= 1;
   p.tmem_cols = cols;
-  if (g.path == PATH_HALO) {
-    p.lbo_a = (uint32_t)kHaloRows * 16u;  // between 16-byte K chunks
-    p.sbo_a = (uint32_t)kHaloW * 16u;     // between tile rows (8-row core-matrix groups)
-    for (int t = 0; t < 9; ++t) p.tap_off[t] = (t / 3) * kHaloW + (t % 3);
-  } else {
-    p.lbo_a = 128u * 16u;
-    p.sbo_a = 128u;
-    for (int t = 0; t < 9; ++t) p.tap_off[t] = 0;
-  }
+  p.lbo_a = (uint32_t)kHaloRows * 16u;  // between 16-byte K chunks
+  p.sbo_a = (uint32_t)kHaloW * 16u;     // between tile rows (8-row core-matrix groups)
+  for (int t = 0; t < 9; ++t) p.tap_off[t] = (t / 3) * kHaloW + (t % 3);
   // B: rows held by one CTA x 16 B between 16-byte K chunks
   p.lbo_b = g.path == PATH_HALO ? (uint32_t)g.cout_pad * 16u : (uint32_t)(g.cout_pad / 2) * 16u;
   p.in = lp.in; p.out = lp.out; p.v_init = lp.v_init; p.v_final = lp.v_final; p.counts = lp.counts;
@@ -1258,10 +1242,10 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
     }
   } else {
     switch (g.cout_pad) {
-      case 16: e = launch_kernel<8, PATH_IM2COL, 2>(p, nclusters, st); break;
-      case 32: e = launch_kernel<16, PATH_IM2COL, 2>(p, nclusters, st); break;
-      case 64: e = launch_kernel<32, PATH_IM2COL, 2>(p, nclusters, st); break;
-      default: e = launch_kernel<32, PATH_IM2COL, 4>(p, nclusters, st); break;
+      case 16: e = launch_kernel<8, PATH_H16, 2>(p, nclusters, st); break;
+      case 32: e = launch_kernel<16, PATH_H16, 2>(p, nclusters, st); break;
+      case 64: e = launch_kernel<32, PATH_H16, 2>(p, nclusters, st); break;
+      default: e = launch_kernel<32, PATH_H16, 4>(p, nclusters, st); break;
     }
   }
   ++*launches;

@@ -14,7 +14,8 @@ import torch  # noqa: E402
 
 from paper_2603_13810_b200 import configs, tacsnn  # noqa: E402
 
-NAMES = ["prod_start", "prod_done", "mma_ready", "mma_issued", "epi_full", "epi_released", "epi_done"]
+NAMES = ["prod_start", "prod_done", "mma_ready", "mma_issued", "epi_full", "epi_released", "epi_done",
+         "prod_raw", "prod_issued"]
 
 
 def main():
@@ -32,18 +33,18 @@ def main():
     x = tacsnn.pack((torch.rand((spec.T, spec.B, spec.C_in, spec.H, spec.W), device="cuda",
                                 generator=g) < 0.15).to(torch.uint8))
     tacsnn.conv_lif(spec, prep, x)  # warm
-    buf = torch.zeros(4096 * 8, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")
     tacsnn.lib().tac_debug_set_trace(ctypes.c_void_p(buf.data_ptr()))
     tacsnn.conv_lif(spec, prep, x)
     torch.cuda.synchronize()
     tacsnn.lib().tac_debug_set_trace(None)
-    tr = buf.view(4096, 8).cpu().numpy()
+    tr = buf.view(4096, 16).cpu().numpy()
     n = int((tr[:, 0] > 0).sum())
     t0 = tr[0, 0]
     print(f"layer {a.layer} B={a.B}: {n} group iterations traced on CTA 0")
     print("it " + " ".join(f"{s:>12s}" for s in NAMES))
     for i in list(range(min(a.rows, n))) + list(range(max(a.rows, n - 4), n)):
-        print(f"{i:3d} " + " ".join(f"{(tr[i, j] - t0) / 1e3:12.2f}" for j in range(7)))
+        print(f"{i:3d} " + " ".join(f"{(tr[i, j] - t0) / 1e3:12.2f}" for j in range(9)))
     import numpy as np
     it = tr[1:n]
     d = lambda j0, j1: np.median(it[:, j1] - it[:, j0]) / 1e3
@@ -54,6 +55,9 @@ def main():
     print(f"median epi wait (prev done -> full): {np.median(tr[1:n, 4] - tr[:n-1, 6]) / 1e3:.2f} us; "
           f"MMA wait (prev issued -> ready): {np.median(tr[1:n, 2] - tr[:n-1, 3]) / 1e3:.2f} us; "
           f"producer wait (prev done -> start): {np.median(tr[1:n, 0] - tr[:n-1, 1]) / 1e3:.2f} us")
+    print(f"  TMA issue (done -> issued): {np.median(tr[:n, 8] - tr[:n, 1]) / 1e3:.2f} us")
+    print(f"  of which prev done -> raw ready: {np.median(tr[1:n, 7] - tr[:n-1, 1]) / 1e3:.2f} us, "
+          f"raw ready -> A stage free: {np.median(tr[1:n, 0] - tr[1:n, 7]) / 1e3:.2f} us")
 
 
 if __name__ == "__main__":

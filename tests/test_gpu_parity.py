@@ -77,6 +77,11 @@ LAYER_CASES = [
     ("dvsL5", (8, 5, 128, 8, 8, 128, 1, 2), 3.5, 0.1),
     ("ragged", (8, 3, 3, 13, 11, 24, 1, 1), 2.0, 0.3),
     ("wide_cin", (4, 2, 96, 10, 9, 48, 1, 2), 2.5, 0.2),
+    # fp16-halo path (C_in <= 8): LDG producers (rows not 16-B multiples) and TMA
+    ("rgb", (4, 2, 3, 20, 19, 32, 1, 2), 2.5, 0.2),
+    ("cin6_pad0", (4, 2, 6, 9, 13, 16, 0, 1), 2.5, 0.2),
+    ("cin4_tma", (4, 2, 4, 24, 32, 64, 1, 2), 2.5, 0.2),
+    ("cin8_tma", (4, 2, 8, 17, 48, 128, 1, 1), 2.5, 0.2),
 ]
 
 
