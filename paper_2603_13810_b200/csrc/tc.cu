@@ -526,51 +526,62 @@ __device__ __forceinline__ void lif_step(float &v, float y, float decay, float v
   if (RESET == 1) prev = (prev & ~bitmask) | (~(uint32_t)msk & bitmask);
 }
 
-__device__ __forceinline__ uint32_t lop3_select(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;  // (a & ~c) | (b & c)
-  asm("lop3.b32 %0, %1, %2, %3, 0xD8;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
+// Specialised subtract-reset path (NS > 0) in the shifted state U = V - v_th:
+//   U <- decay U + Y'        with Y' = Y + (decay - 1) v_th folded into the bias
+//   f  = [U >= 0]            = sat(U 2^127 + 1) (ftz: exactly 0 or 1 for every U)
+//   U <- U - v_th f          (one fma, exact when f = 0 or 1)
+// The spike is then bit 23..29 of f (1.0f = 0x3F800000): channel CB + i of a
+// chunk of 8 is OR-ed into accumulator i / 7 at bit 23 + i % 7 on the ALU pipe,
+// and the two accumulators are folded into the spike word once per chunk.
+// Per neuron-step: half an FFMA2 (update), one FFMA.SAT, half an FFMA2 (reset) on
+// the FMA pipe, 1 + 3/8 ALU ops.
+__device__ __forceinline__ float sat_spike(float u) {
+  float f;
+  asm("fma.rn.ftz.sat.f32 %0, %1, 0f7F000000, 0f3F800000;" : "=f"(f) : "f"(u));
+  return f;
 }
 
-// inv += m * (-bit) on the FMA pipe (m in {0,-1}): sets `bit` when m = -1
 template <uint32_t BIT>
-__device__ __forceinline__ uint32_t mad_bit(uint32_t m, uint32_t inv) {
-  uint32_t d;
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(m), "n"(0u - BIT), "r"(inv));
+__device__ __forceinline__ uint32_t or_bit(uint32_t acc, float f) {
+  uint32_t d;  // acc | (f & BIT)
+  asm("lop3.b32 %0, %1, %2, %3, 0xF8;" : "=r"(d) : "r"(acc), "r"(__float_as_uint(f)), "n"(BIT));
   return d;
 }
 
-// two neurons (channels C0, C0+1 of a 32-bit word), NS steps sharing one drive
-// (TAC-TP) or NS = 1 (TAC / dense), subtract reset, packed fp32x2 arithmetic
-// (identical rounding to the scalar form).  Per neuron-step: half an FFMA2 and
-// an FADD2, one SHF + one LOP3 (ALU pipe), one IMAD (FMA pipe) -- balanced pipes.
-// inv[j] bit c is set when channel c did NOT spike.
-template <int NS, int C0>
-__device__ __forceinline__ void lif_pair_sub(float2 &v, float2 y, float2 dec2, float2 nth2,
-                                             uint32_t (&inv)[NS]) {
+// two neurons (chunk channels I, I + 1), NS steps sharing one drive (TAC-TP) or
+// NS = 1 (TAC / dense)
+template <int NS, int I>
+__device__ __forceinline__ void lif_pair_u(float2 &u, float2 y, float2 dec2, float2 nth2,
+                                           uint32_t (&a)[NS][2]) {
 #pragma unroll
   for (int j = 0; j < NS; ++j) {
-    v = __ffma2_rn(dec2, v, y);                       // V <- beta V + Y
-    const float2 v2 = __fadd2_rn(v, nth2);            // V - v_th
-    const uint32_t a0 = __float_as_uint(v2.x), a1 = __float_as_uint(v2.y);
-    // sign masks: one on the ALU pipe (SHF), one on the FMA pipe (IMAD.HI) for balance
-    const uint32_t m0 = (uint32_t)((int)a0 >> 31);
-    uint32_t m1;
-    asm("mul.hi.s32 %0, %1, 1;" : "=r"(m1) : "r"(a1));
-    v.x = __uint_as_float(lop3_select(a0, __float_as_uint(v.x), m0));  // spike: V - v_th
-    v.y = __uint_as_float(lop3_select(a1, __float_as_uint(v.y), m1));
-    inv[j] = mad_bit<1u << C0>(m0, inv[j]);
-    inv[j] = mad_bit<1u << (C0 + 1)>(m1, inv[j]);
+    u = __ffma2_rn(dec2, u, y);
+    const float2 f = make_float2(sat_spike(u.x), sat_spike(u.y));
+    u = __ffma2_rn(nth2, f, u);
+    a[j][I / 7] = or_bit<1u << (23 + I % 7)>(a[j][I / 7], f.x);
+    a[j][(I + 1) / 7] = or_bit<1u << (23 + (I + 1) % 7)>(a[j][(I + 1) / 7], f.y);
   }
 }
 
-template <int NSP, int CB>
-__device__ __forceinline__ void lif_chunk8(float2 *V, const float (&yv)[8], float2 dec2,
-                                           float2 nth2, uint32_t (&invp)[NSP]) {
-  lif_pair_sub<NSP, CB + 0>(V[0], make_float2(yv[0], yv[1]), dec2, nth2, invp);
-  lif_pair_sub<NSP, CB + 2>(V[1], make_float2(yv[2], yv[3]), dec2, nth2, invp);
-  lif_pair_sub<NSP, CB + 4>(V[2], make_float2(yv[4], yv[5]), dec2, nth2, invp);
-  lif_pair_sub<NSP, CB + 6>(V[3], make_float2(yv[6], yv[7]), dec2, nth2, invp);
+template <int N>
+__device__ __forceinline__ uint32_t shift_by(uint32_t x) {  // x << N (N may be negative)
+  return N >= 0 ? (x << (N >= 0 ? N : 0)) : (x >> (N < 0 ? -N : 0));
+}
+
+// 8 channels CB .. CB + 7 of the thread's 32-bit spike word(s) spk[j]
+template <int NS, int CB>
+__device__ __forceinline__ void lif_chunk8(float2 *U, const float (&yv)[8], float2 dec2,
+                                           float2 nth2, uint32_t (&spk)[NS]) {
+  uint32_t a[NS][2];
+#pragma unroll
+  for (int j = 0; j < NS; ++j) a[j][0] = a[j][1] = 0u;
+  lif_pair_u<NS, 0>(U[0], make_float2(yv[0], yv[1]), dec2, nth2, a);
+  lif_pair_u<NS, 2>(U[1], make_float2(yv[2], yv[3]), dec2, nth2, a);
+  lif_pair_u<NS, 4>(U[2], make_float2(yv[4], yv[5]), dec2, nth2, a);
+  lif_pair_u<NS, 6>(U[3], make_float2(yv[6], yv[7]), dec2, nth2, a);
+#pragma unroll
+  for (int j = 0; j < NS; ++j)  // bits 23..29 of a0 -> CB..CB+6, bit 23 of a1 -> CB+7
+    spk[j] |= shift_by<CB - 23>(a[j][0]) | shift_by<CB - 16>(a[j][1]);
 }
 
 // Y for 8 channels from the two s32 accumulator slices (see file header)
@@ -639,6 +650,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
                                               int ncl, uint32_t rank, uint32_t warp,
                                               uint32_t lane) {
   constexpr int NWT = NCH >= 32 ? NCH / 32 : 1;  // spike words per epilogue thread
+  static_assert(NS == 0 || NWT == 1, "specialised path: one spike word per thread");
   constexpr int NSM = NS ? NS : kMaxSteps;
   const float *sc = reinterpret_cast<const float *>(smem + p.off_scale);
   const int e = (int)warp;                   // epilogue warps are 0 .. 4 NPART - 1
@@ -687,7 +699,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
         if (co_base + cc < Cout) v0 = __ldg(p.v_init + vbase + cc);
         if (co_base + cc + 1 < Cout) v1 = __ldg(p.v_init + vbase + cc + 1);
       }
-      V[cc / 2] = make_float2(v0, v1);
+      V[cc / 2] = NS > 0 ? make_float2(v0 - vth, v1 - vth) : make_float2(v0, v1);  // U = V - v_th
       if (NS == 0 && p.reset == 1) {  // reading R4
         if (v0 >= vth) prev[cc / 32] |= 1u << (cc % 32);
         if (v1 >= vth) prev[(cc + 1) / 32] |= 1u << ((cc + 1) % 32);
@@ -698,11 +710,15 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
       ptx::mbar_wait(bar_t_full + 8 * acc, aph);
       ptx::tc_fence_after();
       if (e == 0 && lane == 0) trace_mark(p, it, TR_EPI_FULL);
-      uint32_t inv[NSM][NWT];
+      constexpr int NSP = (NS > 0) ? NS : 1;
+      uint32_t inv[NSM][NWT];   // generic path: NOT(spike) bits
+      uint32_t sw1[NSP];          // specialised path (NWT == 1): spike words
 #pragma unroll
       for (int j = 0; j < NSM; ++j)
 #pragma unroll
         for (int w = 0; w < NWT; ++w) inv[j][w] = 0u;
+#pragma unroll
+      for (int j = 0; j < NSP; ++j) sw1[j] = 0u;
       const uint32_t tcol = tmem_base + lane_addr + acc * p.n_total + (uint32_t)co_base;
       constexpr bool F16 = PATH == PATH_H16;  // fp32 Y straight from TMEM
       constexpr int NBUF = (NPART == 2 || F16) ? 2 : 1;  // TMEM prefetch depth (registers)
@@ -725,19 +741,12 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
           combine8(p, sc, co_base + ch * 8, d[cur][0], d[cur][1], yv);
         }
         if (NS > 0) {
-          constexpr int NSP = (NS > 0) ? NS : 1;
-          const int w = (ch * 8) / 32;
-          uint32_t invp[NSP];
-#pragma unroll
-          for (int j = 0; j < NSP; ++j) invp[j] = inv[j][w];
-          switch ((ch * 8) % 32) {  // compile-time after unrolling
-            case 0: lif_chunk8<NSP, 0>(V + ch * 4, yv, dec2, nth2, invp); break;
-            case 8: lif_chunk8<NSP, 8>(V + ch * 4, yv, dec2, nth2, invp); break;
-            case 16: lif_chunk8<NSP, 16>(V + ch * 4, yv, dec2, nth2, invp); break;
-            default: lif_chunk8<NSP, 24>(V + ch * 4, yv, dec2, nth2, invp); break;
+          switch (ch) {  // compile-time after unrolling (NCH <= 32: one spike word)
+            case 0: lif_chunk8<NSP, 0>(V + ch * 4, yv, dec2, nth2, sw1); break;
+            case 1: lif_chunk8<NSP, 8>(V + ch * 4, yv, dec2, nth2, sw1); break;
+            case 2: lif_chunk8<NSP, 16>(V + ch * 4, yv, dec2, nth2, sw1); break;
+            default: lif_chunk8<NSP, 24>(V + ch * 4, yv, dec2, nth2, sw1); break;
           }
-#pragma unroll
-          for (int j = 0; j < NSP; ++j) inv[j][w] = invp[j];
         } else {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -771,6 +780,12 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
       if (e == 0 && lane == 0) trace_mark(p, it, TR_EPI_RELEASED);
 
       // spikes: bit-sliced counters, in-warp 2x2 OR-pool, direct packed stores
+      uint32_t spk[NSM][NWT];
+#pragma unroll
+      for (int j = 0; j < NSM; ++j)
+#pragma unroll
+        for (int w = 0; w < NWT; ++w)
+          spk[j][w] = !valid ? 0u : (NS > 0 ? sw1[j < NSP ? j : 0] : (~inv[j][w] & chmask));
 #pragma unroll
       for (int j = 0; j < NSM; ++j) {
         if (NS > 0 || j < nsteps) {
@@ -778,7 +793,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
           uint32_t *orow_t = orow + (long long)t_out * p.out_st;
 #pragma unroll
           for (int w = 0; w < NWT; ++w) {
-            uint32_t s = valid ? (~inv[j][w] & chmask) : 0u;
+            uint32_t s = spk[j][w];
             if (NS == 0 || NS == 1) {  // ripple add of one word into the counters
               uint32_t cy = s;
 #pragma unroll
@@ -808,7 +823,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
         for (int w = 0; w < NWT; ++w) {
           uint32_t sw[NSM];
 #pragma unroll
-          for (int j = 0; j < NSM; ++j) sw[j] = valid ? (~inv[j][w] & chmask) : 0u;
+          for (int j = 0; j < NSM; ++j) sw[j] = spk[j][w];
           uint32_t P[kPlanes];
 #pragma unroll
           for (int pl = 0; pl < kPlanes; ++pl) P[pl] = planes[pl][w];
@@ -832,8 +847,9 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
     if (p.v_final && valid) {
 #pragma unroll
       for (int cc = 0; cc < NCH; cc += 2) {
-        if (co_base + cc < Cout) p.v_final[vbase + cc] = V[cc / 2].x;
-        if (co_base + cc + 1 < Cout) p.v_final[vbase + cc + 1] = V[cc / 2].y;
+        const float2 v = NS > 0 ? make_float2(V[cc / 2].x + vth, V[cc / 2].y + vth) : V[cc / 2];
+        if (co_base + cc < Cout) p.v_final[vbase + cc] = v.x;
+        if (co_base + cc + 1 < Cout) p.v_final[vbase + cc + 1] = v.y;
       }
     }
   }
@@ -1038,6 +1054,20 @@ const char *tc_unsupported_reason(const tac_conv_lif_desc *d) {
   return r ? r : "supported";
 }
 
+// The specialised subtract-reset epilogue (NS > 0) runs in U = V - v_th and needs
+// the drive Y' = Y + (decay - 1) v_th: the offset is folded into the prepared bias
+// (per-step decay = beta^K for TAC, beta otherwise, as abi.cu computes it).
+static bool lif_u_state(const tac_conv_lif_desc *d) {
+  const int ns = d->mode == TAC_MODE_TACTP ? d->K : 1;
+  return d->reset == TAC_RESET_SUBTRACT && (ns == 1 || ns == 2 || ns == 4 || ns == 8);
+}
+static double lif_bias_offset(const tac_conv_lif_desc *d) {
+  if (!lif_u_state(d)) return 0.0;
+  const int K = d->mode == TAC_MODE_DENSE ? 1 : d->K;
+  const float decay = (float)(d->mode == TAC_MODE_TAC ? std::pow((double)d->beta, (double)K) : d->beta);
+  return ((double)decay - 1.0) * (double)d->v_th;
+}
+
 size_t tc_weights_bytes(const tac_conv_lif_desc *d) {
   const Geometry g = geometry(d);
   return 2 * (size_t)g.w_bytes_cta + 4 * (size_t)g.cout_pad * 4;
@@ -1053,7 +1083,9 @@ void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bi
   const int Co = d->C_out, Ci = d->C_in, Cp = g.cout_pad;
   std::vector<signed char> q1((size_t)Cp * Ci * 9, 0), q2((size_t)Cp * Ci * 9, 0);
   std::vector<float> s1(Cp, 0.f), s2(Cp, 0.f), bs(Cp, 0.f);
+  const double boff = lif_bias_offset(d);
   for (int co = 0; co < Co; ++co) {
+    bs[co] = (float)((bias ? (double)bias[co] : 0.0) + boff);
     double amax = 0.0;
     for (int i = 0; i < Ci * 9; ++i) amax = std::max(amax, std::fabs((double)weight[(size_t)co * Ci * 9 + i]));
     if (amax == 0.0) continue;
@@ -1068,7 +1100,6 @@ void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bi
       q1[(size_t)co * Ci * 9 + i] = (signed char)a;
       q2[(size_t)co * Ci * 9 + i] = (signed char)b;
     }
-    bs[co] = bias ? bias[co] : 0.f;
   }
   auto q_at = [&](int half, int co, int ci, int r, int s) -> signed char {
     const std::vector<signed char> &q = half ? q2 : q1;
@@ -1105,7 +1136,7 @@ void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bi
             double wv = 0.0;
             if (n < Co) {
               if (k < Ci) wv = (double)weight[(((size_t)n * Ci + k) * 3 + tap / 3) * 3 + tap % 3] * agg;
-              else if (k == Ci && tap == 4) wv = bias ? (double)bias[n] : 0.0;
+              else if (k == Ci && tap == 4) wv = (bias ? (double)bias[n] : 0.0) + boff;
             }
             const __half hi = __double2half(wv);
             const __half lo = __double2half(wv - (double)__half2float(hi));

@@ -129,7 +129,14 @@ def test_v_init_chaining(T, O, reset, engine):
     c, vc, _ = T.conv_lif(h, prep, x[4:], v_init=va, want_v_final=True)
     torch.cuda.synchronize()
     assert torch.equal(torch.cat([a, c]), full)
-    assert torch.equal(vc, vf)
+    # the subtract-reset tcgen05 path keeps U = V - v_th internally, so V crosses the
+    # call boundary with one extra fp32 rounding (U + v_th, then V - v_th): equal up
+    # to a few ulp of max(|V|, v_th); the other paths carry V itself (bit-exact)
+    exact = not (reset == "subtract" and spec.engine_used() == "tcgen05")
+    if exact:
+        assert torch.equal(vc, vf)
+    else:
+        assert torch.allclose(vc, vf, rtol=0, atol=4 * 2.0 ** -23 * max(1.0, vf.abs().max().item()))
     # and the chained second half against the oracle with v_init
     P.check_layer(T, O, h, S[4:], w, b, v_init=va.cpu().numpy().transpose(0, 3, 1, 2),
                   label=f"chain/{reset}/{engine}")
