@@ -171,7 +171,8 @@ int32_t tac_last_launch_count(void);
 /* Diagnostics (not needed for computation): route a per-group role timeline of
  * CTA 0 of every tcgen05 launch into `dev_buffer` (device, >= 4096 x 16 u64,
  * %globaltimer ns; slots: producer start/done, MMA ready/issued, epilogue
- * full/released/done), or stop with NULL.  Process-global; not thread-safe. */
+ * full/released/done), or stop with NULL.  Process-global; not thread-safe.
+ * Only a library built with -DTACSNN_TRACE records anything (scripts/trace_layer.py). */
 void tac_debug_set_trace(void *dev_buffer);
 
 #ifdef __cplusplus

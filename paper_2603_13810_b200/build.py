@@ -41,10 +41,11 @@ def _deps(src):
 
 def _compile(src, force, verbose, ptxas_v):
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+    trace = os.environ.get("TACSNN_TRACE") == "1"  # debug timeline build (see tc.cu trace_mark)
     if not force and os.path.exists(obj) and all(
             os.path.getmtime(obj) >= os.path.getmtime(d) for d in _deps(src)):
         return obj, ""
-    cmd = [nvcc(), *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [nvcc(), *ARCH, *FLAGS, *(["-DTACSNN_TRACE"] if trace else []), "-c", src, "-o", obj]
     if ptxas_v:
         cmd += ["-Xptxas", "-v"]
     if verbose:

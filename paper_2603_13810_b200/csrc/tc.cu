@@ -46,6 +46,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -56,6 +57,9 @@ namespace tacsnn {
 
 namespace {
 
+// 3 producer warps: with 16 epilogue warps + the MMA warp the CTA has 20 warps, 5
+// per SM sub-partition, which is what the per-SMSP register file (16 K regs) and
+// the setmaxnreg budget below allow (a 21st warp would cap every warp at 80 regs).
 constexpr int kProdWarps = 3;
 // Warp layout: epilogue warps first (NPART channel parts x 4 TMEM lane quadrants),
 // then the MMA warp, then the producer warps.  The SM warp schedulers favour
@@ -98,15 +102,23 @@ struct TcParams {
   unsigned long long *trace;  // optional: per-(group) role timestamps of CTA 0 (debug)
 };
 
-// trace slots per group iteration (CTA 0 only; TACSNN_TRACE env var)
+// trace slots per group iteration (CTA 0 only).  Compiled in only when the library
+// is built with -DTACSNN_TRACE (TACSNN_TRACE=1 python -m paper_2603_13810_b200.build
+// --force); otherwise trace_mark is empty and costs nothing in the hot loops.
 enum { TR_PROD_START = 0, TR_PROD_DONE, TR_MMA_READY, TR_MMA_ISSUED, TR_EPI_FULL, TR_EPI_RELEASED,
        TR_EPI_DONE, TR_PROD_RAW, TR_PROD_ISSUED, TR_SLOTS = 16 };
 __device__ __forceinline__ void trace_mark(const TcParams &p, uint32_t it, int slot) {
+#ifdef TACSNN_TRACE
   if (p.trace && blockIdx.x == 0 && it < 4096) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     p.trace[it * TR_SLOTS + slot] = t;
   }
+#else
+  (void)p;
+  (void)it;
+  (void)slot;
+#endif
 }
 
 // ------------------------------------------------------------ host helpers --
@@ -135,7 +147,7 @@ struct Geometry {
       off_scale, off_bar, smem_bytes;
 };
 constexpr int kMaxRaw = 4;
-constexpr int kNumBars = 2 * kMaxStages + 2 * kAccs + 1 + kMaxRaw;
+constexpr int kNumBars = 2 * kMaxStages + 2 * kAccs + 1 + 2 * kMaxRaw;
 
 uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
@@ -344,6 +356,31 @@ __device__ __forceinline__ int halo_c0(const TcParams &p, int x0) {
                                                   : -((31 - (x0 - p.pad) * p.Cin) >> 5));
 }
 
+// d | (a & b) in one LOP3
+__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t b, uint32_t d) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(a), "r"(b), "r"(d));
+  return r;
+}
+
+// o[q] (channels q + 8b at byte b) |= frame bit << e with a compile-time frame
+// shift e = j (beta = 1/2, or K = 1): one SHF + one LOP3 per (q, frame)
+template <int K>
+__device__ __forceinline__ void agg_word_m1(uint32_t (&o)[8], const uint32_t (&xj)[K]) {
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const uint32_t mask = 0x01010101u << j;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t t = (q >= j) ? (xj[j] >> (q - j)) : (xj[j] << (j - q));
+      o[q] = and_or(t, mask, o[q]);
+    }
+  }
+}
+
+// TMA raw-halo producer (C_in = 32 nwin): thread owns 32-channel word w of halo
+// pixels row0, row0 + rstep, ...; two pixels per pass with all 2K smem loads
+// issued before any arithmetic (one smem latency per pass).
 template <int K>
 __device__ __forceinline__ void produce_halo_tma(const TcParams &p, const uint32_t *raw,
                                                  uint32_t a_stage, int ptid, int x0) {
@@ -352,27 +389,45 @@ __device__ __forceinline__ void produce_halo_tma(const TcParams &p, const uint32
   raw += c0 - (c0 & ~3);
   const int w = ptid % nwin, row0 = ptid / nwin, rstep = (kProdWarps * 32) / nwin;
   const int mshift = p.m_shift;
+  const uint32_t lbo = p.lbo_a;
+  constexpr int NR = K <= 4 ? 2 : 1;  // pixels per pass (register budget: 64 per producer thread)
 #pragma unroll 1
-  for (int row = row0; row < kHaloRows; row += rstep) {
-    const int hy = row / kHaloW, hx = row - (row / kHaloW) * kHaloW;
-    const uint32_t *src = raw + hy * bw + hx * nwin + w;
-    uint32_t xj[K];
+  for (int row = row0; row < kHaloRows; row += NR * rstep) {
+    const int row1 = row + rstep;
+    const bool two = NR == 2 && row1 < kHaloRows;
+    const int hy0 = row / kHaloW, hx0 = row - hy0 * kHaloW;
+    const int r1 = two ? row1 : row;
+    const int hy1 = r1 / kHaloW, hx1 = r1 - hy1 * kHaloW;
+    const uint32_t *src0 = raw + hy0 * bw + hx0 * nwin + w;
+    const uint32_t *src1 = raw + hy1 * bw + hx1 * nwin + w;
+    uint32_t x0j[K], x1j[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) xj[j] = src[j * fstride];
+    for (int j = 0; j < K; ++j) {
+      x0j[j] = src0[j * fstride];
+      x1j[j] = NR == 2 ? src1[j * fstride] : 0u;
+    }
     uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    agg_word_k<K>(o, xj, mshift);
-    const uint32_t dst = a_stage + (uint32_t)(2 * w) * p.lbo_a + (uint32_t)row * 16u;
-    ptx::st_shared_v4(dst, o[0], o[1], o[2], o[3]);
-    ptx::st_shared_v4(dst + p.lbo_a, o[4], o[5], o[6], o[7]);
+    if (mshift == 1 || K == 1) agg_word_m1<K>(o, x0j); else agg_word_k<K>(o, x0j, mshift);
+    const uint32_t dst0 = a_stage + (uint32_t)(2 * w) * lbo + (uint32_t)row * 16u;
+    ptx::st_shared_v4(dst0, o[0], o[1], o[2], o[3]);
+    ptx::st_shared_v4(dst0 + lbo, o[4], o[5], o[6], o[7]);
+    if (two) {
+      uint32_t o1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (mshift == 1 || K == 1) agg_word_m1<K>(o1, x1j); else agg_word_k<K>(o1, x1j, mshift);
+      const uint32_t dst1 = a_stage + (uint32_t)(2 * w) * lbo + (uint32_t)row1 * 16u;
+      ptx::st_shared_v4(dst1, o1[0], o1[1], o1[2], o1[3]);
+      ptx::st_shared_v4(dst1 + lbo, o1[4], o1[5], o1[6], o1[7]);
+    }
   }
 }
 
-__device__ __forceinline__ int floor_div32(int v) { return v >= 0 ? (v >> 5) : -((31 - v) >> 5); }
-
 // The raw box holds words [c0w, c0w + 8) of each halo row (OOB words are zero, and
 // so are the bits past W*C_in of a row), so pixel xi sits at box bit
-// (xi * C_in - 32 c0w) >= 0 and never straddles past word 7.
-template <int K>
+// (xi * C_in - 32 c0w) >= 0 and never straddles past word 7.  Only the first
+// 16-B chunk (channels 0..7) of a halo row changes per group; chunk 1 (channels
+// 8..15: zeros, or the bias 1.0 when C_in == 8) is written once per A stage by
+// h16_init_stages.  CIN4: C_in <= 4, channels 4..7 of chunk 0 hold only the bias.
+template <int K, bool CIN4>
 __device__ __forceinline__ void produce_h16_tma(const TcParams &p, const uint32_t *raw,
                                                 uint32_t a_stage, int ptid, int x0) {
   const int Cin = p.Cin, bw = p.raw_bw, fstride = kHaloH * p.raw_bw;
@@ -381,31 +436,70 @@ __device__ __forceinline__ void produce_h16_tma(const TcParams &p, const uint32_
   uint32_t one_lo, one_hi, c8;
   h16_bias_slot(Cin, one_lo, one_hi, c8);
   const int mshift = p.m_shift;
+  constexpr int RSTEP = kProdWarps * 32;
+  constexpr int NR = K <= 4 ? 2 : 1;  // pixels per pass (register budget: 64 per producer thread)
 #pragma unroll 1
-  for (int row = ptid; row < kHaloRows; row += kProdWarps * 32) {
-    const int hy = row / kHaloW, hx = row - (row / kHaloW) * kHaloW;
-    const int bitoff = (x0 + hx - p.pad) * Cin - c0w * 32;
-    const uint32_t *src = raw + hy * bw + (bitoff >> 5);
-    const int sh = bitoff & 31;
-    uint32_t lo = one_lo, hi = one_hi;
+  for (int row = ptid; row < kHaloRows; row += NR * RSTEP) {
+    const int row1 = row + RSTEP;
+    const bool two = NR == 2 && row1 < kHaloRows;
+    const int r1 = two ? row1 : row;
+    const int hy0 = row / kHaloW, hx0 = row - hy0 * kHaloW;
+    const int hy1 = r1 / kHaloW, hx1 = r1 - hy1 * kHaloW;
+    const int b0 = (x0 + hx0 - p.pad) * Cin - c0w * 32, b1 = (x0 + hx1 - p.pad) * Cin - c0w * 32;
+    const uint32_t *s0 = raw + hy0 * bw + (b0 >> 5), *s1 = raw + hy1 * bw + (b1 >> 5);
+    const int sh0 = b0 & 31, sh1 = b1 & 31;
+    uint32_t a0[K], a1[K], c0[K], c1[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j)
-      h16_acc(lo, hi, __funnelshift_r(src[j * fstride], src[j * fstride + 1], sh) & cmask, mshift * j);
-    store_h16_row(a_stage + (uint32_t)row * 16u, p.lbo_a, lo, hi, c8);
+    for (int j = 0; j < K; ++j) {
+      a0[j] = s0[j * fstride];
+      a1[j] = s0[j * fstride + 1];
+      c0[j] = NR == 2 ? s1[j * fstride] : 0u;
+      c1[j] = NR == 2 ? s1[j * fstride + 1] : 0u;
+    }
+    uint32_t lo0 = one_lo, hi0 = one_hi, lo1 = one_lo, hi1 = one_hi;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const uint32_t bits0 = __funnelshift_r(a0[j], a1[j], sh0) & cmask;
+      const uint32_t bits1 = __funnelshift_r(c0[j], c1[j], sh1) & cmask;
+      if (CIN4) {
+        lo0 |= ((bits0 * 0x204081u) & 0x01010101u) << (mshift * j);
+        lo1 |= ((bits1 * 0x204081u) & 0x01010101u) << (mshift * j);
+      } else {
+        h16_acc(lo0, hi0, bits0, mshift * j);
+        h16_acc(lo1, hi1, bits1, mshift * j);
+      }
+    }
+    const uint32_t d0 = a_stage + (uint32_t)row * 16u;
+    ptx::st_shared_v4(d0, u8x2_to_f16x2(lo0, 0x5140u), u8x2_to_f16x2(lo0, 0x7362u),
+                      u8x2_to_f16x2(hi0, 0x5140u), u8x2_to_f16x2(hi0, 0x7362u));
+    if (two) {
+      const uint32_t d1 = a_stage + (uint32_t)row1 * 16u;
+      ptx::st_shared_v4(d1, u8x2_to_f16x2(lo1, 0x5140u), u8x2_to_f16x2(lo1, 0x7362u),
+                        u8x2_to_f16x2(hi1, 0x5140u), u8x2_to_f16x2(hi1, 0x7362u));
+    }
   }
 }
 
-// TMA producer pipeline: producer thread 0 keeps nraw raw-halo loads in flight;
-// all 96 producer threads aggregate stage `it % nraw` into A stage `it % nstages`.
-template <int PATH, int K>
-__device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sbase,
-                                                  const uint8_t *smem, uint32_t bar_a_full,
-                                                  uint32_t bar_a_empty, uint32_t bar_raw, int cid,
-                                                  int ncl, uint32_t rank, uint32_t lane,
-                                                  int ptid) {
-  const uint32_t ns = (uint32_t)p.nstages, nr = (uint32_t)p.nraw;
-  int ipair = cid, ik = 0;  // next (pair, group) whose raw halo is to be loaded
-  auto issue = [&](uint32_t slot) {
+// chunk 1 of every halo row of every A stage (constant for the whole kernel)
+__device__ __forceinline__ void h16_init_stages(const TcParams &p, uint32_t sbase, int ptid) {
+  uint32_t one_lo, one_hi, c8;
+  h16_bias_slot(p.Cin, one_lo, one_hi, c8);
+  for (int i = ptid; i < p.nstages * kHaloRows; i += kProdWarps * 32) {
+    const int st = i / kHaloRows, row = i - st * kHaloRows;
+    ptx::st_shared_v4(sbase + p.off_a + st * p.a_stage_bytes + p.lbo_a + (uint32_t)row * 16u, c8,
+                      0u, 0u, 0u);
+  }
+}
+
+// Raw-halo TMA loader, run by one lane of the MMA warp of each CTA: keeps nraw
+// raw-halo loads (K frames x 18 halo rows of this CTA's tile) in flight; slot r is
+// refilled once the producer warps have arrived on raw_empty[r].
+struct RawLoader {
+  int ipair, ik;  // next (pair, group) to load
+  uint32_t n;     // loads issued
+  __device__ __forceinline__ void issue(const TcParams &p, uint32_t sbase, uint32_t bar_raw,
+                                        int ncl, uint32_t rank) {
+    const uint32_t slot = n % (uint32_t)p.nraw;
     int b, y0, x0;
     bool tok;
     tile_origin(p, 2 * ipair + (int)rank, b, y0, x0, tok);
@@ -413,14 +507,45 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
     const uint32_t bar = bar_raw + 8 * slot;
     ptx::mbar_arrive_expect_tx(bar, p.raw_box_bytes);
     ptx::tma_load_4d(sbase + p.off_raw + slot * p.raw_stage_bytes, &p.tmap, c0, y0 - p.pad, b,
-                     ik * K, bar);
+                     ik * p.K, bar);
     if (++ik == p.G) {
       ik = 0;
       ipair += ncl;
     }
-  };
-  if (ptid == 0)
-    for (uint32_t r = 0; r < nr && ipair < p.num_pairs; ++r) issue(r);
+    ++n;
+  }
+  __device__ __forceinline__ bool more(const TcParams &p) const { return ipair < p.num_pairs; }
+  // prime the ring
+  __device__ __forceinline__ void start(const TcParams &p, uint32_t sbase, uint32_t bar_raw, int cid,
+                                        int ncl, uint32_t rank) {
+    ipair = cid;
+    ik = 0;
+    n = 0;
+    for (int r = 0; r < p.nraw && more(p); ++r) issue(p, sbase, bar_raw, ncl, rank);
+  }
+  // after consumption `it` of slot it % nraw: wait until every producer warp is done
+  // with it, then refill the slot
+  __device__ __forceinline__ void refill(const TcParams &p, uint32_t sbase, uint32_t bar_raw,
+                                         uint32_t bar_raw_empty, uint32_t it, int ncl, uint32_t rank) {
+    if (!more(p)) return;
+    const uint32_t nr = (uint32_t)p.nraw;
+    ptx::mbar_wait(bar_raw_empty + 8 * (it % nr), (it / nr) & 1u);
+    issue(p, sbase, bar_raw, ncl, rank);
+  }
+};
+
+// TMA producer pipeline: all 96 producer threads aggregate raw stage `it % nraw`
+// into A stage `it % nstages`; each warp then releases the raw stage (local
+// raw_empty barrier, refilled by the MMA warp's loader) and arrives on the pair's
+// A-full barrier in CTA 0.
+template <int PATH, int K>
+__device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sbase,
+                                                  const uint8_t *smem, uint32_t bar_a_full,
+                                                  uint32_t bar_a_empty, uint32_t bar_raw,
+                                                  uint32_t bar_raw_empty, int cid, int ncl,
+                                                  uint32_t rank, uint32_t lane, int ptid) {
+  const uint32_t ns = (uint32_t)p.nstages, nr = (uint32_t)p.nraw;
+  if (PATH == PATH_H16) h16_init_stages(p, sbase, ptid);  // fenced with the first stage
   uint32_t it = 0;
   for (int pair = cid; pair < p.num_pairs; pair += ncl) {
     int b, y0, x0;
@@ -437,15 +562,17 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
       const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
       if (PATH == PATH_HALO)
         produce_halo_tma<K>(p, raw, a_stage, ptid, x0);
+      else if (p.Cin <= 4)
+        produce_h16_tma<K, true>(p, raw, a_stage, ptid, x0);
       else
-        produce_h16_tma<K>(p, raw, a_stage, ptid, x0);
+        produce_h16_tma<K, false>(p, raw, a_stage, ptid, x0);
       ptx::fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(bar_a_full + 8 * s, 0);
-      ptx::named_bar_sync(2, kProdWarps * 32);  // every producer is done with raw stage r
+      if (lane == 0) {
+        ptx::mbar_arrive_local(bar_raw_empty + 8 * r);  // this warp's smem reads of raw stage r are done
+        ptx::mbar_arrive_cluster_cta(bar_a_full + 8 * s, 0);
+      }
       if (ptid == 0) trace_mark(p, it, TR_PROD_DONE);
-      if (ptid == 0 && ipair < p.num_pairs) issue(r);
-      if (ptid == 0) trace_mark(p, it, TR_PROD_ISSUED);
     }
   }
 }
@@ -468,7 +595,7 @@ __device__ __forceinline__ void producer_role(const TcParams &p, uint32_t sbase,
         produce_h16<K>(p, tile, k, a_stage, ptid);
       ptx::fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(bar_a_full + 8 * s, 0);
+      if (lane == 0) ptx::mbar_arrive_cluster_cta(bar_a_full + 8 * s, 0);
     }
   }
 }
@@ -640,6 +767,203 @@ __device__ __forceinline__ void planes_add4(uint32_t *P, uint32_t s0, uint32_t s
   TAC_LOP3(v, s0, s1, s2, 0xE8);
   const uint32_t u2 = u ^ s3, c = u & s3;
   planes_add3(P, u2, v ^ c, v & c);
+}
+
+// --- specialised subtract-reset epilogue (NS LIF steps per group) -------------
+// State U = V - v_th (drive Y' = Y + (decay - 1) v_th, folded into the bias):
+//   U <- decay U + Y'                      FFMA2 (two neurons)
+//   no-spike bit = sign(U)  -> shift register  nsp = (nsp << 1) | (U >> 31)   SHF
+//   f = sat(U 2^127 + 1) = [U >= 0]        FFMA.SAT (exactly 0 or 1, ftz)
+//   U <- U - v_th f                        FFMA2 (exact for f in {0, 1})
+// Channels are visited from the highest to the lowest so that channel c of the
+// thread's word lands at bit c after NCH shifts: no per-bit masks, no folding.
+// (U = -0 would be a tie V == v_th read as "no spike" by the sign but reset by
+// f; U = V - v_th is never -0 in round-to-nearest unless both addends are -0.)
+__device__ __forceinline__ uint32_t shreg(uint32_t acc, float u) {
+  return __funnelshift_l(__float_as_uint(u), acc, 1);  // (acc << 1) | sign(u)
+}
+
+template <int NS>
+__device__ __forceinline__ void lif_pair_sr(float2 &u, float2 y, float2 dec2, float2 nth2,
+                                            uint32_t (&nsp)[NS]) {
+#pragma unroll
+  for (int j = 0; j < NS; ++j) {
+    u = __ffma2_rn(dec2, u, y);
+    nsp[j] = shreg(nsp[j], u.y);
+    nsp[j] = shreg(nsp[j], u.x);
+    const float2 f = make_float2(sat_spike(u.x), sat_spike(u.y));
+    u = __ffma2_rn(nth2, f, u);
+  }
+}
+
+template <int NCH, int PATH, int NPART, int NS>
+__device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, uint32_t tmem_base,
+                                            uint32_t bar_t_full, uint32_t bar_t_empty, int cid,
+                                            int ncl, uint32_t rank, uint32_t warp, uint32_t lane) {
+  static_assert(NCH <= 32, "one spike word per thread");
+  constexpr int NCHUNK = NCH / 8;
+  constexpr bool F16 = PATH == PATH_H16;
+  constexpr bool LD32 = false;  // F16 && NCH == 32 (one 32-column load) spills at 104 regs
+  constexpr int NBUF = (NPART == 2 || (F16 && NS <= 4)) ? 2 : 1;  // TMEM prefetch depth (registers)
+  const float *sc = reinterpret_cast<const float *>(smem + p.off_scale);
+  const int e = (int)warp;
+  const int quad = (int)(warp & 3);
+  const int half = e >> 2;
+  const int g = quad * 4 + (int)(lane >> 3);
+  const int c = (int)(lane & 7);
+  const int co_base = half * NCH;
+  const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+  const float vth = p.v_th;
+  const float2 dec2 = make_float2(p.decay, p.decay), nth2 = make_float2(-vth, -vth);
+  const int G = p.G, Cout = p.Cout, nwo = p.nwo;
+  const long long out_st = p.out_st;
+  const uint32_t chmask = NCH >= 32 ? 0xFFFFFFFFu : ((1u << NCH) - 1u);
+  const bool pooled = p.pool == 2;
+  const bool active_half = co_base < Cout;
+  // CTA 0's TMEM-empty barriers, mapped once
+  const uint32_t t_empty0 = ptx::mapa_cluster(bar_t_empty, 0), t_empty1 = ptx::mapa_cluster(bar_t_empty + 8, 0);
+  uint32_t it = 0;
+  for (int pair = cid; pair < p.num_pairs; pair += ncl) {
+    const int tile = 2 * pair + (int)rank;
+    int b, y0, x0;
+    bool tok;
+    tile_origin(p, tile, b, y0, x0, tok);
+    const int y = y0 + g, x = x0 + c;
+    const bool valid = tok && y < p.Ho && x < p.Wo;
+    const long long vbase = (((long long)b * p.Ho + y) * p.Wo + x) * Cout + co_base;
+    const int yo = pooled ? (y >> 1) : y, xo = pooled ? (x >> 1) : x;
+    const bool store_lane = valid && active_half && (!pooled || (lane & 9) == 0);
+    const uint32_t vmask = (valid && active_half) ? chmask : 0u;
+    // this lane's output word (NCH == 32) or the word holding its bit field (NCH < 32)
+    const long long obit = (long long)xo * Cout + co_base;
+    uint32_t *optr = p.out + (long long)b * p.out_sb + (long long)yo * p.wpr_out +
+                     (NCH >= 32 ? (long long)xo * nwo + half : (obit >> 5));
+    const int osh = NCH >= 32 ? 0 : (int)(obit & 31);
+    float2 U[NCH / 2];
+#pragma unroll
+    for (int cc = 0; cc < NCH; cc += 2) {
+      float v0 = 0.f, v1 = 0.f;
+      if (p.v_init && valid) {
+        if (co_base + cc < Cout) v0 = __ldg(p.v_init + vbase + cc);
+        if (co_base + cc + 1 < Cout) v1 = __ldg(p.v_init + vbase + cc + 1);
+      }
+      U[cc / 2] = make_float2(v0 - vth, v1 - vth);
+    }
+    uint32_t planes[kPlanes];
+#pragma unroll
+    for (int pl = 0; pl < kPlanes; ++pl) planes[pl] = 0u;
+    int steps_acc = 0;
+    for (int k = 0; k < G; ++k, ++it) {
+      const uint32_t acc = it % kAccs, aph = (it / kAccs) & 1u;
+      ptx::mbar_wait(bar_t_full + 8 * acc, aph);
+      ptx::tc_fence_after();
+      if (e == 0 && lane == 0) trace_mark(p, it, TR_EPI_FULL);
+      uint32_t nsp[NS];
+#pragma unroll
+      for (int j = 0; j < NS; ++j) nsp[j] = 0u;
+      const uint32_t tcol = tmem_base + lane_addr + acc * p.n_total + (uint32_t)co_base;
+      if (LD32) {
+        uint32_t d[32];
+        ptx::tmem_ld32(tcol, d);
+        ptx::tmem_wait_ld32(d);
+#pragma unroll
+        for (int q = NCH / 2 - 1; q >= 0; --q)
+          lif_pair_sr<NS>(U[q], make_float2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1])),
+                          dec2, nth2, nsp);
+      } else {
+        uint32_t d[NBUF][2][8];  // [buffer][hi/lo][col]
+        ptx::tmem_ld8(tcol + (NCHUNK - 1) * 8, d[0][0]);
+        if (!F16) ptx::tmem_ld8(tcol + p.Cout_pad + (NCHUNK - 1) * 8, d[0][1]);
+        ptx::tmem_wait_ld_dep(d[0][0], d[0][1]);
+#pragma unroll
+        for (int i = 0; i < NCHUNK; ++i) {
+          const int ch = NCHUNK - 1 - i;
+          const int cur = NBUF == 2 ? (i & 1) : 0, nxt = NBUF == 2 ? (cur ^ 1) : 0;
+          if (NBUF == 2 && ch > 0) {  // prefetch the next lower 8 columns
+            ptx::tmem_ld8(tcol + (ch - 1) * 8, d[nxt][0]);
+            if (!F16) ptx::tmem_ld8(tcol + p.Cout_pad + (ch - 1) * 8, d[nxt][1]);
+          }
+          float yv[8];
+          if (F16) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) yv[q] = __uint_as_float(d[cur][0][q]);
+          } else {
+            combine8(p, sc, co_base + ch * 8, d[cur][0], d[cur][1], yv);
+          }
+#pragma unroll
+          for (int q = 3; q >= 0; --q)
+            lif_pair_sr<NS>(U[ch * 4 + q], make_float2(yv[2 * q], yv[2 * q + 1]), dec2, nth2, nsp);
+          if (ch > 0) {
+            if (NBUF == 1) {
+              ptx::tmem_ld8(tcol + (ch - 1) * 8, d[0][0]);
+              if (!F16) ptx::tmem_ld8(tcol + p.Cout_pad + (ch - 1) * 8, d[0][1]);
+            }
+            ptx::tmem_wait_ld_dep(d[nxt][0], d[nxt][1]);
+          }
+        }
+      }
+      // accumulator consumed: hand TMEM back to the MMA issuer
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_remote_relaxed(acc ? t_empty1 : t_empty0);
+      if (e == 0 && lane == 0) trace_mark(p, it, TR_EPI_RELEASED);
+
+      uint32_t spk[NS];
+#pragma unroll
+      for (int j = 0; j < NS; ++j) spk[j] = ~nsp[j] & vmask;
+      // per-lane bit-sliced spike counters (pre-pool, valid pixels only)
+      if (NS == 1) {
+        uint32_t cy = spk[0];
+#pragma unroll
+        for (int pl = 0; pl < kPlanes; ++pl) {
+          const uint32_t t = planes[pl] & cy;
+          planes[pl] ^= cy;
+          cy = t;
+        }
+      } else if (NS == 2) {
+        planes_add3(planes, spk[0] ^ spk[NS - 1], spk[0] & spk[NS - 1], 0u);
+      } else {
+#pragma unroll
+        for (int j = 0; j + 3 < NS; j += 4) planes_add4(planes, spk[j], spk[j + 1], spk[j + 2], spk[j + 3]);
+      }
+      // in-warp 2x2 OR-pool (all shuffles first), then branch-free packed stores of
+      // output steps t = k NS + j
+      uint32_t pw[NS];
+#pragma unroll
+      for (int j = 0; j < NS; ++j) pw[j] = spk[j] | (pooled ? __shfl_xor_sync(0xFFFFFFFFu, spk[j], 1) : 0u);
+#pragma unroll
+      for (int j = 0; j < NS; ++j) pw[j] |= pooled ? __shfl_xor_sync(0xFFFFFFFFu, pw[j], 8) : 0u;
+#pragma unroll
+      for (int j = 0; j < NS; ++j) {
+        if (NCH >= 32) {
+          ptx::st_global_pred(optr + j * out_st, pw[j], store_lane);
+        } else if (store_lane && pw[j]) {
+          atomicOr(optr + j * out_st, pw[j] << osh);
+        }
+      }
+      optr += NS * out_st;
+      steps_acc += NS;
+      if (p.counts && (steps_acc + NS > (1 << kPlanes) - 1 || k == G - 1)) {
+        if (tok) {
+          uint32_t pw[kPlanes][1];
+#pragma unroll
+          for (int pl = 0; pl < kPlanes; ++pl) pw[pl][0] = planes[pl];
+          flush_counts<1>(p, pw, b, co_base, NCH, lane);
+        }
+#pragma unroll
+        for (int pl = 0; pl < kPlanes; ++pl) planes[pl] = 0u;
+        steps_acc = 0;
+      }
+      if (e == 0 && lane == 0) trace_mark(p, it, TR_EPI_DONE);
+    }
+    if (p.v_final && valid) {
+#pragma unroll
+      for (int cc = 0; cc < NCH; cc += 2) {
+        if (co_base + cc < Cout) p.v_final[vbase + cc] = U[cc / 2].x + vth;
+        if (co_base + cc + 1 < Cout) p.v_final[vbase + cc + 1] = U[cc / 2].y + vth;
+      }
+    }
+  }
 }
 
 // NS > 0: subtract reset with NS LIF steps per group (specialised hot path);
@@ -870,6 +1194,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
   const uint32_t bar_t_empty = bar_t_full + 8 * kAccs;
   const uint32_t bar_w = bar_t_empty + 8 * kAccs;
   const uint32_t bar_raw = bar_w + 8;
+  const uint32_t bar_raw_empty = bar_raw + 8 * kMaxRaw;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + p.off_bar + 8 * kNumBars);
   float *sc = reinterpret_cast<float *>(smem + p.off_scale);
 
@@ -883,7 +1208,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
       ptx::mbar_init(bar_t_empty + 8 * a, 2 * kEpiWarps);
     }
     ptx::mbar_init(bar_w, 1);
-    for (int r = 0; r < kMaxRaw; ++r) ptx::mbar_init(bar_raw + 8 * r, 1);
+    for (int r = 0; r < kMaxRaw; ++r) {
+      ptx::mbar_init(bar_raw + 8 * r, 1);
+      ptx::mbar_init(bar_raw_empty + 8 * r, kProdWarps);
+    }
     ptx::fence_mbar_init();
     if (p.use_tma) ptx::prefetch_tmap(&p.tmap);
     // resident weights: this CTA's int8 slice of every tap
@@ -916,7 +1244,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
   // sits at the top of its role branch so ptxas sees the register regions.
   constexpr uint32_t kLaunchRegs = NPART == 2 ? 168 : 96;  // ptxas allocation at launch
   constexpr uint32_t kRegsLow = NPART == 2 ? 96 : 64, kRegsHigh = NPART == 2 ? 200 : 104;
-  static_assert(128 * kRegsLow + 32 * epi_warps(NPART) * kRegsHigh <=
+  static_assert(32 * (1 + kProdWarps) * kRegsLow + 32 * epi_warps(NPART) * kRegsHigh <=
                     kernel_threads(NPART) * kLaunchRegs, "register budget");
   const uint32_t kMmaWarp = (uint32_t)kEpiWarps;
   if (warp >= kMmaWarp) {
@@ -926,6 +1254,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
       // The whole warp runs the loop converged (warp-uniform descriptors, no
       // waterfall); one elected lane issues.  Descriptors are built once and only
       // their 14-bit start-address field (addr >> 4, always < 2^14) is advanced.
+      // Lane 0 also runs this CTA's raw-halo TMA loader (RawLoader): after the MMAs of
+      // group `it` (CTA 0) -- or as its only job (CTA 1) -- it refills the raw slot the
+      // producers just released.
+      RawLoader loader;
+      if (p.use_tma && lane == 0) loader.start(p, sbase, bar_raw, cid, ncl, rank);
+      if (rank != 0 && p.use_tma && lane == 0) {
+        const uint32_t total = (uint32_t)((p.num_pairs - cid + ncl - 1) / ncl) * (uint32_t)p.G;
+        for (uint32_t it = 0; it < total; ++it) loader.refill(p, sbase, bar_raw, bar_raw_empty, it, ncl, rank);
+      }
       if (rank == 0) {
         const uint32_t idesc = ptx::idesc_i8(256, p.n_total);
         const uint32_t nhb16 = p.lbo_b >> 4;                        // B rows of this CTA x 16 B
@@ -975,6 +1312,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
             }
             __syncwarp();
             if (lane == 0) trace_mark(p, it, TR_MMA_ISSUED);
+            if (p.use_tma && lane == 0) loader.refill(p, sbase, bar_raw, bar_raw_empty, it, ncl, rank);
+            __syncwarp();
           }
         }
       }
@@ -984,10 +1323,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
       const int ptid = (int)(threadIdx.x - 32 * (kMmaWarp + 1));
       if (p.use_tma) {
         switch (p.K) {
-          case 1: producer_role_tma<PATH, 1>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, cid, ncl, rank, lane, ptid); break;
-          case 2: producer_role_tma<PATH, 2>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, cid, ncl, rank, lane, ptid); break;
-          case 4: producer_role_tma<PATH, 4>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, cid, ncl, rank, lane, ptid); break;
-          default: producer_role_tma<PATH, 8>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, cid, ncl, rank, lane, ptid); break;
+          case 1: producer_role_tma<PATH, 1>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
+          case 2: producer_role_tma<PATH, 2>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
+          case 4: producer_role_tma<PATH, 4>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
+          default: producer_role_tma<PATH, 8>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
         }
       } else {
         switch (p.K) {
@@ -1003,10 +1342,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
     // ================================ epilogue =================================
     const int ns = p.reset == 0 ? p.nsteps : 0;
     switch (ns) {
-      case 1: epilogue_role<NCH, PATH, NPART, 1>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      case 2: epilogue_role<NCH, PATH, NPART, 2>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      case 4: epilogue_role<NCH, PATH, NPART, 4>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      case 8: epilogue_role<NCH, PATH, NPART, 8>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 1: epilogue_sr<NCH, PATH, NPART, 1>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 2: epilogue_sr<NCH, PATH, NPART, 2>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 4: epilogue_sr<NCH, PATH, NPART, 4>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 8: epilogue_sr<NCH, PATH, NPART, 8>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
       default: epilogue_role<NCH, PATH, NPART, 0>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
     }
     }
@@ -1186,7 +1525,8 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
               void *stream, int *launches) {
   // TMA raw-halo producer when the packed input is a legal 4-D tensor-map view
   // (16-B aligned base and strides) and the plan fits in shared memory
-  const bool tma_layout = (lp.wpr_in * 4) % 16 == 0 && (lp.in_sb * 4) % 16 == 0 &&
+  static const bool no_tma = [] { const char *e = std::getenv("TACSNN_NO_TMA"); return e && *e == '1'; }();
+  const bool tma_layout = !no_tma && (lp.wpr_in * 4) % 16 == 0 && (lp.in_sb * 4) % 16 == 0 &&
                           (lp.in_st * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(lp.in) % 16) == 0;
   Geometry g = geometry(d, tma_layout);
   PFN_cuTensorMapEncodeTiled_v12000 encode = g.use_tma ? tensor_map_encoder() : nullptr;

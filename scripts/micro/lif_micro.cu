@@ -93,6 +93,40 @@ template <int C0> __device__ __forceinline__ void v6(float2 &u, float2 y, float2
   acc = or_bit<1u << (23 + ((C0 + 1) % 7))>(acc, f.y);
 }
 
+
+__device__ __forceinline__ uint32_t shreg(uint32_t acc, float u) {  // (acc << 1) | sign(u)
+  uint32_t d; asm("shf.l.wrap.b32 %0, %1, %2, 1;" : "=r"(d) : "r"(__float_as_uint(u)), "r"(acc)); return d;
+}
+// variant 7: FFMA2 update, SAT x2, FFMA2 reset, funnel-shift sign bits
+template <int C0> __device__ __forceinline__ void v7(float2 &u, float2 y, float2 dec2, float2 nth2, uint32_t &acc) {
+  u = __ffma2_rn(dec2, u, y);
+  acc = shreg(acc, u.x); acc = shreg(acc, u.y);
+  const float2 f = make_float2(sat_spike(u.x), sat_spike(u.y));
+  u = __ffma2_rn(nth2, f, u);
+}
+// variant 8: scalar update (uniform beta), SAT, FFMA2 reset, funnel
+template <int C0> __device__ __forceinline__ void v8(float2 &u, float2 y, float2 dec2, float2 nth2, uint32_t &acc) {
+  u.x = fmaf(dec2.x, u.x, y.x); u.y = fmaf(dec2.x, u.y, y.y);
+  acc = shreg(acc, u.x); acc = shreg(acc, u.y);
+  const float2 f = make_float2(sat_spike(u.x), sat_spike(u.y));
+  u = __ffma2_rn(nth2, f, u);
+}
+// variant 9: all scalar (uniform beta / -th), SAT, funnel
+template <int C0> __device__ __forceinline__ void v9(float2 &u, float2 y, float2 dec2, float2 nth2, uint32_t &acc) {
+  u.x = fmaf(dec2.x, u.x, y.x); u.y = fmaf(dec2.x, u.y, y.y);
+  acc = shreg(acc, u.x); acc = shreg(acc, u.y);
+  const float f0 = sat_spike(u.x), f1 = sat_spike(u.y);
+  u.x = fmaf(nth2.x, f0, u.x); u.y = fmaf(nth2.x, f1, u.y);
+}
+
+// variant 10: FFMA2 update, SAT x2, scalar (uniform) resets, funnel
+template <int C0> __device__ __forceinline__ void v10(float2 &u, float2 y, float2 dec2, float2 nth2, uint32_t &acc) {
+  u = __ffma2_rn(dec2, u, y);
+  acc = shreg(acc, u.y); acc = shreg(acc, u.x);
+  const float f0 = sat_spike(u.x), f1 = sat_spike(u.y);
+  u.x = fmaf(nth2.x, f0, u.x); u.y = fmaf(nth2.x, f1, u.y);
+}
+
 template <int V>
 __global__ void __launch_bounds__(512, 1) bench(const float *ys, uint32_t *sink, int groups, long long *cyc, float beta, float th) {
   float2 u[16];
@@ -100,11 +134,14 @@ __global__ void __launch_bounds__(512, 1) bench(const float *ys, uint32_t *sink,
   const float2 dec2 = make_float2(beta, beta), nth2 = make_float2(-th, -th);
   uint32_t x = 0;
   const float *yp = ys + (threadIdx.x & 31) * 32;
+  uint32_t ybits[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) ybits[i] = __float_as_uint(yp[i]);
   long long t0 = clock64();
   for (int g = 0; g < groups; ++g) {
     float yv[32];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) yv[i] = yp[i] + (float)(g & 7) * 0.01f;
+    for (int i = 0; i < 32; ++i) yv[i] = __uint_as_float(ybits[i] ^ (uint32_t)(g & 7));  // 1 ALU op / neuron / group
     uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -141,6 +178,30 @@ __global__ void __launch_bounds__(512, 1) bench(const float *ys, uint32_t *sink,
             CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15)
 #undef CASE
           }
+        } else if (V == 7) {
+          switch (c % 16) {
+#define CASE(k) case k: v7<(2 * k) % 32>(u[c], y, dec2, nth2, w[j]); break;
+            CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15)
+#undef CASE
+          }
+        } else if (V == 8) {
+          switch (c % 16) {
+#define CASE(k) case k: v8<(2 * k) % 32>(u[c], y, dec2, nth2, w[j]); break;
+            CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15)
+#undef CASE
+          }
+        } else if (V == 9) {
+          switch (c % 16) {
+#define CASE(k) case k: v9<(2 * k) % 32>(u[c], y, dec2, nth2, w[j]); break;
+            CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15)
+#undef CASE
+          }
+        } else if (V == 10) {
+          switch (c % 16) {
+#define CASE(k) case k: v10<(2 * k) % 32>(u[c], y, dec2, nth2, w[j]); break;
+            CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15)
+#undef CASE
+          }
         } else if (V == 5) {
           switch (c % 16) {
 #define CASE(k) case k: v5<(2 * k) % 32>(u[c], y, dec2, nth2, w[j]); break;
@@ -167,10 +228,10 @@ __global__ void __launch_bounds__(512, 1) bench(const float *ys, uint32_t *sink,
 int main() {
   const int groups = 2000, blocks = 148, threads = 512;
   float *ys; uint32_t *sink; long long *cyc;
-  cudaMalloc(&ys, 32 * 32 * 4); cudaMalloc(&sink, blocks * threads * 4); cudaMalloc(&cyc, blocks * 8);
-  float h[1024]; for (int i = 0; i < 1024; ++i) h[i] = 0.05f + 0.3f * ((i * 37) % 101) / 101.f;
+  cudaMalloc(&ys, 32 * 32 * 4 * 8); cudaMalloc(&sink, blocks * threads * 4); cudaMalloc(&cyc, blocks * 8);
+  static float h[8192]; for (int i = 0; i < 8192; ++i) h[i] = 0.05f + 0.3f * ((i * 37) % 101) / 101.f;
   cudaMemcpy(ys, h, sizeof h, cudaMemcpyHostToDevice);
-  for (int v = 0; v < 7; ++v) {
+  for (int v = 0; v < 11; ++v) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
       cudaEventRecord(a);
@@ -180,6 +241,10 @@ int main() {
       if (v == 3) bench<3><<<blocks, threads>>>(ys, sink, groups, cyc, 0.9f, 1.f);
       if (v == 4) bench<4><<<blocks, threads>>>(ys, sink, groups, cyc, 0.9f, 1.f);
       if (v == 6) bench<6><<<blocks, threads>>>(ys, sink, groups, cyc, 0.9f, 1.f);
+      if (v == 10) bench<10><<<blocks, threads>>>(ys, sink, groups, cyc, 0.9f, 1.f);
+      if (v == 7) bench<7><<<blocks, threads>>>(ys, sink, groups, cyc, 0.9f, 1.f);
+      if (v == 8) bench<8><<<blocks, threads>>>(ys, sink, groups, cyc, 0.9f, 1.f);
+      if (v == 9) bench<9><<<blocks, threads>>>(ys, sink, groups, cyc, 0.9f, 1.f);
       if (v == 5) bench<5><<<blocks, threads>>>(ys, sink, groups, cyc, 0.9f, 1.f);
       cudaEventRecord(b); cudaEventSynchronize(b);
       float ms; cudaEventElapsedTime(&ms, a, b);

@@ -1,4 +1,5 @@
 """Per-group role timeline of CTA 0 for one layer launch (debug; see tac_debug_set_trace).
+Needs a trace build: TACSNN_TRACE=1 python -m paper_2603_13810_b200.build --force.
 
     python scripts/trace_layer.py --layer 0 --B 256
 Prints, per group iteration, the producer / MMA / epilogue event times (us, relative).
