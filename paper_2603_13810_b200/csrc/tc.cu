@@ -796,6 +796,12 @@ __device__ __forceinline__ void lif_pair_sr(float2 &u, float2 y, float2 dec2, fl
   }
 }
 
+// UT (fp16 first-layer path with C_out = 128): the membrane state U lives in TMEM
+// columns [2 n_total, 2 n_total + 128) (the accumulators use 2 x 128), and is
+// streamed through registers 8 channels at a time -- 32 registers fewer per thread.
+template <int NCH, int PATH, int NPART>
+constexpr bool u_in_tmem() { return PATH == PATH_H16 && NPART == 4 && NCH == 32; }
+
 template <int NCH, int PATH, int NPART, int NS>
 __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, uint32_t tmem_base,
                                             uint32_t bar_t_full, uint32_t bar_t_empty, int cid,
@@ -803,6 +809,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
   static_assert(NCH <= 32, "one spike word per thread");
   constexpr int NCHUNK = NCH / 8;
   constexpr bool F16 = PATH == PATH_H16;
+  constexpr bool UT = u_in_tmem<NCH, PATH, NPART>();
   constexpr bool LD32 = false;  // F16 && NCH == 32 (one 32-column load) spills at 104 regs
   constexpr int NBUF = (NPART == 2 || (F16 && NS <= 4)) ? 2 : 1;  // TMEM prefetch depth (registers)
   const float *sc = reinterpret_cast<const float *>(smem + p.off_scale);
@@ -839,16 +846,24 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
     uint32_t *optr = p.out + (long long)b * p.out_sb + (long long)yo * p.wpr_out +
                      (NCH >= 32 ? (long long)xo * nwo + half : (obit >> 5));
     const int osh = NCH >= 32 ? 0 : (int)(obit & 31);
-    float2 U[NCH / 2];
+    float2 U[UT ? 1 : NCH / 2];
+    const uint32_t ucol = tmem_base + lane_addr + 2u * p.n_total + (uint32_t)co_base;
 #pragma unroll
-    for (int cc = 0; cc < NCH; cc += 2) {
-      float v0 = 0.f, v1 = 0.f;
-      if (p.v_init && valid) {
-        if (co_base + cc < Cout) v0 = __ldg(p.v_init + vbase + cc);
-        if (co_base + cc + 1 < Cout) v1 = __ldg(p.v_init + vbase + cc + 1);
+    for (int ch = 0; ch < NCHUNK; ++ch) {
+      uint32_t ub[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int cc = ch * 8 + q;
+        float v0 = 0.f;
+        if (p.v_init && valid && co_base + cc < Cout) v0 = __ldg(p.v_init + vbase + cc);
+        ub[q] = __float_as_uint(v0 - vth);
+        if (!UT) {
+          if (q & 1) U[UT ? 0 : cc / 2].y = v0 - vth; else U[UT ? 0 : cc / 2].x = v0 - vth;
+        }
       }
-      U[cc / 2] = make_float2(v0 - vth, v1 - vth);
+      if (UT) ptx::tmem_st8(ucol + ch * 8, ub);
     }
+    if (UT) ptx::tmem_wait_st();
     uint32_t planes[kPlanes];
 #pragma unroll
     for (int pl = 0; pl < kPlanes; ++pl) planes[pl] = 0u;
@@ -862,13 +877,32 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
 #pragma unroll
       for (int j = 0; j < NS; ++j) nsp[j] = 0u;
       const uint32_t tcol = tmem_base + lane_addr + acc * p.n_total + (uint32_t)co_base;
-      if (LD32) {
+      if (UT) {
+        // one chunk at a time: Y and U in, LIF, U out
+#pragma unroll
+        for (int i = 0; i < NCHUNK; ++i) {
+          const int ch = NCHUNK - 1 - i;
+          uint32_t dy[8], du[8];
+          ptx::tmem_ld8(tcol + ch * 8, dy);
+          ptx::tmem_ld8(ucol + ch * 8, du);
+          ptx::tmem_wait_ld_dep(dy, du);
+#pragma unroll
+          for (int q = 3; q >= 0; --q) {
+            float2 u = make_float2(__uint_as_float(du[2 * q]), __uint_as_float(du[2 * q + 1]));
+            lif_pair_sr<NS>(u, make_float2(__uint_as_float(dy[2 * q]), __uint_as_float(dy[2 * q + 1])),
+                            dec2, nth2, nsp);
+            du[2 * q] = __float_as_uint(u.x);
+            du[2 * q + 1] = __float_as_uint(u.y);
+          }
+          ptx::tmem_st8(ucol + ch * 8, du);
+        }
+      } else if (LD32) {
         uint32_t d[32];
         ptx::tmem_ld32(tcol, d);
         ptx::tmem_wait_ld32(d);
 #pragma unroll
         for (int q = NCH / 2 - 1; q >= 0; --q)
-          lif_pair_sr<NS>(U[q], make_float2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1])),
+          lif_pair_sr<NS>(U[UT ? 0 : q], make_float2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1])),
                           dec2, nth2, nsp);
       } else {
         uint32_t d[NBUF][2][8];  // [buffer][hi/lo][col]
@@ -892,7 +926,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
           }
 #pragma unroll
           for (int q = 3; q >= 0; --q)
-            lif_pair_sr<NS>(U[ch * 4 + q], make_float2(yv[2 * q], yv[2 * q + 1]), dec2, nth2, nsp);
+            lif_pair_sr<NS>(U[UT ? 0 : ch * 4 + q], make_float2(yv[2 * q], yv[2 * q + 1]), dec2, nth2, nsp);
           if (ch > 0) {
             if (NBUF == 1) {
               ptx::tmem_ld8(tcol + (ch - 1) * 8, d[0][0]);
@@ -902,7 +936,9 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
           }
         }
       }
-      // accumulator consumed: hand TMEM back to the MMA issuer
+      // accumulator consumed: hand TMEM back to the MMA issuer (UT: the U stores of
+      // this group complete before the next group's U loads)
+      if (UT) ptx::tmem_wait_st();
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_remote_relaxed(acc ? t_empty1 : t_empty0);
@@ -956,11 +992,26 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
       }
       if (e == 0 && lane == 0) trace_mark(p, it, TR_EPI_DONE);
     }
-    if (p.v_final && valid) {
+    if (p.v_final) {
 #pragma unroll
-      for (int cc = 0; cc < NCH; cc += 2) {
-        if (co_base + cc < Cout) p.v_final[vbase + cc] = U[cc / 2].x + vth;
-        if (co_base + cc + 1 < Cout) p.v_final[vbase + cc + 1] = U[cc / 2].y + vth;
+      for (int ch = 0; ch < NCHUNK; ++ch) {
+        uint32_t du[8];
+        if (UT) {
+          uint32_t dz[8];
+          ptx::tmem_ld8(ucol + ch * 8, du);
+          ptx::tmem_wait_ld_dep(du, dz);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; q += 2) {
+            du[q] = __float_as_uint(U[UT ? 0 : (ch * 8 + q) / 2].x);
+            du[q + 1] = __float_as_uint(U[UT ? 0 : (ch * 8 + q) / 2].y);
+          }
+        }
+        if (valid) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (co_base + ch * 8 + q < Cout) p.v_final[vbase + ch * 8 + q] = __uint_as_float(du[q]) + vth;
+        }
       }
     }
   }
@@ -1578,7 +1629,8 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   p.smem_bytes = g.smem_bytes; p.w_bytes_cta = g.w_bytes_cta;
   p.n_total = g.path == PATH_HALO ? 2u * g.cout_pad : (uint32_t)g.cout_pad;  // TMEM columns / acc
   uint32_t cols = 32;
-  while (cols < 2u * p.n_total) cols <<= 1;
+  const bool ut = g.path == PATH_H16 && g.cout_pad == 128;  // u_in_tmem(): U after the accumulators
+  while (cols < 2u * p.n_total + (ut ? 128u : 0u)) cols <<= 1;
   p.tmem_cols = cols;
   p.lbo_a = (uint32_t)kHaloRows * 16u;  // between 16-byte K chunks
   p.sbo_a = (uint32_t)kHaloW * 16u;     // between tile rows (8-row core-matrix groups)
