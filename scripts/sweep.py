@@ -1,0 +1,114 @@
+"""Throughput sweep over the BASELINE workloads: every config in its primary mode
+and K values, against the dense per-timestep baseline through the same kernels
+(the paper's comparison, Tables tab:speedup / tab:dvsg), plus the spike-density
+independence check of SURVEY.md section 8(d).
+
+    python scripts/sweep.py [--out gpurun_out/sweep.jsonl] [--iters 5] [--only C5]
+
+One JSON line per (config, mode, K): device ms per forward of the whole conv stack
+(CUDA events on the launch stream, inputs resident, after warm-up), input
+spike-frames/s, per-layer ms and engines, logical conv calls per sample
+(sum_l T_l / K_l) and the speedup over the config's dense run.
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2603_13810_b200 import configs, network, tacsnn  # noqa: E402
+
+RUNS = [
+    ("C1", "dense", 1), ("C1", "tac", 4), ("C1", "tactp", 4),
+    ("C2", "dense", 1), ("C2", "tac", 2), ("C2", "tac", 4), ("C2", "tac", 8),
+    ("C3", "dense", 1), ("C3", "tac", 8),
+    ("C4", "dense", 1), ("C4", "tactp", 2), ("C4", "tac", 2),
+    ("C5", "dense", 1), ("C5", "tactp", 2), ("C5", "tactp", 4), ("C5", "tactp", 8), ("C5", "tac", 4),
+]
+
+
+def time_forward(net, x, iters):
+    stream = torch.cuda.current_stream()
+    for _ in range(2):
+        net.forward(x)
+    torch.cuda.synchronize()
+    nL = len(net.specs)
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(nL)] for _ in range(iters)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(iters):
+        y = x
+        for li, (spec, prep) in enumerate(zip(net.specs, net.prepared)):
+            evs[i][li][0].record(stream)
+            y, _, _ = tacsnn.conv_lif(spec, prep, y)
+            evs[i][li][1].record(stream)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / iters
+    layer_ms = [sum(evs[i][li][0].elapsed_time(evs[i][li][1]) for i in range(iters)) / iters
+                for li in range(nL)]
+    return ms, layer_ms
+
+
+def density_check(iters, out):
+    """Same layer (C4 layer 1: 128->128 @64x64, TAC-TP K=2), inputs of density
+    0.01 vs 0.5: the conv is a dense contraction, so the time must not depend on
+    the spike density (the paper's own premise)."""
+    cfg = configs.CONFIGS["C4"]
+    spec = configs.layer_plan(cfg, B=64)[1]
+    w, b = configs.layer_weights(cfg)[1]
+    net = network.Network([spec], [(w, b)])
+    res = {}
+    g = torch.Generator(device="cuda").manual_seed(0)
+    for rho in (0.01, 0.5):
+        x = tacsnn.pack((torch.rand((spec.T, spec.B, spec.C_in, spec.H, spec.W), device="cuda",
+                                    generator=g) < rho).to(torch.uint8))
+        ms, _ = time_forward(net, x, iters)
+        res[str(rho)] = ms
+    line = {"check": "density_independence", "layer": "C4 L1 128->128 @64x64 TAC-TP K=2, B=64",
+            "ms_rho_0.01": res["0.01"], "ms_rho_0.5": res["0.5"],
+            "ratio": res["0.5"] / res["0.01"]}
+    print(json.dumps(line), flush=True)
+    out.write(json.dumps(line) + "\n")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.jsonl"))
+    ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--only", default=None)
+    a = ap.parse_args()
+    os.makedirs(os.path.dirname(a.out), exist_ok=True)
+    dense_ms = {}
+    with open(a.out, "w") as out:
+        for name, mode, K in RUNS:
+            if a.only and name != a.only:
+                continue
+            cfg = configs.CONFIGS[name]
+            specs = configs.layer_plan(cfg, mode=mode, K=K)
+            net = network.Network(specs, configs.layer_weights(cfg))
+            x = tacsnn.pack(configs.make_inputs(cfg, device="cuda"))
+            ms, layer_ms = time_forward(net, x, a.iters)
+            frames = cfg.B * cfg.T
+            if mode == "dense":
+                dense_ms[name] = ms
+            line = {"config": name, "mode": mode, "K": K, "B": cfg.B, "T": cfg.T,
+                    "ms_per_forward": ms, "frames_per_s": frames / (ms / 1e3),
+                    "speedup_vs_dense": (dense_ms[name] / ms) if name in dense_ms else None,
+                    "conv_calls_per_sample": configs.conv_calls(cfg, mode, K),
+                    "layer_ms": layer_ms, "engines": net.engines()}
+            print(json.dumps(line), flush=True)
+            out.write(json.dumps(line) + "\n")
+            del net, x
+            torch.cuda.empty_cache()
+        if not a.only:
+            density_check(a.iters, out)
+
+
+if __name__ == "__main__":
+    main()
