@@ -92,6 +92,9 @@ struct TcParams {
   uint32_t off_w, off_a, a_stage_bytes, off_scale, off_bar, smem_bytes;
   uint32_t w_bytes_cta, tmem_cols, n_total, lbo_a, sbo_a, lbo_b;
   int tap_off[9];
+  int split;             // A carried as fp16 hi + lo from the 2^K-entry table lut
+  uint32_t off_lut;      // smem copy of lut
+  uint32_t lut[1 << 8];  // idx (bit j = frame j's spike) -> fp16 A_hi | fp16 A_lo << 16
   const uint32_t *in;
   uint32_t *out;
   const float *v_init;
@@ -137,14 +140,36 @@ int cout_pad_of(int Cout) {
   return 128;
 }
 
+// Split-A (fp16) aggregate: when A_k = sum_j beta^{K-1-j} S_{kK+j} is not an exact
+// small integer (beta != 2^-m, e.g. the rate-coded configs' beta = 0.9, or
+// m (K-1) > 7), A is carried as two fp16 values A_hi + A_lo (|A - A_hi - A_lo| <=
+// 2^-22 |A|) looked up from a 2^K-entry table of the K spike bits of a channel,
+// and both ride the fp16 tensor-core path as extra K channels.
+bool split_of(const tac_conv_lif_desc *d) {
+  if (d->mode == TAC_MODE_DENSE || d->K <= 1) return false;
+  const int m = beta_shift(d->beta);
+  return m == 0 || m * (d->K - 1) > 7;
+}
+constexpr int kMaxSplitK = 8;  // 2^K-entry table
+
 int path_of(const tac_conv_lif_desc *d) {
+  if (split_of(d)) return PATH_H16;
   return (d->C_in % 32 == 0) ? PATH_HALO : PATH_H16;
 }
 
+// 16-B K chunks (8 fp16 channels) per halo pixel of the fp16 path: channels
+// [A (C_in) | bias 1.0] or, split, [A_hi (C_in) | A_lo (C_in) | bias 1.0]; even
+// so that every MMA has K = 16.
+int h16_chunks(const tac_conv_lif_desc *d) {
+  const int ch = split_of(d) ? 2 * d->C_in + 1 : d->C_in + 1;
+  const int nck = (ch + 7) / 8;
+  return nck < 2 ? 2 : (nck + 1) / 2 * 2;
+}
+
 struct Geometry {
-  int path, nkc, ntaps, cout_pad, nsteps, nstages, use_tma, nraw, raw_bw;
+  int path, split, nkc, ntaps, cout_pad, nsteps, nstages, use_tma, nraw, raw_bw;
   uint32_t w_bytes_cta, a_stage_bytes, raw_stage_bytes, raw_box_bytes, off_w, off_a, off_raw,
-      off_scale, off_bar, smem_bytes;
+      off_scale, off_lut, off_bar, smem_bytes;
 };
 constexpr int kMaxRaw = 4;
 constexpr int kNumBars = 2 * kMaxStages + 2 * kAccs + 1 + 2 * kMaxRaw;
@@ -156,6 +181,7 @@ uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 Geometry geometry(const tac_conv_lif_desc *d, bool use_tma = false) {
   Geometry g{};
   g.path = path_of(d);
+  g.split = split_of(d) ? 1 : 0;
   g.cout_pad = cout_pad_of(d->C_out);
   const int K = d->mode == TAC_MODE_DENSE ? 1 : d->K;
   g.nsteps = d->mode == TAC_MODE_TACTP ? K : 1;
@@ -168,11 +194,14 @@ Geometry geometry(const tac_conv_lif_desc *d, bool use_tma = false) {
     const int nwin = d->C_in / 32;
     g.raw_bw = nwin == 4 ? kHaloW * 4 : (int)align_up(kHaloW * nwin + 3, 4);
   } else {
-    g.nkc = 2;                              // 16 fp16 channels = two 16-B K chunks
+    g.nkc = h16_chunks(d);                  // 16-B K chunks per halo pixel
     g.ntaps = 9;
-    g.w_bytes_cta = 288u * g.cout_pad;      // [hi/lo][tap][2 chunks][C_out_pad/2 rows][16 B]
-    g.a_stage_bytes = align_up((uint32_t)kHaloRows * 32u, 128);
-    g.raw_bw = 8;  // 16-B aligned start word + the <= 3 words holding 10 px x C_in bits
+    // [hi/lo slice][tap][chunk][C_out_pad/2 rows][16 B] per CTA
+    g.w_bytes_cta = 144u * g.nkc * g.cout_pad;
+    g.a_stage_bytes = align_up((uint32_t)kHaloRows * 16u * g.nkc, 128);
+    // C_in <= 8: 16-B aligned start word + the <= 3 words holding 10 px x C_in bits;
+    // C_in = 32: one word per pixel as in the int8 halo path
+    g.raw_bw = d->C_in >= 32 ? (int)align_up(kHaloW * (d->C_in / 32) + 3, 4) : 8;
   }
   g.raw_box_bytes = (uint32_t)K * kHaloH * g.raw_bw * 4u;
   g.raw_stage_bytes = align_up(g.raw_box_bytes, 128);
@@ -184,7 +213,8 @@ Geometry geometry(const tac_conv_lif_desc *d, bool use_tma = false) {
     g.off_a = align_up(g.w_bytes_cta, 1024);
     g.off_raw = align_up(g.off_a + g.nstages * g.a_stage_bytes, 128);
     g.off_scale = align_up(g.off_raw + g.nraw * g.raw_stage_bytes, 128);
-    g.off_bar = align_up(g.off_scale + 4u * g.cout_pad * 4u, 64);
+    g.off_lut = align_up(g.off_scale + 4u * g.cout_pad * 4u, 16);
+    g.off_bar = align_up(g.off_lut + (g.split ? 4u << kMaxSplitK : 0u), 64);
     g.smem_bytes = g.off_bar + 8u * kNumBars + 16u;
     if (g.smem_bytes <= kSmemLimit) break;
   }
@@ -202,18 +232,17 @@ const char *shape_reason(const tac_conv_lif_desc *d) {
     return "needs C_out in {8,16} or a multiple of 32 up to 128";
   const int K = d->mode == TAC_MODE_DENSE ? 1 : d->K;
   if (d->mode == TAC_MODE_TACTP && K > kMaxSteps) return "TAC-TP needs K <= 8";
-  if (geometry(d).smem_bytes > kSmemLimit) return "shared-memory footprint exceeds 227 KB";
   return nullptr;
 }
 
 const char *reason(const tac_conv_lif_desc *d) {
   const char *r = shape_reason(d);
   if (r) return r;
-  if (d->mode != TAC_MODE_DENSE) {
-    const int m = beta_shift(d->beta);
-    if (!m) return "TAC/TAC-TP on tensor cores needs beta = 2^-m (exact u8 aggregate)";
-    if (m * (d->K - 1) > 7) return "u8 aggregate overflow: needs m*(K-1) <= 7";
+  if (split_of(d)) {
+    if (d->K > kMaxSplitK) return "split (beta != 2^-m) aggregate needs K <= 8";
+    if (!(d->C_in <= 2 || d->C_in == 32)) return "split (beta != 2^-m) aggregate needs C_in in {1, 2, 32}";
   }
+  if (geometry(d).smem_bytes > kSmemLimit) return "shared-memory footprint exceeds 227 KB";
   return nullptr;
 }
 
@@ -348,14 +377,6 @@ __device__ __forceinline__ void produce_h16(const TcParams &p, int tile, int k, 
   }
 }
 
-// --- TMA producers: aggregate from the raw halo in smem (compact loops) --------
-// raw-halo start word of a tile: the TMA box starts 16-B aligned (word c0 & ~3)
-__device__ __forceinline__ int halo_c0(const TcParams &p, int x0) {
-  return p.Cin >= 32 ? (x0 - p.pad) * (p.Cin >> 5)
-                     : ((x0 - p.pad) * p.Cin >= 0 ? ((x0 - p.pad) * p.Cin) >> 5
-                                                  : -((31 - (x0 - p.pad) * p.Cin) >> 5));
-}
-
 // d | (a & b) in one LOP3
 __device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t b, uint32_t d) {
   uint32_t r;
@@ -376,6 +397,99 @@ __device__ __forceinline__ void agg_word_m1(uint32_t (&o)[8], const uint32_t (&x
       o[q] = and_or(t, mask, o[q]);
     }
   }
+}
+
+// --- split-A fp16 rows (beta != 2^-m): A_hi / A_lo from the table ---------------
+// K-bit table index of one channel: bit j <- channel bit c of frame j
+template <int K>
+__device__ __forceinline__ uint32_t frame_index(const uint32_t (&bits)[K], int c) {
+  uint32_t idx = 0;
+#pragma unroll
+  for (int j = 0; j < K; ++j) idx |= ((bits[j] >> c) & 1u) << j;
+  return idx;
+}
+// chunk 0 of a C_in <= 2 split row: [A_hi(0..CIN-1) | A_lo(0..CIN-1) | 1.0 | 0 ...]
+template <int K, int CIN>
+__device__ __forceinline__ uint4 split_row_small(const uint32_t (&bits)[K], const uint32_t *lut) {
+  const uint32_t e0 = lut[frame_index<K>(bits, 0)];
+  if (CIN == 1) return make_uint4(e0, 0x3C00u, 0u, 0u);
+  const uint32_t e1 = lut[frame_index<K>(bits, 1)];
+  return make_uint4(__byte_perm(e0, e1, 0x5410u), __byte_perm(e0, e1, 0x7632u), 0x3C00u, 0u);
+}
+// C_in = 32 split row: 8 index words (byte b of o[q] = channel q + 8b) -> chunks
+// 0..3 A_hi, 4..7 A_lo, 8 = {1.0, 0 ...}, 9 = 0
+__device__ __forceinline__ void store_split32_row(uint32_t dst, uint32_t lbo, const uint32_t (&o)[8],
+                                                  const uint32_t *lut) {
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    uint32_t e[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) e[q] = lut[(o[q] >> (8 * b)) & 0xFFu];
+    ptx::st_shared_v4(dst + b * lbo, __byte_perm(e[0], e[1], 0x5410u), __byte_perm(e[2], e[3], 0x5410u),
+                      __byte_perm(e[4], e[5], 0x5410u), __byte_perm(e[6], e[7], 0x5410u));
+    ptx::st_shared_v4(dst + (4 + b) * lbo, __byte_perm(e[0], e[1], 0x7632u), __byte_perm(e[2], e[3], 0x7632u),
+                      __byte_perm(e[4], e[5], 0x7632u), __byte_perm(e[6], e[7], 0x7632u));
+  }
+  ptx::st_shared_v4(dst + 8 * lbo, 0x3C00u, 0u, 0u, 0u);
+  ptx::st_shared_v4(dst + 9 * lbo, 0u, 0u, 0u, 0u);
+}
+
+// LDG split producers (e.g. MNIST rows, whose 4-B row stride rules out TMA)
+template <int K, int CIN>
+__device__ __forceinline__ void produce_h16s(const TcParams &p, const uint32_t *lut, int tile, int k,
+                                             uint32_t a_stage, int ptid) {
+  int b, y0, x0;
+  bool tok;
+  tile_origin(p, tile, b, y0, x0, tok);
+  const uint32_t *frame0 = p.in + (long long)(k * K) * p.in_st + (long long)b * p.in_sb;
+  for (int row = ptid; row < kHaloRows; row += kProdWarps * 32) {
+    const int hy = row / kHaloW, hx = row - (row / kHaloW) * kHaloW;
+    const int yi = y0 + hy - p.pad, xi = x0 + hx - p.pad;
+    const bool ok = tok && yi >= 0 && yi < p.H && xi >= 0 && xi < p.W;
+    const int bit = ok ? xi * CIN : 0, sh = bit & 31;
+    const bool two = ok && sh + CIN > 32;
+    const uint32_t *src = frame0 + (long long)(ok ? yi : 0) * p.wpr_in + (bit >> 5);
+    uint32_t bits[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const uint32_t w0 = ok ? __ldg(src + (long long)j * p.in_st) : 0u;
+      const uint32_t w1 = two ? __ldg(src + (long long)j * p.in_st + 1) : 0u;
+      bits[j] = __funnelshift_r(w0, w1, sh);
+    }
+    const uint4 c0 = split_row_small<K, CIN>(bits, lut);
+    const uint32_t dst = a_stage + (uint32_t)row * 16u;
+    ptx::st_shared_v4(dst, c0.x, c0.y, c0.z, c0.w);
+    ptx::st_shared_v4(dst + p.lbo_a, 0u, 0u, 0u, 0u);
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void produce_s32(const TcParams &p, const uint32_t *lut, int tile, int k,
+                                            uint32_t a_stage, int ptid) {
+  int b, y0, x0;
+  bool tok;
+  tile_origin(p, tile, b, y0, x0, tok);
+  const uint32_t *frame0 = p.in + (long long)(k * K) * p.in_st + (long long)b * p.in_sb;
+  for (int row = ptid; row < kHaloRows; row += kProdWarps * 32) {
+    const int hy = row / kHaloW, hx = row - (row / kHaloW) * kHaloW;
+    const int yi = y0 + hy - p.pad, xi = x0 + hx - p.pad;
+    const bool ok = tok && yi >= 0 && yi < p.H && xi >= 0 && xi < p.W;
+    const uint32_t *src = frame0 + (long long)(ok ? yi : 0) * p.wpr_in + (ok ? xi : 0);
+    uint32_t x[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) x[j] = ok ? __ldg(src + (long long)j * p.in_st) : 0u;
+    uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    agg_word_m1<K>(o, x);  // byte b of o[q] = K-bit index of channel q + 8b
+    store_split32_row(a_stage + (uint32_t)row * 16u, p.lbo_a, o, lut);
+  }
+}
+
+// --- TMA producers: aggregate from the raw halo in smem (compact loops) --------
+// raw-halo start word of a tile: the TMA box starts 16-B aligned (word c0 & ~3)
+__device__ __forceinline__ int halo_c0(const TcParams &p, int x0) {
+  return p.Cin >= 32 ? (x0 - p.pad) * (p.Cin >> 5)
+                     : ((x0 - p.pad) * p.Cin >= 0 ? ((x0 - p.pad) * p.Cin) >> 5
+                                                  : -((31 - (x0 - p.pad) * p.Cin) >> 5));
 }
 
 // TMA raw-halo producer (C_in = 32 nwin): thread owns 32-channel word w of halo
@@ -480,6 +594,47 @@ __device__ __forceinline__ void produce_h16_tma(const TcParams &p, const uint32_
   }
 }
 
+// TMA split producers (raw halo in smem; see produce_h16_tma / produce_halo_tma)
+template <int K, int CIN>
+__device__ __forceinline__ void produce_h16s_tma(const TcParams &p, const uint32_t *lut,
+                                                 const uint32_t *raw, uint32_t a_stage, int ptid,
+                                                 int x0) {
+  const int bw = p.raw_bw, fstride = kHaloH * p.raw_bw;
+  const int c0w = halo_c0(p, x0) & ~3;
+#pragma unroll 1
+  for (int row = ptid; row < kHaloRows; row += kProdWarps * 32) {
+    const int hy = row / kHaloW, hx = row - hy * kHaloW;
+    const int bitoff = (x0 + hx - p.pad) * CIN - c0w * 32;
+    const uint32_t *src = raw + hy * bw + (bitoff >> 5);
+    const int sh = bitoff & 31;
+    uint32_t bits[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) bits[j] = __funnelshift_r(src[j * fstride], src[j * fstride + 1], sh);
+    const uint4 c = split_row_small<K, CIN>(bits, lut);
+    ptx::st_shared_v4(a_stage + (uint32_t)row * 16u, c.x, c.y, c.z, c.w);
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void produce_s32_tma(const TcParams &p, const uint32_t *lut,
+                                                const uint32_t *raw, uint32_t a_stage, int ptid,
+                                                int x0) {
+  const int bw = p.raw_bw, fstride = kHaloH * p.raw_bw;
+  const int c0 = halo_c0(p, x0);
+  raw += c0 - (c0 & ~3);
+#pragma unroll 1
+  for (int row = ptid; row < kHaloRows; row += kProdWarps * 32) {
+    const int hy = row / kHaloW, hx = row - hy * kHaloW;
+    const uint32_t *src = raw + hy * bw + hx;
+    uint32_t x[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) x[j] = src[j * fstride];
+    uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    agg_word_m1<K>(o, x);
+    store_split32_row(a_stage + (uint32_t)row * 16u, p.lbo_a, o, lut);
+  }
+}
+
 // chunk 1 of every halo row of every A stage (constant for the whole kernel)
 __device__ __forceinline__ void h16_init_stages(const TcParams &p, uint32_t sbase, int ptid) {
   uint32_t one_lo, one_hi, c8;
@@ -560,8 +715,13 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
       if (ptid == 0) trace_mark(p, it, TR_PROD_START);
       const uint32_t *raw = reinterpret_cast<const uint32_t *>(smem + p.off_raw + r * p.raw_stage_bytes);
       const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
+      const uint32_t *lut = reinterpret_cast<const uint32_t *>(smem + p.off_lut);
       if (PATH == PATH_HALO)
         produce_halo_tma<K>(p, raw, a_stage, ptid, x0);
+      else if (p.split && K <= kMaxSplitK && K > 1)
+        p.Cin == 32 ? produce_s32_tma<K>(p, lut, raw, a_stage, ptid, x0)
+                    : (p.Cin == 1 ? produce_h16s_tma<K, 1>(p, lut, raw, a_stage, ptid, x0)
+                                  : produce_h16s_tma<K, 2>(p, lut, raw, a_stage, ptid, x0));
       else if (p.Cin <= 4)
         produce_h16_tma<K, true>(p, raw, a_stage, ptid, x0);
       else
@@ -578,9 +738,10 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
 }
 
 template <int PATH, int K>
-__device__ __forceinline__ void producer_role(const TcParams &p, uint32_t sbase,
+__device__ __forceinline__ void producer_role(const TcParams &p, uint32_t sbase, const uint8_t *smem,
                                               uint32_t bar_a_full, uint32_t bar_a_empty, int cid,
                                               int ncl, uint32_t rank, uint32_t lane, int ptid) {
+  const uint32_t *lut = reinterpret_cast<const uint32_t *>(smem + p.off_lut);
   const uint32_t ns = (uint32_t)p.nstages;
   uint32_t it = 0;
   for (int pair = cid; pair < p.num_pairs; pair += ncl) {
@@ -591,6 +752,10 @@ __device__ __forceinline__ void producer_role(const TcParams &p, uint32_t sbase,
       const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
       if (PATH == PATH_HALO)
         produce_halo<K>(p, tile, k, a_stage, ptid);
+      else if (p.split && K <= kMaxSplitK && K > 1)
+        p.Cin == 32 ? produce_s32<K>(p, lut, tile, k, a_stage, ptid)
+                    : (p.Cin == 1 ? produce_h16s<K, 1>(p, lut, tile, k, a_stage, ptid)
+                                  : produce_h16s<K, 2>(p, lut, tile, k, a_stage, ptid));
       else
         produce_h16<K>(p, tile, k, a_stage, ptid);
       ptx::fence_proxy_async_smem();
@@ -1275,6 +1440,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
     ptx::tmem_alloc_cg2(ptx::smem_u32(tmem_slot), p.tmem_cols);
     ptx::tmem_relinquish_cg2();
   }
+  if (p.split) {
+    uint32_t *lut_s = reinterpret_cast<uint32_t *>(smem + p.off_lut);
+    for (int i = threadIdx.x; i < (1 << kMaxSplitK); i += kThreads) lut_s[i] = p.lut[i];
+  }
   for (int i = threadIdx.x; i < 4 * p.Cout_pad; i += kThreads) {
     const float f = p.scale_bias[i];
     sc[i] = (i / p.Cout_pad == 1) ? f : f * p.agg_scale;  // [s1/254 | bias | s1 | s2]
@@ -1347,15 +1516,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
               } else {
                 // D = sum_taps A_tap (W_hi + W_lo) (+ bias via the constant channel of the
                 // centre tap): 9 taps x 2 fp16 slices, K = 16 each, into one accumulator
+                // (nkc 16-B chunks per halo pixel; K = 16 = two chunks per MMA)
                 const uint32_t idf = ptx::idesc_f16(256, p.n_total);
 #pragma unroll
                 for (int tap = 0; tap < 9; ++tap) {
                   const uint32_t toff = (uint32_t)((tap / 3) * kHaloW + (tap % 3));
 #pragma unroll
                   for (int sl = 0; sl < 2; ++sl)
-                    ptx::mma_f16_cg2(d_tmem, a_base + (uint64_t)toff,
-                                     b_desc0 + (uint64_t)((sl * 9 + tap) * 2 * nhb16), idf,
-                                     (tap | sl) ? 1u : 0u);
+                    for (int kc2 = 0; kc2 < nkc2; ++kc2)
+                      ptx::mma_f16_cg2(d_tmem, a_base + (uint64_t)(toff + 2u * kc2 * lbo16),
+                                       b_desc0 + (uint64_t)(((sl * 9 + tap) * nkc + 2 * kc2) * nhb16), idf,
+                                       (tap | sl | kc2) ? 1u : 0u);
                 }
               }
               ptx::mma_commit_cg2_multicast(bar_a_empty + 8 * s);
@@ -1381,10 +1552,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
         }
       } else {
         switch (p.K) {
-          case 1: producer_role<PATH, 1>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
-          case 2: producer_role<PATH, 2>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
-          case 4: producer_role<PATH, 4>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
-          default: producer_role<PATH, 8>(p, sbase, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
+          case 1: producer_role<PATH, 1>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
+          case 2: producer_role<PATH, 2>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
+          case 4: producer_role<PATH, 4>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
+          default: producer_role<PATH, 8>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
         }
       }
     }
@@ -1510,29 +1681,39 @@ void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bi
         }
     } else {
       // fp16 image, CTA `half` holds output channels [half*Cp/2, (half+1)*Cp/2) of BOTH
-      // slices: [slice][tap][16-B chunk (2)][row (Cp/2)][8 fp16].  Halo channel k < C_in
-      // holds W[n][k][r][s] (tap = 3r + s), channel C_in of the centre tap the bias
-      // (the producers store 1.0 there); the aggregate scale 2^{-m(K-1)} (exact) is
-      // folded into the weights, not the bias.
-      const int m = d->mode == TAC_MODE_DENSE ? 0 : beta_shift(d->beta);
+      // slices: [slice][tap][16-B chunk (nkc)][row (Cp/2)][8 fp16].  Halo channel k:
+      //   exact u8 aggregate : k < C_in -> W[n][k][r][s] * 2^{-m(K-1)} (folded scale),
+      //                        k == C_in of the centre tap -> bias (producers store 1.0)
+      //   split A (hi | lo)  : k < C_in -> W (hi slice: fp16 hi, lo slice: fp16 lo),
+      //                        C_in <= k < 2 C_in -> W hi in the hi slice (times A_lo),
+      //                        0 in the lo slice (A_lo W_lo ~ 2^-33 |A W|), bias at 2 C_in
+      // so D = sum (A_hi + A_lo) W_hi + A_hi W_lo + bias, accumulated in fp32.
+      const bool split = g.split != 0;
+      const int m = (d->mode == TAC_MODE_DENSE || split) ? 0 : beta_shift(d->beta);
       const int Kg = d->mode == TAC_MODE_DENSE ? 1 : d->K;
-      const double agg = std::ldexp(1.0, -m * (Kg - 1));
-      const int nh = Cp / 2;
+      const double agg = split ? 1.0 : std::ldexp(1.0, -m * (Kg - 1));
+      const int nh = Cp / 2, nk = g.nkc, kbias = split ? 2 * Ci : Ci;
       uint16_t *img16 = reinterpret_cast<uint16_t *>(img);
       for (int nl = 0; nl < nh; ++nl) {
         const int n = half * nh + nl;
         for (int tap = 0; tap < 9; ++tap)
-          for (int k = 0; k < 16; ++k) {
+          for (int k = 0; k < 8 * nk; ++k) {
             double wv = 0.0;
+            bool hi_only = false;
             if (n < Co) {
-              if (k < Ci) wv = (double)weight[(((size_t)n * Ci + k) * 3 + tap / 3) * 3 + tap % 3] * agg;
-              else if (k == Ci && tap == 4) wv = (bias ? (double)bias[n] : 0.0) + boff;
+              const int ci = k < Ci ? k : (split && k < 2 * Ci ? k - Ci : -1);
+              if (ci >= 0) {
+                wv = (double)weight[(((size_t)n * Ci + ci) * 3 + tap / 3) * 3 + tap % 3] * agg;
+                hi_only = k >= Ci;
+              } else if (k == kbias && tap == 4) {
+                wv = (bias ? (double)bias[n] : 0.0) + boff;
+              }
             }
             const __half hi = __double2half(wv);
-            const __half lo = __double2half(wv - (double)__half2float(hi));
+            const __half lo = hi_only ? __double2half(0.0) : __double2half(wv - (double)__half2float(hi));
             const int ck = k / 8, e = k % 8;
-            img16[((((size_t)0 * 9 + tap) * 2 + ck) * nh + nl) * 8 + e] = __half_as_ushort(hi);
-            img16[((((size_t)1 * 9 + tap) * 2 + ck) * nh + nl) * 8 + e] = __half_as_ushort(lo);
+            img16[((((size_t)0 * 9 + tap) * nk + ck) * nh + nl) * 8 + e] = __half_as_ushort(hi);
+            img16[((((size_t)1 * 9 + tap) * nk + ck) * nh + nl) * 8 + e] = __half_as_ushort(lo);
           }
       }
     }
@@ -1611,7 +1792,19 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   p.num_pairs = (p.num_tiles + 1) / 2;
   p.nstages = g.nstages;
   p.nkc = g.nkc; p.ntaps = g.ntaps;
-  p.m_shift = d->mode == TAC_MODE_DENSE ? 0 : beta_shift(d->beta);
+  p.m_shift = (d->mode == TAC_MODE_DENSE || g.split) ? 0 : beta_shift(d->beta);
+  p.split = g.split;
+  p.off_lut = g.off_lut;
+  if (g.split) {  // A = sum_j bit_j beta^{K-1-j} in fp64, as fp16 hi + lo
+    for (int idx = 0; idx < (1 << kMaxSplitK); ++idx) {
+      double a = 0.0;
+      for (int j = 0; j < lp.K && j < kMaxSplitK; ++j)
+        if ((idx >> j) & 1) a += std::pow((double)d->beta, (double)(lp.K - 1 - j));
+      const __half hi = __double2half(a);
+      const __half lo = __double2half(a - (double)__half2float(hi));
+      p.lut[idx] = (uint32_t)__half_as_ushort(hi) | ((uint32_t)__half_as_ushort(lo) << 16);
+    }
+  }
   p.wpr_in = lp.wpr_in; p.wpr_out = lp.wpr_out;
   p.nwo = lp.Cout % 32 == 0 ? lp.Cout / 32 : 1;
   const bool out_atomic = g.cout_pad < 64;  // sub-word or shared-word output fields

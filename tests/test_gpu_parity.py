@@ -100,6 +100,31 @@ def test_layer_parity(T, O, case, mode, K, beta, engine):
     assert 0.0 < st["rate"] < 0.9, st
 
 
+SPLIT_CASES = [
+    # beta != 2^-m (or m (K-1) > 7): A carried as fp16 hi + lo on the tensor cores
+    ("C1", (8, 4, 1, 28, 28, 8, 0, 1), 2.5, 0.1),             # LDG producer, C_in 1
+    ("mnistL1", (8, 3, 1, 28, 28, 32, 0, 2), 2.5, 0.15),
+    ("mnistL2", (8, 3, 32, 13, 13, 64, 0, 1), 3.5, 0.15),     # LDG producer, C_in 32
+    ("dvsL1s", (8, 2, 2, 64, 64, 128, 1, 2), 7.1, 0.05),       # TMA producer, C_in 2
+    ("cin32_tma", (8, 2, 32, 12, 16, 64, 1, 2), 2.5, 0.15),   # TMA producer, C_in 32
+]
+
+
+@pytest.mark.parametrize("mode,K,beta", [("tac", 2, 0.9), ("tac", 4, 0.9), ("tac", 8, 0.9),
+                                         ("tactp", 4, 0.9), ("tactp", 8, 0.25)])
+@pytest.mark.parametrize("case", SPLIT_CASES, ids=[c[0] for c in SPLIT_CASES])
+def test_split_aggregate_parity(T, O, case, mode, K, beta):
+    """tcgen05 path with the split fp16 aggregate (the rate-coded configs' beta = 0.9)."""
+    name, (Tn, B, Cin, H, W, Cout, pad, pool), gain, rho = case
+    spec = T.LayerSpec(T=Tn, B=B, C_in=Cin, H=H, W=W, C_out=Cout, pad=pad, K=K, mode=mode,
+                       beta=beta, out_pool=pool, engine="tcgen05")
+    assert spec.engine_used() == "tcgen05"
+    S = _spikes(zlib.crc32(name.encode()) % 997, (Tn, B, Cin, H, W), rho)
+    w, b = _w(8, Cout, Cin, gain)
+    _, _, st = P.check_layer(T, O, spec, S, w, b, label=f"split/{name}/{mode}/K{K}/b{beta}")
+    assert 0.0 < st["rate"] < 0.9, st
+
+
 @pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("reset", ["delayed", "hard"])
 @pytest.mark.parametrize("mode", ["dense", "tac", "tactp"])
