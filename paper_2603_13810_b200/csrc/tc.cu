@@ -76,7 +76,9 @@ constexpr int kHaloH = kTileH + 2, kHaloW = kTileW + 2;  // 3x3 halo
 constexpr int kHaloRows = kHaloH * kHaloW;              // 180 halo pixels
 constexpr uint32_t kSmemLimit = 232448;
 
-enum { PATH_HALO = 0, PATH_H16 = 1 };  // int8 halo (C_in % 32 == 0) | fp16 halo (C_in <= 8)
+// int8 halo (C_in % 32 == 0) | fp16 halo (C_in <= 8) | fp16 halo with the split A_hi + A_lo
+// aggregate (kernel template only: the host geometry of PATH_SPLIT is that of PATH_H16)
+enum { PATH_HALO = 0, PATH_H16 = 1, PATH_SPLIT = 2 };
 
 struct TcParams {
   CUtensorMap tmap;  // 4-D [T][B][H][WPR] u32 view of the input spikes (TMA producer)
@@ -700,7 +702,7 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
                                                   uint32_t bar_raw_empty, int cid, int ncl,
                                                   uint32_t rank, uint32_t lane, int ptid) {
   const uint32_t ns = (uint32_t)p.nstages, nr = (uint32_t)p.nraw;
-  if (PATH == PATH_H16) h16_init_stages(p, sbase, ptid);  // fenced with the first stage
+  if (PATH != PATH_HALO) h16_init_stages(p, sbase, ptid);  // fenced with the first stage
   uint32_t it = 0;
   for (int pair = cid; pair < p.num_pairs; pair += ncl) {
     int b, y0, x0;
@@ -718,7 +720,7 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
       const uint32_t *lut = reinterpret_cast<const uint32_t *>(smem + p.off_lut);
       if (PATH == PATH_HALO)
         produce_halo_tma<K>(p, raw, a_stage, ptid, x0);
-      else if (p.split && K <= kMaxSplitK && K > 1)
+      else if (PATH == PATH_SPLIT && K > 1)
         p.Cin == 32 ? produce_s32_tma<K>(p, lut, raw, a_stage, ptid, x0)
                     : (p.Cin == 1 ? produce_h16s_tma<K, 1>(p, lut, raw, a_stage, ptid, x0)
                                   : produce_h16s_tma<K, 2>(p, lut, raw, a_stage, ptid, x0));
@@ -752,7 +754,7 @@ __device__ __forceinline__ void producer_role(const TcParams &p, uint32_t sbase,
       const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
       if (PATH == PATH_HALO)
         produce_halo<K>(p, tile, k, a_stage, ptid);
-      else if (p.split && K <= kMaxSplitK && K > 1)
+      else if (PATH == PATH_SPLIT && K > 1)
         p.Cin == 32 ? produce_s32<K>(p, lut, tile, k, a_stage, ptid)
                     : (p.Cin == 1 ? produce_h16s<K, 1>(p, lut, tile, k, a_stage, ptid)
                                   : produce_h16s<K, 2>(p, lut, tile, k, a_stage, ptid));
@@ -965,7 +967,7 @@ __device__ __forceinline__ void lif_pair_sr(float2 &u, float2 y, float2 dec2, fl
 // columns [2 n_total, 2 n_total + 128) (the accumulators use 2 x 128), and is
 // streamed through registers 8 channels at a time -- 32 registers fewer per thread.
 template <int NCH, int PATH, int NPART>
-constexpr bool u_in_tmem() { return PATH == PATH_H16 && NPART == 4 && NCH == 32; }
+constexpr bool u_in_tmem() { return PATH != PATH_HALO && NPART == 4 && NCH == 32; }
 
 template <int NCH, int PATH, int NPART, int NS>
 __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, uint32_t tmem_base,
@@ -973,7 +975,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
                                             int ncl, uint32_t rank, uint32_t warp, uint32_t lane) {
   static_assert(NCH <= 32, "one spike word per thread");
   constexpr int NCHUNK = NCH / 8;
-  constexpr bool F16 = PATH == PATH_H16;
+  constexpr bool F16 = PATH != PATH_HALO;
   constexpr bool UT = u_in_tmem<NCH, PATH, NPART>();
   constexpr bool LD32 = false;  // F16 && NCH == 32 (one 32-column load) spills at 104 regs
   constexpr int NBUF = (NPART == 2 || (F16 && NS <= 4)) ? 2 : 1;  // TMEM prefetch depth (registers)
@@ -1260,7 +1262,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
 #pragma unroll
       for (int j = 0; j < NSP; ++j) sw1[j] = 0u;
       const uint32_t tcol = tmem_base + lane_addr + acc * p.n_total + (uint32_t)co_base;
-      constexpr bool F16 = PATH == PATH_H16;  // fp32 Y straight from TMEM
+      constexpr bool F16 = PATH != PATH_HALO;  // fp32 Y straight from TMEM
       constexpr int NBUF = (NPART == 2 || F16) ? 2 : 1;  // TMEM prefetch depth (registers)
       uint32_t d[NBUF][2][8];                    // [buffer][hi/lo][col]
       ptx::tmem_ld8(tcol, d[0][0]);
@@ -1395,6 +1397,31 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
   }
 }
 
+// fp16-path MMAs of one group: 9 taps x {hi, lo} weight slices x NKC2 K=16 steps
+template <int NKC2>
+__device__ __forceinline__ void mma_tap_h16(int tap, uint32_t d_tmem, uint64_t a_base, uint64_t b_desc0,
+                                            uint32_t idf, uint32_t lbo16, uint32_t nhb16) {
+  const uint32_t toff = (uint32_t)((tap / 3) * kHaloW + (tap % 3));
+#pragma unroll
+  for (int sl = 0; sl < 2; ++sl)
+#pragma unroll
+    for (int kc2 = 0; kc2 < NKC2; ++kc2)
+      ptx::mma_f16_cg2(d_tmem, a_base + (uint64_t)(toff + 2u * kc2 * lbo16),
+                       b_desc0 + (uint64_t)(((sl * 9 + tap) * 2 * NKC2 + 2 * kc2) * nhb16), idf,
+                       (tap | sl | kc2) ? 1u : 0u);
+}
+template <int NKC2>
+__device__ __forceinline__ void mma_group_h16(uint32_t d_tmem, uint64_t a_base, uint64_t b_desc0,
+                                              uint32_t idf, uint32_t lbo16, uint32_t nhb16) {
+  if constexpr (NKC2 == 1) {
+#pragma unroll
+    for (int tap = 0; tap < 9; ++tap) mma_tap_h16<NKC2>(tap, d_tmem, a_base, b_desc0, idf, lbo16, nhb16);
+  } else {
+#pragma unroll 1
+    for (int tap = 0; tap < 9; ++tap) mma_tap_h16<NKC2>(tap, d_tmem, a_base, b_desc0, idf, lbo16, nhb16);
+  }
+}
+
 template <int NCH, int PATH, int NPART>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART), 1)
     tc_conv_lif_kernel(const __grid_constant__ TcParams p) {
@@ -1516,18 +1543,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
               } else {
                 // D = sum_taps A_tap (W_hi + W_lo) (+ bias via the constant channel of the
                 // centre tap): 9 taps x 2 fp16 slices, K = 16 each, into one accumulator
-                // (nkc 16-B chunks per halo pixel; K = 16 = two chunks per MMA)
+                // (nkc 16-B chunks per halo pixel; K = 16 = two chunks per MMA; the
+                // common chunk counts are fully unrolled: no per-MMA address arithmetic)
                 const uint32_t idf = ptx::idesc_f16(256, p.n_total);
-#pragma unroll
-                for (int tap = 0; tap < 9; ++tap) {
-                  const uint32_t toff = (uint32_t)((tap / 3) * kHaloW + (tap % 3));
-#pragma unroll
-                  for (int sl = 0; sl < 2; ++sl)
-                    for (int kc2 = 0; kc2 < nkc2; ++kc2)
-                      ptx::mma_f16_cg2(d_tmem, a_base + (uint64_t)(toff + 2u * kc2 * lbo16),
-                                       b_desc0 + (uint64_t)(((sl * 9 + tap) * nkc + 2 * kc2) * nhb16), idf,
-                                       (tap | sl | kc2) ? 1u : 0u);
-                }
+                if (PATH == PATH_H16 || nkc2 == 1)
+                  mma_group_h16<1>(d_tmem, a_base, b_desc0, idf, lbo16, nhb16);
+                else
+                  mma_group_h16<5>(d_tmem, a_base, b_desc0, idf, lbo16, nhb16);
               }
               ptx::mma_commit_cg2_multicast(bar_a_empty + 8 * s);
               ptx::mma_commit_cg2_multicast(bar_t_full + 8 * acc);
@@ -1856,12 +1878,19 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
       case 64: e = launch_kernel<32, PATH_HALO, 2>(p, nclusters, st); break;
       default: e = launch_kernel<32, PATH_HALO, 4>(p, nclusters, st); break;
     }
-  } else {
+  } else if (!g.split) {
     switch (g.cout_pad) {
       case 16: e = launch_kernel<8, PATH_H16, 2>(p, nclusters, st); break;
       case 32: e = launch_kernel<16, PATH_H16, 2>(p, nclusters, st); break;
       case 64: e = launch_kernel<32, PATH_H16, 2>(p, nclusters, st); break;
       default: e = launch_kernel<32, PATH_H16, 4>(p, nclusters, st); break;
+    }
+  } else {
+    switch (g.cout_pad) {
+      case 16: e = launch_kernel<8, PATH_SPLIT, 2>(p, nclusters, st); break;
+      case 32: e = launch_kernel<16, PATH_SPLIT, 2>(p, nclusters, st); break;
+      case 64: e = launch_kernel<32, PATH_SPLIT, 2>(p, nclusters, st); break;
+      default: e = launch_kernel<32, PATH_SPLIT, 4>(p, nclusters, st); break;
     }
   }
   ++*launches;
