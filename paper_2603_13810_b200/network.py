@@ -40,6 +40,21 @@ class Network:
                 outs.append(x)
         return x, counts, outs, vfs
 
+    def capture(self, x: torch.Tensor):
+        """Record one forward on the static input buffer `x` as a CUDA graph (the
+        launch-bound small configs: one graph replay instead of 2 launches and a
+        host round of argument checks per layer).  Returns (graph, outputs of
+        forward); replaying the graph refreshes the outputs in place."""
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            self.forward(x)                      # warm-up outside the capture
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            outs = self.forward(x)
+        return graph, outs
+
     def launches_per_forward(self) -> int:
         """Kernels one forward launches (measured from the library's counter)."""
         return self._launches

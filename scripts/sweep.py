@@ -55,6 +55,21 @@ def time_forward(net, x, iters):
     return ms, layer_ms
 
 
+def time_graph(net, x, iters):
+    """Same forward replayed from a CUDA graph (Network.capture)."""
+    graph, _ = net.capture(x)
+    for _ in range(2):
+        graph.replay()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(iters):
+        graph.replay()
+    t1.record()
+    torch.cuda.synchronize()
+    return t0.elapsed_time(t1) / iters
+
+
 def density_check(iters, out):
     """Same layer (C4 layer 1: 128->128 @64x64, TAC-TP K=2), inputs of density
     0.01 vs 0.5: the conv is a dense contraction, so the time must not depend on
@@ -94,6 +109,7 @@ def main():
             net = network.Network(specs, configs.layer_weights(cfg))
             x = tacsnn.pack(configs.make_inputs(cfg, device="cuda"))
             ms, layer_ms = time_forward(net, x, a.iters)
+            graph_ms = time_graph(net, x, max(a.iters, 20)) if name in ("C1", "C2", "C3", "C4") else None
             frames = cfg.B * cfg.T
             if mode == "dense":
                 dense_ms[name] = ms
@@ -101,7 +117,9 @@ def main():
                     "ms_per_forward": ms, "frames_per_s": frames / (ms / 1e3),
                     "speedup_vs_dense": (dense_ms[name] / ms) if name in dense_ms else None,
                     "conv_calls_per_sample": configs.conv_calls(cfg, mode, K),
-                    "layer_ms": layer_ms, "engines": net.engines()}
+                    "layer_ms": layer_ms, "engines": net.engines(),
+                    "graph_ms_per_forward": graph_ms,
+                    "graph_frames_per_s": None if graph_ms is None else frames / (graph_ms / 1e3)}
             print(json.dumps(line), flush=True)
             out.write(json.dumps(line) + "\n")
             del net, x
