@@ -19,8 +19,12 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(ROOT, "build", "obj")
-LIB = os.path.join(PKG, "libtacsnn.so")
+# Variant builds for A/B timing: TACSNN_LIB_NAME=libtacsnn_x.so TACSNN_DEFS="-DFOO=1"
+# (load with TACSNN_LIB=<pkg>/libtacsnn_x.so); the default build is libtacsnn.so.
+_NAME = os.environ.get("TACSNN_LIB_NAME", "libtacsnn.so")
+_DEFS = os.environ.get("TACSNN_DEFS", "").split()
+OBJ = os.path.join(ROOT, "build", "obj" if _NAME == "libtacsnn.so" else "obj_" + _NAME.replace(".so", ""))
+LIB = os.path.join(PKG, _NAME)
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
@@ -45,7 +49,7 @@ def _compile(src, force, verbose, ptxas_v):
     if not force and os.path.exists(obj) and all(
             os.path.getmtime(obj) >= os.path.getmtime(d) for d in _deps(src)):
         return obj, ""
-    cmd = [nvcc(), *ARCH, *FLAGS, *(["-DTACSNN_TRACE"] if trace else []), "-c", src, "-o", obj]
+    cmd = [nvcc(), *ARCH, *FLAGS, *(["-DTACSNN_TRACE"] if trace else []), *_DEFS, "-c", src, "-o", obj]
     if ptxas_v:
         cmd += ["-Xptxas", "-v"]
     if verbose:

@@ -61,6 +61,12 @@ namespace {
 // per SM sub-partition, which is what the per-SMSP register file (16 K regs) and
 // the setmaxnreg budget below allow (a 21st warp would cap every warp at 80 regs).
 constexpr int kProdWarps = 3;
+#ifndef TACSNN_HALO_NR
+#define TACSNN_HALO_NR 2  // halo producer pixels per pass (K <= 4)
+#endif
+#ifndef TACSNN_HALO_MAP
+#define TACSNN_HALO_MAP 1  // 1: 8-thread groups own consecutive pixels of one word
+#endif
 // Warp layout: epilogue warps first (NPART channel parts x 4 TMEM lane quadrants),
 // then the MMA warp, then the producer warps.  The SM warp schedulers favour
 // higher warp ids, so the warps feeding the tensor pipe (MMA, producers) win
@@ -282,7 +288,11 @@ __device__ __forceinline__ void produce_halo(const TcParams &p, int tile, int k,
                                              int ptid) {
   constexpr int RB = K >= 8 ? 2 : (K >= 4 ? 4 : 8);
   const int nwin = p.Cin >> 5;
-  const int w = ptid % nwin, row0 = ptid / nwin, rstep = (kProdWarps * 32) / nwin;
+  // groups of 8 consecutive threads own 8 consecutive halo pixels of one 32-channel
+  // word w: their 16-B A-stage stores are contiguous (no bank conflicts) and their
+  // raw-halo loads (pixel stride nwin words, 4 words in a group) hit distinct banks
+  const int g8 = ptid >> 3, w = g8 % nwin, row0 = (g8 / nwin) * 8 + (ptid & 7);
+  const int rstep = (kProdWarps * 32) / nwin;
   int b, y0, x0;
   bool tok;
   tile_origin(p, tile, b, y0, x0, tok);
@@ -386,10 +396,67 @@ __device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t b, uint32_t d) {
   return r;
 }
 
+// beta = 1/2 aggregate by SWAR bit interleaving (K = 2, 4, 8): byte b of o[q] =
+// sum_j 2^j bit(x_j, q + 8b).  Frames are paired into 2-bit fields (e: even
+// channels, f: odd), pairs into 4-bit fields per channel class c % 4 (n[r]), and
+// nibbles split into bytes: 28 ops per 32-channel word for K = 4 instead of 64.
+__device__ __forceinline__ uint32_t bsel(uint32_t m, uint32_t a, uint32_t b) {  // (a & m) | (b & ~m)
+  return (a & m) | (b & ~m);
+}
+__device__ __forceinline__ void pair_fields(uint32_t x0, uint32_t x1, uint32_t &e, uint32_t &f) {
+  e = bsel(0x55555555u, x0, x1 << 1);  // channel 2i   -> bits 2i, 2i+1 = (x0, x1)
+  f = bsel(0x55555555u, x0 >> 1, x1);  // channel 2i+1 -> bits 2i, 2i+1
+}
+// 4 frames -> nibble words: n[r] holds channel 4k + r at bits 4k..4k+3
+__device__ __forceinline__ void quad_fields(const uint32_t *x, uint32_t (&n)[4]) {
+  uint32_t e, f, g, h;
+  pair_fields(x[0], x[1], e, f);
+  pair_fields(x[2], x[3], g, h);
+  n[0] = bsel(0x33333333u, e, g << 2);
+  n[2] = bsel(0x33333333u, e >> 2, g);
+  n[1] = bsel(0x33333333u, f, h << 2);
+  n[3] = bsel(0x33333333u, f >> 2, h);
+}
+template <int K>
+__device__ __forceinline__ void agg_word_swar(uint32_t (&o)[8], const uint32_t (&xj)[K]) {
+  static_assert(K == 2 || K == 4 || K == 8, "SWAR aggregate: K in {2, 4, 8}");
+  if constexpr (K == 2) {
+    uint32_t e, f;
+    pair_fields(xj[0], xj[1], e, f);
+#pragma unroll
+    for (int q = 0; q < 8; q += 2) {
+      o[q] = (e >> q) & 0x03030303u;
+      o[q + 1] = (f >> q) & 0x03030303u;
+    }
+  } else {
+    uint32_t n[4];
+    quad_fields(xj, n);
+    if constexpr (K == 8) {
+      uint32_t m[4];
+      quad_fields(xj + 4, m);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {  // frames 0-3 in the low nibble, 4-7 in the high one
+        o[r] = bsel(0x0F0F0F0Fu, n[r], m[r] << 4);
+        o[r + 4] = bsel(0x0F0F0F0Fu, n[r] >> 4, m[r]);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        o[r] = n[r] & 0x0F0F0F0Fu;
+        o[r + 4] = (n[r] >> 4) & 0x0F0F0F0Fu;
+      }
+    }
+  }
+}
+
 // o[q] (channels q + 8b at byte b) |= frame bit << e with a compile-time frame
 // shift e = j (beta = 1/2, or K = 1): one SHF + one LOP3 per (q, frame)
 template <int K>
 __device__ __forceinline__ void agg_word_m1(uint32_t (&o)[8], const uint32_t (&xj)[K]) {
+  if constexpr (K == 2 || K == 4 || K == 8) {
+    agg_word_swar<K>(o, xj);
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const uint32_t mask = 0x01010101u << j;
@@ -495,7 +562,7 @@ __device__ __forceinline__ int halo_c0(const TcParams &p, int x0) {
 }
 
 // TMA raw-halo producer (C_in = 32 nwin): thread owns 32-channel word w of halo
-// pixels row0, row0 + rstep, ...; two pixels per pass with all 2K smem loads
+// pixels row0, row0 + rstep, ...; NR pixels per pass with all NR K smem loads
 // issued before any arithmetic (one smem latency per pass).
 template <int K>
 __device__ __forceinline__ void produce_halo_tma(const TcParams &p, const uint32_t *raw,
@@ -503,36 +570,40 @@ __device__ __forceinline__ void produce_halo_tma(const TcParams &p, const uint32
   const int nwin = p.Cin >> 5, bw = p.raw_bw, fstride = kHaloH * p.raw_bw;
   const int c0 = halo_c0(p, x0);
   raw += c0 - (c0 & ~3);
-  const int w = ptid % nwin, row0 = ptid / nwin, rstep = (kProdWarps * 32) / nwin;
+  // groups of 8 consecutive threads own 8 consecutive halo pixels of one 32-channel
+  // word w: their 16-B A-stage stores are contiguous (no bank conflicts) and their
+  // raw-halo loads (pixel stride nwin words, 4 words in a group) hit distinct banks
+#if TACSNN_HALO_MAP
+  const int g8 = ptid >> 3, w = g8 % nwin, row0 = (g8 / nwin) * 8 + (ptid & 7);
+#else
+  const int w = ptid % nwin, row0 = ptid / nwin;
+#endif
+  const int rstep = (kProdWarps * 32) / nwin;
   const int mshift = p.m_shift;
   const uint32_t lbo = p.lbo_a;
-  constexpr int NR = K <= 4 ? 2 : 1;  // pixels per pass (register budget: 64 per producer thread)
+  constexpr int NR = K <= 4 ? TACSNN_HALO_NR : 2;  // pixels per pass (64 registers per producer thread)
 #pragma unroll 1
   for (int row = row0; row < kHaloRows; row += NR * rstep) {
-    const int row1 = row + rstep;
-    const bool two = NR == 2 && row1 < kHaloRows;
-    const int hy0 = row / kHaloW, hx0 = row - hy0 * kHaloW;
-    const int r1 = two ? row1 : row;
-    const int hy1 = r1 / kHaloW, hx1 = r1 - hy1 * kHaloW;
-    const uint32_t *src0 = raw + hy0 * bw + hx0 * nwin + w;
-    const uint32_t *src1 = raw + hy1 * bw + hx1 * nwin + w;
-    uint32_t x0j[K], x1j[K];
+    uint32_t x[NR][K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      x0j[j] = src0[j * fstride];
-      x1j[j] = NR == 2 ? src1[j * fstride] : 0u;
+    for (int r = 0; r < NR; ++r) {  // all NR x K smem loads first
+      const int rr = row + r * rstep;
+      const bool ok = rr < kHaloRows;
+      const int hy = ok ? rr / kHaloW : 0, hx = ok ? rr - hy * kHaloW : 0;
+      const uint32_t *src = raw + hy * bw + hx * nwin + w;
+#pragma unroll
+      for (int j = 0; j < K; ++j) x[r][j] = ok ? src[j * fstride] : 0u;
     }
-    uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (mshift == 1 || K == 1) agg_word_m1<K>(o, x0j); else agg_word_k<K>(o, x0j, mshift);
-    const uint32_t dst0 = a_stage + (uint32_t)(2 * w) * lbo + (uint32_t)row * 16u;
-    ptx::st_shared_v4(dst0, o[0], o[1], o[2], o[3]);
-    ptx::st_shared_v4(dst0 + lbo, o[4], o[5], o[6], o[7]);
-    if (two) {
-      uint32_t o1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      if (mshift == 1 || K == 1) agg_word_m1<K>(o1, x1j); else agg_word_k<K>(o1, x1j, mshift);
-      const uint32_t dst1 = a_stage + (uint32_t)(2 * w) * lbo + (uint32_t)row1 * 16u;
-      ptx::st_shared_v4(dst1, o1[0], o1[1], o1[2], o1[3]);
-      ptx::st_shared_v4(dst1 + lbo, o1[4], o1[5], o1[6], o1[7]);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int rr = row + r * rstep;
+      if (rr < kHaloRows) {
+        uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (mshift == 1 || K == 1) agg_word_m1<K>(o, x[r]); else agg_word_k<K>(o, x[r], mshift);
+        const uint32_t dst = a_stage + (uint32_t)(2 * w) * lbo + (uint32_t)rr * 16u;
+        ptx::st_shared_v4(dst, o[0], o[1], o[2], o[3]);
+        ptx::st_shared_v4(dst + lbo, o[4], o[5], o[6], o[7]);
+      }
     }
   }
 }

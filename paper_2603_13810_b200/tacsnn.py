@@ -16,6 +16,8 @@ import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libtacsnn.so")
+# A/B experiments: TACSNN_LIB=<path> loads a variant build (build.py TACSNN_LIB_NAME)
+LIB_PATH = os.environ.get("TACSNN_LIB", LIB_PATH)
 
 MODES = {"dense": 0, "tac": 1, "tactp": 2}
 RESETS = {"subtract": 0, "delayed": 1, "hard": 2}

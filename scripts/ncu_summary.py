@@ -29,17 +29,18 @@ KEYS = [
 def main():
     rep = sys.argv[1]
     rows = ncu_csv(rep, "--page", "raw")
-    hdr, units, vals = rows[0], rows[1], rows[2]
-    d = {h: (v, u) for h, v, u in zip(hdr, vals, units)}
-    print("kernel:", d.get("Kernel Name", ("?",))[0][:100])
-    for k in KEYS:
-        if k in d:
-            print(f"  {k:70s} {d[k][0]:>16s} {d[k][1]}")
-    stalls = {k: float(v[0] or 0) for k, v in d.items()
-              if k.startswith("smsp__average_warps_issue_stalled") and k.endswith("per_issue_active.ratio")}
-    print("  stall reasons (warps per issue):")
-    for k, v in sorted(stalls.items(), key=lambda kv: -kv[1])[:8]:
-        print(f"    {k.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', ''):24s} {v:.3f}")
+    hdr, units = rows[0], rows[1]
+    for vals in rows[2:]:                      # one row per profiled launch
+        d = {h: (v, u) for h, v, u in zip(hdr, vals, units)}
+        print("kernel:", d.get("Kernel Name", ("?",))[0][:100])
+        for k in KEYS:
+            if k in d:
+                print(f"  {k:70s} {d[k][0]:>16s} {d[k][1]}")
+        stalls = {k: float(v[0] or 0) for k, v in d.items()
+                  if k.startswith("smsp__average_warps_issue_stalled") and k.endswith("per_issue_active.ratio")}
+        print("  stall reasons (warps per issue):")
+        for k, v in sorted(stalls.items(), key=lambda kv: -kv[1])[:8]:
+            print(f"    {k.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', ''):24s} {v:.3f}")
     if "--sass" in sys.argv:
         rows = ncu_csv(rep, "--page", "source", "--print-source", "sass")
         hdr = rows[1]
