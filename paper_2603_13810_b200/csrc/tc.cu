@@ -725,20 +725,27 @@ __device__ __forceinline__ void h16_init_stages(const TcParams &p, uint32_t sbas
 struct RawLoader {
   int ipair, ik;  // next (pair, group) to load
   uint32_t n;     // loads issued
+  int b, ty, tx;  // tile coordinates of ipair (advanced incrementally: no divisions per load)
+  int db, dty, dtx;
   __device__ __forceinline__ void issue(const TcParams &p, uint32_t sbase, uint32_t bar_raw,
-                                        int ncl, uint32_t rank) {
+                                        int ncl) {
     const uint32_t slot = n % (uint32_t)p.nraw;
-    int b, y0, x0;
-    bool tok;
-    tile_origin(p, 2 * ipair + (int)rank, b, y0, x0, tok);
+    const int x0 = tx * kTileW;
     const int c0 = halo_c0(p, x0) & ~3;  // 16-B aligned box start
     const uint32_t bar = bar_raw + 8 * slot;
     ptx::mbar_arrive_expect_tx(bar, p.raw_box_bytes);
-    ptx::tma_load_4d(sbase + p.off_raw + slot * p.raw_stage_bytes, &p.tmap, c0, y0 - p.pad, b,
+    ptx::tma_load_4d(sbase + p.off_raw + slot * p.raw_stage_bytes, &p.tmap, c0, ty * kTileH - p.pad, b,
                      ik * p.K, bar);
     if (++ik == p.G) {
       ik = 0;
       ipair += ncl;
+      tx += dtx;
+      int cy = tx >= p.tiles_x;
+      tx -= cy ? p.tiles_x : 0;
+      ty += dty + cy;
+      cy = ty >= p.tiles_y;
+      ty -= cy ? p.tiles_y : 0;
+      b += db + cy;
     }
     ++n;
   }
@@ -749,16 +756,23 @@ struct RawLoader {
     ipair = cid;
     ik = 0;
     n = 0;
-    for (int r = 0; r < p.nraw && more(p); ++r) issue(p, sbase, bar_raw, ncl, rank);
+    const int per = p.tiles_x * p.tiles_y, t0 = 2 * cid + (int)rank, dt = 2 * ncl;
+    b = t0 / per;
+    ty = (t0 - b * per) / p.tiles_x;
+    tx = t0 - b * per - ty * p.tiles_x;
+    db = dt / per;
+    dty = (dt - db * per) / p.tiles_x;
+    dtx = dt - db * per - dty * p.tiles_x;
+    for (int r = 0; r < p.nraw && more(p); ++r) issue(p, sbase, bar_raw, ncl);
   }
   // after consumption `it` of slot it % nraw: wait until every producer warp is done
   // with it, then refill the slot
   __device__ __forceinline__ void refill(const TcParams &p, uint32_t sbase, uint32_t bar_raw,
-                                         uint32_t bar_raw_empty, uint32_t it, int ncl, uint32_t rank) {
+                                         uint32_t bar_raw_empty, uint32_t it, int ncl) {
     if (!more(p)) return;
     const uint32_t nr = (uint32_t)p.nraw;
     ptx::mbar_wait(bar_raw_empty + 8 * (it % nr), (it / nr) & 1u);
-    issue(p, sbase, bar_raw, ncl, rank);
+    issue(p, sbase, bar_raw, ncl);
   }
 };
 
@@ -1579,7 +1593,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
       if (p.use_tma && lane == 0) loader.start(p, sbase, bar_raw, cid, ncl, rank);
       if (rank != 0 && p.use_tma && lane == 0) {
         const uint32_t total = (uint32_t)((p.num_pairs - cid + ncl - 1) / ncl) * (uint32_t)p.G;
-        for (uint32_t it = 0; it < total; ++it) loader.refill(p, sbase, bar_raw, bar_raw_empty, it, ncl, rank);
+        for (uint32_t it = 0; it < total; ++it) loader.refill(p, sbase, bar_raw, bar_raw_empty, it, ncl);
       }
       if (rank == 0) {
         const uint32_t idesc = ptx::idesc_i8(256, p.n_total);
@@ -1627,7 +1641,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
             }
             __syncwarp();
             if (lane == 0) trace_mark(p, it, TR_MMA_ISSUED);
-            if (p.use_tma && lane == 0) loader.refill(p, sbase, bar_raw, bar_raw_empty, it, ncl, rank);
+            // lane 0 refills the raw-halo slot group `it` consumed (cheap: incremental tile
+            // coordinates, the wait on raw_empty has long completed)
+            if (p.use_tma && lane == 0) loader.refill(p, sbase, bar_raw, bar_raw_empty, it, ncl);
             __syncwarp();
           }
         }

@@ -25,9 +25,11 @@ def main():
     ap.add_argument("--layer", type=int, default=0)
     ap.add_argument("--B", type=int, default=256)
     ap.add_argument("--rows", type=int, default=24)
+    ap.add_argument("--mode", default=None)
+    ap.add_argument("--K", type=int, default=None)
     a = ap.parse_args()
     cfg = configs.CONFIGS[a.config]
-    spec = configs.layer_plan(cfg, B=a.B)[a.layer]
+    spec = configs.layer_plan(cfg, mode=a.mode, K=a.K, B=a.B)[a.layer]
     w, b = configs.layer_weights(cfg)[a.layer]
     prep = tacsnn.prepare_weights(spec, w, b)
     g = torch.Generator(device="cuda").manual_seed(0)
