@@ -284,7 +284,8 @@ def main():
         for li, (spec, prep) in enumerate(zip(net.specs, net.prepared)):
             s = spec if spec.B == B_ else spec.replace(B=B_)
             ev[i][li][0].record(stream)
-            xin, _, cnt = tacsnn.conv_lif(s, prep, xin)
+            # the spike-count readout of the final layer only, as Network.forward
+            xin, _, cnt = tacsnn.conv_lif(s, prep, xin, want_counts=(li == nL - 1))
             ev[i][li][1].record(stream)
         gather(xin, cnt)
         return xin

@@ -64,6 +64,9 @@ constexpr int kProdWarps = 3;
 #ifndef TACSNN_HALO_NR
 #define TACSNN_HALO_NR 2  // halo producer pixels per pass (K <= 4)
 #endif
+#ifndef TACSNN_UNIFORM_WARP
+#define TACSNN_UNIFORM_WARP 1
+#endif
 #ifndef TACSNN_HALO_MAP
 #define TACSNN_HALO_MAP 1  // 1: 8-thread groups own consecutive pixels of one word
 #endif
@@ -1199,8 +1202,10 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
       uint32_t spk[NS];
 #pragma unroll
       for (int j = 0; j < NS; ++j) spk[j] = ~nsp[j] & vmask;
-      // per-lane bit-sliced spike counters (pre-pool, valid pixels only)
-      if (NS == 1) {
+      // per-lane bit-sliced spike counters (pre-pool, valid pixels only; skipped when
+      // the caller asked for no counts)
+      if (!p.counts) {
+      } else if (NS == 1) {
         uint32_t cy = spk[0];
 #pragma unroll
         for (int pl = 0; pl < kPlanes; ++pl) {
@@ -1513,7 +1518,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
   constexpr int kThreads = kernel_threads(NPART);
   constexpr int kEpiWarps = epi_warps(NPART);
   extern __shared__ __align__(1024) uint8_t smem[];
+  // warp index broadcast from lane 0: the compiler then knows it is warp-uniform and keeps
+  // the role / TMEM-address arithmetic derived from it in uniform registers
+#if TACSNN_UNIFORM_WARP
+  const uint32_t warp = __shfl_sync(0xFFFFFFFFu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31;
+#else
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#endif
   const uint32_t rank = ptx::cluster_ctarank();
   const uint32_t sbase = ptx::smem_u32(smem);
   const uint32_t bar_a_full = sbase + p.off_bar;

@@ -25,15 +25,18 @@ class Network:
         return [s.engine_used() for s in self.specs]
 
     def forward(self, x: torch.Tensor, keep: bool = False, want_v_final: bool = False,
-                want_counts: bool = True):
+                want_counts: bool | str = "last"):
         """x: packed int32 [T, B, H, WPR] on the device.  Returns (final spikes,
-        per-layer counts, per-layer outputs if keep, per-layer v_final if asked)."""
+        per-layer counts, per-layer outputs if keep, per-layer v_final if asked).
+        want_counts: True (every layer), "last" (only the final layer's spike-count
+        readout; the others are None) or False."""
         B = x.shape[1]
         counts, outs, vfs = [], [], []
-        for spec, prep in zip(self.specs, self.prepared):
+        n = len(self.specs)
+        for i, (spec, prep) in enumerate(zip(self.specs, self.prepared)):
             s = spec if spec.B == B else spec.replace(B=B)
-            x, vf, cnt = tacsnn.conv_lif(s, prep, x, want_v_final=want_v_final,
-                                         want_counts=want_counts)
+            wc = want_counts is True or (want_counts == "last" and i == n - 1)
+            x, vf, cnt = tacsnn.conv_lif(s, prep, x, want_v_final=want_v_final, want_counts=wc)
             counts.append(cnt)
             vfs.append(vf)
             if keep:

@@ -246,7 +246,7 @@ def test_c5_full_size_sampled(T, O):
     weights = configs.layer_weights(cfg)
     net = network.Network(specs, weights)
     x = T.pack(configs.make_inputs(cfg, device="cuda"))
-    _, counts, outs, _ = net.forward(x, keep=True)
+    _, counts, outs, _ = net.forward(x, keep=True, want_counts=True)
     torch.cuda.synchronize()
     rng = np.random.default_rng(0)
     samples = [0, cfg.B - 1] + sorted(rng.choice(np.arange(1, cfg.B - 1), 2, replace=False).tolist())
