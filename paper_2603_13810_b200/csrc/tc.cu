@@ -64,6 +64,9 @@ constexpr int kProdWarps = 3;
 #ifndef TACSNN_HALO_NR
 #define TACSNN_HALO_NR 2  // halo producer pixels per pass (K <= 4)
 #endif
+#ifndef TACSNN_H16_ACCS
+#define TACSNN_H16_ACCS 3  // TMEM accumulators on the fp16 paths (2 or 3)
+#endif
 #ifndef TACSNN_UNIFORM_WARP
 #define TACSNN_UNIFORM_WARP 1
 #endif
@@ -77,7 +80,7 @@ constexpr int kProdWarps = 3;
 constexpr int epi_warps(int npart) { return 4 * npart; }
 constexpr int kernel_threads(int npart) { return 32 * (1 + kProdWarps + epi_warps(npart)); }
 constexpr int kMaxStages = 3;
-constexpr int kAccs = 2;
+constexpr int kAccs = 3;  // max TMEM accumulators (p.naccs: 3 on the fp16 paths, 2 on int8)
 constexpr int kMaxSteps = 8;
 constexpr int kPlanes = 6;  // bit-sliced spike counters (<= 63 steps per flush)
 constexpr int kTileH = 16, kTileW = 8;                 // output pixels per CTA tile
@@ -103,6 +106,7 @@ struct TcParams {
   uint32_t off_w, off_a, a_stage_bytes, off_scale, off_bar, smem_bytes;
   uint32_t w_bytes_cta, tmem_cols, n_total, lbo_a, sbo_a, lbo_b;
   int tap_off[9];
+  int naccs;             // TMEM accumulators in the MMA -> epilogue ring
   int split;             // A carried as fp16 hi + lo from the 2^K-entry table lut
   uint32_t off_lut;      // smem copy of lut
   uint32_t lut[1 << 8];  // idx (bit j = frame j's spike) -> fp16 A_hi | fp16 A_lo << 16
@@ -1083,7 +1087,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
   const bool pooled = p.pool == 2;
   const bool active_half = co_base < Cout;
   // CTA 0's TMEM-empty barriers, mapped once
-  const uint32_t t_empty0 = ptx::mapa_cluster(bar_t_empty, 0), t_empty1 = ptx::mapa_cluster(bar_t_empty + 8, 0);
+  const uint32_t t_empty_remote = ptx::mapa_cluster(bar_t_empty, 0);  // CTA 0's TMEM-empty barriers
   uint32_t it = 0;
   for (int pair = cid; pair < p.num_pairs; pair += ncl) {
     const int tile = 2 * pair + (int)rank;
@@ -1102,7 +1106,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
                      (NCH >= 32 ? (long long)xo * nwo + half : (obit >> 5));
     const int osh = NCH >= 32 ? 0 : (int)(obit & 31);
     float2 U[UT ? 1 : NCH / 2];
-    const uint32_t ucol = tmem_base + lane_addr + 2u * p.n_total + (uint32_t)co_base;
+    const uint32_t ucol = tmem_base + lane_addr + (uint32_t)p.naccs * p.n_total + (uint32_t)co_base;
 #pragma unroll
     for (int ch = 0; ch < NCHUNK; ++ch) {
       uint32_t ub[8];
@@ -1124,7 +1128,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
     for (int pl = 0; pl < kPlanes; ++pl) planes[pl] = 0u;
     int steps_acc = 0;
     for (int k = 0; k < G; ++k, ++it) {
-      const uint32_t acc = it % kAccs, aph = (it / kAccs) & 1u;
+      const uint32_t acc = it % p.naccs, aph = (it / p.naccs) & 1u;
       ptx::mbar_wait(bar_t_full + 8 * acc, aph);
       ptx::tc_fence_after();
       if (e == 0 && lane == 0) trace_mark(p, it, TR_EPI_FULL);
@@ -1196,7 +1200,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
       if (UT) ptx::tmem_wait_st();
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_remote_relaxed(acc ? t_empty1 : t_empty0);
+      if (lane == 0) ptx::mbar_arrive_remote_relaxed(t_empty_remote + 8 * acc);
       if (e == 0 && lane == 0) trace_mark(p, it, TR_EPI_RELEASED);
 
       uint32_t spk[NS];
@@ -1338,7 +1342,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
       }
     }
     for (int k = 0; k < G; ++k, ++it) {
-      const uint32_t acc = it % kAccs, aph = (it / kAccs) & 1u;
+      const uint32_t acc = it % p.naccs, aph = (it / p.naccs) & 1u;
       ptx::mbar_wait(bar_t_full + 8 * acc, aph);
       ptx::tc_fence_after();
       if (e == 0 && lane == 0) trace_mark(p, it, TR_EPI_FULL);
@@ -1618,7 +1622,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
         for (int pair = cid; pair < p.num_pairs; pair += ncl) {
           for (int k = 0; k < p.G; ++k, ++it) {
             const uint32_t s = it % ns, ph = (it / ns) & 1u;
-            const uint32_t acc = it % kAccs, aph = (it / kAccs) & 1u;
+            const uint32_t acc = it % p.naccs, aph = (it / p.naccs) & 1u;
             ptx::mbar_wait(bar_t_empty + 8 * acc, aph ^ 1u);
             ptx::mbar_wait(bar_a_full + 8 * s, ph);
             ptx::tc_fence_after();
@@ -1943,7 +1947,10 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   p.n_total = g.path == PATH_HALO ? 2u * g.cout_pad : (uint32_t)g.cout_pad;  // TMEM columns / acc
   uint32_t cols = 32;
   const bool ut = g.path == PATH_H16 && g.cout_pad == 128;  // u_in_tmem(): U after the accumulators
-  while (cols < 2u * p.n_total + (ut ? 128u : 0u)) cols <<= 1;
+  // accumulators: 3 on the fp16 paths (n_total = C_out_pad; with U in TMEM 3 x 128 +
+  // 128 = 512 columns), 2 on the int8 path (n_total = 2 C_out_pad)
+  p.naccs = g.path == PATH_HALO ? 2 : TACSNN_H16_ACCS;
+  while (cols < (uint32_t)p.naccs * p.n_total + (ut ? 128u : 0u)) cols <<= 1;
   p.tmem_cols = cols;
   p.lbo_a = (uint32_t)kHaloRows * 16u;  // between 16-byte K chunks
   p.sbo_a = (uint32_t)kHaloW * 16u;     // between tile rows (8-row core-matrix groups)
