@@ -273,6 +273,18 @@ __device__ __forceinline__ void tile_origin(const TcParams &p, int tile, int &b,
   ok = tile < p.num_tiles;
 }
 
+// circular-buffer position (slot, phase parity) advanced by one per use: no integer
+// division by the runtime ring sizes in the role loops
+struct Ring {
+  uint32_t i = 0, ph = 0;
+  __device__ __forceinline__ void next(uint32_t n) {
+    if (++i == n) {
+      i = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
 // --- producers: build the u8 aggregate A_k * 2^{m(K-1)} in the MMA layout ---
 // byte b of output word q <- input channel (q + 8b) of a 32-channel word; bit
 // e_j = m*j of that byte <- frame j (weights 2^{m j}, oldest frame = 1)
@@ -734,14 +746,16 @@ struct RawLoader {
   uint32_t n;     // loads issued
   int b, ty, tx;  // tile coordinates of ipair (advanced incrementally: no divisions per load)
   int db, dty, dtx;
+  Ring slot, rel;  // slot of the next load; raw_empty phase of the next refill
   __device__ __forceinline__ void issue(const TcParams &p, uint32_t sbase, uint32_t bar_raw,
                                         int ncl) {
-    const uint32_t slot = n % (uint32_t)p.nraw;
+    const uint32_t sl = slot.i;
+    slot.next((uint32_t)p.nraw);
     const int x0 = tx * kTileW;
     const int c0 = halo_c0(p, x0) & ~3;  // 16-B aligned box start
-    const uint32_t bar = bar_raw + 8 * slot;
+    const uint32_t bar = bar_raw + 8 * sl;
     ptx::mbar_arrive_expect_tx(bar, p.raw_box_bytes);
-    ptx::tma_load_4d(sbase + p.off_raw + slot * p.raw_stage_bytes, &p.tmap, c0, ty * kTileH - p.pad, b,
+    ptx::tma_load_4d(sbase + p.off_raw + sl * p.raw_stage_bytes, &p.tmap, c0, ty * kTileH - p.pad, b,
                      ik * p.K, bar);
     if (++ik == p.G) {
       ik = 0;
@@ -763,6 +777,8 @@ struct RawLoader {
     ipair = cid;
     ik = 0;
     n = 0;
+    slot = Ring();
+    rel = Ring();
     const int per = p.tiles_x * p.tiles_y, t0 = 2 * cid + (int)rank, dt = 2 * ncl;
     b = t0 / per;
     ty = (t0 - b * per) / p.tiles_x;
@@ -776,9 +792,10 @@ struct RawLoader {
   // with it, then refill the slot
   __device__ __forceinline__ void refill(const TcParams &p, uint32_t sbase, uint32_t bar_raw,
                                          uint32_t bar_raw_empty, uint32_t it, int ncl) {
+    (void)it;  // refills come in consumption order: rel tracks it % nraw and its phase
     if (!more(p)) return;
-    const uint32_t nr = (uint32_t)p.nraw;
-    ptx::mbar_wait(bar_raw_empty + 8 * (it % nr), (it / nr) & 1u);
+    ptx::mbar_wait(bar_raw_empty + 8 * rel.i, rel.ph);
+    rel.next((uint32_t)p.nraw);
     issue(p, sbase, bar_raw, ncl);
   }
 };
@@ -796,13 +813,15 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
   const uint32_t ns = (uint32_t)p.nstages, nr = (uint32_t)p.nraw;
   if (PATH != PATH_HALO) h16_init_stages(p, sbase, ptid);  // fenced with the first stage
   uint32_t it = 0;
+  Ring st, rw;
   for (int pair = cid; pair < p.num_pairs; pair += ncl) {
     int b, y0, x0;
     bool tok;
     tile_origin(p, 2 * pair + (int)rank, b, y0, x0, tok);
     for (int k = 0; k < p.G; ++k, ++it) {
-      const uint32_t s = it % ns, ph = (it / ns) & 1u;
-      const uint32_t r = it % nr, rph = (it / nr) & 1u;
+      const uint32_t s = st.i, ph = st.ph, r = rw.i, rph = rw.ph;
+      st.next(ns);
+      rw.next(nr);
       ptx::mbar_wait(bar_raw + 8 * r, rph);
       if (ptid == 0) trace_mark(p, it, TR_PROD_RAW);
       ptx::mbar_wait(bar_a_empty + 8 * s, ph ^ 1u);
@@ -838,10 +857,12 @@ __device__ __forceinline__ void producer_role(const TcParams &p, uint32_t sbase,
   const uint32_t *lut = reinterpret_cast<const uint32_t *>(smem + p.off_lut);
   const uint32_t ns = (uint32_t)p.nstages;
   uint32_t it = 0;
+  Ring st;
   for (int pair = cid; pair < p.num_pairs; pair += ncl) {
     const int tile = 2 * pair + (int)rank;
     for (int k = 0; k < p.G; ++k, ++it) {
-      const uint32_t s = it % ns, ph = (it / ns) & 1u;
+      const uint32_t s = st.i, ph = st.ph;
+      st.next(ns);
       ptx::mbar_wait(bar_a_empty + 8 * s, ph ^ 1u);
       const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
       if (PATH == PATH_HALO)
@@ -1089,6 +1110,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
   // CTA 0's TMEM-empty barriers, mapped once
   const uint32_t t_empty_remote = ptx::mapa_cluster(bar_t_empty, 0);  // CTA 0's TMEM-empty barriers
   uint32_t it = 0;
+  Ring ar;
   for (int pair = cid; pair < p.num_pairs; pair += ncl) {
     const int tile = 2 * pair + (int)rank;
     int b, y0, x0;
@@ -1128,7 +1150,8 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
     for (int pl = 0; pl < kPlanes; ++pl) planes[pl] = 0u;
     int steps_acc = 0;
     for (int k = 0; k < G; ++k, ++it) {
-      const uint32_t acc = it % p.naccs, aph = (it / p.naccs) & 1u;
+      const uint32_t acc = ar.i, aph = ar.ph;
+      ar.next((uint32_t)p.naccs);
       ptx::mbar_wait(bar_t_full + 8 * acc, aph);
       ptx::tc_fence_after();
       if (e == 0 && lane == 0) trace_mark(p, it, TR_EPI_FULL);
@@ -1304,6 +1327,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
   const bool pooled = p.pool == 2;
   const bool active_half = co_base < Cout;
   uint32_t it = 0;
+  Ring ar;
   for (int pair = cid; pair < p.num_pairs; pair += ncl) {
     const int tile = 2 * pair + (int)rank;
     int b, y0, x0;
@@ -1342,7 +1366,8 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
       }
     }
     for (int k = 0; k < G; ++k, ++it) {
-      const uint32_t acc = it % p.naccs, aph = (it / p.naccs) & 1u;
+      const uint32_t acc = ar.i, aph = ar.ph;
+      ar.next((uint32_t)p.naccs);
       ptx::mbar_wait(bar_t_full + 8 * acc, aph);
       ptx::tc_fence_after();
       if (e == 0 && lane == 0) trace_mark(p, it, TR_EPI_FULL);
@@ -1619,10 +1644,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
         const int nkc = p.nkc, nkc2 = p.nkc >> 1;
         const uint32_t ns = (uint32_t)p.nstages;
         uint32_t it = 0;
+        Ring st, ar;
         for (int pair = cid; pair < p.num_pairs; pair += ncl) {
           for (int k = 0; k < p.G; ++k, ++it) {
-            const uint32_t s = it % ns, ph = (it / ns) & 1u;
-            const uint32_t acc = it % p.naccs, aph = (it / p.naccs) & 1u;
+            const uint32_t s = st.i, ph = st.ph, acc = ar.i, aph = ar.ph;
+            st.next(ns);
+            ar.next((uint32_t)p.naccs);
             ptx::mbar_wait(bar_t_empty + 8 * acc, aph ^ 1u);
             ptx::mbar_wait(bar_a_full + 8 * s, ph);
             ptx::tc_fence_after();
