@@ -64,6 +64,12 @@ constexpr int kProdWarps = 3;
 #ifndef TACSNN_HALO_NR
 #define TACSNN_HALO_NR 2  // halo producer pixels per pass (K <= 4)
 #endif
+#ifndef TACSNN_BDESC_OPAQUE
+#define TACSNN_BDESC_OPAQUE 1
+#endif
+#ifndef TACSNN_UT_MIN_NS
+#define TACSNN_UT_MIN_NS 4  // U in TMEM for the fp16 paths from this many LIF steps per group
+#endif
 #ifndef TACSNN_H16_ACCS
 #define TACSNN_H16_ACCS 3  // TMEM accumulators on the fp16 paths (2 or 3)
 #endif
@@ -168,9 +174,10 @@ bool split_of(const tac_conv_lif_desc *d) {
 constexpr int kMaxSplitK = 8;  // 2^K-entry table
 
 int path_of(const tac_conv_lif_desc *d) {
-  if (split_of(d)) return PATH_H16;
+  if (split_of(d)) return PATH_H16;  // (kernel template PATH_SPLIT)
   return (d->C_in % 32 == 0) ? PATH_HALO : PATH_H16;
 }
+
 
 // 16-B K chunks (8 fp16 channels) per halo pixel of the fp16 path: channels
 // [A (C_in) | bias 1.0] or, split, [A_hi (C_in) | A_lo (C_in) | bias 1.0]; even
@@ -229,7 +236,7 @@ Geometry geometry(const tac_conv_lif_desc *d, bool use_tma = false) {
     g.off_raw = align_up(g.off_a + g.nstages * g.a_stage_bytes, 128);
     g.off_scale = align_up(g.off_raw + g.nraw * g.raw_stage_bytes, 128);
     g.off_lut = align_up(g.off_scale + 4u * g.cout_pad * 4u, 16);
-    g.off_bar = align_up(g.off_lut + (g.split ? 4u << kMaxSplitK : 0u), 64);
+    g.off_bar = align_up(g.off_lut + (g.split ? 4u << kMaxSplitK : 0u), 64);  // split: 2^K table
     g.smem_bytes = g.off_bar + 8u * kNumBars + 16u;
     if (g.smem_bytes <= kSmemLimit) break;
   }
@@ -842,7 +849,7 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        ptx::mbar_arrive_local(bar_raw_empty + 8 * r);  // this warp's smem reads of raw stage r are done
+        ptx::mbar_arrive_local(bar_raw_empty + 8 * r);  // this warp's reads of raw stage r are done
         ptx::mbar_arrive_cluster_cta(bar_a_full + 8 * s, 0);
       }
       if (ptid == 0) trace_mark(p, it, TR_PROD_DONE);
@@ -1089,7 +1096,8 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
   static_assert(NCH <= 32, "one spike word per thread");
   constexpr int NCHUNK = NCH / 8;
   constexpr bool F16 = PATH != PATH_HALO;
-  constexpr bool UT = u_in_tmem<NCH, PATH, NPART>();
+  // (U in TMEM only pays when the K LIF steps per group make registers scarce)
+  constexpr bool UT = u_in_tmem<NCH, PATH, NPART>() && NS >= TACSNN_UT_MIN_NS;
   constexpr bool LD32 = false;  // F16 && NCH == 32 (one 32-column load) spills at 104 regs
   constexpr int NBUF = (NPART == 2 || (F16 && NS <= 4)) ? 2 : 1;  // TMEM prefetch depth (registers)
   const float *sc = reinterpret_cast<const float *>(smem + p.off_scale);
@@ -1639,7 +1647,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
         const uint32_t idesc = ptx::idesc_i8(256, p.n_total);
         const uint32_t nhb16 = p.lbo_b >> 4;                        // B rows of this CTA x 16 B
         const uint64_t a_desc0 = ptx::smem_desc(sbase + p.off_a, p.lbo_a, p.sbo_a);
+#if TACSNN_BDESC_OPAQUE
+        const uint64_t b_desc0_ = ptx::smem_desc(sbase + p.off_w, p.lbo_b, 128u);
+#else
         const uint64_t b_desc0 = ptx::smem_desc(sbase + p.off_w, p.lbo_b, 128u);
+#endif
         const uint32_t lbo16 = p.lbo_a >> 4, stage16 = p.a_stage_bytes >> 4;
         const int nkc = p.nkc, nkc2 = p.nkc >> 1;
         const uint32_t ns = (uint32_t)p.nstages;
@@ -1655,6 +1667,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
             ptx::tc_fence_after();
             if (lane == 0) trace_mark(p, it, TR_MMA_READY);
             const uint64_t a_base = a_desc0 + (uint64_t)(s * stage16);
+#if TACSNN_BDESC_OPAQUE
+            // launder the (loop-invariant) B base through an opaque move each group: the
+            // compiler then derives the per-MMA B descriptors in uniform registers next to
+            // the MMAs instead of hoisting 9-18 of them into vector registers (R2UR each)
+            uint64_t b_desc0 = b_desc0_;
+            asm volatile("mov.b64 %0, %0;" : "+l"(b_desc0));
+#endif
             const uint32_t d_tmem = tmem_base + acc * p.n_total;
             if (ptx::elect_one()) {
               if (PATH == PATH_HALO) {
@@ -1973,7 +1992,7 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   p.smem_bytes = g.smem_bytes; p.w_bytes_cta = g.w_bytes_cta;
   p.n_total = g.path == PATH_HALO ? 2u * g.cout_pad : (uint32_t)g.cout_pad;  // TMEM columns / acc
   uint32_t cols = 32;
-  const bool ut = g.path == PATH_H16 && g.cout_pad == 128;  // u_in_tmem(): U after the accumulators
+  const bool ut = g.path != PATH_HALO && g.cout_pad == 128;  // u_in_tmem(): U after the accumulators
   // accumulators: 3 on the fp16 paths (n_total = C_out_pad; with U in TMEM 3 x 128 +
   // 128 = 512 columns), 2 on the int8 path (n_total = 2 C_out_pad)
   p.naccs = g.path == PATH_HALO ? 2 : TACSNN_H16_ACCS;
