@@ -69,7 +69,7 @@
 extern "C" {
 #endif
 
-#define TACSNN_ABI_VERSION 1
+#define TACSNN_ABI_VERSION 2 /* 2: input_kind + tac_conv_lif_forward_real */
 
 typedef enum { TAC_MODE_DENSE = 0, TAC_MODE_TAC = 1, TAC_MODE_TACTP = 2 } tac_mode;
 
@@ -78,6 +78,12 @@ typedef enum {
   TAC_RESET_SUBTRACT_DELAYED = 1, /* Eq. (1): V_t = bV_{t-1} + I_t - v_th s_{t-1} */
   TAC_RESET_HARD = 2              /* V = v_reset on spike                         */
 } tac_reset;
+
+/* What the layer reads (desc.input_kind).  REAL is the continuous-valued first
+ * layer of the paper's DVS network (log-normalised event counts):
+ * A_k = sum_j beta^{K-1-j} X_{kK+j} is then real-valued and the conv of the
+ * aggregate is still exact by linearity. */
+typedef enum { TAC_INPUT_SPIKES = 0, TAC_INPUT_REAL = 1 } tac_input;
 
 typedef enum {
   TAC_ENGINE_AUTO = 0,    /* TCGEN05 when the layer qualifies, else SIMT        */
@@ -110,8 +116,10 @@ typedef struct tac_conv_lif_desc {
   int32_t reset;                    /* tac_reset                                    */
   int32_t out_pool;                 /* 1 = none, 2 = fused 2x2 OR-pool (even H', W') */
   int32_t engine;                   /* tac_engine                                   */
-  int64_t in_stride_t, in_stride_b; /* u32 words; 0 = packed default               */
+  int64_t in_stride_t, in_stride_b; /* u32 words (REAL input: floats); 0 = default  */
   int64_t out_stride_t, out_stride_b;
+  int32_t input_kind;               /* tac_input (0 = packed spikes)                */
+  int32_t reserved0;                /* must be 0                                    */
 } tac_conv_lif_desc;
 
 /* Validate a descriptor (no device access).  TAC_OK or the first violation. */
@@ -153,6 +161,20 @@ tac_status tac_conv_lif_forward(const tac_conv_lif_desc *desc, const void *prepa
                                 uint32_t *spikes_out, float *v_final,
                                 uint32_t *counts, void *ws, size_t ws_bytes,
                                 void *stream);
+
+/* The same layer on a continuous-valued input (desc.input_kind = TAC_INPUT_REAL;
+ * tac_conv_lif_forward rejects such a descriptor and this call rejects spikes):
+ *   x_in  device fp32 [T][B][H][W][C_in] (channels last, 4-B aligned); the t and b
+ *         strides (desc.in_stride_t / in_stride_b) are in floats, 0 = contiguous
+ *         (H*W*C_in, B*H*W*C_in).
+ * Everything else (prepared weights from a descriptor with the same input_kind,
+ * outputs, errors, ordering) as tac_conv_lif_forward.  tcgen05 takes C_in <= 2
+ * (the aggregate is carried as fp16 hi + lo, |error| <= 2^-22 |A|); the SIMT engine
+ * any shape. */
+tac_status tac_conv_lif_forward_real(const tac_conv_lif_desc *desc, const void *prepared,
+                                     const float *x_in, const float *v_init,
+                                     uint32_t *spikes_out, float *v_final, uint32_t *counts,
+                                     void *ws, size_t ws_bytes, void *stream);
 
 /* u8 {0,1} [T][B][C][H][W] (device) <-> packed [T][B][H][WPR] (device).
  * pack treats any non-zero byte as a spike. */

@@ -50,6 +50,8 @@ def lib():
             L.tac_oracle_forward.argtypes = [P, P, P] + [i] * 12 + [d, d, d, i] + \
                 [P, P, P, P, P, d, P, P]
             L.tac_oracle_forward.restype = i
+            L.tac_oracle_forward_x.argtypes = L.tac_oracle_forward.argtypes
+            L.tac_oracle_forward_x.restype = i
             L.tac_oracle_conv2d.argtypes = [P, P, P] + [i] * 9 + [P]
             L.tac_oracle_conv2d.restype = i
             L.tac_oracle_or_pool2.argtypes = [P, i, i, i, i, P]
@@ -88,7 +90,9 @@ def conv2d(X, Wt, bias=None, stride=1, pad=0):
 
 def forward(S, Wt, bias=None, *, K=1, mode="tac", beta=0.9, v_th=1.0, v_reset=0.0,
             reset="subtract", stride=1, pad=0, v_init=None, replay=None, band=1e-3):
-    """One Conv-LIF layer (Eq. 1 / Alg. 1 / Alg. 2) on u8 spikes S [T,B,Cin,H,W].
+    """One Conv-LIF layer (Eq. 1 / Alg. 1 / Alg. 2) on u8 spikes S [T,B,Cin,H,W]
+    or, when S is a floating array, on continuous-valued input frames (computed
+    in fp64; the DVS first layer's log-normalised counts).
 
     Returns dict(out u8 [T_out,B,Cout,Ho,Wo], v_final f64 [B,Cout,Ho,Wo],
     counts i64 [B,Cout], mismatch, excused).  ``beta``/``v_th``/``v_reset`` are
@@ -96,7 +100,8 @@ def forward(S, Wt, bias=None, *, K=1, mode="tac", beta=0.9, v_th=1.0, v_reset=0.
     used in fp64.  With ``replay`` (device spikes, same layout as out) the
     trajectory follows the replay protocol described in tac_oracle.c.
     """
-    S = np.ascontiguousarray(S, dtype=np.uint8)
+    real = np.issubdtype(np.asarray(S).dtype, np.floating)
+    S = np.ascontiguousarray(S, dtype=np.float64 if real else np.uint8)
     Wt = np.ascontiguousarray(Wt, dtype=np.float32)
     bias = None if bias is None else np.ascontiguousarray(bias, dtype=np.float32)
     T, B, Cin, H, W = S.shape
@@ -121,7 +126,8 @@ def forward(S, Wt, bias=None, *, K=1, mode="tac", beta=0.9, v_th=1.0, v_reset=0.
     mism = np.zeros(1, np.int64)
     exc = np.zeros(1, np.int64)
     f32 = lambda v: float(np.float32(v))
-    rc = lib().tac_oracle_forward(
+    fwd = lib().tac_oracle_forward_x if real else lib().tac_oracle_forward
+    rc = fwd(
         _ptr(S), _ptr(Wt), _ptr(bias), T, B, Cin, H, W, Cout, R, Sk, stride, pad, K, m,
         f32(beta), f32(v_th), f32(v_reset), RESETS[reset], _ptr(v_init), _ptr(out),
         _ptr(v_final), _ptr(counts), _ptr(replay), float(band), _ptr(mism), _ptr(exc))

@@ -132,13 +132,13 @@ static int lif_step(double *V, int *s_prev, double I, double decay, double v_th,
  *   mismatch/excused : int64 scalars (may be NULL when replay is NULL)
  * Returns 0, or -1 on a bad argument (K not dividing T, etc.).
  */
-int tac_oracle_forward(const uint8_t *S, const float *Wt, const float *bias,
-                       int T, int B, int Cin, int H, int W, int Cout, int R,
-                       int Sk, int stride, int pad, int K, int mode,
-                       double beta, double v_th, double v_reset, int reset,
-                       const double *v_init, uint8_t *out, double *v_final,
-                       int64_t *counts, const uint8_t *replay, double band,
-                       int64_t *mismatch_out, int64_t *excused_out) {
+static int forward_impl(const uint8_t *S, const double *X, const float *Wt, const float *bias,
+                        int T, int B, int Cin, int H, int W, int Cout, int R,
+                        int Sk, int stride, int pad, int K, int mode,
+                        double beta, double v_th, double v_reset, int reset,
+                        const double *v_init, uint8_t *out, double *v_final,
+                        int64_t *counts, const uint8_t *replay, double band,
+                        int64_t *mismatch_out, int64_t *excused_out) {
   if (mode == OR_MODE_DENSE) K = 1;
   if (K < 1 || T < 1 || T % K != 0) return -1;
   int Ho = (H + 2 * pad - R) / stride + 1, Wo = (W + 2 * pad - Sk) / stride + 1;
@@ -165,8 +165,12 @@ int tac_oracle_forward(const uint8_t *S, const float *Wt, const float *bias,
       for (size_t i = 0; i < nin; ++i) A[i] = 0.0;
       for (int j = 0; j < K; ++j) {
         double wj = pow(beta, (double)(K - 1 - j));
-        const uint8_t *St = S + ((size_t)(k * K + j) * B + b) * nin;
-        for (size_t i = 0; i < nin; ++i) A[i] += wj * (double)St[i];
+        const size_t off = ((size_t)(k * K + j) * B + b) * nin;
+        if (X) { /* continuous-valued input frames, same definition */
+          for (size_t i = 0; i < nin; ++i) A[i] += wj * X[off + i];
+        } else {
+          for (size_t i = 0; i < nin; ++i) A[i] += wj * (double)S[off + i];
+        }
       }
       /* Y_k = Conv2d(A_k, W): one conv call per group (Alg.1 l.4, Alg.2 l.4). */
       conv_one(A, Wt, bias, Cin, H, W, Cout, R, Sk, stride, pad, Ho, Wo, Y);
@@ -191,6 +195,35 @@ int tac_oracle_forward(const uint8_t *S, const float *Wt, const float *bias,
   if (mismatch_out) *mismatch_out = mism;
   if (excused_out) *excused_out = exc;
   return 0;
+}
+
+int tac_oracle_forward(const uint8_t *S, const float *Wt, const float *bias,
+                       int T, int B, int Cin, int H, int W, int Cout, int R,
+                       int Sk, int stride, int pad, int K, int mode,
+                       double beta, double v_th, double v_reset, int reset,
+                       const double *v_init, uint8_t *out, double *v_final,
+                       int64_t *counts, const uint8_t *replay, double band,
+                       int64_t *mismatch_out, int64_t *excused_out) {
+  if (!S) return -1;
+  return forward_impl(S, NULL, Wt, bias, T, B, Cin, H, W, Cout, R, Sk, stride, pad, K, mode,
+                      beta, v_th, v_reset, reset, v_init, out, v_final, counts, replay, band,
+                      mismatch_out, excused_out);
+}
+
+/* Same layer on continuous-valued input frames X: fp64 [T][B][Cin][H][W] (the DVS
+ * network's first-layer input is log-normalised event counts; the aggregate
+ * A_k = sum_j beta^{K-1-j} X_{kK+j} and everything after it are unchanged). */
+int tac_oracle_forward_x(const double *X, const float *Wt, const float *bias,
+                         int T, int B, int Cin, int H, int W, int Cout, int R,
+                         int Sk, int stride, int pad, int K, int mode,
+                         double beta, double v_th, double v_reset, int reset,
+                         const double *v_init, uint8_t *out, double *v_final,
+                         int64_t *counts, const uint8_t *replay, double band,
+                         int64_t *mismatch_out, int64_t *excused_out) {
+  if (!X) return -1;
+  return forward_impl(NULL, X, Wt, bias, T, B, Cin, H, W, Cout, R, Sk, stride, pad, K, mode,
+                      beta, v_th, v_reset, reset, v_init, out, v_final, counts, replay, band,
+                      mismatch_out, excused_out);
 }
 
 /* 2x2 stride-2 OR pool of binary maps (= max-pool of {0,1}, "MaxPool(2)").

@@ -73,6 +73,9 @@ tac_status check(const tac_conv_lif_desc *d, Geo *g) {
     return fail(TAC_ERR_SHAPE, "row too wide");
   if (d->in_stride_t < 0 || d->in_stride_b < 0 || d->out_stride_t < 0 || d->out_stride_b < 0)
     return fail(TAC_ERR_SHAPE, "negative stride");
+  if (d->input_kind != TAC_INPUT_SPIKES && d->input_kind != TAC_INPUT_REAL)
+    return fail(TAC_ERR_PARAM, "input_kind=%d not in {0,1}", d->input_kind);
+  if (d->reserved0 != 0) return fail(TAC_ERR_PARAM, "reserved0 must be 0");
   g->K = K;
   g->Ho = Ho;
   g->Wo = Wo;
@@ -83,13 +86,15 @@ tac_status check(const tac_conv_lif_desc *d, Geo *g) {
   g->nsteps = d->mode == TAC_MODE_TACTP ? K : 1;
   g->wpr_in = (d->W * d->C_in + 31) / 32;
   g->wpr_out = (g->Wq * d->C_out + 31) / 32;
-  const long long in_plane = (long long)d->H * g->wpr_in;
+  // packed spikes: u32 words per (t, b) plane; REAL input: floats [H][W][C_in]
+  const long long in_plane = d->input_kind == TAC_INPUT_REAL ? (long long)d->H * d->W * d->C_in
+                                                              : (long long)d->H * g->wpr_in;
   const long long out_plane = (long long)g->Hq * g->wpr_out;
   g->in_sb = d->in_stride_b ? d->in_stride_b : in_plane;
   g->in_st = d->in_stride_t ? d->in_stride_t : in_plane * d->B;
   g->out_sb = d->out_stride_b ? d->out_stride_b : out_plane;
   g->out_st = d->out_stride_t ? d->out_stride_t : out_plane * d->B;
-  if (g->in_sb < in_plane) return fail(TAC_ERR_SHAPE, "in_stride_b < H*WPR");
+  if (g->in_sb < in_plane) return fail(TAC_ERR_SHAPE, "in_stride_b < one input plane");
   if (g->out_sb < out_plane) return fail(TAC_ERR_SHAPE, "out_stride_b < H_o*WPR_out");
   return TAC_OK;
 }
@@ -217,30 +222,36 @@ tac_status tac_prepare_weights(const tac_conv_lif_desc *desc, const float *weigh
   return TAC_OK;
 }
 
-tac_status tac_conv_lif_forward(const tac_conv_lif_desc *desc, const void *prepared,
-                                const uint32_t *spikes_in, const float *v_init,
-                                uint32_t *spikes_out, float *v_final, uint32_t *counts,
-                                void *ws, size_t ws_bytes, void *stream) {
+}  // extern "C"
+
+namespace {
+// shared body of tac_conv_lif_forward / tac_conv_lif_forward_real
+tac_status forward_impl(const tac_conv_lif_desc *desc, const void *prepared, const void *input,
+                        bool real, const float *v_init, uint32_t *spikes_out, float *v_final,
+                        uint32_t *counts, void *stream) {
   g_detail.clear();
   Geo g;
   tac_status st = check(desc, &g);
   if (st != TAC_OK) return st;
+  if ((desc->input_kind == TAC_INPUT_REAL) != real)
+    return fail(TAC_ERR_PARAM, real ? "tac_conv_lif_forward_real needs input_kind = TAC_INPUT_REAL"
+                                    : "input_kind = TAC_INPUT_REAL needs tac_conv_lif_forward_real");
+  const uint32_t *spikes_in = real ? nullptr : static_cast<const uint32_t *>(input);
   if (!prepared) return fail(TAC_ERR_NULL, "prepared is NULL");
-  if (!spikes_in) return fail(TAC_ERR_NULL, "spikes_in is NULL");
+  if (!input) return fail(TAC_ERR_NULL, real ? "x_in is NULL" : "spikes_in is NULL");
   if (!spikes_out) return fail(TAC_ERR_NULL, "spikes_out is NULL");
-  (void)ws;
-  (void)ws_bytes;
   const int engine = resolve_engine(desc);
   if (engine < 0)
     return fail(TAC_ERR_UNSUPPORTED, "engine TCGEN05 cannot run this layer: %s",
                 tacsnn::tc_unsupported_reason(desc));
-  if ((uintptr_t)spikes_in % 4 || (uintptr_t)spikes_out % 4 || (uintptr_t)prepared % 256)
+  if ((uintptr_t)input % 4 || (uintptr_t)spikes_out % 4 || (uintptr_t)prepared % 256)
     return fail(TAC_ERR_ALIGN, "misaligned pointer");
   if (v_init && (uintptr_t)v_init % 16) return fail(TAC_ERR_ALIGN, "v_init must be 16-B aligned");
   if (v_final && (uintptr_t)v_final % 16) return fail(TAC_ERR_ALIGN, "v_final must be 16-B aligned");
   if (counts && (uintptr_t)counts % 4) return fail(TAC_ERR_ALIGN, "counts misaligned");
-  const void *dev_ptrs[] = {prepared, spikes_in, spikes_out, v_init, v_final, counts};
-  const char *names[] = {"prepared", "spikes_in", "spikes_out", "v_init", "v_final", "counts"};
+  const void *dev_ptrs[] = {prepared, input, spikes_out, v_init, v_final, counts};
+  const char *names[] = {"prepared", real ? "x_in" : "spikes_in", "spikes_out", "v_init", "v_final",
+                         "counts"};
   for (int i = 0; i < 6; ++i)
     if (dev_ptrs[i] && !is_device_ptr(dev_ptrs[i]))
       return fail(TAC_ERR_PARAM, "%s is not device memory", names[i]);
@@ -257,6 +268,7 @@ tac_status tac_conv_lif_forward(const tac_conv_lif_desc *desc, const void *prepa
   p.decay = (float)(desc->mode == TAC_MODE_TAC ? std::pow(beta, (double)g.K) : beta);
   for (int j = 0; j < g.K; ++j) p.coef[j] = (float)std::pow(beta, (double)(g.K - 1 - j));
   p.in = spikes_in; p.out = spikes_out; p.v_init = v_init; p.v_final = v_final; p.counts = counts;
+  p.xin = real ? static_cast<const float *>(input) : nullptr;
   const PrepLayout L = prep_layout(desc);
   const unsigned char *base = static_cast<const unsigned char *>(prepared);
   p.w = reinterpret_cast<const float *>(base + L.simt_off);
@@ -273,6 +285,27 @@ tac_status tac_conv_lif_forward(const tac_conv_lif_desc *desc, const void *prepa
   if (err) return fail(TAC_ERR_CUDA, "launch failed: %s", cudaGetErrorString((cudaError_t)err));
   g_launches = launches;
   return TAC_OK;
+}
+}  // namespace
+
+extern "C" {
+
+tac_status tac_conv_lif_forward(const tac_conv_lif_desc *desc, const void *prepared,
+                                const uint32_t *spikes_in, const float *v_init,
+                                uint32_t *spikes_out, float *v_final, uint32_t *counts,
+                                void *ws, size_t ws_bytes, void *stream) {
+  (void)ws;
+  (void)ws_bytes;
+  return forward_impl(desc, prepared, spikes_in, false, v_init, spikes_out, v_final, counts, stream);
+}
+
+tac_status tac_conv_lif_forward_real(const tac_conv_lif_desc *desc, const void *prepared,
+                                     const float *x_in, const float *v_init,
+                                     uint32_t *spikes_out, float *v_final, uint32_t *counts,
+                                     void *ws, size_t ws_bytes, void *stream) {
+  (void)ws;
+  (void)ws_bytes;
+  return forward_impl(desc, prepared, x_in, true, v_init, spikes_out, v_final, counts, stream);
 }
 
 tac_status tac_pack_spikes(const uint8_t *dense01, uint32_t *packed, int32_t T, int32_t B,

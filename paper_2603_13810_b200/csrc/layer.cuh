@@ -23,7 +23,8 @@ struct LayerParams {
   float decay;       // beta (dense / TAC-TP) or beta^K (TAC), rounded from fp64
   float coef[kMaxK]; // beta^{K-1-j}, rounded from fp64 (A_k weights)
   // buffers
-  const uint32_t *in;
+  const uint32_t *in;     // packed spikes (input_kind SPIKES)
+  const float *xin;       // fp32 [T][B][H][W][C_in] (input_kind REAL); strides in floats
   uint32_t *out;
   const float *v_init;
   float *v_final;

@@ -78,16 +78,21 @@ __global__ void __launch_bounds__(128) simt_conv_lif_kernel(const LayerParams p)
         uint32_t words[kMaxK];
         int cur = -1;
         for (int ci = 0; ci < p.Cin; ++ci) {
-          const long long bit = (long long)xi * p.Cin + ci;
-          const int wi = (int)(bit >> 5), sh = (int)(bit & 31);
-          if (wi != cur) {
-            for (int j = 0; j < p.K; ++j)
-              words[j] = __ldg(p.in + (long long)(g * p.K + j) * p.in_st + rowoff + wi);
-            cur = wi;
-          }
           float a = 0.f;
-          for (int j = 0; j < p.K; ++j)
-            if ((words[j] >> sh) & 1u) a += p.coef[j];
+          if (p.xin) {  // continuous input: A = sum_j beta^{K-1-j} X_{gK+j} (fp32)
+            const float *xp = p.xin + (long long)b * p.in_sb + ((long long)yi * p.W + xi) * p.Cin + ci;
+            for (int j = 0; j < p.K; ++j) a = fmaf(p.coef[j], __ldg(xp + (long long)(g * p.K + j) * p.in_st), a);
+          } else {
+            const long long bit = (long long)xi * p.Cin + ci;
+            const int wi = (int)(bit >> 5), sh = (int)(bit & 31);
+            if (wi != cur) {
+              for (int j = 0; j < p.K; ++j)
+                words[j] = __ldg(p.in + (long long)(g * p.K + j) * p.in_st + rowoff + wi);
+              cur = wi;
+            }
+            for (int j = 0; j < p.K; ++j)
+              if ((words[j] >> sh) & 1u) a += p.coef[j];
+          }
           if (a != 0.f) {
             const float *wp = p.w + ((long long)(ci * p.R + r) * p.S + s) * p.Cout + co0;
 #pragma unroll

@@ -114,6 +114,9 @@ struct TcParams {
   int tap_off[9];
   int naccs;             // TMEM accumulators in the MMA -> epilogue ring
   int split;             // A carried as fp16 hi + lo from the 2^K-entry table lut
+  int real;              // continuous input xin (A computed from fp32 frames, then hi + lo)
+  const float *xin;      // fp32 [T][B][H][W][C_in], strides in_st / in_sb in floats
+  float coef[8];         // beta^{K-1-j}, fp32 (from fp64)
   uint32_t off_lut;      // smem copy of lut
   uint32_t lut[1 << 8];  // idx (bit j = frame j's spike) -> fp16 A_hi | fp16 A_lo << 16
   const uint32_t *in;
@@ -167,6 +170,7 @@ int cout_pad_of(int Cout) {
 // 2^-22 |A|) looked up from a 2^K-entry table of the K spike bits of a channel,
 // and both ride the fp16 tensor-core path as extra K channels.
 bool split_of(const tac_conv_lif_desc *d) {
+  if (d->input_kind == TAC_INPUT_REAL) return true;  // continuous input: A is any real
   if (d->mode == TAC_MODE_DENSE || d->K <= 1) return false;
   const int m = beta_shift(d->beta);
   return m == 0 || m * (d->K - 1) > 7;
@@ -254,12 +258,15 @@ const char *shape_reason(const tac_conv_lif_desc *d) {
     return "needs C_out in {8,16} or a multiple of 32 up to 128";
   const int K = d->mode == TAC_MODE_DENSE ? 1 : d->K;
   if (d->mode == TAC_MODE_TACTP && K > kMaxSteps) return "TAC-TP needs K <= 8";
+  // the producers and LIF epilogues are instantiated for these group sizes
+  if (!(K == 1 || K == 2 || K == 4 || K == 8)) return "needs K in {1, 2, 4, 8}";
   return nullptr;
 }
 
 const char *reason(const tac_conv_lif_desc *d) {
   const char *r = shape_reason(d);
   if (r) return r;
+  if (d->input_kind == TAC_INPUT_REAL && d->C_in > 2) return "continuous input needs C_in <= 2";
   if (split_of(d)) {
     if (d->K > kMaxSplitK) return "split (beta != 2^-m) aggregate needs K <= 8";
     if (!(d->C_in <= 2 || d->C_in == 32)) return "split (beta != 2^-m) aggregate needs C_in in {1, 2, 32}";
@@ -527,6 +534,44 @@ __device__ __forceinline__ void store_split32_row(uint32_t dst, uint32_t lbo, co
   }
   ptx::st_shared_v4(dst + 8 * lbo, 0x3C00u, 0u, 0u, 0u);
   ptx::st_shared_v4(dst + 9 * lbo, 0u, 0u, 0u, 0u);
+}
+
+// continuous-input producer (input_kind REAL, C_in <= 2): A_c = sum_j beta^{K-1-j}
+// X_{kK+j, c} in fp32 (the oracle's order), then the same [A_hi | A_lo | 1.0] row as
+// the split path
+template <int K, int CIN>
+__device__ __forceinline__ void produce_h16x(const TcParams &p, int tile, int k, uint32_t a_stage,
+                                             int ptid) {
+  int b, y0, x0;
+  bool tok;
+  tile_origin(p, tile, b, y0, x0, tok);
+  const float *frame0 = p.xin + (long long)(k * K) * p.in_st + (long long)b * p.in_sb;
+  for (int row = ptid; row < kHaloRows; row += kProdWarps * 32) {
+    const int hy = row / kHaloW, hx = row - (row / kHaloW) * kHaloW;
+    const int yi = y0 + hy - p.pad, xi = x0 + hx - p.pad;
+    const bool ok = tok && yi >= 0 && yi < p.H && xi >= 0 && xi < p.W;
+    const float *src = frame0 + ((long long)(ok ? yi : 0) * p.W + (ok ? xi : 0)) * CIN;
+    float a[CIN];
+#pragma unroll
+    for (int c = 0; c < CIN; ++c) a[c] = 0.f;
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+#pragma unroll
+      for (int c = 0; c < CIN; ++c) a[c] = fmaf(p.coef[j], ok ? __ldg(src + (long long)j * p.in_st + c) : 0.f, a[c]);
+    uint32_t e[CIN];
+#pragma unroll
+    for (int c = 0; c < CIN; ++c) {
+      const __half hi = __float2half_rn(a[c]);
+      const __half lo = __float2half_rn(a[c] - __half2float(hi));
+      e[c] = (uint32_t)__half_as_ushort(hi) | ((uint32_t)__half_as_ushort(lo) << 16);
+    }
+    uint4 c0;
+    if (CIN == 1) c0 = make_uint4(e[0], 0x3C00u, 0u, 0u);
+    else c0 = make_uint4(__byte_perm(e[0], e[CIN - 1], 0x5410u), __byte_perm(e[0], e[CIN - 1], 0x7632u), 0x3C00u, 0u);
+    const uint32_t dst = a_stage + (uint32_t)row * 16u;
+    ptx::st_shared_v4(dst, c0.x, c0.y, c0.z, c0.w);
+    ptx::st_shared_v4(dst + p.lbo_a, 0u, 0u, 0u, 0u);
+  }
 }
 
 // LDG split producers (e.g. MNIST rows, whose 4-B row stride rules out TMA)
@@ -874,6 +919,8 @@ __device__ __forceinline__ void producer_role(const TcParams &p, uint32_t sbase,
       const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
       if (PATH == PATH_HALO)
         produce_halo<K>(p, tile, k, a_stage, ptid);
+      else if (PATH == PATH_SPLIT && p.real)
+        p.Cin == 1 ? produce_h16x<K, 1>(p, tile, k, a_stage, ptid) : produce_h16x<K, 2>(p, tile, k, a_stage, ptid);
       else if (PATH == PATH_SPLIT && K > 1)
         p.Cin == 32 ? produce_s32<K>(p, lut, tile, k, a_stage, ptid)
                     : (p.Cin == 1 ? produce_h16s<K, 1>(p, lut, tile, k, a_stage, ptid)
@@ -1928,7 +1975,7 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   // TMA raw-halo producer when the packed input is a legal 4-D tensor-map view
   // (16-B aligned base and strides) and the plan fits in shared memory
   static const bool no_tma = [] { const char *e = std::getenv("TACSNN_NO_TMA"); return e && *e == '1'; }();
-  const bool tma_layout = !no_tma && (lp.wpr_in * 4) % 16 == 0 && (lp.in_sb * 4) % 16 == 0 &&
+  const bool tma_layout = !no_tma && !lp.xin && (lp.wpr_in * 4) % 16 == 0 && (lp.in_sb * 4) % 16 == 0 &&
                           (lp.in_st * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(lp.in) % 16) == 0;
   Geometry g = geometry(d, tma_layout);
   PFN_cuTensorMapEncodeTiled_v12000 encode = g.use_tma ? tensor_map_encoder() : nullptr;
@@ -1965,7 +2012,10 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   p.m_shift = (d->mode == TAC_MODE_DENSE || g.split) ? 0 : beta_shift(d->beta);
   p.split = g.split;
   p.off_lut = g.off_lut;
-  if (g.split) {  // A = sum_j bit_j beta^{K-1-j} in fp64, as fp16 hi + lo
+  p.real = lp.xin ? 1 : 0;
+  p.xin = lp.xin;
+  for (int j = 0; j < 8; ++j) p.coef[j] = j < lp.K ? lp.coef[j] : 0.f;
+  if (g.split && !p.real) {  // A = sum_j bit_j beta^{K-1-j} in fp64, as fp16 hi + lo
     for (int idx = 0; idx < (1 << kMaxSplitK); ++idx) {
       double a = 0.0;
       for (int j = 0; j < lp.K && j < kMaxSplitK; ++j)

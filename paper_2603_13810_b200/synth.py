@@ -177,6 +177,17 @@ def dvs_events(seed: int, T: int, B: int, H: int = 128, W: int = 128, b0: int = 
     return out
 
 
+def dvs_log_counts(seed: int, T: int, B: int, H: int = 128, W: int = 128, b0: int = 0,
+                   device="cpu", sub: int = 4) -> torch.Tensor:
+    """Continuous-valued DVS-like input (the paper's first-layer input is log-normalised
+    event counts): each of the T bins sums `sub` consecutive event-
+    occurrence frames of dvs_events, then x = log(1 + count) / log(1 + sub) in [0, 1].
+    fp32 [T, B, 2, H, W]."""
+    ev = dvs_events(seed, T * sub, B, H, W, b0=b0, device=device)
+    cnt = ev.view(T, sub, B, 2, H, W).sum(dim=1, dtype=torch.int32).to(torch.float64)
+    return (torch.log1p(cnt) / torch.log1p(torch.tensor(float(sub), dtype=torch.float64))).to(torch.float32)
+
+
 def weights(seed: int, C_out: int, C_in: int, R: int = 3, S: int = 3, gain: float = 1.0):
     """fp32 [C_out, C_in, R, S] ~ N(0, (gain/sqrt(C_in R S))^2) and bias U(-0.1, 0.1)."""
     g = torch.Generator().manual_seed(seed)

@@ -23,9 +23,12 @@ MODES = {"dense": 0, "tac": 1, "tactp": 2}
 RESETS = {"subtract": 0, "delayed": 1, "hard": 2}
 ENGINES = {"auto": 0, "simt": 1, "tcgen05": 2}
 ENGINE_NAMES = {v: k for k, v in ENGINES.items()}
+INPUTS = {"spikes": 0, "real": 1}
+ABI_VERSION = 2
 
 EXPORTS = ("tac_desc_check", "tac_out_shape", "tac_select_engine", "tac_weights_bytes",
            "tac_prepare_weights", "tac_workspace_bytes", "tac_conv_lif_forward",
+           "tac_conv_lif_forward_real",
            "tac_pack_spikes", "tac_unpack_spikes", "tac_status_string",
            "tac_last_error_detail", "tac_abi_version", "tac_last_launch_count",
            "tac_debug_set_trace")
@@ -38,7 +41,8 @@ class Desc(ctypes.Structure):
                [("beta", ctypes.c_float), ("v_th", ctypes.c_float), ("v_reset", ctypes.c_float),
                 ("reset", ctypes.c_int32), ("out_pool", ctypes.c_int32), ("engine", ctypes.c_int32),
                 ("in_stride_t", ctypes.c_int64), ("in_stride_b", ctypes.c_int64),
-                ("out_stride_t", ctypes.c_int64), ("out_stride_b", ctypes.c_int64)]
+                ("out_stride_t", ctypes.c_int64), ("out_stride_b", ctypes.c_int64),
+                ("input_kind", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
 
 
 _lock = threading.Lock()
@@ -64,6 +68,7 @@ def lib():
                 "tac_prepare_weights": ([D, P, P, P, sz, P], i32),
                 "tac_workspace_bytes": ([D, ctypes.POINTER(sz)], i32),
                 "tac_conv_lif_forward": ([D, P, P, P, P, P, P, P, sz, P], i32),
+                "tac_conv_lif_forward_real": ([D, P, P, P, P, P, P, P, sz, P], i32),
                 "tac_pack_spikes": ([P, P, i32, i32, i32, i32, i32, P], i32),
                 "tac_unpack_spikes": ([P, P, i32, i32, i32, i32, i32, P], i32),
                 "tac_status_string": ([i32], ctypes.c_char_p),
@@ -107,6 +112,7 @@ class LayerSpec:
     reset: str = "subtract"
     out_pool: int = 1
     engine: str = "auto"
+    input: str = "spikes"     # "real": continuous-valued fp32 input frames (tac_conv_lif_forward_real)
 
     def replace(self, **kw) -> "LayerSpec":
         return dataclasses.replace(self, **kw)
@@ -116,7 +122,7 @@ class LayerSpec:
                     self.stride, self.pad, 1 if self.mode == "dense" else self.K,
                     MODES[self.mode], self.beta, self.v_th, self.v_reset, RESETS[self.reset],
                     self.out_pool, ENGINES[self.engine], in_strides[0], in_strides[1],
-                    out_strides[0], out_strides[1])
+                    out_strides[0], out_strides[1], INPUTS[self.input], 0)
 
     @property
     def conv_hw(self):
@@ -177,11 +183,19 @@ def conv_lif(spec: LayerSpec, prepared: torch.Tensor, x: torch.Tensor, *, v_init
     """Run one layer (tac_conv_lif_forward) on the current stream.
 
     x: int32/uint32-bit packed spikes [T, B, H, WPR] (rows contiguous; T and B
-    strides taken from the tensor).  Returns (spikes_out [T_out,B,H_o,WPR_out]
-    int32, v_final [B,H',W',C_out] fp32 or None, counts [B,C_out] int32 or None).
+    strides taken from the tensor), or for spec.input == "real" fp32 frames
+    [T, B, H, W, C_in] (tac_conv_lif_forward_real; each (t, b) plane contiguous).
+    Returns (spikes_out [T_out,B,H_o,WPR_out] int32, v_final [B,H',W',C_out] fp32 or
+    None, counts [B,C_out] int32 or None).
     """
-    assert x.is_cuda and x.dtype == torch.int32 and x.dim() == 4
-    assert x.stride(3) == 1 and x.stride(2) == spec.in_words_per_row, "rows must be packed"
+    real = spec.input == "real"
+    if real:
+        assert x.is_cuda and x.dtype == torch.float32 and x.dim() == 5
+        assert x.shape[2:] == (spec.H, spec.W, spec.C_in)
+        assert x.stride(4) == 1 and x.stride(3) == spec.C_in and x.stride(2) == spec.W * spec.C_in
+    else:
+        assert x.is_cuda and x.dtype == torch.int32 and x.dim() == 4
+        assert x.stride(3) == 1 and x.stride(2) == spec.in_words_per_row, "rows must be packed"
     T_out, Ho, Wo, wpr = spec.out_shape()
     if out is None:
         out = torch.empty((T_out, spec.B, Ho, wpr), dtype=torch.int32, device=x.device)
@@ -195,9 +209,9 @@ def conv_lif(spec: LayerSpec, prepared: torch.Tensor, x: torch.Tensor, *, v_init
         assert v_init.is_cuda and v_init.dtype == torch.float32 and v_init.is_contiguous()
         assert tuple(v_init.shape) == (spec.B, hc, wc, spec.C_out)
     d = spec.desc((x.stride(0), x.stride(1)), (out.stride(0), out.stride(1)))
-    _check(lib().tac_conv_lif_forward(ctypes.byref(d), _ptr(prepared), _ptr(x), _ptr(v_init),
-                                      _ptr(out), _ptr(v_final), _ptr(counts), None, 0,
-                                      _stream(x.device)))
+    fwd = lib().tac_conv_lif_forward_real if real else lib().tac_conv_lif_forward
+    _check(fwd(ctypes.byref(d), _ptr(prepared), _ptr(x), _ptr(v_init), _ptr(out), _ptr(v_final),
+               _ptr(counts), None, 0, _stream(x.device)))
     return out, v_final, counts
 
 

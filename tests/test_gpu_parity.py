@@ -125,6 +125,77 @@ def test_split_aggregate_parity(T, O, case, mode, K, beta):
     assert 0.0 < st["rate"] < 0.9, st
 
 
+REAL_CASES = [
+    # continuous-valued first layer (log-normalised DVS-like event counts)
+    ("dvsL1r", (8, 2, 2, 64, 64, 128, 1, 2), 4.0),
+    ("mnistL1r", (8, 3, 1, 28, 28, 32, 0, 2), 2.5),
+    ("c1r", (8, 4, 1, 28, 28, 8, 0, 1), 2.5),
+]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("mode,K,beta", [("dense", 1, 0.5), ("tac", 4, 0.5), ("tactp", 2, 0.9),
+                                         ("tac", 8, 0.9), ("tactp", 4, 0.5)])
+@pytest.mark.parametrize("case", REAL_CASES, ids=[c[0] for c in REAL_CASES])
+def test_real_input_parity(T, O, case, mode, K, beta, engine):
+    """tac_conv_lif_forward_real against the fp64 oracle on the same float frames."""
+    from paper_2603_13810_b200 import synth
+    name, (Tn, B, Cin, H, W, Cout, pad, pool), gain = case
+    spec = T.LayerSpec(T=Tn, B=B, C_in=Cin, H=H, W=W, C_out=Cout, pad=pad, K=K, mode=mode,
+                       beta=beta, out_pool=pool, input="real")
+    spec = _engine_or_skip(spec, engine)
+    X = synth.dvs_log_counts(zlib.crc32(name.encode()) % 991, Tn, B, H, W)[:, :, :Cin]  # [T,B,C,H,W]
+    w, b = _w(10, Cout, Cin, gain)
+    prep = T.prepare_weights(spec, w, b)
+    x = X.permute(0, 1, 3, 4, 2).contiguous().cuda()                                   # [T,B,H,W,C]
+    s1 = spec.replace(out_pool=1)
+    out, vf, cnt = T.conv_lif(s1, prep, x, want_v_final=True)
+    torch.cuda.synchronize()
+    hc, wc = s1.conv_hw
+    D = O.unpack_spikes(P.to_u32(out), Cout, wc)
+    r = O.forward(X.numpy().astype(np.float64), w.numpy(), b.numpy(), K=s1.K, mode=mode,
+                  beta=beta, pad=pad, replay=D, band=P.BAND)
+    assert r["mismatch"] == 0, f"{name}: {r['mismatch']} out-of-band mismatches"
+    assert 0.0 < D.mean() < 0.9, D.mean()
+    v_dev = vf.cpu().numpy().transpose(0, 3, 1, 2).astype(np.float64)
+    err = np.abs(v_dev - r["v_final"])
+    assert np.all(err <= P.VTOL * np.maximum(np.abs(r["v_final"]), 1.0)), err.max()
+    assert np.array_equal(cnt.cpu().numpy().astype(np.int64), r["counts"])
+    if pool == 2:
+        dev_p, _, _ = T.conv_lif(spec, prep, x, want_counts=False)
+        torch.cuda.synchronize()
+        assert np.array_equal(O.unpack_spikes(P.to_u32(dev_p), Cout, wc // 2), O.or_pool2(r["out"]))
+
+
+def test_real_input_rejects_spike_call(T):
+    """A REAL-input descriptor through tac_conv_lif_forward is refused before launch."""
+    import ctypes
+    spec = T.LayerSpec(T=4, B=1, C_in=2, H=8, W=8, C_out=16, pad=1, K=2, mode="tac", beta=0.5,
+                       input="real")
+    prep = T.prepare_weights(spec, *_w(1, 16, 2, 1.0))
+    x = T.pack(torch.zeros((4, 1, 2, 8, 8), dtype=torch.uint8, device="cuda"))
+    d = spec.desc()
+    out = torch.empty((2, 1, 4, 16), dtype=torch.int32, device="cuda")
+    st = T.lib().tac_conv_lif_forward(ctypes.byref(d), ctypes.c_void_p(prep.data_ptr()),
+                                      ctypes.c_void_p(x.data_ptr()), None,
+                                      ctypes.c_void_p(out.data_ptr()), None, None, None, 0, None)
+    assert st == 4 and b"tac_conv_lif_forward_real" in T.lib().tac_last_error_detail()
+
+
+@pytest.mark.parametrize("mode", ["tac", "tactp"])
+def test_odd_group_size_runs_on_simt(T, O, mode):
+    """K = 3 (T = 6) is outside the tcgen05 envelope (K in {1,2,4,8}): AUTO must pick
+    the SIMT engine, an explicit tcgen05 request must be refused, results exact."""
+    spec = T.LayerSpec(T=6, B=2, C_in=32, H=10, W=12, C_out=32, pad=1, K=3, mode=mode,
+                       beta=0.5, out_pool=2)
+    assert spec.engine_used() == "simt"
+    with pytest.raises(RuntimeError):
+        spec.replace(engine="tcgen05").engine_used()
+    S = _spikes(21, (6, 2, 32, 10, 12), 0.2)
+    w, b = _w(9, 32, 32, 1.5)
+    P.check_layer(T, O, spec, S, w, b, label=f"K3/{mode}")
+
+
 @pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("reset", ["delayed", "hard"])
 @pytest.mark.parametrize("mode", ["dense", "tac", "tactp"])

@@ -33,8 +33,12 @@ with open(os.path.join(HERE, "golden", "lif_scalar_cases.json")) as f:
 
 @pytest.mark.parametrize("case", GOLDEN, ids=[c["name"] for c in GOLDEN])
 def test_golden_scalar_cases(oracle_mod, case):
-    T = len(case["S"])
-    S = np.array(case["S"], np.uint8).reshape(T, 1, 1, 1, 1)
+    if "X" in case:   # continuous-valued input frames (fp64 oracle path)
+        T = len(case["X"])
+        S = np.array(case["X"], np.float64).reshape(T, 1, 1, 1, 1)
+    else:
+        T = len(case["S"])
+        S = np.array(case["S"], np.uint8).reshape(T, 1, 1, 1, 1)
     W = np.full((1, 1, 1, 1), case["w"], np.float32)
     bias = None if case["bias"] is None else np.array([case["bias"]], np.float32)
     r = oracle_mod.forward(S, W, bias, K=case["K"], mode=case["mode"], beta=case["beta"],
@@ -311,3 +315,30 @@ def test_pack_roundtrip(oracle_mod, C, W):
     p = oracle_mod.pack_spikes(d)
     assert p.shape == (3, 2, 4, (W * C + 31) // 32)
     assert np.array_equal(oracle_mod.unpack_spikes(p, C, W), d)
+
+
+# --- continuous-valued input ------------------------
+@pytest.mark.parametrize("mode", ["dense", "tac", "tactp"])
+def test_real_input_path_equals_spike_path_on_binary_frames(oracle_mod, mode):
+    """{0,1} frames given as floats follow the same arithmetic as u8 spikes: bitwise."""
+    rng = np.random.default_rng(31)
+    S = (rng.random((8, 2, 2, 9, 9)) < 0.3).astype(np.uint8)
+    W = _rand_w(rng, 4, 2, gain=2.0)
+    b = (rng.standard_normal(4) * 0.1).astype(np.float32)
+    r1 = oracle_mod.forward(S, W, b, K=4, mode=mode, beta=0.9, pad=1)
+    r2 = oracle_mod.forward(S.astype(np.float64), W, b, K=4, mode=mode, beta=0.9, pad=1)
+    assert np.array_equal(r1["out"], r2["out"]) and np.array_equal(r1["v_final"], r2["v_final"])
+
+
+@pytest.mark.parametrize("K", [2, 4])
+def test_real_input_no_spike_tac_equals_dense(oracle_mod, K):
+    """Linearity holds for continuous input too: with no spikes and no bias,
+    V^TAC after group k equals V^dense at t = kK + K - 1."""
+    rng = np.random.default_rng(32)
+    X = rng.gamma(1.0, 0.5, (8, 2, 2, 7, 7))
+    W = _rand_w(rng, 3, 2)
+    for k in range(8 // K):
+        T = (k + 1) * K
+        d = oracle_mod.forward(X[:T], W, None, K=1, mode="dense", beta=0.9, v_th=1e30, pad=1)
+        t = oracle_mod.forward(X[:T], W, None, K=K, mode="tac", beta=0.9, v_th=1e30, pad=1)
+        np.testing.assert_allclose(t["v_final"], d["v_final"], rtol=1e-12, atol=1e-12)
