@@ -64,6 +64,9 @@ constexpr int kProdWarps = 3;
 #ifndef TACSNN_HALO_NR
 #define TACSNN_HALO_NR 2  // halo producer pixels per pass (K <= 4)
 #endif
+#ifndef TACSNN_REFILL_EARLY
+#define TACSNN_REFILL_EARLY 1
+#endif
 #ifndef TACSNN_BDESC_OPAQUE
 #define TACSNN_BDESC_OPAQUE 1
 #endif
@@ -1709,8 +1712,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
             const uint32_t s = st.i, ph = st.ph, acc = ar.i, aph = ar.ph;
             st.next(ns);
             ar.next((uint32_t)p.naccs);
-            ptx::mbar_wait(bar_t_empty + 8 * acc, aph ^ 1u);
             ptx::mbar_wait(bar_a_full + 8 * s, ph);
+#if TACSNN_REFILL_EARLY
+            // A-full(it) implies every producer released raw slot it % nraw: refill it now,
+            // before the MMA issue below (which blocks while the tensor queue is full)
+            if (p.use_tma && lane == 0) loader.refill(p, sbase, bar_raw, bar_raw_empty, it, ncl);
+            __syncwarp();
+#endif
+            ptx::mbar_wait(bar_t_empty + 8 * acc, aph ^ 1u);
             ptx::tc_fence_after();
             if (lane == 0) trace_mark(p, it, TR_MMA_READY);
             const uint64_t a_base = a_desc0 + (uint64_t)(s * stage16);
@@ -1749,10 +1758,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
             }
             __syncwarp();
             if (lane == 0) trace_mark(p, it, TR_MMA_ISSUED);
-            // lane 0 refills the raw-halo slot group `it` consumed (cheap: incremental tile
-            // coordinates, the wait on raw_empty has long completed)
+#if !TACSNN_REFILL_EARLY
             if (p.use_tma && lane == 0) loader.refill(p, sbase, bar_raw, bar_raw_empty, it, ncl);
             __syncwarp();
+#endif
           }
         }
       }
