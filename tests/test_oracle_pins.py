@@ -342,3 +342,25 @@ def test_real_input_no_spike_tac_equals_dense(oracle_mod, K):
         d = oracle_mod.forward(X[:T], W, None, K=1, mode="dense", beta=0.9, v_th=1e30, pad=1)
         t = oracle_mod.forward(X[:T], W, None, K=K, mode="tac", beta=0.9, v_th=1e30, pad=1)
         np.testing.assert_allclose(t["v_final"], d["v_final"], rtol=1e-12, atol=1e-12)
+
+
+def test_theorem1_statistical_c1_shape(oracle_mod):
+    """P11: the literal Theorem 1 bound at a C1-like shape (Bernoulli
+    rho=0.1 inputs, beta=0.9, T=16, 1->8 channels 3x3 on 28x28, pad 0, 40 samples):
+    E||V^dense_T - V^TAC_T||^2 <= V_th^2 N / (1 - beta^{2K}) * rho (1-rho) K ||W||_F^2
+    (N = output pixels) holds, with the error growing in K."""
+    rng = np.random.default_rng(40)
+    T, B, rho = 16, 40, 0.1
+    S = _rand_spikes(rng, (T, B, 1, 28, 28), rho)
+    W = _rand_w(rng, 8, 1, gain=1.0)
+    d = oracle_mod.forward(S, W, K=1, mode="dense", beta=0.9)
+    b32 = float(np.float32(0.9))
+    prev = -1.0
+    for K in (2, 4, 8):
+        t = oracle_mod.forward(S, W, K=K, mode="tac", beta=0.9)
+        err = float(((d["v_final"] - t["v_final"]) ** 2).sum(axis=(1, 2, 3)).mean())
+        n_spatial = 26 * 26
+        bound = n_spatial / (1 - b32 ** (2 * K)) * rho * (1 - rho) * K * float((W.astype(np.float64) ** 2).sum())
+        assert err <= bound, (K, err, bound)
+        assert err > prev, (K, err, prev)
+        prev = err
