@@ -990,62 +990,12 @@ __device__ __forceinline__ void lif_step(float &v, float y, float decay, float v
   if (RESET == 1) prev = (prev & ~bitmask) | (~(uint32_t)msk & bitmask);
 }
 
-// Specialised subtract-reset path (NS > 0) in the shifted state U = V - v_th:
-//   U <- decay U + Y'        with Y' = Y + (decay - 1) v_th folded into the bias
-//   f  = [U >= 0]            = sat(U 2^127 + 1) (ftz: exactly 0 or 1 for every U)
-//   U <- U - v_th f          (one fma, exact when f = 0 or 1)
-// The spike is then bit 23..29 of f (1.0f = 0x3F800000): channel CB + i of a
-// chunk of 8 is OR-ed into accumulator i / 7 at bit 23 + i % 7 on the ALU pipe,
-// and the two accumulators are folded into the spike word once per chunk.
-// Per neuron-step: half an FFMA2 (update), one FFMA.SAT, half an FFMA2 (reset) on
-// the FMA pipe, 1 + 3/8 ALU ops.
+// f = [U >= 0] = sat(U 2^127 + 1): exactly 0 or 1 for every U (ftz), used by the
+// subtract-reset epilogue (epilogue_sr) as U <- U - v_th f.
 __device__ __forceinline__ float sat_spike(float u) {
   float f;
   asm("fma.rn.ftz.sat.f32 %0, %1, 0f7F000000, 0f3F800000;" : "=f"(f) : "f"(u));
   return f;
-}
-
-template <uint32_t BIT>
-__device__ __forceinline__ uint32_t or_bit(uint32_t acc, float f) {
-  uint32_t d;  // acc | (f & BIT)
-  asm("lop3.b32 %0, %1, %2, %3, 0xF8;" : "=r"(d) : "r"(acc), "r"(__float_as_uint(f)), "n"(BIT));
-  return d;
-}
-
-// two neurons (chunk channels I, I + 1), NS steps sharing one drive (TAC-TP) or
-// NS = 1 (TAC / dense)
-template <int NS, int I>
-__device__ __forceinline__ void lif_pair_u(float2 &u, float2 y, float2 dec2, float2 nth2,
-                                           uint32_t (&a)[NS][2]) {
-#pragma unroll
-  for (int j = 0; j < NS; ++j) {
-    u = __ffma2_rn(dec2, u, y);
-    const float2 f = make_float2(sat_spike(u.x), sat_spike(u.y));
-    u = __ffma2_rn(nth2, f, u);
-    a[j][I / 7] = or_bit<1u << (23 + I % 7)>(a[j][I / 7], f.x);
-    a[j][(I + 1) / 7] = or_bit<1u << (23 + (I + 1) % 7)>(a[j][(I + 1) / 7], f.y);
-  }
-}
-
-template <int N>
-__device__ __forceinline__ uint32_t shift_by(uint32_t x) {  // x << N (N may be negative)
-  return N >= 0 ? (x << (N >= 0 ? N : 0)) : (x >> (N < 0 ? -N : 0));
-}
-
-// 8 channels CB .. CB + 7 of the thread's 32-bit spike word(s) spk[j]
-template <int NS, int CB>
-__device__ __forceinline__ void lif_chunk8(float2 *U, const float (&yv)[8], float2 dec2,
-                                           float2 nth2, uint32_t (&spk)[NS]) {
-  uint32_t a[NS][2];
-#pragma unroll
-  for (int j = 0; j < NS; ++j) a[j][0] = a[j][1] = 0u;
-  lif_pair_u<NS, 0>(U[0], make_float2(yv[0], yv[1]), dec2, nth2, a);
-  lif_pair_u<NS, 2>(U[1], make_float2(yv[2], yv[3]), dec2, nth2, a);
-  lif_pair_u<NS, 4>(U[2], make_float2(yv[4], yv[5]), dec2, nth2, a);
-  lif_pair_u<NS, 6>(U[3], make_float2(yv[6], yv[7]), dec2, nth2, a);
-#pragma unroll
-  for (int j = 0; j < NS; ++j)  // bits 23..29 of a0 -> CB..CB+6, bit 23 of a1 -> CB+7
-    spk[j] |= shift_by<CB - 23>(a[j][0]) | shift_by<CB - 16>(a[j][1]);
 }
 
 // Y for 8 channels from the two s32 accumulator slices (see file header)
@@ -1148,7 +1098,6 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
   constexpr bool F16 = PATH != PATH_HALO;
   // (U in TMEM only pays when the K LIF steps per group make registers scarce)
   constexpr bool UT = u_in_tmem<NCH, PATH, NPART>() && NS >= TACSNN_UT_MIN_NS;
-  constexpr bool LD32 = false;  // F16 && NCH == 32 (one 32-column load) spills at 104 regs
   constexpr int NBUF = (NPART == 2 || (F16 && NS <= 4)) ? 2 : 1;  // TMEM prefetch depth (registers)
   const float *sc = reinterpret_cast<const float *>(smem + p.off_scale);
   const int e = (int)warp;
@@ -1236,14 +1185,6 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
           }
           ptx::tmem_st8(ucol + ch * 8, du);
         }
-      } else if (LD32) {
-        uint32_t d[32];
-        ptx::tmem_ld32(tcol, d);
-        ptx::tmem_wait_ld32(d);
-#pragma unroll
-        for (int q = NCH / 2 - 1; q >= 0; --q)
-          lif_pair_sr<NS>(U[UT ? 0 : q], make_float2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1])),
-                          dec2, nth2, nsp);
       } else {
         uint32_t d[NBUF][2][8];  // [buffer][hi/lo][col]
         ptx::tmem_ld8(tcol + (NCHUNK - 1) * 8, d[0][0]);
@@ -1359,16 +1300,16 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
   }
 }
 
-// NS > 0: subtract reset with NS LIF steps per group (specialised hot path);
-// NS == 0: any reset, runtime step count.
-template <int NCH, int PATH, int NPART, int NS>
-__device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, uint32_t tmem_base,
+// Generic epilogue: any reset form (subtract / delayed / hard) and a runtime number
+// of LIF steps per group, V itself in registers (the subtract-reset configurations
+// with 1, 2, 4 or 8 steps run epilogue_sr instead).
+template <int NCH, int PATH, int NPART>
+__device__ __forceinline__ void epilogue_generic(const TcParams &p, uint8_t *smem, uint32_t tmem_base,
                                               uint32_t bar_t_full, uint32_t bar_t_empty, int cid,
                                               int ncl, uint32_t rank, uint32_t warp,
                                               uint32_t lane) {
   constexpr int NWT = NCH >= 32 ? NCH / 32 : 1;  // spike words per epilogue thread
-  static_assert(NS == 0 || NWT == 1, "specialised path: one spike word per thread");
-  constexpr int NSM = NS ? NS : kMaxSteps;
+  constexpr int NSM = kMaxSteps;
   const float *sc = reinterpret_cast<const float *>(smem + p.off_scale);
   const int e = (int)warp;                   // epilogue warps are 0 .. 4 NPART - 1
   const int quad = (int)(warp & 3);           // TMEM lane quadrant of this warp
@@ -1378,8 +1319,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
   const int co_base = half * NCH;
   const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
   const float decay = p.decay, vth = p.v_th, vres = p.v_reset;
-  const float2 dec2 = make_float2(decay, decay), nth2 = make_float2(-vth, -vth);
-  const int nsteps = NS ? NS : p.nsteps;
+  const int nsteps = p.nsteps;
   const int G = p.G, K = p.K, mode = p.mode, nwo = p.nwo, Cout = p.Cout, Cp = p.Cout_pad;
   const uint32_t chmask = NCH >= 32 ? 0xFFFFFFFFu : ((1u << NCH) - 1u);
   const bool pooled = p.pool == 2;
@@ -1417,8 +1357,8 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
         if (co_base + cc < Cout) v0 = __ldg(p.v_init + vbase + cc);
         if (co_base + cc + 1 < Cout) v1 = __ldg(p.v_init + vbase + cc + 1);
       }
-      V[cc / 2] = NS > 0 ? make_float2(v0 - vth, v1 - vth) : make_float2(v0, v1);  // U = V - v_th
-      if (NS == 0 && p.reset == 1) {  // reading R4
+      V[cc / 2] = make_float2(v0, v1);
+      if (p.reset == 1) {  // reading R4
         if (v0 >= vth) prev[cc / 32] |= 1u << (cc % 32);
         if (v1 >= vth) prev[(cc + 1) / 32] |= 1u << ((cc + 1) % 32);
       }
@@ -1429,15 +1369,11 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
       ptx::mbar_wait(bar_t_full + 8 * acc, aph);
       ptx::tc_fence_after();
       if (e == 0 && lane == 0) trace_mark(p, it, TR_EPI_FULL);
-      constexpr int NSP = (NS > 0) ? NS : 1;
-      uint32_t inv[NSM][NWT];   // generic path: NOT(spike) bits
-      uint32_t sw1[NSP];          // specialised path (NWT == 1): spike words
+      uint32_t inv[NSM][NWT];   // NOT(spike) bits
 #pragma unroll
       for (int j = 0; j < NSM; ++j)
 #pragma unroll
         for (int w = 0; w < NWT; ++w) inv[j][w] = 0u;
-#pragma unroll
-      for (int j = 0; j < NSP; ++j) sw1[j] = 0u;
       const uint32_t tcol = tmem_base + lane_addr + acc * p.n_total + (uint32_t)co_base;
       constexpr bool F16 = PATH != PATH_HALO;  // fp32 Y straight from TMEM
       constexpr int NBUF = (NPART == 2 || F16) ? 2 : 1;  // TMEM prefetch depth (registers)
@@ -1459,14 +1395,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
         } else {
           combine8(p, sc, co_base + ch * 8, d[cur][0], d[cur][1], yv);
         }
-        if (NS > 0) {
-          switch (ch) {  // compile-time after unrolling (NCH <= 32: one spike word)
-            case 0: lif_chunk8<NSP, 0>(V + ch * 4, yv, dec2, nth2, sw1); break;
-            case 1: lif_chunk8<NSP, 8>(V + ch * 4, yv, dec2, nth2, sw1); break;
-            case 2: lif_chunk8<NSP, 16>(V + ch * 4, yv, dec2, nth2, sw1); break;
-            default: lif_chunk8<NSP, 24>(V + ch * 4, yv, dec2, nth2, sw1); break;
-          }
-        } else {
+        {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int cc = ch * 8 + i;
@@ -1504,16 +1433,16 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
       for (int j = 0; j < NSM; ++j)
 #pragma unroll
         for (int w = 0; w < NWT; ++w)
-          spk[j][w] = !valid ? 0u : (NS > 0 ? sw1[j < NSP ? j : 0] : (~inv[j][w] & chmask));
+          spk[j][w] = !valid ? 0u : (~inv[j][w] & chmask);
 #pragma unroll
       for (int j = 0; j < NSM; ++j) {
-        if (NS > 0 || j < nsteps) {
+        if (j < nsteps) {
           const int t_out = mode == 1 ? k : k * K + j;
           uint32_t *orow_t = orow + (long long)t_out * p.out_st;
 #pragma unroll
           for (int w = 0; w < NWT; ++w) {
             uint32_t s = spk[j][w];
-            if (NS == 0 || NS == 1) {  // ripple add of one word into the counters
+            {  // ripple add of one word into the counters
               uint32_t cy = s;
 #pragma unroll
               for (int pl = 0; pl < kPlanes; ++pl) {
@@ -1537,25 +1466,6 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
           }
         }
       }
-      if (NS >= 2) {  // carry-save counting of this group's NS spike words
-#pragma unroll
-        for (int w = 0; w < NWT; ++w) {
-          uint32_t sw[NSM];
-#pragma unroll
-          for (int j = 0; j < NSM; ++j) sw[j] = spk[j][w];
-          uint32_t P[kPlanes];
-#pragma unroll
-          for (int pl = 0; pl < kPlanes; ++pl) P[pl] = planes[pl][w];
-          if (NS == 2) {
-            planes_add3(P, sw[0] ^ sw[1], sw[0] & sw[1], 0u);
-          } else {
-#pragma unroll
-            for (int j = 0; j < NSM; j += 4) planes_add4(P, sw[j], sw[j + 1], sw[j + 2], sw[j + 3]);
-          }
-#pragma unroll
-          for (int pl = 0; pl < kPlanes; ++pl) planes[pl][w] = P[pl];
-        }
-      }
       steps_acc += nsteps;
       if (p.counts && (steps_acc + nsteps > (1 << kPlanes) - 1 || k == G - 1)) {
         if (tok) flush_counts<NWT>(p, planes, b, co_base, NCH, lane);
@@ -1566,7 +1476,7 @@ __device__ __forceinline__ void epilogue_role(const TcParams &p, uint8_t *smem, 
     if (p.v_final && valid) {
 #pragma unroll
       for (int cc = 0; cc < NCH; cc += 2) {
-        const float2 v = NS > 0 ? make_float2(V[cc / 2].x + vth, V[cc / 2].y + vth) : V[cc / 2];
+        const float2 v = V[cc / 2];
         if (co_base + cc < Cout) p.v_final[vbase + cc] = v.x;
         if (co_base + cc + 1 < Cout) p.v_final[vbase + cc + 1] = v.y;
       }
@@ -1794,7 +1704,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
       case 2: epilogue_sr<NCH, PATH, NPART, 2>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
       case 4: epilogue_sr<NCH, PATH, NPART, 4>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
       case 8: epilogue_sr<NCH, PATH, NPART, 8>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      default: epilogue_role<NCH, PATH, NPART, 0>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      default: epilogue_generic<NCH, PATH, NPART>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
     }
     }
 

@@ -128,9 +128,15 @@ template <int C0> __device__ __forceinline__ void v10(float2 &u, float2 y, float
 }
 
 template <int V>
-__global__ void __launch_bounds__(512, 1) bench(const float *ys, uint32_t *sink, int groups, long long *cyc, float beta, float th) {
-  float2 u[16];
-  for (int i = 0; i < 16; ++i) u[i] = make_float2(0.f, 0.f);
+#ifndef NP
+#define NP 16  // neuron pairs per thread
+#endif
+#ifndef THREADS
+#define THREADS 512
+#endif
+__global__ void __launch_bounds__(THREADS, 1) bench(const float *ys, uint32_t *sink, int groups, long long *cyc, float beta, float th) {
+  float2 u[NP];
+  for (int i = 0; i < NP; ++i) u[i] = make_float2(0.f, 0.f);
   const float2 dec2 = make_float2(beta, beta), nth2 = make_float2(-th, -th);
   uint32_t x = 0;
   const float *yp = ys + (threadIdx.x & 31) * 32;
@@ -146,7 +152,7 @@ __global__ void __launch_bounds__(512, 1) bench(const float *ys, uint32_t *sink,
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
+      for (int c = 0; c < NP; ++c) {
         const float2 y = make_float2(yv[2 * c], yv[2 * c + 1]);
         if (V == 0) {
           switch (c % 16) {
@@ -220,13 +226,13 @@ __global__ void __launch_bounds__(512, 1) bench(const float *ys, uint32_t *sink,
     x ^= w[0] + 3 * w[1] + 5 * w[2] + 7 * w[3];
   }
   long long t1 = clock64();
-  float s = 0; for (int i = 0; i < 16; ++i) s += u[i].x + u[i].y;
+  float s = 0; for (int i = 0; i < NP; ++i) s += u[i].x + u[i].y;
   sink[blockIdx.x * blockDim.x + threadIdx.x] = x ^ __float_as_uint(s);
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
 int main() {
-  const int groups = 2000, blocks = 148, threads = 512;
+  const int groups = 2000, blocks = 148, threads = THREADS;
   float *ys; uint32_t *sink; long long *cyc;
   cudaMalloc(&ys, 32 * 32 * 4 * 8); cudaMalloc(&sink, blocks * threads * 4); cudaMalloc(&cyc, blocks * 8);
   static float h[8192]; for (int i = 0; i < 8192; ++i) h[i] = 0.05f + 0.3f * ((i * 37) % 101) / 101.f;
@@ -250,7 +256,7 @@ int main() {
       float ms; cudaEventElapsedTime(&ms, a, b);
       long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
       // per SMSP: 4 warps x groups x 4 steps x 32 neurons (warp-level neuron-steps)
-      double per = (double)c / (4.0 * groups * 4 * 32);
+      double per = (double)c / ((THREADS / 128.0) * groups * 4 * 2 * NP);
       if (rep) printf("variant %d: %.3f ms, %.3f cycles per warp-neuron-step per SMSP (%s)\n", v, ms, per,
                       cudaGetErrorString(cudaGetLastError()));
     }
