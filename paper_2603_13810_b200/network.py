@@ -62,12 +62,15 @@ class Network:
         """Kernels one forward launches (measured from the library's counter)."""
         return self._launches
 
-    def count_launches(self, x):
+    def count_launches(self, x, want_counts: bool | str = "last"):
+        """Kernels one forward (same counts policy as forward) launches."""
         n = 0
         B = x.shape[1]
-        for spec, prep in zip(self.specs, self.prepared):
+        nl = len(self.specs)
+        for i, (spec, prep) in enumerate(zip(self.specs, self.prepared)):
             s = spec if spec.B == B else spec.replace(B=B)
-            x, _, _ = tacsnn.conv_lif(s, prep, x)
+            wc = want_counts is True or (want_counts == "last" and i == nl - 1)
+            x, _, _ = tacsnn.conv_lif(s, prep, x, want_counts=wc)
             n += tacsnn.last_launch_count()
         self._launches = n
         return n
