@@ -64,6 +64,9 @@ constexpr int kProdWarps = 3;
 #ifndef TACSNN_HALO_NR
 #define TACSNN_HALO_NR 2  // halo producer pixels per pass (K <= 4)
 #endif
+#ifndef TACSNN_H16_PACK
+#define TACSNN_H16_PACK 1
+#endif
 #ifndef TACSNN_REFILL_EARLY
 #define TACSNN_REFILL_EARLY 1
 #endif
@@ -116,6 +119,7 @@ struct TcParams {
   uint32_t w_bytes_cta, tmem_cols, n_total, lbo_a, sbo_a, lbo_b;
   int tap_off[9];
   int naccs;             // TMEM accumulators in the MMA -> epilogue ring
+  int packed;            // fp16 path, C_in <= 3: hi and lo weight slices share one K=16 MMA
   int split;             // A carried as fp16 hi + lo from the 2^K-entry table lut
   int real;              // continuous input xin (A computed from fp32 frames, then hi + lo)
   const float *xin;      // fp32 [T][B][H][W][C_in], strides in_st / in_sb in floats
@@ -193,6 +197,11 @@ int h16_chunks(const tac_conv_lif_desc *d) {
   const int ch = split_of(d) ? 2 * d->C_in + 1 : d->C_in + 1;
   const int nck = (ch + 7) / 8;
   return nck < 2 ? 2 : (nck + 1) / 2 * 2;
+}
+
+// fp16 path with both weight slices in one K = 16 MMA per tap (C_in + 1 <= 4 channels each)
+bool packed_of(const tac_conv_lif_desc *d) {
+  return TACSNN_H16_PACK && !split_of(d) && path_of(d) == PATH_H16 && d->C_in <= 3;
 }
 
 struct Geometry {
@@ -379,6 +388,15 @@ __device__ __forceinline__ void h16_acc(uint32_t &lo, uint32_t &hi, uint32_t bit
   hi |= ((((bits >> 4) & 0xFu) * 0x204081u) & 0x01010101u) << e;
 }
 
+// packed slices (C_in <= 3): the C_in + 1 bytes [A | 1] of lo repeated right after
+// themselves, so K channels [A | 1 | A | 1] meet [W_hi | b_hi | W_lo | b_lo]
+__device__ __forceinline__ void h16_pack_slices(uint32_t &lo, uint32_t &hi, int Cin) {
+  uint64_t v = lo;
+  v |= v << (8 * (Cin + 1));
+  lo = (uint32_t)v;
+  hi = (uint32_t)(v >> 32);
+}
+
 __device__ __forceinline__ uint32_t u8x2_to_f16x2(uint32_t bytes, uint32_t sel) {
   uint32_t h = __byte_perm(bytes, 0x64646464u, sel), r;
   asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(h), "r"(0x64006400u));
@@ -421,6 +439,7 @@ __device__ __forceinline__ void produce_h16(const TcParams &p, int tile, int k, 
     uint32_t lo = one_lo, hi = one_hi;
 #pragma unroll
     for (int j = 0; j < K; ++j) h16_acc(lo, hi, __funnelshift_r(w0[j], w1[j], sh) & cmask, p.m_shift * j);
+    if (p.packed) h16_pack_slices(lo, hi, Cin);
     store_h16_row(a_stage + (uint32_t)row * 16u, p.lbo_a, lo, hi, c8);
   }
 }
@@ -729,6 +748,10 @@ __device__ __forceinline__ void produce_h16_tma(const TcParams &p, const uint32_
         h16_acc(lo0, hi0, bits0, mshift * j);
         h16_acc(lo1, hi1, bits1, mshift * j);
       }
+    }
+    if (p.packed) {
+      h16_pack_slices(lo0, hi0, Cin);
+      h16_pack_slices(lo1, hi1, Cin);
     }
     const uint32_t d0 = a_stage + (uint32_t)row * 16u;
     ptx::st_shared_v4(d0, u8x2_to_f16x2(lo0, 0x5140u), u8x2_to_f16x2(lo0, 0x7362u),
@@ -1485,27 +1508,28 @@ __device__ __forceinline__ void epilogue_generic(const TcParams &p, uint8_t *sme
 }
 
 // fp16-path MMAs of one group: 9 taps x {hi, lo} weight slices x NKC2 K=16 steps
-template <int NKC2>
+template <int NKC2, int NSL>
 __device__ __forceinline__ void mma_tap_h16(int tap, uint32_t d_tmem, uint64_t a_base, uint64_t b_desc0,
                                             uint32_t idf, uint32_t lbo16, uint32_t nhb16) {
   const uint32_t toff = (uint32_t)((tap / 3) * kHaloW + (tap % 3));
 #pragma unroll
-  for (int sl = 0; sl < 2; ++sl)
+  for (int sl = 0; sl < NSL; ++sl)
 #pragma unroll
     for (int kc2 = 0; kc2 < NKC2; ++kc2)
       ptx::mma_f16_cg2(d_tmem, a_base + (uint64_t)(toff + 2u * kc2 * lbo16),
                        b_desc0 + (uint64_t)(((sl * 9 + tap) * 2 * NKC2 + 2 * kc2) * nhb16), idf,
                        (tap | sl | kc2) ? 1u : 0u);
 }
-template <int NKC2>
+// NSL = 1: packed slices (one MMA per tap computes A W_hi + A W_lo + bias)
+template <int NKC2, int NSL>
 __device__ __forceinline__ void mma_group_h16(uint32_t d_tmem, uint64_t a_base, uint64_t b_desc0,
                                               uint32_t idf, uint32_t lbo16, uint32_t nhb16) {
   if constexpr (NKC2 == 1) {
 #pragma unroll
-    for (int tap = 0; tap < 9; ++tap) mma_tap_h16<NKC2>(tap, d_tmem, a_base, b_desc0, idf, lbo16, nhb16);
+    for (int tap = 0; tap < 9; ++tap) mma_tap_h16<NKC2, NSL>(tap, d_tmem, a_base, b_desc0, idf, lbo16, nhb16);
   } else {
 #pragma unroll 1
-    for (int tap = 0; tap < 9; ++tap) mma_tap_h16<NKC2>(tap, d_tmem, a_base, b_desc0, idf, lbo16, nhb16);
+    for (int tap = 0; tap < 9; ++tap) mma_tap_h16<NKC2, NSL>(tap, d_tmem, a_base, b_desc0, idf, lbo16, nhb16);
   }
 }
 
@@ -1658,10 +1682,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
                 // (nkc 16-B chunks per halo pixel; K = 16 = two chunks per MMA; the
                 // common chunk counts are fully unrolled: no per-MMA address arithmetic)
                 const uint32_t idf = ptx::idesc_f16(256, p.n_total);
-                if (PATH == PATH_H16 || nkc2 == 1)
-                  mma_group_h16<1>(d_tmem, a_base, b_desc0, idf, lbo16, nhb16);
+                if (PATH == PATH_H16 && p.packed)
+                  mma_group_h16<1, 1>(d_tmem, a_base, b_desc0, idf, lbo16, nhb16);
+                else if (PATH == PATH_H16 || nkc2 == 1)
+                  mma_group_h16<1, 2>(d_tmem, a_base, b_desc0, idf, lbo16, nhb16);
                 else
-                  mma_group_h16<5>(d_tmem, a_base, b_desc0, idf, lbo16, nhb16);
+                  mma_group_h16<5, 2>(d_tmem, a_base, b_desc0, idf, lbo16, nhb16);
               }
               ptx::mma_commit_cg2_multicast(bar_a_empty + 8 * s);
               ptx::mma_commit_cg2_multicast(bar_t_full + 8 * acc);
@@ -1830,6 +1856,26 @@ void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bi
       const double agg = split ? 1.0 : std::ldexp(1.0, -m * (Kg - 1));
       const int nh = Cp / 2, nk = g.nkc, kbias = split ? 2 * Ci : Ci;
       uint16_t *img16 = reinterpret_cast<uint16_t *>(img);
+      if (packed_of(d)) {
+        // packed slices (one MMA per tap): slice 0 holds [W_hi | b_hi | W_lo | b_lo] against
+        // the halo channels [A | 1 | A | 1]; slice 1 stays zero (not read)
+        for (int nl = 0; nl < nh; ++nl) {
+          const int n = half * nh + nl;
+          for (int tap = 0; tap < 9; ++tap)
+            for (int k = 0; k < 8 * nk; ++k) {
+              const int part = k / (Ci + 1), kk = k % (Ci + 1);  // 0: hi, 1: lo
+              double wv = 0.0;
+              if (n < Co && part < 2) {
+                if (kk < Ci) wv = (double)weight[(((size_t)n * Ci + kk) * 3 + tap / 3) * 3 + tap % 3] * agg;
+                else if (tap == 4) wv = (bias ? (double)bias[n] : 0.0) + boff;
+              }
+              const __half hi = __double2half(wv);
+              const __half v = part == 0 ? hi : __double2half(part == 1 ? wv - (double)__half2float(hi) : 0.0);
+              img16[((((size_t)0 * 9 + tap) * nk + k / 8) * nh + nl) * 8 + k % 8] = __half_as_ushort(v);
+            }
+        }
+        continue;
+      }
       for (int nl = 0; nl < nh; ++nl) {
         const int n = half * nh + nl;
         for (int tap = 0; tap < 9; ++tap)
@@ -1965,6 +2011,7 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   // accumulators: 3 on the fp16 paths (n_total = C_out_pad; with U in TMEM 3 x 128 +
   // 128 = 512 columns), 2 on the int8 path (n_total = 2 C_out_pad)
   p.naccs = g.path == PATH_HALO ? 2 : TACSNN_H16_ACCS;
+  p.packed = packed_of(d) ? 1 : 0;
   while (cols < (uint32_t)p.naccs * p.n_total + (ut ? 128u : 0u)) cols <<= 1;
   p.tmem_cols = cols;
   p.lbo_a = (uint32_t)kHaloRows * 16u;  // between 16-byte K chunks
