@@ -200,8 +200,10 @@ int h16_chunks(const tac_conv_lif_desc *d) {
 }
 
 // fp16 path with both weight slices in one K = 16 MMA per tap (C_in + 1 <= 4 channels each)
+// (split aggregate: [A_hi | A_lo | 1 | A_hi | 1] x [W_hi | W_hi | b_hi | W_lo | b_lo], C_in <= 2)
 bool packed_of(const tac_conv_lif_desc *d) {
-  return TACSNN_H16_PACK && !split_of(d) && path_of(d) == PATH_H16 && d->C_in <= 3;
+  if (!TACSNN_H16_PACK || path_of(d) != PATH_H16) return false;
+  return split_of(d) ? d->C_in <= 2 : d->C_in <= 3;
 }
 
 struct Geometry {
@@ -533,12 +535,21 @@ __device__ __forceinline__ uint32_t frame_index(const uint32_t (&bits)[K], int c
   return idx;
 }
 // chunk 0 of a C_in <= 2 split row: [A_hi(0..CIN-1) | A_lo(0..CIN-1) | 1.0 | 0 ...]
+// e_c = fp16 A_hi | fp16 A_lo << 16 of channel c -> chunk 0 of a split row; packed:
+// [A_hi | A_lo | 1 | A_hi | 1] (both weight slices in one MMA), else [A_hi | A_lo | 1]
+template <int CIN>
+__device__ __forceinline__ uint4 split_row_words(uint32_t e0, uint32_t e1, bool packed) {
+  if (CIN == 1)
+    return packed ? make_uint4(e0, 0x3C00u | (e0 << 16), 0x3C00u, 0u) : make_uint4(e0, 0x3C00u, 0u, 0u);
+  const uint32_t his = __byte_perm(e0, e1, 0x5410u), los = __byte_perm(e0, e1, 0x7632u);
+  return packed ? make_uint4(his, los, 0x3C00u | (e0 << 16), (e1 & 0xFFFFu) | 0x3C000000u)
+                : make_uint4(his, los, 0x3C00u, 0u);
+}
 template <int K, int CIN>
-__device__ __forceinline__ uint4 split_row_small(const uint32_t (&bits)[K], const uint32_t *lut) {
+__device__ __forceinline__ uint4 split_row_small(const uint32_t (&bits)[K], const uint32_t *lut, bool packed) {
   const uint32_t e0 = lut[frame_index<K>(bits, 0)];
-  if (CIN == 1) return make_uint4(e0, 0x3C00u, 0u, 0u);
-  const uint32_t e1 = lut[frame_index<K>(bits, 1)];
-  return make_uint4(__byte_perm(e0, e1, 0x5410u), __byte_perm(e0, e1, 0x7632u), 0x3C00u, 0u);
+  const uint32_t e1 = CIN == 2 ? lut[frame_index<K>(bits, 1)] : 0u;
+  return split_row_words<CIN>(e0, e1, packed);
 }
 // C_in = 32 split row: 8 index words (byte b of o[q] = channel q + 8b) -> chunks
 // 0..3 A_hi, 4..7 A_lo, 8 = {1.0, 0 ...}, 9 = 0
@@ -587,9 +598,7 @@ __device__ __forceinline__ void produce_h16x(const TcParams &p, int tile, int k,
       const __half lo = __float2half_rn(a[c] - __half2float(hi));
       e[c] = (uint32_t)__half_as_ushort(hi) | ((uint32_t)__half_as_ushort(lo) << 16);
     }
-    uint4 c0;
-    if (CIN == 1) c0 = make_uint4(e[0], 0x3C00u, 0u, 0u);
-    else c0 = make_uint4(__byte_perm(e[0], e[CIN - 1], 0x5410u), __byte_perm(e[0], e[CIN - 1], 0x7632u), 0x3C00u, 0u);
+    const uint4 c0 = split_row_words<CIN>(e[0], e[CIN - 1], p.packed);
     const uint32_t dst = a_stage + (uint32_t)row * 16u;
     ptx::st_shared_v4(dst, c0.x, c0.y, c0.z, c0.w);
     ptx::st_shared_v4(dst + p.lbo_a, 0u, 0u, 0u, 0u);
@@ -618,7 +627,7 @@ __device__ __forceinline__ void produce_h16s(const TcParams &p, const uint32_t *
       const uint32_t w1 = two ? __ldg(src + (long long)j * p.in_st + 1) : 0u;
       bits[j] = __funnelshift_r(w0, w1, sh);
     }
-    const uint4 c0 = split_row_small<K, CIN>(bits, lut);
+    const uint4 c0 = split_row_small<K, CIN>(bits, lut, p.packed);
     const uint32_t dst = a_stage + (uint32_t)row * 16u;
     ptx::st_shared_v4(dst, c0.x, c0.y, c0.z, c0.w);
     ptx::st_shared_v4(dst + p.lbo_a, 0u, 0u, 0u, 0u);
@@ -780,7 +789,7 @@ __device__ __forceinline__ void produce_h16s_tma(const TcParams &p, const uint32
     uint32_t bits[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) bits[j] = __funnelshift_r(src[j * fstride], src[j * fstride + 1], sh);
-    const uint4 c = split_row_small<K, CIN>(bits, lut);
+    const uint4 c = split_row_small<K, CIN>(bits, lut, p.packed);
     ptx::st_shared_v4(a_stage + (uint32_t)row * 16u, c.x, c.y, c.z, c.w);
   }
 }
@@ -1682,7 +1691,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
                 // (nkc 16-B chunks per halo pixel; K = 16 = two chunks per MMA; the
                 // common chunk counts are fully unrolled: no per-MMA address arithmetic)
                 const uint32_t idf = ptx::idesc_f16(256, p.n_total);
-                if (PATH == PATH_H16 && p.packed)
+                if (p.packed)
                   mma_group_h16<1, 1>(d_tmem, a_base, b_desc0, idf, lbo16, nhb16);
                 else if (PATH == PATH_H16 || nkc2 == 1)
                   mma_group_h16<1, 2>(d_tmem, a_base, b_desc0, idf, lbo16, nhb16);
@@ -1863,11 +1872,15 @@ void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bi
           const int n = half * nh + nl;
           for (int tap = 0; tap < 9; ++tap)
             for (int k = 0; k < 8 * nk; ++k) {
-              const int part = k / (Ci + 1), kk = k % (Ci + 1);  // 0: hi, 1: lo
+              // exact: [W (C_in) | b] hi then lo; split: [W (C_in) | W (C_in) | b] hi then [W | b] lo
+              const int nhi = split ? 2 * Ci + 1 : Ci + 1;
+              const int part = k < nhi ? 0 : (k < nhi + Ci + 1 ? 1 : 2);  // 0: hi, 1: lo, 2: pad
+              const int kk = part == 0 ? k : k - nhi;
+              const int nw = part == 0 && split ? 2 * Ci : Ci;  // weight channels before the bias
               double wv = 0.0;
               if (n < Co && part < 2) {
-                if (kk < Ci) wv = (double)weight[(((size_t)n * Ci + kk) * 3 + tap / 3) * 3 + tap % 3] * agg;
-                else if (tap == 4) wv = (bias ? (double)bias[n] : 0.0) + boff;
+                if (kk < nw) wv = (double)weight[(((size_t)n * Ci + kk % Ci) * 3 + tap / 3) * 3 + tap % 3] * agg;
+                else if (kk == nw && tap == 4) wv = (bias ? (double)bias[n] : 0.0) + boff;
               }
               const __half hi = __double2half(wv);
               const __half v = part == 0 ? hi : __double2half(part == 1 ? wv - (double)__half2float(hi) : 0.0);
