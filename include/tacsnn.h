@@ -119,7 +119,16 @@ typedef struct tac_conv_lif_desc {
   int64_t in_stride_t, in_stride_b; /* u32 words (REAL input: floats); 0 = default  */
   int64_t out_stride_t, out_stride_b;
   int32_t input_kind;               /* tac_input (0 = packed spikes)                */
-  int32_t reserved0;                /* must be 0                                    */
+  int32_t partial_last_group;       /* 0: K must divide T (TAC_ERR_K_NOT_DIVIDING_T);
+                                       1: G = ceil(T/K) groups, the last one of
+                                       K' = T - (G-1)K frames is a complete group of
+                                       size K' (A_k with beta^{K'-1-j}, TAC decay
+                                       beta^{K'}, K' TAC-TP steps) -- the paper's
+                                       T = 25 with K = 4/8/16.
+                                       Runs as the full groups + the short group
+                                       chained through the membrane state; needs a
+                                       workspace (tac_workspace_bytes); a short group
+                                       outside the tcgen05 envelope runs on SIMT.  */
 } tac_conv_lif_desc;
 
 /* Validate a descriptor (no device access).  TAC_OK or the first violation. */
@@ -144,7 +153,9 @@ tac_status tac_prepare_weights(const tac_conv_lif_desc *desc, const float *weigh
                                const float *bias, void *prepared, size_t bytes,
                                void *stream);
 
-/* Workspace bytes tac_conv_lif_forward needs (may be 0). */
+/* Workspace bytes tac_conv_lif_forward needs: 0, except with partial_last_group
+ * and K not dividing T (the membrane state between the full groups and the short
+ * last group, fp32 [B][H'][W'][C_out], plus u32 [B][C_out] counts). */
 tac_status tac_workspace_bytes(const tac_conv_lif_desc *desc, size_t *bytes);
 
 /* The layer (one call = whole sequence, all groups).

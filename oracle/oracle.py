@@ -89,7 +89,8 @@ def conv2d(X, Wt, bias=None, stride=1, pad=0):
 
 
 def forward(S, Wt, bias=None, *, K=1, mode="tac", beta=0.9, v_th=1.0, v_reset=0.0,
-            reset="subtract", stride=1, pad=0, v_init=None, replay=None, band=1e-3):
+            reset="subtract", stride=1, pad=0, v_init=None, replay=None, band=1e-3,
+            partial=False):
     """One Conv-LIF layer (Eq. 1 / Alg. 1 / Alg. 2) on u8 spikes S [T,B,Cin,H,W]
     or, when S is a floating array, on continuous-valued input frames (computed
     in fp64; the DVS first layer's log-normalised counts).
@@ -110,10 +111,10 @@ def forward(S, Wt, bias=None, *, K=1, mode="tac", beta=0.9, v_th=1.0, v_reset=0.
     m = MODES[mode]
     if m == 0:
         K = 1
-    if T % K:
+    if T % K and not partial:
         raise ValueError(f"K={K} does not divide T={T}")
     Ho, Wo = out_hw(H, W, R, Sk, stride, pad)
-    T_out = T // K if m == 1 else T
+    T_out = -(-T // K) if m == 1 else T   # partial=True: ceil(T/K) groups, the last one short
     out = np.empty((T_out, B, Cout, Ho, Wo), np.uint8)
     v_final = np.empty((B, Cout, Ho, Wo), np.float64)
     counts = np.empty((B, Cout), np.int64)
@@ -128,7 +129,8 @@ def forward(S, Wt, bias=None, *, K=1, mode="tac", beta=0.9, v_th=1.0, v_reset=0.
     f32 = lambda v: float(np.float32(v))
     fwd = lib().tac_oracle_forward_x if real else lib().tac_oracle_forward
     rc = fwd(
-        _ptr(S), _ptr(Wt), _ptr(bias), T, B, Cin, H, W, Cout, R, Sk, stride, pad, K, m,
+        _ptr(S), _ptr(Wt), _ptr(bias), T, B, Cin, H, W, Cout, R, Sk, stride, pad,
+        -K if (partial and m != 0) else K, m,
         f32(beta), f32(v_th), f32(v_reset), RESETS[reset], _ptr(v_init), _ptr(out),
         _ptr(v_final), _ptr(counts), _ptr(replay), float(band), _ptr(mism), _ptr(exc))
     if rc != 0:

@@ -140,10 +140,14 @@ static int forward_impl(const uint8_t *S, const double *X, const float *Wt, cons
                         int64_t *counts, const uint8_t *replay, double band,
                         int64_t *mismatch_out, int64_t *excused_out) {
   if (mode == OR_MODE_DENSE) K = 1;
-  if (K < 1 || T < 1 || T % K != 0) return -1;
+  const int partial = K < 0;  /* K < 0: group size -K with a partial last group (ceil) */
+  if (partial) K = -K;
+  if (K < 1 || T < 1 || (!partial && T % K != 0)) return -1;
   int Ho = (H + 2 * pad - R) / stride + 1, Wo = (W + 2 * pad - Sk) / stride + 1;
   if (Ho < 1 || Wo < 1) return -1;
-  const int G = T / K;
+  /* K | T: G = T/K groups.  Partial (reading D6'): G = ceil(T/K), the last group
+   * has K_g = T - (G-1)K frames and is exactly a K = K_g group (A, decay, steps). */
+  const int G = (T + K - 1) / K;
   const int T_out = (mode == OR_MODE_TAC) ? G : T;
   const size_t nin = (size_t)Cin * H * W, nout = (size_t)Cout * Ho * Wo;
   int64_t mism = 0, exc = 0;
@@ -161,10 +165,11 @@ static int forward_impl(const uint8_t *S, const double *X, const float *Wt, cons
     if (counts) for (int co = 0; co < Cout; ++co) counts[(size_t)b * Cout + co] = 0;
 
     for (int k = 0; k < G; ++k) {
+      const int Kg = (T - k * K < K) ? T - k * K : K; /* frames in this group */
       /* A_k = sum_{j=0}^{K-1} beta^{K-1-j} S_{kK+j}.  Dense: A = S_t. */
       for (size_t i = 0; i < nin; ++i) A[i] = 0.0;
-      for (int j = 0; j < K; ++j) {
-        double wj = pow(beta, (double)(K - 1 - j));
+      for (int j = 0; j < Kg; ++j) {
+        double wj = pow(beta, (double)(Kg - 1 - j));
         const size_t off = ((size_t)(k * K + j) * B + b) * nin;
         if (X) { /* continuous-valued input frames, same definition */
           for (size_t i = 0; i < nin; ++i) A[i] += wj * X[off + i];
@@ -175,8 +180,8 @@ static int forward_impl(const uint8_t *S, const double *X, const float *Wt, cons
       /* Y_k = Conv2d(A_k, W): one conv call per group (Alg.1 l.4, Alg.2 l.4). */
       conv_one(A, Wt, bias, Cin, H, W, Cout, R, Sk, stride, pad, Ho, Wo, Y);
 
-      int nsteps = (mode == OR_MODE_TACTP) ? K : 1;
-      double decay = (mode == OR_MODE_TAC) ? pow(beta, (double)K) : beta;
+      int nsteps = (mode == OR_MODE_TACTP) ? Kg : 1;
+      double decay = (mode == OR_MODE_TAC) ? pow(beta, (double)Kg) : beta;
       for (int j = 0; j < nsteps; ++j) {
         int t_out = (mode == OR_MODE_TAC) ? k : k * K + j;
         size_t ob = ((size_t)t_out * B + b) * nout;

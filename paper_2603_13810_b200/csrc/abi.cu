@@ -32,6 +32,7 @@ tac_status fail(tac_status st, const char *fmt, ...) {
 
 struct Geo {
   int Ho, Wo, Hq, Wq, G, T_out, nsteps, wpr_in, wpr_out, K;
+  int K_last;  // frames of the last group (== K unless partial_last_group and K does not divide T)
   long long in_st, in_sb, out_st, out_sb;
 };
 
@@ -57,7 +58,7 @@ tac_status check(const tac_conv_lif_desc *d, Geo *g) {
     return fail(TAC_ERR_PARAM, "beta=%g not in (0,1) (PAPER.md:105)", (double)d->beta);
   if (!(d->v_th > 0.f)) return fail(TAC_ERR_PARAM, "v_th=%g must be > 0", (double)d->v_th);
   const int K = d->mode == TAC_MODE_DENSE ? 1 : d->K;
-  if (K < 1 || d->T % K != 0)
+  if (K < 1 || (d->T % K != 0 && d->partial_last_group != 1))
     return fail(TAC_ERR_K_NOT_DIVIDING_T, "K=%d must be >= 1 and divide T=%d (PAPER.md:444)",
                 d->K, d->T);
   if (K > tacsnn::kMaxK) return fail(TAC_ERR_UNSUPPORTED, "K=%d > %d", K, tacsnn::kMaxK);
@@ -75,13 +76,15 @@ tac_status check(const tac_conv_lif_desc *d, Geo *g) {
     return fail(TAC_ERR_SHAPE, "negative stride");
   if (d->input_kind != TAC_INPUT_SPIKES && d->input_kind != TAC_INPUT_REAL)
     return fail(TAC_ERR_PARAM, "input_kind=%d not in {0,1}", d->input_kind);
-  if (d->reserved0 != 0) return fail(TAC_ERR_PARAM, "reserved0 must be 0");
+  if (d->partial_last_group != 0 && d->partial_last_group != 1)
+    return fail(TAC_ERR_PARAM, "partial_last_group=%d not in {0,1}", d->partial_last_group);
   g->K = K;
   g->Ho = Ho;
   g->Wo = Wo;
   g->Hq = d->out_pool == 2 ? Ho / 2 : Ho;
   g->Wq = d->out_pool == 2 ? Wo / 2 : Wo;
-  g->G = d->T / K;
+  g->G = (d->T + K - 1) / K;
+  g->K_last = d->T - (g->G - 1) * K;
   g->T_out = d->mode == TAC_MODE_TAC ? g->G : d->T;
   g->nsteps = d->mode == TAC_MODE_TACTP ? K : 1;
   g->wpr_in = (d->W * d->C_in + 31) / 32;
@@ -117,6 +120,41 @@ PrepLayout prep_layout(const tac_conv_lif_desc *d) {
   L.tc_bytes = tacsnn::tc_shape_ok(d) ? tacsnn::tc_weights_bytes(d) : 0;
   L.total = align256(L.tc_off + L.tc_bytes);
   return L;
+}
+
+// A layer with a short last group runs as two calls: the full groups (T1 = (G-1) K frames,
+// group size K) and the last K' frames as one group of size K', chained through v_init /
+// v_final in the workspace.  Each part has its own prepared image (the tcgen05 image
+// depends on K), stored back to back.
+bool is_split_call(const tac_conv_lif_desc *d, const Geo &g) {
+  return d->partial_last_group == 1 && d->mode != TAC_MODE_DENSE && g.K_last != g.K;
+}
+tac_conv_lif_desc part_desc(const tac_conv_lif_desc *d, const Geo &g, bool last) {
+  tac_conv_lif_desc p = *d;
+  p.partial_last_group = 0;
+  p.T = last ? g.K_last : (g.G - 1) * g.K;
+  p.K = last ? g.K_last : g.K;
+  p.in_stride_t = g.in_st;  // explicit: the parts keep the caller's layout
+  p.in_stride_b = g.in_sb;
+  p.out_stride_t = g.out_st;
+  p.out_stride_b = g.out_sb;
+  // a short last group outside the tcgen05 envelope (K' not in {1,2,4,8}) runs on SIMT
+  if (last && p.engine == TAC_ENGINE_TCGEN05 && !tacsnn::tc_supported(&p)) p.engine = TAC_ENGINE_AUTO;
+  return p;
+}
+size_t prep_total(const tac_conv_lif_desc *d, const Geo &g) {
+  if (!is_split_call(d, g)) return prep_layout(d).total;
+  size_t n = 0;
+  if (g.G > 1) {
+    const tac_conv_lif_desc a = part_desc(d, g, false);
+    n += prep_layout(&a).total;
+  }
+  const tac_conv_lif_desc b = part_desc(d, g, true);
+  return n + prep_layout(&b).total;
+}
+size_t ws_total(const tac_conv_lif_desc *d, const Geo &g) {
+  if (!is_split_call(d, g) || g.G == 1) return 0;
+  return align256((size_t)d->B * g.Ho * g.Wo * d->C_out * 4) + align256((size_t)d->B * d->C_out * 4);
 }
 
 bool is_device_ptr(const void *p) {
@@ -171,7 +209,7 @@ tac_status tac_weights_bytes(const tac_conv_lif_desc *desc, size_t *bytes) {
   tac_status st = check(desc, &g);
   if (st != TAC_OK) return st;
   if (!bytes) return fail(TAC_ERR_NULL, "bytes is NULL");
-  *bytes = prep_layout(desc).total;
+  *bytes = prep_total(desc, g);
   return TAC_OK;
 }
 
@@ -181,7 +219,7 @@ tac_status tac_workspace_bytes(const tac_conv_lif_desc *desc, size_t *bytes) {
   tac_status st = check(desc, &g);
   if (st != TAC_OK) return st;
   if (!bytes) return fail(TAC_ERR_NULL, "bytes is NULL");
-  *bytes = 0;
+  *bytes = ws_total(desc, g);
   return TAC_OK;
 }
 
@@ -194,8 +232,8 @@ tac_status tac_prepare_weights(const tac_conv_lif_desc *desc, const float *weigh
   if (st != TAC_OK) return st;
   if (!weight) return fail(TAC_ERR_NULL, "weight is NULL");
   if (!prepared) return fail(TAC_ERR_NULL, "prepared is NULL");
-  const PrepLayout L = prep_layout(desc);
-  if (bytes < L.total) return fail(TAC_ERR_WORKSPACE, "prepared buffer %zu < %zu bytes", bytes, L.total);
+  const size_t total = prep_total(desc, g);
+  if (bytes < total) return fail(TAC_ERR_WORKSPACE, "prepared buffer %zu < %zu bytes", bytes, total);
   if ((uintptr_t)prepared % 256) return fail(TAC_ERR_ALIGN, "prepared must be 256-B aligned");
   if (!is_device_ptr(prepared)) return fail(TAC_ERR_PARAM, "prepared is not device memory");
   const int Co = desc->C_out, Ci = desc->C_in, R = desc->R, S = desc->S;
@@ -205,17 +243,30 @@ tac_status tac_prepare_weights(const tac_conv_lif_desc *desc, const float *weigh
   if (bias)
     for (int i = 0; i < Co; ++i)
       if (!std::isfinite(bias[i])) return fail(TAC_ERR_NONFINITE, "bias[%d] is not finite", i);
-  std::vector<unsigned char> img(L.total, 0);
-  float *ws = reinterpret_cast<float *>(img.data() + L.simt_off);
-  for (int co = 0; co < Co; ++co)
-    for (int ci = 0; ci < Ci; ++ci)
-      for (int r = 0; r < R; ++r)
-        for (int s = 0; s < S; ++s)
-          ws[((size_t)(ci * R + r) * S + s) * Co + co] = weight[((size_t)(co * Ci + ci) * R + r) * S + s];
-  float *bs = reinterpret_cast<float *>(img.data() + L.bias_off);
-  for (int co = 0; co < Co; ++co) bs[co] = bias ? bias[co] : 0.f;
-  if (L.tc_bytes) tacsnn::tc_prepare(desc, weight, bias, img.data() + L.tc_off);
-  cudaError_t e = cudaMemcpyAsync(prepared, img.data(), L.total, cudaMemcpyHostToDevice,
+  std::vector<unsigned char> img(total, 0);
+  // one image per part (two when the last group is short): [full groups | last group]
+  std::vector<tac_conv_lif_desc> parts;
+  if (is_split_call(desc, g)) {
+    if (g.G > 1) parts.push_back(part_desc(desc, g, false));
+    parts.push_back(part_desc(desc, g, true));
+  } else {
+    parts.push_back(*desc);
+  }
+  size_t base = 0;
+  for (const tac_conv_lif_desc &pd : parts) {
+    const PrepLayout L = prep_layout(&pd);
+    float *ws = reinterpret_cast<float *>(img.data() + base + L.simt_off);
+    for (int co = 0; co < Co; ++co)
+      for (int ci = 0; ci < Ci; ++ci)
+        for (int r = 0; r < R; ++r)
+          for (int s = 0; s < S; ++s)
+            ws[((size_t)(ci * R + r) * S + s) * Co + co] = weight[((size_t)(co * Ci + ci) * R + r) * S + s];
+    float *bs = reinterpret_cast<float *>(img.data() + base + L.bias_off);
+    for (int co = 0; co < Co; ++co) bs[co] = bias ? bias[co] : 0.f;
+    if (L.tc_bytes) tacsnn::tc_prepare(&pd, weight, bias, img.data() + base + L.tc_off);
+    base += L.total;
+  }
+  cudaError_t e = cudaMemcpyAsync(prepared, img.data(), total, cudaMemcpyHostToDevice,
                                   (cudaStream_t)stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
   if (e != cudaSuccess) return fail(TAC_ERR_CUDA, "prepare copy: %s", cudaGetErrorString(e));
@@ -228,11 +279,63 @@ namespace {
 // shared body of tac_conv_lif_forward / tac_conv_lif_forward_real
 tac_status forward_impl(const tac_conv_lif_desc *desc, const void *prepared, const void *input,
                         bool real, const float *v_init, uint32_t *spikes_out, float *v_final,
-                        uint32_t *counts, void *stream) {
+                        uint32_t *counts, void *ws, size_t ws_bytes, void *stream);
+
+// K does not divide T with partial_last_group: the full groups, then the short last
+// group, chained through the membrane state in the workspace (see part_desc)
+tac_status forward_split(const tac_conv_lif_desc *desc, const Geo &g, const void *prepared,
+                         const void *input, bool real, const float *v_init, uint32_t *spikes_out,
+                         float *v_final, uint32_t *counts, void *ws, size_t ws_bytes, void *stream) {
+  const tac_conv_lif_desc last = part_desc(desc, g, true);
+  if (g.G == 1)  // T < K: the whole sequence is one short group
+    return forward_impl(&last, prepared, input, real, v_init, spikes_out, v_final, counts, nullptr, 0,
+                        stream);
+  const size_t need = ws_total(desc, g);
+  if (!ws) return fail(TAC_ERR_NULL, "partial_last_group with K not dividing T needs a workspace");
+  if (ws_bytes < need) return fail(TAC_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  if ((uintptr_t)ws % 256) return fail(TAC_ERR_ALIGN, "workspace must be 256-B aligned");
+  const tac_conv_lif_desc full = part_desc(desc, g, false);
+  float *v_mid = static_cast<float *>(ws);
+  uint32_t *cnt2 = reinterpret_cast<uint32_t *>(static_cast<unsigned char *>(ws) +
+                                                align256((size_t)desc->B * g.Ho * g.Wo * desc->C_out * 4));
+  tac_status st = forward_impl(&full, prepared, input, real, v_init, spikes_out, v_mid, counts, nullptr, 0,
+                               stream);
+  if (st != TAC_OK) return st;
+  const int launches1 = g_launches;
+  const size_t esz = real ? sizeof(float) : sizeof(uint32_t);
+  const void *in2 = static_cast<const unsigned char *>(input) + (size_t)full.T * g.in_st * esz;
+  const int t_out1 = desc->mode == TAC_MODE_TAC ? g.G - 1 : full.T;
+  uint32_t *out2 = spikes_out + (size_t)t_out1 * g.out_st;
+  const void *prep2 = static_cast<const unsigned char *>(prepared) + prep_layout(&full).total;
+  st = forward_impl(&last, prep2, in2, real, v_mid, out2, v_final, counts ? cnt2 : nullptr, nullptr, 0,
+                    stream);
+  if (st != TAC_OK) return st;
+  int launches = launches1 + g_launches;
+  if (counts) {
+    const int e = tacsnn::launch_add_u32(counts, cnt2, (long long)desc->B * desc->C_out, stream);
+    if (e) return fail(TAC_ERR_CUDA, "count merge: %s", cudaGetErrorString((cudaError_t)e));
+    ++launches;
+  }
+  g_launches = launches;
+  return TAC_OK;
+}
+
+tac_status forward_impl(const tac_conv_lif_desc *desc, const void *prepared, const void *input,
+                        bool real, const float *v_init, uint32_t *spikes_out, float *v_final,
+                        uint32_t *counts, void *ws, size_t ws_bytes, void *stream) {
   g_detail.clear();
   Geo g;
   tac_status st = check(desc, &g);
   if (st != TAC_OK) return st;
+  if (is_split_call(desc, g)) {
+    if ((desc->input_kind == TAC_INPUT_REAL) != real)
+      return fail(TAC_ERR_PARAM, "input_kind does not match the entry point");
+    if (!prepared || !input || !spikes_out) return fail(TAC_ERR_NULL, "NULL buffer");
+    return forward_split(desc, g, prepared, input, real, v_init, spikes_out, v_final, counts, ws,
+                         ws_bytes, stream);
+  }
+  (void)ws;
+  (void)ws_bytes;
   if ((desc->input_kind == TAC_INPUT_REAL) != real)
     return fail(TAC_ERR_PARAM, real ? "tac_conv_lif_forward_real needs input_kind = TAC_INPUT_REAL"
                                     : "input_kind = TAC_INPUT_REAL needs tac_conv_lif_forward_real");
@@ -294,18 +397,16 @@ tac_status tac_conv_lif_forward(const tac_conv_lif_desc *desc, const void *prepa
                                 const uint32_t *spikes_in, const float *v_init,
                                 uint32_t *spikes_out, float *v_final, uint32_t *counts,
                                 void *ws, size_t ws_bytes, void *stream) {
-  (void)ws;
-  (void)ws_bytes;
-  return forward_impl(desc, prepared, spikes_in, false, v_init, spikes_out, v_final, counts, stream);
+  return forward_impl(desc, prepared, spikes_in, false, v_init, spikes_out, v_final, counts, ws, ws_bytes,
+                      stream);
 }
 
 tac_status tac_conv_lif_forward_real(const tac_conv_lif_desc *desc, const void *prepared,
                                      const float *x_in, const float *v_init,
                                      uint32_t *spikes_out, float *v_final, uint32_t *counts,
                                      void *ws, size_t ws_bytes, void *stream) {
-  (void)ws;
-  (void)ws_bytes;
-  return forward_impl(desc, prepared, x_in, true, v_init, spikes_out, v_final, counts, stream);
+  return forward_impl(desc, prepared, x_in, true, v_init, spikes_out, v_final, counts, ws, ws_bytes,
+                      stream);
 }
 
 tac_status tac_pack_spikes(const uint8_t *dense01, uint32_t *packed, int32_t T, int32_t B,

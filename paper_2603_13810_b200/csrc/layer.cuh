@@ -39,6 +39,7 @@ enum { RESET_SUBTRACT = 0, RESET_DELAYED = 1, RESET_HARD = 2 };
 // Launchers implemented in simt.cu / tc.cu.  Return cudaGetLastError() as int.
 int launch_zero_outputs(const LayerParams &p, void *stream, int *launches);
 int launch_simt_conv_lif(const LayerParams &p, void *stream, int *launches);
+int launch_add_u32(uint32_t *dst, const uint32_t *src, long long n, void *stream);  // dst += src
 int launch_pack(const uint8_t *dense, uint32_t *packed, int T, int B, int C, int H,
                 int W, void *stream);
 int launch_unpack(const uint32_t *packed, uint8_t *dense, int T, int B, int C, int H,

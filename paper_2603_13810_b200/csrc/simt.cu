@@ -12,6 +12,8 @@
 // zero_outputs_kernel in the same stream).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "layer.cuh"
 
 namespace tacsnn {
@@ -33,6 +35,12 @@ __global__ void zero_outputs_kernel(uint32_t *out, int T_out, int B, long long p
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ncounts;
          i += (long long)gridDim.x * blockDim.x)
       counts[i] = 0u;
+}
+
+__global__ void add_u32_kernel(uint32_t *dst, const uint32_t *src, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] += src[i];
 }
 
 constexpr int CH = 32;  // output channels per thread
@@ -192,6 +200,12 @@ int launch_zero_outputs(const LayerParams &p, void *stream, int *launches) {
                         256, 0, (cudaStream_t)stream>>>(
       p.out, p.T_out, p.B, plane, p.out_st, p.out_sb, p.counts, (long long)p.B * p.Cout);
   ++*launches;
+  return (int)cudaGetLastError();
+}
+
+int launch_add_u32(uint32_t *dst, const uint32_t *src, long long n, void *stream) {
+  const int grid = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
+  add_u32_kernel<<<grid > 0 ? grid : 1, 256, 0, (cudaStream_t)stream>>>(dst, src, n);
   return (int)cudaGetLastError();
 }
 

@@ -42,7 +42,7 @@ class Desc(ctypes.Structure):
                 ("reset", ctypes.c_int32), ("out_pool", ctypes.c_int32), ("engine", ctypes.c_int32),
                 ("in_stride_t", ctypes.c_int64), ("in_stride_b", ctypes.c_int64),
                 ("out_stride_t", ctypes.c_int64), ("out_stride_b", ctypes.c_int64),
-                ("input_kind", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
+                ("input_kind", ctypes.c_int32), ("partial_last_group", ctypes.c_int32)]
 
 
 _lock = threading.Lock()
@@ -113,6 +113,7 @@ class LayerSpec:
     out_pool: int = 1
     engine: str = "auto"
     input: str = "spikes"     # "real": continuous-valued fp32 input frames (tac_conv_lif_forward_real)
+    partial: bool = False     # K need not divide T: ceil(T/K) groups, the last one short
 
     def replace(self, **kw) -> "LayerSpec":
         return dataclasses.replace(self, **kw)
@@ -122,7 +123,7 @@ class LayerSpec:
                     self.stride, self.pad, 1 if self.mode == "dense" else self.K,
                     MODES[self.mode], self.beta, self.v_th, self.v_reset, RESETS[self.reset],
                     self.out_pool, ENGINES[self.engine], in_strides[0], in_strides[1],
-                    out_strides[0], out_strides[1], INPUTS[self.input], 0)
+                    out_strides[0], out_strides[1], INPUTS[self.input], int(self.partial))
 
     @property
     def conv_hw(self):
@@ -209,9 +210,12 @@ def conv_lif(spec: LayerSpec, prepared: torch.Tensor, x: torch.Tensor, *, v_init
         assert v_init.is_cuda and v_init.dtype == torch.float32 and v_init.is_contiguous()
         assert tuple(v_init.shape) == (spec.B, hc, wc, spec.C_out)
     d = spec.desc((x.stride(0), x.stride(1)), (out.stride(0), out.stride(1)))
+    wsb = ctypes.c_size_t()
+    _check(lib().tac_workspace_bytes(ctypes.byref(d), ctypes.byref(wsb)))
+    ws = torch.empty(wsb.value, dtype=torch.uint8, device=x.device) if wsb.value else None
     fwd = lib().tac_conv_lif_forward_real if real else lib().tac_conv_lif_forward
     _check(fwd(ctypes.byref(d), _ptr(prepared), _ptr(x), _ptr(v_init), _ptr(out), _ptr(v_final),
-               _ptr(counts), None, 0, _stream(x.device)))
+               _ptr(counts), _ptr(ws), wsb.value, _stream(x.device)))
     return out, v_final, counts
 
 

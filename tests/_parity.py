@@ -41,7 +41,7 @@ def check_layer(T, O, spec, S_u8: np.ndarray, w, b, *, x_packed=None, v_init=Non
     D = O.unpack_spikes(to_u32(out), s1.C_out, wc)
     r = O.forward(S_u8, w.numpy(), None if b is None else b.numpy(), K=s1.K, mode=s1.mode,
                   beta=s1.beta, v_th=s1.v_th, v_reset=s1.v_reset, reset=s1.reset,
-                  stride=s1.stride, pad=s1.pad,
+                  stride=s1.stride, pad=s1.pad, partial=s1.partial,
                   v_init=None if v_init is None else v_init.astype(np.float32).astype(np.float64),
                   replay=D, band=BAND)
     assert r["mismatch"] == 0, f"{label}: {r['mismatch']} out-of-band spike mismatches " \

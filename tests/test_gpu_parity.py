@@ -182,6 +182,35 @@ def test_real_input_rejects_spike_call(T):
     assert st == 4 and b"tac_conv_lif_forward_real" in T.lib().tac_last_error_detail()
 
 
+PARTIAL_CASES = [
+    # (T, K): last group of K' = T - (G-1) K frames (the paper's T = 25)
+    ("T10K4", 10, 4), ("T6K4", 6, 4), ("T3K4", 3, 4), ("T25K8", 25, 8),
+]
+PARTIAL_LAYERS = [
+    ("int8", (2, 32, 12, 16, 64, 1, 2), 0.5, 2.5),       # C_in 32, exact aggregate
+    ("fp16", (2, 2, 32, 32, 128, 1, 2), 0.5, 6.0),       # first layer, packed slices
+    ("split", (2, 1, 28, 28, 32, 0, 2), 0.9, 2.5),       # beta = 0.9 split aggregate
+]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("mode", ["tac", "tactp"])
+@pytest.mark.parametrize("layer", PARTIAL_LAYERS, ids=[c[0] for c in PARTIAL_LAYERS])
+@pytest.mark.parametrize("tk", PARTIAL_CASES, ids=[c[0] for c in PARTIAL_CASES])
+def test_partial_last_group_parity(T, O, tk, layer, mode, engine):
+    """K need not divide T (desc.partial_last_group): against the oracle's short-group
+    semantics, on the path each layer type takes."""
+    _, Tn, K = tk
+    name, (B, Cin, H, W, Cout, pad, pool), beta, gain = layer
+    spec = T.LayerSpec(T=Tn, B=B, C_in=Cin, H=H, W=W, C_out=Cout, pad=pad, K=K, mode=mode,
+                       beta=beta, out_pool=pool, partial=True)
+    spec = _engine_or_skip(spec, engine)
+    S = _spikes(zlib.crc32((name + tk[0]).encode()) % 977, (Tn, B, Cin, H, W), 0.15)
+    w, b = _w(12, Cout, Cin, gain)
+    _, _, st = P.check_layer(T, O, spec, S, w, b, label=f"partial/{tk[0]}/{name}/{mode}/{engine}")
+    assert 0.0 < st["rate"] < 0.95, st
+
+
 @pytest.mark.parametrize("mode", ["tac", "tactp"])
 def test_odd_group_size_runs_on_simt(T, O, mode):
     """K = 3 (T = 6) is outside the tcgen05 envelope (K in {1,2,4,8}): AUTO must pick

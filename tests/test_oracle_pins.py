@@ -364,3 +364,36 @@ def test_theorem1_statistical_c1_shape(oracle_mod):
         assert err <= bound, (K, err, bound)
         assert err > prev, (K, err, prev)
         prev = err
+
+
+# --- partial last group (K does not divide T, reading D6') -----
+@pytest.mark.parametrize("reset", RESETS)
+@pytest.mark.parametrize("mode", ["tac", "tactp"])
+def test_partial_last_group_is_a_short_group(oracle_mod, mode, reset):
+    """With partial=True and T = (G-1) K + K', the layer equals the first (G-1) K frames
+    with group size K followed, through v_init = v_final, by the last K' frames as one
+    group of size K' (A, decay beta^K' and step count all of the short group)."""
+    rng = np.random.default_rng(50)
+    S = _rand_spikes(rng, (10, 2, 2, 6, 6), 0.3)
+    W = _rand_w(rng, 3, 2, gain=2.5)
+    b = (rng.random(3) * 0.2 - 0.1).astype(np.float32)
+    kw = dict(mode=mode, beta=0.8, v_th=1.0, v_reset=0.1, reset=reset, pad=1)
+    full = oracle_mod.forward(S, W, b, K=4, partial=True, **kw)
+    a = oracle_mod.forward(S[:8], W, b, K=4, **kw)
+    c = oracle_mod.forward(S[8:], W, b, K=2, v_init=a["v_final"], **kw)
+    assert np.array_equal(np.concatenate([a["out"], c["out"]]), full["out"])
+    assert np.array_equal(c["v_final"], full["v_final"])
+    assert full["out"].shape[0] == (3 if mode == "tac" else 10)
+
+
+def test_partial_groups_paper_T25(oracle_mod):
+    """The paper's T = 25 with K = 4 / 8 / 16: a TAC layer emits
+    ceil(25/K) = 7 / 4 / 2 steps (one per conv call) instead of 25."""
+    rng = np.random.default_rng(51)
+    S = _rand_spikes(rng, (25, 1, 1, 5, 5), 0.2)
+    W = _rand_w(rng, 2, 1)
+    steps = [oracle_mod.forward(S, W, K=K, mode="tac", partial=True, pad=1)["out"].shape[0]
+             for K in (4, 8, 16)]
+    assert steps == [7, 4, 2]
+    with pytest.raises(ValueError):
+        oracle_mod.forward(S, W, K=4, mode="tac", pad=1)   # K must divide T without partial
