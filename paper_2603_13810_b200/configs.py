@@ -94,20 +94,23 @@ CONFIGS = {
 
 
 def layer_plan(cfg: Config, mode: str | None = None, K: int | None = None, B: int | None = None,
-               engine: str = "auto"):
-    """LayerSpecs of the stack (imports the binding lazily)."""
+               engine: str = "auto", T: int | None = None):
+    """LayerSpecs of the stack (imports the binding lazily).  With T not a multiple of
+    K (the paper's T = 25) the layers use a partial last group (reading D6') and a TAC
+    layer passes ceil(T_l / K_l) steps on."""
     from .tacsnn import LayerSpec
     mode = mode or cfg.mode
     K = cfg.K if K is None else K
     B = cfg.B if B is None else B
-    specs, t = [], cfg.T
+    specs, t = [], cfg.T if T is None else T
     for L in cfg.layers:
         Kl = 1 if mode == "dense" else min(K, t)
         specs.append(LayerSpec(T=t, B=B, C_in=L.C_in, H=L.H, W=L.W, C_out=L.C_out, R=3, S=3,
                                stride=1, pad=L.pad, K=Kl, mode=mode, beta=cfg.beta, v_th=1.0,
-                               v_reset=0.0, reset="subtract", out_pool=L.pool, engine=engine))
+                               v_reset=0.0, reset="subtract", out_pool=L.pool, engine=engine,
+                               partial=(t % Kl != 0)))
         if mode == "tac":
-            t //= Kl
+            t = -(-t // Kl)
     return specs
 
 
@@ -130,6 +133,6 @@ def make_inputs(cfg: Config, B: int | None = None, b0: int = 0, seed: int | None
     return synth.rate_coded(cfg.inputs, seed, T, B, cfg.H, cfg.W, b0=b0, rho=0.1, device=device)
 
 
-def conv_calls(cfg: Config, mode: str | None = None, K: int | None = None) -> int:
-    """Logical conv calls of the stack per sample: sum_l T_l / K_l."""
-    return sum(s.T // (1 if s.mode == "dense" else s.K) for s in layer_plan(cfg, mode, K, B=1))
+def conv_calls(cfg: Config, mode: str | None = None, K: int | None = None, T: int | None = None) -> int:
+    """Logical conv calls of the stack per sample: sum_l ceil(T_l / K_l)."""
+    return sum(-(-s.T // (1 if s.mode == "dense" else s.K)) for s in layer_plan(cfg, mode, K, B=1, T=T))

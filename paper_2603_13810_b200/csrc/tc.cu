@@ -272,8 +272,8 @@ const char *shape_reason(const tac_conv_lif_desc *d) {
     return "needs C_out in {8,16} or a multiple of 32 up to 128";
   const int K = d->mode == TAC_MODE_DENSE ? 1 : d->K;
   if (d->mode == TAC_MODE_TACTP && K > kMaxSteps) return "TAC-TP needs K <= 8";
-  // the producers and LIF epilogues are instantiated for these group sizes
-  if (!(K == 1 || K == 2 || K == 4 || K == 8)) return "needs K in {1, 2, 4, 8}";
+  // the producers are instantiated for these group sizes (3: short last groups, e.g. T = 7, K = 4)
+  if (!(K == 1 || K == 2 || K == 3 || K == 4 || K == 8)) return "needs K in {1, 2, 3, 4, 8}";
   return nullptr;
 }
 
@@ -1718,6 +1718,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
         switch (p.K) {
           case 1: producer_role_tma<PATH, 1>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
           case 2: producer_role_tma<PATH, 2>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
+          case 3: producer_role_tma<PATH, 3>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
           case 4: producer_role_tma<PATH, 4>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
           default: producer_role_tma<PATH, 8>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
         }
@@ -1725,6 +1726,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
         switch (p.K) {
           case 1: producer_role<PATH, 1>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
           case 2: producer_role<PATH, 2>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
+          case 3: producer_role<PATH, 3>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
           case 4: producer_role<PATH, 4>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
           default: producer_role<PATH, 8>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
         }

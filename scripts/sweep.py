@@ -29,6 +29,8 @@ RUNS = [
     ("C4", "dense", 1), ("C4", "tactp", 2), ("C4", "tac", 2),
     ("C5", "dense", 1), ("C5", "tactp", 2), ("C5", "tactp", 4), ("C5", "tactp", 8), ("C5", "tac", 4),
 ]
+# the paper's MNIST setting T = 25 with K = 4 / 8 / 16: partial last groups
+RUNS_T25 = [("C2", "dense", 1), ("C2", "tac", 4), ("C2", "tac", 8), ("C2", "tac", 16)]
 
 
 def time_forward(net, x, iters):
@@ -125,6 +127,25 @@ def main():
             del net, x
             torch.cuda.empty_cache()
         if not a.only:
+            t25_dense = None
+            for name, mode, K in RUNS_T25:
+                cfg = configs.CONFIGS[name]
+                specs = configs.layer_plan(cfg, mode=mode, K=K, T=25)
+                net = network.Network(specs, configs.layer_weights(cfg))
+                x = tacsnn.pack(configs.make_inputs(cfg, T=25, device="cuda"))
+                ms, layer_ms = time_forward(net, x, a.iters)
+                g_ms = time_graph(net, x, max(a.iters, 20))
+                if mode == "dense":
+                    t25_dense = g_ms
+                line = {"config": name + "@T25", "mode": mode, "K": K, "B": cfg.B, "T": 25,
+                        "ms_per_forward": ms, "graph_ms_per_forward": g_ms,
+                        "frames_per_s": cfg.B * 25 / (ms / 1e3),
+                        "graph_speedup_vs_dense": t25_dense / g_ms,
+                        "conv_calls_per_sample": configs.conv_calls(cfg, mode, K, T=25),
+                        "layer_ms": layer_ms, "engines": net.engines(),
+                        "partial": [s.partial for s in specs]}
+                print(json.dumps(line), flush=True)
+                out.write(json.dumps(line) + "\n")
             density_check(a.iters, out)
 
 

@@ -212,17 +212,31 @@ def test_partial_last_group_parity(T, O, tk, layer, mode, engine):
 
 
 @pytest.mark.parametrize("mode", ["tac", "tactp"])
+@pytest.mark.parametrize("layer", PARTIAL_LAYERS, ids=[c[0] for c in PARTIAL_LAYERS])
+def test_group_size_3_on_tcgen05(T, O, layer, mode):
+    """K = 3 (short last groups such as T = 7, K = 4) runs on the tcgen05 engine."""
+    name, (B, Cin, H, W, Cout, pad, pool), beta, gain = layer
+    spec = T.LayerSpec(T=6, B=B, C_in=Cin, H=H, W=W, C_out=Cout, pad=pad, K=3, mode=mode,
+                       beta=beta, out_pool=pool, engine="tcgen05")
+    assert spec.engine_used() == "tcgen05"
+    S = _spikes(zlib.crc32(name.encode()) % 971, (6, B, Cin, H, W), 0.15)
+    w, b = _w(13, Cout, Cin, gain)
+    _, _, st = P.check_layer(T, O, spec, S, w, b, label=f"K3/{name}/{mode}")
+    assert 0.0 < st["rate"] < 0.95, st
+
+
+@pytest.mark.parametrize("mode", ["tac", "tactp"])
 def test_odd_group_size_runs_on_simt(T, O, mode):
-    """K = 3 (T = 6) is outside the tcgen05 envelope (K in {1,2,4,8}): AUTO must pick
+    """K = 5 (T = 10) is outside the tcgen05 envelope (K in {1,2,3,4,8}): AUTO must pick
     the SIMT engine, an explicit tcgen05 request must be refused, results exact."""
-    spec = T.LayerSpec(T=6, B=2, C_in=32, H=10, W=12, C_out=32, pad=1, K=3, mode=mode,
+    spec = T.LayerSpec(T=10, B=2, C_in=32, H=10, W=12, C_out=32, pad=1, K=5, mode=mode,
                        beta=0.5, out_pool=2)
     assert spec.engine_used() == "simt"
     with pytest.raises(RuntimeError):
         spec.replace(engine="tcgen05").engine_used()
-    S = _spikes(21, (6, 2, 32, 10, 12), 0.2)
+    S = _spikes(21, (10, 2, 32, 10, 12), 0.2)
     w, b = _w(9, 32, 32, 1.5)
-    P.check_layer(T, O, spec, S, w, b, label=f"K3/{mode}")
+    P.check_layer(T, O, spec, S, w, b, label=f"K5/{mode}")
 
 
 @pytest.mark.parametrize("engine", ENGINES)
