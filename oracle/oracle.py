@@ -140,8 +140,10 @@ def forward(S, Wt, bias=None, *, K=1, mode="tac", beta=0.9, v_th=1.0, v_reset=0.
 
 
 def or_pool2(x):
-    """2x2 OR-pool of binary maps (P:235 MaxPool(2) on {0,1}); x [..., C, H, W]."""
-    x = np.ascontiguousarray(x, dtype=np.uint8)
+    """2x2 OR-pool of binary maps (P:235 MaxPool(2) on {0,1}); x [..., C, H, W].
+    Odd extents: floor mode (the last row / column is dropped, as MaxPool2d)."""
+    x = np.asarray(x, dtype=np.uint8)
+    x = np.ascontiguousarray(x[..., : x.shape[-2] // 2 * 2, : x.shape[-1] // 2 * 2])
     *lead, C, H, W = x.shape
     N = int(np.prod(lead)) if lead else 1
     y = np.empty((*lead, C, H // 2, W // 2), np.uint8)

@@ -22,6 +22,7 @@ from . import synth
 # (scripts/calibrate_gains.py); frozen here.
 GAINS = {
     "mnist": [0.78, 0.46],
+    "mnist_fc": [2.0, 2.0],   # FC(1600->128), FC(128->10) of the whole network (set below)
     "dvs": [7.1, 1.08, 1.01, 1.01, 0.89],
 }
 
@@ -136,3 +137,37 @@ def make_inputs(cfg: Config, B: int | None = None, b0: int = 0, seed: int | None
 def conv_calls(cfg: Config, mode: str | None = None, K: int | None = None, T: int | None = None) -> int:
     """Logical conv calls of the stack per sample: sum_l ceil(T_l / K_l)."""
     return sum(-(-s.T // (1 if s.mode == "dense" else s.K)) for s in layer_plan(cfg, mode, K, B=1, T=T))
+
+
+# --- whole MNIST/FMNIST network (SURVEY.md 8(f) #2): conv stack + FC head ------
+# Conv(1->32)->LIF->Pool(2)->Conv(32->64)->LIF->Pool(2) [11x11 -> 5x5, floor]
+# ->FC(1600->128)->LIF->FC(128->10)->LIF (PAPER.md:234); the FC layers are 1x1
+# "convolutions" of a 1x1 image (C_in = 1600 / 128), TAC-aggregated like the convs
+# (they are linear too); the readout is the final layer's spike counts (P:589).
+def network_plan(cfg: Config, mode: str | None = None, K: int | None = None, B: int | None = None,
+                 engine: str = "auto", T: int | None = None):
+    from .tacsnn import LayerSpec
+    assert cfg.inputs in ("mnist", "fmnist"), "whole-network plan: MNIST-shaped configs"
+    convs = layer_plan(cfg, mode=mode, K=K, B=B, engine=engine, T=T)
+    convs[1] = convs[1].replace(out_pool=2)            # 11x11 -> 5x5 (floor)
+    mode = mode or cfg.mode
+    K = cfg.K if K is None else K
+    t = convs[1].T if mode != "tac" else -(-convs[1].T // convs[1].K)
+    specs = list(convs)
+    for c_in, c_out in ((64 * 5 * 5, 128), (128, 10)):
+        Kl = 1 if mode == "dense" else min(K, t)
+        specs.append(LayerSpec(T=t, B=convs[0].B, C_in=c_in, H=1, W=1, C_out=c_out, R=1, S=1,
+                               stride=1, pad=0, K=Kl, mode=mode, beta=cfg.beta, v_th=1.0,
+                               v_reset=0.0, reset="subtract", out_pool=1, engine=engine,
+                               partial=(t % Kl != 0)))
+        if mode == "tac":
+            t = -(-t // Kl)
+    return specs
+
+
+def network_weights(cfg: Config, seed: int | None = None):
+    seed = cfg.seeds[0] if seed is None else seed
+    w = layer_weights(cfg, seed)
+    for i, ((c_in, c_out), g) in enumerate(zip(((1600, 128), (128, 10)), GAINS["mnist_fc"])):
+        w.append(synth.weights(seed * 1000 + 10 + i, c_out, c_in, 1, 1, gain=g))
+    return w

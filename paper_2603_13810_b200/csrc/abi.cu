@@ -68,8 +68,8 @@ tac_status check(const tac_conv_lif_desc *d, Geo *g) {
     return fail(TAC_ERR_SHAPE, "output height H'=(H+2pad-R)/stride+1 < 1");
   if (d->W + 2 * d->pad < d->S || Wo < 1)
     return fail(TAC_ERR_SHAPE, "output width W'=(W+2pad-S)/stride+1 < 1");
-  if (d->out_pool == 2 && (Ho % 2 || Wo % 2))
-    return fail(TAC_ERR_SHAPE, "out_pool=2 needs even H'=%d, W'=%d", Ho, Wo);
+  if (d->out_pool == 2 && (Ho < 2 || Wo < 2))
+    return fail(TAC_ERR_SHAPE, "out_pool=2 needs H', W' >= 2 (H'=%d, W'=%d)", Ho, Wo);
   if ((long long)d->W * d->C_in > (1LL << 30) || (long long)Wo * d->C_out > (1LL << 30))
     return fail(TAC_ERR_SHAPE, "row too wide");
   if (d->in_stride_t < 0 || d->in_stride_b < 0 || d->out_stride_t < 0 || d->out_stride_b < 0)

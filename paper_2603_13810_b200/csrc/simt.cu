@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(128) simt_conv_lif_kernel(const LayerParams p)
         V[c] = v;
       }
       if (p.reset == RESET_DELAYED) sprev = bits;
-      if (bits) {
+      if (bits && yo < p.Hq && xo < p.Wq) {  // floor pooling drops an odd last row / column
         const int t_out = (p.mode == MODE_TAC) ? g : g * p.K + j;
         uint32_t *row = p.out + (long long)t_out * p.out_st + (long long)b * p.out_sb +
                         (long long)yo * p.wpr_out;

@@ -109,6 +109,7 @@ struct TcParams {
   int use_tma, raw_bw, nraw;
   uint32_t off_raw, raw_stage_bytes, raw_box_bytes;
   int B, H, W, Cin, Cout, Cout_pad, pad, Ho, Wo, pool;
+  int Hq, Wq;  // stored (pooled) extent: floor(H'/2), floor(W'/2) when pool == 2
   int K, G, nsteps, mode, reset;
   int tiles_x, tiles_y, num_tiles, num_pairs, nstages;
   int nkc, ntaps, m_shift;
@@ -1159,7 +1160,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
     const bool valid = tok && y < p.Ho && x < p.Wo;
     const long long vbase = (((long long)b * p.Ho + y) * p.Wo + x) * Cout + co_base;
     const int yo = pooled ? (y >> 1) : y, xo = pooled ? (x >> 1) : x;
-    const bool store_lane = valid && active_half && (!pooled || (lane & 9) == 0);
+    const bool store_lane = valid && active_half && (!pooled || (lane & 9) == 0) && yo < p.Hq && xo < p.Wq;
     const uint32_t vmask = (valid && active_half) ? chmask : 0u;
     // this lane's output word (NCH == 32) or the word holding its bit field (NCH < 32)
     const long long obit = (long long)xo * Cout + co_base;
@@ -1370,7 +1371,7 @@ __device__ __forceinline__ void epilogue_generic(const TcParams &p, uint8_t *sme
     // (lane & 9) == 0 store, after the in-warp OR)
     const int yo = pooled ? (y >> 1) : y, xo = pooled ? (x >> 1) : x;
     uint32_t *orow = p.out + (long long)b * p.out_sb + (long long)yo * p.wpr_out;
-    const bool store_lane = valid && active_half && (!pooled || (lane & 9) == 0);
+    const bool store_lane = valid && active_half && (!pooled || (lane & 9) == 0) && yo < p.Hq && xo < p.Wq;
     long long obit = (long long)xo * Cout + co_base;  // NCH < 32: bit offset of the field
     float2 V[NCH / 2];
     uint32_t prev[NWT];
@@ -1981,7 +1982,7 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   p.raw_stage_bytes = g.raw_stage_bytes;
   p.raw_box_bytes = g.raw_box_bytes;
   p.B = lp.B; p.H = lp.H; p.W = lp.W; p.Cin = lp.Cin; p.Cout = lp.Cout; p.Cout_pad = g.cout_pad;
-  p.pad = lp.pad; p.Ho = lp.Ho; p.Wo = lp.Wo; p.pool = lp.pool;
+  p.pad = lp.pad; p.Ho = lp.Ho; p.Wo = lp.Wo; p.pool = lp.pool; p.Hq = lp.Hq; p.Wq = lp.Wq;
   p.K = lp.K; p.G = lp.G; p.nsteps = lp.nsteps; p.mode = lp.mode; p.reset = lp.reset;
   p.tiles_x = (lp.Wo + kTileW - 1) / kTileW;
   p.tiles_y = (lp.Ho + kTileH - 1) / kTileH;

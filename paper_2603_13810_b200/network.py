@@ -13,6 +13,16 @@ from . import tacsnn
 from .tacsnn import LayerSpec
 
 
+def flatten_for(spec: LayerSpec, x: torch.Tensor) -> torch.Tensor:
+    """A fully connected layer is a 1x1 conv of a 1x1 image: its packed input row is the
+    previous layer's whole (H, W, C) map, i.e. the packed rows concatenated (a view when
+    every row is a whole number of words)."""
+    if spec.H == 1 and spec.W == 1 and x.shape[2] != 1:
+        assert spec.C_in == x.shape[2] * x.shape[3] * 32, "rows must be whole words"
+        x = x.reshape(x.shape[0], x.shape[1], 1, x.shape[2] * x.shape[3])
+    return x
+
+
 class Network:
     def __init__(self, specs: list[LayerSpec], weights, device="cuda"):
         assert len(specs) == len(weights)
@@ -36,6 +46,7 @@ class Network:
         for i, (spec, prep) in enumerate(zip(self.specs, self.prepared)):
             s = spec if spec.B == B else spec.replace(B=B)
             wc = want_counts is True or (want_counts == "last" and i == n - 1)
+            x = flatten_for(s, x)
             x, vf, cnt = tacsnn.conv_lif(s, prep, x, want_v_final=want_v_final, want_counts=wc)
             counts.append(cnt)
             vfs.append(vf)
@@ -70,6 +81,7 @@ class Network:
         for i, (spec, prep) in enumerate(zip(self.specs, self.prepared)):
             s = spec if spec.B == B else spec.replace(B=B)
             wc = want_counts is True or (want_counts == "last" and i == nl - 1)
+            x = flatten_for(s, x)
             x, _, _ = tacsnn.conv_lif(s, prep, x, want_counts=wc)
             n += tacsnn.last_launch_count()
         self._launches = n

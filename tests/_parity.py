@@ -73,6 +73,12 @@ def check_stack(T, O, specs, weights, S_u8, label=""):
     S = S_u8
     stats = []
     for i, (spec, (w, b)) in enumerate(zip(specs, weights)):
+        if spec.H == 1 and spec.W == 1 and S.shape[-1] != 1:
+            # fully connected layer: the (h, w, c)-ordered flattening of the previous map,
+            # which is the device's packed row layout (x*C + c, rows concatenated)
+            Tn, Bn = S.shape[:2]
+            S = np.ascontiguousarray(S.transpose(0, 1, 3, 4, 2).reshape(Tn, Bn, -1, 1, 1))
+            x_dev = x_dev.reshape(x_dev.shape[0], x_dev.shape[1], 1, -1)
         ref_out, dev_out, st = check_layer(T, O, spec, S, w, b, x_packed=x_dev,
                                            label=f"{label} layer {i}")
         stats.append(st)

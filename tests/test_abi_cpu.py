@@ -54,6 +54,7 @@ def test_validation_statuses(T):
     st, detail = _status(T, base.replace(K=3))
     assert st == 3 and "K=3" in detail                      # K does not divide T
     assert _status(T, base.replace(K=0))[0] == 3
+    assert _status(T, base.replace(K=3, partial=True))[0] == 0      # opt-in short last group
     assert _status(T, base.replace(mode="dense", K=3))[0] == 0   # K ignored for dense
     assert _status(T, base.replace(beta=1.0))[0] == 4
     assert _status(T, base.replace(beta=0.0))[0] == 4
@@ -63,7 +64,9 @@ def test_validation_statuses(T):
     assert _status(T, base.replace(H=0))[0] == 2
     assert _status(T, base.replace(H=1, pad=0))[0] == 2         # H' < 1
     assert _status(T, base.replace(out_pool=3))[0] == 4
-    assert _status(T, base.replace(W=31, out_pool=2))[0] == 2   # odd pooled extent
+    assert _status(T, base.replace(W=31, out_pool=2))[0] == 0   # odd extent: floor pooling
+    assert base.replace(W=31, out_pool=2).out_shape()[2] == 15
+    assert _status(T, base.replace(W=3, pad=0, out_pool=2))[0] == 2   # W' = 1: nothing to pool
     assert _status(T, base.replace(T=64, K=64))[0] == 7         # K > 32
     d = base.desc()
     assert T.lib().tac_desc_check(None) == 1

@@ -349,6 +349,19 @@ def test_config_stack_parity(T, O, cfg_name, B, mode):
     assert stats[0]["rate"] > 0.0   # deep layers may legitimately fall silent (dense DVS)
 
 
+@pytest.mark.parametrize("cfg_name,B,mode,K", [("C2", 6, "tac", 4), ("C2", 4, "dense", 1),
+                                               ("C3", 4, "tac", 8), ("C2", 4, "tactp", 2)])
+def test_whole_mnist_network_parity(T, O, cfg_name, B, mode, K):
+    """conv stack + floor-pooled 5x5 map + FC(1600->128) + FC(128->10),
+    layer by layer against the oracle (the FC layers run as 1x1 convs of a 1x1 image)."""
+    from paper_2603_13810_b200 import configs
+    cfg = configs.CONFIGS[cfg_name]
+    specs = configs.network_plan(cfg, mode=mode, K=K, B=B)
+    S = configs.make_inputs(cfg, B=B).numpy()
+    stats = P.check_stack(T, O, specs, configs.network_weights(cfg), S, label=f"{cfg_name}/net/{mode}")
+    assert stats[-1]["rate"] > 0.0
+
+
 @pytest.mark.slow
 def test_c5_full_size_sampled(T, O):
     """C5 at its full batch (2048) in the bench launch configuration; sampled
