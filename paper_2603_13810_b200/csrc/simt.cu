@@ -43,6 +43,68 @@ __global__ void add_u32_kernel(uint32_t *dst, const uint32_t *src, long long n) 
     dst[i] += src[i];
 }
 
+// Fully connected LIF layer (a 1x1 conv of a 1x1 image: H = W = R = S = 1): one block
+// per (sample, 32 output channels); the 8 warps split the C_in inputs (lane = output
+// channel, weights [C_in][C_out] read coalesced, the group aggregate of input i
+// broadcast), partial sums meet in shared memory, warp 0 keeps V in registers for the
+// whole sequence and writes each step's 32 spike bits with one ballot.
+constexpr int FC_WARPS = 8;
+__global__ void __launch_bounds__(32 * FC_WARPS) fc_lif_kernel(const LayerParams p) {
+  __shared__ float part[FC_WARPS][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x, co = blockIdx.y * 32 + lane;
+  const bool cok = co < p.Cout;
+  float V = 0.f;
+  int cnt = 0;
+  bool sprev = false;  // pending delayed reset (reading R4)
+  if (warp == 0 && cok) {
+    V = p.v_init ? p.v_init[(long long)b * p.Cout + co] : 0.f;
+    sprev = p.reset == RESET_DELAYED && V >= p.v_th;
+  }
+  const long long rowb = (long long)b * p.in_sb;
+  for (int g = 0; g < p.G; ++g) {
+    float y = 0.f;
+    for (int i = warp; i < p.Cin; i += FC_WARPS) {
+      float a = 0.f;  // A_g of input i
+      if (p.xin) {
+        for (int j = 0; j < p.K; ++j) a = fmaf(p.coef[j], __ldg(p.xin + (long long)(g * p.K + j) * p.in_st + rowb + i), a);
+      } else {
+        for (int j = 0; j < p.K; ++j)
+          if ((__ldg(p.in + (long long)(g * p.K + j) * p.in_st + rowb + (i >> 5)) >> (i & 31)) & 1u) a += p.coef[j];
+      }
+      if (a != 0.f && cok) y = fmaf(__ldg(p.w + (long long)i * p.Cout + co), a, y);
+    }
+    part[warp][lane] = y;
+    __syncthreads();
+    if (warp == 0) {
+      float Y = cok ? __ldg(p.bias + co) : 0.f;
+#pragma unroll
+      for (int w = 0; w < FC_WARPS; ++w) Y += part[w][lane];
+      for (int j = 0; j < p.nsteps; ++j) {
+        float v = fmaf(p.decay, V, Y);
+        if (p.reset == RESET_DELAYED && sprev) v -= p.v_th;
+        const bool s = cok && v >= p.v_th;
+        if (s) {
+          if (p.reset == RESET_SUBTRACT) v -= p.v_th;
+          else if (p.reset == RESET_HARD) v = p.v_reset;
+          ++cnt;
+        }
+        sprev = s;
+        V = v;
+        const uint32_t bits = __ballot_sync(0xFFFFFFFFu, s);
+        const int t_out = (p.mode == MODE_TAC) ? g : g * p.K + j;
+        if (lane == 0)
+          p.out[(long long)t_out * p.out_st + (long long)b * p.out_sb + (blockIdx.y * 32 >> 5)] = bits;
+      }
+    }
+    __syncthreads();
+  }
+  if (warp == 0 && cok) {
+    if (p.v_final) p.v_final[(long long)b * p.Cout + co] = V;
+    if (p.counts && cnt) atomicAdd(p.counts + (long long)b * p.Cout + co, (uint32_t)cnt);
+  }
+}
+
 constexpr int CH = 32;  // output channels per thread
 
 __global__ void __launch_bounds__(128) simt_conv_lif_kernel(const LayerParams p) {
@@ -210,6 +272,12 @@ int launch_add_u32(uint32_t *dst, const uint32_t *src, long long n, void *stream
 }
 
 int launch_simt_conv_lif(const LayerParams &p, void *stream, int *launches) {
+  if (p.H == 1 && p.W == 1 && p.R == 1 && p.S == 1 && p.pad == 0 && p.pool == 1) {
+    fc_lif_kernel<<<dim3((unsigned)p.B, (unsigned)((p.Cout + 31) / 32)), 32 * FC_WARPS, 0,
+                    (cudaStream_t)stream>>>(p);
+    ++*launches;
+    return (int)cudaGetLastError();
+  }
   const long long npix = (long long)p.B * p.Ho * p.Wo;
   dim3 grid((unsigned)((npix + 127) / 128), (unsigned)((p.Cout + CH - 1) / CH));
   simt_conv_lif_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(p);

@@ -146,6 +146,23 @@ def main():
                         "partial": [s.partial for s in specs]}
                 print(json.dumps(line), flush=True)
                 out.write(json.dumps(line) + "\n")
+            # the whole MNIST / FMNIST network (conv stack + FC head)
+            for name, runs in (("C2", (("dense", 1), ("tac", 4), ("tac", 8))), ("C3", (("dense", 1), ("tac", 8)))):
+                cfg = configs.CONFIGS[name]
+                d_ms = None
+                for mode, K in runs:
+                    specs = configs.network_plan(cfg, mode=mode, K=K)
+                    net = network.Network(specs, configs.network_weights(cfg))
+                    x = tacsnn.pack(configs.make_inputs(cfg, device="cuda"))
+                    g_ms = time_graph(net, x, max(a.iters, 20))
+                    d_ms = g_ms if mode == "dense" else d_ms
+                    line = {"config": name + "+FC", "mode": mode, "K": K, "B": cfg.B, "T": cfg.T,
+                            "ms_per_forward": g_ms, "graph_ms_per_forward": g_ms,
+                            "frames_per_s": cfg.B * cfg.T / (g_ms / 1e3), "speedup_vs_dense": d_ms / g_ms,
+                            "conv_calls_per_sample": sum(-(-s.T // s.K) for s in specs),
+                            "engines": net.engines()}
+                    print(json.dumps(line), flush=True)
+                    out.write(json.dumps(line) + "\n")
             density_check(a.iters, out)
 
 

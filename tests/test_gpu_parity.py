@@ -349,6 +349,19 @@ def test_config_stack_parity(T, O, cfg_name, B, mode):
     assert stats[0]["rate"] > 0.0   # deep layers may legitimately fall silent (dense DVS)
 
 
+@pytest.mark.parametrize("reset", ["subtract", "delayed", "hard"])
+@pytest.mark.parametrize("mode,K", [("dense", 1), ("tac", 4), ("tactp", 2)])
+def test_fc_layer_parity(T, O, mode, K, reset):
+    """Fully connected LIF layer (1x1 conv of a 1x1 image; SIMT fc kernel), C_in not a
+    multiple of 32 and C_out spanning two spike words."""
+    spec = T.LayerSpec(T=8, B=5, C_in=200, H=1, W=1, C_out=40, R=1, S=1, pad=0, K=K, mode=mode,
+                       beta=0.9, v_reset=-0.2, reset=reset)
+    S = _spikes(31, (8, 5, 200, 1, 1), 0.2)
+    w, b = _w(14, 40, 200, 3.0, r=1, s=1)
+    _, _, st = P.check_layer(T, O, spec, S, w, b, label=f"fc/{mode}/{reset}")
+    assert 0.0 < st["rate"] < 0.95, st
+
+
 @pytest.mark.parametrize("cfg_name,B,mode,K", [("C2", 6, "tac", 4), ("C2", 4, "dense", 1),
                                                ("C3", 4, "tac", 8), ("C2", 4, "tactp", 2)])
 def test_whole_mnist_network_parity(T, O, cfg_name, B, mode, K):
