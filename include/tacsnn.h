@@ -31,7 +31,8 @@
  *   (the paper's layout, Alg. 1 "Require").
  * Output spikes use the same layout with C = C_out, (H, W) = the layer output
  *   extent -- after the optional fused 2x2 OR-pool (= MaxPool(2) of binary
- *   spikes) when out_pool = 2.  T_out = T/K for TAC, else T.
+ *   spikes) when out_pool = 2; odd H', W' pool in floor mode
+ *   (H_o = floor(H'/2): the last row / column is dropped, as MaxPool2d).  T_out = T/K for TAC, else T.
  * v_init / v_final: fp32 [B][H'][W'][C_out] (channels last, PRE-pool extent
  *   H' = (H+2 pad-R)/stride+1), contiguous.  v_final is V after the last step
  *   (post-reset for SUBTRACT / HARD; R5).  NULL v_init means V=0
@@ -94,7 +95,7 @@ typedef enum {
 typedef enum {
   TAC_OK = 0,
   TAC_ERR_NULL = 1,             /* a required pointer is NULL                   */
-  TAC_ERR_SHAPE = 2,            /* non-positive extent, H' < 1, odd pooled extent */
+  TAC_ERR_SHAPE = 2,            /* non-positive extent, H' < 1, pooled extent < 1  */
   TAC_ERR_K_NOT_DIVIDING_T = 3, /* K < 1 or T % K != 0 */
   TAC_ERR_PARAM = 4,            /* beta not in (0,1), v_th <= 0, bad enum        */
   TAC_ERR_NONFINITE = 5,        /* non-finite weight, bias, beta, v_th, v_reset  */
@@ -114,7 +115,7 @@ typedef struct tac_conv_lif_desc {
   float v_th;                       /* threshold > 0                                */
   float v_reset;                    /* HARD reset value                             */
   int32_t reset;                    /* tac_reset                                    */
-  int32_t out_pool;                 /* 1 = none, 2 = fused 2x2 OR-pool (even H', W') */
+  int32_t out_pool;                 /* 1 = none, 2 = fused 2x2 OR-pool (floor mode)  */
   int32_t engine;                   /* tac_engine                                   */
   int64_t in_stride_t, in_stride_b; /* u32 words (REAL input: floats); 0 = default  */
   int64_t out_stride_t, out_stride_b;
