@@ -32,7 +32,8 @@
  * Output spikes use the same layout with C = C_out, (H, W) = the layer output
  *   extent -- after the optional fused 2x2 OR-pool (= MaxPool(2) of binary
  *   spikes) when out_pool = 2; odd H', W' pool in floor mode
- *   (H_o = floor(H'/2): the last row / column is dropped, as MaxPool2d).  T_out = T/K for TAC, else T.
+ *   (H_o = floor(H'/2): the last row / column is dropped, as MaxPool2d).  T_out = T/K for TAC
+ *   (ceil(T/K) with partial_last_group), else T.
  * v_init / v_final: fp32 [B][H'][W'][C_out] (channels last, PRE-pool extent
  *   H' = (H+2 pad-R)/stride+1), contiguous.  v_final is V after the last step
  *   (post-reset for SUBTRACT / HARD; R5).  NULL v_init means V=0

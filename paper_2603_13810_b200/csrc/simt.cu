@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(32 * FC_WARPS) fc_lif_kernel(const LayerParams
   const long long rowb = (long long)b * p.in_sb;
   for (int g = 0; g < p.G; ++g) {
     float y = 0.f;
+#pragma unroll 4
     for (int i = warp; i < p.Cin; i += FC_WARPS) {
       float a = 0.f;  // A_g of input i
       if (p.xin) {
