@@ -375,6 +375,26 @@ def test_whole_mnist_network_parity(T, O, cfg_name, B, mode, K):
     assert stats[-1]["rate"] > 0.0
 
 
+def test_graph_replay_equals_eager(T):
+    """Network.capture: a CUDA-graph replay of the stack gives bitwise the eager outputs
+    (and refreshes them when the static input changes)."""
+    from paper_2603_13810_b200 import configs, network
+    cfg = configs.CONFIGS["C2"]
+    net = network.Network(configs.network_plan(cfg, mode="tac", K=4, B=8), configs.network_weights(cfg))
+    x = T.pack(configs.make_inputs(cfg, B=8, device="cuda"))
+    y_eager, c_eager, _, _ = net.forward(x)
+    graph, (y_g, c_g, _, _) = net.capture(x)
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y_g, y_eager) and torch.equal(c_g[-1], c_eager[-1])
+    x.copy_(T.pack(configs.make_inputs(cfg, B=8, seed=1, device="cuda")))
+    y2, c2, _, _ = net.forward(x)
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y_g, y2) and torch.equal(c_g[-1], c2[-1])
+    assert not torch.equal(y2, y_eager) or not torch.equal(c2[-1], c_eager[-1])
+
+
 @pytest.mark.slow
 def test_c5_full_size_sampled(T, O):
     """C5 at its full batch (2048) in the bench launch configuration; sampled
