@@ -73,6 +73,9 @@ constexpr int kProdWarps = 3;
 #ifndef TACSNN_BDESC_OPAQUE
 #define TACSNN_BDESC_OPAQUE 1
 #endif
+#ifndef TACSNN_UT_PREFETCH
+#define TACSNN_UT_PREFETCH 1
+#endif
 #ifndef TACSNN_UT_MIN_NS
 #define TACSNN_UT_MIN_NS 4  // U in TMEM for the fp16 paths from this many LIF steps per group
 #endif
@@ -1199,7 +1202,31 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
 #pragma unroll
       for (int j = 0; j < NS; ++j) nsp[j] = 0u;
       const uint32_t tcol = tmem_base + lane_addr + acc * p.n_total + (uint32_t)co_base;
-      if (UT) {
+      if (UT && TACSNN_UT_PREFETCH) {
+        // chunk by chunk (Y and U in, LIF, U out), the next chunk's loads in flight
+        uint32_t dy[2][8], du[2][8];
+        ptx::tmem_ld8(tcol + (NCHUNK - 1) * 8, dy[0]);
+        ptx::tmem_ld8(ucol + (NCHUNK - 1) * 8, du[0]);
+        ptx::tmem_wait_ld_dep(dy[0], du[0]);
+#pragma unroll
+        for (int i = 0; i < NCHUNK; ++i) {
+          const int ch = NCHUNK - 1 - i, cur = i & 1, nxt = cur ^ 1;
+          if (ch > 0) {
+            ptx::tmem_ld8(tcol + (ch - 1) * 8, dy[nxt]);
+            ptx::tmem_ld8(ucol + (ch - 1) * 8, du[nxt]);
+          }
+#pragma unroll
+          for (int q = 3; q >= 0; --q) {
+            float2 u = make_float2(__uint_as_float(du[cur][2 * q]), __uint_as_float(du[cur][2 * q + 1]));
+            lif_pair_sr<NS>(u, make_float2(__uint_as_float(dy[cur][2 * q]), __uint_as_float(dy[cur][2 * q + 1])),
+                            dec2, nth2, nsp);
+            du[cur][2 * q] = __float_as_uint(u.x);
+            du[cur][2 * q + 1] = __float_as_uint(u.y);
+          }
+          ptx::tmem_st8(ucol + ch * 8, du[cur]);
+          if (ch > 0) ptx::tmem_wait_ld_dep(dy[nxt], du[nxt]);
+        }
+      } else if (UT) {
         // one chunk at a time: Y and U in, LIF, U out
 #pragma unroll
         for (int i = 0; i < NCHUNK; ++i) {
