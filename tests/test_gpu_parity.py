@@ -167,6 +167,30 @@ def test_real_input_parity(T, O, case, mode, K, beta, engine):
         assert np.array_equal(O.unpack_spikes(P.to_u32(dev_p), Cout, wc // 2), O.or_pool2(r["out"]))
 
 
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("mode", ["tac", "tactp"])
+def test_real_input_partial_last_group(T, O, mode, engine):
+    """Continuous input with K not dividing T (T = 10, K = 4: groups 4, 4, 2)."""
+    from paper_2603_13810_b200 import synth
+    Tn, B, Cin, H, W, Cout = 10, 2, 2, 32, 32, 128
+    spec = T.LayerSpec(T=Tn, B=B, C_in=Cin, H=H, W=W, C_out=Cout, pad=1, K=4, mode=mode, beta=0.5,
+                       out_pool=1, input="real", partial=True)
+    spec = _engine_or_skip(spec, engine)
+    X = synth.dvs_log_counts(5, Tn, B, H, W)                                   # [T,B,C,H,W]
+    w, b = _w(15, Cout, Cin, 4.0)
+    prep = T.prepare_weights(spec, w, b)
+    out, vf, cnt = T.conv_lif(spec, prep, X.permute(0, 1, 3, 4, 2).contiguous().cuda(),
+                              want_v_final=True)
+    torch.cuda.synchronize()
+    D = O.unpack_spikes(P.to_u32(out), Cout, W)
+    r = O.forward(X.numpy().astype(np.float64), w.numpy(), b.numpy(), K=4, mode=mode, beta=0.5,
+                  pad=1, replay=D, band=P.BAND, partial=True)
+    assert r["mismatch"] == 0 and 0.0 < D.mean() < 0.9
+    err = np.abs(vf.cpu().numpy().transpose(0, 3, 1, 2) - r["v_final"])
+    assert np.all(err <= P.VTOL * np.maximum(np.abs(r["v_final"]), 1.0))
+    assert np.array_equal(cnt.cpu().numpy().astype(np.int64), r["counts"])
+
+
 def test_real_input_rejects_spike_call(T):
     """A REAL-input descriptor through tac_conv_lif_forward is refused before launch."""
     import ctypes
