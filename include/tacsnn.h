@@ -71,7 +71,9 @@
 extern "C" {
 #endif
 
-#define TACSNN_ABI_VERSION 2 /* 2: input_kind + tac_conv_lif_forward_real */
+#define TACSNN_ABI_VERSION 3 /* 2: input_kind + tac_conv_lif_forward_real;
+                                3: tac_plan (prepared image + descriptor fingerprint),
+                                   desc.agg_weights (learnable aggregation weights) */
 
 typedef enum { TAC_MODE_DENSE = 0, TAC_MODE_TAC = 1, TAC_MODE_TACTP = 2 } tac_mode;
 
@@ -131,7 +133,37 @@ typedef struct tac_conv_lif_desc {
                                        chained through the membrane state; needs a
                                        workspace (tac_workspace_bytes); a short group
                                        outside the tcgen05 envelope runs on SIMT.  */
+  const float *agg_weights;         /* HOST fp32 [K] or NULL.  Learnable aggregation
+                                       weights alpha_j replacing beta^{K-1-j} in
+                                       A_k = sum_j alpha_j S_{kK+j} (the paper's
+                                       "learnable aggregation weights", PAPER.md:427;
+                                       DESIGN.md reading R11).  Read during
+                                       tac_prepare_weights and every call that takes
+                                       the desc; must be finite.  The membrane decay
+                                       (beta^K for TAC, beta per TAC-TP step) is not
+                                       affected.  A short last group of K' frames uses
+                                       the last K' entries alpha_{K-K'+j} (with the
+                                       default alpha_j = beta^{K-1-j} that is exactly
+                                       beta^{K'-1-j}, reading D6').  NULL = beta^{K-1-j}. */
 } tac_conv_lif_desc;
+
+/* Prepared layer ("plan"): a plain host struct the caller owns (stack, heap, ...),
+ * filled by tac_prepare_weights and passed by pointer to every forward call.  It
+ * names the caller's device image and carries a fingerprint of the descriptor
+ * fields the image depends on (C_in, C_out, R, S, stride, pad, K, mode, beta,
+ * v_th, reset, input_kind, the short-group size, agg_weights), so a forward call
+ * with a descriptor the image was NOT prepared for -- e.g. weights prepared for TAC
+ * run as TAC-TP, whose folded bias and aggregate scale differ -- is refused with
+ * TAC_ERR_PARAM before anything is launched.  Fields that do not enter the image
+ * (T when K divides it, B, H, W, strides, out_pool, engine, v_reset) may differ
+ * between preparation and the call (batch shards, chunked sequences). */
+typedef struct tac_plan {
+  void *prepared;        /* device image (caller-owned, >= tac_weights_bytes, 256-B aligned) */
+  size_t bytes;          /* size of the image                                               */
+  uint64_t fingerprint;  /* of the descriptor at preparation (opaque)                       */
+  int32_t abi_version;   /* TACSNN_ABI_VERSION of the library that prepared it              */
+  int32_t reserved;
+} tac_plan;
 
 /* Validate a descriptor (no device access).  TAC_OK or the first violation. */
 tac_status tac_desc_check(const tac_conv_lif_desc *desc);
@@ -149,11 +181,12 @@ tac_status tac_weights_bytes(const tac_conv_lif_desc *desc, size_t *bytes);
 
 /* Prepare weights once per (desc, W, b): validates finiteness,
  * builds every engine's device format and copies it into `prepared` (device,
- * >= tac_weights_bytes, 256-B aligned).  weight: HOST fp32 [C_out][C_in][R][S];
- * bias: HOST fp32 [C_out] or NULL (= 0).  Synchronous host->device copy. */
+ * >= tac_weights_bytes, 256-B aligned), then fills *plan (host, caller-owned).
+ * weight: HOST fp32 [C_out][C_in][R][S]; bias: HOST fp32 [C_out] or NULL (= 0).
+ * Synchronous host->device copy.  On error *plan is left untouched. */
 tac_status tac_prepare_weights(const tac_conv_lif_desc *desc, const float *weight,
                                const float *bias, void *prepared, size_t bytes,
-                               void *stream);
+                               void *stream, tac_plan *plan);
 
 /* Workspace bytes tac_conv_lif_forward needs: 0, except with partial_last_group
  * and K not dividing T (the membrane state between the full groups and the short
@@ -161,7 +194,8 @@ tac_status tac_prepare_weights(const tac_conv_lif_desc *desc, const float *weigh
 tac_status tac_workspace_bytes(const tac_conv_lif_desc *desc, size_t *bytes);
 
 /* The layer (one call = whole sequence, all groups).
- *   prepared   device, from tac_prepare_weights with an identical desc
+ *   plan       host, filled by tac_prepare_weights for a descriptor with the same
+ *              image-relevant fields (see tac_plan; TAC_ERR_PARAM otherwise)
  *   spikes_in  device u32, packed layout above (4-B aligned)
  *   v_init     device fp32 [B][H'][W'][C_out] or NULL (= 0)
  *   spikes_out device u32, packed, T_out x B x H_o x WPR_out (with strides)
@@ -169,7 +203,7 @@ tac_status tac_workspace_bytes(const tac_conv_lif_desc *desc, size_t *bytes);
  *   counts     device u32 [B][C_out] or NULL (overwritten, not accumulated)
  *   ws         device workspace of ws_bytes >= tac_workspace_bytes (or NULL if 0)
  * spikes_out must not alias spikes_in. */
-tac_status tac_conv_lif_forward(const tac_conv_lif_desc *desc, const void *prepared,
+tac_status tac_conv_lif_forward(const tac_conv_lif_desc *desc, const tac_plan *plan,
                                 const uint32_t *spikes_in, const float *v_init,
                                 uint32_t *spikes_out, float *v_final,
                                 uint32_t *counts, void *ws, size_t ws_bytes,
@@ -180,11 +214,11 @@ tac_status tac_conv_lif_forward(const tac_conv_lif_desc *desc, const void *prepa
  *   x_in  device fp32 [T][B][H][W][C_in] (channels last, 4-B aligned); the t and b
  *         strides (desc.in_stride_t / in_stride_b) are in floats, 0 = contiguous
  *         (H*W*C_in, B*H*W*C_in).
- * Everything else (prepared weights from a descriptor with the same input_kind,
+ * Everything else (a plan prepared from a descriptor with the same input_kind,
  * outputs, errors, ordering) as tac_conv_lif_forward.  tcgen05 takes C_in <= 2
  * (the aggregate is carried as fp16 hi + lo, |error| <= 2^-22 |A|); the SIMT engine
  * any shape. */
-tac_status tac_conv_lif_forward_real(const tac_conv_lif_desc *desc, const void *prepared,
+tac_status tac_conv_lif_forward_real(const tac_conv_lif_desc *desc, const tac_plan *plan,
                                      const float *x_in, const float *v_init,
                                      uint32_t *spikes_out, float *v_final, uint32_t *counts,
                                      void *ws, size_t ws_bytes, void *stream);

@@ -77,6 +77,13 @@ LAYER_CASES = [
     ("dvsL5", (8, 5, 128, 8, 8, 128, 1, 2), 3.5, 0.1),
     ("ragged", (8, 3, 3, 13, 11, 24, 1, 1), 2.0, 0.3),
     ("wide_cin", (4, 2, 96, 10, 9, 48, 1, 2), 2.5, 0.2),
+    # every C_in / C_out the int8 tcgen05 envelope admits (C_in 32k <= 128, C_out 8, 16, 32k)
+    ("cin64", (4, 2, 64, 12, 16, 32, 1, 2), 2.5, 0.15),
+    ("cin96_cout96", (4, 2, 96, 10, 9, 96, 1, 2), 2.5, 0.2),
+    ("cin64_cout128", (4, 2, 64, 9, 20, 128, 0, 1), 2.5, 0.15),
+    ("cout8_int8", (4, 2, 32, 12, 12, 8, 1, 1), 2.5, 0.2),
+    ("cout16_int8", (4, 3, 32, 11, 14, 16, 1, 2), 2.5, 0.2),
+    ("cin128_cout96", (4, 2, 128, 8, 8, 96, 1, 2), 3.0, 0.1),
     # fp16-halo path (C_in <= 8): LDG producers (rows not 16-B multiples) and TMA
     ("rgb", (4, 2, 3, 20, 19, 32, 1, 2), 2.5, 0.2),
     ("cin6_pad0", (4, 2, 6, 9, 13, 16, 0, 1), 2.5, 0.2),
