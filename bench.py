@@ -5,6 +5,10 @@
                     [--K 4] [--impl ours|reference] [--no-cpu-baseline]
     torchrun --nproc-per-node N bench.py --gpus N ...       (one rank per GPU)
 
+With --gpus N > 1 and no torchrun environment, bench.py re-launches itself through
+torch.distributed.run with N ranks (127.0.0.1); under torchrun WORLD_SIZE must equal
+--gpus (a mismatch is an error, not a silent 1-rank run).
+
 A step is one forward pass of the config's whole Conv-LIF stack (every row of
 SURVEY.md section 8(a): aggregation, per-group conv, LIF, packed/pool/counts
 outputs) over the rank's batch shard, followed by the NCCL all_gather of the
@@ -49,7 +53,34 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-T", type=int, default=8)
     ap.add_argument("--layer-detail", action="store_true")
+    ap.add_argument("--no-v-final", action="store_true",
+                    help="skip the extra timing with every layer writing v_final")
+    ap.add_argument("--launcher-check", action="store_true",
+                    help="CPU/gloo check of the rank launcher, shard and gather plumbing only "
+                         "(no kernels, no timing; used by tests/test_bench_launcher.py)")
     return ap.parse_args()
+
+
+def free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def ensure_ranks(a):
+    """--gpus N: run as N ranks.  Outside torchrun, re-exec through torch.distributed.run;
+    inside, insist that WORLD_SIZE == --gpus."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is None:
+        if a.gpus > 1:
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                   f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1",
+                   "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+            os.execv(sys.executable, cmd)
+        return
+    if int(world) != a.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {a.gpus}; launch one rank per GPU")
 
 
 # ------------------------------------------------------------------ helpers --
@@ -155,6 +186,33 @@ def algorithmic_bytes_per_sample(specs):
     return out
 
 
+def dtype_note(specs, engines):
+    """The arithmetic the step runs in, per operand path."""
+    parts = []
+    for i, (s, e) in enumerate(zip(specs, engines)):
+        if e != "tcgen05":
+            parts.append(f"L{i}: f32 (SIMT)")
+        elif s.C_in % 32 == 0 and s.input == "spikes":
+            parts.append(f"L{i}: u8 x 2 i8 slices -> s32")
+        else:
+            parts.append(f"L{i}: f16 x (f16 hi + lo) -> f32")
+    return "; ".join(parts) + "; LIF f32"
+
+
+def l2_note(specs, B):
+    """Timing rule: inputs larger than L2, or a per-step working set that evicts them."""
+    inb = 4.0 * specs[0].T * B * specs[0].H * specs[0].in_words_per_row
+    ws = inb
+    for s in specs:
+        T_out, Ho, _, wpr = s.out_shape()
+        ws += 4.0 * T_out * B * Ho * wpr
+    return (f"per-rank packed input {inb / 2**20:.0f} MiB, per-step working set (input + every "
+            f"layer's packed output) {ws / 2**20:.0f} MiB vs 126 MB L2: "
+            + ("inputs alone exceed L2" if inb > 126e6 else
+               "working set exceeds L2, so each step's input is evicted by the time it is re-read"
+               if ws > 2 * 126e6 else "WARNING: working set fits L2"))
+
+
 # --------------------------------------------------------------- CPU oracle --
 def time_oracle(cfg, specs, weights, B, T_sample):
     """Run the oracle over the stack on a bounded sample; returns (seconds, frames)."""
@@ -174,6 +232,17 @@ def time_oracle(cfg, specs, weights, B, T_sample):
     return time.perf_counter() - t0, B * T_sample
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(cfg, specs, weights, T_sample):
     from oracle import oracle as O
     thr = O.threads()
@@ -181,9 +250,16 @@ def cpu_baseline(cfg, specs, weights, T_sample):
     K = specs[0].K if specs[0].mode != "dense" else 1
     T_sample = max(K, (T_sample // K) * K)
     dt, frames = time_oracle(cfg, specs, weights, B, T_sample)
+    # single-core figure: one sample through one thread
+    O.set_threads(1)
+    try:
+        dt1, frames1 = time_oracle(cfg, specs, weights, 1, T_sample)
+    finally:
+        O.set_threads(thr)
     return {"value": frames / dt, "unit": UNIT, "cores": thr, "kind": "oracle",
+            "single_core_value": frames1 / dt1, "cpu_model": cpu_model(),
             "sample": f"{cfg.name} stack, {B} samples x T={T_sample} (fp64 C oracle, OpenMP "
-                      f"over samples), {dt:.1f} s"}
+                      f"over samples), {dt:.1f} s; single core: 1 sample, {dt1:.1f} s"}
 
 
 # --------------------------------------------------------------- reference --
@@ -221,8 +297,33 @@ def run_reference(a, cfg, specs_fn, rank, world):
 
 
 # -------------------------------------------------------------------- ours --
+def launcher_check(a, rank, world):
+    """Plumbing of the multi-rank bench on CPU (gloo): shard ranges and the output gather
+    exactly as the GPU run uses them, one JSON line from rank 0 (tests/test_bench_launcher.py)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2603_13810_b200 import dist as D
+    if world > 1:
+        dist.init_process_group("gloo")
+    B_global = a.B or 16
+    b0, B = D.shard_range(B_global, world, rank)
+    y = torch.arange(b0, b0 + B, dtype=torch.int32).reshape(1, B, 1).expand(2, B, 3).contiguous()
+    cnt = torch.arange(b0, b0 + B, dtype=torch.int32).reshape(B, 1)
+    if world > 1:
+        y = D.gather_batch(y, dim=1)
+        cnt = D.gather_batch(cnt, dim=0)
+    ok = bool((y[0, :, 0] == torch.arange(B_global)).all()) and bool((cnt[:, 0] == torch.arange(B_global)).all())
+    if rank == 0:
+        print(json.dumps({"launcher_check": True, "n_gpus": world, "gpus_flag": a.gpus,
+                          "global_batch": B_global, "per_rank_batch": B, "gather_ok": ok}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     a = parse()
+    ensure_ranks(a)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -235,6 +336,8 @@ def main():
     def specs_fn(B):
         return configs.layer_plan(cfg, mode=a.mode, K=a.K, B=B, engine=a.engine)
 
+    if a.launcher_check:
+        return launcher_check(a, rank, world)
     if a.impl == "reference":
         return run_reference(a, cfg, specs_fn, rank, world)
 
@@ -427,8 +530,28 @@ def main():
                                "nominal dense int8 = 4.5 POPS",
                        "ncu_tensor_active": "profiles/ncu_c5_layer1_r01*.txt (sm__pipe_tensor_cycles_active)"}
 
+    # ---------------- v_final on: every layer also writes its fp32 membrane state
+    # (SURVEY.md 8(d) "measure with and without it"); a few extra steps after the timed region
+    vfinal = None
+    if not a.no_v_final:
+        nvf = max(2, min(a.steps, 5))
+        for _ in range(1):
+            net.forward(x, want_v_final=True)
+        torch.cuda.synchronize()
+        v0e, v1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0e.record(stream)
+        for _ in range(nvf):
+            net.forward(x, want_v_final=True)
+        v1e.record(stream)
+        torch.cuda.synchronize()
+        vms = v0e.elapsed_time(v1e) / nvf
+        vbytes = sum(4.0 * s_.B * s_.conv_hw[0] * s_.conv_hw[1] * s_.C_out for s_ in specs)
+        vfinal = {"ms_per_step": vms, "value": frames_per_step / (vms / 1e3),
+                  "v_final_bytes_per_step": vbytes, "steps": nvf,
+                  "note": "rank-local: every layer writes fp32 v_final [B,H',W',C_out]"}
+
     cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+    if rank == 0 and not a.no_cpu_baseline:
         cpu = cpu_baseline(cfg, specs, weights, a.cpu_sample_T)
 
     if rank == 0:
@@ -436,19 +559,20 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None,
-            "dtype": "u8 x i8 -> s32 (tcgen05 conv), f32 (LIF)" if "tcgen05" in engines else "f32",
+            "dtype": dtype_note(specs, engines),
             "data": "synthetic",
             "config": {"workload": cfg.name, "description": cfg.description,
                        "mode": specs[0].mode, "K": specs[0].K, "global_batch": B_global,
                        "per_rank_batch": B, "T": cfg.T, "parallelism": f"dp{world}",
                        "layers": len(specs), "engines": engines,
-                       "l2": "inputs+activations > 126 MB L2 (no flush needed)"},
+                       "l2": l2_note(specs, B)},
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": launches_per_step * a.steps,
             "roofline": roof,
             "tensor_pipe": tensor_pipe,
             "cpu_baseline": cpu,
+            "v_final_on": vfinal,
             "layers": layer_rows,
             "peaks": peaks,
         }

@@ -52,17 +52,26 @@ def lib():
             L.tac_oracle_forward.restype = i
             L.tac_oracle_forward_x.argtypes = L.tac_oracle_forward.argtypes
             L.tac_oracle_forward_x.restype = i
+            L.tac_oracle_forward_alpha.argtypes = [P, P, P] + L.tac_oracle_forward.argtypes[1:]
+            L.tac_oracle_forward_alpha.restype = i
             L.tac_oracle_conv2d.argtypes = [P, P, P] + [i] * 9 + [P]
             L.tac_oracle_conv2d.restype = i
             L.tac_oracle_or_pool2.argtypes = [P, i, i, i, i, P]
             L.tac_oracle_or_pool2.restype = i
             L.tac_oracle_threads.restype = i
+            L.tac_oracle_set_threads.argtypes = [i]
+            L.tac_oracle_set_threads.restype = None
             _lib = L
     return _lib
 
 
 def threads() -> int:
     return int(lib().tac_oracle_threads())
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of later oracle calls (single-core baseline timing)."""
+    lib().tac_oracle_set_threads(int(n))
 
 
 def _ptr(a):
@@ -90,7 +99,7 @@ def conv2d(X, Wt, bias=None, stride=1, pad=0):
 
 def forward(S, Wt, bias=None, *, K=1, mode="tac", beta=0.9, v_th=1.0, v_reset=0.0,
             reset="subtract", stride=1, pad=0, v_init=None, replay=None, band=1e-3,
-            partial=False):
+            partial=False, alpha=None):
     """One Conv-LIF layer (Eq. 1 / Alg. 1 / Alg. 2) on u8 spikes S [T,B,Cin,H,W]
     or, when S is a floating array, on continuous-valued input frames (computed
     in fp64; the DVS first layer's log-normalised counts).
@@ -100,6 +109,8 @@ def forward(S, Wt, bias=None, *, K=1, mode="tac", beta=0.9, v_th=1.0, v_reset=0.
     rounded to fp32 first (the layer's parameters are fp32 in the ABI) and then
     used in fp64.  With ``replay`` (device spikes, same layout as out) the
     trajectory follows the replay protocol described in tac_oracle.c.
+    ``alpha`` (K values, rounded to fp32 like the ABI's agg_weights): learnable
+    aggregation weights in place of beta^{K-1-j} (reading R11).
     """
     real = np.issubdtype(np.asarray(S).dtype, np.floating)
     S = np.ascontiguousarray(S, dtype=np.float64 if real else np.uint8)
@@ -127,7 +138,14 @@ def forward(S, Wt, bias=None, *, K=1, mode="tac", beta=0.9, v_th=1.0, v_reset=0.
     mism = np.zeros(1, np.int64)
     exc = np.zeros(1, np.int64)
     f32 = lambda v: float(np.float32(v))
-    fwd = lib().tac_oracle_forward_x if real else lib().tac_oracle_forward
+    L = lib()
+    if alpha is not None:
+        alpha = np.ascontiguousarray(np.asarray(alpha, np.float32).astype(np.float64))
+        assert alpha.shape == (K,), (alpha.shape, K)
+        fwd = lambda S_, *rest: L.tac_oracle_forward_alpha(
+            None if real else S_, S_ if real else None, _ptr(alpha), *rest)
+    else:
+        fwd = L.tac_oracle_forward_x if real else L.tac_oracle_forward
     rc = fwd(
         _ptr(S), _ptr(Wt), _ptr(bias), T, B, Cin, H, W, Cout, R, Sk, stride, pad,
         -K if (partial and m != 0) else K, m,

@@ -59,6 +59,15 @@ int tac_oracle_threads(void) {
 #endif
 }
 
+/* Thread count of later calls (timing the single-core baseline). */
+void tac_oracle_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 /* Direct-loop 2-D cross-correlation of ONE sample.
  * X [Cin][H][W], Wt [Cout][Cin][R][S], bias [Cout] or NULL, Y [Cout][Ho][Wo]. */
 static void conv_one(const double *X, const float *Wt, const float *bias,
@@ -132,7 +141,8 @@ static int lif_step(double *V, int *s_prev, double I, double decay, double v_th,
  *   mismatch/excused : int64 scalars (may be NULL when replay is NULL)
  * Returns 0, or -1 on a bad argument (K not dividing T, etc.).
  */
-static int forward_impl(const uint8_t *S, const double *X, const float *Wt, const float *bias,
+static int forward_impl(const uint8_t *S, const double *X, const double *alpha,
+                        const float *Wt, const float *bias,
                         int T, int B, int Cin, int H, int W, int Cout, int R,
                         int Sk, int stride, int pad, int K, int mode,
                         double beta, double v_th, double v_reset, int reset,
@@ -166,10 +176,13 @@ static int forward_impl(const uint8_t *S, const double *X, const float *Wt, cons
 
     for (int k = 0; k < G; ++k) {
       const int Kg = (T - k * K < K) ? T - k * K : K; /* frames in this group */
-      /* A_k = sum_{j=0}^{K-1} beta^{K-1-j} S_{kK+j}.  Dense: A = S_t. */
+      /* A_k = sum_{j=0}^{K-1} beta^{K-1-j} S_{kK+j}.  Dense: A = S_t.
+       * Learnable weights (reading R11): alpha_j in place of beta^{K-1-j}; a short
+       * group of Kg frames takes the last Kg entries alpha[K-Kg+j] (reading D6'). */
       for (size_t i = 0; i < nin; ++i) A[i] = 0.0;
       for (int j = 0; j < Kg; ++j) {
-        double wj = pow(beta, (double)(Kg - 1 - j));
+        double wj = (alpha && mode != OR_MODE_DENSE) ? alpha[K - Kg + j]
+                                                     : pow(beta, (double)(Kg - 1 - j));
         const size_t off = ((size_t)(k * K + j) * B + b) * nin;
         if (X) { /* continuous-valued input frames, same definition */
           for (size_t i = 0; i < nin; ++i) A[i] += wj * X[off + i];
@@ -210,7 +223,7 @@ int tac_oracle_forward(const uint8_t *S, const float *Wt, const float *bias,
                        int64_t *counts, const uint8_t *replay, double band,
                        int64_t *mismatch_out, int64_t *excused_out) {
   if (!S) return -1;
-  return forward_impl(S, NULL, Wt, bias, T, B, Cin, H, W, Cout, R, Sk, stride, pad, K, mode,
+  return forward_impl(S, NULL, NULL, Wt, bias, T, B, Cin, H, W, Cout, R, Sk, stride, pad, K, mode,
                       beta, v_th, v_reset, reset, v_init, out, v_final, counts, replay, band,
                       mismatch_out, excused_out);
 }
@@ -226,7 +239,23 @@ int tac_oracle_forward_x(const double *X, const float *Wt, const float *bias,
                          int64_t *counts, const uint8_t *replay, double band,
                          int64_t *mismatch_out, int64_t *excused_out) {
   if (!X) return -1;
-  return forward_impl(NULL, X, Wt, bias, T, B, Cin, H, W, Cout, R, Sk, stride, pad, K, mode,
+  return forward_impl(NULL, X, NULL, Wt, bias, T, B, Cin, H, W, Cout, R, Sk, stride, pad, K, mode,
+                      beta, v_th, v_reset, reset, v_init, out, v_final, counts, replay, band,
+                      mismatch_out, excused_out);
+}
+
+/* Either input kind (exactly one of S, X non-NULL) with learnable aggregation weights
+ * alpha [K] (fp64; NULL = beta^{K-1-j}). */
+int tac_oracle_forward_alpha(const uint8_t *S, const double *X, const double *alpha,
+                             const float *Wt, const float *bias,
+                             int T, int B, int Cin, int H, int W, int Cout, int R,
+                             int Sk, int stride, int pad, int K, int mode,
+                             double beta, double v_th, double v_reset, int reset,
+                             const double *v_init, uint8_t *out, double *v_final,
+                             int64_t *counts, const uint8_t *replay, double band,
+                             int64_t *mismatch_out, int64_t *excused_out) {
+  if ((S == NULL) == (X == NULL)) return -1;
+  return forward_impl(S, X, alpha, Wt, bias, T, B, Cin, H, W, Cout, R, Sk, stride, pad, K, mode,
                       beta, v_th, v_reset, reset, v_init, out, v_final, counts, replay, band,
                       mismatch_out, excused_out);
 }

@@ -78,6 +78,10 @@ tac_status check(const tac_conv_lif_desc *d, Geo *g) {
     return fail(TAC_ERR_PARAM, "input_kind=%d not in {0,1}", d->input_kind);
   if (d->partial_last_group != 0 && d->partial_last_group != 1)
     return fail(TAC_ERR_PARAM, "partial_last_group=%d not in {0,1}", d->partial_last_group);
+  if (d->agg_weights && d->mode != TAC_MODE_DENSE)
+    for (int j = 0; j < K; ++j)
+      if (!std::isfinite(d->agg_weights[j]))
+        return fail(TAC_ERR_NONFINITE, "agg_weights[%d] is not finite", j);
   g->K = K;
   g->Ho = Ho;
   g->Wo = Wo;
@@ -138,6 +142,8 @@ tac_conv_lif_desc part_desc(const tac_conv_lif_desc *d, const Geo &g, bool last)
   p.in_stride_b = g.in_sb;
   p.out_stride_t = g.out_st;
   p.out_stride_b = g.out_sb;
+  // the short group of K' frames aggregates with the last K' weights (reading R11)
+  if (last && d->agg_weights && d->mode != TAC_MODE_DENSE) p.agg_weights = d->agg_weights + (g.K - g.K_last);
   // a short last group outside the tcgen05 envelope (K' not in {1,2,4,8}) runs on SIMT
   if (last && p.engine == TAC_ENGINE_TCGEN05 && !tacsnn::tc_supported(&p)) p.engine = TAC_ENGINE_AUTO;
   return p;
@@ -157,13 +163,78 @@ size_t ws_total(const tac_conv_lif_desc *d, const Geo &g) {
   return align256((size_t)d->B * g.Ho * g.Wo * d->C_out * 4) + align256((size_t)d->B * d->C_out * 4);
 }
 
+// Device-pointer check with a small per-thread cache of device allocation ranges
+// (cuMemGetAddressRange): a launch-bound layer call then costs no
+// cudaPointerGetAttributes round trips for buffers it has seen before (the torch
+// caching allocator keeps its segments, so the ranges are stable).
+struct Range {
+  uintptr_t lo, hi;
+};
+thread_local Range g_ranges[32];
+thread_local int g_nranges = 0, g_next_range = 0;
+typedef int (*PFN_getAddressRange)(unsigned long long *, size_t *, unsigned long long);
+PFN_getAddressRange address_range_fn() {
+  static PFN_getAddressRange fn = [] {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      f = nullptr;
+    }
+    return reinterpret_cast<PFN_getAddressRange>(f);
+  }();
+  return fn;
+}
 bool is_device_ptr(const void *p) {
+  const uintptr_t u = reinterpret_cast<uintptr_t>(p);
+  for (int i = 0; i < g_nranges; ++i)
+    if (u >= g_ranges[i].lo && u < g_ranges[i].hi) return true;
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
-  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+  const bool dev = a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+  if (dev && a.type == cudaMemoryTypeDevice) {
+    PFN_getAddressRange fn = address_range_fn();
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (fn && fn(&base, &size, (unsigned long long)u) == 0 && size) {
+      g_ranges[g_next_range] = Range{(uintptr_t)base, (uintptr_t)base + size};
+      g_next_range = (g_next_range + 1) % 32;
+      if (g_nranges < 32) ++g_nranges;
+    }
+  }
+  return dev;
+}
+
+// Fingerprint of the descriptor fields the prepared image depends on (tac_plan):
+// FNV-1a over the geometry, the effective K, mode, beta / v_th bits, reset,
+// input kind, the short-group size of a split call and the aggregation weights.
+uint64_t fingerprint(const tac_conv_lif_desc *d, const Geo &g, bool split) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&h](uint64_t v) {
+    for (int i = 0; i < 8; ++i) {
+      h ^= (v >> (8 * i)) & 0xFFu;
+      h *= 1099511628211ull;
+    }
+  };
+  uint32_t bits;
+  mix((uint64_t)TACSNN_ABI_VERSION);
+  mix((uint64_t)d->C_in); mix((uint64_t)d->C_out); mix((uint64_t)d->R); mix((uint64_t)d->S);
+  mix((uint64_t)d->stride); mix((uint64_t)d->pad); mix((uint64_t)g.K); mix((uint64_t)d->mode);
+  std::memcpy(&bits, &d->beta, 4); mix(bits);
+  std::memcpy(&bits, &d->v_th, 4); mix(bits);
+  mix((uint64_t)d->reset); mix((uint64_t)d->input_kind);
+  mix(split ? (uint64_t)g.K_last : 0ull);
+  mix(d->agg_weights && d->mode != TAC_MODE_DENSE ? 1ull : 0ull);
+  if (d->agg_weights && d->mode != TAC_MODE_DENSE)
+    for (int j = 0; j < g.K; ++j) {
+      std::memcpy(&bits, &d->agg_weights[j], 4);
+      mix(bits);
+    }
+  return h;
 }
 
 int resolve_engine(const tac_conv_lif_desc *d) {
@@ -225,12 +296,13 @@ tac_status tac_workspace_bytes(const tac_conv_lif_desc *desc, size_t *bytes) {
 
 tac_status tac_prepare_weights(const tac_conv_lif_desc *desc, const float *weight,
                                const float *bias, void *prepared, size_t bytes,
-                               void *stream) {
+                               void *stream, tac_plan *plan) {
   g_detail.clear();
   Geo g;
   tac_status st = check(desc, &g);
   if (st != TAC_OK) return st;
   if (!weight) return fail(TAC_ERR_NULL, "weight is NULL");
+  if (!plan) return fail(TAC_ERR_NULL, "plan is NULL");
   if (!prepared) return fail(TAC_ERR_NULL, "prepared is NULL");
   const size_t total = prep_total(desc, g);
   if (bytes < total) return fail(TAC_ERR_WORKSPACE, "prepared buffer %zu < %zu bytes", bytes, total);
@@ -270,77 +342,25 @@ tac_status tac_prepare_weights(const tac_conv_lif_desc *desc, const float *weigh
                                   (cudaStream_t)stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
   if (e != cudaSuccess) return fail(TAC_ERR_CUDA, "prepare copy: %s", cudaGetErrorString(e));
+  plan->prepared = prepared;
+  plan->bytes = total;
+  plan->fingerprint = fingerprint(desc, g, is_split_call(desc, g));
+  plan->abi_version = TACSNN_ABI_VERSION;
+  plan->reserved = 0;
   return TAC_OK;
 }
 
 }  // extern "C"
 
 namespace {
-// shared body of tac_conv_lif_forward / tac_conv_lif_forward_real
-tac_status forward_impl(const tac_conv_lif_desc *desc, const void *prepared, const void *input,
-                        bool real, const float *v_init, uint32_t *spikes_out, float *v_final,
-                        uint32_t *counts, void *ws, size_t ws_bytes, void *stream);
-
-// K does not divide T with partial_last_group: the full groups, then the short last
-// group, chained through the membrane state in the workspace (see part_desc)
-tac_status forward_split(const tac_conv_lif_desc *desc, const Geo &g, const void *prepared,
-                         const void *input, bool real, const float *v_init, uint32_t *spikes_out,
-                         float *v_final, uint32_t *counts, void *ws, size_t ws_bytes, void *stream) {
-  const tac_conv_lif_desc last = part_desc(desc, g, true);
-  if (g.G == 1)  // T < K: the whole sequence is one short group
-    return forward_impl(&last, prepared, input, real, v_init, spikes_out, v_final, counts, nullptr, 0,
-                        stream);
-  const size_t need = ws_total(desc, g);
-  if (!ws) return fail(TAC_ERR_NULL, "partial_last_group with K not dividing T needs a workspace");
-  if (ws_bytes < need) return fail(TAC_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
-  if ((uintptr_t)ws % 256) return fail(TAC_ERR_ALIGN, "workspace must be 256-B aligned");
-  const tac_conv_lif_desc full = part_desc(desc, g, false);
-  float *v_mid = static_cast<float *>(ws);
-  uint32_t *cnt2 = reinterpret_cast<uint32_t *>(static_cast<unsigned char *>(ws) +
-                                                align256((size_t)desc->B * g.Ho * g.Wo * desc->C_out * 4));
-  tac_status st = forward_impl(&full, prepared, input, real, v_init, spikes_out, v_mid, counts, nullptr, 0,
-                               stream);
-  if (st != TAC_OK) return st;
-  const int launches1 = g_launches;
-  const size_t esz = real ? sizeof(float) : sizeof(uint32_t);
-  const void *in2 = static_cast<const unsigned char *>(input) + (size_t)full.T * g.in_st * esz;
-  const int t_out1 = desc->mode == TAC_MODE_TAC ? g.G - 1 : full.T;
-  uint32_t *out2 = spikes_out + (size_t)t_out1 * g.out_st;
-  const void *prep2 = static_cast<const unsigned char *>(prepared) + prep_layout(&full).total;
-  st = forward_impl(&last, prep2, in2, real, v_mid, out2, v_final, counts ? cnt2 : nullptr, nullptr, 0,
-                    stream);
-  if (st != TAC_OK) return st;
-  int launches = launches1 + g_launches;
-  if (counts) {
-    const int e = tacsnn::launch_add_u32(counts, cnt2, (long long)desc->B * desc->C_out, stream);
-    if (e) return fail(TAC_ERR_CUDA, "count merge: %s", cudaGetErrorString((cudaError_t)e));
-    ++launches;
-  }
-  g_launches = launches;
-  return TAC_OK;
-}
-
-tac_status forward_impl(const tac_conv_lif_desc *desc, const void *prepared, const void *input,
-                        bool real, const float *v_init, uint32_t *spikes_out, float *v_final,
-                        uint32_t *counts, void *ws, size_t ws_bytes, void *stream) {
-  g_detail.clear();
-  Geo g;
-  tac_status st = check(desc, &g);
-  if (st != TAC_OK) return st;
-  if (is_split_call(desc, g)) {
-    if ((desc->input_kind == TAC_INPUT_REAL) != real)
-      return fail(TAC_ERR_PARAM, "input_kind does not match the entry point");
-    if (!prepared || !input || !spikes_out) return fail(TAC_ERR_NULL, "NULL buffer");
-    return forward_split(desc, g, prepared, input, real, v_init, spikes_out, v_final, counts, ws,
-                         ws_bytes, stream);
-  }
-  (void)ws;
-  (void)ws_bytes;
+// Argument checks of one (non-split) launch, before anything is enqueued.
+tac_status validate_call(const tac_conv_lif_desc *desc, const void *prepared, const void *input,
+                         bool real, const float *v_init, const uint32_t *spikes_out,
+                         const float *v_final, const uint32_t *counts, int *engine_out) {
   if ((desc->input_kind == TAC_INPUT_REAL) != real)
     return fail(TAC_ERR_PARAM, real ? "tac_conv_lif_forward_real needs input_kind = TAC_INPUT_REAL"
                                     : "input_kind = TAC_INPUT_REAL needs tac_conv_lif_forward_real");
-  const uint32_t *spikes_in = real ? nullptr : static_cast<const uint32_t *>(input);
-  if (!prepared) return fail(TAC_ERR_NULL, "prepared is NULL");
+  if (!prepared) return fail(TAC_ERR_NULL, "plan->prepared is NULL");
   if (!input) return fail(TAC_ERR_NULL, real ? "x_in is NULL" : "spikes_in is NULL");
   if (!spikes_out) return fail(TAC_ERR_NULL, "spikes_out is NULL");
   const int engine = resolve_engine(desc);
@@ -358,7 +378,14 @@ tac_status forward_impl(const tac_conv_lif_desc *desc, const void *prepared, con
   for (int i = 0; i < 6; ++i)
     if (dev_ptrs[i] && !is_device_ptr(dev_ptrs[i]))
       return fail(TAC_ERR_PARAM, "%s is not device memory", names[i]);
+  *engine_out = engine;
+  return TAC_OK;
+}
 
+// Enqueue one validated (non-split) call.
+tac_status launch_call(const tac_conv_lif_desc *desc, const Geo &g, int engine, const void *prepared,
+                       const void *input, bool real, const float *v_init, uint32_t *spikes_out,
+                       float *v_final, uint32_t *counts, void *stream, int *launches) {
   tacsnn::LayerParams p{};
   p.T = desc->T; p.B = desc->B; p.Cin = desc->C_in; p.H = desc->H; p.W = desc->W;
   p.Cout = desc->C_out; p.R = desc->R; p.S = desc->S; p.stride = desc->stride; p.pad = desc->pad;
@@ -369,23 +396,107 @@ tac_status forward_impl(const tac_conv_lif_desc *desc, const void *prepared, con
   p.v_th = desc->v_th; p.v_reset = desc->v_reset;
   const double beta = (double)desc->beta;
   p.decay = (float)(desc->mode == TAC_MODE_TAC ? std::pow(beta, (double)g.K) : beta);
-  for (int j = 0; j < g.K; ++j) p.coef[j] = (float)std::pow(beta, (double)(g.K - 1 - j));
-  p.in = spikes_in; p.out = spikes_out; p.v_init = v_init; p.v_final = v_final; p.counts = counts;
+  // A_k weights: beta^{K-1-j} or the learnable alpha_j
+  const bool alpha = desc->agg_weights && desc->mode != TAC_MODE_DENSE;
+  for (int j = 0; j < g.K; ++j)
+    p.coef[j] = alpha ? desc->agg_weights[j] : (float)std::pow(beta, (double)(g.K - 1 - j));
+  p.in = real ? nullptr : static_cast<const uint32_t *>(input);
+  p.out = spikes_out; p.v_init = v_init; p.v_final = v_final; p.counts = counts;
   p.xin = real ? static_cast<const float *>(input) : nullptr;
   const PrepLayout L = prep_layout(desc);
   const unsigned char *base = static_cast<const unsigned char *>(prepared);
   p.w = reinterpret_cast<const float *>(base + L.simt_off);
   p.bias = reinterpret_cast<const float *>(base + L.bias_off);
-
-  int launches = 0;
   int err = 0;
   if (engine == TAC_ENGINE_TCGEN05) {
-    err = tacsnn::tc_launch(desc, p, base + L.tc_off, stream, &launches);
+    err = tacsnn::tc_launch(desc, p, base + L.tc_off, stream, launches);
   } else {
-    err = tacsnn::launch_zero_outputs(p, stream, &launches);
-    if (!err) err = tacsnn::launch_simt_conv_lif(p, stream, &launches);
+    err = tacsnn::launch_zero_outputs(p, stream, launches);
+    if (!err) err = tacsnn::launch_simt_conv_lif(p, stream, launches);
   }
   if (err) return fail(TAC_ERR_CUDA, "launch failed: %s", cudaGetErrorString((cudaError_t)err));
+  return TAC_OK;
+}
+
+// shared body of tac_conv_lif_forward / tac_conv_lif_forward_real: plan check, then
+// one launch, or -- K not dividing T with partial_last_group -- the full groups and
+// the short last group chained through the membrane state in the workspace (both
+// parts validated before the first launch)
+tac_status forward_impl(const tac_conv_lif_desc *desc, const tac_plan *plan, const void *input,
+                        bool real, const float *v_init, uint32_t *spikes_out, float *v_final,
+                        uint32_t *counts, void *ws, size_t ws_bytes, void *stream) {
+  g_detail.clear();
+  g_launches = 0;
+  Geo g;
+  tac_status st = check(desc, &g);
+  if (st != TAC_OK) return st;
+  if (!plan) return fail(TAC_ERR_NULL, "plan is NULL");
+  if (plan->abi_version != TACSNN_ABI_VERSION)
+    return fail(TAC_ERR_PARAM, "plan prepared by ABI version %d, library is %d", plan->abi_version,
+                TACSNN_ABI_VERSION);
+  const bool split = is_split_call(desc, g);
+  if (plan->fingerprint != fingerprint(desc, g, split))
+    return fail(TAC_ERR_PARAM, "plan was prepared for a different descriptor (C_in, C_out, kernel, "
+                               "K, mode, beta, v_th, reset, input kind, short group or agg_weights "
+                               "differ; see tac_plan)");
+  const size_t need = prep_total(desc, g);
+  if (plan->bytes < need) return fail(TAC_ERR_WORKSPACE, "plan image %zu < %zu bytes", plan->bytes, need);
+  const void *prepared = plan->prepared;
+  int launches = 0;
+  if (!split) {
+    int engine;
+    st = validate_call(desc, prepared, input, real, v_init, spikes_out, v_final, counts, &engine);
+    if (st != TAC_OK) return st;
+    st = launch_call(desc, g, engine, prepared, input, real, v_init, spikes_out, v_final, counts, stream,
+                     &launches);
+    if (st == TAC_OK) g_launches = launches;
+    return st;
+  }
+  const tac_conv_lif_desc last = part_desc(desc, g, true);
+  Geo gl;
+  if ((st = check(&last, &gl)) != TAC_OK) return st;
+  if (g.G == 1) {  // T < K: the whole sequence is one short group
+    int engine;
+    st = validate_call(&last, prepared, input, real, v_init, spikes_out, v_final, counts, &engine);
+    if (st != TAC_OK) return st;
+    st = launch_call(&last, gl, engine, prepared, input, real, v_init, spikes_out, v_final, counts, stream,
+                     &launches);
+    if (st == TAC_OK) g_launches = launches;
+    return st;
+  }
+  if (!input || !spikes_out) return fail(TAC_ERR_NULL, "NULL buffer");
+  if (!ws) return fail(TAC_ERR_NULL, "partial_last_group with K not dividing T needs a workspace");
+  const size_t wneed = ws_total(desc, g);
+  if (ws_bytes < wneed) return fail(TAC_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, wneed);
+  if ((uintptr_t)ws % 256) return fail(TAC_ERR_ALIGN, "workspace must be 256-B aligned");
+  const tac_conv_lif_desc full = part_desc(desc, g, false);
+  Geo gf;
+  if ((st = check(&full, &gf)) != TAC_OK) return st;
+  float *v_mid = static_cast<float *>(ws);
+  uint32_t *cnt2 = reinterpret_cast<uint32_t *>(static_cast<unsigned char *>(ws) +
+                                                align256((size_t)desc->B * g.Ho * g.Wo * desc->C_out * 4));
+  const size_t esz = real ? sizeof(float) : sizeof(uint32_t);
+  const void *in2 = static_cast<const unsigned char *>(input) + (size_t)full.T * g.in_st * esz;
+  const int t_out1 = desc->mode == TAC_MODE_TAC ? g.G - 1 : full.T;
+  uint32_t *out2 = spikes_out + (size_t)t_out1 * g.out_st;
+  const void *prep2 = static_cast<const unsigned char *>(prepared) + prep_layout(&full).total;
+  int eng1, eng2;
+  if ((st = validate_call(&full, prepared, input, real, v_init, spikes_out, v_mid, counts, &eng1)) != TAC_OK)
+    return st;
+  if ((st = validate_call(&last, prep2, in2, real, v_mid, out2, v_final, counts ? cnt2 : nullptr, &eng2)) !=
+      TAC_OK)
+    return st;
+  if ((st = launch_call(&full, gf, eng1, prepared, input, real, v_init, spikes_out, v_mid, counts, stream,
+                        &launches)) != TAC_OK)
+    return st;
+  if ((st = launch_call(&last, gl, eng2, prep2, in2, real, v_mid, out2, v_final, counts ? cnt2 : nullptr,
+                        stream, &launches)) != TAC_OK)
+    return st;
+  if (counts) {
+    const int e = tacsnn::launch_add_u32(counts, cnt2, (long long)desc->B * desc->C_out, stream);
+    if (e) return fail(TAC_ERR_CUDA, "count merge: %s", cudaGetErrorString((cudaError_t)e));
+    ++launches;
+  }
   g_launches = launches;
   return TAC_OK;
 }
@@ -393,19 +504,19 @@ tac_status forward_impl(const tac_conv_lif_desc *desc, const void *prepared, con
 
 extern "C" {
 
-tac_status tac_conv_lif_forward(const tac_conv_lif_desc *desc, const void *prepared,
+tac_status tac_conv_lif_forward(const tac_conv_lif_desc *desc, const tac_plan *plan,
                                 const uint32_t *spikes_in, const float *v_init,
                                 uint32_t *spikes_out, float *v_final, uint32_t *counts,
                                 void *ws, size_t ws_bytes, void *stream) {
-  return forward_impl(desc, prepared, spikes_in, false, v_init, spikes_out, v_final, counts, ws, ws_bytes,
+  return forward_impl(desc, plan, spikes_in, false, v_init, spikes_out, v_final, counts, ws, ws_bytes,
                       stream);
 }
 
-tac_status tac_conv_lif_forward_real(const tac_conv_lif_desc *desc, const void *prepared,
+tac_status tac_conv_lif_forward_real(const tac_conv_lif_desc *desc, const tac_plan *plan,
                                      const float *x_in, const float *v_init,
                                      uint32_t *spikes_out, float *v_final, uint32_t *counts,
                                      void *ws, size_t ws_bytes, void *stream) {
-  return forward_impl(desc, prepared, x_in, true, v_init, spikes_out, v_final, counts, ws, ws_bytes,
+  return forward_impl(desc, plan, x_in, true, v_init, spikes_out, v_final, counts, ws, ws_bytes,
                       stream);
 }
 

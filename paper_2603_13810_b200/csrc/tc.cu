@@ -127,9 +127,9 @@ struct TcParams {
   int split;             // A carried as fp16 hi + lo from the 2^K-entry table lut
   int real;              // continuous input xin (A computed from fp32 frames, then hi + lo)
   const float *xin;      // fp32 [T][B][H][W][C_in], strides in_st / in_sb in floats
-  float coef[8];         // beta^{K-1-j}, fp32 (from fp64)
-  uint32_t off_lut;      // smem copy of lut
-  uint32_t lut[1 << 8];  // idx (bit j = frame j's spike) -> fp16 A_hi | fp16 A_lo << 16
+  float coef[16];        // A_k weights beta^{K-1-j} or alpha_j (fp32)
+  uint32_t off_lut;      // smem copy of the aggregate tables (split path)
+  const uint32_t *lut_g; // the tables in the prepared image (see tc_prepare)
   const uint32_t *in;
   uint32_t *out;
   const float *v_init;
@@ -137,6 +137,7 @@ struct TcParams {
   uint32_t *counts;
   const unsigned char *w_img;
   const float *scale_bias;
+  const float *yscale;        // [2^e, 2^-e]: fp16-path prescale of Y (see tc_prepare)
   unsigned long long *trace;  // optional: per-(group) role timestamps of CTA 0 (debug)
 };
 
@@ -180,13 +181,26 @@ int cout_pad_of(int Cout) {
 // m (K-1) > 7), A is carried as two fp16 values A_hi + A_lo (|A - A_hi - A_lo| <=
 // 2^-22 |A|) looked up from a 2^K-entry table of the K spike bits of a channel,
 // and both ride the fp16 tensor-core path as extra K channels.
+constexpr bool templ_k(int K);
 bool split_of(const tac_conv_lif_desc *d) {
   if (d->input_kind == TAC_INPUT_REAL) return true;  // continuous input: A is any real
-  if (d->mode == TAC_MODE_DENSE || d->K <= 1) return false;
+  if (d->mode == TAC_MODE_DENSE) return false;
+  if (d->agg_weights) return true;                   // learnable alpha_j: any real
+  if (d->K <= 1) return false;
+  // a group size without a templated exact producer runs the runtime-K table producer
+  // (exact values are exact table entries too); first layers only (envelope)
+  if (!templ_k(d->K) && d->C_in <= 2) return true;
   const int m = beta_shift(d->beta);
   return m == 0 || m * (d->K - 1) > 7;
 }
-constexpr int kMaxSplitK = 8;  // 2^K-entry table
+// Aggregate tables of the split path: K <= 8: 2^K entries fp16 A_hi | A_lo << 16 indexed
+// by the K spike bits of a channel (bit j = frame j); 8 < K <= 16 (first layers, C_in <= 2):
+// two fp32 tables, frames 0..K-9 and K-8..K-1, summed in fp32 and split in the producer.
+constexpr int kMaxSplitK = 16;
+constexpr int kLutWords = 3 << 8;  // [fp16-pair table | fp32 table A | fp32 table B]
+// group sizes the templated producers are instantiated for; other K <= 16 run the
+// runtime-K split producer (C_in <= 2)
+constexpr bool templ_k(int K) { return K == 1 || K == 2 || K == 3 || K == 4 || K == 8; }
 
 int path_of(const tac_conv_lif_desc *d) {
   if (split_of(d)) return PATH_H16;  // (kernel template PATH_SPLIT)
@@ -258,7 +272,7 @@ Geometry geometry(const tac_conv_lif_desc *d, bool use_tma = false) {
     g.off_raw = align_up(g.off_a + g.nstages * g.a_stage_bytes, 128);
     g.off_scale = align_up(g.off_raw + g.nraw * g.raw_stage_bytes, 128);
     g.off_lut = align_up(g.off_scale + 4u * g.cout_pad * 4u, 16);
-    g.off_bar = align_up(g.off_lut + (g.split ? 4u << kMaxSplitK : 0u), 64);  // split: 2^K table
+    g.off_bar = align_up(g.off_lut + (g.split ? 4u * kLutWords : 0u), 64);  // split: aggregate tables
     g.smem_bytes = g.off_bar + 8u * kNumBars + 16u;
     if (g.smem_bytes <= kSmemLimit) break;
   }
@@ -276,8 +290,7 @@ const char *shape_reason(const tac_conv_lif_desc *d) {
     return "needs C_out in {8,16} or a multiple of 32 up to 128";
   const int K = d->mode == TAC_MODE_DENSE ? 1 : d->K;
   if (d->mode == TAC_MODE_TACTP && K > kMaxSteps) return "TAC-TP needs K <= 8";
-  // the producers are instantiated for these group sizes (3: short last groups, e.g. T = 7, K = 4)
-  if (!(K == 1 || K == 2 || K == 3 || K == 4 || K == 8)) return "needs K in {1, 2, 3, 4, 8}";
+  if (K > kMaxSplitK) return "needs K <= 16";
   return nullptr;
 }
 
@@ -285,9 +298,15 @@ const char *reason(const tac_conv_lif_desc *d) {
   const char *r = shape_reason(d);
   if (r) return r;
   if (d->input_kind == TAC_INPUT_REAL && d->C_in > 2) return "continuous input needs C_in <= 2";
+  const int K = d->mode == TAC_MODE_DENSE ? 1 : d->K;
   if (split_of(d)) {
-    if (d->K > kMaxSplitK) return "split (beta != 2^-m) aggregate needs K <= 8";
-    if (!(d->C_in <= 2 || d->C_in == 32)) return "split (beta != 2^-m) aggregate needs C_in in {1, 2, 32}";
+    if (!(d->C_in <= 2 || d->C_in == 32))
+      return "split (beta != 2^-m, learnable or continuous) aggregate needs C_in in {1, 2, 32}";
+    // any K <= 16 on the first layers (runtime-K producer); the producers are instantiated
+    // for K in {1, 2, 3, 4, 8} (3: short last groups, e.g. T = 7, K = 4)
+    if (d->C_in == 32 && !templ_k(K)) return "split aggregate with C_in = 32 needs K in {1, 2, 3, 4, 8}";
+  } else if (!templ_k(K)) {
+    return "needs K in {1, 2, 3, 4, 8} (or a split aggregate on C_in <= 2 with K <= 16)";
   }
   if (geometry(d).smem_bytes > kSmemLimit) return "shared-memory footprint exceeds 227 KB";
   return nullptr;
@@ -573,6 +592,22 @@ __device__ __forceinline__ void store_split32_row(uint32_t dst, uint32_t lbo, co
   ptx::st_shared_v4(dst + 9 * lbo, 0u, 0u, 0u, 0u);
 }
 
+// Runtime group size (any K <= 16; split path, C_in <= 2): the K-bit index of a channel
+// is gathered frame by frame; K <= 8 reads the fp16-pair table, 8 < K <= 16 adds the two
+// fp32 half tables (frames 0..K-9 | K-8..K-1) and splits the sum into fp16 hi + lo
+// (|A - A_hi - A_lo| <= 2^-22 |A| + fp32 rounding of the table sum).
+__device__ __forceinline__ uint32_t f32_to_h16pair(float a) {
+  const __half hi = __float2half_rn(a);
+  const __half lo = __float2half_rn(a - __half2float(hi));
+  return (uint32_t)__half_as_ushort(hi) | ((uint32_t)__half_as_ushort(lo) << 16);
+}
+__device__ __forceinline__ uint32_t split_lookup(uint32_t idx, int K, const uint32_t *lut) {
+  if (K <= 8) return lut[idx];
+  const int ka = K - 8;
+  return f32_to_h16pair(__uint_as_float(lut[256 + (idx & ((1u << ka) - 1u))]) +
+                        __uint_as_float(lut[512 + (idx >> ka)]));
+}
+
 // continuous-input producer (input_kind REAL, C_in <= 2): A_c = sum_j beta^{K-1-j}
 // X_{kK+j, c} in fp32 (the oracle's order), then the same [A_hi | A_lo | 1.0] row as
 // the split path
@@ -582,7 +617,7 @@ __device__ __forceinline__ void produce_h16x(const TcParams &p, int tile, int k,
   int b, y0, x0;
   bool tok;
   tile_origin(p, tile, b, y0, x0, tok);
-  const float *frame0 = p.xin + (long long)(k * K) * p.in_st + (long long)b * p.in_sb;
+  const float *frame0 = p.xin + (long long)(k * (K ? K : p.K)) * p.in_st + (long long)b * p.in_sb;
   for (int row = ptid; row < kHaloRows; row += kProdWarps * 32) {
     const int hy = row / kHaloW, hx = row - (row / kHaloW) * kHaloW;
     const int yi = y0 + hy - p.pad, xi = x0 + hx - p.pad;
@@ -591,17 +626,16 @@ __device__ __forceinline__ void produce_h16x(const TcParams &p, int tile, int k,
     float a[CIN];
 #pragma unroll
     for (int c = 0; c < CIN; ++c) a[c] = 0.f;
+    constexpr int KU = K ? K : kMaxSplitK;  // K == 0: runtime p.K <= 16
 #pragma unroll
-    for (int j = 0; j < K; ++j)
+    for (int j = 0; j < KU; ++j)
+      if (K || j < p.K) {
 #pragma unroll
-      for (int c = 0; c < CIN; ++c) a[c] = fmaf(p.coef[j], ok ? __ldg(src + (long long)j * p.in_st + c) : 0.f, a[c]);
+        for (int c = 0; c < CIN; ++c) a[c] = fmaf(p.coef[j], ok ? __ldg(src + (long long)j * p.in_st + c) : 0.f, a[c]);
+      }
     uint32_t e[CIN];
 #pragma unroll
-    for (int c = 0; c < CIN; ++c) {
-      const __half hi = __float2half_rn(a[c]);
-      const __half lo = __float2half_rn(a[c] - __half2float(hi));
-      e[c] = (uint32_t)__half_as_ushort(hi) | ((uint32_t)__half_as_ushort(lo) << 16);
-    }
+    for (int c = 0; c < CIN; ++c) e[c] = f32_to_h16pair(a[c]);
     const uint4 c0 = split_row_words<CIN>(e[0], e[CIN - 1], p.packed);
     const uint32_t dst = a_stage + (uint32_t)row * 16u;
     ptx::st_shared_v4(dst, c0.x, c0.y, c0.z, c0.w);
@@ -632,6 +666,39 @@ __device__ __forceinline__ void produce_h16s(const TcParams &p, const uint32_t *
       bits[j] = __funnelshift_r(w0, w1, sh);
     }
     const uint4 c0 = split_row_small<K, CIN>(bits, lut, p.packed);
+    const uint32_t dst = a_stage + (uint32_t)row * 16u;
+    ptx::st_shared_v4(dst, c0.x, c0.y, c0.z, c0.w);
+    ptx::st_shared_v4(dst + p.lbo_a, 0u, 0u, 0u, 0u);
+  }
+}
+
+template <int CIN>
+__device__ __forceinline__ void produce_h16s_rt(const TcParams &p, const uint32_t *lut, int tile, int k,
+                                                uint32_t a_stage, int ptid) {
+  int b, y0, x0;
+  bool tok;
+  tile_origin(p, tile, b, y0, x0, tok);
+  const int K = p.K;
+  const uint32_t *frame0 = p.in + (long long)(k * K) * p.in_st + (long long)b * p.in_sb;
+  for (int row = ptid; row < kHaloRows; row += kProdWarps * 32) {
+    const int hy = row / kHaloW, hx = row - (row / kHaloW) * kHaloW;
+    const int yi = y0 + hy - p.pad, xi = x0 + hx - p.pad;
+    const bool ok = tok && yi >= 0 && yi < p.H && xi >= 0 && xi < p.W;
+    const int bit = ok ? xi * CIN : 0, sh = bit & 31;
+    const bool two = ok && sh + CIN > 32;
+    const uint32_t *src = frame0 + (long long)(ok ? yi : 0) * p.wpr_in + (bit >> 5);
+    uint32_t i0 = 0, i1 = 0;
+#pragma unroll
+    for (int j = 0; j < kMaxSplitK; ++j)
+      if (j < K) {
+        const uint32_t w0 = ok ? __ldg(src + (long long)j * p.in_st) : 0u;
+        const uint32_t w1 = two ? __ldg(src + (long long)j * p.in_st + 1) : 0u;
+        const uint32_t bits = __funnelshift_r(w0, w1, sh);
+        i0 |= (bits & 1u) << j;
+        i1 |= ((bits >> 1) & 1u) << j;
+      }
+    const uint32_t e0 = split_lookup(i0, K, lut), e1 = CIN == 2 ? split_lookup(i1, K, lut) : 0u;
+    const uint4 c0 = split_row_words<CIN>(e0, e1, p.packed);
     const uint32_t dst = a_stage + (uint32_t)row * 16u;
     ptx::st_shared_v4(dst, c0.x, c0.y, c0.z, c0.w);
     ptx::st_shared_v4(dst + p.lbo_a, 0u, 0u, 0u, 0u);
@@ -798,6 +865,32 @@ __device__ __forceinline__ void produce_h16s_tma(const TcParams &p, const uint32
   }
 }
 
+template <int CIN>
+__device__ __forceinline__ void produce_h16s_tma_rt(const TcParams &p, const uint32_t *lut,
+                                                    const uint32_t *raw, uint32_t a_stage, int ptid,
+                                                    int x0) {
+  const int bw = p.raw_bw, fstride = kHaloH * p.raw_bw, K = p.K;
+  const int c0w = halo_c0(p, x0) & ~3;
+#pragma unroll 1
+  for (int row = ptid; row < kHaloRows; row += kProdWarps * 32) {
+    const int hy = row / kHaloW, hx = row - hy * kHaloW;
+    const int bitoff = (x0 + hx - p.pad) * CIN - c0w * 32;
+    const uint32_t *src = raw + hy * bw + (bitoff >> 5);
+    const int sh = bitoff & 31;
+    uint32_t i0 = 0, i1 = 0;
+#pragma unroll
+    for (int j = 0; j < kMaxSplitK; ++j)
+      if (j < K) {
+        const uint32_t bits = __funnelshift_r(src[j * fstride], src[j * fstride + 1], sh);
+        i0 |= (bits & 1u) << j;
+        i1 |= ((bits >> 1) & 1u) << j;
+      }
+    const uint32_t e0 = split_lookup(i0, K, lut), e1 = CIN == 2 ? split_lookup(i1, K, lut) : 0u;
+    const uint4 c = split_row_words<CIN>(e0, e1, p.packed);
+    ptx::st_shared_v4(a_stage + (uint32_t)row * 16u, c.x, c.y, c.z, c.w);
+  }
+}
+
 template <int K>
 __device__ __forceinline__ void produce_s32_tma(const TcParams &p, const uint32_t *lut,
                                                 const uint32_t *raw, uint32_t a_stage, int ptid,
@@ -920,16 +1013,21 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
       const uint32_t *raw = reinterpret_cast<const uint32_t *>(smem + p.off_raw + r * p.raw_stage_bytes);
       const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
       const uint32_t *lut = reinterpret_cast<const uint32_t *>(smem + p.off_lut);
-      if (PATH == PATH_HALO)
+      if constexpr (K == 0) {  // runtime group size: split path, C_in <= 2 (envelope)
+        if (PATH == PATH_SPLIT)
+          p.Cin == 1 ? produce_h16s_tma_rt<1>(p, lut, raw, a_stage, ptid, x0)
+                     : produce_h16s_tma_rt<2>(p, lut, raw, a_stage, ptid, x0);
+      } else if (PATH == PATH_HALO) {
         produce_halo_tma<K>(p, raw, a_stage, ptid, x0);
-      else if (PATH == PATH_SPLIT && K > 1)
+      } else if (PATH == PATH_SPLIT) {
         p.Cin == 32 ? produce_s32_tma<K>(p, lut, raw, a_stage, ptid, x0)
                     : (p.Cin == 1 ? produce_h16s_tma<K, 1>(p, lut, raw, a_stage, ptid, x0)
                                   : produce_h16s_tma<K, 2>(p, lut, raw, a_stage, ptid, x0));
-      else if (p.Cin <= 4)
+      } else if (p.Cin <= 4) {
         produce_h16_tma<K, true>(p, raw, a_stage, ptid, x0);
-      else
+      } else {
         produce_h16_tma<K, false>(p, raw, a_stage, ptid, x0);
+      }
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
@@ -956,16 +1054,21 @@ __device__ __forceinline__ void producer_role(const TcParams &p, uint32_t sbase,
       st.next(ns);
       ptx::mbar_wait(bar_a_empty + 8 * s, ph ^ 1u);
       const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
-      if (PATH == PATH_HALO)
-        produce_halo<K>(p, tile, k, a_stage, ptid);
-      else if (PATH == PATH_SPLIT && p.real)
+      if (PATH == PATH_SPLIT && p.real) {
         p.Cin == 1 ? produce_h16x<K, 1>(p, tile, k, a_stage, ptid) : produce_h16x<K, 2>(p, tile, k, a_stage, ptid);
-      else if (PATH == PATH_SPLIT && K > 1)
+      } else if constexpr (K == 0) {  // runtime group size: split path, C_in <= 2 (envelope)
+        if (PATH == PATH_SPLIT)
+          p.Cin == 1 ? produce_h16s_rt<1>(p, lut, tile, k, a_stage, ptid)
+                     : produce_h16s_rt<2>(p, lut, tile, k, a_stage, ptid);
+      } else if (PATH == PATH_HALO) {
+        produce_halo<K>(p, tile, k, a_stage, ptid);
+      } else if (PATH == PATH_SPLIT) {
         p.Cin == 32 ? produce_s32<K>(p, lut, tile, k, a_stage, ptid)
                     : (p.Cin == 1 ? produce_h16s<K, 1>(p, lut, tile, k, a_stage, ptid)
                                   : produce_h16s<K, 2>(p, lut, tile, k, a_stage, ptid));
-      else
+      } else {
         produce_h16<K>(p, tile, k, a_stage, ptid);
+      }
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_cluster_cta(bar_a_full + 8 * s, 0);
@@ -1143,8 +1246,12 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
   const int c = (int)(lane & 7);
   const int co_base = half * NCH;
   const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-  const float vth = p.v_th;
-  const float2 dec2 = make_float2(p.decay, p.decay), nth2 = make_float2(-vth, -vth);
+  // fp16 paths: TMEM holds Y 2^e (the prescaled operands, tc_prepare); the LIF runs in
+  // the scaled state U 2^e with threshold v_th 2^e -- power-of-two scaling commutes with
+  // every fp32 rounding, so spikes and membranes are bitwise those of the unscaled update
+  const float ysc = F16 ? __ldg(p.yscale) : 1.f, iysc = F16 ? __ldg(p.yscale + 1) : 1.f;
+  const float vth = p.v_th, vths = p.v_th * ysc;
+  const float2 dec2 = make_float2(p.decay, p.decay), nth2 = make_float2(-vths, -vths);
   const int G = p.G, Cout = p.Cout, nwo = p.nwo;
   const long long out_st = p.out_st;
   const uint32_t chmask = NCH >= 32 ? 0xFFFFFFFFu : ((1u << NCH) - 1u);
@@ -1180,9 +1287,10 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
         const int cc = ch * 8 + q;
         float v0 = 0.f;
         if (p.v_init && valid && co_base + cc < Cout) v0 = __ldg(p.v_init + vbase + cc);
-        ub[q] = __float_as_uint(v0 - vth);
+        const float u0 = (v0 - vth) * ysc;
+        ub[q] = __float_as_uint(u0);
         if (!UT) {
-          if (q & 1) U[UT ? 0 : cc / 2].y = v0 - vth; else U[UT ? 0 : cc / 2].x = v0 - vth;
+          if (q & 1) U[UT ? 0 : cc / 2].y = u0; else U[UT ? 0 : cc / 2].x = u0;
         }
       }
       if (UT) ptx::tmem_st8(ucol + ch * 8, ub);
@@ -1353,7 +1461,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
         if (valid) {
 #pragma unroll
           for (int q = 0; q < 8; ++q)
-            if (co_base + ch * 8 + q < Cout) p.v_final[vbase + ch * 8 + q] = __uint_as_float(du[q]) + vth;
+            if (co_base + ch * 8 + q < Cout) p.v_final[vbase + ch * 8 + q] = __uint_as_float(du[q]) * iysc + vth;
         }
       }
     }
@@ -1378,7 +1486,10 @@ __device__ __forceinline__ void epilogue_generic(const TcParams &p, uint8_t *sme
   const int c = (int)(lane & 7);              // tile column
   const int co_base = half * NCH;
   const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-  const float decay = p.decay, vth = p.v_th, vres = p.v_reset;
+  // fp16 paths: V, v_th, v_reset in the Y 2^e scale (see epilogue_sr)
+  constexpr bool F16P = PATH != PATH_HALO;
+  const float ysc = F16P ? __ldg(p.yscale) : 1.f, iysc = F16P ? __ldg(p.yscale + 1) : 1.f;
+  const float decay = p.decay, vth = p.v_th * ysc, vres = p.v_reset * ysc;
   const int nsteps = p.nsteps;
   const int G = p.G, K = p.K, mode = p.mode, nwo = p.nwo, Cout = p.Cout, Cp = p.Cout_pad;
   const uint32_t chmask = NCH >= 32 ? 0xFFFFFFFFu : ((1u << NCH) - 1u);
@@ -1414,8 +1525,8 @@ __device__ __forceinline__ void epilogue_generic(const TcParams &p, uint8_t *sme
     for (int cc = 0; cc < NCH; cc += 2) {
       float v0 = 0.f, v1 = 0.f;
       if (p.v_init && valid) {
-        if (co_base + cc < Cout) v0 = __ldg(p.v_init + vbase + cc);
-        if (co_base + cc + 1 < Cout) v1 = __ldg(p.v_init + vbase + cc + 1);
+        if (co_base + cc < Cout) v0 = __ldg(p.v_init + vbase + cc) * ysc;
+        if (co_base + cc + 1 < Cout) v1 = __ldg(p.v_init + vbase + cc + 1) * ysc;
       }
       V[cc / 2] = make_float2(v0, v1);
       if (p.reset == 1) {  // reading R4
@@ -1537,8 +1648,8 @@ __device__ __forceinline__ void epilogue_generic(const TcParams &p, uint8_t *sme
 #pragma unroll
       for (int cc = 0; cc < NCH; cc += 2) {
         const float2 v = V[cc / 2];
-        if (co_base + cc < Cout) p.v_final[vbase + cc] = v.x;
-        if (co_base + cc + 1 < Cout) p.v_final[vbase + cc + 1] = v.y;
+        if (co_base + cc < Cout) p.v_final[vbase + cc] = v.x * iysc;
+        if (co_base + cc + 1 < Cout) p.v_final[vbase + cc + 1] = v.y * iysc;
       }
     }
   }
@@ -1621,9 +1732,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
     ptx::tmem_alloc_cg2(ptx::smem_u32(tmem_slot), p.tmem_cols);
     ptx::tmem_relinquish_cg2();
   }
-  if (p.split) {
+  if (p.split && !p.real) {
     uint32_t *lut_s = reinterpret_cast<uint32_t *>(smem + p.off_lut);
-    for (int i = threadIdx.x; i < (1 << kMaxSplitK); i += kThreads) lut_s[i] = p.lut[i];
+    for (int i = threadIdx.x; i < kLutWords; i += kThreads) lut_s[i] = __ldg(p.lut_g + i);
   }
   for (int i = threadIdx.x; i < 4 * p.Cout_pad; i += kThreads) {
     const float f = p.scale_bias[i];
@@ -1748,7 +1859,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
           case 2: producer_role_tma<PATH, 2>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
           case 3: producer_role_tma<PATH, 3>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
           case 4: producer_role_tma<PATH, 4>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
-          default: producer_role_tma<PATH, 8>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
+          case 8: producer_role_tma<PATH, 8>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
+          default: producer_role_tma<PATH, 0>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
         }
       } else {
         switch (p.K) {
@@ -1756,7 +1868,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
           case 2: producer_role<PATH, 2>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
           case 3: producer_role<PATH, 3>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
           case 4: producer_role<PATH, 4>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
-          default: producer_role<PATH, 8>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
+          case 8: producer_role<PATH, 8>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
+          default: producer_role<PATH, 0>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
         }
       }
     }
@@ -1830,9 +1943,14 @@ static double lif_bias_offset(const tac_conv_lif_desc *d) {
   return ((double)decay - 1.0) * (double)d->v_th;
 }
 
+// Image: [slice 0 | slice 1 | fp32 [s1/254 | bias | s1 | s2] x C_out_pad | fp32 yscale [4] |
+//         u32 aggregate tables [kLutWords] (split path only)]
+static size_t scale_off(const Geometry &g) { return 2 * (size_t)g.w_bytes_cta; }
+static size_t yscale_off(const Geometry &g) { return scale_off(g) + 16 * (size_t)g.cout_pad; }
+static size_t lut_off(const Geometry &g) { return yscale_off(g) + 16; }
 size_t tc_weights_bytes(const tac_conv_lif_desc *d) {
   const Geometry g = geometry(d);
-  return 2 * (size_t)g.w_bytes_cta + 4 * (size_t)g.cout_pad * 4;
+  return lut_off(g) + (g.split ? 4 * (size_t)kLutWords : 0);
 }
 
 // Two int8 slices per output channel, laid out as the smem image of each CTA:
@@ -1867,6 +1985,18 @@ void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bi
     const std::vector<signed char> &q = half ? q2 : q1;
     return q[(((size_t)co * Ci + ci) * 3 + r) * 3 + s];
   };
+  double ysc = 1.0;  // fp16 paths: 2^e (see below); int8 path: 1
+  if (g.path != PATH_HALO) {
+    const int m = (d->mode == TAC_MODE_DENSE || g.split) ? 0 : beta_shift(d->beta);
+    const int Kg = d->mode == TAC_MODE_DENSE ? 1 : d->K;
+    const double agg = g.split ? 1.0 : std::ldexp(1.0, -m * (Kg - 1));
+    double mx = 0.0;
+    for (int co = 0; co < Co; ++co) {
+      for (int i = 0; i < Ci * 9; ++i) mx = std::max(mx, std::fabs((double)weight[(size_t)co * Ci * 9 + i]) * agg);
+      mx = std::max(mx, std::fabs((bias ? (double)bias[co] : 0.0) + boff));
+    }
+    if (mx > 0.0) ysc = std::ldexp(1.0, std::max(-60, std::min(60, -std::ilogb(mx))));
+  }
   for (int half = 0; half < 2; ++half) {
     unsigned char *img = dst + (size_t)half * g.w_bytes_cta;
     std::memset(img, 0, g.w_bytes_cta);
@@ -1892,7 +2022,11 @@ void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bi
       const bool split = g.split != 0;
       const int m = (d->mode == TAC_MODE_DENSE || split) ? 0 : beta_shift(d->beta);
       const int Kg = d->mode == TAC_MODE_DENSE ? 1 : d->K;
-      const double agg = split ? 1.0 : std::ldexp(1.0, -m * (Kg - 1));
+      // layer prescale 2^e: the largest operand |w agg| or |bias + offset| lands in [1, 2),
+      // so the fp16 hi + lo pair keeps ~22 bits of every value relative to the layer's
+      // scale (no absolute 2^-24 quantum, no overflow past 65504); the epilogue runs the
+      // LIF in the same scale (yscale)
+      const double agg = (split ? 1.0 : std::ldexp(1.0, -m * (Kg - 1))) * ysc;
       const int nh = Cp / 2, nk = g.nkc, kbias = split ? 2 * Ci : Ci;
       uint16_t *img16 = reinterpret_cast<uint16_t *>(img);
       if (packed_of(d)) {
@@ -1910,7 +2044,7 @@ void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bi
               double wv = 0.0;
               if (n < Co && part < 2) {
                 if (kk < nw) wv = (double)weight[(((size_t)n * Ci + kk % Ci) * 3 + tap / 3) * 3 + tap % 3] * agg;
-                else if (kk == nw && tap == 4) wv = (bias ? (double)bias[n] : 0.0) + boff;
+                else if (kk == nw && tap == 4) wv = ((bias ? (double)bias[n] : 0.0) + boff) * ysc;
               }
               const __half hi = __double2half(wv);
               const __half v = part == 0 ? hi : __double2half(part == 1 ? wv - (double)__half2float(hi) : 0.0);
@@ -1931,7 +2065,7 @@ void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bi
                 wv = (double)weight[(((size_t)n * Ci + ci) * 3 + tap / 3) * 3 + tap % 3] * agg;
                 hi_only = k >= Ci;
               } else if (k == kbias && tap == 4) {
-                wv = (bias ? (double)bias[n] : 0.0) + boff;
+                wv = ((bias ? (double)bias[n] : 0.0) + boff) * ysc;
               }
             }
             const __half hi = __double2half(wv);
@@ -1944,12 +2078,47 @@ void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bi
     }
   }
   // [s1/254 | bias | s1 | s2] (the kernel multiplies all but bias by 2^{-m(K-1)})
-  float *sb = reinterpret_cast<float *>(dst + 2 * (size_t)g.w_bytes_cta);
+  float *sb = reinterpret_cast<float *>(dst + scale_off(g));
   for (int i = 0; i < Cp; ++i) {
     sb[i] = (float)((double)s1[i] / 254.0);
     sb[Cp + i] = bs[i];
     sb[2 * Cp + i] = s1[i];
     sb[3 * Cp + i] = s2[i];
+  }
+  float *ys = reinterpret_cast<float *>(dst + yscale_off(g));
+  ys[0] = (float)ysc;
+  ys[1] = (float)(1.0 / ysc);
+  ys[2] = ys[3] = 0.f;
+  if (g.split) {
+    // aggregate tables (split path): A = sum_j c_j bit_j with c_j = alpha_j (learnable,
+    // PAPER.md:427) or beta^{K-1-j} (Definition TAC), built in fp64
+    uint32_t *lut = reinterpret_cast<uint32_t *>(dst + lut_off(g));
+    std::memset(lut, 0, 4 * (size_t)kLutWords);
+    const int K = d->mode == TAC_MODE_DENSE ? 1 : d->K;
+    std::vector<double> c(K);
+    for (int j = 0; j < K; ++j)
+      c[j] = d->agg_weights ? (double)d->agg_weights[j] : std::pow((double)d->beta, (double)(K - 1 - j));
+    auto sum_bits = [&](int idx, int j0, int n) {
+      double a = 0.0;
+      for (int j = 0; j < n; ++j)
+        if ((idx >> j) & 1) a += c[j0 + j];
+      return a;
+    };
+    if (K <= 8) {
+      for (int idx = 0; idx < 256; ++idx) {
+        const double a = sum_bits(idx, 0, K);
+        const __half hi = __double2half(a);
+        const __half lo = __double2half(a - (double)__half2float(hi));
+        lut[idx] = (uint32_t)__half_as_ushort(hi) | ((uint32_t)__half_as_ushort(lo) << 16);
+      }
+    } else {  // two fp32 half tables: frames 0..K-9 and K-8..K-1
+      const int ka = K - 8;
+      for (int idx = 0; idx < 256; ++idx) {
+        const float fa = (float)sum_bits(idx, 0, ka), fb = (float)sum_bits(idx, ka, 8);
+        std::memcpy(&lut[256 + idx], &fa, 4);
+        std::memcpy(&lut[512 + idx], &fb, 4);
+      }
+    }
   }
 }
 
@@ -2022,17 +2191,9 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   p.off_lut = g.off_lut;
   p.real = lp.xin ? 1 : 0;
   p.xin = lp.xin;
-  for (int j = 0; j < 8; ++j) p.coef[j] = j < lp.K ? lp.coef[j] : 0.f;
-  if (g.split && !p.real) {  // A = sum_j bit_j beta^{K-1-j} in fp64, as fp16 hi + lo
-    for (int idx = 0; idx < (1 << kMaxSplitK); ++idx) {
-      double a = 0.0;
-      for (int j = 0; j < lp.K && j < kMaxSplitK; ++j)
-        if ((idx >> j) & 1) a += std::pow((double)d->beta, (double)(lp.K - 1 - j));
-      const __half hi = __double2half(a);
-      const __half lo = __double2half(a - (double)__half2float(hi));
-      p.lut[idx] = (uint32_t)__half_as_ushort(hi) | ((uint32_t)__half_as_ushort(lo) << 16);
-    }
-  }
+  for (int j = 0; j < 16; ++j) p.coef[j] = j < lp.K ? lp.coef[j] : 0.f;
+  p.lut_g = reinterpret_cast<const uint32_t *>(tc_prep + lut_off(g));  // split: prepared tables
+  p.yscale = reinterpret_cast<const float *>(tc_prep + yscale_off(g));
   p.wpr_in = lp.wpr_in; p.wpr_out = lp.wpr_out;
   p.nwo = lp.Cout % 32 == 0 ? lp.Cout / 32 : 1;
   const bool out_atomic = g.cout_pad < 64;  // sub-word or shared-word output fields
@@ -2065,7 +2226,7 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   p.in = lp.in; p.out = lp.out; p.v_init = lp.v_init; p.v_final = lp.v_final; p.counts = lp.counts;
   p.trace = tacsnn_trace_buffer();
   p.w_img = tc_prep;
-  p.scale_bias = reinterpret_cast<const float *>(tc_prep + 2 * (size_t)g.w_bytes_cta);
+  p.scale_bias = reinterpret_cast<const float *>(tc_prep + scale_off(g));
 
   cudaStream_t st = (cudaStream_t)stream;
   if (out_atomic || p.counts) {

@@ -24,7 +24,7 @@ RESETS = {"subtract": 0, "delayed": 1, "hard": 2}
 ENGINES = {"auto": 0, "simt": 1, "tcgen05": 2}
 ENGINE_NAMES = {v: k for k, v in ENGINES.items()}
 INPUTS = {"spikes": 0, "real": 1}
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 EXPORTS = ("tac_desc_check", "tac_out_shape", "tac_select_engine", "tac_weights_bytes",
            "tac_prepare_weights", "tac_workspace_bytes", "tac_conv_lif_forward",
@@ -42,7 +42,28 @@ class Desc(ctypes.Structure):
                 ("reset", ctypes.c_int32), ("out_pool", ctypes.c_int32), ("engine", ctypes.c_int32),
                 ("in_stride_t", ctypes.c_int64), ("in_stride_b", ctypes.c_int64),
                 ("out_stride_t", ctypes.c_int64), ("out_stride_b", ctypes.c_int64),
-                ("input_kind", ctypes.c_int32), ("partial_last_group", ctypes.c_int32)]
+                ("input_kind", ctypes.c_int32), ("partial_last_group", ctypes.c_int32),
+                ("agg_weights", ctypes.POINTER(ctypes.c_float))]
+
+
+class Plan(ctypes.Structure):
+    """Mirror of tac_plan (filled by tac_prepare_weights)."""
+    _fields_ = [("prepared", ctypes.c_void_p), ("bytes", ctypes.c_size_t),
+                ("fingerprint", ctypes.c_uint64), ("abi_version", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+class Prepared:
+    """A prepared layer: the device image (torch uint8 tensor, kept alive here) and the
+    host tac_plan that names it."""
+
+    def __init__(self, buf: torch.Tensor, plan: Plan):
+        self.buf = buf
+        self.plan = plan
+
+    @property
+    def device(self):
+        return self.buf.device
 
 
 _lock = threading.Lock()
@@ -65,10 +86,10 @@ def lib():
                 "tac_out_shape": ([D, P, P, P, P], i32),
                 "tac_select_engine": ([D], i32),
                 "tac_weights_bytes": ([D, ctypes.POINTER(sz)], i32),
-                "tac_prepare_weights": ([D, P, P, P, sz, P], i32),
+                "tac_prepare_weights": ([D, P, P, P, sz, P, ctypes.POINTER(Plan)], i32),
                 "tac_workspace_bytes": ([D, ctypes.POINTER(sz)], i32),
-                "tac_conv_lif_forward": ([D, P, P, P, P, P, P, P, sz, P], i32),
-                "tac_conv_lif_forward_real": ([D, P, P, P, P, P, P, P, sz, P], i32),
+                "tac_conv_lif_forward": ([D, ctypes.POINTER(Plan), P, P, P, P, P, P, sz, P], i32),
+                "tac_conv_lif_forward_real": ([D, ctypes.POINTER(Plan), P, P, P, P, P, P, sz, P], i32),
                 "tac_pack_spikes": ([P, P, i32, i32, i32, i32, i32, P], i32),
                 "tac_unpack_spikes": ([P, P, i32, i32, i32, i32, i32, P], i32),
                 "tac_status_string": ([i32], ctypes.c_char_p),
@@ -114,16 +135,24 @@ class LayerSpec:
     engine: str = "auto"
     input: str = "spikes"     # "real": continuous-valued fp32 input frames (tac_conv_lif_forward_real)
     partial: bool = False     # K need not divide T: ceil(T/K) groups, the last one short
+    agg_weights: tuple | None = None  # learnable aggregation weights alpha_j (K floats)
 
     def replace(self, **kw) -> "LayerSpec":
         return dataclasses.replace(self, **kw)
 
     def desc(self, in_strides=(0, 0), out_strides=(0, 0)) -> Desc:
-        return Desc(self.T, self.B, self.C_in, self.H, self.W, self.C_out, self.R, self.S,
-                    self.stride, self.pad, 1 if self.mode == "dense" else self.K,
-                    MODES[self.mode], self.beta, self.v_th, self.v_reset, RESETS[self.reset],
-                    self.out_pool, ENGINES[self.engine], in_strides[0], in_strides[1],
-                    out_strides[0], out_strides[1], INPUTS[self.input], int(self.partial))
+        alpha = None
+        if self.agg_weights is not None:
+            assert len(self.agg_weights) == self.K, "agg_weights needs K entries"
+            alpha = (ctypes.c_float * self.K)(*self.agg_weights)
+        d = Desc(self.T, self.B, self.C_in, self.H, self.W, self.C_out, self.R, self.S,
+                 self.stride, self.pad, 1 if self.mode == "dense" else self.K,
+                 MODES[self.mode], self.beta, self.v_th, self.v_reset, RESETS[self.reset],
+                 self.out_pool, ENGINES[self.engine], in_strides[0], in_strides[1],
+                 out_strides[0], out_strides[1], INPUTS[self.input], int(self.partial),
+                 ctypes.cast(alpha, ctypes.POINTER(ctypes.c_float)) if alpha is not None else None)
+        d._alpha_keepalive = alpha
+        return d
 
     @property
     def conv_hw(self):
@@ -163,8 +192,8 @@ def _ptr(t):
 
 
 def prepare_weights(spec: LayerSpec, weight: torch.Tensor, bias: torch.Tensor | None = None,
-                    device="cuda") -> torch.Tensor:
-    """Build the device prepared-weights buffer (tac_prepare_weights)."""
+                    device="cuda") -> Prepared:
+    """Build the device image and its tac_plan (tac_prepare_weights)."""
     d = spec.desc()
     nbytes = ctypes.c_size_t()
     _check(lib().tac_weights_bytes(ctypes.byref(d), ctypes.byref(nbytes)))
@@ -174,12 +203,13 @@ def prepare_weights(spec: LayerSpec, weight: torch.Tensor, bias: torch.Tensor | 
     buf = torch.empty(nbytes.value + 256, dtype=torch.uint8, device=device)
     off = (-buf.data_ptr()) % 256
     prep = buf[off:off + nbytes.value]
+    plan = Plan()
     _check(lib().tac_prepare_weights(ctypes.byref(d), _ptr(w), _ptr(b), _ptr(prep),
-                                     nbytes.value, _stream(prep.device)))
-    return prep
+                                     nbytes.value, _stream(prep.device), ctypes.byref(plan)))
+    return Prepared(prep, plan)
 
 
-def conv_lif(spec: LayerSpec, prepared: torch.Tensor, x: torch.Tensor, *, v_init=None,
+def conv_lif(spec: LayerSpec, prepared: Prepared, x: torch.Tensor, *, v_init=None,
              want_v_final=False, want_counts=True, out: torch.Tensor | None = None):
     """Run one layer (tac_conv_lif_forward) on the current stream.
 
@@ -191,12 +221,19 @@ def conv_lif(spec: LayerSpec, prepared: torch.Tensor, x: torch.Tensor, *, v_init
     """
     real = spec.input == "real"
     if real:
-        assert x.is_cuda and x.dtype == torch.float32 and x.dim() == 5
-        assert x.shape[2:] == (spec.H, spec.W, spec.C_in)
-        assert x.stride(4) == 1 and x.stride(3) == spec.C_in and x.stride(2) == spec.W * spec.C_in
+        if not (x.is_cuda and x.dtype == torch.float32 and x.dim() == 5):
+            raise ValueError("real input: fp32 cuda tensor [T, B, H, W, C_in]")
+        if tuple(x.shape) != (spec.T, spec.B, spec.H, spec.W, spec.C_in):
+            raise ValueError(f"x shape {tuple(x.shape)} != {(spec.T, spec.B, spec.H, spec.W, spec.C_in)}")
+        if not (x.stride(4) == 1 and x.stride(3) == spec.C_in and x.stride(2) == spec.W * spec.C_in):
+            raise ValueError("each (t, b) plane of x must be contiguous")
     else:
-        assert x.is_cuda and x.dtype == torch.int32 and x.dim() == 4
-        assert x.stride(3) == 1 and x.stride(2) == spec.in_words_per_row, "rows must be packed"
+        if not (x.is_cuda and x.dtype == torch.int32 and x.dim() == 4):
+            raise ValueError("spikes: packed int32 cuda tensor [T, B, H, WPR]")
+        if tuple(x.shape) != (spec.T, spec.B, spec.H, spec.in_words_per_row):
+            raise ValueError(f"x shape {tuple(x.shape)} != {(spec.T, spec.B, spec.H, spec.in_words_per_row)}")
+        if not (x.stride(3) == 1 and x.stride(2) == spec.in_words_per_row):
+            raise ValueError("rows must be packed")
     T_out, Ho, Wo, wpr = spec.out_shape()
     if out is None:
         out = torch.empty((T_out, spec.B, Ho, wpr), dtype=torch.int32, device=x.device)
@@ -214,7 +251,7 @@ def conv_lif(spec: LayerSpec, prepared: torch.Tensor, x: torch.Tensor, *, v_init
     _check(lib().tac_workspace_bytes(ctypes.byref(d), ctypes.byref(wsb)))
     ws = torch.empty(wsb.value, dtype=torch.uint8, device=x.device) if wsb.value else None
     fwd = lib().tac_conv_lif_forward_real if real else lib().tac_conv_lif_forward
-    _check(fwd(ctypes.byref(d), _ptr(prepared), _ptr(x), _ptr(v_init), _ptr(out), _ptr(v_final),
+    _check(fwd(ctypes.byref(d), ctypes.byref(prepared.plan), _ptr(x), _ptr(v_init), _ptr(out), _ptr(v_final),
                _ptr(counts), _ptr(ws), wsb.value, _stream(x.device)))
     return out, v_final, counts
 

@@ -1,7 +1,7 @@
 """Parity helpers: run a layer through the C ABI and check it against the oracle
 with the replay protocol.
 
-  * spikes: bit-exact wherever |V - v_th| > band (1e-3, north_star); inside the
+  * spikes: bit-exact wherever |V - v_th| > band (1e-3 v_th, north_star; reading D9); inside the
     band the oracle takes the device's decision (excused) and continues, so
     after a zero-mismatch replay the oracle's own output equals the device's.
   * v_final: |V_dev - V_oracle| <= 1e-3 * max(|V_oracle|, v_th) elementwise.
@@ -43,7 +43,7 @@ def check_layer(T, O, spec, S_u8: np.ndarray, w, b, *, x_packed=None, v_init=Non
                   beta=s1.beta, v_th=s1.v_th, v_reset=s1.v_reset, reset=s1.reset,
                   stride=s1.stride, pad=s1.pad, partial=s1.partial,
                   v_init=None if v_init is None else v_init.astype(np.float32).astype(np.float64),
-                  replay=D, band=BAND)
+                  replay=D, band=BAND * s1.v_th, alpha=s1.agg_weights)
     assert r["mismatch"] == 0, f"{label}: {r['mismatch']} out-of-band spike mismatches " \
                                f"({r['excused']} excused of {D.size})"
     assert np.array_equal(r["out"], D)

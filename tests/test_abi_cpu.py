@@ -31,7 +31,7 @@ def test_exports_every_declared_symbol(T):
     for name in decl:
         assert hasattr(L, name), f"{name} declared in include/tacsnn.h but not exported"
     assert set(decl) == set(T.EXPORTS)
-    assert T.abi_version() == T.ABI_VERSION == 2
+    assert T.abi_version() == T.ABI_VERSION == 3
 
 
 def test_status_strings(T):

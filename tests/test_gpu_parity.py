@@ -207,7 +207,7 @@ def test_real_input_rejects_spike_call(T):
     x = T.pack(torch.zeros((4, 1, 2, 8, 8), dtype=torch.uint8, device="cuda"))
     d = spec.desc()
     out = torch.empty((2, 1, 4, 16), dtype=torch.int32, device="cuda")
-    st = T.lib().tac_conv_lif_forward(ctypes.byref(d), ctypes.c_void_p(prep.data_ptr()),
+    st = T.lib().tac_conv_lif_forward(ctypes.byref(d), ctypes.byref(prep.plan),
                                       ctypes.c_void_p(x.data_ptr()), None,
                                       ctypes.c_void_p(out.data_ptr()), None, None, None, 0, None)
     assert st == 4 and b"tac_conv_lif_forward_real" in T.lib().tac_last_error_detail()
@@ -326,6 +326,148 @@ def test_exhaustive_tiny_batch(T, O, engine):
         P.check_layer(T, O, spec, S, w, b, label=f"exhaustive/{mode}/{engine}")
 
 
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("reset", ["subtract", "delayed", "hard"])
+@pytest.mark.parametrize("mode", ["dense", "tac", "tactp"])
+def test_exhaustive_batch_bitwise_vs_bruteforce(T, mode, reset, engine):
+    """P9, device vs the independent brute force (tests/bruteforce.py) on all 2^16 inputs:
+    weights n/64 with max |n| = 127 are exact in both tensor-core operand formats (int8
+    slice step max|w|/127 = 1/64; fp16), beta = 1/2 and the small binary fractions keep every
+    sum exact in fp32 -- so spikes, counts and v_final must agree BITWISE, no band."""
+    import bruteforce
+    bits = np.array(list(itertools.product([0, 1], repeat=16)), np.uint8)
+    S = np.ascontiguousarray(bits.reshape(-1, 4, 1, 2, 2).transpose(1, 0, 2, 3, 4))
+    rng = np.random.default_rng(11)
+    n = rng.integers(-100, 101, (16, 1, 3, 3))
+    n[:, 0, 1, 1] = 127                                        # max |n| = 127 in every channel
+    w = torch.from_numpy((n / 64.0).astype(np.float32) * 0.5)  # 0.5 n/64 = n/128: still exact
+    b = torch.from_numpy((rng.integers(-4, 5, 16) / 16.0).astype(np.float32))
+    spec = T.LayerSpec(T=4, B=S.shape[1], C_in=1, H=2, W=2, C_out=16, pad=1, K=2, mode=mode,
+                       beta=0.5, v_reset=-0.25, reset=reset, out_pool=1)
+    spec = _engine_or_skip(spec, engine)
+    prep = T.prepare_weights(spec, w, b)
+    out, vf, cnt = T.conv_lif(spec, prep, T.pack(torch.from_numpy(S).cuda()), want_v_final=True)
+    torch.cuda.synchronize()
+    ref, V = bruteforce.layer(S, w.numpy(), b.numpy(), K=2, mode=mode, beta=0.5, v_th=1.0,
+                              reset=reset, v_reset=-0.25, pad=1)
+    from oracle import oracle as O
+    D = O.unpack_spikes(P.to_u32(out), 16, 2)
+    assert 0.02 < ref.mean() < 0.98
+    assert np.array_equal(D, ref)
+    assert np.array_equal(vf.cpu().numpy().transpose(0, 3, 1, 2).astype(np.float64), V)
+    assert np.array_equal(cnt.cpu().numpy().astype(np.int64), ref.sum(axis=(0, 3, 4)))
+
+
+def test_plan_mismatch_refused(T):
+    """tac_plan: weights prepared for TAC and run as TAC-TP (different folded bias and
+    aggregate scale) are refused with TAC_ERR_PARAM before any launch; a batch shard of the
+    same layer (different B) is accepted."""
+    spec = T.LayerSpec(T=8, B=4, C_in=32, H=12, W=12, C_out=32, pad=1, K=4, mode="tac", beta=0.5)
+    prep = T.prepare_weights(spec, *_w(2, 32, 32, 1.0))
+    x = T.pack(torch.zeros((8, 4, 32, 12, 12), dtype=torch.uint8, device="cuda"))
+    for bad in (spec.replace(mode="tactp"), spec.replace(K=2), spec.replace(beta=0.25),
+                spec.replace(v_th=2.0), spec.replace(reset="hard"), spec.replace(pad=0),
+                spec.replace(agg_weights=(0.125, 0.25, 0.5, 1.0))):
+        with pytest.raises(RuntimeError, match="TAC_ERR_PARAM.*different descriptor"):
+            T.conv_lif(bad, prep, x if bad.pad == 1 else x)
+    T.conv_lif(spec.replace(B=2), prep, x[:, :2])       # batch shard: same image
+    T.conv_lif(spec.replace(T=4), prep, x[:4])           # chunked sequence: same image
+    torch.cuda.synchronize()
+
+
+ALPHA_CASES = [
+    # learnable aggregation weights alpha_j (PAPER.md:427): split (table) path on tcgen05
+    ("c1", (8, 3, 1, 28, 28, 32, 0, 2), 2.5),
+    ("c2", (8, 2, 2, 32, 32, 128, 1, 2), 6.0),
+    ("c32", (8, 2, 32, 12, 16, 64, 1, 2), 2.5),
+    ("c128_simt", (8, 2, 128, 8, 8, 128, 1, 2), 3.0),   # outside the split envelope: SIMT
+]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("mode,K,alpha", [("tac", 4, (0.3, -0.2, 1.1, 0.7)),
+                                          ("tactp", 2, (0.45, 0.9)),
+                                          ("tac", 8, (0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8))])
+@pytest.mark.parametrize("case", ALPHA_CASES, ids=[c[0] for c in ALPHA_CASES])
+def test_agg_weights_parity(T, O, case, mode, K, alpha, engine):
+    name, (Tn, B, Cin, H, W, Cout, pad, pool), gain = case
+    spec = T.LayerSpec(T=Tn, B=B, C_in=Cin, H=H, W=W, C_out=Cout, pad=pad, K=K, mode=mode,
+                       beta=0.9, out_pool=pool, agg_weights=alpha)
+    if name.endswith("simt") and engine == "tcgen05":
+        with pytest.raises(RuntimeError):
+            spec.replace(engine="tcgen05").engine_used()
+        return
+    spec = _engine_or_skip(spec, engine)
+    S = _spikes(zlib.crc32(name.encode()) % 983, (Tn, B, Cin, H, W), 0.15)
+    w, b = _w(16, Cout, Cin, gain)
+    _, _, st = P.check_layer(T, O, spec, S, w, b, label=f"alpha/{name}/{mode}/K{K}/{engine}")
+    assert 0.0 < st["rate"] < 0.95, st
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("mode", ["tac", "tactp"])
+def test_agg_weights_partial_last_group(T, O, mode, engine):
+    """T = 10, K = 4 with alpha: the short group (2 frames) uses alpha_2, alpha_3 (reading R11)."""
+    spec = T.LayerSpec(T=10, B=2, C_in=2, H=24, W=24, C_out=64, pad=1, K=4, mode=mode, beta=0.9,
+                       out_pool=2, partial=True, agg_weights=(0.2, 0.4, -0.3, 0.9))
+    spec = _engine_or_skip(spec, engine)
+    S = _spikes(77, (10, 2, 2, 24, 24), 0.2)
+    w, b = _w(17, 64, 2, 5.0)
+    _, _, st = P.check_layer(T, O, spec, S, w, b, label=f"alpha-partial/{mode}/{engine}")
+    assert 0.0 < st["rate"] < 0.95, st
+
+
+RUNTIME_K = [5, 6, 7, 9, 12, 16]
+
+
+@pytest.mark.parametrize("beta", [0.9, 0.5])
+@pytest.mark.parametrize("K", RUNTIME_K)
+@pytest.mark.parametrize("cin", [1, 2])
+def test_runtime_group_size_on_tcgen05(T, O, cin, K, beta):
+    """Any K <= 16 on the first layers (split table path, runtime-K producers; K > 8 uses the
+    two fp32 half tables): TAC (and TAC-TP for K <= 8) against the oracle."""
+    Tn = 2 * K
+    H, W, Cout = (28, 28, 32) if cin == 1 else (32, 32, 128)
+    for mode in (["tac", "tactp"] if K <= 8 else ["tac"]):
+        spec = T.LayerSpec(T=Tn, B=2, C_in=cin, H=H, W=W, C_out=Cout, pad=0 if cin == 1 else 1,
+                           K=K, mode=mode, beta=beta, out_pool=2, engine="tcgen05")
+        assert spec.engine_used() == "tcgen05"
+        S = _spikes(K * 10 + cin, (Tn, 2, cin, H, W), 0.12)
+        w, b = _w(18, Cout, cin, 2.0 if mode == "tac" else 1.0)
+        _, _, st = P.check_layer(T, O, spec, S, w, b, label=f"K{K}/{cin}/{mode}/b{beta}")
+        assert 0.0 < st["rate"] < 0.95, st
+
+
+@pytest.mark.parametrize("K", [16, 8, 4])
+def test_mnist_T25_on_tcgen05(T, O, K):
+    """The paper's MNIST setting T = 25 with K = 4/8/16: partial last
+    groups (K' = 1, 1, 9), every layer of the C2-shaped stack on the tensor cores."""
+    from paper_2603_13810_b200 import configs
+    cfg = configs.CONFIGS["C2"]
+    specs = configs.layer_plan(cfg, mode="tac", K=K, B=3, T=25)
+    assert all(s.engine_used() == "tcgen05" for s in specs), [s.engine_used() for s in specs]
+    S = configs.make_inputs(cfg, B=3, T=25).numpy()
+    stats = P.check_stack(T, O, specs, configs.layer_weights(cfg), S, label=f"C2@T25/K{K}")
+    assert stats[0]["rate"] > 0.0
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("scale", [1e-4, 1.0, 300.0])
+def test_fp16_operand_prescale(T, O, scale, engine):
+    """The fp16 operand paths prescale the layer by 2^e (tc_prepare): weights, bias and v_th
+    scaled together by `scale` (far from 1 both ways) give the same spikes as scale 1, and
+    parity with the oracle holds (no absolute 2^-24 quantum, no fp16 overflow)."""
+    for cin, beta, K in ((2, 0.5, 4), (1, 0.9, 4)):
+        spec = T.LayerSpec(T=8, B=2, C_in=cin, H=20, W=20, C_out=32, pad=1, K=K, mode="tactp",
+                           beta=beta, v_th=scale, v_reset=0.0, out_pool=1)
+        spec = _engine_or_skip(spec, engine)
+        w, b = _w(19, 32, cin, 4.0)
+        S = _spikes(5 + cin, (8, 2, cin, 20, 20), 0.2)
+        _, _, st = P.check_layer(T, O, spec, S, w * scale, b * scale,
+                                 label=f"prescale/{scale}/{cin}/{engine}")
+        assert 0.0 < st["rate"] < 0.95, st
+
+
 def test_shard_invariance(T):
     """P13: a batch-shard view gives bitwise the same per-sample outputs."""
     spec = T.LayerSpec(T=8, B=6, C_in=128, H=16, W=16, C_out=128, pad=1, K=4, mode="tactp",
@@ -357,7 +499,7 @@ def test_errors_launch_nothing(T):
     import ctypes
     d = spec.desc()
     out = torch.empty((2, 2, 8, 4), dtype=torch.int32, device="cuda")
-    st = T.lib().tac_conv_lif_forward(ctypes.byref(d), ctypes.c_void_p(prep.data_ptr()),
+    st = T.lib().tac_conv_lif_forward(ctypes.byref(d), ctypes.byref(prep.plan),
                                       ctypes.c_void_p(xc.data_ptr()), None,
                                       ctypes.c_void_p(out.data_ptr()), None, None, None, 0, None)
     assert st == 4 and b"not device memory" in T.lib().tac_last_error_detail()

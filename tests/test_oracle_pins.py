@@ -43,7 +43,8 @@ def test_golden_scalar_cases(oracle_mod, case):
     bias = None if case["bias"] is None else np.array([case["bias"]], np.float32)
     r = oracle_mod.forward(S, W, bias, K=case["K"], mode=case["mode"], beta=case["beta"],
                            v_th=case["v_th"], v_reset=case.get("v_reset", 0.0),
-                           reset=case["reset"], pad=0)
+                           reset=case["reset"], pad=0, partial=case.get("partial", False),
+                           alpha=case.get("alpha"))
     assert r["out"].ravel().tolist() == case["out"]
     assert r["v_final"].ravel()[0] == pytest.approx(case["v_final"], abs=1e-12)
     assert int(r["counts"].sum()) == sum(case["out"])
@@ -397,3 +398,48 @@ def test_partial_groups_paper_T25(oracle_mod):
     assert steps == [7, 4, 2]
     with pytest.raises(ValueError):
         oracle_mod.forward(S, W, K=4, mode="tac", pad=1)   # K must divide T without partial
+
+
+# --- P9: exhaustive batch, oracle vs an independent brute force ---------------
+def _exhaustive_inputs():
+    """Every binary input of a 1-channel 2x2 image over T = 4 steps: [4, 65536, 1, 2, 2]."""
+    bits = np.array(list(itertools.product([0, 1], repeat=16)), np.uint8)
+    return np.ascontiguousarray(bits.reshape(-1, 4, 1, 2, 2).transpose(1, 0, 2, 3, 4))
+
+
+@pytest.mark.parametrize("reset", RESETS)
+@pytest.mark.parametrize("mode", ["dense", "tac", "tactp"])
+def test_exhaustive_batch_bruteforce(oracle_mod, mode, reset):
+    """SURVEY P9 on CPU: all 2^16 inputs in one batch; binary-exact weights, bias, beta and
+    v_reset make every value exact in fp64, so the C oracle and the brute force
+    (tests/bruteforce.py: loops straight from Eq. (1) / Alg. 1 / Alg. 2) must agree bitwise."""
+    import bruteforce
+    S = _exhaustive_inputs()
+    rng = np.random.default_rng(9)
+    W = (rng.integers(-24, 25, (4, 1, 3, 3)) / 16.0).astype(np.float32)
+    b = (rng.integers(-2, 3, 4) / 16.0).astype(np.float32)
+    kw = dict(K=2, mode=mode, beta=0.5, v_th=1.0, reset=reset, v_reset=-0.25)
+    r = oracle_mod.forward(S, W, b, pad=1, **kw)
+    out, V = bruteforce.layer(S, W, b, pad=1, **kw)
+    assert 0.02 < out.mean() < 0.98
+    assert np.array_equal(r["out"], out)
+    assert np.array_equal(r["v_final"], V)
+    assert np.array_equal(r["counts"], out.sum(axis=(0, 3, 4)))
+
+
+@pytest.mark.parametrize("mode", ["tac", "tactp"])
+def test_agg_weights_equal_default_when_alpha_is_beta_powers(oracle_mod, mode):
+    """alpha_j = beta^{K-1-j} (binary-exact at beta = 1/2) reproduces the default
+    aggregation bitwise; alpha scaled by 2 with W halved is the same layer (linearity)."""
+    rng = np.random.default_rng(4)
+    S = _rand_spikes(rng, (6, 2, 2, 7, 7), 0.3)
+    W = (rng.integers(-24, 25, (3, 2, 3, 3)) / 32.0).astype(np.float32)
+    kw = dict(K=3, mode=mode, beta=0.5, v_th=1.0, pad=1)
+    d = oracle_mod.forward(S, W, None, **kw)
+    a = oracle_mod.forward(S, W, None, alpha=[0.25, 0.5, 1.0], **kw)
+    h = oracle_mod.forward(S, W / 2, None, alpha=[0.5, 1.0, 2.0], **kw)
+    assert d["out"].sum() > 0
+    for r in (a, h):
+        assert np.array_equal(r["out"], d["out"]) and np.array_equal(r["v_final"], d["v_final"])
+    o = oracle_mod.forward(S, W, None, alpha=[1.0, 0.5, 0.25], **kw)   # reversed: a different layer
+    assert not np.array_equal(o["v_final"], d["v_final"])
