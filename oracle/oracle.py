@@ -59,6 +59,9 @@ def lib():
             L.tac_oracle_or_pool2.argtypes = [P, i, i, i, i, P]
             L.tac_oracle_or_pool2.restype = i
             L.tac_oracle_threads.restype = i
+            L.tac_oracle_backward.argtypes = [P, P, P, P, P] + [i] * 12 + [d, d, i, d, i] + \
+                [P, P, d, P, P, P, P, P, P, P]
+            L.tac_oracle_backward.restype = i
             L.tac_oracle_set_threads.argtypes = [i]
             L.tac_oracle_set_threads.restype = None
             _lib = L
@@ -155,6 +158,53 @@ def forward(S, Wt, bias=None, *, K=1, mode="tac", beta=0.9, v_th=1.0, v_reset=0.
         raise ValueError("tac_oracle_forward rejected its arguments")
     return dict(out=out, v_final=v_final, counts=counts, mismatch=int(mism[0]),
                 excused=int(exc[0]))
+
+
+SURROGATES = {"fast_sigmoid": 0, "arctan": 1}
+
+
+def backward(S, Wt, bias, g_out, *, K=1, mode="tac", beta=0.9, v_th=1.0, stride=1, pad=0,
+             surrogate="fast_sigmoid", sg_alpha=25.0, detach_reset=False, v_init=None,
+             g_vfinal=None, replay=None, band=1e-3, alpha=None, want_input=True):
+    """Surrogate-gradient BPTT of one Conv-LIF layer (subtract reset; see the
+    backward section of tac_oracle.c for the equations and citations).
+    S: u8 spikes or float frames [T,B,Cin,H,W]; g_out fp64 [T_out,B,Cout,Ho,Wo] = dL/ds.
+    Returns dict(g_W [Cout,Cin,R,S], g_b [Cout], g_in [T,B,Cin,H,W] or None,
+    g_vinit [B,Cout,Ho,Wo], g_alpha [K] or None), all fp64."""
+    real = np.issubdtype(np.asarray(S).dtype, np.floating)
+    S = np.ascontiguousarray(S, dtype=np.float64 if real else np.uint8)
+    Wt = np.ascontiguousarray(Wt, dtype=np.float32)
+    bias = None if bias is None else np.ascontiguousarray(bias, dtype=np.float32)
+    T, B, Cin, H, W = S.shape
+    Cout, _, R, Sk = Wt.shape
+    m = MODES[mode]
+    if m == 0:
+        K = 1
+    Ho, Wo = out_hw(H, W, R, Sk, stride, pad)
+    g_out = np.ascontiguousarray(g_out, dtype=np.float64)
+    g_W = np.empty((Cout, Cin, R, Sk))
+    g_b = np.empty(Cout)
+    g_in = np.empty((T, B, Cin, H, W)) if want_input else None
+    g_vinit = np.empty((B, Cout, Ho, Wo))
+    g_alpha = np.empty(K) if alpha is not None else None
+    if alpha is not None:
+        alpha = np.ascontiguousarray(np.asarray(alpha, np.float32).astype(np.float64))
+    if v_init is not None:
+        v_init = np.ascontiguousarray(v_init, dtype=np.float64)
+    if g_vfinal is not None:
+        g_vfinal = np.ascontiguousarray(g_vfinal, dtype=np.float64)
+    if replay is not None:
+        replay = np.ascontiguousarray(replay, dtype=np.uint8)
+    f32 = lambda v: float(np.float32(v))
+    rc = lib().tac_oracle_backward(
+        None if real else _ptr(S), _ptr(S) if real else None, _ptr(alpha), _ptr(Wt), _ptr(bias),
+        T, B, Cin, H, W, Cout, R, Sk, stride, pad, K, m, f32(beta), f32(v_th),
+        SURROGATES[surrogate], float(sg_alpha), int(bool(detach_reset)), _ptr(v_init), _ptr(replay),
+        float(band), _ptr(g_out), _ptr(g_vfinal), _ptr(g_W), _ptr(g_b), _ptr(g_in), _ptr(g_vinit),
+        _ptr(g_alpha))
+    if rc != 0:
+        raise ValueError("tac_oracle_backward rejected its arguments")
+    return dict(g_W=g_W, g_b=g_b, g_in=g_in, g_vinit=g_vinit, g_alpha=g_alpha)
 
 
 def or_pool2(x):

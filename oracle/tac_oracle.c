@@ -275,3 +275,164 @@ int tac_oracle_or_pool2(const uint8_t *in, int N, int C, int H, int W, uint8_t *
         }
   return 0;
 }
+
+/* ------------------------------------------------------------------------
+ * Backward pass: surrogate-gradient BPTT through the grouped LIF (SURVEY.md
+ * 8(f) #3).  The paper trains every network it reports with backpropagation
+ * through time and a surrogate spike derivative (App. E P:587-588:
+ * fast sigmoid slope 25 for MNIST/FMNIST, arctan alpha 2 with a detached reset
+ * for DVS-Gesture).  Subtract reset only (the reset the paper trains with).
+ *
+ * Forward (recomputed here in fp64, the order of Alg. 1 / Alg. 2 / Eq. (1)):
+ *   A_k = sum_j a_j S_{kK+j} ;  Y_k = conv(A_k) + b
+ *   per LIF step t of group k:  V_t = decay U_{t-1} + Y_k ;  s_t = Theta(V_t - v_th) ;
+ *                               U_t = V_t - v_th s_t           (U_{-1} = v_init)
+ * Surrogate: ds_t/dV_t := h(V_t - v_th) with
+ *   fast sigmoid: h(u) = 1 / (alpha |u| + 1)^2          (snnTorch fast_sigmoid, slope alpha)
+ *   arctan      : h(u) = (alpha/2) / (1 + (pi/2 alpha u)^2)   (snnTorch atan)
+ * Detached reset: dU_t/dV_t = 1 (the reset term carries no gradient); otherwise
+ * dU_t/dV_t = 1 - v_th h.
+ * Backward, t = S-1 .. 0, gU = dL/dU_{S-1} = g_vfinal (0 if NULL):
+ *   dV_t = (g_out_t - [!detach] v_th gU) h_t + gU ;  gY_k += dV_t ;  gU <- decay dV_t
+ *   g_vinit = gU ;  g_b += sum_pixels gY_k ;  g_W += corr(gY_k, A_k) ;
+ *   gA_k = conv^T(gY_k, W) ;  g_in_{kK+j} = a_j gA_k ;  g_alpha_j += <gA_k, S_{kK+j}>
+ * Replay: as forward (device spikes inside the band), so the trajectory the
+ * gradient is taken along is the device's.
+ *   g_out   : fp64 [S][B][Cout][Ho][Wo] (dL/ds per output step; S = T_out)
+ *   outputs : g_W [Cout][Cin][R][Sk], g_b [Cout] (overwritten); g_in [T][B][Cin][H][W],
+ *             g_vinit [B][Cout][Ho][Wo], g_alpha [K]: each may be NULL.
+ * K must divide T (no partial groups).  Returns 0 or -1.
+ * ------------------------------------------------------------------------ */
+static double surrogate(int kind, double a, double u) {
+  if (kind == 0) {
+    const double d = a * fabs(u) + 1.0;
+    return 1.0 / (d * d);
+  }
+  const double z = 1.5707963267948966 * a * u;
+  return 0.5 * a / (1.0 + z * z);
+}
+
+int tac_oracle_backward(const uint8_t *S, const double *X, const double *alpha,
+                        const float *Wt, const float *bias,
+                        int T, int B, int Cin, int H, int W, int Cout, int R, int Sk,
+                        int stride, int pad, int K, int mode, double beta, double v_th,
+                        int sg_kind, double sg_alpha, int detach,
+                        const double *v_init, const uint8_t *replay, double band,
+                        const double *g_out, const double *g_vfinal,
+                        double *g_W, double *g_b, double *g_in, double *g_vinit, double *g_alpha) {
+  if ((S == NULL) == (X == NULL) || !g_out || !g_W || !g_b) return -1;
+  if (mode == OR_MODE_DENSE) K = 1;
+  if (K < 1 || T < 1 || T % K != 0) return -1;
+  const int Ho = (H + 2 * pad - R) / stride + 1, Wo = (W + 2 * pad - Sk) / stride + 1;
+  if (Ho < 1 || Wo < 1) return -1;
+  const int G = T / K;
+  const int ns = (mode == OR_MODE_TACTP) ? K : 1;
+  const int Sout = G * ns;
+  const double decay = (mode == OR_MODE_TAC) ? pow(beta, (double)K) : beta;
+  const size_t nin = (size_t)Cin * H * W, nout = (size_t)Cout * Ho * Wo, nw = (size_t)Cout * Cin * R * Sk;
+  double *aj = (double *)malloc((size_t)K * sizeof(double));
+  for (int j = 0; j < K; ++j)
+    aj[j] = (alpha && mode != OR_MODE_DENSE) ? alpha[j] : pow(beta, (double)(K - 1 - j));
+  for (size_t i = 0; i < nw; ++i) g_W[i] = 0.0;
+  for (int co = 0; co < Cout; ++co) g_b[co] = 0.0;
+  if (g_alpha) for (int j = 0; j < K; ++j) g_alpha[j] = 0.0;
+  int rc = 0;
+  for (int b = 0; b < B; ++b) {   /* sequential over samples: the gradients are sums over b */
+    double *A = (double *)malloc((size_t)G * nin * sizeof(double));
+    double *Vp = (double *)malloc((size_t)Sout * nout * sizeof(double));
+    double *Y = (double *)malloc(nout * sizeof(double));
+    double *gY = (double *)malloc((size_t)G * nout * sizeof(double));
+    double *gU = (double *)malloc(nout * sizeof(double));
+    double *U = (double *)malloc(nout * sizeof(double));
+    double *gA = (double *)malloc(nin * sizeof(double));
+    if (!A || !Vp || !Y || !gY || !gU || !U || !gA) { rc = -1; goto done_b; }
+    /* forward recompute */
+    for (size_t n = 0; n < nout; ++n) U[n] = v_init ? v_init[(size_t)b * nout + n] : 0.0;
+    for (int k = 0; k < G; ++k) {
+      double *Ak = A + (size_t)k * nin;
+      for (size_t i = 0; i < nin; ++i) Ak[i] = 0.0;
+      for (int j = 0; j < K; ++j) {
+        const size_t off = ((size_t)(k * K + j) * B + b) * nin;
+        for (size_t i = 0; i < nin; ++i) Ak[i] += aj[j] * (X ? X[off + i] : (double)S[off + i]);
+      }
+      conv_one(Ak, Wt, bias, Cin, H, W, Cout, R, Sk, stride, pad, Ho, Wo, Y);
+      for (int j = 0; j < ns; ++j) {
+        const int t = k * ns + j;
+        const size_t ob = ((size_t)t * B + b) * nout;
+        for (size_t n = 0; n < nout; ++n) {
+          const double v = decay * U[n] + Y[n];
+          int s = v >= v_th;
+          if (replay && fabs(v - v_th) <= band) s = replay[ob + n] ? 1 : 0;
+          Vp[(size_t)t * nout + n] = v;
+          U[n] = v - v_th * (double)s;
+        }
+      }
+    }
+    /* BPTT through the LIF steps, latest first */
+    for (size_t n = 0; n < nout; ++n) gU[n] = g_vfinal ? g_vfinal[(size_t)b * nout + n] : 0.0;
+    for (size_t i = 0; i < (size_t)G * nout; ++i) gY[i] = 0.0;
+    for (int t = Sout - 1; t >= 0; --t) {
+      const int k = t / ns;
+      const size_t ob = ((size_t)t * B + b) * nout;
+      for (size_t n = 0; n < nout; ++n) {
+        const double h = surrogate(sg_kind, sg_alpha, Vp[(size_t)t * nout + n] - v_th);
+        const double dV = (g_out[ob + n] - (detach ? 0.0 : v_th * gU[n])) * h + gU[n];
+        gY[(size_t)k * nout + n] += dV;
+        gU[n] = decay * dV;
+      }
+    }
+    if (g_vinit) memcpy(g_vinit + (size_t)b * nout, gU, nout * sizeof(double));
+    /* the group convolution's gradients */
+    for (int k = 0; k < G; ++k) {
+      const double *gYk = gY + (size_t)k * nout, *Ak = A + (size_t)k * nin;
+      for (int co = 0; co < Cout; ++co)
+        for (int y = 0; y < Ho; ++y)
+          for (int x = 0; x < Wo; ++x) {
+            const double g = gYk[((size_t)co * Ho + y) * Wo + x];
+            g_b[co] += g;
+            for (int ci = 0; ci < Cin; ++ci)
+              for (int r = 0; r < R; ++r) {
+                const int yi = y * stride + r - pad;
+                if (yi < 0 || yi >= H) continue;
+                for (int s = 0; s < Sk; ++s) {
+                  const int xi = x * stride + s - pad;
+                  if (xi < 0 || xi >= W) continue;
+                  g_W[((size_t)(co * Cin + ci) * R + r) * Sk + s] += g * Ak[((size_t)ci * H + yi) * W + xi];
+                }
+              }
+          }
+      if (!g_in && !g_alpha) continue;
+      for (size_t i = 0; i < nin; ++i) gA[i] = 0.0;
+      for (int co = 0; co < Cout; ++co)
+        for (int y = 0; y < Ho; ++y)
+          for (int x = 0; x < Wo; ++x) {
+            const double g = gYk[((size_t)co * Ho + y) * Wo + x];
+            for (int ci = 0; ci < Cin; ++ci)
+              for (int r = 0; r < R; ++r) {
+                const int yi = y * stride + r - pad;
+                if (yi < 0 || yi >= H) continue;
+                for (int s = 0; s < Sk; ++s) {
+                  const int xi = x * stride + s - pad;
+                  if (xi < 0 || xi >= W) continue;
+                  gA[((size_t)ci * H + yi) * W + xi] += g * (double)Wt[((size_t)(co * Cin + ci) * R + r) * Sk + s];
+                }
+              }
+          }
+      for (int j = 0; j < K; ++j) {
+        const size_t off = ((size_t)(k * K + j) * B + b) * nin;
+        if (g_in)
+          for (size_t i = 0; i < nin; ++i) g_in[off + i] = aj[j] * gA[i];
+        if (g_alpha && alpha && mode != OR_MODE_DENSE) {
+          double acc = 0.0;
+          for (size_t i = 0; i < nin; ++i) acc += gA[i] * (X ? X[off + i] : (double)S[off + i]);
+          g_alpha[j] += acc;
+        }
+      }
+    }
+  done_b:
+    free(A); free(Vp); free(Y); free(gY); free(gU); free(U); free(gA);
+    if (rc) break;
+  }
+  free(aj);
+  return rc;
+}
