@@ -223,6 +223,78 @@ tac_status tac_conv_lif_forward_real(const tac_conv_lif_desc *desc, const tac_pl
                                      uint32_t *spikes_out, float *v_final, uint32_t *counts,
                                      void *ws, size_t ws_bytes, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Training: surrogate-gradient backpropagation through time
+ * through the grouped LIF, as the paper trains every network it reports
+ * (App. E).  Subtract reset (the one the paper
+ * trains with), K | T, out_pool = 1 (pool with tac_or_pool2), at most 64 LIF
+ * steps per call; other descriptors return TAC_ERR_UNSUPPORTED.
+ *
+ *   forward   V_t = decay U_{t-1} + Y_k ; s_t = Theta(V_t - v_th) ; U_t = V_t - v_th s_t
+ *   surrogate ds_t/dV_t := h(V_t - v_th):
+ *               FAST_SIGMOID  h(u) = 1 / (alpha |u| + 1)^2            (MNIST/FMNIST: alpha 25)
+ *               ARCTAN        h(u) = (alpha/2) / (1 + (pi/2 alpha u)^2) (DVS-Gesture: alpha 2)
+ *   reset     detach_reset = 1: dU_t/dV_t = 1 (DVS, "detach reset"); 0: 1 - v_th h
+ *   BPTT      dV_t = (dL/ds_t - [!detach] v_th gU) h + gU ; gU <- decay dV_t ;
+ *             dL/dY_k = sum_t in group k dV_t ; dL/dv_init = gU
+ *   conv      dL/dW = sum_k corr(dL/dY_k, A_k) ; dL/db = sum dL/dY_k ;
+ *             dL/dS_{kK+j} = a_j conv^T(dL/dY_k, W) ; dL/da_j = sum_k <conv^T(dL/dY_k, W), S_{kK+j}>
+ * (a_j = desc.agg_weights or beta^{K-1-j}).  The conv gradients run once per group,
+ * like the forward conv: G = T/K instead of T.
+ * ------------------------------------------------------------------------- */
+typedef enum { TAC_SURROGATE_FAST_SIGMOID = 0, TAC_SURROGATE_ARCTAN = 1 } tac_surrogate;
+
+typedef struct tac_grad_desc {
+  int32_t surrogate;     /* tac_surrogate                                  */
+  float alpha;           /* surrogate sharpness, finite and > 0            */
+  int32_t detach_reset;  /* 1: the reset term carries no gradient          */
+} tac_grad_desc;
+
+/* Training forward: tac_conv_lif_forward (or _real, by desc.input_kind: `input` is the
+ * packed spikes or the fp32 frames) that also writes
+ *   y_seq  device fp32 [G][B][H'][W'][C_out], G = T/K: the per-group drive exactly as
+ *          the LIF integrator consumed it (engine-specific offset / scale; opaque, read
+ *          only by tac_conv_lif_backward with the same desc and plan).
+ * Other arguments, ordering and errors as tac_conv_lif_forward. */
+tac_status tac_conv_lif_forward_train(const tac_conv_lif_desc *desc, const tac_plan *plan,
+                                      const void *input, const float *v_init,
+                                      uint32_t *spikes_out, float *v_final, uint32_t *counts,
+                                      float *y_seq, void *stream);
+
+/* Workspace of tac_conv_lif_backward: fp32 dL/dY [G][B][H'][W'][C_out]. */
+tac_status tac_backward_workspace_bytes(const tac_conv_lif_desc *desc, size_t *bytes);
+
+/* Backward of one training forward (same desc, plan, input, v_init; its y_seq):
+ *   g_spikes       device fp32 [T_out][B][H'][W'][C_out] = dL/ds (output spikes, channels last)
+ *   g_v_final      device fp32 [B][H'][W'][C_out] = dL/dv_final, or NULL (= 0)
+ *   g_weight       device fp32 [C_out][C_in][R][S]   (overwritten)
+ *   g_bias         device fp32 [C_out]               (overwritten)
+ *   g_input        device fp32 [T][B][H][W][C_in] = dL/d(input frames), or NULL
+ *   g_v_init       device fp32 [B][H'][W'][C_out], or NULL
+ *   g_agg_weights  device fp32 [K] = dL/da_j, or NULL
+ *   ws             device, >= tac_backward_workspace_bytes
+ * Gradients are sums over the batch (fp32, atomics: the summation order, and so the
+ * last bits, may vary from run to run). */
+tac_status tac_conv_lif_backward(const tac_conv_lif_desc *desc, const tac_plan *plan,
+                                 const tac_grad_desc *grad, const void *input, const float *v_init,
+                                 const float *y_seq, const float *g_spikes, const float *g_v_final,
+                                 float *g_weight, float *g_bias, float *g_input, float *g_v_init,
+                                 float *g_agg_weights, void *ws, size_t ws_bytes, void *stream);
+
+/* 2x2 OR-pool (= MaxPool(2) of binary spikes; floor mode) of packed spikes
+ * [T][B][H][WPR(W, C)] -> [T][B][H/2][WPR(W/2, C)], both contiguous. */
+tac_status tac_or_pool2(const uint32_t *in, uint32_t *out, int32_t T, int32_t B, int32_t C,
+                        int32_t H, int32_t W, void *stream);
+
+/* Its backward with MaxPool2d semantics: the gradient of a window goes to the window's
+ * first maximal element in row-major order (the first spike, or the top-left element of
+ * an all-zero window); rows / columns dropped by the floor get 0.
+ *   spikes_prepool packed [T][B][H][WPR(W, C)]; g_pooled fp32 [T][B][H/2][W/2][C];
+ *   g_prepool fp32 [T][B][H][W][C] (overwritten). */
+tac_status tac_or_pool2_backward(const uint32_t *spikes_prepool, const float *g_pooled,
+                                 float *g_prepool, int32_t T, int32_t B, int32_t C, int32_t H,
+                                 int32_t W, void *stream);
+
 /* u8 {0,1} [T][B][C][H][W] (device) <-> packed [T][B][H][WPR] (device).
  * pack treats any non-zero byte as a spike. */
 tac_status tac_pack_spikes(const uint8_t *dense01, uint32_t *packed, int32_t T,

@@ -385,7 +385,8 @@ tac_status validate_call(const tac_conv_lif_desc *desc, const void *prepared, co
 // Enqueue one validated (non-split) call.
 tac_status launch_call(const tac_conv_lif_desc *desc, const Geo &g, int engine, const void *prepared,
                        const void *input, bool real, const float *v_init, uint32_t *spikes_out,
-                       float *v_final, uint32_t *counts, void *stream, int *launches) {
+                       float *v_final, uint32_t *counts, void *stream, int *launches,
+                       float *y_seq = nullptr) {
   tacsnn::LayerParams p{};
   p.T = desc->T; p.B = desc->B; p.Cin = desc->C_in; p.H = desc->H; p.W = desc->W;
   p.Cout = desc->C_out; p.R = desc->R; p.S = desc->S; p.stride = desc->stride; p.pad = desc->pad;
@@ -403,6 +404,7 @@ tac_status launch_call(const tac_conv_lif_desc *desc, const Geo &g, int engine, 
   p.in = real ? nullptr : static_cast<const uint32_t *>(input);
   p.out = spikes_out; p.v_init = v_init; p.v_final = v_final; p.counts = counts;
   p.xin = real ? static_cast<const float *>(input) : nullptr;
+  p.y_seq = y_seq;
   const PrepLayout L = prep_layout(desc);
   const unsigned char *base = static_cast<const unsigned char *>(prepared);
   p.w = reinterpret_cast<const float *>(base + L.simt_off);
@@ -518,6 +520,154 @@ tac_status tac_conv_lif_forward_real(const tac_conv_lif_desc *desc, const tac_pl
                                      void *ws, size_t ws_bytes, void *stream) {
   return forward_impl(desc, plan, x_in, true, v_init, spikes_out, v_final, counts, ws, ws_bytes,
                       stream);
+}
+
+}  // extern "C"
+
+namespace {
+// shared checks of the training calls: plan, no split call, subtract reset, unpooled output,
+// at most kMaxTrainSteps LIF steps
+constexpr int kMaxTrainSteps = 64;
+tac_status train_checks(const tac_conv_lif_desc *desc, const tac_plan *plan, Geo *g) {
+  tac_status st = check(desc, g);
+  if (st != TAC_OK) return st;
+  if (!plan) return fail(TAC_ERR_NULL, "plan is NULL");
+  if (plan->abi_version != TACSNN_ABI_VERSION) return fail(TAC_ERR_PARAM, "plan from another ABI version");
+  if (is_split_call(desc, *g))
+    return fail(TAC_ERR_UNSUPPORTED, "training calls need K | T (no partial last group)");
+  if (plan->fingerprint != fingerprint(desc, *g, false))
+    return fail(TAC_ERR_PARAM, "plan was prepared for a different descriptor (see tac_plan)");
+  if (plan->bytes < prep_total(desc, *g)) return fail(TAC_ERR_WORKSPACE, "plan image too small");
+  if (desc->reset != TAC_RESET_SUBTRACT)
+    return fail(TAC_ERR_UNSUPPORTED, "training calls support the subtract reset (PAPER.md:587-588)");
+  if (desc->out_pool != 1)
+    return fail(TAC_ERR_UNSUPPORTED, "training calls need out_pool = 1 (pool with tac_or_pool2)");
+  if (g->G * g->nsteps > kMaxTrainSteps)
+    return fail(TAC_ERR_UNSUPPORTED, "training calls support at most %d LIF steps", kMaxTrainSteps);
+  return TAC_OK;
+}
+}  // namespace
+
+extern "C" {
+
+tac_status tac_conv_lif_forward_train(const tac_conv_lif_desc *desc, const tac_plan *plan, const void *input,
+                                      const float *v_init, uint32_t *spikes_out, float *v_final,
+                                      uint32_t *counts, float *y_seq, void *stream) {
+  g_detail.clear();
+  g_launches = 0;
+  Geo g;
+  tac_status st = train_checks(desc, plan, &g);
+  if (st != TAC_OK) return st;
+  if (!y_seq) return fail(TAC_ERR_NULL, "y_seq is NULL");
+  if ((uintptr_t)y_seq % 4) return fail(TAC_ERR_ALIGN, "y_seq misaligned");
+  if (!is_device_ptr(y_seq)) return fail(TAC_ERR_PARAM, "y_seq is not device memory");
+  const bool real = desc->input_kind == TAC_INPUT_REAL;
+  int engine;
+  st = validate_call(desc, plan->prepared, input, real, v_init, spikes_out, v_final, counts, &engine);
+  if (st != TAC_OK) return st;
+  int launches = 0;
+  st = launch_call(desc, g, engine, plan->prepared, input, real, v_init, spikes_out, v_final, counts, stream,
+                   &launches, y_seq);
+  if (st == TAC_OK) g_launches = launches;
+  return st;
+}
+
+tac_status tac_backward_workspace_bytes(const tac_conv_lif_desc *desc, size_t *bytes) {
+  g_detail.clear();
+  Geo g;
+  tac_status st = check(desc, &g);
+  if (st != TAC_OK) return st;
+  if (!bytes) return fail(TAC_ERR_NULL, "bytes is NULL");
+  *bytes = align256((size_t)g.G * desc->B * g.Ho * g.Wo * desc->C_out * 4);
+  return TAC_OK;
+}
+
+tac_status tac_conv_lif_backward(const tac_conv_lif_desc *desc, const tac_plan *plan,
+                                 const tac_grad_desc *grad, const void *input, const float *v_init,
+                                 const float *y_seq, const float *g_spikes, const float *g_v_final,
+                                 float *g_weight, float *g_bias, float *g_input, float *g_v_init,
+                                 float *g_agg_weights, void *ws, size_t ws_bytes, void *stream) {
+  g_detail.clear();
+  g_launches = 0;
+  Geo g;
+  tac_status st = train_checks(desc, plan, &g);
+  if (st != TAC_OK) return st;
+  if (!grad) return fail(TAC_ERR_NULL, "grad is NULL");
+  if (grad->surrogate != TAC_SURROGATE_FAST_SIGMOID && grad->surrogate != TAC_SURROGATE_ARCTAN)
+    return fail(TAC_ERR_PARAM, "surrogate=%d not in {0,1}", grad->surrogate);
+  if (!std::isfinite(grad->alpha) || !(grad->alpha > 0.f))
+    return fail(TAC_ERR_PARAM, "surrogate alpha must be finite and > 0");
+  if (grad->detach_reset != 0 && grad->detach_reset != 1) return fail(TAC_ERR_PARAM, "detach_reset not in {0,1}");
+  if (!input || !y_seq || !g_spikes || !g_weight || !g_bias) return fail(TAC_ERR_NULL, "NULL buffer");
+  size_t need = 0;
+  tac_backward_workspace_bytes(desc, &need);
+  if (!ws) return fail(TAC_ERR_NULL, "workspace is NULL");
+  if (ws_bytes < need) return fail(TAC_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  const bool real = desc->input_kind == TAC_INPUT_REAL;
+  const void *ptrs[] = {input, v_init, y_seq, g_spikes, g_v_final, g_weight, g_bias, g_input, g_v_init,
+                        g_agg_weights, ws};
+  const char *names[] = {"input", "v_init", "y_seq", "g_spikes", "g_v_final", "g_weight", "g_bias", "g_input",
+                         "g_v_init", "g_agg_weights", "ws"};
+  for (int i = 0; i < 11; ++i) {
+    if (ptrs[i] && (uintptr_t)ptrs[i] % 4) return fail(TAC_ERR_ALIGN, "%s misaligned", names[i]);
+    if (ptrs[i] && !is_device_ptr(ptrs[i])) return fail(TAC_ERR_PARAM, "%s is not device memory", names[i]);
+  }
+  const int engine = resolve_engine(desc);
+  if (engine < 0) return fail(TAC_ERR_UNSUPPORTED, "engine TCGEN05 cannot run this layer");
+  const PrepLayout L = prep_layout(desc);
+  const unsigned char *base = static_cast<const unsigned char *>(plan->prepared);
+  tacsnn::BwdParams p{};
+  p.T = desc->T; p.B = desc->B; p.Cin = desc->C_in; p.H = desc->H; p.W = desc->W; p.Cout = desc->C_out;
+  p.R = desc->R; p.S = desc->S; p.stride = desc->stride; p.pad = desc->pad; p.K = g.K; p.mode = desc->mode;
+  p.G = g.G; p.nsteps = g.nsteps; p.Ho = g.Ho; p.Wo = g.Wo; p.wpr_in = g.wpr_in;
+  p.in_st = g.in_st; p.in_sb = g.in_sb;
+  const double beta = (double)desc->beta;
+  p.decay = (float)(desc->mode == TAC_MODE_TAC ? std::pow(beta, (double)g.K) : beta);  // as the forward
+  p.v_th = desc->v_th;
+  const bool alpha = desc->agg_weights && desc->mode != TAC_MODE_DENSE;
+  for (int j = 0; j < g.K; ++j)
+    p.coef[j] = alpha ? desc->agg_weights[j] : (float)std::pow(beta, (double)(g.K - 1 - j));
+  p.udomain = engine == TAC_ENGINE_TCGEN05 && tacsnn::tc_u_domain(desc);
+  p.yscale = engine == TAC_ENGINE_TCGEN05 ? tacsnn::tc_yscale_ptr(desc, base + L.tc_off) : nullptr;
+  p.surrogate = grad->surrogate;
+  p.detach = grad->detach_reset;
+  p.sg_alpha = grad->alpha;
+  p.in = real ? nullptr : static_cast<const uint32_t *>(input);
+  p.xin = real ? static_cast<const float *>(input) : nullptr;
+  p.v_init = v_init; p.y_seq = y_seq; p.g_spikes = g_spikes; p.g_vfinal = g_v_final;
+  p.g_y = static_cast<float *>(ws); p.g_vinit = g_v_init;
+  p.w = reinterpret_cast<const float *>(base + L.simt_off);
+  p.g_w = g_weight; p.g_b = g_bias; p.g_in = g_input; p.g_alpha = g_agg_weights;
+  int launches = 0;
+  const int e = tacsnn::launch_backward(p, stream, &launches);
+  if (e) return fail(TAC_ERR_CUDA, "backward launch: %s", cudaGetErrorString((cudaError_t)e));
+  g_launches = launches;
+  return TAC_OK;
+}
+
+tac_status tac_or_pool2(const uint32_t *in, uint32_t *out, int32_t T, int32_t B, int32_t C, int32_t H,
+                        int32_t W, void *stream) {
+  g_detail.clear();
+  if (!in || !out) return fail(TAC_ERR_NULL, "NULL buffer");
+  if (T < 1 || B < 1 || C < 1 || H < 2 || W < 2) return fail(TAC_ERR_SHAPE, "extent < 1 (H, W >= 2)");
+  if ((uintptr_t)in % 4 || (uintptr_t)out % 4) return fail(TAC_ERR_ALIGN, "misaligned");
+  const int e = tacsnn::launch_or_pool2(in, out, T, B, C, H, W, stream);
+  if (e) return fail(TAC_ERR_CUDA, "or_pool2: %s", cudaGetErrorString((cudaError_t)e));
+  g_launches = 1;
+  return TAC_OK;
+}
+
+tac_status tac_or_pool2_backward(const uint32_t *spikes_prepool, const float *g_pooled, float *g_prepool,
+                                 int32_t T, int32_t B, int32_t C, int32_t H, int32_t W, void *stream) {
+  g_detail.clear();
+  if (!spikes_prepool || !g_pooled || !g_prepool) return fail(TAC_ERR_NULL, "NULL buffer");
+  if (T < 1 || B < 1 || C < 1 || H < 2 || W < 2) return fail(TAC_ERR_SHAPE, "extent < 1 (H, W >= 2)");
+  if ((uintptr_t)spikes_prepool % 4 || (uintptr_t)g_pooled % 4 || (uintptr_t)g_prepool % 4)
+    return fail(TAC_ERR_ALIGN, "misaligned");
+  const int e = tacsnn::launch_or_pool2_backward(spikes_prepool, g_pooled, g_prepool, T, B, C, H, W, stream);
+  if (e) return fail(TAC_ERR_CUDA, "or_pool2_backward: %s", cudaGetErrorString((cudaError_t)e));
+  g_launches = 1;
+  return TAC_OK;
 }
 
 tac_status tac_pack_spikes(const uint8_t *dense01, uint32_t *packed, int32_t T, int32_t B,

@@ -31,6 +31,7 @@ struct LayerParams {
   uint32_t *counts;
   const float *w;     // SIMT weights, fp32 [Cin][R][S][Cout]
   const float *bias;  // fp32 [Cout]
+  float *y_seq;       // training forward: per-group drive [G][B][Ho][Wo][Cout] as the LIF consumed it
 };
 
 enum { MODE_DENSE = 0, MODE_TAC = 1, MODE_TACTP = 2 };
@@ -44,5 +45,38 @@ int launch_pack(const uint8_t *dense, uint32_t *packed, int T, int B, int C, int
                 int W, void *stream);
 int launch_unpack(const uint32_t *packed, uint8_t *dense, int T, int B, int C, int H,
                   int W, void *stream);
+
+// ---- backward (backward.cu) ----
+struct BwdParams {
+  // layer geometry / LIF (as the forward)
+  int T, B, Cin, H, W, Cout, R, S, stride, pad, K, mode, G, nsteps, Ho, Wo, wpr_in;
+  long long in_st, in_sb;  // packed words (spikes) or floats (real input)
+  float decay, v_th, coef[kMaxK];
+  // replay of the forward integrator (backward LIF): U-domain (tcgen05 subtract epilogue:
+  // y = (Y + (decay - 1) v_th) s, state U s) or V-domain (y = Y s, state V s); s = 2^e
+  int udomain;
+  const float *yscale;  // device [s, 1/s] or NULL (= 1)
+  // surrogate
+  int surrogate, detach;
+  float sg_alpha;
+  // buffers
+  const uint32_t *in;   // packed input spikes, or
+  const float *xin;     // fp32 input frames [T][B][H][W][Cin]
+  const float *v_init;  // [B][Ho][Wo][Cout] or NULL
+  const float *y_seq;   // [G][B][Ho][Wo][Cout]
+  const float *g_spikes;  // [nsteps * G][B][Ho][Wo][Cout]
+  const float *g_vfinal;  // or NULL
+  float *g_y;           // workspace [G][B][Ho][Wo][Cout]
+  float *g_vinit;       // or NULL
+  const float *w;       // SIMT weights [Cin][R][S][Cout]
+  float *g_w;           // [Cout][Cin][R][S]
+  float *g_b;           // [Cout]
+  float *g_in;          // [T][B][H][W][Cin] or NULL
+  float *g_alpha;       // [K] or NULL
+};
+int launch_backward(const BwdParams &p, void *stream, int *launches);
+int launch_or_pool2(const uint32_t *in, uint32_t *out, int T, int B, int C, int H, int W, void *stream);
+int launch_or_pool2_backward(const uint32_t *pre, const float *g_pooled, float *g_pre, int T, int B,
+                             int C, int H, int W, void *stream);
 
 }  // namespace tacsnn

@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(32 * FC_WARPS) fc_lif_kernel(const LayerParams
       float Y = cok ? __ldg(p.bias + co) : 0.f;
 #pragma unroll
       for (int w = 0; w < FC_WARPS; ++w) Y += part[w][lane];
+      if (p.y_seq && cok) p.y_seq[((long long)g * p.B + b) * p.Cout + co] = Y;
       for (int j = 0; j < p.nsteps; ++j) {
         float v = fmaf(p.decay, V, Y);
         if (p.reset == RESET_DELAYED && sprev) v -= p.v_th;
@@ -172,6 +173,12 @@ __global__ void __launch_bounds__(128) simt_conv_lif_kernel(const LayerParams p)
           }
         }
       }
+    }
+    if (p.y_seq) {  // training forward: the group's drive (V-domain, unscaled)
+      float *ys = p.y_seq + (long long)g * p.B * p.Ho * p.Wo * p.Cout + vbase;
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+        if (c < nch) ys[c] = Y[c];
     }
     // LIF steps sharing Y_k
     for (int j = 0; j < p.nsteps; ++j) {

@@ -138,6 +138,8 @@ struct TcParams {
   const unsigned char *w_img;
   const float *scale_bias;
   const float *yscale;        // [2^e, 2^-e]: fp16-path prescale of Y (see tc_prepare)
+  float *y_seq;               // training forward: per-group drive [G][B][Ho][Wo][Cout] (or NULL)
+  long long yseq_plane;       // B * Ho * Wo * Cout
   unsigned long long *trace;  // optional: per-(group) role timestamps of CTA 0 (debug)
 };
 
@@ -1137,6 +1139,15 @@ __device__ __forceinline__ float sat_spike(float u) {
   return f;
 }
 
+// training forward: the drive of one 8-channel chunk as the LIF consumes it -> y_seq
+__device__ __forceinline__ void store_yseq8(const TcParams &p, int k, long long vbase, int cc0, int nvalid,
+                                            const float (&y)[8]) {
+  float *dst = p.y_seq + (long long)k * p.yseq_plane + vbase + cc0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    if (q < nvalid) dst[q] = y[q];
+}
+
 // Y for 8 channels from the two s32 accumulator slices (see file header)
 __device__ __forceinline__ void combine8(const TcParams &p, const float *sc, int co,
                                          const uint32_t (&d1)[8], const uint32_t (&d2)[8],
@@ -1331,6 +1342,12 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
             du[cur][2 * q] = __float_as_uint(u.x);
             du[cur][2 * q + 1] = __float_as_uint(u.y);
           }
+          if (p.y_seq && valid && active_half) {
+            float yv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) yv[q] = __uint_as_float(dy[cur][q]);
+            store_yseq8(p, k, vbase, ch * 8, Cout - co_base - ch * 8, yv);
+          }
           ptx::tmem_st8(ucol + ch * 8, du[cur]);
           if (ch > 0) ptx::tmem_wait_ld_dep(dy[nxt], du[nxt]);
         }
@@ -1350,6 +1367,12 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
                             dec2, nth2, nsp);
             du[2 * q] = __float_as_uint(u.x);
             du[2 * q + 1] = __float_as_uint(u.y);
+          }
+          if (p.y_seq && valid && active_half) {
+            float yv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) yv[q] = __uint_as_float(dy[q]);
+            store_yseq8(p, k, vbase, ch * 8, Cout - co_base - ch * 8, yv);
           }
           ptx::tmem_st8(ucol + ch * 8, du);
         }
@@ -1376,6 +1399,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
 #pragma unroll
           for (int q = 3; q >= 0; --q)
             lif_pair_sr<NS>(U[UT ? 0 : ch * 4 + q], make_float2(yv[2 * q], yv[2 * q + 1]), dec2, nth2, nsp);
+          if (p.y_seq && valid && active_half) store_yseq8(p, k, vbase, ch * 8, Cout - co_base - ch * 8, yv);
           if (ch > 0) {
             if (NBUF == 1) {
               ptx::tmem_ld8(tcol + (ch - 1) * 8, d[0][0]);
@@ -1566,6 +1590,7 @@ __device__ __forceinline__ void epilogue_generic(const TcParams &p, uint8_t *sme
         } else {
           combine8(p, sc, co_base + ch * 8, d[cur][0], d[cur][1], yv);
         }
+        if (p.y_seq && valid && active_half) store_yseq8(p, k, vbase, ch * 8, Cout - co_base - ch * 8, yv);
         {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -1922,6 +1947,8 @@ __global__ void tc_zero_kernel(uint32_t *out, int T_out, int B, long long plane,
 }  // namespace
 
 // ------------------------------------------------------------------ host API --
+static bool lif_u_state(const tac_conv_lif_desc *d);
+bool tc_u_domain(const tac_conv_lif_desc *d) { return lif_u_state(d); }
 bool tc_shape_ok(const tac_conv_lif_desc *d) { return shape_reason(d) == nullptr; }
 bool tc_supported(const tac_conv_lif_desc *d) { return reason(d) == nullptr; }
 const char *tc_unsupported_reason(const tac_conv_lif_desc *d) {
@@ -1951,6 +1978,10 @@ static size_t lut_off(const Geometry &g) { return yscale_off(g) + 16; }
 size_t tc_weights_bytes(const tac_conv_lif_desc *d) {
   const Geometry g = geometry(d);
   return lut_off(g) + (g.split ? 4 * (size_t)kLutWords : 0);
+}
+const float *tc_yscale_ptr(const tac_conv_lif_desc *d, const unsigned char *tc_prep) {
+  const Geometry g = geometry(d);
+  return g.path == PATH_HALO ? nullptr : reinterpret_cast<const float *>(tc_prep + yscale_off(g));
 }
 
 // Two int8 slices per output channel, laid out as the smem image of each CTA:
@@ -2224,6 +2255,8 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   // B: rows held by one CTA x 16 B between 16-byte K chunks
   p.lbo_b = g.path == PATH_HALO ? (uint32_t)g.cout_pad * 16u : (uint32_t)(g.cout_pad / 2) * 16u;
   p.in = lp.in; p.out = lp.out; p.v_init = lp.v_init; p.v_final = lp.v_final; p.counts = lp.counts;
+  p.y_seq = lp.y_seq;
+  p.yseq_plane = (long long)lp.B * lp.Ho * lp.Wo * lp.Cout;
   p.trace = tacsnn_trace_buffer();
   p.w_img = tc_prep;
   p.scale_bias = reinterpret_cast<const float *>(tc_prep + scale_off(g));

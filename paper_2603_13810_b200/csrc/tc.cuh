@@ -16,6 +16,11 @@ const char *tc_unsupported_reason(const tac_conv_lif_desc *d);
 size_t tc_weights_bytes(const tac_conv_lif_desc *d);
 void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bias,
                 unsigned char *dst);
+// backward replay of the forward integrator: does the subtract epilogue run in the
+// shifted state U = V - v_th with the (decay - 1) v_th offset folded into Y (tc.cu)?
+bool tc_u_domain(const tac_conv_lif_desc *d);
+// device [2^e, 2^-e] Y prescale of the fp16 operand paths, NULL on the int8 path
+const float *tc_yscale_ptr(const tac_conv_lif_desc *d, const unsigned char *tc_prep);
 int tc_launch(const tac_conv_lif_desc *d, const LayerParams &p, const unsigned char *tc_prep,
               void *stream, int *launches);
 

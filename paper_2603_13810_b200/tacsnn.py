@@ -31,7 +31,9 @@ EXPORTS = ("tac_desc_check", "tac_out_shape", "tac_select_engine", "tac_weights_
            "tac_conv_lif_forward_real",
            "tac_pack_spikes", "tac_unpack_spikes", "tac_status_string",
            "tac_last_error_detail", "tac_abi_version", "tac_last_launch_count",
-           "tac_debug_set_trace")
+           "tac_debug_set_trace", "tac_conv_lif_forward_train", "tac_backward_workspace_bytes",
+           "tac_conv_lif_backward", "tac_or_pool2", "tac_or_pool2_backward")
+SURROGATES = {"fast_sigmoid": 0, "arctan": 1}
 
 
 class Desc(ctypes.Structure):
@@ -51,6 +53,11 @@ class Plan(ctypes.Structure):
     _fields_ = [("prepared", ctypes.c_void_p), ("bytes", ctypes.c_size_t),
                 ("fingerprint", ctypes.c_uint64), ("abi_version", ctypes.c_int32),
                 ("reserved", ctypes.c_int32)]
+
+
+class GradDesc(ctypes.Structure):
+    """Mirror of tac_grad_desc."""
+    _fields_ = [("surrogate", ctypes.c_int32), ("alpha", ctypes.c_float), ("detach_reset", ctypes.c_int32)]
 
 
 class Prepared:
@@ -97,6 +104,12 @@ def lib():
                 "tac_abi_version": ([], i32),
                 "tac_last_launch_count": ([], i32),
                 "tac_debug_set_trace": ([P], None),
+                "tac_conv_lif_forward_train": ([D, ctypes.POINTER(Plan), P, P, P, P, P, P, P], i32),
+                "tac_backward_workspace_bytes": ([D, ctypes.POINTER(sz)], i32),
+                "tac_conv_lif_backward": ([D, ctypes.POINTER(Plan), ctypes.POINTER(GradDesc), P, P, P, P, P,
+                                           P, P, P, P, P, P, sz, P], i32),
+                "tac_or_pool2": ([P, P, i32, i32, i32, i32, i32, P], i32),
+                "tac_or_pool2_backward": ([P, P, P, i32, i32, i32, i32, i32, P], i32),
             }
             for name, (args, res) in sig.items():
                 f = getattr(L, name)
@@ -254,6 +267,82 @@ def conv_lif(spec: LayerSpec, prepared: Prepared, x: torch.Tensor, *, v_init=Non
     _check(fwd(ctypes.byref(d), ctypes.byref(prepared.plan), _ptr(x), _ptr(v_init), _ptr(out), _ptr(v_final),
                _ptr(counts), _ptr(ws), wsb.value, _stream(x.device)))
     return out, v_final, counts
+
+
+def _check_input(spec: LayerSpec, x: torch.Tensor):
+    if spec.input == "real":
+        if not (x.is_cuda and x.dtype == torch.float32 and tuple(x.shape) == (spec.T, spec.B, spec.H, spec.W, spec.C_in)):
+            raise ValueError("real input: fp32 cuda [T, B, H, W, C_in]")
+    elif not (x.is_cuda and x.dtype == torch.int32 and tuple(x.shape) == (spec.T, spec.B, spec.H, spec.in_words_per_row)
+              and x.stride(3) == 1 and x.stride(2) == spec.in_words_per_row):
+        raise ValueError("spikes: packed int32 cuda [T, B, H, WPR] with packed rows")
+
+
+def conv_lif_train(spec: LayerSpec, prepared: Prepared, x: torch.Tensor, *, v_init=None,
+                   want_v_final=False, want_counts=False):
+    """Training forward (tac_conv_lif_forward_train): as conv_lif, plus y_seq, the per-group
+    drive fp32 [G, B, H', W', C_out] that conv_lif_backward replays.
+    Returns (spikes_out, v_final or None, counts or None, y_seq)."""
+    _check_input(spec, x)
+    T_out, Ho, Wo, wpr = spec.out_shape()
+    hc, wc = spec.conv_hw
+    G = spec.T // (1 if spec.mode == "dense" else spec.K)
+    out = torch.empty((T_out, spec.B, Ho, wpr), dtype=torch.int32, device=x.device)
+    v_final = torch.empty((spec.B, hc, wc, spec.C_out), dtype=torch.float32, device=x.device) if want_v_final else None
+    counts = torch.empty((spec.B, spec.C_out), dtype=torch.int32, device=x.device) if want_counts else None
+    y_seq = torch.empty((G, spec.B, hc, wc, spec.C_out), dtype=torch.float32, device=x.device)
+    d = spec.desc((x.stride(0), x.stride(1)), (out.stride(0), out.stride(1)))
+    _check(lib().tac_conv_lif_forward_train(ctypes.byref(d), ctypes.byref(prepared.plan), _ptr(x), _ptr(v_init),
+                                            _ptr(out), _ptr(v_final), _ptr(counts), _ptr(y_seq),
+                                            _stream(x.device)))
+    return out, v_final, counts, y_seq
+
+
+def conv_lif_backward(spec: LayerSpec, prepared: Prepared, x: torch.Tensor, y_seq: torch.Tensor,
+                      g_spikes: torch.Tensor, *, v_init=None, g_v_final=None, surrogate="fast_sigmoid",
+                      alpha=25.0, detach_reset=False, want_input_grad=True, want_v_init_grad=False,
+                      want_agg_grad=False):
+    """Surrogate-gradient BPTT of one layer (tac_conv_lif_backward).  g_spikes: fp32
+    [T_out, B, H', W', C_out] = dL/ds.  Returns dict(g_weight [C_out,C_in,R,S], g_bias,
+    g_input [T,B,H,W,C_in] or None, g_v_init or None, g_agg_weights or None)."""
+    _check_input(spec, x)
+    hc, wc = spec.conv_hw
+    dev = x.device
+    g_w = torch.empty((spec.C_out, spec.C_in, spec.R, spec.S), dtype=torch.float32, device=dev)
+    g_b = torch.empty((spec.C_out,), dtype=torch.float32, device=dev)
+    g_in = torch.empty((spec.T, spec.B, spec.H, spec.W, spec.C_in), dtype=torch.float32,
+                       device=dev) if want_input_grad else None
+    g_vi = torch.empty((spec.B, hc, wc, spec.C_out), dtype=torch.float32, device=dev) if want_v_init_grad else None
+    g_a = torch.empty((spec.K,), dtype=torch.float32, device=dev) if want_agg_grad else None
+    d = spec.desc((x.stride(0), x.stride(1)), (0, 0))
+    wsb = ctypes.c_size_t()
+    _check(lib().tac_backward_workspace_bytes(ctypes.byref(d), ctypes.byref(wsb)))
+    ws = torch.empty(wsb.value, dtype=torch.uint8, device=dev)
+    gd = GradDesc(SURROGATES[surrogate], float(alpha), int(bool(detach_reset)))
+    _check(lib().tac_conv_lif_backward(ctypes.byref(d), ctypes.byref(prepared.plan), ctypes.byref(gd), _ptr(x),
+                                       _ptr(v_init), _ptr(y_seq), _ptr(g_spikes.contiguous()), _ptr(g_v_final),
+                                       _ptr(g_w), _ptr(g_b), _ptr(g_in), _ptr(g_vi), _ptr(g_a), _ptr(ws),
+                                       wsb.value, _stream(dev)))
+    return dict(g_weight=g_w, g_bias=g_b, g_input=g_in, g_v_init=g_vi, g_agg_weights=g_a)
+
+
+def or_pool2(x: torch.Tensor, C: int, W: int) -> torch.Tensor:
+    """2x2 OR-pool of packed spikes [T, B, H, WPR] (tac_or_pool2)."""
+    T, B, H, wpr = x.shape
+    assert x.is_cuda and x.dtype == torch.int32 and x.is_contiguous() and wpr == (W * C + 31) // 32
+    out = torch.empty((T, B, H // 2, ((W // 2) * C + 31) // 32), dtype=torch.int32, device=x.device)
+    _check(lib().tac_or_pool2(_ptr(x), _ptr(out), T, B, C, H, W, _stream(x.device)))
+    return out
+
+
+def or_pool2_backward(pre: torch.Tensor, g_pooled: torch.Tensor, C: int, W: int) -> torch.Tensor:
+    """MaxPool2d-semantics backward of or_pool2: g_pooled fp32 [T, B, H/2, W/2, C] ->
+    fp32 [T, B, H, W, C] (tac_or_pool2_backward)."""
+    T, B, H, _ = pre.shape
+    g = torch.empty((T, B, H, W, C), dtype=torch.float32, device=pre.device)
+    _check(lib().tac_or_pool2_backward(_ptr(pre.contiguous()), _ptr(g_pooled.contiguous()), _ptr(g), T, B, C, H,
+                                       W, _stream(pre.device)))
+    return g
 
 
 def pack(dense: torch.Tensor) -> torch.Tensor:

@@ -21,7 +21,7 @@ def _declared_functions():
     with open(os.path.join(ROOT, "include", "tacsnn.h")) as f:
         src = f.read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(tac_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(tac_[a-z_0-9]+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol(T):
