@@ -55,6 +55,11 @@ def parse():
     ap.add_argument("--layer-detail", action="store_true")
     ap.add_argument("--no-v-final", action="store_true",
                     help="skip the extra timing with every layer writing v_final")
+    ap.add_argument("--train", action="store_true",
+                    help="time a training step (forward + surrogate-gradient BPTT backward) of the "
+                         "config's network, TAC/TAC-TP against dense (SURVEY.md 8(f) #3)")
+    ap.add_argument("--whole-net", action="store_true",
+                    help="--train on the whole MNIST/FMNIST network (conv blocks + FC head)")
     ap.add_argument("--launcher-check", action="store_true",
                     help="CPU/gloo check of the rank launcher, shard and gather plumbing only "
                          "(no kernels, no timing; used by tests/test_bench_launcher.py)")
@@ -296,6 +301,110 @@ def run_reference(a, cfg, specs_fn, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- training --
+TRAIN_METRIC = "Conv-LIF training spike-frames/s (forward + surrogate-gradient BPTT backward)"
+
+
+def run_train(a, cfg, rank, world, local, B_global):
+    """One training step = the training forward of every layer (tac_conv_lif_forward_train,
+    tac_or_pool2), a spike-count loss, and the backward of every layer
+    (tac_conv_lif_backward, tac_or_pool2_backward); multi-GPU adds the NCCL all-reduce of
+    the weight gradients (the data-parallel exchange step of training).  The paper's
+    speedups are training speedups: the same step is timed
+    for the dense per-timestep baseline, and the ratio is reported."""
+    import torch
+    import torch.distributed as dist
+    from paper_2603_13810_b200 import configs, dist as D, network, tacsnn
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    b0, B = D.shard_range(B_global, world, rank)
+    rate = cfg.inputs != "dvs"
+    sg = dict(surrogate="fast_sigmoid", alpha=25.0, detach_reset=False) if rate else \
+        dict(surrogate="arctan", alpha=2.0, detach_reset=True)          # App. E, P:587-588
+
+    def build(mode, K):
+        if a.whole_net:
+            specs = configs.network_plan(cfg, mode=mode, K=K, B=B, engine=a.engine)
+            weights = configs.network_weights(cfg)
+        else:
+            specs = configs.layer_plan(cfg, mode=mode, K=K, B=B, engine=a.engine)
+            weights = configs.layer_weights(cfg)
+        return network.TrainableNetwork(specs, weights, device=dev, **sg)
+
+    x = tacsnn.pack(configs.make_inputs(cfg, B=B, b0=b0, device=dev))
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(net):
+        last = net.specs[-1]
+        g = torch.Generator(device=dev).manual_seed(7 + rank)
+        target = torch.zeros((B, last.C_out), device=dev)
+        target[torch.arange(B, device=dev), torch.randint(0, last.C_out, (B,), generator=g, device=dev)] = 1.0
+
+        def step():
+            _, cnt, tape = net.forward_train(x)
+            s_last = tape[-1][0]
+            hc, wc = s_last.conv_hw
+            T_out = tape[-1][4].shape[0]
+            norm = float(T_out * hc * wc)
+            # loss glue (user code): L = 0.5 sum (count / norm - target)^2  (spike-count readout, P:589)
+            err = (cnt.float() / norm - target) / norm
+            g_out = err[None, :, None, None, :].expand(T_out, B, hc, wc, s_last.C_out).contiguous()
+            grads = net.backward(tape, g_out)
+            if world > 1:   # data-parallel gradient exchange
+                flat = torch.cat([torch.cat([r["g_weight"].reshape(-1), r["g_bias"]]) for r in grads])
+                dist.all_reduce(flat)
+            return grads
+
+        launches = 0
+        for _ in range(a.warmup):
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = torch.tensor([e0.elapsed_time(e1) / a.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return float(ms.item())
+
+    mode = a.mode or cfg.mode
+    K = cfg.K if a.K is None else a.K
+    net = build(mode, K)
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms = timed(net)
+    clk = clocks.stop()
+    engines = net.engines()
+    del net
+    ms_dense = timed(build("dense", 1))
+    frames = B_global * cfg.T
+    if rank == 0:
+        line = {"metric": TRAIN_METRIC, "value": frames / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+                "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": a.scaling, "vs_baseline": None, "dtype": "f32 gradients; forward as inference",
+                "data": "synthetic",
+                "config": {"workload": cfg.name + ("+FC" if a.whole_net else ""), "mode": mode, "K": K,
+                           "global_batch": B_global, "per_rank_batch": B, "T": cfg.T,
+                           "parallelism": f"dp{world}", "engines": engines, "surrogate": sg,
+                           "loss": "0.5 sum (spike count / steps*pixels - one-hot)^2 (user glue)"},
+                "dense_ms_per_step": ms_dense, "speedup_vs_dense": ms_dense / ms,
+                "paper_context": "TAC training speedups 5.3-13.8x (M3 Max, MNIST K=4/8/16, P:255-257), "
+                                 "5.1-13.1x (V100, P:331-337)",
+                "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 # -------------------------------------------------------------------- ours --
 def launcher_check(a, rank, world):
     """Plumbing of the multi-rank bench on CPU (gloo): shard ranges and the output gather
@@ -338,6 +447,8 @@ def main():
 
     if a.launcher_check:
         return launcher_check(a, rank, world)
+    if a.train and a.impl != "reference":
+        return run_train(a, cfg, rank, world, local, B_global)
     if a.impl == "reference":
         return run_reference(a, cfg, specs_fn, rank, world)
 

@@ -86,3 +86,52 @@ class Network:
             n += tacsnn.last_launch_count()
         self._launches = n
         return n
+
+
+class TrainableNetwork(Network):
+    """The same stack for training: every layer runs
+    tac_conv_lif_forward_train with its pool as a separate tac_or_pool2 (the backward
+    needs the pre-pool spikes), and backward() chains tac_conv_lif_backward and
+    tac_or_pool2_backward from the last layer to the first.  The plans are the
+    inference plans (the image does not depend on out_pool)."""
+
+    def __init__(self, specs, weights, device="cuda", surrogate="fast_sigmoid", alpha=25.0,
+                 detach_reset=False):
+        super().__init__(specs, weights, device)
+        self.surrogate, self.alpha, self.detach = surrogate, alpha, detach_reset
+
+    def forward_train(self, x: torch.Tensor):
+        """Returns (final spikes, final counts, tape)."""
+        B = x.shape[1]
+        tape = []
+        cnt = None
+        n = len(self.specs)
+        for i, (spec, prep) in enumerate(zip(self.specs, self.prepared)):
+            s = (spec if spec.B == B else spec.replace(B=B)).replace(out_pool=1)
+            x = flatten_for(s, x)
+            out, _, cnt, y = tacsnn.conv_lif_train(s, prep, x, want_counts=(i == n - 1))
+            tape.append((s, prep, x, y, out, spec.out_pool))
+            hc, wc = s.conv_hw
+            x = tacsnn.or_pool2(out, s.C_out, wc) if spec.out_pool == 2 else out
+        return x, cnt, tape
+
+    def backward(self, tape, g_out: torch.Tensor, prepool: bool = True):
+        """g_out: dL/ds of the last layer's output spikes, fp32 [T_out,B,H,W,C] -- the
+        unpooled spikes the count readout reads (prepool=True, H,W = H',W') or, if the last
+        layer pools, the pooled map (prepool=False).  Returns the per-layer gradient dicts
+        (first layer first)."""
+        grads = [None] * len(tape)
+        g = g_out
+        for i in range(len(tape) - 1, -1, -1):
+            s, prep, x, y, out, pool = tape[i]
+            if pool == 2 and not (prepool and i == len(tape) - 1):
+                # g is w.r.t. the pooled map: route it back through the OR-pool
+                hc, wc = s.conv_hw
+                g = tacsnn.or_pool2_backward(out, g.reshape(out.shape[0], s.B, hc // 2, wc // 2, s.C_out),
+                                             s.C_out, wc)
+            r = tacsnn.conv_lif_backward(s, prep, x, y, g.reshape(out.shape[0], s.B, *s.conv_hw, s.C_out),
+                                         surrogate=self.surrogate, alpha=self.alpha,
+                                         detach_reset=self.detach, want_input_grad=i > 0)
+            grads[i] = r
+            g = r["g_input"]
+        return grads

@@ -193,3 +193,30 @@ def test_two_layer_stack_backward(T, O):
     ref1 = O.backward(S, w1.numpy(), b1.numpy(), g1_ref, K=specs[0].K, replay=D1, want_input=False, **kw)
     _close(r1["g_weight"].cpu().numpy(), ref1["g_W"], "L1 g_W", tol)
     _close(r1["g_bias"].cpu().numpy(), ref1["g_b"], "L1 g_b", tol)
+
+
+@pytest.mark.parametrize("cfg_name,mode,K", [("C2", "tac", 4), ("C2", "dense", 1), ("C4", "tactp", 2)])
+def test_trainable_network_forward_equals_inference(T, cfg_name, mode, K):
+    """TrainableNetwork: the training forward (unpooled layers + tac_or_pool2) gives bitwise
+    the inference forward's final spikes and counts; the backward chain yields finite
+    gradients of the right shapes for every layer."""
+    from paper_2603_13810_b200 import configs, network
+    cfg = configs.CONFIGS[cfg_name]
+    B = 4 if cfg_name == "C2" else 1
+    if cfg.inputs == "dvs":
+        specs, weights = configs.layer_plan(cfg, mode=mode, K=K, B=B), configs.layer_weights(cfg)
+    else:
+        specs, weights = configs.network_plan(cfg, mode=mode, K=K, B=B), configs.network_weights(cfg)
+    x = T.pack(configs.make_inputs(cfg, B=B, device="cuda"))
+    y_inf, c_inf, _, _ = network.Network(specs, weights).forward(x)
+    tnet = network.TrainableNetwork(specs, weights)
+    y, cnt, tape = tnet.forward_train(x)
+    assert torch.equal(y, y_inf) and torch.equal(cnt, c_inf[-1])
+    s_last = tape[-1][0]
+    g = torch.ones((tape[-1][4].shape[0], B, *s_last.conv_hw, s_last.C_out), device="cuda") * 0.01
+    grads = tnet.backward(tape, g)
+    torch.cuda.synchronize()
+    for spec, r in zip(specs, grads):
+        assert tuple(r["g_weight"].shape) == (spec.C_out, spec.C_in, spec.R, spec.S)
+        assert torch.isfinite(r["g_weight"]).all() and torch.isfinite(r["g_bias"]).all()
+    assert any(float(r["g_weight"].abs().sum()) > 0 for r in grads)
