@@ -108,8 +108,11 @@ constexpr uint32_t kSmemLimit = 232448;
 enum { PATH_HALO = 0, PATH_H16 = 1, PATH_SPLIT = 2 };
 
 struct TcParams {
-  CUtensorMap tmap;  // 4-D [T][B][H][WPR] u32 view of the input spikes (TMA producer)
-  int use_tma, raw_bw, nraw;
+  CUtensorMap tmap;  // 4-D [T][B][H][WPR] u32 view of the input spikes (TMA producer), or
+                     // 3-D [T][B][H*WPR] (plane mode: whole narrow frames, e.g. 28x28x1 = 112 B)
+  int use_tma, raw_bw, nraw;  // use_tma: 0 LDG, 1 halo boxes, 2 whole planes (raw_bw = plane words)
+  int warp_stage;             // 1: each producer warp builds whole A stages (stage it -> warp it % 3)
+  int prod_step;              // halo-row stride of the pixel-wise producers: 96, or 32 with warp_stage
   uint32_t off_raw, raw_stage_bytes, raw_box_bytes;
   int B, H, W, Cin, Cout, Cout_pad, pad, Ho, Wo, pool;
   int Hq, Wq;  // stored (pooled) extent: floor(H'/2), floor(W'/2) when pool == 2
@@ -238,7 +241,7 @@ uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
 // Shared-memory plan.  With use_tma the producers aggregate from a TMA-loaded
 // raw halo ([K][18][raw_bw] u32 per stage) instead of loading from global.
-Geometry geometry(const tac_conv_lif_desc *d, bool use_tma = false) {
+Geometry geometry(const tac_conv_lif_desc *d, bool use_tma = false, int plane_words = 0) {
   Geometry g{};
   g.path = path_of(d);
   g.split = split_of(d) ? 1 : 0;
@@ -263,7 +266,8 @@ Geometry geometry(const tac_conv_lif_desc *d, bool use_tma = false) {
     // C_in = 32: one word per pixel as in the int8 halo path
     g.raw_bw = d->C_in >= 32 ? (int)align_up(kHaloW * (d->C_in / 32) + 3, 4) : 8;
   }
-  g.raw_box_bytes = (uint32_t)K * kHaloH * g.raw_bw * 4u;
+  if (plane_words > 0) g.raw_bw = plane_words;  // plane mode: K whole frames per stage
+  g.raw_box_bytes = (uint32_t)K * (plane_words > 0 ? 1 : kHaloH) * g.raw_bw * 4u;
   g.raw_stage_bytes = align_up(g.raw_box_bytes, 128);
   const int combos[6][2] = {{3, 4}, {3, 3}, {3, 2}, {2, 2}, {3, 1}, {2, 1}};
   for (int ci = 0; ci < (use_tma ? 6 : 2); ++ci) {
@@ -437,11 +441,20 @@ __device__ __forceinline__ void store_h16_row(uint32_t dst, uint32_t lbo, uint32
   ptx::st_shared_v4(dst + lbo, c8, 0u, 0u, 0u);
 }
 
+// Source of the pixel-wise producers: packed frames in global memory (LDG, frame stride
+// in_st) or, in plane mode, the group's K whole frames staged in shared memory by TMA
+// (frame stride = plane words); the indexing is the same.
+template <bool SMEM>
+__device__ __forceinline__ uint32_t ld_src(const uint32_t *a) {
+  if constexpr (SMEM) return *a;
+  else return __ldg(a);
+}
+
 // LDG fallback: one halo pixel per thread and pass; the C_in <= 8 bits of pixel
 // xi start at row bit xi * C_in and straddle at most two words.
-template <int K>
+template <int K, bool SMEM = false>
 __device__ __forceinline__ void produce_h16(const TcParams &p, int tile, int k, uint32_t a_stage,
-                                            int ptid) {
+                                            int ptid, const uint32_t *plane = nullptr) {
   int b, y0, x0;
   bool tok;
   tile_origin(p, tile, b, y0, x0, tok);
@@ -449,8 +462,9 @@ __device__ __forceinline__ void produce_h16(const TcParams &p, int tile, int k, 
   const uint32_t cmask = (1u << Cin) - 1u;
   uint32_t one_lo, one_hi, c8;
   h16_bias_slot(Cin, one_lo, one_hi, c8);
-  const uint32_t *frame0 = p.in + (long long)(k * K) * p.in_st + (long long)b * p.in_sb;
-  for (int row = ptid; row < kHaloRows; row += kProdWarps * 32) {
+  const uint32_t *frame0 = SMEM ? plane : p.in + (long long)(k * K) * p.in_st + (long long)b * p.in_sb;
+  const long long fst = SMEM ? (long long)p.raw_bw : p.in_st;
+  for (int row = ptid; row < kHaloRows; row += p.prod_step) {
     const int hy = row / kHaloW, hx = row - (row / kHaloW) * kHaloW;
     const int yi = y0 + hy - p.pad, xi = x0 + hx - p.pad;
     const bool ok = tok && yi >= 0 && yi < p.H && xi >= 0 && xi < p.W;
@@ -460,8 +474,8 @@ __device__ __forceinline__ void produce_h16(const TcParams &p, int tile, int k, 
     uint32_t w0[K], w1[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-      w0[j] = ok ? __ldg(src + (long long)j * p.in_st) : 0u;
-      w1[j] = two ? __ldg(src + (long long)j * p.in_st + 1) : 0u;
+      w0[j] = ok ? ld_src<SMEM>(src + (long long)j * fst) : 0u;
+      w1[j] = two ? ld_src<SMEM>(src + (long long)j * fst + 1) : 0u;
     }
     uint32_t lo = one_lo, hi = one_hi;
 #pragma unroll
@@ -620,7 +634,7 @@ __device__ __forceinline__ void produce_h16x(const TcParams &p, int tile, int k,
   bool tok;
   tile_origin(p, tile, b, y0, x0, tok);
   const float *frame0 = p.xin + (long long)(k * (K ? K : p.K)) * p.in_st + (long long)b * p.in_sb;
-  for (int row = ptid; row < kHaloRows; row += kProdWarps * 32) {
+  for (int row = ptid; row < kHaloRows; row += p.prod_step) {
     const int hy = row / kHaloW, hx = row - (row / kHaloW) * kHaloW;
     const int yi = y0 + hy - p.pad, xi = x0 + hx - p.pad;
     const bool ok = tok && yi >= 0 && yi < p.H && xi >= 0 && xi < p.W;
@@ -645,15 +659,17 @@ __device__ __forceinline__ void produce_h16x(const TcParams &p, int tile, int k,
   }
 }
 
-// LDG split producers (e.g. MNIST rows, whose 4-B row stride rules out TMA)
-template <int K, int CIN>
+// LDG split producers (e.g. MNIST rows, whose 4-B row stride rules out halo-box TMA;
+// SMEM: plane mode, the whole frames in shared memory)
+template <int K, int CIN, bool SMEM = false>
 __device__ __forceinline__ void produce_h16s(const TcParams &p, const uint32_t *lut, int tile, int k,
-                                             uint32_t a_stage, int ptid) {
+                                             uint32_t a_stage, int ptid, const uint32_t *plane = nullptr) {
   int b, y0, x0;
   bool tok;
   tile_origin(p, tile, b, y0, x0, tok);
-  const uint32_t *frame0 = p.in + (long long)(k * K) * p.in_st + (long long)b * p.in_sb;
-  for (int row = ptid; row < kHaloRows; row += kProdWarps * 32) {
+  const uint32_t *frame0 = SMEM ? plane : p.in + (long long)(k * K) * p.in_st + (long long)b * p.in_sb;
+  const long long fst = SMEM ? (long long)p.raw_bw : p.in_st;
+  for (int row = ptid; row < kHaloRows; row += p.prod_step) {
     const int hy = row / kHaloW, hx = row - (row / kHaloW) * kHaloW;
     const int yi = y0 + hy - p.pad, xi = x0 + hx - p.pad;
     const bool ok = tok && yi >= 0 && yi < p.H && xi >= 0 && xi < p.W;
@@ -663,8 +679,8 @@ __device__ __forceinline__ void produce_h16s(const TcParams &p, const uint32_t *
     uint32_t bits[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-      const uint32_t w0 = ok ? __ldg(src + (long long)j * p.in_st) : 0u;
-      const uint32_t w1 = two ? __ldg(src + (long long)j * p.in_st + 1) : 0u;
+      const uint32_t w0 = ok ? ld_src<SMEM>(src + (long long)j * fst) : 0u;
+      const uint32_t w1 = two ? ld_src<SMEM>(src + (long long)j * fst + 1) : 0u;
       bits[j] = __funnelshift_r(w0, w1, sh);
     }
     const uint4 c0 = split_row_small<K, CIN>(bits, lut, p.packed);
@@ -674,15 +690,16 @@ __device__ __forceinline__ void produce_h16s(const TcParams &p, const uint32_t *
   }
 }
 
-template <int CIN>
+template <int CIN, bool SMEM = false>
 __device__ __forceinline__ void produce_h16s_rt(const TcParams &p, const uint32_t *lut, int tile, int k,
-                                                uint32_t a_stage, int ptid) {
+                                                uint32_t a_stage, int ptid, const uint32_t *plane = nullptr) {
   int b, y0, x0;
   bool tok;
   tile_origin(p, tile, b, y0, x0, tok);
   const int K = p.K;
-  const uint32_t *frame0 = p.in + (long long)(k * K) * p.in_st + (long long)b * p.in_sb;
-  for (int row = ptid; row < kHaloRows; row += kProdWarps * 32) {
+  const uint32_t *frame0 = SMEM ? plane : p.in + (long long)(k * K) * p.in_st + (long long)b * p.in_sb;
+  const long long fst = SMEM ? (long long)p.raw_bw : p.in_st;
+  for (int row = ptid; row < kHaloRows; row += p.prod_step) {
     const int hy = row / kHaloW, hx = row - (row / kHaloW) * kHaloW;
     const int yi = y0 + hy - p.pad, xi = x0 + hx - p.pad;
     const bool ok = tok && yi >= 0 && yi < p.H && xi >= 0 && xi < p.W;
@@ -693,8 +710,8 @@ __device__ __forceinline__ void produce_h16s_rt(const TcParams &p, const uint32_
 #pragma unroll
     for (int j = 0; j < kMaxSplitK; ++j)
       if (j < K) {
-        const uint32_t w0 = ok ? __ldg(src + (long long)j * p.in_st) : 0u;
-        const uint32_t w1 = two ? __ldg(src + (long long)j * p.in_st + 1) : 0u;
+        const uint32_t w0 = ok ? ld_src<SMEM>(src + (long long)j * fst) : 0u;
+        const uint32_t w1 = two ? ld_src<SMEM>(src + (long long)j * fst + 1) : 0u;
         const uint32_t bits = __funnelshift_r(w0, w1, sh);
         i0 |= (bits & 1u) << j;
         i1 |= ((bits >> 1) & 1u) << j;
@@ -714,7 +731,7 @@ __device__ __forceinline__ void produce_s32(const TcParams &p, const uint32_t *l
   bool tok;
   tile_origin(p, tile, b, y0, x0, tok);
   const uint32_t *frame0 = p.in + (long long)(k * K) * p.in_st + (long long)b * p.in_sb;
-  for (int row = ptid; row < kHaloRows; row += kProdWarps * 32) {
+  for (int row = ptid; row < kHaloRows; row += p.prod_step) {
     const int hy = row / kHaloW, hx = row - (row / kHaloW) * kHaloW;
     const int yi = y0 + hy - p.pad, xi = x0 + hx - p.pad;
     const bool ok = tok && yi >= 0 && yi < p.H && xi >= 0 && xi < p.W;
@@ -941,8 +958,11 @@ struct RawLoader {
     const int c0 = halo_c0(p, x0) & ~3;  // 16-B aligned box start
     const uint32_t bar = bar_raw + 8 * sl;
     ptx::mbar_arrive_expect_tx(bar, p.raw_box_bytes);
-    ptx::tma_load_4d(sbase + p.off_raw + sl * p.raw_stage_bytes, &p.tmap, c0, ty * kTileH - p.pad, b,
-                     ik * p.K, bar);
+    if (p.use_tma == 2)
+      ptx::tma_load_3d(sbase + p.off_raw + sl * p.raw_stage_bytes, &p.tmap, 0, b, ik * p.K, bar);
+    else
+      ptx::tma_load_4d(sbase + p.off_raw + sl * p.raw_stage_bytes, &p.tmap, c0, ty * kTileH - p.pad, b,
+                       ik * p.K, bar);
     if (++ik == p.G) {
       ik = 0;
       ipair += ncl;
@@ -998,6 +1018,13 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
                                                   uint32_t rank, uint32_t lane, int ptid) {
   const uint32_t ns = (uint32_t)p.nstages, nr = (uint32_t)p.nraw;
   if (PATH != PATH_HALO) h16_init_stages(p, sbase, ptid);  // fenced with the first stage
+  const bool ws = p.warp_stage != 0;
+  if (ws) {  // every producer warp's init writes are visible before any warp's first stage
+    ptx::fence_proxy_async_smem();
+    ptx::named_bar_sync(1, 32 * kProdWarps);
+  }
+  const uint32_t pw = (uint32_t)ptid >> 5;
+  const int wptid = ws ? (int)lane : ptid;
   uint32_t it = 0;
   Ring st, rw;
   for (int pair = cid; pair < p.num_pairs; pair += ncl) {
@@ -1008,14 +1035,29 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
       const uint32_t s = st.i, ph = st.ph, r = rw.i, rph = rw.ph;
       st.next(ns);
       rw.next(nr);
+      if (ws && it % kProdWarps != pw) continue;  // another producer warp builds this stage
       ptx::mbar_wait(bar_raw + 8 * r, rph);
-      if (ptid == 0) trace_mark(p, it, TR_PROD_RAW);
+      if (wptid == 0) trace_mark(p, it, TR_PROD_RAW);
       ptx::mbar_wait(bar_a_empty + 8 * s, ph ^ 1u);
-      if (ptid == 0) trace_mark(p, it, TR_PROD_START);
+      if (wptid == 0) trace_mark(p, it, TR_PROD_START);
       const uint32_t *raw = reinterpret_cast<const uint32_t *>(smem + p.off_raw + r * p.raw_stage_bytes);
       const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
       const uint32_t *lut = reinterpret_cast<const uint32_t *>(smem + p.off_lut);
-      if constexpr (K == 0) {  // runtime group size: split path, C_in <= 2 (envelope)
+      const int tile = 2 * pair + (int)rank;
+      if (p.use_tma == 2) {  // plane mode: whole frames in smem, pixel-wise producers read them
+        if constexpr (PATH != PATH_HALO) {
+          if constexpr (K == 0) {
+            if (PATH == PATH_SPLIT)
+              p.Cin == 1 ? produce_h16s_rt<1, true>(p, lut, tile, k, a_stage, wptid, raw)
+                         : produce_h16s_rt<2, true>(p, lut, tile, k, a_stage, wptid, raw);
+          } else if (PATH == PATH_SPLIT) {
+            p.Cin == 1 ? produce_h16s<K, 1, true>(p, lut, tile, k, a_stage, wptid, raw)
+                       : produce_h16s<K, 2, true>(p, lut, tile, k, a_stage, wptid, raw);
+          } else {
+            produce_h16<K, true>(p, tile, k, a_stage, wptid, raw);
+          }
+        }
+      } else if constexpr (K == 0) {  // runtime group size: split path, C_in <= 2 (envelope)
         if (PATH == PATH_SPLIT)
           p.Cin == 1 ? produce_h16s_tma_rt<1>(p, lut, raw, a_stage, ptid, x0)
                      : produce_h16s_tma_rt<2>(p, lut, raw, a_stage, ptid, x0);
@@ -1036,7 +1078,7 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
         ptx::mbar_arrive_local(bar_raw_empty + 8 * r);  // this warp's reads of raw stage r are done
         ptx::mbar_arrive_cluster_cta(bar_a_full + 8 * s, 0);
       }
-      if (ptid == 0) trace_mark(p, it, TR_PROD_DONE);
+      if (wptid == 0) trace_mark(p, it, TR_PROD_DONE);
     }
   }
 }
@@ -1047,6 +1089,9 @@ __device__ __forceinline__ void producer_role(const TcParams &p, uint32_t sbase,
                                               int ncl, uint32_t rank, uint32_t lane, int ptid) {
   const uint32_t *lut = reinterpret_cast<const uint32_t *>(smem + p.off_lut);
   const uint32_t ns = (uint32_t)p.nstages;
+  const bool ws = p.warp_stage != 0;
+  const uint32_t pw = (uint32_t)ptid >> 5;
+  if (ws) ptid = (int)lane;  // each warp builds whole stages (stage it -> warp it % 3)
   uint32_t it = 0;
   Ring st;
   for (int pair = cid; pair < p.num_pairs; pair += ncl) {
@@ -1054,6 +1099,7 @@ __device__ __forceinline__ void producer_role(const TcParams &p, uint32_t sbase,
     for (int k = 0; k < p.G; ++k, ++it) {
       const uint32_t s = st.i, ph = st.ph;
       st.next(ns);
+      if (ws && it % kProdWarps != pw) continue;
       ptx::mbar_wait(bar_a_empty + 8 * s, ph ^ 1u);
       const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
       if (PATH == PATH_SPLIT && p.real) {
@@ -1733,7 +1779,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMaxStages; ++s) {
-      ptx::mbar_init(bar_a_full + 8 * s, 2 * kProdWarps);
+      ptx::mbar_init(bar_a_full + 8 * s, p.warp_stage ? 2 : 2 * kProdWarps);
       ptx::mbar_init(bar_a_empty + 8 * s, 1);
     }
     for (int a = 0; a < kAccs; ++a) {
@@ -1743,7 +1789,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
     ptx::mbar_init(bar_w, 1);
     for (int r = 0; r < kMaxRaw; ++r) {
       ptx::mbar_init(bar_raw + 8 * r, 1);
-      ptx::mbar_init(bar_raw_empty + 8 * r, kProdWarps);
+      ptx::mbar_init(bar_raw_empty + 8 * r, p.warp_stage ? 1 : kProdWarps);
     }
     ptx::fence_mbar_init();
     if (p.use_tma) ptx::prefetch_tmap(&p.tmap);
@@ -2185,11 +2231,28 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   static const bool no_tma = [] { const char *e = std::getenv("TACSNN_NO_TMA"); return e && *e == '1'; }();
   const bool tma_layout = !no_tma && !lp.xin && (lp.wpr_in * 4) % 16 == 0 && (lp.in_sb * 4) % 16 == 0 &&
                           (lp.in_st * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(lp.in) % 16) == 0;
-  Geometry g = geometry(d, tma_layout);
+  // plane mode: narrow first-layer frames (e.g. 28 x 28 x 1 = 28 words = 112 B) whose row
+  // stride is below TMA's 16-B granularity but whose whole frame is a legal box: one
+  // 3-D box [K frames][H * WPR words] per group replaces per-pixel global loads
+  const int plane = lp.H * lp.wpr_in;
+  static const bool no_plane = [] { const char *e = std::getenv("TACSNN_NO_PLANE"); return e && *e == '1'; }();
+  const bool plane_layout = !no_tma && !no_plane && !tma_layout && !lp.xin && lp.Cin <= 8 && plane <= 256 &&
+                            (plane * 4) % 16 == 0 && (lp.in_sb * 4) % 16 == 0 && (lp.in_st * 4) % 16 == 0 &&
+                            (reinterpret_cast<uintptr_t>(lp.in) % 16) == 0;
+  Geometry g = plane_layout ? geometry(d, true, plane) : geometry(d, tma_layout);
   PFN_cuTensorMapEncodeTiled_v12000 encode = g.use_tma ? tensor_map_encoder() : nullptr;
   if (!encode) g = geometry(d, false);
   TcParams p{};
-  if (g.use_tma) {
+  if (g.use_tma && plane_layout) {
+    const cuuint64_t dims[3] = {(cuuint64_t)plane, (cuuint64_t)lp.B, (cuuint64_t)lp.T};
+    const cuuint64_t strides[2] = {(cuuint64_t)lp.in_sb * 4, (cuuint64_t)lp.in_st * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)plane, 1u, (cuuint32_t)lp.K};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, (void *)lp.in, dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) g = geometry(d, false);
+  } else if (g.use_tma) {
     const int K = lp.K;
     const cuuint64_t dims[4] = {(cuuint64_t)lp.wpr_in, (cuuint64_t)lp.H, (cuuint64_t)lp.B,
                                 (cuuint64_t)lp.T};
@@ -2202,7 +2265,13 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) g = geometry(d, false);
   }
-  p.use_tma = g.use_tma;
+  p.use_tma = g.use_tma ? (plane_layout ? 2 : 1) : 0;
+  // first layers with pixel-wise producers (LDG or whole-plane TMA): a producer warp per A
+  // stage, so three stages are built concurrently (one stage's latency -- loads, table
+  // lookups, the async-proxy fence -- no longer serialises the pipeline)
+  static const bool no_ws = [] { const char *e = std::getenv("TACSNN_NO_WARP_STAGE"); return e && *e == '1'; }();
+  p.warp_stage = (!no_ws && g.path != PATH_HALO && p.use_tma != 1) ? 1 : 0;
+  p.prod_step = p.warp_stage ? 32 : 32 * kProdWarps;
   p.raw_bw = g.raw_bw;
   p.nraw = g.nraw;
   p.off_raw = g.off_raw;

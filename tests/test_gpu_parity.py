@@ -444,7 +444,7 @@ def test_mnist_T25_on_tcgen05(T, O, K):
     groups (K' = 1, 1, 9), every layer of the C2-shaped stack on the tensor cores."""
     from paper_2603_13810_b200 import configs
     cfg = configs.CONFIGS["C2"]
-    specs = configs.layer_plan(cfg, mode="tac", K=K, B=3, T=25)
+    specs = configs.layer_plan(cfg, mode="tac", K=K, B=3, T=25, engine="tcgen05")
     assert all(s.engine_used() == "tcgen05" for s in specs), [s.engine_used() for s in specs]
     S = configs.make_inputs(cfg, B=3, T=25).numpy()
     stats = P.check_stack(T, O, specs, configs.layer_weights(cfg), S, label=f"C2@T25/K{K}")
@@ -595,3 +595,4 @@ def test_c5_full_size_sampled(T, O):
             assert np.array_equal(counts[i][bsel].cpu().numpy().astype(np.int64),
                                   st["counts"][0]), f"counts layer {i} sample {bsel}"
             S, x_dev = ref_out, dev_out
+
