@@ -162,7 +162,7 @@ typedef struct tac_plan {
   size_t bytes;          /* size of the image                                               */
   uint64_t fingerprint;  /* of the descriptor at preparation (opaque)                       */
   int32_t abi_version;   /* TACSNN_ABI_VERSION of the library that prepared it              */
-  int32_t reserved;
+  int32_t scale_code;    /* library-private: the image's operand prescale exponents; do not modify */
 } tac_plan;
 
 /* Validate a descriptor (no device access).  TAC_OK or the first violation. */

@@ -325,6 +325,8 @@ tac_status tac_prepare_weights(const tac_conv_lif_desc *desc, const float *weigh
     parts.push_back(*desc);
   }
   size_t base = 0;
+  uint32_t code = 0;  // fp16-path prescale exponent of each image part (plan->scale_code)
+  int part = 0;
   for (const tac_conv_lif_desc &pd : parts) {
     const PrepLayout L = prep_layout(&pd);
     float *ws = reinterpret_cast<float *>(img.data() + base + L.simt_off);
@@ -335,8 +337,12 @@ tac_status tac_prepare_weights(const tac_conv_lif_desc *desc, const float *weigh
             ws[((size_t)(ci * R + r) * S + s) * Co + co] = weight[((size_t)(co * Ci + ci) * R + r) * S + s];
     float *bs = reinterpret_cast<float *>(img.data() + base + L.bias_off);
     for (int co = 0; co < Co; ++co) bs[co] = bias ? bias[co] : 0.f;
-    if (L.tc_bytes) tacsnn::tc_prepare(&pd, weight, bias, img.data() + base + L.tc_off);
+    if (L.tc_bytes) {
+      const int e = tacsnn::tc_prepare(&pd, weight, bias, img.data() + base + L.tc_off);
+      code |= (uint32_t)(uint8_t)(int8_t)e << (8 * part);
+    }
     base += L.total;
+    ++part;
   }
   cudaError_t e = cudaMemcpyAsync(prepared, img.data(), total, cudaMemcpyHostToDevice,
                                   (cudaStream_t)stream);
@@ -346,13 +352,17 @@ tac_status tac_prepare_weights(const tac_conv_lif_desc *desc, const float *weigh
   plan->bytes = total;
   plan->fingerprint = fingerprint(desc, g, is_split_call(desc, g));
   plan->abi_version = TACSNN_ABI_VERSION;
-  plan->reserved = 0;
+  plan->scale_code = (int32_t)code;
   return TAC_OK;
 }
 
 }  // extern "C"
 
 namespace {
+// fp16-path operand prescale exponent of image part `part` (0: the whole / full-group
+// image, 1: the short last group's), as tac_prepare_weights recorded it
+int plan_exp(const tac_plan *plan, int part) { return (int)(int8_t)((uint32_t)plan->scale_code >> (8 * part)); }
+
 // Argument checks of one (non-split) launch, before anything is enqueued.
 tac_status validate_call(const tac_conv_lif_desc *desc, const void *prepared, const void *input,
                          bool real, const float *v_init, const uint32_t *spikes_out,
@@ -384,7 +394,7 @@ tac_status validate_call(const tac_conv_lif_desc *desc, const void *prepared, co
 
 // Enqueue one validated (non-split) call.
 tac_status launch_call(const tac_conv_lif_desc *desc, const Geo &g, int engine, const void *prepared,
-                       const void *input, bool real, const float *v_init, uint32_t *spikes_out,
+                       int yexp, const void *input, bool real, const float *v_init, uint32_t *spikes_out,
                        float *v_final, uint32_t *counts, void *stream, int *launches,
                        float *y_seq = nullptr) {
   tacsnn::LayerParams p{};
@@ -405,6 +415,7 @@ tac_status launch_call(const tac_conv_lif_desc *desc, const Geo &g, int engine, 
   p.out = spikes_out; p.v_init = v_init; p.v_final = v_final; p.counts = counts;
   p.xin = real ? static_cast<const float *>(input) : nullptr;
   p.y_seq = y_seq;
+  p.yscale_exp = yexp;
   const PrepLayout L = prep_layout(desc);
   const unsigned char *base = static_cast<const unsigned char *>(prepared);
   p.w = reinterpret_cast<const float *>(base + L.simt_off);
@@ -449,7 +460,7 @@ tac_status forward_impl(const tac_conv_lif_desc *desc, const tac_plan *plan, con
     int engine;
     st = validate_call(desc, prepared, input, real, v_init, spikes_out, v_final, counts, &engine);
     if (st != TAC_OK) return st;
-    st = launch_call(desc, g, engine, prepared, input, real, v_init, spikes_out, v_final, counts, stream,
+    st = launch_call(desc, g, engine, prepared, plan_exp(plan, 0), input, real, v_init, spikes_out, v_final, counts, stream,
                      &launches);
     if (st == TAC_OK) g_launches = launches;
     return st;
@@ -461,7 +472,7 @@ tac_status forward_impl(const tac_conv_lif_desc *desc, const tac_plan *plan, con
     int engine;
     st = validate_call(&last, prepared, input, real, v_init, spikes_out, v_final, counts, &engine);
     if (st != TAC_OK) return st;
-    st = launch_call(&last, gl, engine, prepared, input, real, v_init, spikes_out, v_final, counts, stream,
+    st = launch_call(&last, gl, engine, prepared, plan_exp(plan, 0), input, real, v_init, spikes_out, v_final, counts, stream,
                      &launches);
     if (st == TAC_OK) g_launches = launches;
     return st;
@@ -488,10 +499,10 @@ tac_status forward_impl(const tac_conv_lif_desc *desc, const tac_plan *plan, con
   if ((st = validate_call(&last, prep2, in2, real, v_mid, out2, v_final, counts ? cnt2 : nullptr, &eng2)) !=
       TAC_OK)
     return st;
-  if ((st = launch_call(&full, gf, eng1, prepared, input, real, v_init, spikes_out, v_mid, counts, stream,
+  if ((st = launch_call(&full, gf, eng1, prepared, plan_exp(plan, 0), input, real, v_init, spikes_out, v_mid, counts, stream,
                         &launches)) != TAC_OK)
     return st;
-  if ((st = launch_call(&last, gl, eng2, prep2, in2, real, v_mid, out2, v_final, counts ? cnt2 : nullptr,
+  if ((st = launch_call(&last, gl, eng2, prep2, plan_exp(plan, 1), in2, real, v_mid, out2, v_final, counts ? cnt2 : nullptr,
                         stream, &launches)) != TAC_OK)
     return st;
   if (counts) {
@@ -566,7 +577,7 @@ tac_status tac_conv_lif_forward_train(const tac_conv_lif_desc *desc, const tac_p
   st = validate_call(desc, plan->prepared, input, real, v_init, spikes_out, v_final, counts, &engine);
   if (st != TAC_OK) return st;
   int launches = 0;
-  st = launch_call(desc, g, engine, plan->prepared, input, real, v_init, spikes_out, v_final, counts, stream,
+  st = launch_call(desc, g, engine, plan->prepared, plan_exp(plan, 0), input, real, v_init, spikes_out, v_final, counts, stream,
                    &launches, y_seq);
   if (st == TAC_OK) g_launches = launches;
   return st;

@@ -32,6 +32,7 @@ struct LayerParams {
   const float *w;     // SIMT weights, fp32 [Cin][R][S][Cout]
   const float *bias;  // fp32 [Cout]
   float *y_seq;       // training forward: per-group drive [G][B][Ho][Wo][Cout] as the LIF consumed it
+  int yscale_exp;     // tcgen05 fp16 paths: the image's operand prescale 2^e (tac_plan::scale_code)
 };
 
 enum { MODE_DENSE = 0, MODE_TAC = 1, MODE_TACTP = 2 };

@@ -14,8 +14,11 @@ bool tc_shape_ok(const tac_conv_lif_desc *d);
 bool tc_supported(const tac_conv_lif_desc *d);
 const char *tc_unsupported_reason(const tac_conv_lif_desc *d);
 size_t tc_weights_bytes(const tac_conv_lif_desc *d);
-void tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bias,
-                unsigned char *dst);
+// builds the tcgen05 image; returns the exponent e of the fp16-path operand prescale
+// 2^e (0 on the int8 path), which the caller keeps in the plan and passes back in
+// LayerParams::yscale_exp
+int tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bias,
+               unsigned char *dst);
 // backward replay of the forward integrator: does the subtract epilogue run in the
 // shifted state U = V - v_th with the (decay - 1) v_th offset folded into Y (tc.cu)?
 bool tc_u_domain(const tac_conv_lif_desc *d);

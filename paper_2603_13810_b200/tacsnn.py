@@ -52,7 +52,7 @@ class Plan(ctypes.Structure):
     """Mirror of tac_plan (filled by tac_prepare_weights)."""
     _fields_ = [("prepared", ctypes.c_void_p), ("bytes", ctypes.c_size_t),
                 ("fingerprint", ctypes.c_uint64), ("abi_version", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("scale_code", ctypes.c_int32)]
 
 
 class GradDesc(ctypes.Structure):

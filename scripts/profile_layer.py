@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--engine", default="auto")
     ap.add_argument("--mode", default=None)
     ap.add_argument("--K", type=int, default=None)
+    ap.add_argument("--no-counts", action="store_true", help="as the bench (counts on the last layer only)")
     a = ap.parse_args()
     cfg = configs.CONFIGS[a.config]
     specs = configs.layer_plan(cfg, mode=a.mode, K=a.K, B=a.B, engine=a.engine)
@@ -40,7 +41,7 @@ def main():
     for _ in range(a.iters):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        out, _, cnt = tacsnn.conv_lif(spec, prep, x, out=out)
+        out, _, cnt = tacsnn.conv_lif(spec, prep, x, out=out, want_counts=not a.no_counts)
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
@@ -49,8 +50,8 @@ def main():
     flops = 2.0 * spec.C_out * hc * wc * spec.C_in * 9 * G * spec.B
     print(f"layer {a.layer} {spec} engine={spec.engine_used()}")
     for t in times:
-        print(f"  {t:.3f} ms  useful {flops / t / 1e9:.1f} TFLOP/s  "
-              f"rate {cnt.sum().item() / (spec.B * spec.C_out * hc * wc * spec.T):.4f}")
+        rate = "" if cnt is None else f"rate {cnt.sum().item() / (spec.B * spec.C_out * hc * wc * spec.T):.4f}"
+        print(f"  {t:.3f} ms  useful {flops / t / 1e9:.1f} TFLOP/s  {rate}")
 
 
 if __name__ == "__main__":
