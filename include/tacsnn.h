@@ -295,6 +295,16 @@ tac_status tac_or_pool2_backward(const uint32_t *spikes_prepool, const float *g_
                                  float *g_prepool, int32_t T, int32_t B, int32_t C, int32_t H,
                                  int32_t W, void *stream);
 
+/* VotingLayer readout of the DVS network ("LIF -> VotingLayer(10 voters,
+ * 11 classes)", :595): the class score is the mean firing rate of the class's voters,
+ *   scores[b][j] = (sum_{v < voters} counts[b][j voters + v]) / (voters T_out)
+ * (the sum is exact in u32, one fp32 division).  counts u32 [B][C] (device, e.g. the
+ * counts of the last FC-LIF layer), C % voters == 0; scores fp32 [B][C / voters]
+ * (device, overwritten).  TAC_ERR_SHAPE on a bad extent, TAC_ERR_NULL / _ALIGN on
+ * bad pointers; nothing is launched on error. */
+tac_status tac_vote(const uint32_t *counts, int32_t B, int32_t C, int32_t voters, int32_t T_out,
+                    float *scores, void *stream);
+
 /* u8 {0,1} [T][B][C][H][W] (device) <-> packed [T][B][H][WPR] (device).
  * pack treats any non-zero byte as a spike. */
 tac_status tac_pack_spikes(const uint8_t *dense01, uint32_t *packed, int32_t T,

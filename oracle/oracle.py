@@ -207,6 +207,16 @@ def backward(S, Wt, bias, g_out, *, K=1, mode="tac", beta=0.9, v_th=1.0, stride=
     return dict(g_W=g_W, g_b=g_b, g_in=g_in, g_vinit=g_vinit, g_alpha=g_alpha)
 
 
+def vote(counts, voters, T_out):
+    """VotingLayer of the DVS network ("VotingLayer(10 voters, 11 classes)",
+    :595): class j's score is the mean firing rate of its voters j*voters .. j*voters +
+    voters - 1, i.e. their spike counts summed and divided by voters * T_out (fp64)."""
+    counts = np.asarray(counts, dtype=np.float64)
+    B, C = counts.shape
+    assert C % voters == 0
+    return counts.reshape(B, C // voters, voters).sum(axis=2) / (voters * T_out)
+
+
 def or_pool2(x):
     """2x2 OR-pool of binary maps (P:235 MaxPool(2) on {0,1}); x [..., C, H, W].
     Odd extents: floor mode (the last row / column is dropped, as MaxPool2d)."""

@@ -1,7 +1,7 @@
 """The five BASELINE.json workloads (configs C1-C5) as stacks of Conv-LIF layers.
 
-Architectures follow PAPER.md:234-235 restricted to the conv blocks (FC layers
-and the VotingLayer are out of the hot path):
+Architectures follow PAPER.md:234-235; layer_plan is the conv blocks, network_plan the
+whole network with its FC head (see below):
   MNIST/FMNIST: Conv(1->32,3,pad 0)->LIF->Pool(2)->Conv(32->64,3,pad 0)->LIF
                 (pad 0 from FC(1600)=64*5*5; the odd 11x11
                 output of layer 2 is left unpooled, reading D13)
@@ -24,6 +24,7 @@ GAINS = {
     "mnist": [0.78, 0.46],
     "mnist_fc": [2.0, 2.0],   # FC(1600->128), FC(128->10) of the whole network (set below)
     "dvs": [7.1, 1.08, 1.01, 1.01, 0.89],
+    "dvs_fc": [0.81, 1.48],   # FC(2048->512), FC(512->110) of the DVS network (--head, C4 B=2)
 }
 
 
@@ -139,22 +140,52 @@ def conv_calls(cfg: Config, mode: str | None = None, K: int | None = None, T: in
     return sum(-(-s.T // (1 if s.mode == "dense" else s.K)) for s in layer_plan(cfg, mode, K, B=1, T=T))
 
 
-# --- whole MNIST/FMNIST network: conv stack + FC head ------
-# Conv(1->32)->LIF->Pool(2)->Conv(32->64)->LIF->Pool(2) [11x11 -> 5x5, floor]
-# ->FC(1600->128)->LIF->FC(128->10)->LIF; the FC layers are 1x1
-# "convolutions" of a 1x1 image (C_in = 1600 / 128), TAC-aggregated like the convs
-# (they are linear too); the readout is the final layer's spike counts.
+# --- whole networks: conv stack + FC head ----------------------
+# MNIST/FMNIST: Conv(1->32)->LIF->Pool(2)->Conv(32->64)->LIF->Pool(2) [11x11 -> 5x5,
+#   floor] ->FC(1600->128)->LIF->FC(128->10)->LIF; readout = the final
+#   layer's spike counts ("LIF + spike count").
+# DVS: 5 x {Conv(128)->LIF->MaxPool(2)} ->FC(->512)->LIF->FC(512->110)->LIF->VotingLayer
+#   (10 voters, 11 classes; FC widths SURVEY.md App. A 7).  At the
+#   paper's 64x64 input the flattened map is 2x2x128 = 512; the BASELINE configs'
+#   128x128 input gives 4x4x128 = 2048 (reading D14).  The VotingLayer averages the
+#   firing rates of each class's 10 voters (tac_vote).
+# The FC layers are 1x1 "convolutions" of a 1x1 image (C_in = flattened map), TAC-
+# aggregated like the convs (they are linear too) and run on the tcgen05 FC kernel.
+HEADS = {"mnist": (128, 10), "dvs": (512, 110)}
+VOTERS = {"mnist": None, "dvs": 10}
+
+
+def head_kind(cfg: Config) -> str:
+    return "dvs" if cfg.inputs == "dvs" else "mnist"
+
+
+def _flat_in(cfg: Config) -> int:
+    h, w = cfg.H, cfg.W
+    for L in cfg.layers:
+        h, w = h + 2 * L.pad - 2, w + 2 * L.pad - 2
+        if L.pool == 2 or cfg.inputs != "dvs":   # MNIST pools both blocks (layer 2 floor 11 -> 5)
+            h, w = h // 2, w // 2
+    return h * w * cfg.layers[-1].C_out
+
+
+def head_dims(cfg: Config):
+    """((C_in, C_out) of FC 1, (C_in, C_out) of FC 2)."""
+    h1, h2 = HEADS[head_kind(cfg)]
+    return ((_flat_in(cfg), h1), (h1, h2))
+
+
 def network_plan(cfg: Config, mode: str | None = None, K: int | None = None, B: int | None = None,
                  engine: str = "auto", T: int | None = None):
     from .tacsnn import LayerSpec
-    assert cfg.inputs in ("mnist", "fmnist"), "whole-network plan: MNIST-shaped configs"
     convs = layer_plan(cfg, mode=mode, K=K, B=B, engine=engine, T=T)
-    convs[1] = convs[1].replace(out_pool=2)            # 11x11 -> 5x5 (floor)
+    if head_kind(cfg) == "mnist":
+        convs[1] = convs[1].replace(out_pool=2)        # 11x11 -> 5x5 (floor)
     mode = mode or cfg.mode
     K = cfg.K if K is None else K
-    t = convs[1].T if mode != "tac" else -(-convs[1].T // convs[1].K)
+    last = convs[-1]
+    t = last.T if mode != "tac" else -(-last.T // last.K)
     specs = list(convs)
-    for c_in, c_out in ((64 * 5 * 5, 128), (128, 10)):
+    for c_in, c_out in head_dims(cfg):
         Kl = 1 if mode == "dense" else min(K, t)
         specs.append(LayerSpec(T=t, B=convs[0].B, C_in=c_in, H=1, W=1, C_out=c_out, R=1, S=1,
                                stride=1, pad=0, K=Kl, mode=mode, beta=cfg.beta, v_th=1.0,
@@ -168,6 +199,6 @@ def network_plan(cfg: Config, mode: str | None = None, K: int | None = None, B: 
 def network_weights(cfg: Config, seed: int | None = None):
     seed = cfg.seeds[0] if seed is None else seed
     w = layer_weights(cfg, seed)
-    for i, ((c_in, c_out), g) in enumerate(zip(((1600, 128), (128, 10)), GAINS["mnist_fc"])):
+    for i, ((c_in, c_out), g) in enumerate(zip(head_dims(cfg), GAINS[head_kind(cfg) + "_fc"])):
         w.append(synth.weights(seed * 1000 + 10 + i, c_out, c_in, 1, 1, gain=g))
     return w

@@ -681,6 +681,19 @@ tac_status tac_or_pool2_backward(const uint32_t *spikes_prepool, const float *g_
   return TAC_OK;
 }
 
+tac_status tac_vote(const uint32_t *counts, int32_t B, int32_t C, int32_t voters, int32_t T_out,
+                    float *scores, void *stream) {
+  g_detail.clear();
+  if (!counts || !scores) return fail(TAC_ERR_NULL, "NULL buffer");
+  if (B < 1 || C < 1 || voters < 1 || T_out < 1 || C % voters)
+    return fail(TAC_ERR_SHAPE, "need B, C, voters, T_out >= 1 and C %% voters == 0");
+  if ((uintptr_t)counts % 4 || (uintptr_t)scores % 4) return fail(TAC_ERR_ALIGN, "misaligned");
+  const int e = tacsnn::launch_vote(counts, B, C, voters, T_out, scores, stream);
+  if (e) return fail(TAC_ERR_CUDA, "vote: %s", cudaGetErrorString((cudaError_t)e));
+  g_launches = 1;
+  return TAC_OK;
+}
+
 tac_status tac_pack_spikes(const uint8_t *dense01, uint32_t *packed, int32_t T, int32_t B,
                            int32_t C, int32_t H, int32_t W, void *stream) {
   g_detail.clear();

@@ -42,6 +42,7 @@ enum { RESET_SUBTRACT = 0, RESET_DELAYED = 1, RESET_HARD = 2 };
 int launch_zero_outputs(const LayerParams &p, void *stream, int *launches);
 int launch_simt_conv_lif(const LayerParams &p, void *stream, int *launches);
 int launch_add_u32(uint32_t *dst, const uint32_t *src, long long n, void *stream);  // dst += src
+int launch_vote(const uint32_t *counts, int B, int C, int voters, int T_out, float *scores, void *stream);
 int launch_pack(const uint8_t *dense, uint32_t *packed, int T, int B, int C, int H,
                 int W, void *stream);
 int launch_unpack(const uint32_t *packed, uint8_t *dense, int T, int B, int C, int H,

@@ -279,6 +279,24 @@ int launch_add_u32(uint32_t *dst, const uint32_t *src, long long n, void *stream
   return (int)cudaGetLastError();
 }
 
+// VotingLayer (tac_vote): one thread per (sample, class)
+__global__ void vote_kernel(const uint32_t *counts, int B, int C, int voters, float inv, float *scores) {
+  const int ncls = C / voters;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)B * ncls) return;
+  const long long b = i / ncls, j = i - b * ncls;
+  const uint32_t *c = counts + b * C + j * voters;
+  uint32_t s = 0;
+  for (int v = 0; v < voters; ++v) s += c[v];
+  scores[i] = (float)s * inv;
+}
+int launch_vote(const uint32_t *counts, int B, int C, int voters, int T_out, float *scores, void *stream) {
+  const long long n = (long long)B * (C / voters);
+  const float inv = (float)(1.0 / ((double)voters * T_out));
+  vote_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(counts, B, C, voters, inv, scores);
+  return (int)cudaGetLastError();
+}
+
 int launch_simt_conv_lif(const LayerParams &p, void *stream, int *launches) {
   if (p.H == 1 && p.W == 1 && p.R == 1 && p.S == 1 && p.pad == 0 && p.pool == 1) {
     fc_lif_kernel<<<dim3((unsigned)p.B, (unsigned)((p.Cout + 31) / 32)), 32 * FC_WARPS, 0,

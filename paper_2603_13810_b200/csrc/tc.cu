@@ -26,11 +26,13 @@ __global__ void tc_zero_kernel(uint32_t *out, int T_out, int B, long long plane,
 
 // ------------------------------------------------------------------ host API --
 static bool lif_u_state(const tac_conv_lif_desc *d);
-bool tc_u_domain(const tac_conv_lif_desc *d) { return lif_u_state(d); }
-bool tc_shape_ok(const tac_conv_lif_desc *d) { return shape_reason(d) == nullptr; }
-bool tc_supported(const tac_conv_lif_desc *d) { return reason(d) == nullptr; }
+bool tc_u_domain(const tac_conv_lif_desc *d) { return !fc_is_fc(d) && lif_u_state(d); }
+bool tc_shape_ok(const tac_conv_lif_desc *d) {
+  return fc_is_fc(d) ? fc_reason(d) == nullptr : shape_reason(d) == nullptr;
+}
+bool tc_supported(const tac_conv_lif_desc *d) { return fc_is_fc(d) ? fc_reason(d) == nullptr : reason(d) == nullptr; }
 const char *tc_unsupported_reason(const tac_conv_lif_desc *d) {
-  const char *r = reason(d);
+  const char *r = fc_is_fc(d) ? fc_reason(d) : reason(d);
   return r ? r : "supported";
 }
 
@@ -54,10 +56,12 @@ static size_t scale_off(const Geometry &g) { return 2 * (size_t)g.w_bytes_cta; }
 static size_t yscale_off(const Geometry &g) { return scale_off(g) + 16 * (size_t)g.cout_pad; }
 static size_t lut_off(const Geometry &g) { return yscale_off(g) + 16; }
 size_t tc_weights_bytes(const tac_conv_lif_desc *d) {
+  if (fc_is_fc(d)) return fc_weights_bytes(d);
   const Geometry g = geometry(d);
   return lut_off(g) + (g.split ? 4 * (size_t)kLutWords : 0);
 }
 const float *tc_yscale_ptr(const tac_conv_lif_desc *d, const unsigned char *tc_prep) {
+  if (fc_is_fc(d)) return nullptr;  // the FC epilogue hands the LIF the unscaled Y (V domain)
   const Geometry g = geometry(d);
   return g.path == PATH_HALO ? nullptr : reinterpret_cast<const float *>(tc_prep + yscale_off(g));
 }
@@ -68,6 +72,7 @@ const float *tc_yscale_ptr(const tac_conv_lif_desc *d, const unsigned char *tc_p
 // followed by fp32 [s1/254 | bias | s1 | s2] per padded output channel.
 int tc_prepare(const tac_conv_lif_desc *d, const float *weight, const float *bias,
                unsigned char *dst) {
+  if (fc_is_fc(d)) return fc_prepare(d, weight, dst);
   const Geometry g = geometry(d);
   const int Co = d->C_out, Ci = d->C_in, Cp = g.cout_pad;
   std::vector<signed char> q1((size_t)Cp * Ci * 9, 0), q2((size_t)Cp * Ci * 9, 0);
@@ -261,6 +266,7 @@ extern "C" void tac_debug_set_trace(void *dev) {
 
 int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned char *tc_prep,
               void *stream, int *launches) {
+  if (fc_is_fc(d)) return fc_launch(d, lp, tc_prep, stream, launches);
   // TMA raw-halo producer when the packed input is a legal 4-D tensor-map view
   // (16-B aligned base and strides) and the plan fits in shared memory
   static const bool no_tma = [] { const char *e = std::getenv("TACSNN_NO_TMA"); return e && *e == '1'; }();

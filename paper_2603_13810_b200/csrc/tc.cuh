@@ -27,4 +27,13 @@ const float *tc_yscale_ptr(const tac_conv_lif_desc *d, const unsigned char *tc_p
 int tc_launch(const tac_conv_lif_desc *d, const LayerParams &p, const unsigned char *tc_prep,
               void *stream, int *launches);
 
+// fully connected layers (H = W = R = S = 1) on tcgen05 (fc.cu); the tc_* entry points
+// above dispatch to these for such shapes
+bool fc_is_fc(const tac_conv_lif_desc *d);
+const char *fc_reason(const tac_conv_lif_desc *d);  // NULL when the FC kernel can run it
+size_t fc_weights_bytes(const tac_conv_lif_desc *d);
+int fc_prepare(const tac_conv_lif_desc *d, const float *weight, unsigned char *dst);
+int fc_launch(const tac_conv_lif_desc *d, const LayerParams &p, const unsigned char *img, void *stream,
+              int *launches);
+
 }  // namespace tacsnn

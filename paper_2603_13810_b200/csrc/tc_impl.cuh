@@ -1351,9 +1351,13 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int cc = ch * 8 + q;
-        float v0 = 0.f;
-        if (p.v_init && valid && co_base + cc < Cout) v0 = __ldg(p.v_init + vbase + cc);
-        const float u0 = (v0 - vth) * ysc;
+        // V_0 = v_init, or 0 (U_0 = -v_th 2^e, a kernel constant: no per-tile loads)
+        float u0 = p.nvth_s;
+        if (p.v_init) {
+          float v0 = 0.f;
+          if (valid && co_base + cc < Cout) v0 = __ldg(p.v_init + vbase + cc);
+          u0 = (v0 - vth) * ysc;
+        }
         ub[q] = __float_as_uint(u0);
         if (!UT) {
           if (q & 1) U[UT ? 0 : cc / 2].y = u0; else U[UT ? 0 : cc / 2].x = u0;
@@ -1474,7 +1478,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
 
       uint32_t spk[NS];
 #pragma unroll
-      for (int j = 0; j < NS; ++j) spk[j] = ~nsp[j] & vmask;
+      for (int j = 0; j < NS; ++j) TAC_LOP3(spk[j], nsp[j], vmask, vmask, 0x0C);  // ~nsp & vmask, one LOP3
       // per-lane bit-sliced spike counters (pre-pool, valid pixels only; skipped when
       // the caller asked for no counts)
       if (!p.counts) {
@@ -1500,14 +1504,14 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
 #pragma unroll
       for (int j = 0; j < NS; ++j) pw[j] |= pooled ? __shfl_xor_sync(0xFFFFFFFFu, pw[j], 8) : 0u;
 #pragma unroll
-      for (int j = 0; j < NS; ++j) {
+      for (int j = 0; j < NS; ++j) {  // one 64-bit pointer step per stored word
         if (NCH >= 32) {
-          ptx::st_global_pred(optr + j * out_st, pw[j], store_lane);
+          ptx::st_global_pred(optr, pw[j], store_lane);
         } else if (store_lane && pw[j]) {
-          atomicOr(optr + j * out_st, pw[j] << osh);
+          atomicOr(optr, pw[j] << osh);
         }
+        optr += out_st;
       }
-      optr += NS * out_st;
       steps_acc += NS;
       if (p.counts && (steps_acc + NS > (1 << kPlanes) - 1 || k == G - 1)) {
         if (tok) {

@@ -24,9 +24,12 @@ def flatten_for(spec: LayerSpec, x: torch.Tensor) -> torch.Tensor:
 
 
 class Network:
-    def __init__(self, specs: list[LayerSpec], weights, device="cuda"):
+    def __init__(self, specs: list[LayerSpec], weights, device="cuda", voters: int | None = None):
+        """voters: the VotingLayer size of the DVS network (10); None for the
+        spike-count readout (MNIST/FMNIST)."""
         assert len(specs) == len(weights)
         self.specs = list(specs)
+        self.voters = voters
         self.device = torch.device(device)
         self.prepared = [tacsnn.prepare_weights(s, w, b, device=self.device)
                          for s, (w, b) in zip(self.specs, weights)]
@@ -53,6 +56,16 @@ class Network:
             if keep:
                 outs.append(x)
         return x, counts, outs, vfs
+
+    def readout(self, counts_last: torch.Tensor) -> torch.Tensor:
+        """Class scores of the network from the last layer's spike counts [B, C_out]: the
+        VotingLayer (tac_vote: each class's voters' mean firing rate) when the network has
+        voters, else the firing rates count / T_out."""
+        last = self.specs[-1]
+        T_out = last.out_shape()[0]
+        if self.voters:
+            return tacsnn.vote(counts_last, self.voters, T_out)
+        return tacsnn.vote(counts_last, 1, T_out)
 
     def capture(self, x: torch.Tensor):
         """Record one forward on the static input buffer `x` as a CUDA graph (the

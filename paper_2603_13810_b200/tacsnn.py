@@ -32,7 +32,7 @@ EXPORTS = ("tac_desc_check", "tac_out_shape", "tac_select_engine", "tac_weights_
            "tac_pack_spikes", "tac_unpack_spikes", "tac_status_string",
            "tac_last_error_detail", "tac_abi_version", "tac_last_launch_count",
            "tac_debug_set_trace", "tac_conv_lif_forward_train", "tac_backward_workspace_bytes",
-           "tac_conv_lif_backward", "tac_or_pool2", "tac_or_pool2_backward")
+           "tac_conv_lif_backward", "tac_or_pool2", "tac_or_pool2_backward", "tac_vote")
 SURROGATES = {"fast_sigmoid": 0, "arctan": 1}
 
 
@@ -110,6 +110,7 @@ def lib():
                                            P, P, P, P, P, P, sz, P], i32),
                 "tac_or_pool2": ([P, P, i32, i32, i32, i32, i32, P], i32),
                 "tac_or_pool2_backward": ([P, P, P, i32, i32, i32, i32, i32, P], i32),
+                "tac_vote": ([P, i32, i32, i32, i32, P, P], i32),
             }
             for name, (args, res) in sig.items():
                 f = getattr(L, name)
@@ -343,6 +344,16 @@ def or_pool2_backward(pre: torch.Tensor, g_pooled: torch.Tensor, C: int, W: int)
     _check(lib().tac_or_pool2_backward(_ptr(pre.contiguous()), _ptr(g_pooled.contiguous()), _ptr(g), T, B, C, H,
                                        W, _stream(pre.device)))
     return g
+
+
+def vote(counts: torch.Tensor, voters: int, T_out: int) -> torch.Tensor:
+    """VotingLayer (tac_vote): counts int32 [B, C] -> fp32 class scores [B, C // voters],
+    the mean firing rate of each class's voters."""
+    assert counts.is_cuda and counts.dtype == torch.int32 and counts.is_contiguous() and counts.dim() == 2
+    B, C = counts.shape
+    scores = torch.empty((B, C // voters), dtype=torch.float32, device=counts.device)
+    _check(lib().tac_vote(_ptr(counts), B, C, voters, T_out, _ptr(scores), _stream(counts.device)))
+    return scores
 
 
 def pack(dense: torch.Tensor) -> torch.Tensor:

@@ -29,7 +29,11 @@ def main():
     ap.add_argument("--B", type=int, default=2)
     ap.add_argument("--target", type=float, default=0.1)
     ap.add_argument("--iters", type=int, default=8)
+    ap.add_argument("--head", action="store_true",
+                    help="keep the frozen conv gains and calibrate the FC head (network_plan)")
     a = ap.parse_args()
+    if a.head:
+        return calibrate_head(a)
     cfg = configs.CONFIGS[a.config]
     x = configs.make_inputs(cfg, B=a.B).numpy()
     t = cfg.T
@@ -56,6 +60,40 @@ def main():
         if cfg.mode == "tac":
             t //= K
     print("GAINS", gains)
+
+
+def calibrate_head(a):
+    """FC head gains: the conv stack runs with its frozen gains, its (pooled) output is
+    flattened in (h, w, c) order (the packed row layout) and each FC layer's gain is bisected."""
+    cfg = configs.CONFIGS[a.config]
+    specs = configs.network_plan(cfg, B=a.B)
+    weights = configs.layer_weights(cfg)
+    x = configs.make_inputs(cfg, B=a.B).numpy()
+    nconv = len(cfg.layers)
+    for s, (w, b) in zip(specs[:nconv], weights):
+        r = O.forward(x, w.numpy(), b.numpy(), K=s.K, mode=s.mode, beta=s.beta, pad=s.pad,
+                      partial=s.partial)
+        x = O.or_pool2(r["out"]) if s.out_pool == 2 else r["out"]
+        print(f"  conv rate {float(r['out'].mean()):.4f}", flush=True)
+    Tn, Bn = x.shape[:2]
+    x = np.ascontiguousarray(x.transpose(0, 1, 3, 4, 2).reshape(Tn, Bn, -1, 1, 1))
+    gains = []
+    for i, s in enumerate(specs[nconv:]):
+        lo, hi = 0.25, 32.0
+        best = None
+        for _ in range(a.iters):
+            g = math.sqrt(lo * hi)
+            w, b = synth.weights(cfg.seeds[0] * 1000 + 10 + i, s.C_out, s.C_in, 1, 1, gain=g)
+            r = O.forward(x, w.numpy(), b.numpy(), K=s.K, mode=s.mode, beta=s.beta, pad=0,
+                          partial=s.partial)
+            rate = float(r["out"].mean())
+            best = (g, rate, r["out"])
+            print(f"  FC {i} gain {g:.3f} rate {rate:.4f}", flush=True)
+            lo, hi = (g, hi) if rate < a.target else (lo, g)
+        g, rate, out = best
+        gains.append(round(g, 2))
+        x = out
+    print("FC GAINS", gains)
 
 
 if __name__ == "__main__":

@@ -8,7 +8,11 @@ independence check of SURVEY.md section 8(d).
 One JSON line per (config, mode, K): device ms per forward of the whole conv stack
 (CUDA events on the launch stream, inputs resident, after warm-up), input
 spike-frames/s, per-layer ms and engines, logical conv calls per sample
-(sum_l T_l / K_l) and the speedup over the config's dense run.
+(sum_l T_l / K_l) and the speedup over the config's dense run,
+the slowest layer's roofline fractions (LIF ops vs the 148 x 128-lane ALU issue peak,
+useful conv FLOP/s vs the tensor peak of its operand type, packed bytes vs HBM) and the
+SM clocks / throttle reasons sampled while the line was timed.  "+FC" lines are the
+whole networks (conv stack + FC head, the DVS one with the VotingLayer readout).
 """
 import argparse
 import json
@@ -21,6 +25,25 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 from paper_2603_13810_b200 import configs, network, tacsnn  # noqa: E402
+import bench  # noqa: E402  (peaks, clock sampler, per-layer work counts)
+
+PEAKS = bench.load_peaks()
+
+
+def roofline(specs, layer_ms, B, engines):
+    """Roofline fractions of the slowest layer (per-sample work x B / its time)."""
+    i = max(range(len(layer_ms)), key=lambda j: layer_ms[j])
+    t = layer_ms[i] / 1e3
+    ns = bench.neuron_steps_per_sample(specs)[i] * B
+    fl = bench.useful_flops_per_sample(specs)[i] * B
+    by = bench.algorithmic_bytes_per_sample(specs)[i] * B
+    alu_peak = 148 * 128 * PEAKS["sm_max_mhz"] * 1e6
+    s = specs[i]
+    int8 = engines[i] == "tcgen05" and s.C_in % 32 == 0 and s.H > 1
+    tc_peak = PEAKS["bf16"] * 1e12 * (2.0 if int8 else 1.0)
+    return {"layer": i, "ms": layer_ms[i], "alu_frac": bench.LIF_ALG_OPS * ns / t / alu_peak,
+            "tensor_frac": fl / t / tc_peak, "tensor_peak": "int8 (2 x measured bf16)" if int8 else "bf16 (measured)",
+            "hbm_frac": by / t / (PEAKS["hbm"] * 1e9)}
 
 RUNS = [
     ("C1", "dense", 1), ("C1", "tac", 4), ("C1", "tactp", 4),
@@ -110,8 +133,11 @@ def main():
             specs = configs.layer_plan(cfg, mode=mode, K=K)
             net = network.Network(specs, configs.layer_weights(cfg))
             x = tacsnn.pack(configs.make_inputs(cfg, device="cuda"))
+            clk = bench.ClockSampler(0)
+            clk.start()
             ms, layer_ms = time_forward(net, x, a.iters)
             graph_ms = time_graph(net, x, max(a.iters, 20)) if name in ("C1", "C2", "C3", "C4") else None
+            clocks = clk.stop()
             frames = cfg.B * cfg.T
             if mode == "dense":
                 dense_ms[name] = ms
@@ -121,7 +147,8 @@ def main():
                     "conv_calls_per_sample": configs.conv_calls(cfg, mode, K),
                     "layer_ms": layer_ms, "engines": net.engines(),
                     "graph_ms_per_forward": graph_ms,
-                    "graph_frames_per_s": None if graph_ms is None else frames / (graph_ms / 1e3)}
+                    "graph_frames_per_s": None if graph_ms is None else frames / (graph_ms / 1e3),
+                    "roofline": roofline(specs, layer_ms, cfg.B, net.engines()), "clocks": clocks}
             print(json.dumps(line), flush=True)
             out.write(json.dumps(line) + "\n")
             del net, x
@@ -146,23 +173,37 @@ def main():
                         "partial": [s.partial for s in specs]}
                 print(json.dumps(line), flush=True)
                 out.write(json.dumps(line) + "\n")
-            # the whole MNIST / FMNIST network (conv stack + FC head)
-            for name, runs in (("C2", (("dense", 1), ("tac", 4), ("tac", 8))), ("C3", (("dense", 1), ("tac", 8)))):
+            # the whole networks (conv stack + FC head): MNIST / FMNIST with
+            # the spike-count readout, DVS with the VotingLayer (tac_vote on the last counts)
+            for name, runs in (("C2", (("dense", 1), ("tac", 4), ("tac", 8))), ("C3", (("dense", 1), ("tac", 8))),
+                               ("C4", (("dense", 1), ("tactp", 2), ("tac", 2))),
+                               ("C5", (("dense", 1), ("tactp", 4)))):
                 cfg = configs.CONFIGS[name]
                 d_ms = None
                 for mode, K in runs:
                     specs = configs.network_plan(cfg, mode=mode, K=K)
-                    net = network.Network(specs, configs.network_weights(cfg))
+                    net = network.Network(specs, configs.network_weights(cfg),
+                                          voters=configs.VOTERS[configs.head_kind(cfg)])
                     x = tacsnn.pack(configs.make_inputs(cfg, device="cuda"))
-                    g_ms = time_graph(net, x, max(a.iters, 20))
+                    clk = bench.ClockSampler(0)
+                    clk.start()
+                    ms, layer_ms = time_forward(net, x, a.iters)
+                    g_ms = time_graph(net, x, max(a.iters, 20)) if name != "C5" else ms
+                    clocks = clk.stop()
                     d_ms = g_ms if mode == "dense" else d_ms
+                    nconv = len(cfg.layers)
                     line = {"config": name + "+FC", "mode": mode, "K": K, "B": cfg.B, "T": cfg.T,
-                            "ms_per_forward": g_ms, "graph_ms_per_forward": g_ms,
+                            "ms_per_forward": g_ms, "eager_ms_per_forward": ms,
+                            "graph_ms_per_forward": g_ms if name != "C5" else None,
                             "frames_per_s": cfg.B * cfg.T / (g_ms / 1e3), "speedup_vs_dense": d_ms / g_ms,
                             "conv_calls_per_sample": sum(-(-s.T // s.K) for s in specs),
-                            "engines": net.engines()}
+                            "layer_ms": layer_ms, "fc_ms": sum(layer_ms[nconv:]),
+                            "fc_share": sum(layer_ms[nconv:]) / sum(layer_ms),
+                            "engines": net.engines(), "clocks": clocks}
                     print(json.dumps(line), flush=True)
                     out.write(json.dumps(line) + "\n")
+                    del net, x
+                    torch.cuda.empty_cache()
             density_check(a.iters, out)
 
 

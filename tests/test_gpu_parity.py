@@ -535,6 +535,68 @@ def test_fc_layer_parity(T, O, mode, K, reset):
     assert 0.0 < st["rate"] < 0.95, st
 
 
+# FC shapes of both whole networks on the tcgen05 FC kernel (fc.cu) and the SIMT one:
+# C_in, C_out, B (ragged 128-sample M tiles), T, mode, K, beta
+FC_CASES = [(1600, 128, 130, 8, "tac", 4, 0.9), (2048, 512, 40, 8, "tactp", 4, 0.5),
+            (512, 110, 3, 6, "dense", 1, 0.5), (128, 10, 5, 4, "tac", 2, 0.9),
+            (96, 40, 7, 6, "tactp", 2, 0.9), (200, 64, 257, 8, "tactp", 8, 0.5)]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("reset", ["subtract", "delayed", "hard"])
+@pytest.mark.parametrize("case", FC_CASES, ids=lambda c: f"{c[0]}x{c[1]}b{c[2]}{c[4]}{c[5]}")
+def test_fc_engines_parity(T, O, case, reset, engine):
+    """Fully connected LIF layers on both engines: the tcgen05 FC
+    GEMM (M = 128 samples, fp16 hi + lo operands, aggregate table) and the SIMT kernel."""
+    c_in, c_out, B, Tn, mode, K, beta = case
+    spec = T.LayerSpec(T=Tn, B=B, C_in=c_in, H=1, W=1, C_out=c_out, R=1, S=1, pad=0, K=K,
+                       mode=mode, beta=beta, v_reset=-0.2, reset=reset)
+    spec = _engine_or_skip(spec, engine)
+    seed = zlib.crc32(repr(case).encode()) & 0xFFFF
+    S = _spikes(seed, (Tn, B, c_in, 1, 1), 0.2)
+    w, b = _w(seed + 1, c_out, c_in, 3.0, r=1, s=1)
+    _, _, st = P.check_layer(T, O, spec, S, w, b, label=f"fc/{case}/{reset}/{engine}")
+    assert 0.0 < st["rate"] < 0.95, st
+
+
+def test_fc_tcgen05_envelope(T):
+    """The FC shapes the whole networks use all run on tcgen05 (no silent SIMT fallback)."""
+    from paper_2603_13810_b200 import configs
+    for name in ("C2", "C3", "C4", "C5"):
+        for mode in ("dense", "tac", "tactp"):
+            for s in configs.network_plan(configs.CONFIGS[name], mode=mode, B=8):
+                if s.H == 1:
+                    assert s.engine_used() == "tcgen05", (name, mode, s)
+
+
+@pytest.mark.parametrize("mode,K", [("tactp", 2), ("dense", 1)])
+def test_whole_dvs_network_parity(T, O, mode, K):
+    """SURVEY.md 8(f) #2, DVS: 5 conv blocks + FC(2048->512) + FC(512->110), layer by layer
+    against the oracle, then the VotingLayer (10 voters, 11 classes) on the device counts
+    against oracle.vote of the oracle counts."""
+    from paper_2603_13810_b200 import configs
+    cfg = configs.CONFIGS["C4"]
+    specs = configs.network_plan(cfg, mode=mode, K=K, B=1)
+    S = configs.make_inputs(cfg, B=1).numpy()
+    stats = P.check_stack(T, O, specs, configs.network_weights(cfg), S, label=f"C4/net/{mode}")
+    assert stats[-1]["rate"] > 0.0
+    last = specs[-1]
+    T_out = last.T if last.mode != "tac" else -(-last.T // last.K)
+    counts = torch.from_numpy(stats[-1]["counts"].astype(np.int32)).cuda()
+    scores = T.vote(counts, 10, T_out).cpu().numpy()
+    ref = O.vote(stats[-1]["counts"], 10, T_out)
+    assert scores.shape == (1, 11)
+    np.testing.assert_allclose(scores, ref, rtol=1e-6, atol=0)
+
+
+def test_vote_parity(T, O):
+    """tac_vote against oracle.vote on random counts (exact u32 sums, one fp32 division)."""
+    g = torch.Generator().manual_seed(5)
+    counts = torch.randint(0, 33, (37, 110), generator=g, dtype=torch.int32)
+    scores = T.vote(counts.cuda(), 10, 32).cpu().numpy()
+    np.testing.assert_allclose(scores, O.vote(counts.numpy(), 10, 32), rtol=1e-6, atol=0)
+
+
 @pytest.mark.parametrize("cfg_name,B,mode,K", [("C2", 6, "tac", 4), ("C2", 4, "dense", 1),
                                                ("C3", 4, "tac", 8), ("C2", 4, "tactp", 2)])
 def test_whole_mnist_network_parity(T, O, cfg_name, B, mode, K):

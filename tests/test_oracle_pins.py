@@ -443,3 +443,12 @@ def test_agg_weights_equal_default_when_alpha_is_beta_powers(oracle_mod, mode):
         assert np.array_equal(r["out"], d["out"]) and np.array_equal(r["v_final"], d["v_final"])
     o = oracle_mod.forward(S, W, None, alpha=[1.0, 0.5, 0.25], **kw)   # reversed: a different layer
     assert not np.array_equal(o["v_final"], d["v_final"])
+
+
+def test_vote_pin():
+    """VotingLayer by hand: 2 classes x 3 voters, T_out = 4: class
+    scores are the voters' mean firing rates, (1 + 2 + 3) / 12 and (0 + 4 + 4) / 12."""
+    from oracle import oracle as O
+    s = O.vote(np.array([[1, 2, 3, 0, 4, 4]]), 3, 4)
+    assert s.shape == (1, 2)
+    assert s[0, 0] == 0.5 and abs(s[0, 1] - 8 / 12) < 1e-15
