@@ -116,10 +116,26 @@ def layer_plan(cfg: Config, mode: str | None = None, K: int | None = None, B: in
     return specs
 
 
-def layer_weights(cfg: Config, seed: int | None = None):
+# Mode-specific gains: the DVS stack run DENSE (one LIF step per frame with beta = 0.5
+# and the sparse event input) goes nearly silent in its deep layers with the TAC-TP
+# gains, which would make deep-layer parity vacuous; these are calibrated the same way
+# in dense mode (scripts/calibrate_gains.py C4 --mode dense [--head]).
+MODE_GAINS = {
+    ("dvs", "dense"): (15.49, 1.59, 1.59, 1.49, 1.31),   # C4 --mode dense, B=2: each layer ~10 %
+    ("dvs_fc", "dense"): (1.18, 2.34),                   # C4 --mode dense --head
+}
+
+
+def gains_for(cfg: Config, mode: str | None = None):
+    g = MODE_GAINS.get((head_kind(cfg), mode or cfg.mode))
+    return tuple(g) if g else cfg.gains
+
+
+def layer_weights(cfg: Config, seed: int | None = None, mode: str | None = None):
+    """Seeded weights of the conv stack; `mode` selects mode-specific gains (MODE_GAINS)."""
     seed = cfg.seeds[0] if seed is None else seed
     out = []
-    for i, (L, g) in enumerate(zip(cfg.layers, cfg.gains)):
+    for i, (L, g) in enumerate(zip(cfg.layers, gains_for(cfg, mode))):
         out.append(synth.weights(seed * 1000 + i, L.C_out, L.C_in, 3, 3, gain=g))
     return out
 
@@ -196,9 +212,10 @@ def network_plan(cfg: Config, mode: str | None = None, K: int | None = None, B: 
     return specs
 
 
-def network_weights(cfg: Config, seed: int | None = None):
+def network_weights(cfg: Config, seed: int | None = None, mode: str | None = None):
     seed = cfg.seeds[0] if seed is None else seed
-    w = layer_weights(cfg, seed)
-    for i, ((c_in, c_out), g) in enumerate(zip(head_dims(cfg), GAINS[head_kind(cfg) + "_fc"])):
+    w = layer_weights(cfg, seed, mode)
+    fc = MODE_GAINS.get((head_kind(cfg) + "_fc", mode or cfg.mode)) or GAINS[head_kind(cfg) + "_fc"]
+    for i, ((c_in, c_out), g) in enumerate(zip(head_dims(cfg), fc)):
         w.append(synth.weights(seed * 1000 + 10 + i, c_out, c_in, 1, 1, gain=g))
     return w

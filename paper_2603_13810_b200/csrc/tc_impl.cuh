@@ -733,6 +733,66 @@ __device__ __forceinline__ void produce_h16s_rt(const TcParams &p, const uint32_
   }
 }
 
+// Plane-mode row producer (first layers with C_in <= 2 whose K whole frames sit in smem,
+// e.g. MNIST 28 x 28 x 1): lane hy (< 18) builds halo row hy.  The K frame words covering
+// the row's 10 halo pixels are funnel-shifted to bit 0 once (K loads per ROW instead of
+// per pixel), transposed so that byte b of o[q] is the K-bit frame index of row bit
+// q + 8 b, and each pixel's index feeds the aggregate table (split path) or is the
+// exact aggregate itself (beta = 1/2 or dense: sum_j bit_j 2^j).  Chunk 1 of every
+// row is constant (h16_init_stages), so only chunk 0 is stored.
+template <int K, int CIN, bool SPLIT>
+__device__ __forceinline__ void produce_plane_rows(const TcParams &p, const uint32_t *lut, int tile,
+                                                   uint32_t a_stage, int lane, const uint32_t *plane) {
+  static_assert(K >= 1 && K <= 8 && (CIN == 1 || CIN == 2), "row producer envelope");
+  if (lane >= kHaloH) return;
+  int b, y0, x0;
+  bool tok;
+  tile_origin(p, tile, b, y0, x0, tok);
+  const int yi = y0 + lane - p.pad;
+  const bool rok = tok && yi >= 0 && yi < p.H;
+  const int bit0 = (x0 - p.pad) * CIN;       // row bit of halo column 0 (-CIN with left padding)
+  const int wb = bit0 >> 5, sh = bit0 & 31;  // floor division
+  const int wpr = p.wpr_in;
+  const uint32_t *row = plane + (rok ? yi : 0) * wpr;
+  uint32_t v[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const uint32_t *fr = row + j * p.raw_bw;
+    const uint32_t w0 = (rok && wb >= 0 && wb < wpr) ? fr[wb] : 0u;
+    const uint32_t w1 = (rok && wb + 1 >= 0 && wb + 1 < wpr) ? fr[wb + 1] : 0u;
+    v[j] = __funnelshift_r(w0, w1, sh);      // bits beyond W C_in are 0 in a packed row
+  }
+  uint32_t o[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) t |= ((v[j] >> q) & 0x01010101u) << j;
+    o[q] = t;
+  }
+  uint32_t one_lo, one_hi, c8;
+  h16_bias_slot(CIN, one_lo, one_hi, c8);
+  const uint32_t dst0 = a_stage + (uint32_t)(lane * kHaloW) * 16u;
+#pragma unroll
+  for (int c = 0; c < kHaloW; ++c) {
+    uint32_t idx[CIN];
+#pragma unroll
+    for (int ch = 0; ch < CIN; ++ch) {
+      const int bp = c * CIN + ch;            // compile-time
+      idx[ch] = (o[bp & 7] >> (8 * (bp >> 3))) & 0xFFu;
+    }
+    if constexpr (SPLIT) {
+      const uint4 w = split_row_words<CIN>(lut[idx[0]], CIN == 2 ? lut[idx[CIN - 1]] : 0u, p.packed);
+      ptx::st_shared_v4(dst0 + c * 16u, w.x, w.y, w.z, w.w);
+    } else {
+      uint32_t lo = one_lo | idx[0] | (CIN == 2 ? idx[CIN - 1] << 8 : 0u), hi = one_hi;
+      if (p.packed) h16_pack_slices(lo, hi, CIN);
+      ptx::st_shared_v4(dst0 + c * 16u, u8x2_to_f16x2(lo, 0x5140u), u8x2_to_f16x2(lo, 0x7362u),
+                        u8x2_to_f16x2(hi, 0x5140u), u8x2_to_f16x2(hi, 0x7362u));
+    }
+  }
+}
+
 template <int K>
 __device__ __forceinline__ void produce_s32(const TcParams &p, const uint32_t *lut, int tile, int k,
                                             uint32_t a_stage, int ptid) {
@@ -1059,6 +1119,16 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
             if (PATH == PATH_SPLIT)
               p.Cin == 1 ? produce_h16s_rt<1, true>(p, lut, tile, k, a_stage, wptid, raw)
                          : produce_h16s_rt<2, true>(p, lut, tile, k, a_stage, wptid, raw);
+          } else if (ws && K <= 8 && p.Cin <= 2 && (PATH == PATH_SPLIT || p.m_shift <= 1)) {
+            // one warp builds the stage row by row (see produce_plane_rows)
+            if constexpr (K <= 8) {
+              if (PATH == PATH_SPLIT)
+                p.Cin == 1 ? produce_plane_rows<K, 1, true>(p, lut, tile, a_stage, wptid, raw)
+                           : produce_plane_rows<K, 2, true>(p, lut, tile, a_stage, wptid, raw);
+              else
+                p.Cin == 1 ? produce_plane_rows<K, 1, false>(p, lut, tile, a_stage, wptid, raw)
+                           : produce_plane_rows<K, 2, false>(p, lut, tile, a_stage, wptid, raw);
+            }
           } else if (PATH == PATH_SPLIT) {
             p.Cin == 1 ? produce_h16s<K, 1, true>(p, lut, tile, k, a_stage, wptid, raw)
                        : produce_h16s<K, 2, true>(p, lut, tile, k, a_stage, wptid, raw);

@@ -29,12 +29,15 @@ def main():
     ap.add_argument("--B", type=int, default=2)
     ap.add_argument("--target", type=float, default=0.1)
     ap.add_argument("--iters", type=int, default=8)
+    ap.add_argument("--mode", default=None, help="calibrate for this mode instead of the config's primary one")
     ap.add_argument("--head", action="store_true",
                     help="keep the frozen conv gains and calibrate the FC head (network_plan)")
     a = ap.parse_args()
     if a.head:
         return calibrate_head(a)
     cfg = configs.CONFIGS[a.config]
+    if a.mode:
+        cfg = dataclasses_replace(cfg, mode=a.mode)
     x = configs.make_inputs(cfg, B=a.B).numpy()
     t = cfg.T
     gains = []
@@ -62,12 +65,19 @@ def main():
     print("GAINS", gains)
 
 
+def dataclasses_replace(cfg, **kw):
+    import dataclasses
+    return dataclasses.replace(cfg, **kw)
+
+
 def calibrate_head(a):
     """FC head gains: the conv stack runs with its frozen gains, its (pooled) output is
     flattened in (h, w, c) order (the packed row layout) and each FC layer's gain is bisected."""
     cfg = configs.CONFIGS[a.config]
+    if a.mode:
+        cfg = dataclasses_replace(cfg, mode=a.mode)
     specs = configs.network_plan(cfg, B=a.B)
-    weights = configs.layer_weights(cfg)
+    weights = configs.layer_weights(cfg, mode=cfg.mode)
     x = configs.make_inputs(cfg, B=a.B).numpy()
     nconv = len(cfg.layers)
     for s, (w, b) in zip(specs[:nconv], weights):

@@ -70,6 +70,7 @@ def time_forward(net, x, iters):
         y = x
         for li, (spec, prep) in enumerate(zip(net.specs, net.prepared)):
             evs[i][li][0].record(stream)
+            y = network.flatten_for(spec, y)   # FC head: the previous map as one packed row
             y, _, _ = tacsnn.conv_lif(spec, prep, y, want_counts=(li == nL - 1))  # readout: last layer
             evs[i][li][1].record(stream)
     t1.record(stream)

@@ -516,10 +516,13 @@ def test_config_stack_parity(T, O, cfg_name, B, mode):
     specs = configs.layer_plan(cfg, mode=mode, B=B)
     if mode == "tac" and cfg.inputs == "dvs":
         specs = configs.layer_plan(cfg, mode=mode, K=2, B=B)[:4]   # 16/2^4 = 1 step left
-    weights = configs.layer_weights(cfg)[:len(specs)]
+    weights = configs.layer_weights(cfg, mode=mode)[:len(specs)]   # mode-specific gains
     S = configs.make_inputs(cfg, B=B).numpy()
     stats = P.check_stack(T, O, specs, weights, S, label=f"{cfg_name}/{mode}")
-    assert stats[0]["rate"] > 0.0   # deep layers may legitimately fall silent (dense DVS)
+    # every layer fires (the DVS dense stack runs with its own calibrated gains, so its
+    # deep-layer parity is not vacuous); the last layer of a short C1 / MNIST run may be sparse
+    for i, st in enumerate(stats):
+        assert st["rate"] > (0.005 if cfg.inputs == "dvs" else 0.0), (i, st["rate"])
 
 
 @pytest.mark.parametrize("reset", ["subtract", "delayed", "hard"])
@@ -578,8 +581,9 @@ def test_whole_dvs_network_parity(T, O, mode, K):
     cfg = configs.CONFIGS["C4"]
     specs = configs.network_plan(cfg, mode=mode, K=K, B=1)
     S = configs.make_inputs(cfg, B=1).numpy()
-    stats = P.check_stack(T, O, specs, configs.network_weights(cfg), S, label=f"C4/net/{mode}")
-    assert stats[-1]["rate"] > 0.0
+    stats = P.check_stack(T, O, specs, configs.network_weights(cfg, mode=mode), S, label=f"C4/net/{mode}")
+    for i, st in enumerate(stats):
+        assert st["rate"] > 0.005, (i, st["rate"])
     last = specs[-1]
     T_out = last.T if last.mode != "tac" else -(-last.T // last.K)
     counts = torch.from_numpy(stats[-1]["counts"].astype(np.int32)).cuda()
