@@ -123,6 +123,7 @@ def layer_plan(cfg: Config, mode: str | None = None, K: int | None = None, B: in
 MODE_GAINS = {
     ("dvs", "dense"): (15.49, 1.59, 1.59, 1.49, 1.31),   # C4 --mode dense, B=2: each layer ~10 %
     ("dvs_fc", "dense"): (1.18, 2.34),                   # C4 --mode dense --head
+    ("dvs", "tac"): (11.19, 1.4, 1.49, 1.4, 1.81),        # C4 --mode tac (K = 2 cascade)
 }
 
 

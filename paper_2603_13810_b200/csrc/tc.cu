@@ -313,6 +313,8 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   static const bool no_ws = [] { const char *e = std::getenv("TACSNN_NO_WARP_STAGE"); return e && *e == '1'; }();
   p.warp_stage = (!no_ws && g.path != PATH_HALO && p.use_tma != 1) ? 1 : 0;
   p.prod_step = p.warp_stage ? 32 : 32 * kProdWarps;
+  static const bool no_pr = [] { const char *e = std::getenv("TACSNN_NO_PROD_REFILL"); return e && *e == '1'; }();
+  p.prod_refill = (!no_pr && p.warp_stage && p.use_tma == 2) ? 1 : 0;
   p.raw_bw = g.raw_bw;
   p.nraw = g.nraw;
   p.off_raw = g.off_raw;
@@ -358,6 +360,7 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   // accumulators: 3 on the fp16 paths (n_total = C_out_pad; with U in TMEM 3 x 128 +
   // 128 = 512 columns), 2 on the int8 path (n_total = 2 C_out_pad)
   p.naccs = g.path == PATH_HALO ? 2 : TACSNN_H16_ACCS;
+  if (p.warp_stage && g.cout_pad <= 64) p.naccs = kAccs;  // small first layers: deeper TMEM ring
   p.packed = packed_of(d) ? 1 : 0;
   while (cols < (uint32_t)p.naccs * p.n_total + (ut ? 128u : 0u)) cols <<= 1;
   p.tmem_cols = cols;

@@ -65,6 +65,7 @@ struct TcParams {
                      // 3-D [T][B][H*WPR] (plane mode: whole narrow frames, e.g. 28x28x1 = 112 B)
   int use_tma, raw_bw, nraw;  // use_tma: 0 LDG, 1 halo boxes, 2 whole planes (raw_bw = plane words)
   int warp_stage;             // 1: each producer warp builds whole A stages (stage it -> warp it % 3)
+  int prod_refill;            // 1 (plane mode + warp_stage): the warp that consumed raw slot r refills it
   int prod_step;              // halo-row stride of the pixel-wise producers: 96, or 32 with warp_stage
   uint32_t off_raw, raw_stage_bytes, raw_box_bytes;
   int B, H, W, Cin, Cout, Cout_pad, pad, Ho, Wo, pool;
@@ -141,8 +142,12 @@ constexpr int kProdWarps = 3;
 // issue slots over the 16 compute-heavy epilogue warps.
 constexpr int epi_warps(int npart) { return 4 * npart; }
 constexpr int kernel_threads(int npart) { return 32 * (1 + kProdWarps + epi_warps(npart)); }
-constexpr int kMaxStages = 3;
-constexpr int kAccs = 3;  // max TMEM accumulators (p.naccs: 3 on the fp16 paths, 2 on int8)
+// A stages / TMEM accumulators: 3 / 2 (int8), 3 / 3 (fp16, C_out 128); the small first
+// layers (pixel-wise producers, C_out <= 64) run deeper rings -- their per-group work is
+// short, so the producer -> MMA -> epilogue round trip, not any role's busy time, sets
+// the period unless more groups are in flight (scripts/trace_layer.py)
+constexpr int kMaxStages = 8;
+constexpr int kAccs = 6;  // max TMEM accumulators (p.naccs)
 constexpr int kMaxSteps = 8;
 constexpr int kPlanes = 6;  // bit-sliced spike counters (<= 63 steps per flush)
 constexpr int kTileH = 16, kTileW = 8;                 // output pixels per CTA tile
@@ -159,13 +164,19 @@ enum { PATH_HALO = 0, PATH_H16 = 1, PATH_SPLIT = 2 };
 // is built with -DTACSNN_TRACE (TACSNN_TRACE=1 python -m paper_2603_13810_b200.build
 // --force); otherwise trace_mark is empty and costs nothing in the hot loops.
 enum { TR_PROD_START = 0, TR_PROD_DONE, TR_MMA_READY, TR_MMA_ISSUED, TR_EPI_FULL, TR_EPI_RELEASED,
-       TR_EPI_DONE, TR_PROD_RAW, TR_PROD_ISSUED, TR_SLOTS = 16 };
+       TR_EPI_DONE, TR_PROD_RAW, TR_PROD_ISSUED, TR_MMA_AFULL, TR_MMA_REFILLED,
+       TR_P1_START, TR_P1_DONE, TR_P1_RAW, TR_SLOTS = 16 };
 __device__ __forceinline__ void trace_mark(const TcParams &p, uint32_t it, int slot) {
 #ifdef TACSNN_TRACE
-  if (p.trace && blockIdx.x == 0 && it < 4096) {
+  // CTA 0 records every role; CTA 1 (the pair's other CTA) its producers' events
+  const int sl = blockIdx.x == 0 ? slot
+                 : (blockIdx.x == 1 && slot == TR_PROD_START) ? TR_P1_START
+                 : (blockIdx.x == 1 && slot == TR_PROD_DONE) ? TR_P1_DONE
+                 : (blockIdx.x == 1 && slot == TR_PROD_RAW) ? TR_P1_RAW : -1;
+  if (p.trace && sl >= 0 && it < 4096) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.trace[it * TR_SLOTS + slot] = t;
+    p.trace[it * TR_SLOTS + sl] = t;
   }
 #else
   (void)p;
@@ -243,7 +254,7 @@ struct Geometry {
   uint32_t w_bytes_cta, a_stage_bytes, raw_stage_bytes, raw_box_bytes, off_w, off_a, off_raw,
       off_scale, off_lut, off_bar, smem_bytes;
 };
-constexpr int kMaxRaw = 4;
+constexpr int kMaxRaw = 8;  // raw (TMA) stages: 4 for halo boxes, up to 8 tiny plane boxes
 constexpr int kNumBars = 2 * kMaxStages + 2 * kAccs + 1 + 2 * kMaxRaw;
 
 uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
@@ -278,9 +289,11 @@ Geometry geometry(const tac_conv_lif_desc *d, bool use_tma = false, int plane_wo
   if (plane_words > 0) g.raw_bw = plane_words;  // plane mode: K whole frames per stage
   g.raw_box_bytes = (uint32_t)K * (plane_words > 0 ? 1 : kHaloH) * g.raw_bw * 4u;
   g.raw_stage_bytes = align_up(g.raw_box_bytes, 128);
-  const int combos[6][2] = {{3, 4}, {3, 3}, {3, 2}, {2, 2}, {3, 1}, {2, 1}};
-  for (int ci = 0; ci < (use_tma ? 6 : 2); ++ci) {
-    g.nstages = use_tma ? combos[ci][0] : (ci == 0 ? 3 : 2);
+  // pixel-wise producers (plane mode or LDG, fp16 paths) try deeper A rings first
+  const bool deep = g.path != PATH_HALO && (plane_words > 0 || !use_tma);
+  const int combos[11][2] = {{8, 8}, {8, 4}, {6, 4}, {4, 4}, {3, 4}, {3, 3}, {3, 2}, {2, 2}, {3, 1}, {2, 1}, {2, 0}};
+  for (int ci = deep ? 0 : 4; ci < 11; ++ci) {
+    g.nstages = combos[ci][0];
     g.nraw = use_tma ? combos[ci][1] : 0;
     g.off_w = 0;
     g.off_a = align_up(g.w_bytes_cta, 1024);
@@ -1075,6 +1088,21 @@ struct RawLoader {
   }
 };
 
+// Plane-mode raw refill by the producer warp (p.prod_refill): load number L (the L-th
+// (tile pair, group) of this CTA in issue order) into raw slot r.
+__device__ __forceinline__ void refill_plane(const TcParams &p, uint32_t sbase, uint32_t bar_raw, uint32_t L,
+                                             uint32_t r, int cid, int ncl, uint32_t rank) {
+  const int pi = (int)(L / (uint32_t)p.G), k = (int)(L - (uint32_t)pi * (uint32_t)p.G);
+  const int pair = cid + pi * ncl;
+  if (pair >= p.num_pairs) return;
+  int b, y0, x0;
+  bool tok;
+  tile_origin(p, 2 * pair + (int)rank, b, y0, x0, tok);
+  const uint32_t bar = bar_raw + 8 * r;
+  ptx::mbar_arrive_expect_tx(bar, p.raw_box_bytes);
+  ptx::tma_load_3d(sbase + p.off_raw + r * p.raw_stage_bytes, &p.tmap, 0, b, k * p.K, bar);
+}
+
 // TMA producer pipeline: all 96 producer threads aggregate raw stage `it % nraw`
 // into A stage `it % nstages`; each warp then releases the raw stage (local
 // raw_empty barrier, refilled by the MMA warp's loader) and arrives on the pair's
@@ -1156,6 +1184,9 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
       if (lane == 0) {
         ptx::mbar_arrive_local(bar_raw_empty + 8 * r);  // this warp's reads of raw stage r are done
         ptx::mbar_arrive_cluster_cta(bar_a_full + 8 * s, 0);
+        // plane mode: this warp was raw slot r's only reader, so it refills the slot with the
+        // planes of group it + nraw itself -- the MMA warp's issue loop carries no TMA work
+        if (p.prod_refill) refill_plane(p, sbase, bar_raw, it + nr, r, cid, ncl, rank);
       }
       if (wptid == 0) trace_mark(p, it, TR_PROD_DONE);
     }
@@ -1924,7 +1955,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
       // producers just released.
       RawLoader loader;
       if (p.use_tma && lane == 0) loader.start(p, sbase, bar_raw, cid, ncl, rank);
-      if (rank != 0 && p.use_tma && lane == 0) {
+      if (rank != 0 && p.use_tma && !p.prod_refill && lane == 0) {
         const uint32_t total = (uint32_t)((p.num_pairs - cid + ncl - 1) / ncl) * (uint32_t)p.G;
         for (uint32_t it = 0; it < total; ++it) loader.refill(p, sbase, bar_raw, bar_raw_empty, it, ncl);
       }
@@ -1948,11 +1979,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
             st.next(ns);
             ar.next((uint32_t)p.naccs);
             ptx::mbar_wait(bar_a_full + 8 * s, ph);
+            if (lane == 0) trace_mark(p, it, TR_MMA_AFULL);
 #if TACSNN_REFILL_EARLY
             // A-full(it) implies every producer released raw slot it % nraw: refill it now,
             // before the MMA issue below (which blocks while the tensor queue is full)
-            if (p.use_tma && lane == 0) loader.refill(p, sbase, bar_raw, bar_raw_empty, it, ncl);
+            if (p.use_tma && !p.prod_refill && lane == 0) loader.refill(p, sbase, bar_raw, bar_raw_empty, it, ncl);
             __syncwarp();
+            if (lane == 0) trace_mark(p, it, TR_MMA_REFILLED);
 #endif
             ptx::mbar_wait(bar_t_empty + 8 * acc, aph ^ 1u);
             ptx::tc_fence_after();
@@ -1996,7 +2029,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
             __syncwarp();
             if (lane == 0) trace_mark(p, it, TR_MMA_ISSUED);
 #if !TACSNN_REFILL_EARLY
-            if (p.use_tma && lane == 0) loader.refill(p, sbase, bar_raw, bar_raw_empty, it, ncl);
+            if (p.use_tma && !p.prod_refill && lane == 0) loader.refill(p, sbase, bar_raw, bar_raw_empty, it, ncl);
             __syncwarp();
 #endif
           }

@@ -16,7 +16,8 @@ import torch  # noqa: E402
 from paper_2603_13810_b200 import configs, tacsnn  # noqa: E402
 
 NAMES = ["prod_start", "prod_done", "mma_ready", "mma_issued", "epi_full", "epi_released", "epi_done",
-         "prod_raw", "prod_issued"]
+         "prod_raw", "prod_issued", "mma_afull", "mma_refill", "p1_start", "p1_done", "p1_raw"]
+SHOW = [0, 1, 7, 11, 12, 13, 9, 10, 2, 3, 4, 5, 6]
 
 
 def main():
@@ -45,9 +46,9 @@ def main():
     n = int((tr[:, 0] > 0).sum())
     t0 = tr[0, 0]
     print(f"layer {a.layer} B={a.B}: {n} group iterations traced on CTA 0")
-    print("it " + " ".join(f"{s:>12s}" for s in NAMES))
+    print("it " + " ".join(f"{NAMES[j]:>11s}" for j in SHOW))
     for i in list(range(min(a.rows, n))) + list(range(max(a.rows, n - 4), n)):
-        print(f"{i:3d} " + " ".join(f"{(tr[i, j] - t0) / 1e3:12.2f}" for j in range(9)))
+        print(f"{i:3d} " + " ".join(f"{(tr[i, j] - t0) / 1e3 if tr[i, j] else float('nan'):11.2f}" for j in SHOW))
     import numpy as np
     it = tr[1:n]
     d = lambda j0, j1: np.median(it[:, j1] - it[:, j0]) / 1e3
@@ -55,10 +56,17 @@ def main():
     print(f"median per-group period (epi_done diff): {per:.2f} us")
     print(f"median producer busy: {d(0, 1):.2f} us, MMA ready->issued: {d(2, 3):.2f} us, "
           f"epi full->released: {d(4, 5):.2f} us, epi released->done: {d(5, 6):.2f} us")
+    print(f"MMA: prev issued -> A-full {np.median(tr[1:n, 9] - tr[:n-1, 3]) / 1e3:.2f} us, A-full -> refilled "
+          f"{np.median(tr[:n, 10] - tr[:n, 9]) / 1e3:.2f} us, refilled -> ready (t_empty) {np.median(tr[:n, 2] - tr[:n, 10]) / 1e3:.2f} us; "
+          f"CTA 1 producer done - CTA 0 producer done {np.median(tr[:n, 12] - tr[:n, 1]) / 1e3:.2f} us")
     print(f"median epi wait (prev done -> full): {np.median(tr[1:n, 4] - tr[:n-1, 6]) / 1e3:.2f} us; "
           f"MMA wait (prev issued -> ready): {np.median(tr[1:n, 2] - tr[:n-1, 3]) / 1e3:.2f} us; "
           f"producer wait (prev done -> start): {np.median(tr[1:n, 0] - tr[:n-1, 1]) / 1e3:.2f} us")
-    print(f"  TMA issue (done -> issued): {np.median(tr[:n, 8] - tr[:n, 1]) / 1e3:.2f} us")
+    # warp-stage producers (first layers): stage it is built by the warp that built it - 3
+    if n > 4:
+        print(f"  per producer warp (stage it vs it-3): raw wait {np.median(tr[3:n, 7] - tr[:n-3, 1]) / 1e3:.2f} us, "
+              f"A-stage wait {np.median(tr[3:n, 0] - tr[3:n, 7]) / 1e3:.2f} us, "
+              f"stage-to-stage {np.median(tr[3:n, 1] - tr[:n-3, 1]) / 1e3:.2f} us")
     print(f"  of which prev done -> raw ready: {np.median(tr[1:n, 7] - tr[:n-1, 1]) / 1e3:.2f} us, "
           f"raw ready -> A stage free: {np.median(tr[1:n, 0] - tr[1:n, 7]) / 1e3:.2f} us")
 
