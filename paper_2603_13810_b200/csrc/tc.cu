@@ -387,7 +387,11 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return (int)e;
   }
-  const int nclusters = std::max(1, std::min(p.num_pairs, 74));
+  // two pipelines per SM for the small first layers when their smem and TMEM halve
+  static const bool no_occ2 = [] { const char *e = std::getenv("TACSNN_NO_OCC2"); return e && *e == '1'; }();
+  p.occ = (!no_occ2 && p.warp_stage && g.path != PATH_HALO && g.cout_pad <= 32 && p.smem_bytes <= 112u * 1024u &&
+           p.tmem_cols <= 256u) ? 2 : 1;
+  const int nclusters = std::max(1, std::min(p.num_pairs, 74 * p.occ));
   const bool train = lp.y_seq != nullptr;
   cudaError_t e;
   if (g.path == PATH_HALO)

@@ -66,6 +66,7 @@ struct TcParams {
   int use_tma, raw_bw, nraw;  // use_tma: 0 LDG, 1 halo boxes, 2 whole planes (raw_bw = plane words)
   int warp_stage;             // 1: each producer warp builds whole A stages (stage it -> warp it % 3)
   int prod_refill;            // 1 (plane mode + warp_stage): the warp that consumed raw slot r refills it
+  int occ;                    // CTA pairs per SM pair (1, or 2 for small first layers: OCC kernels)
   int prod_step;              // halo-row stride of the pixel-wise producers: 96, or 32 with warp_stage
   uint32_t off_raw, raw_stage_bytes, raw_box_bytes;
   int B, H, W, Cin, Cout, Cout_pad, pad, Ho, Wo, pool;
@@ -1865,8 +1866,11 @@ __device__ __forceinline__ void mma_group_h16(uint32_t d_tmem, uint64_t a_base, 
   }
 }
 
-template <int NCH, int PATH, int NPART, bool TRAIN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART), 1)
+// OCC = 2: two CTA pairs per SM pair (small first layers: every role of one pipeline is
+// latency-bound, so a second independent pipeline per SM fills the idle issue slots);
+// the register budget is then 64 K / (2 x threads) per thread and no setmaxnreg.
+template <int NCH, int PATH, int NPART, bool TRAIN, int OCC = 1>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART), OCC)
     tc_conv_lif_kernel(const __grid_constant__ TcParams p) {
   constexpr int kThreads = kernel_threads(NPART);
   constexpr int kEpiWarps = epi_warps(NPART);
@@ -1944,7 +1948,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
                     kernel_threads(NPART) * kLaunchRegs, "register budget");
   const uint32_t kMmaWarp = (uint32_t)kEpiWarps;
   if (warp >= kMmaWarp) {
-    ptx::setmaxnreg_dec<kRegsLow>();
+    if constexpr (OCC == 1) ptx::setmaxnreg_dec<kRegsLow>();
     if (warp == kMmaWarp) {
       // ================================ MMA issuer (CTA 0 of the pair) =========
       // The whole warp runs the loop converged (warp-uniform descriptors, no
@@ -2060,7 +2064,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
       }
     }
   } else {
-    ptx::setmaxnreg_inc<kRegsHigh>();
+    if constexpr (OCC == 1) ptx::setmaxnreg_inc<kRegsHigh>();
     // ================================ epilogue =================================
     const int ns = p.reset == 0 ? p.nsteps : 0;
     switch (ns) {
@@ -2081,9 +2085,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
   }
 }
 
-template <int NCH, int PATH, int NPART, bool TRAIN>
+template <int NCH, int PATH, int NPART, bool TRAIN, int OCC = 1>
 cudaError_t launch_kernel(const TcParams &p, int nclusters, cudaStream_t stream) {
-  auto kern = tc_conv_lif_kernel<NCH, PATH, NPART, TRAIN>;
+  auto kern = tc_conv_lif_kernel<NCH, PATH, NPART, TRAIN, OCC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -2109,6 +2113,12 @@ template <> cudaError_t tc_launch_path<PATH_SPLIT, true>(const TcParams &, int, 
 template <>
 cudaError_t tc_launch_path<TAC_TC_PATH, TAC_TC_TRAIN>(const TcParams &p, int cout_pad, int nclusters,
                                                      cudaStream_t stream) {
+  if constexpr (TAC_TC_PATH != PATH_HALO) {
+    if (p.occ == 2) {
+      if (cout_pad == 16) return launch_kernel<8, TAC_TC_PATH, 2, TAC_TC_TRAIN, 2>(p, nclusters, stream);
+      if (cout_pad == 32) return launch_kernel<16, TAC_TC_PATH, 2, TAC_TC_TRAIN, 2>(p, nclusters, stream);
+    }
+  }
   switch (cout_pad) {
     case 16: return launch_kernel<8, TAC_TC_PATH, 2, TAC_TC_TRAIN>(p, nclusters, stream);
     case 32: return launch_kernel<16, TAC_TC_PATH, 2, TAC_TC_TRAIN>(p, nclusters, stream);
