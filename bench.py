@@ -51,6 +51,7 @@ def parse():
                     help="strong: the config's global batch is sharded; weak: B per rank")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-head", action="store_true", help="skip the whole-network (FC head) timing")
     ap.add_argument("--cpu-sample-T", type=int, default=8)
     ap.add_argument("--layer-detail", action="store_true")
     ap.add_argument("--no-v-final", action="store_true",
@@ -639,7 +640,7 @@ def main():
                        "note": "int8 operands beat the measured cuBLAS bf16 rate (72 % of nominal), so "
                                "the derived int8 peak (measured bf16 x 2) is below what int8 issues; "
                                "nominal dense int8 = 4.5 POPS",
-                       "ncu_tensor_active": "profiles/ncu_c5_layer1_r01*.txt (sm__pipe_tensor_cycles_active)"}
+                       "ncu_tensor_active": "profiles/ncu_c5_layer1_r02.txt (sm__pipe_tensor_cycles_active)"}
 
     # ---------------- v_final on: every layer also writes its fp32 membrane state
     # (SURVEY.md 8(d) "measure with and without it"); a few extra steps after the timed region
@@ -660,6 +661,37 @@ def main():
         vfinal = {"ms_per_step": vms, "value": frames_per_step / (vms / 1e3),
                   "v_final_bytes_per_step": vbytes, "steps": nvf,
                   "note": "rank-local: every layer writes fp32 v_final [B,H',W',C_out]"}
+
+    # ---------------- the whole network: the FC head (+ VotingLayer for DVS) on the stack's
+    # output, timed the same way after the main region
+    whole = None
+    if not a.no_head:
+        nconv = len(cfg.layers)
+        hspecs = configs.network_plan(cfg, mode=a.mode, K=a.K, B=B, engine=a.engine)[nconv:]
+        head = network.Network(hspecs, configs.network_weights(cfg)[nconv:], device=dev,
+                               voters=configs.VOTERS[configs.head_kind(cfg)])
+        y0, _, _, _ = net.forward(x)
+
+        def head_step():
+            _, hc, _, _ = head.forward(y0)
+            return head.readout(hc[-1])
+        head_step()
+        torch.cuda.synchronize()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nh = max(3, min(a.steps, 10))
+        h0.record(stream)
+        for _ in range(nh):
+            head_step()
+        h1.record(stream)
+        torch.cuda.synchronize()
+        hms = h0.elapsed_time(h1) / nh
+        whole = {"head_ms_per_step": hms, "ms_per_step": ms_per_step + hms,
+                 "value": frames_per_step / ((ms_per_step + hms) / 1e3),
+                 "head": " -> ".join(f"FC({s_.C_in}->{s_.C_out})" for s_ in hspecs) +
+                         (f" -> VotingLayer({head.voters})" if head.voters else " -> spike counts"),
+                 "head_engines": head.engines(),
+                 "note": "rank-local head after the timed conv stack; value = B*T / (stack + head)"}
+        del head, y0
 
     cpu = None
     if rank == 0 and not a.no_cpu_baseline:
@@ -684,6 +716,7 @@ def main():
             "tensor_pipe": tensor_pipe,
             "cpu_baseline": cpu,
             "v_final_on": vfinal,
+            "whole_network": whole,
             "layers": layer_rows,
             "peaks": peaks,
         }

@@ -188,9 +188,15 @@ tac_status tac_prepare_weights(const tac_conv_lif_desc *desc, const float *weigh
                                const float *bias, void *prepared, size_t bytes,
                                void *stream, tac_plan *plan);
 
-/* Workspace bytes tac_conv_lif_forward needs: 0, except with partial_last_group
- * and K not dividing T (the membrane state between the full groups and the short
- * last group, fp32 [B][H'][W'][C_out], plus u32 [B][C_out] counts). */
+/* Workspace bytes tac_conv_lif_forward uses (device, 256-B aligned):
+ *  - partial_last_group with K not dividing T: REQUIRED -- the membrane state between
+ *    the full groups and the short last group, fp32 [B][H'][W'][C_out], plus u32
+ *    [B][C_out] counts;
+ *  - a fully connected layer (H = W = R = S = 1) on tcgen05 whose batch gives few
+ *    128-sample tiles: OPTIONAL -- with it the layer runs two-phase (the group GEMMs
+ *    split over the SMs into the workspace, fp32 [S][G][B][C_out], then the LIF); with
+ *    ws = NULL it runs fused (one CTA per tile, slower for small B).
+ *  - otherwise 0. */
 tac_status tac_workspace_bytes(const tac_conv_lif_desc *desc, size_t *bytes);
 
 /* The layer (one call = whole sequence, all groups).

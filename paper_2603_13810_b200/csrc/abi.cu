@@ -158,8 +158,13 @@ size_t prep_total(const tac_conv_lif_desc *d, const Geo &g) {
   const tac_conv_lif_desc b = part_desc(d, g, true);
   return n + prep_layout(&b).total;
 }
+int resolve_engine(const tac_conv_lif_desc *d);
 size_t ws_total(const tac_conv_lif_desc *d, const Geo &g) {
-  if (!is_split_call(d, g) || g.G == 1) return 0;
+  // a fully connected layer with few 128-sample tiles runs the two-phase tcgen05 FC
+  // (GEMM units -> workspace -> LIF); without a workspace it runs fused
+  if (!is_split_call(d, g))
+    return (tacsnn::fc_is_fc(d) && resolve_engine(d) == TAC_ENGINE_TCGEN05) ? align256(tacsnn::fc_ws_bytes(d)) : 0;
+  if (g.G == 1) return 0;
   return align256((size_t)d->B * g.Ho * g.Wo * d->C_out * 4) + align256((size_t)d->B * d->C_out * 4);
 }
 
@@ -396,7 +401,7 @@ tac_status validate_call(const tac_conv_lif_desc *desc, const void *prepared, co
 tac_status launch_call(const tac_conv_lif_desc *desc, const Geo &g, int engine, const void *prepared,
                        int yexp, const void *input, bool real, const float *v_init, uint32_t *spikes_out,
                        float *v_final, uint32_t *counts, void *stream, int *launches,
-                       float *y_seq = nullptr) {
+                       float *y_seq = nullptr, void *ws = nullptr, size_t ws_bytes = 0) {
   tacsnn::LayerParams p{};
   p.T = desc->T; p.B = desc->B; p.Cin = desc->C_in; p.H = desc->H; p.W = desc->W;
   p.Cout = desc->C_out; p.R = desc->R; p.S = desc->S; p.stride = desc->stride; p.pad = desc->pad;
@@ -416,6 +421,8 @@ tac_status launch_call(const tac_conv_lif_desc *desc, const Geo &g, int engine, 
   p.xin = real ? static_cast<const float *>(input) : nullptr;
   p.y_seq = y_seq;
   p.yscale_exp = yexp;
+  p.ws = ws;
+  p.ws_bytes = ws_bytes;
   const PrepLayout L = prep_layout(desc);
   const unsigned char *base = static_cast<const unsigned char *>(prepared);
   p.w = reinterpret_cast<const float *>(base + L.simt_off);
@@ -460,8 +467,15 @@ tac_status forward_impl(const tac_conv_lif_desc *desc, const tac_plan *plan, con
     int engine;
     st = validate_call(desc, prepared, input, real, v_init, spikes_out, v_final, counts, &engine);
     if (st != TAC_OK) return st;
+    // optional workspace (two-phase tcgen05 FC layers); NULL runs the fused path
+    const size_t wneed = ws_total(desc, g);
+    if (ws && wneed) {
+      if (ws_bytes < wneed) return fail(TAC_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, wneed);
+      if ((uintptr_t)ws % 256) return fail(TAC_ERR_ALIGN, "workspace must be 256-B aligned");
+      if (!is_device_ptr(ws)) return fail(TAC_ERR_PARAM, "workspace is not device memory");
+    }
     st = launch_call(desc, g, engine, prepared, plan_exp(plan, 0), input, real, v_init, spikes_out, v_final, counts, stream,
-                     &launches);
+                     &launches, nullptr, wneed ? ws : nullptr, wneed ? ws_bytes : 0);
     if (st == TAC_OK) g_launches = launches;
     return st;
   }

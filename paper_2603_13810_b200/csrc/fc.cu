@@ -59,7 +59,42 @@ struct FcParams {
   const float *bias;           // fp32 [Cout]
   const uint32_t *lut;         // [256] fp16 A_hi | A_lo << 16
   uint32_t a_bytes, b_bytes, stage_bytes, off_lut, off_bar, smem_bytes, tmem_cols;
+  // two-phase mode (few 128-sample tiles): units are (tile, group, K split) GEMMs whose
+  // raw accumulators go to ws [S][G][B][C_out]; fc_lif_from_y then runs the LIF
+  int splits, cps;             // K splits, chunks per split
+  float *ws;
 };
+
+// One unit of work: fused mode = a whole (M, N) tile with all its groups in order (V
+// stays resident); GEMM mode = one (tile, group, K split).  Every role walks the same
+// unit sequence (CTA-strided).
+struct FcUnit {
+  int mt, nt, k0, k1, c0, c1, s;
+};
+template <bool GEMM>
+__device__ __forceinline__ int fc_units(const FcParams &p) {
+  return p.m_tiles * p.n_tiles * (GEMM ? p.G * p.splits : 1);
+}
+template <bool GEMM>
+__device__ __forceinline__ FcUnit fc_unit(const FcParams &p, int u) {
+  FcUnit r;
+  int tile = u;
+  if (GEMM) {
+    const int per = p.G * p.splits;
+    tile = u / per;
+    const int q = u - tile * per;
+    r.k0 = q / p.splits;
+    r.s = q - r.k0 * p.splits;
+    r.k1 = r.k0 + 1;
+    r.c0 = r.s * p.cps;
+    r.c1 = min(p.nchunks, r.c0 + p.cps);
+  } else {
+    r.k0 = 0; r.k1 = p.G; r.c0 = 0; r.c1 = p.nchunks; r.s = 0;
+  }
+  r.mt = tile / p.n_tiles;
+  r.nt = tile - r.mt * p.n_tiles;
+  return r;
+}
 
 constexpr int fc_threads(int npart) { return 32 * (4 * npart + 1 + kFcProd); }
 
@@ -107,15 +142,16 @@ __device__ __forceinline__ void fc_produce_row(const FcParams &p, const uint32_t
   }
 }
 
-template <int K>
+template <int K, bool GEMM>
 __device__ __forceinline__ void fc_producer(const FcParams &p, uint32_t sbase, const uint32_t *lut,
                                             uint32_t bar_full, uint32_t bar_empty, int ptid, uint32_t lane) {
   uint32_t it = 0;
-  const int ntiles = p.m_tiles * p.n_tiles;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
-    for (int k = 0; k < p.G; ++k)
-      for (int c = 0; c < p.nchunks; ++c, ++it) {
+  const int nunits = fc_units<GEMM>(p);
+  for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const FcUnit w = fc_unit<GEMM>(p, u);
+    const int mt = w.mt, nt = w.nt;
+    for (int k = w.k0; k < w.k1; ++k)
+      for (int c = w.c0; c < w.c1; ++c, ++it) {
         const uint32_t s = it % kFcStages, ph = (it / kFcStages) & 1u;
         ptx::mbar_wait(bar_empty + 8 * s, ph ^ 1u);
         const uint32_t stage = sbase + s * p.stage_bytes;
@@ -141,6 +177,42 @@ __device__ __forceinline__ void fc_planes_add(uint32_t (&P)[kFcPlanes], uint32_t
     const uint32_t c = P[pl] & v;
     P[pl] ^= v;
     v = c;
+  }
+}
+
+// GEMM mode: the raw accumulators of one unit -> ws [s][k][b][co] (fc_lif_from_y adds
+// the splits in order, scales and runs the LIF)
+template <int NPART>
+__device__ __forceinline__ void fc_store_partials(const FcParams &p, uint32_t tmem_base, uint32_t bar_tfull,
+                                                  uint32_t bar_tempty, uint32_t warp, uint32_t lane) {
+  const int quad = (int)(warp & 3), part = (int)(warp >> 2);
+  const int row = quad * 32 + (int)lane;
+  const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+  uint32_t it = 0;
+  const int nunits = fc_units<true>(p);
+  for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
+    const FcUnit w = fc_unit<true>(p, u);
+    const int b = w.mt * kFcM + row;
+    const int co0 = w.nt * p.N + part * 32;
+    const uint32_t acc = it & 1u, aph = (it >> 1) & 1u;
+    ptx::mbar_wait(bar_tfull + 8 * acc, aph);
+    ptx::tc_fence_after();
+    const uint32_t tcol = tmem_base + lane_addr + acc * (uint32_t)p.N + (uint32_t)(part * 32);
+    float *dst = p.ws + (((long long)w.s * p.G + w.k0) * p.B + b) * p.Cout + co0;
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      uint32_t d[8], dz[8];
+      ptx::tmem_ld8(tcol + cc * 8, d);
+      ptx::tmem_wait_ld_dep(d, dz);
+      if (b < p.B) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (co0 + cc * 8 + q < p.Cout) dst[cc * 8 + q] = __uint_as_float(d[q]);
+      }
+    }
+    ptx::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive_local(bar_tempty + 8 * acc);
   }
 }
 
@@ -238,7 +310,7 @@ __device__ __forceinline__ void fc_epilogue(const FcParams &p, uint32_t tmem_bas
 }
 
 // ---------------------------------------------------------------- kernel ------
-template <int NPART, int NS, bool TRAIN>
+template <int NPART, int NS, bool TRAIN, bool GEMM = false>
 __global__ void __launch_bounds__(fc_threads(NPART), 1) fc_lif_tc_kernel(const __grid_constant__ FcParams p) {
   constexpr int kEpiWarps = 4 * NPART;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -272,21 +344,25 @@ __global__ void __launch_bounds__(fc_threads(NPART), 1) fc_lif_tc_kernel(const _
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp < (uint32_t)kEpiWarps) {
-    fc_epilogue<NPART, NS, TRAIN>(p, tmem_base, bar_tfull, bar_tempty, warp, lane);
+    if constexpr (GEMM)
+      fc_store_partials<NPART>(p, tmem_base, bar_tfull, bar_tempty, warp, lane);
+    else
+      fc_epilogue<NPART, NS, TRAIN>(p, tmem_base, bar_tfull, bar_tempty, warp, lane);
   } else if (warp == (uint32_t)kEpiWarps) {
     // MMA issuer: per group, all chunks into one accumulator; commits free the stage
     // and, after the last chunk, hand the accumulator to the epilogue
     const uint32_t idesc = ptx::idesc_f16(kFcM, (uint32_t)p.N);
     const uint32_t lbo_a = kFcM * 16u, lbo_b = (uint32_t)p.N * 16u;
     uint32_t it = 0, g = 0;
-    const int ntiles = p.m_tiles * p.n_tiles;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-      for (int k = 0; k < p.G; ++k, ++g) {
+    const int nunits = fc_units<GEMM>(p);
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      const FcUnit w = fc_unit<GEMM>(p, u);
+      for (int k = w.k0; k < w.k1; ++k, ++g) {
         const uint32_t acc = g & 1u, aph = (g >> 1) & 1u;
         ptx::mbar_wait(bar_tempty + 8 * acc, aph ^ 1u);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * (uint32_t)p.N;
-        for (int c = 0; c < p.nchunks; ++c, ++it) {
+        for (int c = w.c0; c < w.c1; ++c, ++it) {
           const uint32_t s = it % kFcStages, ph = (it / kFcStages) & 1u;
           ptx::mbar_wait(bar_full + 8 * s, ph);
           ptx::tc_fence_after();
@@ -298,27 +374,28 @@ __global__ void __launch_bounds__(fc_threads(NPART), 1) fc_lif_tc_kernel(const _
               const uint64_t alo = ptx::smem_desc(stage + 8 * lbo_a + ks * 2 * lbo_a, lbo_a, 128u);
               const uint64_t bhi = ptx::smem_desc(stage + p.a_bytes + ks * 2 * lbo_b, lbo_b, 128u);
               const uint64_t blo = ptx::smem_desc(stage + p.a_bytes + 8 * lbo_b + ks * 2 * lbo_b, lbo_b, 128u);
-              ptx::mma_f16_cg1(d_tmem, ahi, bhi, idesc, (c | ks) ? 1u : 0u);
+              ptx::mma_f16_cg1(d_tmem, ahi, bhi, idesc, (c != w.c0 || ks) ? 1u : 0u);
               ptx::mma_f16_cg1(d_tmem, ahi, blo, idesc, 1u);
               if (p.split) ptx::mma_f16_cg1(d_tmem, alo, bhi, idesc, 1u);
             }
             ptx::mma_commit_cg1(bar_empty + 8 * s);
-            if (c == p.nchunks - 1) ptx::mma_commit_cg1(bar_tfull + 8 * acc);
+            if (c == w.c1 - 1) ptx::mma_commit_cg1(bar_tfull + 8 * acc);
           }
           __syncwarp();
         }
       }
+    }
   } else {
     const int ptid = (int)(threadIdx.x - 32 * (kEpiWarps + 1));
     switch (p.K) {
-      case 1: fc_producer<1>(p, sbase, lut, bar_full, bar_empty, ptid, lane); break;
-      case 2: fc_producer<2>(p, sbase, lut, bar_full, bar_empty, ptid, lane); break;
-      case 3: fc_producer<3>(p, sbase, lut, bar_full, bar_empty, ptid, lane); break;
-      case 4: fc_producer<4>(p, sbase, lut, bar_full, bar_empty, ptid, lane); break;
-      case 5: fc_producer<5>(p, sbase, lut, bar_full, bar_empty, ptid, lane); break;
-      case 6: fc_producer<6>(p, sbase, lut, bar_full, bar_empty, ptid, lane); break;
-      case 7: fc_producer<7>(p, sbase, lut, bar_full, bar_empty, ptid, lane); break;
-      default: fc_producer<8>(p, sbase, lut, bar_full, bar_empty, ptid, lane); break;
+      case 1: fc_producer<1, GEMM>(p, sbase, lut, bar_full, bar_empty, ptid, lane); break;
+      case 2: fc_producer<2, GEMM>(p, sbase, lut, bar_full, bar_empty, ptid, lane); break;
+      case 3: fc_producer<3, GEMM>(p, sbase, lut, bar_full, bar_empty, ptid, lane); break;
+      case 4: fc_producer<4, GEMM>(p, sbase, lut, bar_full, bar_empty, ptid, lane); break;
+      case 5: fc_producer<5, GEMM>(p, sbase, lut, bar_full, bar_empty, ptid, lane); break;
+      case 6: fc_producer<6, GEMM>(p, sbase, lut, bar_full, bar_empty, ptid, lane); break;
+      case 7: fc_producer<7, GEMM>(p, sbase, lut, bar_full, bar_empty, ptid, lane); break;
+      default: fc_producer<8, GEMM>(p, sbase, lut, bar_full, bar_empty, ptid, lane); break;
     }
   }
   ptx::tc_fence_before();
@@ -329,9 +406,9 @@ __global__ void __launch_bounds__(fc_threads(NPART), 1) fc_lif_tc_kernel(const _
   }
 }
 
-template <int NPART, int NS, bool TRAIN>
+template <int NPART, int NS, bool TRAIN, bool GEMM = false>
 cudaError_t fc_launch_kernel(const FcParams &p, int grid, cudaStream_t st) {
-  auto kern = fc_lif_tc_kernel<NPART, NS, TRAIN>;
+  auto kern = fc_lif_tc_kernel<NPART, NS, TRAIN, GEMM>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
   kern<<<grid, fc_threads(NPART), p.smem_bytes, st>>>(p);
@@ -346,6 +423,44 @@ cudaError_t fc_launch_ns(const FcParams &p, int ns, int grid, cudaStream_t st) {
     case 4: return fc_launch_kernel<NPART, 4, TRAIN>(p, grid, st);
     default: return fc_launch_kernel<NPART, 8, TRAIN>(p, grid, st);
   }
+}
+
+// Phase 2 of the two-phase mode: one warp per (sample, 32 outputs), lane = output
+// channel; Y_k = (sum over the K splits in order) 2^-e + b, then the LIF with the fused
+// epilogue's fp32 sequence; spike words by ballot.
+template <int NS>
+__global__ void __launch_bounds__(32) fc_lif_from_y_kernel(const FcParams p) {
+  const int b = blockIdx.x, lane = threadIdx.x, co = blockIdx.y * 32 + lane;
+  const bool ok = co < p.Cout;
+  float V = (ok && p.v_init) ? __ldg(p.v_init + (long long)b * p.Cout + co) : 0.f;
+  bool sprev = p.reset == 1 && V >= p.v_th;
+  const float bias = ok ? __ldg(p.bias + co) : 0.f;
+  uint32_t cnt = 0;
+  uint32_t *optr = p.out + (long long)b * p.out_sb + blockIdx.y;
+  for (int k = 0; k < p.G; ++k) {
+    float acc = 0.f;
+    for (int s = 0; s < p.splits; ++s)
+      acc += ok ? __ldg(p.ws + (((long long)s * p.G + k) * p.B + b) * p.Cout + co) : 0.f;
+    const float y = fmaf(acc, p.iysc, bias);
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      float v = fmaf(p.decay, V, y);
+      if (p.reset == 1 && sprev) v -= p.v_th;
+      const bool sp = ok && v >= p.v_th;
+      if (sp) {
+        if (p.reset == 0) v -= p.v_th;
+        else if (p.reset == 2) v = p.v_reset;
+        ++cnt;
+      }
+      sprev = sp;
+      V = v;
+      const uint32_t bits = __ballot_sync(0xFFFFFFFFu, sp);
+      if (lane == 0) *optr = bits;
+      optr += p.out_st;
+    }
+  }
+  if (ok && p.v_final) p.v_final[(long long)b * p.Cout + co] = V;
+  if (ok && p.counts) p.counts[(long long)b * p.Cout + co] = cnt;
 }
 
 // ---------------------------------------------------------------- host --------
@@ -375,7 +490,26 @@ bool fc_split(const tac_conv_lif_desc *d) {
   return false;
 }
 
+int fc_groups(const tac_conv_lif_desc *d) {
+  const int K = fc_group(d);
+  return (d->T + K - 1) / K;
+}
+
+// Two-phase plan: 0 = fused (enough (M, N) tiles to fill the GPU), else the number of K
+// splits S so that (M tiles x N tiles x groups x S) units cover the 148 SMs
+int fc_two_phase_splits(const tac_conv_lif_desc *d) {
+  const int N = fc_n_tile(d->C_out), nt = (d->C_out + N - 1) / N, mt = (d->B + kFcM - 1) / kFcM;
+  if (mt * nt >= 74) return 0;
+  const int units = mt * nt * fc_groups(d);
+  return std::max(1, std::min(fc_nchunks(d->C_in), (148 + units - 1) / units));
+}
+
 }  // namespace
+
+size_t fc_ws_bytes(const tac_conv_lif_desc *d) {
+  const int S = fc_two_phase_splits(d);
+  return S ? (size_t)S * fc_groups(d) * d->B * d->C_out * 4 : 0;
+}
 
 bool fc_is_fc(const tac_conv_lif_desc *d) {
   return d->H == 1 && d->W == 1 && d->R == 1 && d->S == 1 && d->pad == 0 && d->stride == 1 &&
@@ -467,11 +601,36 @@ int fc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   p.smem_bytes = p.off_bar + 8 * (2 * kFcStages + 4) + 16;
   p.tmem_cols = p.N <= 16 ? 32u : 2u * (uint32_t)p.N;
   const int ns = lp.nsteps;
-  const int grid = std::max(1, std::min(p.m_tiles * p.n_tiles, 148));
   cudaStream_t st = (cudaStream_t)stream;
   const bool train = lp.y_seq != nullptr;
   const int npart = p.N / 32;
   cudaError_t e;
+  p.splits = train ? 0 : fc_two_phase_splits(d);
+  if (p.splits && lp.ws && lp.ws_bytes >= fc_ws_bytes(d)) {
+    // two-phase: the GEMM units fill the GPU, then one warp per (sample, 32 outputs) integrates
+    p.cps = (p.nchunks + p.splits - 1) / p.splits;
+    p.splits = (p.nchunks + p.cps - 1) / p.cps;  // no empty split
+    p.ws = static_cast<float *>(lp.ws);
+    const int units = p.m_tiles * p.n_tiles * p.G * p.splits;
+    const int g1 = std::max(1, std::min(units, 148));
+    if (npart == 1) e = fc_launch_kernel<1, 1, false, true>(p, g1, st);
+    else if (npart == 2) e = fc_launch_kernel<2, 1, false, true>(p, g1, st);
+    else e = fc_launch_kernel<4, 1, false, true>(p, g1, st);
+    ++*launches;
+    if (e != cudaSuccess) return (int)e;
+    const dim3 g2((unsigned)p.B, (unsigned)((p.Cout + 31) / 32));
+    switch (ns) {
+      case 1: fc_lif_from_y_kernel<1><<<g2, 32, 0, st>>>(p); break;
+      case 2: fc_lif_from_y_kernel<2><<<g2, 32, 0, st>>>(p); break;
+      case 4: fc_lif_from_y_kernel<4><<<g2, 32, 0, st>>>(p); break;
+      default: fc_lif_from_y_kernel<8><<<g2, 32, 0, st>>>(p); break;
+    }
+    ++*launches;
+    return (int)cudaGetLastError();
+  }
+  p.splits = 1;
+  p.cps = p.nchunks;
+  const int grid = std::max(1, std::min(p.m_tiles * p.n_tiles, 148));
   if (npart == 1) e = train ? fc_launch_ns<1, true>(p, ns, grid, st) : fc_launch_ns<1, false>(p, ns, grid, st);
   else if (npart == 2) e = train ? fc_launch_ns<2, true>(p, ns, grid, st) : fc_launch_ns<2, false>(p, ns, grid, st);
   else e = train ? fc_launch_ns<4, true>(p, ns, grid, st) : fc_launch_ns<4, false>(p, ns, grid, st);

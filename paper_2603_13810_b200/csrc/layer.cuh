@@ -33,6 +33,8 @@ struct LayerParams {
   const float *bias;  // fp32 [Cout]
   float *y_seq;       // training forward: per-group drive [G][B][Ho][Wo][Cout] as the LIF consumed it
   int yscale_exp;     // tcgen05 fp16 paths: the image's operand prescale 2^e (tac_plan::scale_code)
+  void *ws;           // the call's device workspace (two-phase FC layers), or NULL
+  size_t ws_bytes;
 };
 
 enum { MODE_DENSE = 0, MODE_TAC = 1, MODE_TACTP = 2 };

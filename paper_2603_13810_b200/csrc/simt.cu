@@ -238,6 +238,48 @@ __global__ void pack_kernel(const uint8_t *__restrict__ dense, uint32_t *__restr
   }
 }
 
+// Vectorised pack for the input layers (C = 1 or 2, W a multiple of 32 / C): one thread per
+// output word reads 32 / C consecutive pixels of each channel plane as 16-B vectors
+// (a warp reads 512 contiguous bytes per plane), compacts the 0/1 bytes to bits with one
+// multiply per 4 bytes and, for C = 2, interleaves the two planes' bits (bit 2x + c).
+__device__ __forceinline__ uint32_t bytes4_to_bits(uint32_t x) {  // nonzero byte k -> bit k
+  const uint32_t b = __vcmpne4(x, 0u) & 0x01010101u;
+  return ((b * 0x01020408u) >> 24) & 0xFu;
+}
+__device__ __forceinline__ uint32_t bytes16_to_bits(uint4 v) {
+  return bytes4_to_bits(v.x) | (bytes4_to_bits(v.y) << 4) | (bytes4_to_bits(v.z) << 8) | (bytes4_to_bits(v.w) << 12);
+}
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {  // bit i -> bit 2i
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  return (x | (x << 1)) & 0x55555555u;
+}
+template <int C>
+__global__ void pack_vec_kernel(const uint8_t *__restrict__ dense, uint32_t *__restrict__ packed,
+                                long long nrows, int H, int W, int wpr) {
+  const long long nwords = nrows * wpr;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nwords;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int wi = (int)(i % wpr);
+    const long long tby = i / wpr;  // (t B + b) H + y
+    const long long tb = tby / H;
+    const int yy = (int)(tby - tb * H);
+    const int x0 = wi * (32 / C);
+    uint32_t word;
+    if (C == 1) {
+      const uint4 *src = reinterpret_cast<const uint4 *>(dense + (tb * H + yy) * (long long)W + x0);
+      word = bytes16_to_bits(__ldg(src)) | (bytes16_to_bits(__ldg(src + 1)) << 16);
+    } else {
+      const uint8_t *row0 = dense + ((tb * 2) * H + yy) * (long long)W + x0;
+      const uint32_t p0 = bytes16_to_bits(__ldg(reinterpret_cast<const uint4 *>(row0)));
+      const uint32_t p1 = bytes16_to_bits(__ldg(reinterpret_cast<const uint4 *>(row0 + (long long)H * W)));
+      word = spread16(p0) | (spread16(p1) << 1);
+    }
+    packed[i] = word;
+  }
+}
+
 __global__ void unpack_kernel(const uint32_t *__restrict__ packed, uint8_t *__restrict__ dense,
                               int T, int B, int C, int H, int W, int wpr) {
   const long long n = (long long)T * B * C * H * W;
@@ -314,8 +356,16 @@ int launch_simt_conv_lif(const LayerParams &p, void *stream, int *launches) {
 int launch_pack(const uint8_t *dense, uint32_t *packed, int T, int B, int C, int H, int W,
                 void *stream) {
   const int wpr = (W * C + 31) / 32;
-  pack_kernel<<<grid_for((long long)T * B * H * wpr, 256), 256, 0, (cudaStream_t)stream>>>(
-      dense, packed, T, B, C, H, W, wpr);
+  const bool vec = (C == 1 || C == 2) && W % (32 / C) == 0 && reinterpret_cast<uintptr_t>(dense) % 16 == 0;
+  if (vec && C == 1)
+    pack_vec_kernel<1><<<grid_for((long long)T * B * H * wpr, 256), 256, 0, (cudaStream_t)stream>>>(
+        dense, packed, (long long)T * B * H, H, W, wpr);
+  else if (vec)
+    pack_vec_kernel<2><<<grid_for((long long)T * B * H * wpr, 256), 256, 0, (cudaStream_t)stream>>>(
+        dense, packed, (long long)T * B * H, H, W, wpr);
+  else
+    pack_kernel<<<grid_for((long long)T * B * H * wpr, 256), 256, 0, (cudaStream_t)stream>>>(
+        dense, packed, T, B, C, H, W, wpr);
   return (int)cudaGetLastError();
 }
 

@@ -32,6 +32,8 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &p, const unsigned c
 bool fc_is_fc(const tac_conv_lif_desc *d);
 const char *fc_reason(const tac_conv_lif_desc *d);  // NULL when the FC kernel can run it
 size_t fc_weights_bytes(const tac_conv_lif_desc *d);
+// device workspace of the two-phase FC mode (0: this layer runs fused)
+size_t fc_ws_bytes(const tac_conv_lif_desc *d);
 int fc_prepare(const tac_conv_lif_desc *d, const float *weight, unsigned char *dst);
 int fc_launch(const tac_conv_lif_desc *d, const LayerParams &p, const unsigned char *img, void *stream,
               int *launches);

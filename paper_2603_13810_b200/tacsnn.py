@@ -224,7 +224,8 @@ def prepare_weights(spec: LayerSpec, weight: torch.Tensor, bias: torch.Tensor | 
 
 
 def conv_lif(spec: LayerSpec, prepared: Prepared, x: torch.Tensor, *, v_init=None,
-             want_v_final=False, want_counts=True, out: torch.Tensor | None = None):
+             want_v_final=False, want_counts=True, out: torch.Tensor | None = None,
+             workspace: bool = True):
     """Run one layer (tac_conv_lif_forward) on the current stream.
 
     x: int32/uint32-bit packed spikes [T, B, H, WPR] (rows contiguous; T and B
@@ -263,10 +264,13 @@ def conv_lif(spec: LayerSpec, prepared: Prepared, x: torch.Tensor, *, v_init=Non
     d = spec.desc((x.stride(0), x.stride(1)), (out.stride(0), out.stride(1)))
     wsb = ctypes.c_size_t()
     _check(lib().tac_workspace_bytes(ctypes.byref(d), ctypes.byref(wsb)))
-    ws = torch.empty(wsb.value, dtype=torch.uint8, device=x.device) if wsb.value else None
+    # workspace: required for K not dividing T; optional for two-phase tcgen05 FC layers
+    # (workspace=False exercises their fused path -- the library then needs none)
+    need_ws = wsb.value and (workspace or (spec.partial and spec.T % spec.K != 0 and spec.mode != "dense"))
+    ws = torch.empty(wsb.value, dtype=torch.uint8, device=x.device) if need_ws else None
     fwd = lib().tac_conv_lif_forward_real if real else lib().tac_conv_lif_forward
     _check(fwd(ctypes.byref(d), ctypes.byref(prepared.plan), _ptr(x), _ptr(v_init), _ptr(out), _ptr(v_final),
-               _ptr(counts), _ptr(ws), wsb.value, _stream(x.device)))
+               _ptr(counts), _ptr(ws), wsb.value if ws is not None else 0, _stream(x.device)))
     return out, v_final, counts
 
 

@@ -26,7 +26,7 @@ def to_u32(t: torch.Tensor) -> np.ndarray:
 
 
 def check_layer(T, O, spec, S_u8: np.ndarray, w, b, *, x_packed=None, v_init=None,
-                label=""):
+                label="", workspace=True):
     """Run `spec` on the device and the oracle; returns (oracle output u8
     [T_out,B,C,Hq,Wq] after the spec's pool, device output packed tensor as
     stored with the spec's pool, stats)."""
@@ -39,7 +39,7 @@ def check_layer(T, O, spec, S_u8: np.ndarray, w, b, *, x_packed=None, v_init=Non
         vi_dev = torch.from_numpy(np.ascontiguousarray(
             v_init.transpose(0, 2, 3, 1)).astype(np.float32)).cuda()
     prep = T.prepare_weights(spec, w, b)
-    out, vf, cnt = T.conv_lif(s1, prep, x_packed, v_init=vi_dev, want_v_final=True)
+    out, vf, cnt = T.conv_lif(s1, prep, x_packed, v_init=vi_dev, want_v_final=True, workspace=workspace)
     torch.cuda.synchronize()
     hc, wc = s1.conv_hw
     D = O.unpack_spikes(to_u32(out), s1.C_out, wc)

@@ -57,7 +57,7 @@ def _engine_or_skip(spec, engine):
 
 # ---------------------------------------------------------------- formats ----
 @pytest.mark.parametrize("C,H,W", [(1, 28, 28), (2, 128, 128), (32, 13, 13), (128, 8, 8),
-                                   (3, 5, 7), (8, 26, 26)])
+                                   (3, 5, 7), (8, 26, 26), (1, 5, 96), (2, 7, 48)])
 def test_pack_unpack_match_oracle_format(T, O, C, H, W):
     d = _spikes(C * 100 + W, (3, 2, C, H, W), 0.3)
     p = T.pack(torch.from_numpy(d).cuda())
@@ -545,20 +545,24 @@ FC_CASES = [(1600, 128, 130, 8, "tac", 4, 0.9), (2048, 512, 40, 8, "tactp", 4, 0
             (96, 40, 7, 6, "tactp", 2, 0.9), (200, 64, 257, 8, "tactp", 8, 0.5)]
 
 
-@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("engine", ["simt", "tcgen05", "tcgen05-fused"])
 @pytest.mark.parametrize("reset", ["subtract", "delayed", "hard"])
 @pytest.mark.parametrize("case", FC_CASES, ids=lambda c: f"{c[0]}x{c[1]}b{c[2]}{c[4]}{c[5]}")
 def test_fc_engines_parity(T, O, case, reset, engine):
     """Fully connected LIF layers on both engines: the tcgen05 FC
-    GEMM (M = 128 samples, fp16 hi + lo operands, aggregate table) and the SIMT kernel."""
+    GEMM (M = 128 samples, fp16 hi + lo operands, aggregate table) -- two-phase (group
+    GEMMs split over the SMs into the workspace, then the LIF) and, without a workspace,
+    fused -- and the SIMT kernel."""
     c_in, c_out, B, Tn, mode, K, beta = case
+    fused = engine == "tcgen05-fused"
+    engine = "tcgen05" if fused else engine
     spec = T.LayerSpec(T=Tn, B=B, C_in=c_in, H=1, W=1, C_out=c_out, R=1, S=1, pad=0, K=K,
                        mode=mode, beta=beta, v_reset=-0.2, reset=reset)
     spec = _engine_or_skip(spec, engine)
     seed = zlib.crc32(repr(case).encode()) & 0xFFFF
     S = _spikes(seed, (Tn, B, c_in, 1, 1), 0.2)
     w, b = _w(seed + 1, c_out, c_in, 3.0, r=1, s=1)
-    _, _, st = P.check_layer(T, O, spec, S, w, b, label=f"fc/{case}/{reset}/{engine}")
+    _, _, st = P.check_layer(T, O, spec, S, w, b, label=f"fc/{case}/{reset}/{engine}", workspace=not fused)
     assert 0.0 < st["rate"] < 0.95, st
 
 
