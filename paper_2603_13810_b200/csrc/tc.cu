@@ -311,10 +311,11 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   // stage, so three stages are built concurrently (one stage's latency -- loads, table
   // lookups, the async-proxy fence -- no longer serialises the pipeline)
   static const bool no_ws = [] { const char *e = std::getenv("TACSNN_NO_WARP_STAGE"); return e && *e == '1'; }();
-  p.warp_stage = (!no_ws && g.path != PATH_HALO && p.use_tma != 1) ? 1 : 0;
+  static const bool no_hrows = [] { const char *e = std::getenv("TACSNN_NO_HALO_ROWS"); return e && *e == '1'; }();
+  p.warp_stage = (!no_ws && g.path != PATH_HALO && (p.use_tma != 1 || (!no_hrows && rows_ok(d)))) ? 1 : 0;
   p.prod_step = p.warp_stage ? 32 : 32 * kProdWarps;
   static const bool no_pr = [] { const char *e = std::getenv("TACSNN_NO_PROD_REFILL"); return e && *e == '1'; }();
-  p.prod_refill = (!no_pr && p.warp_stage && p.use_tma == 2) ? 1 : 0;
+  p.prod_refill = (!no_pr && p.warp_stage && p.use_tma != 0) ? 1 : 0;
   p.raw_bw = g.raw_bw;
   p.nraw = g.nraw;
   p.off_raw = g.off_raw;

@@ -262,6 +262,15 @@ uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
 // Shared-memory plan.  With use_tma the producers aggregate from a TMA-loaded
 // raw halo ([K][18][raw_bw] u32 per stage) instead of loading from global.
+// the row producers (produce_plane_rows / produce_halo_rows) take this layer: C_in <= 2,
+// a templated K <= 8, spike input, and a table (split) or an exact beta = 1/2 / dense aggregate
+bool rows_ok(const tac_conv_lif_desc *d) {
+  const int K = d->mode == TAC_MODE_DENSE ? 1 : d->K;
+  const bool exact_m1 = d->mode == TAC_MODE_DENSE || K == 1 || beta_shift(d->beta) == 1;
+  return path_of(d) != PATH_HALO && d->C_in <= 2 && templ_k(K) && K <= 8 && d->input_kind == TAC_INPUT_SPIKES &&
+         (split_of(d) || exact_m1);
+}
+
 Geometry geometry(const tac_conv_lif_desc *d, bool use_tma = false, int plane_words = 0) {
   Geometry g{};
   g.path = path_of(d);
@@ -291,7 +300,7 @@ Geometry geometry(const tac_conv_lif_desc *d, bool use_tma = false, int plane_wo
   g.raw_box_bytes = (uint32_t)K * (plane_words > 0 ? 1 : kHaloH) * g.raw_bw * 4u;
   g.raw_stage_bytes = align_up(g.raw_box_bytes, 128);
   // pixel-wise producers (plane mode or LDG, fp16 paths) try deeper A rings first
-  const bool deep = g.path != PATH_HALO && (plane_words > 0 || !use_tma);
+  const bool deep = g.path != PATH_HALO && (plane_words > 0 || !use_tma || rows_ok(d));
   const int combos[11][2] = {{8, 8}, {8, 4}, {6, 4}, {4, 4}, {3, 4}, {3, 3}, {3, 2}, {2, 2}, {3, 1}, {2, 1}, {2, 0}};
   for (int ci = deep ? 0 : 4; ci < 11; ++ci) {
     g.nstages = combos[ci][0];
@@ -754,28 +763,11 @@ __device__ __forceinline__ void produce_h16s_rt(const TcParams &p, const uint32_
 // q + 8 b, and each pixel's index feeds the aggregate table (split path) or is the
 // exact aggregate itself (beta = 1/2 or dense: sum_j bit_j 2^j).  Chunk 1 of every
 // row is constant (h16_init_stages), so only chunk 0 is stored.
+__device__ __forceinline__ int halo_c0(const TcParams &p, int x0);
+// v[j]: frame j's bits of halo row `lane`, halo column 0 at bit 0 -> the row's 10 A rows
 template <int K, int CIN, bool SPLIT>
-__device__ __forceinline__ void produce_plane_rows(const TcParams &p, const uint32_t *lut, int tile,
-                                                   uint32_t a_stage, int lane, const uint32_t *plane) {
-  static_assert(K >= 1 && K <= 8 && (CIN == 1 || CIN == 2), "row producer envelope");
-  if (lane >= kHaloH) return;
-  int b, y0, x0;
-  bool tok;
-  tile_origin(p, tile, b, y0, x0, tok);
-  const int yi = y0 + lane - p.pad;
-  const bool rok = tok && yi >= 0 && yi < p.H;
-  const int bit0 = (x0 - p.pad) * CIN;       // row bit of halo column 0 (-CIN with left padding)
-  const int wb = bit0 >> 5, sh = bit0 & 31;  // floor division
-  const int wpr = p.wpr_in;
-  const uint32_t *row = plane + (rok ? yi : 0) * wpr;
-  uint32_t v[K];
-#pragma unroll
-  for (int j = 0; j < K; ++j) {
-    const uint32_t *fr = row + j * p.raw_bw;
-    const uint32_t w0 = (rok && wb >= 0 && wb < wpr) ? fr[wb] : 0u;
-    const uint32_t w1 = (rok && wb + 1 >= 0 && wb + 1 < wpr) ? fr[wb + 1] : 0u;
-    v[j] = __funnelshift_r(w0, w1, sh);      // bits beyond W C_in are 0 in a packed row
-  }
+__device__ __forceinline__ void emit_halo_row(const TcParams &p, const uint32_t *lut, uint32_t a_stage,
+                                              int lane, const uint32_t (&v)[K]) {
   uint32_t o[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
@@ -805,6 +797,49 @@ __device__ __forceinline__ void produce_plane_rows(const TcParams &p, const uint
                         u8x2_to_f16x2(hi, 0x5140u), u8x2_to_f16x2(hi, 0x7362u));
     }
   }
+}
+
+// The same row producer on a TMA raw HALO box ([K][18][raw_bw] words from the 16-B
+// aligned word c0w; the box's out-of-bounds zero fill is the conv padding): the DVS first
+// layer (2 x 128 x 128, one producer warp per stage).
+template <int K, int CIN, bool SPLIT>
+__device__ __forceinline__ void produce_halo_rows(const TcParams &p, const uint32_t *lut, const uint32_t *raw,
+                                                  uint32_t a_stage, int lane, int x0) {
+  static_assert(K >= 1 && K <= 8 && (CIN == 1 || CIN == 2), "row producer envelope");
+  if (lane >= kHaloH) return;
+  const int bw = p.raw_bw, fstride = kHaloH * p.raw_bw;
+  const int bit0 = (x0 - p.pad) * CIN - (halo_c0(p, x0) & ~3) * 32;  // >= 0
+  const uint32_t *row = raw + lane * bw + (bit0 >> 5);
+  const int sh = bit0 & 31;
+  uint32_t v[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) v[j] = __funnelshift_r(row[j * fstride], row[j * fstride + 1], sh);
+  emit_halo_row<K, CIN, SPLIT>(p, lut, a_stage, lane, v);
+}
+
+template <int K, int CIN, bool SPLIT>
+__device__ __forceinline__ void produce_plane_rows(const TcParams &p, const uint32_t *lut, int tile,
+                                                   uint32_t a_stage, int lane, const uint32_t *plane) {
+  static_assert(K >= 1 && K <= 8 && (CIN == 1 || CIN == 2), "row producer envelope");
+  if (lane >= kHaloH) return;
+  int b, y0, x0;
+  bool tok;
+  tile_origin(p, tile, b, y0, x0, tok);
+  const int yi = y0 + lane - p.pad;
+  const bool rok = tok && yi >= 0 && yi < p.H;
+  const int bit0 = (x0 - p.pad) * CIN;       // row bit of halo column 0 (-CIN with left padding)
+  const int wb = bit0 >> 5, sh = bit0 & 31;  // floor division
+  const int wpr = p.wpr_in;
+  const uint32_t *row = plane + (rok ? yi : 0) * wpr;
+  uint32_t v[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const uint32_t *fr = row + j * p.raw_bw;
+    const uint32_t w0 = (rok && wb >= 0 && wb < wpr) ? fr[wb] : 0u;
+    const uint32_t w1 = (rok && wb + 1 >= 0 && wb + 1 < wpr) ? fr[wb + 1] : 0u;
+    v[j] = __funnelshift_r(w0, w1, sh);      // bits beyond W C_in are 0 in a packed row
+  }
+  emit_halo_row<K, CIN, SPLIT>(p, lut, a_stage, lane, v);
 }
 
 template <int K>
@@ -1101,7 +1136,11 @@ __device__ __forceinline__ void refill_plane(const TcParams &p, uint32_t sbase, 
   tile_origin(p, 2 * pair + (int)rank, b, y0, x0, tok);
   const uint32_t bar = bar_raw + 8 * r;
   ptx::mbar_arrive_expect_tx(bar, p.raw_box_bytes);
-  ptx::tma_load_3d(sbase + p.off_raw + r * p.raw_stage_bytes, &p.tmap, 0, b, k * p.K, bar);
+  if (p.use_tma == 2)
+    ptx::tma_load_3d(sbase + p.off_raw + r * p.raw_stage_bytes, &p.tmap, 0, b, k * p.K, bar);
+  else
+    ptx::tma_load_4d(sbase + p.off_raw + r * p.raw_stage_bytes, &p.tmap, halo_c0(p, x0) & ~3, y0 - p.pad, b,
+                     k * p.K, bar);
 }
 
 // TMA producer pipeline: all 96 producer threads aggregate raw stage `it % nraw`
@@ -1171,6 +1210,15 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
                      : produce_h16s_tma_rt<2>(p, lut, raw, a_stage, ptid, x0);
       } else if (PATH == PATH_HALO) {
         produce_halo_tma<K>(p, raw, a_stage, ptid, x0);
+      } else if (ws) {  // halo boxes, one producer warp per stage (host: rows_ok)
+        if constexpr (K <= 8) {
+          if (PATH == PATH_SPLIT)
+            p.Cin == 1 ? produce_halo_rows<K, 1, true>(p, lut, raw, a_stage, wptid, x0)
+                       : produce_halo_rows<K, 2, true>(p, lut, raw, a_stage, wptid, x0);
+          else
+            p.Cin == 1 ? produce_halo_rows<K, 1, false>(p, lut, raw, a_stage, wptid, x0)
+                       : produce_halo_rows<K, 2, false>(p, lut, raw, a_stage, wptid, x0);
+        }
       } else if (PATH == PATH_SPLIT) {
         p.Cin == 32 ? produce_s32_tma<K>(p, lut, raw, a_stage, ptid, x0)
                     : (p.Cin == 1 ? produce_h16s_tma<K, 1>(p, lut, raw, a_stage, ptid, x0)
