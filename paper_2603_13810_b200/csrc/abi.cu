@@ -597,13 +597,22 @@ tac_status tac_conv_lif_forward_train(const tac_conv_lif_desc *desc, const tac_p
   return st;
 }
 
+// the tcgen05 input gradient's weight image (bwd_tc.cu) follows dL/dY in the backward
+// workspace for the shapes it takes (a layer whose forward runs on tcgen05)
+size_t bwd_dgrad_img_bytes(const tac_conv_lif_desc *d) {
+  const bool ok = resolve_engine(d) == TAC_ENGINE_TCGEN05 && d->R == 3 && d->S == 3 && d->stride == 1 &&
+                  (d->pad == 0 || d->pad == 1) && (d->C_in == 32 || d->C_in == 64 || d->C_in == 128) &&
+                  d->C_out % 32 == 0;
+  return ok ? align256(tacsnn::dgrad_tc_ws_bytes(d->C_in, d->C_out)) : 0;
+}
+
 tac_status tac_backward_workspace_bytes(const tac_conv_lif_desc *desc, size_t *bytes) {
   g_detail.clear();
   Geo g;
   tac_status st = check(desc, &g);
   if (st != TAC_OK) return st;
   if (!bytes) return fail(TAC_ERR_NULL, "bytes is NULL");
-  *bytes = align256((size_t)g.G * desc->B * g.Ho * g.Wo * desc->C_out * 4);
+  *bytes = align256((size_t)g.G * desc->B * g.Ho * g.Wo * desc->C_out * 4) + bwd_dgrad_img_bytes(desc);
   return TAC_OK;
 }
 
@@ -661,6 +670,8 @@ tac_status tac_conv_lif_backward(const tac_conv_lif_desc *desc, const tac_plan *
   p.xin = real ? static_cast<const float *>(input) : nullptr;
   p.v_init = v_init; p.y_seq = y_seq; p.g_spikes = g_spikes; p.g_vfinal = g_v_final;
   p.g_y = static_cast<float *>(ws); p.g_vinit = g_v_init;
+  const size_t gy_bytes = align256((size_t)g.G * desc->B * g.Ho * g.Wo * desc->C_out * 4);
+  p.dg_img = bwd_dgrad_img_bytes(desc) ? static_cast<unsigned char *>(ws) + gy_bytes : nullptr;
   p.w = reinterpret_cast<const float *>(base + L.simt_off);
   p.g_w = g_weight; p.g_b = g_bias; p.g_in = g_input; p.g_alpha = g_agg_weights;
   int launches = 0;

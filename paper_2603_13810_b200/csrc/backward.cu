@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "layer.cuh"
 
@@ -393,7 +394,11 @@ int launch_backward(const BwdParams &p, void *stream, int *launches) {
     wgrad_direct_kernel<<<grid1(nw + p.Cout, 128), 128, 0, st>>>(p);
   }
   ++*launches;
-  if (p.g_in || p.g_alpha) {
+  static const bool no_dgtc = [] { const char *e = std::getenv("TACSNN_NO_DGRAD_TC"); return e && *e == '1'; }();
+  if ((p.g_in || p.g_alpha) && p.dg_img && !no_dgtc && dgrad_tc_ok(p)) {
+    const int e = launch_dgrad_tc(p, p.dg_img, stream, launches);
+    if (e) return e;
+  } else if (p.g_in || p.g_alpha) {
     const long long npix = (long long)p.G * p.B * p.H * p.W;
     dim3 grid((unsigned)((npix + 127) / 128), (unsigned)((p.Cin + kDgradCh - 1) / kDgradCh));
     dgrad_kernel<<<grid, 128, 0, st>>>(p);

@@ -1,0 +1,344 @@
+// bwd_tc.cu -- the input gradient of the training backward on the
+// tensor cores.  Per group k the conv's data gradient is the transposed conv
+//   dL/dA_k[b][yi][xi][ci] = sum_{r,s,co} dL/dY_k[b][yi + pad - r][xi + pad - s][co] W[co][ci][r][s]
+// i.e. a forward 3x3 conv of dL/dY_k (C_out channels, padding 2 - pad) with the flipped,
+// transposed weights W'[ci][co][r'][s'] = W[co][ci][2 - r'][2 - s'].  It runs as a tcgen05
+// implicit GEMM exactly like the forward conv (16 x 8 output tile = M 128, the 18 x 10 halo
+// K-major without swizzle so every tap is a descriptor offset), with real-valued operands
+// carried as bf16 hi + lo pairs (x = x_hi + x_lo, |x - x_hi - x_lo| <= 2^-17 |x|; bf16 keeps
+// fp32's exponent range, so tiny gradients do not underflow) and three MMAs per K step
+// (hi.hi + hi.lo + lo.hi) into an fp32 TMEM accumulator.  The epilogue writes
+// dL/dS_{kK+j} = a_j dL/dA_k (PAPER.md:115 / :427 weights a_j) and the dL/da_j partial sums.
+//
+// Roles (one CTA per SM, cta_group::1): 4 NPART epilogue warps (TMEM lane quadrant x 32 input
+// channels), 1 MMA warp, 1 weight loader warp (bulk copies of the per-(chunk, tap) bf16
+// weight blocks, prepared on the device by dg_weights_kernel), 4 producer warps (the dL/dY
+// halo of one 32-channel chunk, fp32 -> bf16 hi / lo).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "layer.cuh"
+#include "ptx.cuh"
+
+namespace tacsnn {
+namespace {
+
+constexpr int kDgTileH = 16, kDgTileW = 8;
+constexpr int kDgHaloH = 18, kDgHaloW = 10, kDgHaloRows = 180;
+constexpr int kDgCo = 32;          // dL/dY channels per K chunk (4 16-B K chunks of 8 bf16)
+constexpr int kDgAStages = 2, kDgBStages = 4, kDgProd = 4;
+constexpr uint32_t kDgASlice = kDgHaloRows * 4 * 16;  // one of hi / lo: [4 kc][180 rows][16 B]
+
+struct DgParams {
+  int G, B, H, W, Cin, Cout, K, pad, Ho, Wo, wpr_in;
+  int tiles_x, tiles_y, nunits, nchunks;
+  long long in_st, in_sb;
+  float coef[kMaxK];
+  const float *g_y;            // [G][B][Ho][Wo][Cout]
+  const unsigned char *wimg;   // [chunk][tap][slice][4 kc][Cin][16 B] bf16
+  const uint32_t *in;          // packed input spikes (dL/da_j)
+  float *g_in;                 // [T][B][H][W][Cin] or NULL
+  float *g_alpha;              // [K] or NULL
+  uint32_t b_bytes, off_b, off_bar, smem_bytes, tmem_cols;
+};
+
+constexpr int dg_threads(int npart) { return 32 * (4 * npart + 2 + kDgProd); }
+
+__device__ __forceinline__ void dg_unit(const DgParams &p, int u, int &k, int &b, int &y0, int &x0) {
+  const int per = p.tiles_x * p.tiles_y;
+  int t = u % per;
+  const int kb = u / per;
+  b = kb % p.B;
+  k = kb / p.B;
+  const int ty = t / p.tiles_x;
+  y0 = ty * kDgTileH;
+  x0 = (t - ty * p.tiles_x) * kDgTileW;
+}
+
+__device__ __forceinline__ uint32_t bf16x2_hi(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t *>(&v);
+}
+// x -> (hi, lo) bf16 pairs of two values: hi = bf16(x), lo = bf16(x - hi)
+__device__ __forceinline__ void split2(float a, float b, uint32_t &hi, uint32_t &lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  const float2 hf = __bfloat1622float2(h);
+  const __nv_bfloat162 l = __floats2bfloat162_rn(a - hf.x, b - hf.y);
+  hi = *reinterpret_cast<const uint32_t *>(&h);
+  lo = *reinterpret_cast<const uint32_t *>(&l);
+}
+
+// producers: the dL/dY_k halo of one 32-channel chunk -> bf16 hi | lo K-major stages
+__device__ __forceinline__ void dg_producer(const DgParams &p, uint32_t sbase, uint32_t bar_afull,
+                                            uint32_t bar_aempty, int ptid, uint32_t lane) {
+  uint32_t it = 0;
+  const int org = 2 - p.pad;  // halo origin offset of the transposed conv
+  const long long N = (long long)p.B * p.Ho * p.Wo * p.Cout;
+  for (int u = blockIdx.x; u < p.nunits; u += gridDim.x) {
+    int k, b, y0, x0;
+    dg_unit(p, u, k, b, y0, x0);
+    for (int c = 0; c < p.nchunks; ++c, ++it) {
+      const uint32_t s = it % kDgAStages, ph = (it / kDgAStages) & 1u;
+      ptx::mbar_wait(bar_aempty + 8 * s, ph ^ 1u);
+      const uint32_t st = sbase + s * 2 * kDgASlice;
+      for (int i = ptid; i < kDgHaloRows * 4; i += 32 * kDgProd) {
+        const int row = i >> 2, kc = i & 3;
+        const int hy = row / kDgHaloW, hx = row - hy * kDgHaloW;
+        const int y = y0 + hy - org, x = x0 + hx - org;
+        float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+        if (y >= 0 && y < p.Ho && x >= 0 && x < p.Wo) {
+          const float4 *src = reinterpret_cast<const float4 *>(
+              p.g_y + (long long)k * N + (((long long)b * p.Ho + y) * p.Wo + x) * p.Cout + c * kDgCo + kc * 8);
+          v0 = __ldg(src);
+          v1 = __ldg(src + 1);
+        }
+        uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
+        split2(v0.x, v0.y, h0, l0);
+        split2(v0.z, v0.w, h1, l1);
+        split2(v1.x, v1.y, h2, l2);
+        split2(v1.z, v1.w, h3, l3);
+        const uint32_t dst = st + (uint32_t)(kc * kDgHaloRows + row) * 16u;
+        ptx::st_shared_v4(dst, h0, h1, h2, h3);
+        ptx::st_shared_v4(dst + kDgASlice, l0, l1, l2, l3);
+      }
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_local(bar_afull + 8 * s);
+    }
+  }
+}
+
+template <int NPART>
+__device__ __forceinline__ void dg_epilogue(const DgParams &p, uint32_t tmem_base, uint32_t bar_tfull,
+                                            uint32_t bar_tempty, uint32_t warp, uint32_t lane) {
+  const int quad = (int)(warp & 3), part = (int)(warp >> 2);
+  const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+  const int g = quad * 4 + (int)(lane >> 3), cx = (int)(lane & 7);  // tile pixel of this lane (row i = 8 g + c)
+  const int ci0 = part * 32;
+  const long long plane = (long long)p.H * p.W * p.Cin;
+  uint32_t it = 0;
+  for (int u = blockIdx.x; u < p.nunits; u += gridDim.x, ++it) {
+    int k, b, y0, x0;
+    dg_unit(p, u, k, b, y0, x0);
+    const int yi = y0 + g, xi = x0 + cx;
+    const bool ok = yi < p.H && xi < p.W;
+    const uint32_t acc = it & 1u, aph = (it >> 1) & 1u;
+    ptx::mbar_wait(bar_tfull + 8 * acc, aph);
+    ptx::tc_fence_after();
+    const uint32_t tcol = tmem_base + lane_addr + acc * (uint32_t)p.Cin + (uint32_t)ci0;
+    float dA[32];
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      uint32_t d[8], dz[8];
+      ptx::tmem_ld8(tcol + cc * 8, d);
+      ptx::tmem_wait_ld_dep(d, dz);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) dA[cc * 8 + q] = __uint_as_float(d[q]);
+    }
+    ptx::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive_local(bar_tempty + 8 * acc);
+    for (int j = 0; j < p.K; ++j) {
+      const int t = k * p.K + j;
+      const float aj = p.coef[j];
+      if (p.g_in && ok) {
+        float4 *dst = reinterpret_cast<float4 *>(p.g_in + ((long long)t * p.B + b) * plane +
+                                                 ((long long)yi * p.W + xi) * p.Cin + ci0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          dst[q] = make_float4(aj * dA[4 * q], aj * dA[4 * q + 1], aj * dA[4 * q + 2], aj * dA[4 * q + 3]);
+      }
+      if (p.g_alpha) {  // dL/da_j = sum <dL/dA_k, S_{kK+j}> (uniform branch: whole warp shuffles)
+        float s = 0.f;
+        if (ok) {
+          const uint32_t w = __ldg(p.in + (long long)t * p.in_st + (long long)b * p.in_sb +
+                                   (long long)yi * p.wpr_in + (((long long)xi * p.Cin + ci0) >> 5));
+#pragma unroll
+          for (int q = 0; q < 32; ++q) s += ((w >> q) & 1u) ? dA[q] : 0.f;
+        }
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+        if (lane == 0 && s != 0.f) atomicAdd(p.g_alpha + j, s);
+      }
+    }
+  }
+}
+
+template <int NPART>
+__global__ void __launch_bounds__(dg_threads(NPART), 1) dgrad_tc_kernel(const __grid_constant__ DgParams p) {
+  constexpr int kEpi = 4 * NPART;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t warp = __shfl_sync(0xFFFFFFFFu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31;
+  const uint32_t sbase = ptx::smem_u32(smem);
+  const uint32_t bar_afull = sbase + p.off_bar, bar_aempty = bar_afull + 8 * kDgAStages;
+  const uint32_t bar_bfull = bar_aempty + 8 * kDgAStages, bar_bempty = bar_bfull + 8 * kDgBStages;
+  const uint32_t bar_tfull = bar_bempty + 8 * kDgBStages, bar_tempty = bar_tfull + 16;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + p.off_bar + 8 * (2 * kDgAStages + 2 * kDgBStages + 4));
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kDgAStages; ++s) {
+      ptx::mbar_init(bar_afull + 8 * s, kDgProd);
+      ptx::mbar_init(bar_aempty + 8 * s, 1);
+    }
+    for (int s = 0; s < kDgBStages; ++s) {
+      ptx::mbar_init(bar_bfull + 8 * s, 1);
+      ptx::mbar_init(bar_bempty + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(bar_tfull + 8 * a, 1);
+      ptx::mbar_init(bar_tempty + 8 * a, kEpi);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == (uint32_t)kEpi) {
+    ptx::tmem_alloc_cg1(ptx::smem_u32(tmem_slot), p.tmem_cols);
+    ptx::tmem_relinquish_cg1();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp < (uint32_t)kEpi) {
+    dg_epilogue<NPART>(p, tmem_base, bar_tfull, bar_tempty, warp, lane);
+  } else if (warp == (uint32_t)kEpi) {
+    // MMA issuer: per unit, chunks x taps x 2 K steps x 3 MMAs into one accumulator
+    const uint32_t idesc = ptx::idesc_bf16((uint32_t)128, (uint32_t)p.Cin);
+    const uint32_t lbo_a = kDgHaloRows * 16u, lbo_b = (uint32_t)p.Cin * 16u;
+    uint32_t ia = 0, ib = 0;
+    for (int u = blockIdx.x, uu = 0; u < p.nunits; u += gridDim.x, ++uu) {
+      const uint32_t acc = (uint32_t)uu & 1u, aph = ((uint32_t)uu >> 1) & 1u;
+      ptx::mbar_wait(bar_tempty + 8 * acc, aph ^ 1u);
+      ptx::tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * (uint32_t)p.Cin;
+      for (int c = 0; c < p.nchunks; ++c, ++ia) {
+        const uint32_t sa = ia % kDgAStages, pha = (ia / kDgAStages) & 1u;
+        ptx::mbar_wait(bar_afull + 8 * sa, pha);
+        const uint32_t ast = sbase + sa * 2 * kDgASlice;
+        for (int tap = 0; tap < 9; ++tap, ++ib) {
+          const uint32_t sb = ib % kDgBStages, phb = (ib / kDgBStages) & 1u;
+          ptx::mbar_wait(bar_bfull + 8 * sb, phb);
+          ptx::tc_fence_after();
+          const uint32_t bst = sbase + p.off_b + sb * p.b_bytes;
+          const uint32_t toff = (uint32_t)((tap / 3) * kDgHaloW + (tap % 3)) * 16u;
+          if (ptx::elect_one()) {
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+              const uint64_t ahi = ptx::smem_desc(ast + toff + ks * 2 * lbo_a, lbo_a, kDgHaloW * 16u);
+              const uint64_t alo = ptx::smem_desc(ast + kDgASlice + toff + ks * 2 * lbo_a, lbo_a, kDgHaloW * 16u);
+              const uint64_t bhi = ptx::smem_desc(bst + ks * 2 * lbo_b, lbo_b, 128u);
+              const uint64_t blo = ptx::smem_desc(bst + 4 * lbo_b + ks * 2 * lbo_b, lbo_b, 128u);
+              ptx::mma_f16_cg1(d_tmem, ahi, bhi, idesc, (c | tap | ks) ? 1u : 0u);
+              ptx::mma_f16_cg1(d_tmem, ahi, blo, idesc, 1u);
+              ptx::mma_f16_cg1(d_tmem, alo, bhi, idesc, 1u);
+            }
+            ptx::mma_commit_cg1(bar_bempty + 8 * sb);
+            if (tap == 8) ptx::mma_commit_cg1(bar_aempty + 8 * sa);
+            if (tap == 8 && c == p.nchunks - 1) ptx::mma_commit_cg1(bar_tfull + 8 * acc);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp == (uint32_t)kEpi + 1) {
+    // weight loader: the (chunk, tap) bf16 blocks in MMA order, kDgBStages ahead
+    if (lane == 0) {
+      uint32_t ib = 0;
+      for (int u = blockIdx.x; u < p.nunits; u += gridDim.x)
+        for (int c = 0; c < p.nchunks; ++c)
+          for (int tap = 0; tap < 9; ++tap, ++ib) {
+            const uint32_t sb = ib % kDgBStages, ph = (ib / kDgBStages) & 1u;
+            ptx::mbar_wait(bar_bempty + 8 * sb, ph ^ 1u);
+            ptx::mbar_arrive_expect_tx(bar_bfull + 8 * sb, p.b_bytes);
+            ptx::bulk_g2s(sbase + p.off_b + sb * p.b_bytes, p.wimg + ((size_t)c * 9 + tap) * p.b_bytes, p.b_bytes,
+                          bar_bfull + 8 * sb);
+          }
+    }
+    __syncwarp();
+  } else {
+    dg_producer(p, sbase, bar_afull, bar_aempty, (int)(threadIdx.x - 32 * (kEpi + 2)), lane);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == (uint32_t)kEpi) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_cg1(tmem_base, p.tmem_cols);
+  }
+}
+
+// W (SIMT layout fp32 [Cin][R][S][Cout]) -> flipped, transposed bf16 hi / lo blocks
+// [chunk][tap'][slice][kc][ci][8]: element (ci, co = 32 chunk + 8 kc + e) of tap' = 3 r' + s'
+// is W[co][ci][2 - r'][2 - s'].
+__global__ void dg_weights_kernel(const float *w, int Cin, int Cout, unsigned char *img) {
+  const long long n = (long long)Cin * Cout * 9;
+  __nv_bfloat16 *h = reinterpret_cast<__nv_bfloat16 *>(img);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int co = (int)(i % Cout);
+    const long long q = i / Cout;
+    const int tap = (int)(q % 9), ci = (int)(q / 9);
+    const int r = 2 - tap / 3, s = 2 - tap % 3;
+    const float v = w[((long long)(ci * 3 + r) * 3 + s) * Cout + co];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+    const int chunk = co / kDgCo, kc = (co % kDgCo) / 8, e = co % 8;
+    const long long blk = ((long long)chunk * 9 + tap) * 2;               // [chunk][tap][slice]
+    const long long off = ((long long)kc * Cin + ci) * 8 + e;             // [kc][ci][8]
+    const long long slice = (long long)4 * Cin * 8;                        // halves per slice
+    h[blk * slice + off] = hi;
+    h[(blk + 1) * slice + off] = lo;
+  }
+}
+
+template <int NPART>
+cudaError_t dg_launch(const DgParams &p, cudaStream_t st) {
+  auto kern = dgrad_tc_kernel<NPART>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+  if (e != cudaSuccess) return e;
+  kern<<<std::min(p.nunits, 148), dg_threads(NPART), p.smem_bytes, st>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool dgrad_tc_ok(const BwdParams &p) {
+  return (p.g_alpha ? (p.in && !p.xin) : true) && p.R == 3 && p.S == 3 && p.stride == 1 && (p.pad == 0 || p.pad == 1) &&
+         (p.Cin == 32 || p.Cin == 64 || p.Cin == 128) && p.Cout % kDgCo == 0 && p.Cin % 32 == 0 &&
+         p.K <= kMaxK;
+}
+
+size_t dgrad_tc_ws_bytes(int Cin, int Cout) { return (size_t)Cin * Cout * 9 * 2 * 2; }
+
+int launch_dgrad_tc(const BwdParams &bp, void *img, void *stream, int *launches) {
+  cudaStream_t st = (cudaStream_t)stream;
+  dg_weights_kernel<<<148, 256, 0, st>>>(bp.w, bp.Cin, bp.Cout, static_cast<unsigned char *>(img));
+  ++*launches;
+  DgParams p{};
+  p.G = bp.G; p.B = bp.B; p.H = bp.H; p.W = bp.W; p.Cin = bp.Cin; p.Cout = bp.Cout; p.K = bp.K;
+  p.pad = bp.pad; p.Ho = bp.Ho; p.Wo = bp.Wo; p.wpr_in = bp.wpr_in;
+  p.tiles_x = (bp.W + kDgTileW - 1) / kDgTileW;
+  p.tiles_y = (bp.H + kDgTileH - 1) / kDgTileH;
+  p.nunits = bp.G * bp.B * p.tiles_x * p.tiles_y;
+  p.nchunks = bp.Cout / kDgCo;
+  p.in_st = bp.in_st; p.in_sb = bp.in_sb;
+  for (int j = 0; j < kMaxK; ++j) p.coef[j] = bp.coef[j];
+  p.g_y = bp.g_y;
+  p.wimg = static_cast<const unsigned char *>(img);
+  p.in = bp.in;
+  p.g_in = bp.g_in;
+  p.g_alpha = bp.g_alpha;
+  p.b_bytes = 2u * 4u * (uint32_t)bp.Cin * 16u;  // [slice][4 kc][Cin][16 B]
+  p.off_b = kDgAStages * 2 * kDgASlice;
+  p.off_bar = p.off_b + kDgBStages * p.b_bytes;
+  p.smem_bytes = p.off_bar + 8 * (2 * kDgAStages + 2 * kDgBStages + 4) + 16;
+  p.tmem_cols = 2u * (uint32_t)bp.Cin <= 32u ? 32u : 2u * (uint32_t)bp.Cin;
+  cudaError_t e;
+  switch (bp.Cin) {
+    case 32: e = dg_launch<1>(p, st); break;
+    case 64: e = dg_launch<2>(p, st); break;
+    default: e = dg_launch<4>(p, st); break;
+  }
+  ++*launches;
+  return (int)e;
+}
+
+}  // namespace tacsnn

@@ -223,6 +223,11 @@ __host__ __device__ constexpr uint32_t idesc_f16(uint32_t M, uint32_t N) {
          | ((M >> 4) << 24);
 }
 
+// kind::f16 with bf16 operands (A, B format BF16), f32 accumulator
+__host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
 __device__ __forceinline__ void mma_f16_cg2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
                                             uint32_t idesc, uint32_t accumulate) {
   asm volatile(
