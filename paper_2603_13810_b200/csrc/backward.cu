@@ -383,7 +383,12 @@ int launch_backward(const BwdParams &p, void *stream, int *launches) {
     zero_f32_kernel<<<1, 32, 0, st>>>(p.g_alpha, p.K);
     ++*launches;
   }
-  if (p.stride == 1 && p.R <= 3 && p.S <= 3) {
+  static const bool no_wgtc = [] { const char *e = std::getenv("TACSNN_NO_WGRAD_TC"); return e && *e == '1'; }();
+  if (p.dg_img && !no_wgtc && wgrad_tc_ok(p)) {
+    const int e = launch_wgrad_tc(p, stream, launches);
+    if (e) return e;
+    --*launches;  // counted below with the SIMT variants
+  } else if (p.stride == 1 && p.R <= 3 && p.S <= 3) {
     const long long nrows = (long long)p.G * p.B * p.Ho;
     const int cob = (p.Cout + kWgCo - 1) / kWgCo, cib = (p.Cin + kWgCi - 1) / kWgCi;
     const long long want = std::max(1LL, 148LL * 4 / (cob * cib));

@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 
 #include "layer.cuh"
 #include "ptx.cuh"
@@ -298,6 +300,208 @@ cudaError_t dg_launch(const DgParams &p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------- weight gradient --
+// dL/dW[co][ci][r][s] = sum_{k,b,y,x} dL/dY_k[b][y][x][co] A_k[b][y + r - pad][x + s - pad][ci]
+// per tap a GEMM with M = C_out, N = C_in and the pixels as the reduction.  Both operands
+// are used MN-major (a 16-B row = 8 consecutive channels of one pixel, i.e. the natural
+// channels-last rows, no transposition): along K (pixels) the rows of a core matrix are
+// consecutive tile pixels, so a spatial tap shift is a descriptor start offset along K --
+// the forward's halo trick with the roles of pixels and channels exchanged.  A CTA owns
+// one kernel row r (its 3 taps s = 0..2 accumulate into 3 x C_in TMEM columns over all of
+// its (group, sample, tile) units) and adds its partial dL/dW once at the end.
+constexpr int kWgAStg = 2;
+constexpr int kWgHaloRows = kDgTileH * kDgHaloW;  // 16 x 10 halo pixels of one kernel row
+
+struct WgParams {
+  int G, B, H, W, Cin, Cout, K, pad, Ho, Wo, wpr_in;
+  int tiles_x, tiles_y, nunits, split, nstages, ncta_r;
+  long long in_st, in_sb;
+  float coef[kMaxK];
+  float a_scale;               // exact path: A carried as integers, true A = a_scale x stored
+  const float *g_y;            // [G][B][Ho][Wo][Cout]
+  const uint32_t *in;          // packed input spikes [T][B][H][WPR]
+  float *g_w;                  // [Cout][Cin][3][3] (accumulated)
+  uint32_t gy_slice, a_slice, stage_bytes, off_bar, smem_bytes;
+};
+
+constexpr int wg_threads() { return 32 * (4 + 1 + kDgProd); }
+
+// MN-major, no swizzle: the leading byte offset is the K-direction stride between 8-row core
+// matrices, the stride byte offset the MN-direction stride between 8-channel chunks
+// (measured: the opposite assignment fails the dL/dW parity test)
+__device__ __forceinline__ uint64_t mn_desc(const WgParams &p, uint32_t addr, uint32_t mn_stride, uint32_t k_stride) {
+  (void)p;
+  return ptx::smem_desc(addr, k_stride, mn_stride);
+}
+
+__device__ __forceinline__ void wg_producer(const WgParams &p, uint32_t sbase, uint32_t bar_full, uint32_t bar_empty,
+                                            int r, int cta_r, int ptid, uint32_t lane) {
+  uint32_t it = 0;
+  const long long N = (long long)p.B * p.Ho * p.Wo * p.Cout;
+  const int coch = 128 / 8, cich = p.Cin / 8;
+  for (int u = cta_r; u < p.nunits; u += p.ncta_r, ++it) {
+    int k, b, y0, x0;
+    {
+      const int per = p.tiles_x * p.tiles_y, t = u % per, kb = u / per;
+      b = kb % p.B; k = kb / p.B;
+      const int ty = t / p.tiles_x;
+      y0 = ty * kDgTileH; x0 = (t - ty * p.tiles_x) * kDgTileW;
+    }
+    const uint32_t s = it % (uint32_t)p.nstages, ph = (it / (uint32_t)p.nstages) & 1u;
+    ptx::mbar_wait(bar_empty + 8 * s, ph ^ 1u);
+    const uint32_t st = sbase + s * p.stage_bytes;
+    // dL/dY tile (M = 128 rows of co, zero above C_out): [co chunk][128 px][16 B] hi | lo
+    for (int i = ptid; i < 128 * coch; i += 32 * kDgProd) {
+      const int px = i & 127, cc = i >> 7;
+      const int y = y0 + (px >> 3), x = x0 + (px & 7);
+      float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+      if (y < p.Ho && x < p.Wo && cc * 8 < p.Cout) {
+        const float4 *src = reinterpret_cast<const float4 *>(
+            p.g_y + (long long)k * N + (((long long)b * p.Ho + y) * p.Wo + x) * p.Cout + cc * 8);
+        v0 = __ldg(src);
+        v1 = __ldg(src + 1);
+      }
+      uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
+      split2(v0.x, v0.y, h0, l0);
+      split2(v0.z, v0.w, h1, l1);
+      split2(v1.x, v1.y, h2, l2);
+      split2(v1.z, v1.w, h3, l3);
+      const uint32_t dst = st + (uint32_t)(cc * 128 + px) * 16u;
+      ptx::st_shared_v4(dst, h0, h1, h2, h3);
+      ptx::st_shared_v4(dst + p.gy_slice, l0, l1, l2, l3);
+    }
+    // A_k halo of kernel row r: [ci chunk][16 x 10 px][16 B], A = sum_j c_j S_{kK+j}
+    const uint32_t ast = st + 2 * p.gy_slice;
+    for (int i = ptid; i < kWgHaloRows * cich; i += 32 * kDgProd) {
+      const int hp = i % kWgHaloRows, cc = i / kWgHaloRows;
+      const int yi = y0 + hp / kDgHaloW + r - p.pad, xi = x0 + hp % kDgHaloW - p.pad;
+      float a[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a[e] = 0.f;
+      if (yi >= 0 && yi < p.H && xi >= 0 && xi < p.W) {
+        const long long bit = (long long)xi * p.Cin + cc * 8;
+        const uint32_t *wp = p.in + (long long)b * p.in_sb + (long long)yi * p.wpr_in + (bit >> 5);
+        const int sh = (int)(bit & 31);
+        for (int j = 0; j < p.K; ++j) {
+          const uint32_t byte = (__ldg(wp + (long long)(k * p.K + j) * p.in_st) >> sh) & 0xFFu;
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if ((byte >> e) & 1u) a[e] += p.coef[j];
+        }
+      }
+      uint32_t hi[4], lo[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float s0 = a[2 * q] / p.a_scale, s1 = a[2 * q + 1] / p.a_scale;
+        split2(s0, s1, hi[q], lo[q]);
+      }
+      const uint32_t dst = ast + (uint32_t)(cc * kWgHaloRows + hp) * 16u;
+      ptx::st_shared_v4(dst, hi[0], hi[1], hi[2], hi[3]);
+      if (p.split) ptx::st_shared_v4(dst + p.a_slice, lo[0], lo[1], lo[2], lo[3]);
+    }
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive_local(bar_full + 8 * s);
+  }
+}
+
+__global__ void __launch_bounds__(wg_threads(), 1) wgrad_tc_kernel(const __grid_constant__ WgParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t warp = __shfl_sync(0xFFFFFFFFu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31;
+  const uint32_t sbase = ptx::smem_u32(smem);
+  const int r = (int)blockIdx.x % 3, cta_r = (int)blockIdx.x / 3;
+  const uint32_t bar_full = sbase + p.off_bar, bar_empty = bar_full + 8 * kWgAStg, bar_done = bar_empty + 8 * kWgAStg;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + p.off_bar + 8 * (2 * kWgAStg + 1));
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kWgAStg; ++s) {
+      ptx::mbar_init(bar_full + 8 * s, kDgProd);
+      ptx::mbar_init(bar_empty + 8 * s, 1);
+    }
+    ptx::mbar_init(bar_done, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 4) {
+    ptx::tmem_alloc_cg1(ptx::smem_u32(tmem_slot), 512);
+    ptx::tmem_relinquish_cg1();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const bool any = cta_r < p.nunits;
+  if (warp < 4) {
+    // epilogue, once: TMEM lane = co, columns s C_in + ci -> dL/dW[co][ci][r][s] (+ the CTA's share)
+    if (any) {
+      ptx::mbar_wait(bar_done, 0);
+      ptx::tc_fence_after();
+      const int co = (int)(warp * 32 + lane);
+      const uint32_t lane_addr = (warp * 32u) << 16;
+      for (int s = 0; s < 3; ++s)
+        for (int c8 = 0; c8 < p.Cin; c8 += 8) {
+          uint32_t d[8], dz[8];
+          ptx::tmem_ld8(tmem_base + lane_addr + (uint32_t)(s * p.Cin + c8), d);
+          ptx::tmem_wait_ld_dep(d, dz);
+          if (co < p.Cout) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float v = __uint_as_float(d[e]) * p.a_scale;
+              if (v != 0.f) atomicAdd(p.g_w + (((long long)co * p.Cin + c8 + e) * 3 + r) * 3 + s, v);
+            }
+          }
+        }
+    }
+  } else if (warp == 4) {
+    const uint32_t idesc = ptx::idesc_bf16(128u, (uint32_t)p.Cin) | (1u << 15) | (1u << 16);  // A, B MN-major
+    const uint32_t lbo_gy = 128u * 16u, lbo_a = (uint32_t)kWgHaloRows * 16u;
+    uint32_t it = 0;
+    bool first = true;
+    for (int u = cta_r; u < p.nunits; u += p.ncta_r, ++it) {
+      const uint32_t s = it % (uint32_t)p.nstages, ph = (it / (uint32_t)p.nstages) & 1u;
+      ptx::mbar_wait(bar_full + 8 * s, ph);
+      ptx::tc_fence_after();
+      const uint32_t st = sbase + s * p.stage_bytes, ast = st + 2 * p.gy_slice;
+      if (ptx::elect_one()) {
+        for (int tap = 0; tap < 3; ++tap) {
+          const uint32_t d_tmem = tmem_base + (uint32_t)(tap * p.Cin);
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {  // K = 16 pixels = tile rows 2 ks, 2 ks + 1
+            const uint64_t ghi = mn_desc(p, st + ks * 256u, lbo_gy, 128u);
+            const uint64_t glo = mn_desc(p, st + p.gy_slice + ks * 256u, lbo_gy, 128u);
+            const uint32_t aoff = (uint32_t)(2 * ks * kDgHaloW + tap) * 16u;
+            const uint64_t ahi = mn_desc(p, ast + aoff, lbo_a, kDgHaloW * 16u);
+            const uint64_t alo = mn_desc(p, ast + p.a_slice + aoff, lbo_a, kDgHaloW * 16u);
+            ptx::mma_f16_cg1(d_tmem, ghi, ahi, idesc, (first && ks == 0) ? 0u : 1u);
+            ptx::mma_f16_cg1(d_tmem, glo, ahi, idesc, 1u);
+            if (p.split) ptx::mma_f16_cg1(d_tmem, ghi, alo, idesc, 1u);
+          }
+        }
+        ptx::mma_commit_cg1(bar_empty + 8 * s);
+      }
+      __syncwarp();
+      first = false;
+    }
+    if (any && ptx::elect_one()) ptx::mma_commit_cg1(bar_done);
+    __syncwarp();
+  } else {
+    wg_producer(p, sbase, bar_full, bar_empty, r, cta_r, (int)(threadIdx.x - 32 * 5), lane);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_cg1(tmem_base, 512);
+  }
+}
+
+// dL/db[co] = sum over groups, samples and pixels of dL/dY_k (one block per 64 rows x co)
+__global__ void bias_grad_kernel(const float *g_y, long long rows, int Cout, float *g_b) {
+  const int co = threadIdx.x;
+  float acc = 0.f;
+  for (long long rw = blockIdx.x; rw < rows; rw += gridDim.x)
+    if (co < Cout) acc += __ldg(g_y + rw * Cout + co);
+  if (co < Cout && acc != 0.f) atomicAdd(g_b + co, acc);
+}
+
 }  // namespace
 
 bool dgrad_tc_ok(const BwdParams &p) {
@@ -341,4 +545,55 @@ int launch_dgrad_tc(const BwdParams &bp, void *img, void *stream, int *launches)
   return (int)e;
 }
 
+}  // namespace tacsnn
+
+namespace tacsnn {
+bool wgrad_tc_ok(const BwdParams &p) {
+  return p.in && !p.xin && p.R == 3 && p.S == 3 && p.stride == 1 && (p.pad == 0 || p.pad == 1) &&
+         (p.Cin == 32 || p.Cin == 64 || p.Cin == 128) && p.Cout <= 128 && p.Cout % 8 == 0 && p.K <= kMaxK;
+}
+
+int launch_wgrad_tc(const BwdParams &bp, void *stream, int *launches) {
+  cudaStream_t st = (cudaStream_t)stream;
+  WgParams p{};
+  p.G = bp.G; p.B = bp.B; p.H = bp.H; p.W = bp.W; p.Cin = bp.Cin; p.Cout = bp.Cout; p.K = bp.K;
+  p.pad = bp.pad; p.Ho = bp.Ho; p.Wo = bp.Wo; p.wpr_in = bp.wpr_in;
+  p.tiles_x = (bp.Wo + kDgTileW - 1) / kDgTileW;
+  p.tiles_y = (bp.Ho + kDgTileH - 1) / kDgTileH;
+  p.nunits = bp.G * bp.B * p.tiles_x * p.tiles_y;
+  p.in_st = bp.in_st; p.in_sb = bp.in_sb;
+  // A_k = sum_j c_j S: exact in one bf16 when every coefficient is 2^-m (j) with few bits; the
+  // integer form (a_scale = the smallest coefficient) keeps it <= 255
+  double cmin = 1e30;
+  bool pow2 = true;
+  for (int j = 0; j < bp.K; ++j) {
+    p.coef[j] = bp.coef[j];
+    const double c = (double)bp.coef[j];
+    int e;
+    const double m = std::frexp(c, &e);
+    pow2 = pow2 && c > 0.0 && m == 0.5;
+    cmin = std::min(cmin, c);
+  }
+  double amax = 0.0;
+  for (int j = 0; j < bp.K; ++j) amax += (double)bp.coef[j];
+  p.split = !(pow2 && cmin > 0.0 && amax / cmin <= 255.0);
+  p.a_scale = p.split ? 1.f : (float)cmin;
+  p.g_y = bp.g_y; p.in = bp.in; p.g_w = bp.g_w;
+  p.gy_slice = 128u * 128u * 2u;                                  // [16 co chunks][128 px][16 B]
+  p.a_slice = (uint32_t)kWgHaloRows * (uint32_t)bp.Cin * 2u;      // [ci chunks][160 px][16 B]
+  p.stage_bytes = (2 * p.gy_slice + (p.split ? 2u : 1u) * p.a_slice + 1023u) & ~1023u;
+  p.nstages = 2u * p.stage_bytes + 1024u <= 227u * 1024u ? 2 : 1;
+  p.off_bar = p.nstages * p.stage_bytes;
+  p.smem_bytes = p.off_bar + 8 * (2 * kWgAStg + 1) + 16;
+  p.ncta_r = std::max(1, std::min(49, p.nunits));
+  auto kern = wgrad_tc_kernel;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+  if (e != cudaSuccess) return (int)e;
+  kern<<<3 * p.ncta_r, wg_threads(), p.smem_bytes, st>>>(p);
+  ++*launches;
+  const long long rows = (long long)bp.G * bp.B * bp.Ho * bp.Wo;
+  bias_grad_kernel<<<(unsigned)std::min<long long>(rows, 148LL * 8), 128, 0, st>>>(bp.g_y, rows, bp.Cout, bp.g_b);
+  ++*launches;
+  return (int)cudaGetLastError();
+}
 }  // namespace tacsnn
