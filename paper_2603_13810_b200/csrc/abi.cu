@@ -672,6 +672,7 @@ tac_status tac_conv_lif_backward(const tac_conv_lif_desc *desc, const tac_plan *
   p.g_y = static_cast<float *>(ws); p.g_vinit = g_v_init;
   const size_t gy_bytes = align256((size_t)g.G * desc->B * g.Ho * g.Wo * desc->C_out * 4);
   p.dg_img = bwd_dgrad_img_bytes(desc) ? static_cast<unsigned char *>(ws) + gy_bytes : nullptr;
+  p.tc = engine == TAC_ENGINE_TCGEN05 ? 1 : 0;
   p.w = reinterpret_cast<const float *>(base + L.simt_off);
   p.g_w = g_weight; p.g_b = g_bias; p.g_in = g_input; p.g_alpha = g_agg_weights;
   int launches = 0;

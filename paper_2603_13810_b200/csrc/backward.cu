@@ -336,6 +336,61 @@ __global__ void or_pool2_kernel(const uint32_t *in, uint32_t *out, long long TB,
 
 // MaxPool2d backward on binary maps: g_pre[t][b][y][x][c] = g_pooled of its window if
 // (y, x) is the window's first maximal element in row-major order, else 0
+// C % 32 == 0: one thread per (pooled window, 32 channels): the window's four spike words,
+// per channel the first spiking element in row-major order (top-left when none), one
+// 128-B read of the pooled gradient and four 128-B writes
+__global__ void or_pool2_bwd32_kernel(const uint32_t *pre, const float *g_pooled, float *g_pre, long long TB,
+                                      int C, int H, int W) {
+  const int Hq = H / 2, Wq = W / 2, nw = C / 32;
+  const int wpr = W * nw;
+  const long long n = TB * H * Wq * nw;  // (tb, y, xo, word): rows y of the unpooled map
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int wd = (int)(i % nw);
+    long long q = i / nw;
+    const int xo = (int)(q % Wq);
+    q /= Wq;
+    const int y = (int)(q % H);
+    const long long tb = q / H;
+    const int yo = y >> 1, dy = y & 1;
+    float *dst0 = g_pre + (((tb * H + y) * W + 2 * xo) * C) + wd * 32;
+    float4 *d0 = reinterpret_cast<float4 *>(dst0), *d1 = reinterpret_cast<float4 *>(dst0 + C);
+    if (yo >= Hq) {  // floor mode: the dropped row gets no gradient
+#pragma unroll
+      for (int v = 0; v < 8; ++v) d0[v] = d1[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (2 * xo + 2 == W - 1 && (W & 1)) {  // the dropped last column
+        float4 *d2 = reinterpret_cast<float4 *>(dst0 + 2 * C);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) d2[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      continue;
+    }
+    const uint32_t *r0 = pre + (tb * H + 2 * yo) * wpr + wd, *r1 = r0 + wpr;
+    const uint32_t w00 = r0[(2 * xo) * nw], w01 = r0[(2 * xo + 1) * nw];
+    const uint32_t w10 = r1[(2 * xo) * nw], w11 = r1[(2 * xo + 1) * nw];
+    // masks of the element each channel's gradient goes to (e = 2 dy + dx)
+    const uint32_t m00 = w00 | ~(w00 | w01 | w10 | w11);
+    const uint32_t m01 = w01 & ~w00;
+    const uint32_t m10 = w10 & ~(w00 | w01);
+    const uint32_t m11 = w11 & ~(w00 | w01 | w10);
+    const uint32_t ma = dy ? m10 : m00, mb = dy ? m11 : m01;
+    const float4 *src = reinterpret_cast<const float4 *>(g_pooled + ((tb * Hq + yo) * Wq + xo) * C + wd * 32);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const float4 g = __ldg(src + v);
+      const int b0 = 4 * v;
+      d0[v] = make_float4(((ma >> b0) & 1u) ? g.x : 0.f, ((ma >> (b0 + 1)) & 1u) ? g.y : 0.f,
+                          ((ma >> (b0 + 2)) & 1u) ? g.z : 0.f, ((ma >> (b0 + 3)) & 1u) ? g.w : 0.f);
+      d1[v] = make_float4(((mb >> b0) & 1u) ? g.x : 0.f, ((mb >> (b0 + 1)) & 1u) ? g.y : 0.f,
+                          ((mb >> (b0 + 2)) & 1u) ? g.z : 0.f, ((mb >> (b0 + 3)) & 1u) ? g.w : 0.f);
+    }
+    if (2 * xo + 2 == W - 1 && (W & 1)) {  // floor mode: the dropped last column
+      float4 *d2 = reinterpret_cast<float4 *>(dst0 + 2 * C);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) d2[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+}
+
 __global__ void or_pool2_bwd_kernel(const uint32_t *pre, const float *g_pooled, float *g_pre, long long TB,
                                     int C, int H, int W) {
   const int Hq = H / 2, Wq = W / 2;
@@ -384,7 +439,7 @@ int launch_backward(const BwdParams &p, void *stream, int *launches) {
     ++*launches;
   }
   static const bool no_wgtc = [] { const char *e = std::getenv("TACSNN_NO_WGRAD_TC"); return e && *e == '1'; }();
-  if (p.dg_img && !no_wgtc && wgrad_tc_ok(p)) {
+  if (p.tc && !no_wgtc && wgrad_tc_ok(p)) {
     const int e = launch_wgrad_tc(p, stream, launches);
     if (e) return e;
     --*launches;  // counted below with the SIMT variants
@@ -422,8 +477,12 @@ int launch_or_pool2(const uint32_t *in, uint32_t *out, int T, int B, int C, int 
 int launch_or_pool2_backward(const uint32_t *pre, const float *g_pooled, float *g_pre, int T, int B, int C,
                              int H, int W, void *stream) {
   const long long TB = (long long)T * B;
-  or_pool2_bwd_kernel<<<grid1(TB * H * W * C, 256), 256, 0, (cudaStream_t)stream>>>(pre, g_pooled, g_pre, TB,
-                                                                                    C, H, W);
+  if (C % 32 == 0 && (reinterpret_cast<uintptr_t>(g_pre) | reinterpret_cast<uintptr_t>(g_pooled)) % 16 == 0)
+    or_pool2_bwd32_kernel<<<grid1(TB * H * (W / 2) * (C / 32), 256), 256, 0, (cudaStream_t)stream>>>(
+        pre, g_pooled, g_pre, TB, C, H, W);
+  else
+    or_pool2_bwd_kernel<<<grid1(TB * H * W * C, 256), 256, 0, (cudaStream_t)stream>>>(pre, g_pooled, g_pre, TB,
+                                                                                      C, H, W);
   return (int)cudaGetLastError();
 }
 

@@ -314,6 +314,7 @@ constexpr int kWgHaloRows = kDgTileH * kDgHaloW;  // 16 x 10 halo pixels of one 
 
 struct WgParams {
   int G, B, H, W, Cin, Cout, K, pad, Ho, Wo, wpr_in;
+  int Np;                      // MMA N: C_in padded to a multiple of 16 (>= 16; first layers C_in <= 8)
   int tiles_x, tiles_y, nunits, split, nstages, ncta_r;
   long long in_st, in_sb;
   float coef[kMaxK];
@@ -338,7 +339,7 @@ __device__ __forceinline__ void wg_producer(const WgParams &p, uint32_t sbase, u
                                             int r, int cta_r, int ptid, uint32_t lane) {
   uint32_t it = 0;
   const long long N = (long long)p.B * p.Ho * p.Wo * p.Cout;
-  const int coch = 128 / 8, cich = p.Cin / 8;
+  const int coch = 128 / 8, cich = p.Np / 8;
   for (int u = cta_r; u < p.nunits; u += p.ncta_r, ++it) {
     int k, b, y0, x0;
     {
@@ -378,12 +379,16 @@ __device__ __forceinline__ void wg_producer(const WgParams &p, uint32_t sbase, u
       float a[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) a[e] = 0.f;
-      if (yi >= 0 && yi < p.H && xi >= 0 && xi < p.W) {
+      const int nval = min(8, p.Cin - cc * 8);  // channels of this 8-chunk below C_in
+      if (nval > 0 && yi >= 0 && yi < p.H && xi >= 0 && xi < p.W) {
         const long long bit = (long long)xi * p.Cin + cc * 8;
         const uint32_t *wp = p.in + (long long)b * p.in_sb + (long long)yi * p.wpr_in + (bit >> 5);
         const int sh = (int)(bit & 31);
+        const uint32_t cmask = (1u << nval) - 1u;
         for (int j = 0; j < p.K; ++j) {
-          const uint32_t byte = (__ldg(wp + (long long)(k * p.K + j) * p.in_st) >> sh) & 0xFFu;
+          const uint64_t two = (uint64_t)__ldg(wp + (long long)(k * p.K + j) * p.in_st) |
+                               (sh + nval > 32 ? (uint64_t)__ldg(wp + (long long)(k * p.K + j) * p.in_st + 1) << 32 : 0ull);
+          const uint32_t byte = (uint32_t)(two >> sh) & cmask;
 #pragma unroll
           for (int e = 0; e < 8; ++e)
             if ((byte >> e) & 1u) a[e] += p.coef[j];
@@ -437,21 +442,21 @@ __global__ void __launch_bounds__(wg_threads(), 1) wgrad_tc_kernel(const __grid_
       const int co = (int)(warp * 32 + lane);
       const uint32_t lane_addr = (warp * 32u) << 16;
       for (int s = 0; s < 3; ++s)
-        for (int c8 = 0; c8 < p.Cin; c8 += 8) {
+        for (int c8 = 0; c8 < p.Np; c8 += 8) {
           uint32_t d[8], dz[8];
-          ptx::tmem_ld8(tmem_base + lane_addr + (uint32_t)(s * p.Cin + c8), d);
+          ptx::tmem_ld8(tmem_base + lane_addr + (uint32_t)(s * p.Np + c8), d);
           ptx::tmem_wait_ld_dep(d, dz);
           if (co < p.Cout) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               const float v = __uint_as_float(d[e]) * p.a_scale;
-              if (v != 0.f) atomicAdd(p.g_w + (((long long)co * p.Cin + c8 + e) * 3 + r) * 3 + s, v);
+              if (v != 0.f && c8 + e < p.Cin) atomicAdd(p.g_w + (((long long)co * p.Cin + c8 + e) * 3 + r) * 3 + s, v);
             }
           }
         }
     }
   } else if (warp == 4) {
-    const uint32_t idesc = ptx::idesc_bf16(128u, (uint32_t)p.Cin) | (1u << 15) | (1u << 16);  // A, B MN-major
+    const uint32_t idesc = ptx::idesc_bf16(128u, (uint32_t)p.Np) | (1u << 15) | (1u << 16);  // A, B MN-major
     const uint32_t lbo_gy = 128u * 16u, lbo_a = (uint32_t)kWgHaloRows * 16u;
     uint32_t it = 0;
     bool first = true;
@@ -462,7 +467,7 @@ __global__ void __launch_bounds__(wg_threads(), 1) wgrad_tc_kernel(const __grid_
       const uint32_t st = sbase + s * p.stage_bytes, ast = st + 2 * p.gy_slice;
       if (ptx::elect_one()) {
         for (int tap = 0; tap < 3; ++tap) {
-          const uint32_t d_tmem = tmem_base + (uint32_t)(tap * p.Cin);
+          const uint32_t d_tmem = tmem_base + (uint32_t)(tap * p.Np);
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks) {  // K = 16 pixels = tile rows 2 ks, 2 ks + 1
             const uint64_t ghi = mn_desc(p, st + ks * 256u, lbo_gy, 128u);
@@ -550,7 +555,8 @@ int launch_dgrad_tc(const BwdParams &bp, void *img, void *stream, int *launches)
 namespace tacsnn {
 bool wgrad_tc_ok(const BwdParams &p) {
   return p.in && !p.xin && p.R == 3 && p.S == 3 && p.stride == 1 && (p.pad == 0 || p.pad == 1) &&
-         (p.Cin == 32 || p.Cin == 64 || p.Cin == 128) && p.Cout <= 128 && p.Cout % 8 == 0 && p.K <= kMaxK;
+         (p.Cin <= 8 || (p.Cin % 16 == 0 && p.Cin <= 128)) && p.Cout >= 64 && p.Cout <= 128 && p.Cout % 8 == 0 &&
+         p.K <= kMaxK;  // M = 128 output channels: narrower layers waste most of the tile (SIMT wins)
 }
 
 int launch_wgrad_tc(const BwdParams &bp, void *stream, int *launches) {
@@ -558,6 +564,7 @@ int launch_wgrad_tc(const BwdParams &bp, void *stream, int *launches) {
   WgParams p{};
   p.G = bp.G; p.B = bp.B; p.H = bp.H; p.W = bp.W; p.Cin = bp.Cin; p.Cout = bp.Cout; p.K = bp.K;
   p.pad = bp.pad; p.Ho = bp.Ho; p.Wo = bp.Wo; p.wpr_in = bp.wpr_in;
+  p.Np = std::max(16, (bp.Cin + 15) / 16 * 16);
   p.tiles_x = (bp.Wo + kDgTileW - 1) / kDgTileW;
   p.tiles_y = (bp.Ho + kDgTileH - 1) / kDgTileH;
   p.nunits = bp.G * bp.B * p.tiles_x * p.tiles_y;
@@ -580,7 +587,7 @@ int launch_wgrad_tc(const BwdParams &bp, void *stream, int *launches) {
   p.a_scale = p.split ? 1.f : (float)cmin;
   p.g_y = bp.g_y; p.in = bp.in; p.g_w = bp.g_w;
   p.gy_slice = 128u * 128u * 2u;                                  // [16 co chunks][128 px][16 B]
-  p.a_slice = (uint32_t)kWgHaloRows * (uint32_t)bp.Cin * 2u;      // [ci chunks][160 px][16 B]
+  p.a_slice = (uint32_t)kWgHaloRows * (uint32_t)p.Np * 2u;       // [ci chunks][160 px][16 B]
   p.stage_bytes = (2 * p.gy_slice + (p.split ? 2u : 1u) * p.a_slice + 1023u) & ~1023u;
   p.nstages = 2u * p.stage_bytes + 1024u <= 227u * 1024u ? 2 : 1;
   p.off_bar = p.nstages * p.stage_bytes;

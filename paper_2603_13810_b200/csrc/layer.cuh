@@ -78,6 +78,7 @@ struct BwdParams {
   float *g_in;          // [T][B][H][W][Cin] or NULL
   float *g_alpha;       // [K] or NULL
   void *dg_img;         // workspace for the tcgen05 input-gradient weights (bwd_tc.cu), or NULL
+  int tc;               // the layer's forward ran on tcgen05 (the tcgen05 backward kernels apply)
 };
 int launch_backward(const BwdParams &p, void *stream, int *launches);
 // tcgen05 input gradient (bwd_tc.cu): eligibility, its weight-image bytes, launch

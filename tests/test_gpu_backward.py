@@ -139,7 +139,7 @@ def test_backward_agg_weights_and_real_input(T, O, engine):
     _close(r["g_agg_weights"].cpu().numpy(), ref["g_alpha"], "g_alpha", tol)
 
 
-@pytest.mark.parametrize("C,H,W", [(32, 26, 26), (128, 16, 16), (3, 11, 13)])
+@pytest.mark.parametrize("C,H,W", [(32, 26, 26), (128, 16, 16), (3, 11, 13), (32, 11, 13), (64, 7, 6)])
 def test_or_pool2_and_backward(T, O, C, H, W):
     g = torch.Generator().manual_seed(C + H)
     S = (torch.rand((3, 2, C, H, W), generator=g) < 0.3).to(torch.uint8)
