@@ -599,6 +599,15 @@ tac_status tac_conv_lif_forward_train(const tac_conv_lif_desc *desc, const tac_p
 
 // the tcgen05 input gradient's weight image (bwd_tc.cu) follows dL/dY in the backward
 // workspace for the shapes it takes (a layer whose forward runs on tcgen05)
+// ... and the weight gradient's bf16 A_k buffer (tcgen05 layers with C_out >= 64)
+size_t bwd_wgrad_abuf_bytes(const tac_conv_lif_desc *d, const Geo &g) {
+  const bool ok = resolve_engine(d) == TAC_ENGINE_TCGEN05 && d->R == 3 && d->S == 3 && d->stride == 1 &&
+                  (d->pad == 0 || d->pad == 1) && d->input_kind == TAC_INPUT_SPIKES &&
+                  (d->C_in <= 8 || (d->C_in % 16 == 0 && d->C_in <= 128)) && d->C_out >= 64 && d->C_out <= 128 &&
+                  d->C_out % 8 == 0;
+  return ok ? align256(tacsnn::wgrad_tc_ws_bytes(g.G, d->B, d->H, d->W, d->C_in)) : 0;
+}
+
 size_t bwd_dgrad_img_bytes(const tac_conv_lif_desc *d) {
   const bool ok = resolve_engine(d) == TAC_ENGINE_TCGEN05 && d->R == 3 && d->S == 3 && d->stride == 1 &&
                   (d->pad == 0 || d->pad == 1) && (d->C_in == 32 || d->C_in == 64 || d->C_in == 128) &&
@@ -612,7 +621,8 @@ tac_status tac_backward_workspace_bytes(const tac_conv_lif_desc *desc, size_t *b
   tac_status st = check(desc, &g);
   if (st != TAC_OK) return st;
   if (!bytes) return fail(TAC_ERR_NULL, "bytes is NULL");
-  *bytes = align256((size_t)g.G * desc->B * g.Ho * g.Wo * desc->C_out * 4) + bwd_dgrad_img_bytes(desc);
+  *bytes = align256((size_t)g.G * desc->B * g.Ho * g.Wo * desc->C_out * 4) + bwd_dgrad_img_bytes(desc) +
+           bwd_wgrad_abuf_bytes(desc, g);
   return TAC_OK;
 }
 
@@ -673,6 +683,8 @@ tac_status tac_conv_lif_backward(const tac_conv_lif_desc *desc, const tac_plan *
   const size_t gy_bytes = align256((size_t)g.G * desc->B * g.Ho * g.Wo * desc->C_out * 4);
   p.dg_img = bwd_dgrad_img_bytes(desc) ? static_cast<unsigned char *>(ws) + gy_bytes : nullptr;
   p.tc = engine == TAC_ENGINE_TCGEN05 ? 1 : 0;
+  p.wg_abuf = bwd_wgrad_abuf_bytes(desc, g) ? static_cast<unsigned char *>(ws) + gy_bytes + bwd_dgrad_img_bytes(desc)
+                                            : nullptr;
   p.w = reinterpret_cast<const float *>(base + L.simt_off);
   p.g_w = g_weight; p.g_b = g_bias; p.g_in = g_input; p.g_alpha = g_agg_weights;
   int launches = 0;

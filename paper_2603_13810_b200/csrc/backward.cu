@@ -439,7 +439,7 @@ int launch_backward(const BwdParams &p, void *stream, int *launches) {
     ++*launches;
   }
   static const bool no_wgtc = [] { const char *e = std::getenv("TACSNN_NO_WGRAD_TC"); return e && *e == '1'; }();
-  if (p.tc && !no_wgtc && wgrad_tc_ok(p)) {
+  if (p.tc && p.wg_abuf && !no_wgtc && wgrad_tc_ok(p)) {
     const int e = launch_wgrad_tc(p, stream, launches);
     if (e) return e;
     --*launches;  // counted below with the SIMT variants

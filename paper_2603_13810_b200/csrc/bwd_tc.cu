@@ -14,6 +14,8 @@
 // channels), 1 MMA warp, 1 weight loader warp (bulk copies of the per-(chunk, tap) bf16
 // weight blocks, prepared on the device by dg_weights_kernel), 4 producer warps (the dL/dY
 // halo of one 32-channel chunk, fp32 -> bf16 hi / lo).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -313,6 +315,7 @@ constexpr int kWgAStg = 2;
 constexpr int kWgHaloRows = kDgTileH * kDgHaloW;  // 16 x 10 halo pixels of one kernel row
 
 struct WgParams {
+  CUtensorMap amap[2];         // 5-D views {8 ch, W, H, Cp / 8 chunks, G B} of the bf16 A_k buffer (hi, lo)
   int G, B, H, W, Cin, Cout, K, pad, Ho, Wo, wpr_in;
   int Np;                      // MMA N: C_in padded to a multiple of 16 (>= 16; first layers C_in <= 8)
   int tiles_x, tiles_y, nunits, split, nstages, ncta_r;
@@ -371,38 +374,14 @@ __device__ __forceinline__ void wg_producer(const WgParams &p, uint32_t sbase, u
       ptx::st_shared_v4(dst, h0, h1, h2, h3);
       ptx::st_shared_v4(dst + p.gy_slice, l0, l1, l2, l3);
     }
-    // A_k halo of kernel row r: [ci chunk][16 x 10 px][16 B], A = sum_j c_j S_{kK+j}
-    const uint32_t ast = st + 2 * p.gy_slice;
-    for (int i = ptid; i < kWgHaloRows * cich; i += 32 * kDgProd) {
-      const int hp = i % kWgHaloRows, cc = i / kWgHaloRows;
-      const int yi = y0 + hp / kDgHaloW + r - p.pad, xi = x0 + hp % kDgHaloW - p.pad;
-      float a[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) a[e] = 0.f;
-      const int nval = min(8, p.Cin - cc * 8);  // channels of this 8-chunk below C_in
-      if (nval > 0 && yi >= 0 && yi < p.H && xi >= 0 && xi < p.W) {
-        const long long bit = (long long)xi * p.Cin + cc * 8;
-        const uint32_t *wp = p.in + (long long)b * p.in_sb + (long long)yi * p.wpr_in + (bit >> 5);
-        const int sh = (int)(bit & 31);
-        const uint32_t cmask = (1u << nval) - 1u;
-        for (int j = 0; j < p.K; ++j) {
-          const uint64_t two = (uint64_t)__ldg(wp + (long long)(k * p.K + j) * p.in_st) |
-                               (sh + nval > 32 ? (uint64_t)__ldg(wp + (long long)(k * p.K + j) * p.in_st + 1) << 32 : 0ull);
-          const uint32_t byte = (uint32_t)(two >> sh) & cmask;
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            if ((byte >> e) & 1u) a[e] += p.coef[j];
-        }
-      }
-      uint32_t hi[4], lo[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float s0 = a[2 * q] / p.a_scale, s1 = a[2 * q + 1] / p.a_scale;
-        split2(s0, s1, hi[q], lo[q]);
-      }
-      const uint32_t dst = ast + (uint32_t)(cc * kWgHaloRows + hp) * 16u;
-      ptx::st_shared_v4(dst, hi[0], hi[1], hi[2], hi[3]);
-      if (p.split) ptx::st_shared_v4(dst + p.a_slice, lo[0], lo[1], lo[2], lo[3]);
+    // A_k halo of kernel row r (the pre-pass's bf16 buffer): one 5-D TMA box per slice lands
+    // as [ci chunk][16 x 10 px][16 B]; out-of-bounds pixels / chunks are the zero padding
+    if (ptid == 0) {
+      const uint32_t ast = st + 2 * p.gy_slice;
+      ptx::mbar_arrive_expect_tx(bar_full + 8 * s, (p.split ? 2u : 1u) * p.a_slice);
+      for (int sl = 0; sl < (p.split ? 2 : 1); ++sl)
+        ptx::tma_load_5d(ast + sl * p.a_slice, &p.amap[sl], 0, x0 - p.pad, y0 + r - p.pad, 0, k * p.B + b,
+                         bar_full + 8 * s);
     }
     ptx::fence_proxy_async_smem();
     __syncwarp();
@@ -419,7 +398,7 @@ __global__ void __launch_bounds__(wg_threads(), 1) wgrad_tc_kernel(const __grid_
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + p.off_bar + 8 * (2 * kWgAStg + 1));
   if (threadIdx.x == 0) {
     for (int s = 0; s < kWgAStg; ++s) {
-      ptx::mbar_init(bar_full + 8 * s, kDgProd);
+      ptx::mbar_init(bar_full + 8 * s, kDgProd + 1);  // producer warps + the A box's expect_tx
       ptx::mbar_init(bar_empty + 8 * s, 1);
     }
     ptx::mbar_init(bar_done, 1);
@@ -498,6 +477,51 @@ __global__ void __launch_bounds__(wg_threads(), 1) wgrad_tc_kernel(const __grid_
   }
 }
 
+// pre-pass of the weight gradient: A_k[k][b][y][x][c] = sum_j c_j S_{kK+j} as bf16 (exact
+// integer form / a_scale, or hi + lo), channels padded to Cp (multiple of 8); one thread per
+// (k, b, y, x, 8-channel chunk)
+__global__ void agg_bf16_kernel(const uint32_t *in, long long in_st, long long in_sb, int wpr_in, int G, int B,
+                                int H, int W, int Cin, int Cp, int K, const float *coef_unused, WgParams wp,
+                                __nv_bfloat16 *out_hi, __nv_bfloat16 *out_lo) {
+  (void)coef_unused;
+  const int nch = Cp / 8;
+  const long long n = (long long)G * B * H * W * nch;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int cc = (int)(i % nch);
+    long long q = i / nch;
+    const int x = (int)(q % W);
+    q /= W;
+    const int y = (int)(q % H);
+    q /= H;
+    const int b = (int)(q % B);
+    const int k = (int)(q / B);
+    float a[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) a[e] = 0.f;
+    const int nval = min(8, Cin - cc * 8);
+    if (nval > 0) {
+      const long long bit = (long long)x * Cin + cc * 8;
+      const uint32_t *wp2 = in + (long long)b * in_sb + (long long)y * wpr_in + (bit >> 5);
+      const int sh = (int)(bit & 31);
+      const uint32_t cmask = (1u << nval) - 1u;
+      for (int j = 0; j < K; ++j) {
+        const uint64_t two = (uint64_t)__ldg(wp2 + (long long)(k * K + j) * in_st) |
+                             (sh + nval > 32 ? (uint64_t)__ldg(wp2 + (long long)(k * K + j) * in_st + 1) << 32 : 0ull);
+        const uint32_t byte = (uint32_t)(two >> sh) & cmask;
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if ((byte >> e) & 1u) a[e] += wp.coef[j];
+      }
+    }
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) split2(a[2 * qq] / wp.a_scale, a[2 * qq + 1] / wp.a_scale, hi[qq], lo[qq]);
+    const long long o = i * 8;
+    *reinterpret_cast<uint4 *>(out_hi + o) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    if (out_lo) *reinterpret_cast<uint4 *>(out_lo + o) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  }
+}
+
 // dL/db[co] = sum over groups, samples and pixels of dL/dY_k (one block per 64 rows x co)
 __global__ void bias_grad_kernel(const float *g_y, long long rows, int Cout, float *g_b) {
   const int co = threadIdx.x;
@@ -553,6 +577,26 @@ int launch_dgrad_tc(const BwdParams &bp, void *img, void *stream, int *launches)
 }  // namespace tacsnn
 
 namespace tacsnn {
+static PFN_cuTensorMapEncodeTiled_v12000 wg_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+// bytes of the bf16 A_k buffer (two slices, the worst case) the weight gradient stages through
+size_t wgrad_tc_ws_bytes(int G, int B, int H, int W, int Cin) {
+  const long long Cp = (Cin + 7) / 8 * 8;
+  return (size_t)2 * G * B * H * W * Cp * 2;
+}
+
 bool wgrad_tc_ok(const BwdParams &p) {
   return p.in && !p.xin && p.R == 3 && p.S == 3 && p.stride == 1 && (p.pad == 0 || p.pad == 1) &&
          (p.Cin <= 8 || (p.Cin % 16 == 0 && p.Cin <= 128)) && p.Cout >= 64 && p.Cout <= 128 && p.Cout % 8 == 0 &&
@@ -586,6 +630,28 @@ int launch_wgrad_tc(const BwdParams &bp, void *stream, int *launches) {
   p.split = !(pow2 && cmin > 0.0 && amax / cmin <= 255.0);
   p.a_scale = p.split ? 1.f : (float)cmin;
   p.g_y = bp.g_y; p.in = bp.in; p.g_w = bp.g_w;
+  // pre-pass: A_k as bf16 [k][b][y][x][Cp] (hi; lo after it when split), TMA-loaded per unit
+  const int Cp = (bp.Cin + 7) / 8 * 8;
+  const long long nA = (long long)bp.G * bp.B * bp.H * bp.W * Cp;
+  __nv_bfloat16 *a_hi = static_cast<__nv_bfloat16 *>(bp.wg_abuf), *a_lo = p.split ? a_hi + nA : nullptr;
+  {
+    const long long items = nA / 8;
+    agg_bf16_kernel<<<(unsigned)std::min<long long>((items + 255) / 256, 148LL * 32), 256, 0, st>>>(
+        bp.in, bp.in_st, bp.in_sb, bp.wpr_in, bp.G, bp.B, bp.H, bp.W, bp.Cin, Cp, bp.K, nullptr, p, a_hi, a_lo);
+    ++*launches;
+  }
+  PFN_cuTensorMapEncodeTiled_v12000 enc = wg_encoder();
+  if (!enc) return (int)cudaErrorNotSupported;
+  for (int sl = 0; sl < (p.split ? 2 : 1); ++sl) {
+    const cuuint64_t dims[5] = {8, (cuuint64_t)bp.W, (cuuint64_t)bp.H, (cuuint64_t)(Cp / 8), (cuuint64_t)bp.G * bp.B};
+    const cuuint64_t strides[4] = {(cuuint64_t)Cp * 2, (cuuint64_t)bp.W * Cp * 2, 16, (cuuint64_t)bp.H * bp.W * Cp * 2};
+    const cuuint32_t box[5] = {8, (cuuint32_t)kDgHaloW, (cuuint32_t)kDgTileH, (cuuint32_t)(p.Np / 8), 1};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    const CUresult r = enc(&p.amap[sl], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, (void *)(sl ? a_lo : a_hi), dims, strides,
+                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return (int)cudaErrorInvalidValue;
+  }
   p.gy_slice = 128u * 128u * 2u;                                  // [16 co chunks][128 px][16 B]
   p.a_slice = (uint32_t)kWgHaloRows * (uint32_t)p.Np * 2u;       // [ci chunks][160 px][16 B]
   p.stage_bytes = (2 * p.gy_slice + (p.split ? 2u : 1u) * p.a_slice + 1023u) & ~1023u;

@@ -79,6 +79,7 @@ struct BwdParams {
   float *g_alpha;       // [K] or NULL
   void *dg_img;         // workspace for the tcgen05 input-gradient weights (bwd_tc.cu), or NULL
   int tc;               // the layer's forward ran on tcgen05 (the tcgen05 backward kernels apply)
+  void *wg_abuf;        // workspace for the weight gradient's bf16 A_k buffer, or NULL
 };
 int launch_backward(const BwdParams &p, void *stream, int *launches);
 // tcgen05 input gradient (bwd_tc.cu): eligibility, its weight-image bytes, launch
@@ -87,6 +88,7 @@ size_t dgrad_tc_ws_bytes(int Cin, int Cout);
 int launch_dgrad_tc(const BwdParams &p, void *img, void *stream, int *launches);
 // tcgen05 weight gradient (bwd_tc.cu)
 bool wgrad_tc_ok(const BwdParams &p);
+size_t wgrad_tc_ws_bytes(int G, int B, int H, int W, int Cin);
 int launch_wgrad_tc(const BwdParams &p, void *stream, int *launches);
 int launch_or_pool2(const uint32_t *in, uint32_t *out, int T, int B, int C, int H, int W, void *stream);
 int launch_or_pool2_backward(const uint32_t *pre, const float *g_pooled, float *g_pre, int T, int B,
