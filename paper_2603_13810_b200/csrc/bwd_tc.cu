@@ -525,10 +525,17 @@ __global__ void agg_bf16_kernel(const uint32_t *in, long long in_st, long long i
 // dL/db[co] = sum over groups, samples and pixels of dL/dY_k (one block per 64 rows x co)
 __global__ void bias_grad_kernel(const float *g_y, long long rows, int Cout, float *g_b) {
   const int co = threadIdx.x;
-  float acc = 0.f;
-  for (long long rw = blockIdx.x; rw < rows; rw += gridDim.x)
-    if (co < Cout) acc += __ldg(g_y + rw * Cout + co);
-  if (co < Cout && acc != 0.f) atomicAdd(g_b + co, acc);
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};  // four independent chains: four loads in flight per thread
+  const long long step = gridDim.x;
+  long long rw = blockIdx.x;
+  if (co < Cout) {
+    for (; rw + 3 * step < rows; rw += 4 * step)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] += __ldg(g_y + (rw + u * step) * Cout + co);
+    for (; rw < rows; rw += step) acc[0] += __ldg(g_y + rw * Cout + co);
+  }
+  const float a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  if (co < Cout && a != 0.f) atomicAdd(g_b + co, a);
 }
 
 }  // namespace
