@@ -608,6 +608,12 @@ size_t bwd_wgrad_abuf_bytes(const tac_conv_lif_desc *d, const Geo &g) {
   return ok ? align256(tacsnn::wgrad_tc_ws_bytes(g.G, d->B, d->H, d->W, d->C_in)) : 0;
 }
 
+// ... and, for a fully connected layer, the aggregated input and its gradient (GEMM path)
+size_t bwd_fc_bytes(const tac_conv_lif_desc *d, const Geo &g) {
+  const bool fc = d->H == 1 && d->W == 1 && d->R == 1 && d->S == 1 && d->pad == 0 && d->stride == 1;
+  return fc ? 2 * align256((size_t)g.G * d->B * d->C_in * 4) : 0;
+}
+
 size_t bwd_dgrad_img_bytes(const tac_conv_lif_desc *d) {
   const bool ok = resolve_engine(d) == TAC_ENGINE_TCGEN05 && d->R == 3 && d->S == 3 && d->stride == 1 &&
                   (d->pad == 0 || d->pad == 1) && (d->C_in == 32 || d->C_in == 64 || d->C_in == 128) &&
@@ -622,7 +628,7 @@ tac_status tac_backward_workspace_bytes(const tac_conv_lif_desc *desc, size_t *b
   if (st != TAC_OK) return st;
   if (!bytes) return fail(TAC_ERR_NULL, "bytes is NULL");
   *bytes = align256((size_t)g.G * desc->B * g.Ho * g.Wo * desc->C_out * 4) + bwd_dgrad_img_bytes(desc) +
-           bwd_wgrad_abuf_bytes(desc, g);
+           bwd_wgrad_abuf_bytes(desc, g) + bwd_fc_bytes(desc, g);
   return TAC_OK;
 }
 
@@ -685,6 +691,9 @@ tac_status tac_conv_lif_backward(const tac_conv_lif_desc *desc, const tac_plan *
   p.tc = engine == TAC_ENGINE_TCGEN05 ? 1 : 0;
   p.wg_abuf = bwd_wgrad_abuf_bytes(desc, g) ? static_cast<unsigned char *>(ws) + gy_bytes + bwd_dgrad_img_bytes(desc)
                                             : nullptr;
+  p.fc_ws = bwd_fc_bytes(desc, g) ? static_cast<unsigned char *>(ws) + gy_bytes + bwd_dgrad_img_bytes(desc) +
+                                        bwd_wgrad_abuf_bytes(desc, g)
+                                  : nullptr;
   p.w = reinterpret_cast<const float *>(base + L.simt_off);
   p.g_w = g_weight; p.g_b = g_bias; p.g_in = g_input; p.g_alpha = g_agg_weights;
   int launches = 0;

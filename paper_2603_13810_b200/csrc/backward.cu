@@ -302,6 +302,104 @@ __global__ void wgrad_direct_kernel(const BwdParams p) {
   p.g_w[i] += acc;
 }
 
+// ---- fully connected layers (H = W = R = S = 1): the backward conv is two plain GEMMs
+// over the flattened (group, sample) rows; a shared-memory tiled fp32 GEMM
+//   C[m][n] (=) sum_k A(m, k) B(k, n),  A(m, k) = A[m sam + k sak],  B(k, n) = B[k sbk + n sbn]
+// (64 x 64 tile, 16-deep K slices, 4 x 4 outputs per thread).
+constexpr int kGmT = 64, kGmK = 16;
+__global__ void __launch_bounds__(256) gemm_f32_kernel(int M, int N, int K, const float *A, long long sam,
+                                                       long long sak, const float *Bm, long long sbk, long long sbn,
+                                                       float *C, long long ldc) {
+  __shared__ float sA[kGmK][kGmT + 1], sB[kGmK][kGmT + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int m0 = blockIdx.y * kGmT, n0 = blockIdx.x * kGmT;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += kGmK) {
+    for (int i = threadIdx.x; i < kGmK * kGmT; i += 256) {
+      // consecutive threads walk the unit-stride index of each operand (coalesced loads)
+      const int kk = sam == 1 ? i / kGmT : i % kGmK, mm = sam == 1 ? i % kGmT : i / kGmK;
+      const int m = m0 + mm, k = k0 + kk;
+      sA[kk][mm] = (m < M && k < K) ? __ldg(A + m * sam + k * sak) : 0.f;
+      const int nn = sbn == 1 ? i % kGmT : i / kGmK, kb = sbn == 1 ? i / kGmT : i % kGmK;
+      const int n = n0 + nn, k2 = k0 + kb;
+      sB[kb][nn] = (n < N && k2 < K) ? __ldg(Bm + k2 * sbk + n * sbn) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kGmK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = sA[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = sB[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
+      if (m < M && n < N) C[m * ldc + n] = acc[i][j];
+    }
+}
+
+// A_k[kb][c] (fp32) of a fully connected layer's flattened input
+__global__ void fc_agg_kernel(const BwdParams p, float *out) {
+  const long long n = (long long)p.G * p.B * p.Cin;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % p.Cin);
+    const long long kb = i / p.Cin;
+    out[i] = agg_at(p, (int)(kb / p.B), (int)(kb % p.B), 0, 0, c);
+  }
+}
+
+// dL/dS_{kK+j}[b][c] = a_j dA[kb][c]; dL/da_j partial sums (one block-wide reduction per j)
+__global__ void fc_gin_kernel(const BwdParams p, const float *dA) {
+  __shared__ float red[kMaxK][8];
+  const long long n = (long long)p.G * p.B * p.Cin;
+  float acc[kMaxK];
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j) acc[j] = 0.f;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % p.Cin);
+    const long long kb = i / p.Cin;
+    const int k = (int)(kb / p.B), b = (int)(kb % p.B);
+    const float g = dA[i];
+    for (int j = 0; j < p.K; ++j) {
+      const int t = k * p.K + j;
+      if (p.g_in) p.g_in[((long long)t * p.B + b) * p.Cin + c] = p.coef[j] * g;
+      if (p.g_alpha) acc[j] = fmaf(g, frame_at(p, t, b, 0, 0, c), acc[j]);
+    }
+  }
+  if (p.g_alpha) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    for (int j = 0; j < p.K; ++j) {
+      float v = acc[j];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+      if (l == 0) red[j][w] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < p.K) {
+      float v = 0.f;
+      for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) v += red[threadIdx.x][w2];
+      if (v != 0.f) atomicAdd(p.g_alpha + threadIdx.x, v);
+    }
+  }
+}
+
+__global__ void bias_grad_fc_kernel(const float *g_y, int rows, int Cout, float *g_b) {
+  for (int co = threadIdx.x; co < Cout; co += blockDim.x) {
+    float acc = 0.f;
+    for (int r = blockIdx.x; r < rows; r += gridDim.x) acc += __ldg(g_y + (long long)r * Cout + co);
+    if (acc != 0.f) atomicAdd(g_b + co, acc);
+  }
+}
+
 __global__ void zero_f32_kernel(float *a, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     a[i] = 0.f;
@@ -437,6 +535,24 @@ int launch_backward(const BwdParams &p, void *stream, int *launches) {
   if (p.g_alpha) {
     zero_f32_kernel<<<1, 32, 0, st>>>(p.g_alpha, p.K);
     ++*launches;
+  }
+  const bool fc = p.H == 1 && p.W == 1 && p.R == 1 && p.S == 1 && p.pad == 0 && p.stride == 1 && p.fc_ws;
+  if (fc) {  // fully connected: dW = gY^T A and dA = gY W as tiled GEMMs over the G B rows
+    const int KB = p.G * p.B;
+    float *Aagg = static_cast<float *>(p.fc_ws), *dA = Aagg + (long long)KB * p.Cin;
+    fc_agg_kernel<<<grid1((long long)KB * p.Cin, 256), 256, 0, st>>>(p, Aagg);
+    dim3 gw((p.Cin + kGmT - 1) / kGmT, (p.Cout + kGmT - 1) / kGmT);
+    gemm_f32_kernel<<<gw, 256, 0, st>>>(p.Cout, p.Cin, KB, p.g_y, 1, p.Cout, Aagg, p.Cin, 1, p.g_w, p.Cin);
+    bias_grad_fc_kernel<<<std::min(KB, 148 * 4), 256, 0, st>>>(p.g_y, KB, p.Cout, p.g_b);
+    *launches += 3;
+    if (p.g_in || p.g_alpha) {
+      dim3 gd((p.Cin + kGmT - 1) / kGmT, (KB + kGmT - 1) / kGmT);
+      // W(co, ci) = p.w[ci Cout + co] (SIMT layout [Cin][1][1][Cout])
+      gemm_f32_kernel<<<gd, 256, 0, st>>>(KB, p.Cin, p.Cout, p.g_y, p.Cout, 1, p.w, 1, p.Cout, dA, p.Cin);
+      fc_gin_kernel<<<std::max(1, std::min(grid1((long long)KB * p.Cin, 256), 148 * 4)), 256, 0, st>>>(p, dA);
+      *launches += 2;
+    }
+    return (int)cudaGetLastError();
   }
   static const bool no_wgtc = [] { const char *e = std::getenv("TACSNN_NO_WGRAD_TC"); return e && *e == '1'; }();
   if (p.tc && p.wg_abuf && !no_wgtc && wgrad_tc_ok(p)) {

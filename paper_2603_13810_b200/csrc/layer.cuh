@@ -80,6 +80,7 @@ struct BwdParams {
   void *dg_img;         // workspace for the tcgen05 input-gradient weights (bwd_tc.cu), or NULL
   int tc;               // the layer's forward ran on tcgen05 (the tcgen05 backward kernels apply)
   void *wg_abuf;        // workspace for the weight gradient's bf16 A_k buffer, or NULL
+  void *fc_ws;          // fully connected layers: workspace [A_k | dA] fp32 [G B][C_in] each, or NULL
 };
 int launch_backward(const BwdParams &p, void *stream, int *launches);
 // tcgen05 input gradient (bwd_tc.cu): eligibility, its weight-image bytes, launch

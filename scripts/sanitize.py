@@ -72,6 +72,47 @@ def run(name, kw, engine, real=False):
     print(f"  ok rate={cnt.sum().item() / max(1, out.numel())}", flush=True)
 
 
+FC_CASES = [
+    ("fc_1600_128", dict(T=8, B=130, C_in=1600, H=1, W=1, C_out=128, R=1, S=1, pad=0, K=4, mode="tac", beta=0.9)),
+    ("fc_512_110", dict(T=8, B=3, C_in=512, H=1, W=1, C_out=110, R=1, S=1, pad=0, K=4, mode="tactp", beta=0.5)),
+]
+TRAIN_CASES = [   # training forward + backward: tcgen05 dgrad / wgrad, first-layer wgrad, FC GEMMs
+    ("train_c128", dict(T=4, B=2, C_in=128, H=16, W=16, C_out=128, pad=1, K=2, mode="tactp", beta=0.5)),
+    ("train_c2", dict(T=4, B=2, C_in=2, H=32, W=32, C_out=128, pad=1, K=2, mode="tac", beta=0.5)),
+    ("train_fc", dict(T=4, B=3, C_in=512, H=1, W=1, C_out=110, R=1, S=1, pad=0, K=2, mode="tactp", beta=0.5)),
+]
+
+
+def run_fc(name, kw, workspace):
+    spec = T.LayerSpec(**kw)
+    print(f"case {name}/{spec.engine_used()}/ws={workspace}", flush=True)
+    w, b = synth.weights(1, spec.C_out, spec.C_in, 1, 1, gain=3.0)
+    prep = T.prepare_weights(spec, w, b)
+    g = torch.Generator().manual_seed(3)
+    x = T.pack((torch.rand((spec.T, spec.B, spec.C_in, 1, 1), generator=g) < 0.2).to(torch.uint8).cuda())
+    out, vf, cnt = T.conv_lif(spec, prep, x, want_v_final=True, workspace=workspace)
+    torch.cuda.synchronize()
+    votes = T.vote(cnt, 10, spec.T) if spec.C_out % 10 == 0 else None
+    torch.cuda.synchronize()
+    print(f"  ok rate={cnt.sum().item() / max(1, out.numel())} vote={votes is not None}", flush=True)
+
+
+def run_train(name, kw):
+    spec = T.LayerSpec(**kw, out_pool=1)
+    r = spec.R
+    print(f"case {name}/{spec.engine_used()}", flush=True)
+    w, b = synth.weights(1, spec.C_out, spec.C_in, r, r, gain=3.0)
+    prep = T.prepare_weights(spec, w, b)
+    g = torch.Generator().manual_seed(3)
+    x = T.pack((torch.rand((spec.T, spec.B, spec.C_in, spec.H, spec.W), generator=g) < 0.2).to(torch.uint8).cuda())
+    out, _, _, y = T.conv_lif_train(spec, prep, x)
+    hc, wc = spec.conv_hw
+    gs = torch.randn((out.shape[0], spec.B, hc, wc, spec.C_out), generator=g).cuda()
+    res = T.conv_lif_backward(spec, prep, x, y, gs, surrogate="arctan", alpha=2.0, detach_reset=True)
+    torch.cuda.synchronize()
+    print(f"  ok |gW|={res['g_weight'].abs().sum().item():.3e}", flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true", help="tcgen05 engine only, fewer cases")
@@ -83,6 +124,11 @@ def main():
             run(name, kw, eng)
         for name, kw in REAL_CASES:
             run(name, kw, eng, real=True)
+    for name, kw in FC_CASES:
+        for ws in (True, False):
+            run_fc(name, kw, ws)
+    for name, kw in TRAIN_CASES:
+        run_train(name, kw)
     print("sanitize: all cases ran", flush=True)
 
 

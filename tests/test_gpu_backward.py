@@ -60,6 +60,9 @@ CASES = [
     ("dvsL1", (8, 2, 2, 32, 32, 128, 1), 0.5, 6.0, 0.08),
     ("mnistL2", (8, 3, 32, 13, 13, 64, 0), 0.9, 3.0, 0.15),
     ("dvsL2", (8, 2, 128, 16, 16, 128, 1), 0.5, 3.0, 0.1),
+    # fully connected layers (1x1 conv of a 1x1 image; backward = two tiled GEMMs)
+    ("fc1600", (8, 5, 1600, 1, 1, 128, 0, 1), 0.9, 3.0, 0.15),
+    ("fc512", (8, 3, 512, 1, 1, 110, 0, 1), 0.5, 4.0, 0.1),
 ]
 
 
@@ -67,8 +70,10 @@ CASES = [
 @pytest.mark.parametrize("mode,K", [("dense", 1), ("tac", 4), ("tactp", 2), ("tactp", 4)])
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
 def test_layer_backward_parity(T, O, case, mode, K, engine):
-    name, (Tn, B, Cin, H, W, Cout, pad), beta, gain, rho = case
-    spec = T.LayerSpec(T=Tn, B=B, C_in=Cin, H=H, W=W, C_out=Cout, pad=pad, K=K, mode=mode, beta=beta,
+    name, shape, beta, gain, rho = case
+    Tn, B, Cin, H, W, Cout, pad = shape[:7]
+    R = shape[7] if len(shape) > 7 else 3
+    spec = T.LayerSpec(T=Tn, B=B, C_in=Cin, H=H, W=W, C_out=Cout, R=R, S=R, pad=pad, K=K, mode=mode, beta=beta,
                        out_pool=1, engine=engine)
     try:
         assert spec.engine_used() == engine
@@ -79,7 +84,7 @@ def test_layer_backward_parity(T, O, case, mode, K, engine):
     g = torch.Generator().manual_seed(seed)
     S = (torch.rand((Tn, B, Cin, H, W), generator=g) < rho).to(torch.uint8).numpy()
     from paper_2603_13810_b200 import synth
-    w, b = synth.weights(seed % 1000, Cout, Cin, gain=gain if mode != "tactp" else gain / 1.5)
+    w, b = synth.weights(seed % 1000, Cout, Cin, R, R, gain=gain if mode != "tactp" else gain / 1.5)
     prep = T.prepare_weights(spec, w, b)
     x = T.pack(torch.from_numpy(S).cuda())
     hc, wc = spec.conv_hw
