@@ -128,6 +128,10 @@ constexpr int kProdWarps = 3;
 #ifndef TACSNN_UT_MIN_NS
 #define TACSNN_UT_MIN_NS 4  // U in TMEM for the fp16 paths from this many LIF steps per group
 #endif
+#ifndef TACSNN_UT_UNROLL
+#define TACSNN_UT_UNROLL 4  // chunks per unrolled body of the U-in-TMEM LIF loop (instruction footprint)
+#endif
+constexpr int kUtUnroll = TACSNN_UT_UNROLL;
 #ifndef TACSNN_H16_ACCS
 #define TACSNN_H16_ACCS 3  // TMEM accumulators on the fp16 paths (2 or 3)
 #endif
@@ -1536,7 +1540,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
         ptx::tmem_ld8(tcol + (NCHUNK - 1) * 8, dy[0]);
         ptx::tmem_ld8(ucol + (NCHUNK - 1) * 8, du[0]);
         ptx::tmem_wait_ld_dep(dy[0], du[0]);
-#pragma unroll
+#pragma unroll kUtUnroll
         for (int i = 0; i < NCHUNK; ++i) {
           const int ch = NCHUNK - 1 - i, cur = i & 1, nxt = cur ^ 1;
           if (ch > 0) {
