@@ -342,7 +342,9 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   p.nvth_s = -lp.v_th * p.ysc;
   p.wpr_in = lp.wpr_in; p.wpr_out = lp.wpr_out;
   p.nwo = lp.Cout % 32 == 0 ? lp.Cout / 32 : 1;
-  const bool out_atomic = g.cout_pad < 64;  // sub-word or shared-word output fields
+  static const bool no_c32w = [] { const char *e = std::getenv("TACSNN_NO_C32W"); return e && *e == '1'; }();
+  p.c32w = (!no_c32w && g.path != PATH_HALO && g.cout_pad == 32) ? 1 : 0;
+  const bool out_atomic = g.cout_pad < 64 && !p.c32w;  // sub-word or shared-word output fields
   {  // exact s32 combine 254 D_hi + D_lo possible? |A| <= A_max, |q| <= 127, K_red terms
     double a_max = 0;
     for (int j = 0; j < lp.K; ++j) a_max += std::ldexp(1.0, p.m_shift * j);

@@ -67,6 +67,7 @@ struct TcParams {
   int warp_stage;             // 1: each producer warp builds whole A stages (stage it -> warp it % 3)
   int prod_refill;            // 1 (plane mode + warp_stage): the warp that consumed raw slot r refills it
   int occ;                    // CTA pairs per SM pair (1, or 2 for small first layers: OCC kernels)
+  int c32w;                   // fp16 path, C_out 32: 4 epilogue warps x 32 channels (no atomic sub-word stores)
   int prod_step;              // halo-row stride of the pixel-wise producers: 96, or 32 with warp_stage
   uint32_t off_raw, raw_stage_bytes, raw_box_bytes;
   int B, H, W, Cin, Cout, Cout_pad, pad, Ho, Wo, pool;
@@ -1910,8 +1911,13 @@ template <int NKC2, int NSL>
 __device__ __forceinline__ void mma_group_h16(uint32_t d_tmem, uint64_t a_base, uint64_t b_desc0,
                                               uint32_t idf, uint32_t lbo16, uint32_t nhb16) {
   if constexpr (NKC2 == 1) {
+#ifdef TACSNN_EXP_TAPS
+#pragma unroll
+    for (int tap = 0; tap < TACSNN_EXP_TAPS; ++tap) mma_tap_h16<NKC2, NSL>(tap, d_tmem, a_base, b_desc0, idf, lbo16, nhb16);
+#else
 #pragma unroll
     for (int tap = 0; tap < 9; ++tap) mma_tap_h16<NKC2, NSL>(tap, d_tmem, a_base, b_desc0, idf, lbo16, nhb16);
+#endif
   } else {
 #pragma unroll 1
     for (int tap = 0; tap < 9; ++tap) mma_tap_h16<NKC2, NSL>(tap, d_tmem, a_base, b_desc0, idf, lbo16, nhb16);
@@ -2166,6 +2172,10 @@ template <>
 cudaError_t tc_launch_path<TAC_TC_PATH, TAC_TC_TRAIN>(const TcParams &p, int cout_pad, int nclusters,
                                                      cudaStream_t stream) {
   if constexpr (TAC_TC_PATH != PATH_HALO) {
+    if (cout_pad == 32 && p.c32w) {  // 4 epilogue warps x 32 channels: whole-word stores
+      if (p.occ == 2) return launch_kernel<32, TAC_TC_PATH, 1, TAC_TC_TRAIN, 2>(p, nclusters, stream);
+      return launch_kernel<32, TAC_TC_PATH, 1, TAC_TC_TRAIN>(p, nclusters, stream);
+    }
     if (p.occ == 2) {
       if (cout_pad == 16) return launch_kernel<8, TAC_TC_PATH, 2, TAC_TC_TRAIN, 2>(p, nclusters, stream);
       if (cout_pad == 32) return launch_kernel<16, TAC_TC_PATH, 2, TAC_TC_TRAIN, 2>(p, nclusters, stream);
