@@ -296,7 +296,7 @@ __global__ void dg_weights_kernel(const float *w, int Cin, int Cout, unsigned ch
 template <int NPART>
 cudaError_t dg_launch(const DgParams &p, cudaStream_t st) {
   auto kern = dgrad_tc_kernel<NPART>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void *>(kern), (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
   kern<<<std::min(p.nunits, 148), dg_threads(NPART), p.smem_bytes, st>>>(p);
   return cudaGetLastError();
@@ -667,7 +667,7 @@ int launch_wgrad_tc(const BwdParams &bp, void *stream, int *launches) {
   p.smem_bytes = p.off_bar + 8 * (2 * kWgAStg + 1) + 16;
   p.ncta_r = std::max(1, std::min(49, p.nunits));
   auto kern = wgrad_tc_kernel;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void *>(kern), (int)p.smem_bytes);
   if (e != cudaSuccess) return (int)e;
   kern<<<3 * p.ncta_r, wg_threads(), p.smem_bytes, st>>>(p);
   ++*launches;

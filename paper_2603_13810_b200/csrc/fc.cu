@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(fc_threads(NPART), 1) fc_lif_tc_kernel(const _
 template <int NPART, int NS, bool TRAIN, bool GEMM = false>
 cudaError_t fc_launch_kernel(const FcParams &p, int grid, cudaStream_t st) {
   auto kern = fc_lif_tc_kernel<NPART, NS, TRAIN, GEMM>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void *>(kern), (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
   kern<<<grid, fc_threads(NPART), p.smem_bytes, st>>>(p);
   return cudaGetLastError();

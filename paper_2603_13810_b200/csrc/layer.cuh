@@ -5,6 +5,10 @@
 
 namespace tacsnn {
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, size) instead of
+// on every launch (a host-side cost the launch-bound small layers pay per call)
+cudaError_t ensure_dyn_smem(const void *kern, int bytes);
+
 constexpr int kMaxK = 32;
 
 struct LayerParams {

@@ -2146,8 +2146,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
 template <int NCH, int PATH, int NPART, bool TRAIN, int OCC = 1>
 cudaError_t launch_kernel(const TcParams &p, int nclusters, cudaStream_t stream) {
   auto kern = tc_conv_lif_kernel<NCH, PATH, NPART, TRAIN, OCC>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)p.smem_bytes);
+  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void *>(kern), (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
   kern<<<dim3(2 * nclusters), dim3(kernel_threads(NPART)), p.smem_bytes, stream>>>(p);
   return cudaGetLastError();
