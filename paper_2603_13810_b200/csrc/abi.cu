@@ -622,7 +622,7 @@ size_t bwd_wgrad_abuf_bytes(const tac_conv_lif_desc *d, const Geo &g) {
                   (d->pad == 0 || d->pad == 1) && d->input_kind == TAC_INPUT_SPIKES &&
                   (d->C_in <= 8 || (d->C_in % 16 == 0 && d->C_in <= 128)) && d->C_out >= 64 && d->C_out <= 128 &&
                   d->C_out % 8 == 0;
-  return ok ? align256(tacsnn::wgrad_tc_ws_bytes(g.G, d->B, d->H, d->W, d->C_in)) : 0;
+  return ok ? align256(tacsnn::wgrad_tc_ws_bytes(g.G, d->B, d->H, d->W, d->C_in, g.Ho, g.Wo, d->C_out)) : 0;
 }
 
 // ... and, for a fully connected layer, the aggregated input and its gradient (GEMM path)

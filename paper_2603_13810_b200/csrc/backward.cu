@@ -406,6 +406,20 @@ __global__ void zero_f32_kernel(float *a, long long n) {
 }
 
 // 2x2 OR-pool of packed spikes (floor mode): thread per output word
+// C % 32 == 0: a pooled word is the OR of the same channel word of the window's 4 pixels;
+// grid (ceil(Wq nw / 128), TB Hq): no 64-bit index arithmetic
+__global__ void or_pool2_w32_kernel(const uint32_t *in, uint32_t *out, int C, int H, int W) {
+  const int Hq = H / 2, Wq = W / 2, nw = C / 32;
+  const int idx = blockIdx.y * blockDim.x + threadIdx.x;
+  if (idx >= Wq * nw) return;
+  const int xo = idx / nw, wd = idx - xo * nw;
+  const long long row = blockIdx.x;  // tb Hq + yo
+  const long long tb = row / Hq;
+  const int yo = (int)(row - tb * Hq);
+  const uint32_t *r0 = in + ((tb * H + 2 * yo) * W + 2 * xo) * nw + wd, *r1 = r0 + (long long)W * nw;
+  out[row * Wq * nw + idx] = r0[0] | r0[nw] | r1[0] | r1[nw];
+}
+
 __global__ void or_pool2_kernel(const uint32_t *in, uint32_t *out, long long TB, int C, int H, int W) {
   const int Hq = H / 2, Wq = W / 2;
   const int wpr_in = (W * C + 31) / 32, wpr_out = (Wq * C + 31) / 32;
@@ -434,59 +448,40 @@ __global__ void or_pool2_kernel(const uint32_t *in, uint32_t *out, long long TB,
 
 // MaxPool2d backward on binary maps: g_pre[t][b][y][x][c] = g_pooled of its window if
 // (y, x) is the window's first maximal element in row-major order, else 0
-// C % 32 == 0: one thread per (pooled window, 32 channels): the window's four spike words,
-// per channel the first spiking element in row-major order (top-left when none), one
-// 128-B read of the pooled gradient and four 128-B writes
+// C % 32 == 0: one thread per (pooled window, 4 channels) of one unpooled row y: a warp
+// stores whole 512-B pixel rows (C = 128), reads the pooled gradient as one 512-B row and the
+// window's spike words by broadcast; per channel the gradient goes to the first spiking
+// element in row-major order (top-left when none).  Grid (TB H, ceil(Wq C / 4 / 128)).
 __global__ void or_pool2_bwd32_kernel(const uint32_t *pre, const float *g_pooled, float *g_pre, long long TB,
                                       int C, int H, int W) {
-  const int Hq = H / 2, Wq = W / 2, nw = C / 32;
-  const int wpr = W * nw;
-  const long long n = TB * H * Wq * nw;  // (tb, y, xo, word): rows y of the unpooled map
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const int wd = (int)(i % nw);
-    long long q = i / nw;
-    const int xo = (int)(q % Wq);
-    q /= Wq;
-    const int y = (int)(q % H);
-    const long long tb = q / H;
-    const int yo = y >> 1, dy = y & 1;
-    float *dst0 = g_pre + (((tb * H + y) * W + 2 * xo) * C) + wd * 32;
-    float4 *d0 = reinterpret_cast<float4 *>(dst0), *d1 = reinterpret_cast<float4 *>(dst0 + C);
-    if (yo >= Hq) {  // floor mode: the dropped row gets no gradient
-#pragma unroll
-      for (int v = 0; v < 8; ++v) d0[v] = d1[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (2 * xo + 2 == W - 1 && (W & 1)) {  // the dropped last column
-        float4 *d2 = reinterpret_cast<float4 *>(dst0 + 2 * C);
-#pragma unroll
-        for (int v = 0; v < 8; ++v) d2[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      continue;
-    }
-    const uint32_t *r0 = pre + (tb * H + 2 * yo) * wpr + wd, *r1 = r0 + wpr;
-    const uint32_t w00 = r0[(2 * xo) * nw], w01 = r0[(2 * xo + 1) * nw];
-    const uint32_t w10 = r1[(2 * xo) * nw], w11 = r1[(2 * xo + 1) * nw];
-    // masks of the element each channel's gradient goes to (e = 2 dy + dx)
-    const uint32_t m00 = w00 | ~(w00 | w01 | w10 | w11);
-    const uint32_t m01 = w01 & ~w00;
-    const uint32_t m10 = w10 & ~(w00 | w01);
-    const uint32_t m11 = w11 & ~(w00 | w01 | w10);
-    const uint32_t ma = dy ? m10 : m00, mb = dy ? m11 : m01;
-    const float4 *src = reinterpret_cast<const float4 *>(g_pooled + ((tb * Hq + yo) * Wq + xo) * C + wd * 32);
-#pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      const float4 g = __ldg(src + v);
-      const int b0 = 4 * v;
-      d0[v] = make_float4(((ma >> b0) & 1u) ? g.x : 0.f, ((ma >> (b0 + 1)) & 1u) ? g.y : 0.f,
-                          ((ma >> (b0 + 2)) & 1u) ? g.z : 0.f, ((ma >> (b0 + 3)) & 1u) ? g.w : 0.f);
-      d1[v] = make_float4(((mb >> b0) & 1u) ? g.x : 0.f, ((mb >> (b0 + 1)) & 1u) ? g.y : 0.f,
-                          ((mb >> (b0 + 2)) & 1u) ? g.z : 0.f, ((mb >> (b0 + 3)) & 1u) ? g.w : 0.f);
-    }
-    if (2 * xo + 2 == W - 1 && (W & 1)) {  // floor mode: the dropped last column
-      float4 *d2 = reinterpret_cast<float4 *>(dst0 + 2 * C);
-#pragma unroll
-      for (int v = 0; v < 8; ++v) d2[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+  const int Hq = H / 2, Wq = W / 2, nw = C / 32, nq = C / 4;
+  const int i = blockIdx.y * blockDim.x + threadIdx.x;
+  if (i >= Wq * nq) return;
+  const int xo = i / nq, q = i - xo * nq;
+  const long long rowi = blockIdx.x;
+  const long long tb = rowi / H;
+  const int y = (int)(rowi - tb * H);
+  const int yo = y >> 1, dy = y & 1;
+  float4 *d0 = reinterpret_cast<float4 *>(g_pre + ((tb * H + y) * W + 2 * xo) * C) + q;
+  float4 *d1 = d0 + nq;
+  const bool last_col = (W & 1) && 2 * xo + 2 == W - 1;  // floor mode: the dropped column
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (last_col) d1[nq] = z;
+  if (yo >= Hq) {  // floor mode: the dropped row
+    *d0 = z;
+    *d1 = z;
+    return;
   }
+  const int wd = q >> 3, sh = (q & 7) * 4;
+  const uint32_t *r0 = pre + (tb * H + 2 * yo) * (long long)W * nw + wd, *r1 = r0 + (long long)W * nw;
+  const uint32_t w00 = (r0[(2 * xo) * nw] >> sh) & 0xFu, w01 = (r0[(2 * xo + 1) * nw] >> sh) & 0xFu;
+  const uint32_t w10 = (r1[(2 * xo) * nw] >> sh) & 0xFu, w11 = (r1[(2 * xo + 1) * nw] >> sh) & 0xFu;
+  const uint32_t m00 = (w00 | ~(w00 | w01 | w10 | w11)) & 0xFu, m01 = w01 & ~w00;
+  const uint32_t m10 = w10 & ~(w00 | w01), m11 = w11 & ~(w00 | w01 | w10);
+  const uint32_t ma = dy ? m10 : m00, mb = dy ? m11 : m01;
+  const float4 g = __ldg(reinterpret_cast<const float4 *>(g_pooled + ((tb * Hq + yo) * Wq + xo) * C) + q);
+  *d0 = make_float4((ma & 1u) ? g.x : 0.f, (ma & 2u) ? g.y : 0.f, (ma & 4u) ? g.z : 0.f, (ma & 8u) ? g.w : 0.f);
+  *d1 = make_float4((mb & 1u) ? g.x : 0.f, (mb & 2u) ? g.y : 0.f, (mb & 4u) ? g.z : 0.f, (mb & 8u) ? g.w : 0.f);
 }
 
 __global__ void or_pool2_bwd_kernel(const uint32_t *pre, const float *g_pooled, float *g_pre, long long TB,
@@ -586,16 +581,21 @@ int launch_backward(const BwdParams &p, void *stream, int *launches) {
 int launch_or_pool2(const uint32_t *in, uint32_t *out, int T, int B, int C, int H, int W, void *stream) {
   const long long TB = (long long)T * B;
   const long long n = TB * (H / 2) * (((W / 2) * C + 31) / 32);
-  or_pool2_kernel<<<grid1(n, 256), 256, 0, (cudaStream_t)stream>>>(in, out, TB, C, H, W);
+  if (C % 32 == 0 && W >= 2 && H >= 2 && TB * (H / 2) < (1LL << 31))
+    or_pool2_w32_kernel<<<dim3((unsigned)(TB * (H / 2)), (unsigned)(((W / 2) * (C / 32) + 127) / 128)), 128, 0,
+                          (cudaStream_t)stream>>>(in, out, C, H, W);
+  else
+    or_pool2_kernel<<<grid1(n, 256), 256, 0, (cudaStream_t)stream>>>(in, out, TB, C, H, W);
   return (int)cudaGetLastError();
 }
 
 int launch_or_pool2_backward(const uint32_t *pre, const float *g_pooled, float *g_pre, int T, int B, int C,
                              int H, int W, void *stream) {
   const long long TB = (long long)T * B;
-  if (C % 32 == 0 && (reinterpret_cast<uintptr_t>(g_pre) | reinterpret_cast<uintptr_t>(g_pooled)) % 16 == 0)
-    or_pool2_bwd32_kernel<<<grid1(TB * H * (W / 2) * (C / 32), 256), 256, 0, (cudaStream_t)stream>>>(
-        pre, g_pooled, g_pre, TB, C, H, W);
+  if (C % 32 == 0 && (reinterpret_cast<uintptr_t>(g_pre) | reinterpret_cast<uintptr_t>(g_pooled)) % 16 == 0 &&
+      TB * H < (1LL << 31))
+    or_pool2_bwd32_kernel<<<dim3((unsigned)(TB * H), (unsigned)(((W / 2) * (C / 4) + 127) / 128)), 128, 0,
+                            (cudaStream_t)stream>>>(pre, g_pooled, g_pre, TB, C, H, W);
   else
     or_pool2_bwd_kernel<<<grid1(TB * H * W * C, 256), 256, 0, (cudaStream_t)stream>>>(pre, g_pooled, g_pre, TB,
                                                                                       C, H, W);

@@ -316,6 +316,7 @@ constexpr int kWgHaloRows = kDgTileH * kDgHaloW;  // 16 x 10 halo pixels of one 
 
 struct WgParams {
   CUtensorMap amap[2];         // 5-D views {8 ch, W, H, Cp / 8 chunks, G B} of the bf16 A_k buffer (hi, lo)
+  CUtensorMap gmap[2];         // 5-D views {8 co, Wo, Ho, C_out / 8 chunks, G B} of bf16 dL/dY (hi, lo)
   int G, B, H, W, Cin, Cout, K, pad, Ho, Wo, wpr_in;
   int Np;                      // MMA N: C_in padded to a multiple of 16 (>= 16; first layers C_in <= 8)
   int tiles_x, tiles_y, nunits, split, nstages, ncta_r;
@@ -354,38 +355,16 @@ __device__ __forceinline__ void wg_producer(const WgParams &p, uint32_t sbase, u
     const uint32_t s = it % (uint32_t)p.nstages, ph = (it / (uint32_t)p.nstages) & 1u;
     ptx::mbar_wait(bar_empty + 8 * s, ph ^ 1u);
     const uint32_t st = sbase + s * p.stage_bytes;
-    // dL/dY tile (M = 128 rows of co, zero above C_out): [co chunk][128 px][16 B] hi | lo
-    for (int i = ptid; i < 128 * coch; i += 32 * kDgProd) {
-      const int px = i & 127, cc = i >> 7;
-      const int y = y0 + (px >> 3), x = x0 + (px & 7);
-      float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
-      if (y < p.Ho && x < p.Wo && cc * 8 < p.Cout) {
-        const float4 *src = reinterpret_cast<const float4 *>(
-            p.g_y + (long long)k * N + (((long long)b * p.Ho + y) * p.Wo + x) * p.Cout + cc * 8);
-        v0 = __ldg(src);
-        v1 = __ldg(src + 1);
-      }
-      uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
-      split2(v0.x, v0.y, h0, l0);
-      split2(v0.z, v0.w, h1, l1);
-      split2(v1.x, v1.y, h2, l2);
-      split2(v1.z, v1.w, h3, l3);
-      const uint32_t dst = st + (uint32_t)(cc * 128 + px) * 16u;
-      ptx::st_shared_v4(dst, h0, h1, h2, h3);
-      ptx::st_shared_v4(dst + p.gy_slice, l0, l1, l2, l3);
-    }
-    // A_k halo of kernel row r (the pre-pass's bf16 buffer): one 5-D TMA box per slice lands
-    // as [ci chunk][16 x 10 px][16 B]; out-of-bounds pixels / chunks are the zero padding
-    if (ptid == 0) {
-      const uint32_t ast = st + 2 * p.gy_slice;
-      ptx::mbar_arrive_expect_tx(bar_full + 8 * s, (p.split ? 2u : 1u) * p.a_slice);
-      for (int sl = 0; sl < (p.split ? 2 : 1); ++sl)
-        ptx::tma_load_5d(ast + sl * p.a_slice, &p.amap[sl], 0, x0 - p.pad, y0 + r - p.pad, 0, k * p.B + b,
-                         bar_full + 8 * s);
-    }
-    ptx::fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) ptx::mbar_arrive_local(bar_full + 8 * s);
+    // dL/dY tile and A_k halo of kernel row r from the pre-pass's bf16 buffers, one 5-D TMA box
+    // per slice: dL/dY lands as [co chunk][16 x 8 px][16 B] (chunks above C_out: zero fill =
+    // the unused M rows), A_k as [ci chunk][16 x 10 px][16 B] (out of bounds: the padding)
+    const uint32_t ast = st + 2 * p.gy_slice;
+    ptx::mbar_arrive_expect_tx(bar_full + 8 * s, 2 * p.gy_slice + (p.split ? 2u : 1u) * p.a_slice);
+    for (int sl = 0; sl < 2; ++sl)
+      ptx::tma_load_5d(st + sl * p.gy_slice, &p.gmap[sl], 0, x0, y0, 0, k * p.B + b, bar_full + 8 * s);
+    for (int sl = 0; sl < (p.split ? 2 : 1); ++sl)
+      ptx::tma_load_5d(ast + sl * p.a_slice, &p.amap[sl], 0, x0 - p.pad, y0 + r - p.pad, 0, k * p.B + b,
+                       bar_full + 8 * s);
   }
 }
 
@@ -398,7 +377,7 @@ __global__ void __launch_bounds__(wg_threads(), 1) wgrad_tc_kernel(const __grid_
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + p.off_bar + 8 * (2 * kWgAStg + 1));
   if (threadIdx.x == 0) {
     for (int s = 0; s < kWgAStg; ++s) {
-      ptx::mbar_init(bar_full + 8 * s, kDgProd + 1);  // producer warps + the A box's expect_tx
+      ptx::mbar_init(bar_full + 8 * s, 1);  // the loader thread's expect_tx (all operands by TMA)
       ptx::mbar_init(bar_empty + 8 * s, 1);
     }
     ptx::mbar_init(bar_done, 1);
@@ -467,7 +446,7 @@ __global__ void __launch_bounds__(wg_threads(), 1) wgrad_tc_kernel(const __grid_
     if (any && ptx::elect_one()) ptx::mma_commit_cg1(bar_done);
     __syncwarp();
   } else {
-    wg_producer(p, sbase, bar_full, bar_empty, r, cta_r, (int)(threadIdx.x - 32 * 5), lane);
+    if (threadIdx.x == 32 * 5) wg_producer(p, sbase, bar_full, bar_empty, r, cta_r, 0, lane);
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -519,6 +498,18 @@ __global__ void agg_bf16_kernel(const uint32_t *in, long long in_st, long long i
     const long long o = i * 8;
     *reinterpret_cast<uint4 *>(out_hi + o) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
     if (out_lo) *reinterpret_cast<uint4 *>(out_lo + o) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  }
+}
+
+// pre-pass: dL/dY fp32 -> bf16 hi | lo (two planes of the same [G B][Ho][Wo][C_out] layout)
+__global__ void gy_bf16_kernel(const float *g_y, long long n4, __nv_bfloat16 *hi, __nv_bfloat16 *lo) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = __ldg(reinterpret_cast<const float4 *>(g_y) + i);
+    uint32_t h0, h1, l0, l1;
+    split2(v.x, v.y, h0, l0);
+    split2(v.z, v.w, h1, l1);
+    reinterpret_cast<uint2 *>(hi)[i] = make_uint2(h0, h1);
+    reinterpret_cast<uint2 *>(lo)[i] = make_uint2(l0, l1);
   }
 }
 
@@ -599,9 +590,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 wg_encoder() {
 }
 
 // bytes of the bf16 A_k buffer (two slices, the worst case) the weight gradient stages through
-size_t wgrad_tc_ws_bytes(int G, int B, int H, int W, int Cin) {
+size_t wgrad_tc_ws_bytes(int G, int B, int H, int W, int Cin, int Ho, int Wo, int Cout) {
   const long long Cp = (Cin + 7) / 8 * 8;
-  return (size_t)2 * G * B * H * W * Cp * 2;
+  return (size_t)2 * G * B * H * W * Cp * 2 + 256 + (size_t)2 * G * B * Ho * Wo * Cout * 2;
 }
 
 bool wgrad_tc_ok(const BwdParams &p) {
@@ -647,8 +638,28 @@ int launch_wgrad_tc(const BwdParams &bp, void *stream, int *launches) {
         bp.in, bp.in_st, bp.in_sb, bp.wpr_in, bp.G, bp.B, bp.H, bp.W, bp.Cin, Cp, bp.K, nullptr, p, a_hi, a_lo);
     ++*launches;
   }
+  // dL/dY as bf16 hi | lo after the A_k buffer (256-B aligned)
+  const long long nG = (long long)bp.G * bp.B * bp.Ho * bp.Wo * bp.Cout;
+  __nv_bfloat16 *g_hi = reinterpret_cast<__nv_bfloat16 *>(
+      (reinterpret_cast<uintptr_t>(a_hi + 2 * nA) + 255) & ~static_cast<uintptr_t>(255));
+  __nv_bfloat16 *g_lo = g_hi + nG;
+  gy_bf16_kernel<<<(unsigned)std::min<long long>((nG / 4 + 255) / 256, 148LL * 32), 256, 0, st>>>(bp.g_y, nG / 4,
+                                                                                                  g_hi, g_lo);
+  ++*launches;
   PFN_cuTensorMapEncodeTiled_v12000 enc = wg_encoder();
   if (!enc) return (int)cudaErrorNotSupported;
+  for (int sl = 0; sl < 2; ++sl) {
+    const cuuint64_t dims[5] = {8, (cuuint64_t)bp.Wo, (cuuint64_t)bp.Ho, (cuuint64_t)(bp.Cout / 8),
+                                (cuuint64_t)bp.G * bp.B};
+    const cuuint64_t strides[4] = {(cuuint64_t)bp.Cout * 2, (cuuint64_t)bp.Wo * bp.Cout * 2, 16,
+                                   (cuuint64_t)bp.Ho * bp.Wo * bp.Cout * 2};
+    const cuuint32_t box[5] = {8, (cuuint32_t)kDgTileW, (cuuint32_t)kDgTileH, 16, 1};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    const CUresult r = enc(&p.gmap[sl], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, (void *)(sl ? g_lo : g_hi), dims, strides,
+                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return (int)cudaErrorInvalidValue;
+  }
   for (int sl = 0; sl < (p.split ? 2 : 1); ++sl) {
     const cuuint64_t dims[5] = {8, (cuuint64_t)bp.W, (cuuint64_t)bp.H, (cuuint64_t)(Cp / 8), (cuuint64_t)bp.G * bp.B};
     const cuuint64_t strides[4] = {(cuuint64_t)Cp * 2, (cuuint64_t)bp.W * Cp * 2, 16, (cuuint64_t)bp.H * bp.W * Cp * 2};

@@ -93,7 +93,7 @@ size_t dgrad_tc_ws_bytes(int Cin, int Cout);
 int launch_dgrad_tc(const BwdParams &p, void *img, void *stream, int *launches);
 // tcgen05 weight gradient (bwd_tc.cu)
 bool wgrad_tc_ok(const BwdParams &p);
-size_t wgrad_tc_ws_bytes(int G, int B, int H, int W, int Cin);
+size_t wgrad_tc_ws_bytes(int G, int B, int H, int W, int Cin, int Ho, int Wo, int Cout);
 int launch_wgrad_tc(const BwdParams &p, void *stream, int *launches);
 int launch_or_pool2(const uint32_t *in, uint32_t *out, int T, int B, int C, int H, int W, void *stream);
 int launch_or_pool2_backward(const uint32_t *pre, const float *g_pooled, float *g_pre, int T, int B,

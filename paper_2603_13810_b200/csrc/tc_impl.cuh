@@ -1353,6 +1353,11 @@ __device__ __forceinline__ float sat_spike(float u) {
 __device__ __forceinline__ void store_yseq8(const TcParams &p, int k, long long vbase, int cc0, int nvalid,
                                             const float (&y)[8]) {
   float *dst = p.y_seq + (long long)k * p.yseq_plane + vbase + cc0;
+  if (nvalid >= 8) {  // 32 contiguous bytes (C_out % 8 == 0: 16-B aligned): two vector stores
+    reinterpret_cast<float4 *>(dst)[0] = make_float4(y[0], y[1], y[2], y[3]);
+    reinterpret_cast<float4 *>(dst)[1] = make_float4(y[4], y[5], y[6], y[7]);
+    return;
+  }
 #pragma unroll
   for (int q = 0; q < 8; ++q)
     if (q < nvalid) dst[q] = y[q];
