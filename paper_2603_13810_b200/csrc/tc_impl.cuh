@@ -367,6 +367,39 @@ __device__ __forceinline__ void tile_origin(const TcParams &p, int tile, int &b,
   ok = tile < p.num_tiles;
 }
 
+// origin of one output tile: sample, first output row / column, tile in range
+struct TileXY {
+  int b, y0, x0;
+  bool ok;
+};
+
+// Tiles t0, t0 + dt, t0 + 2 dt, ... as (sample, tile row, tile column), advanced
+// incrementally: the persistent role loops carry no integer division per tile.
+struct TileWalk {
+  int b, ty, tx, db, dty, dtx;
+  __device__ __forceinline__ TileWalk(const TcParams &p, int t0, int dt) {
+    const int per = p.tiles_x * p.tiles_y;
+    b = t0 / per;
+    ty = (t0 - b * per) / p.tiles_x;
+    tx = t0 - b * per - ty * p.tiles_x;
+    db = dt / per;
+    dty = (dt - db * per) / p.tiles_x;
+    dtx = dt - db * per - dty * p.tiles_x;
+  }
+  __device__ __forceinline__ TileXY at(const TcParams &p, int tile) const {
+    return TileXY{b, ty * kTileH, tx * kTileW, tile < p.num_tiles};
+  }
+  __device__ __forceinline__ void step(const TcParams &p) {
+    tx += dtx;
+    int cy = tx >= p.tiles_x;
+    tx -= cy ? p.tiles_x : 0;
+    ty += dty + cy;
+    cy = ty >= p.tiles_y;
+    ty -= cy ? p.tiles_y : 0;
+    b += db + cy;
+  }
+};
+
 // circular-buffer position (slot, phase parity) advanced by one per use: no integer
 // division by the runtime ring sizes in the role loops
 struct Ring {
@@ -397,7 +430,7 @@ __device__ __forceinline__ void agg_word_k(uint32_t (&o)[8], const uint32_t *xj,
 // rstep, ... (96 % nwin == 0).  Loads are issued in batches of RB pixels x K
 // frames before any is consumed, so one memory round trip covers RB pixels.
 template <int K>
-__device__ __forceinline__ void produce_halo(const TcParams &p, int tile, int k, uint32_t a_stage,
+__device__ __forceinline__ void produce_halo(const TcParams &p, const TileXY &tile, int k, uint32_t a_stage,
                                              int ptid) {
   constexpr int RB = K >= 8 ? 2 : (K >= 4 ? 4 : 8);
   const int nwin = p.Cin >> 5;
@@ -406,9 +439,8 @@ __device__ __forceinline__ void produce_halo(const TcParams &p, int tile, int k,
   // raw-halo loads (pixel stride nwin words, 4 words in a group) hit distinct banks
   const int g8 = ptid >> 3, w = g8 % nwin, row0 = (g8 / nwin) * 8 + (ptid & 7);
   const int rstep = (kProdWarps * 32) / nwin;
-  int b, y0, x0;
-  bool tok;
-  tile_origin(p, tile, b, y0, x0, tok);
+  const int b = tile.b, y0 = tile.y0, x0 = tile.x0;
+  const bool tok = tile.ok;
   const uint32_t *frame0 = p.in + (long long)(k * K) * p.in_st + (long long)b * p.in_sb + w;
   const long long in_st = p.in_st;
   const int mshift = p.m_shift;
@@ -490,11 +522,10 @@ __device__ __forceinline__ uint32_t ld_src(const uint32_t *a) {
 // LDG fallback: one halo pixel per thread and pass; the C_in <= 8 bits of pixel
 // xi start at row bit xi * C_in and straddle at most two words.
 template <int K, bool SMEM = false>
-__device__ __forceinline__ void produce_h16(const TcParams &p, int tile, int k, uint32_t a_stage,
+__device__ __forceinline__ void produce_h16(const TcParams &p, const TileXY &tile, int k, uint32_t a_stage,
                                             int ptid, const uint32_t *plane = nullptr) {
-  int b, y0, x0;
-  bool tok;
-  tile_origin(p, tile, b, y0, x0, tok);
+  const int b = tile.b, y0 = tile.y0, x0 = tile.x0;
+  const bool tok = tile.ok;
   const int Cin = p.Cin;
   const uint32_t cmask = (1u << Cin) - 1u;
   uint32_t one_lo, one_hi, c8;
@@ -665,11 +696,10 @@ __device__ __forceinline__ uint32_t split_lookup(uint32_t idx, int K, const uint
 // X_{kK+j, c} in fp32 (the oracle's order), then the same [A_hi | A_lo | 1.0] row as
 // the split path
 template <int K, int CIN>
-__device__ __forceinline__ void produce_h16x(const TcParams &p, int tile, int k, uint32_t a_stage,
+__device__ __forceinline__ void produce_h16x(const TcParams &p, const TileXY &tile, int k, uint32_t a_stage,
                                              int ptid) {
-  int b, y0, x0;
-  bool tok;
-  tile_origin(p, tile, b, y0, x0, tok);
+  const int b = tile.b, y0 = tile.y0, x0 = tile.x0;
+  const bool tok = tile.ok;
   const float *frame0 = p.xin + (long long)(k * (K ? K : p.K)) * p.in_st + (long long)b * p.in_sb;
   for (int row = ptid; row < kHaloRows; row += p.prod_step) {
     const int hy = row / kHaloW, hx = row - (row / kHaloW) * kHaloW;
@@ -699,11 +729,10 @@ __device__ __forceinline__ void produce_h16x(const TcParams &p, int tile, int k,
 // LDG split producers (e.g. MNIST rows, whose 4-B row stride rules out halo-box TMA;
 // SMEM: plane mode, the whole frames in shared memory)
 template <int K, int CIN, bool SMEM = false>
-__device__ __forceinline__ void produce_h16s(const TcParams &p, const uint32_t *lut, int tile, int k,
+__device__ __forceinline__ void produce_h16s(const TcParams &p, const uint32_t *lut, const TileXY &tile, int k,
                                              uint32_t a_stage, int ptid, const uint32_t *plane = nullptr) {
-  int b, y0, x0;
-  bool tok;
-  tile_origin(p, tile, b, y0, x0, tok);
+  const int b = tile.b, y0 = tile.y0, x0 = tile.x0;
+  const bool tok = tile.ok;
   const uint32_t *frame0 = SMEM ? plane : p.in + (long long)(k * K) * p.in_st + (long long)b * p.in_sb;
   const long long fst = SMEM ? (long long)p.raw_bw : p.in_st;
   for (int row = ptid; row < kHaloRows; row += p.prod_step) {
@@ -728,11 +757,10 @@ __device__ __forceinline__ void produce_h16s(const TcParams &p, const uint32_t *
 }
 
 template <int CIN, bool SMEM = false>
-__device__ __forceinline__ void produce_h16s_rt(const TcParams &p, const uint32_t *lut, int tile, int k,
+__device__ __forceinline__ void produce_h16s_rt(const TcParams &p, const uint32_t *lut, const TileXY &tile, int k,
                                                 uint32_t a_stage, int ptid, const uint32_t *plane = nullptr) {
-  int b, y0, x0;
-  bool tok;
-  tile_origin(p, tile, b, y0, x0, tok);
+  const int b = tile.b, y0 = tile.y0, x0 = tile.x0;
+  const bool tok = tile.ok;
   const int K = p.K;
   const uint32_t *frame0 = SMEM ? plane : p.in + (long long)(k * K) * p.in_st + (long long)b * p.in_sb;
   const long long fst = SMEM ? (long long)p.raw_bw : p.in_st;
@@ -823,13 +851,12 @@ __device__ __forceinline__ void produce_halo_rows(const TcParams &p, const uint3
 }
 
 template <int K, int CIN, bool SPLIT>
-__device__ __forceinline__ void produce_plane_rows(const TcParams &p, const uint32_t *lut, int tile,
+__device__ __forceinline__ void produce_plane_rows(const TcParams &p, const uint32_t *lut, const TileXY &tile,
                                                    uint32_t a_stage, int lane, const uint32_t *plane) {
   static_assert(K >= 1 && K <= 8 && (CIN == 1 || CIN == 2), "row producer envelope");
   if (lane >= kHaloH) return;
-  int b, y0, x0;
-  bool tok;
-  tile_origin(p, tile, b, y0, x0, tok);
+  const int b = tile.b, y0 = tile.y0, x0 = tile.x0;
+  const bool tok = tile.ok;
   const int yi = y0 + lane - p.pad;
   const bool rok = tok && yi >= 0 && yi < p.H;
   const int bit0 = (x0 - p.pad) * CIN;       // row bit of halo column 0 (-CIN with left padding)
@@ -848,11 +875,10 @@ __device__ __forceinline__ void produce_plane_rows(const TcParams &p, const uint
 }
 
 template <int K>
-__device__ __forceinline__ void produce_s32(const TcParams &p, const uint32_t *lut, int tile, int k,
+__device__ __forceinline__ void produce_s32(const TcParams &p, const uint32_t *lut, const TileXY &tile, int k,
                                             uint32_t a_stage, int ptid) {
-  int b, y0, x0;
-  bool tok;
-  tile_origin(p, tile, b, y0, x0, tok);
+  const int b = tile.b, y0 = tile.y0, x0 = tile.x0;
+  const bool tok = tile.ok;
   const uint32_t *frame0 = p.in + (long long)(k * K) * p.in_st + (long long)b * p.in_sb;
   for (int row = ptid; row < kHaloRows; row += p.prod_step) {
     const int hy = row / kHaloW, hx = row - (row / kHaloW) * kHaloW;
@@ -1169,10 +1195,10 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
   const int wptid = ws ? (int)lane : ptid;
   uint32_t it = 0;
   Ring st, rw;
-  for (int pair = cid; pair < p.num_pairs; pair += ncl) {
-    int b, y0, x0;
-    bool tok;
-    tile_origin(p, 2 * pair + (int)rank, b, y0, x0, tok);
+  TileWalk tw(p, 2 * cid + (int)rank, 2 * ncl);
+  for (int pair = cid; pair < p.num_pairs; pair += ncl, tw.step(p)) {
+    const TileXY tile = tw.at(p, 2 * pair + (int)rank);
+    const int x0 = tile.x0;
     for (int k = 0; k < p.G; ++k, ++it) {
       const uint32_t s = st.i, ph = st.ph, r = rw.i, rph = rw.ph;
       st.next(ns);
@@ -1185,7 +1211,6 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
       const uint32_t *raw = reinterpret_cast<const uint32_t *>(smem + p.off_raw + r * p.raw_stage_bytes);
       const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
       const uint32_t *lut = reinterpret_cast<const uint32_t *>(smem + p.off_lut);
-      const int tile = 2 * pair + (int)rank;
       if (p.use_tma == 2) {  // plane mode: whole frames in smem, pixel-wise producers read them
         if constexpr (PATH != PATH_HALO) {
           if constexpr (K == 0) {
@@ -1258,8 +1283,9 @@ __device__ __forceinline__ void producer_role(const TcParams &p, uint32_t sbase,
   if (ws) ptid = (int)lane;  // each warp builds whole stages (stage it -> warp it % 3)
   uint32_t it = 0;
   Ring st;
-  for (int pair = cid; pair < p.num_pairs; pair += ncl) {
-    const int tile = 2 * pair + (int)rank;
+  TileWalk tw(p, 2 * cid + (int)rank, 2 * ncl);
+  for (int pair = cid; pair < p.num_pairs; pair += ncl, tw.step(p)) {
+    const TileXY tile = tw.at(p, 2 * pair + (int)rank);
     for (int k = 0; k < p.G; ++k, ++it) {
       const uint32_t s = st.i, ph = st.ph;
       st.next(ns);
@@ -1487,11 +1513,11 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
   const uint32_t t_empty_remote = ptx::mapa_cluster(bar_t_empty, 0);  // CTA 0's TMEM-empty barriers
   uint32_t it = 0;
   Ring ar;
-  for (int pair = cid; pair < p.num_pairs; pair += ncl) {
+  TileWalk tw(p, 2 * cid + (int)rank, 2 * ncl);
+  for (int pair = cid; pair < p.num_pairs; pair += ncl, tw.step(p)) {
     const int tile = 2 * pair + (int)rank;
-    int b, y0, x0;
-    bool tok;
-    tile_origin(p, tile, b, y0, x0, tok);
+    const int b = tw.b, y0 = tw.ty * kTileH, x0 = tw.tx * kTileW;
+    const bool tok = tile < p.num_tiles;
     const int y = y0 + g, x = x0 + c;
     const bool valid = tok && y < p.Ho && x < p.Wo;
     const long long vbase = (((long long)b * p.Ho + y) * p.Wo + x) * Cout + co_base;
@@ -1503,33 +1529,128 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
     uint32_t *optr = p.out + (long long)b * p.out_sb + (long long)yo * p.wpr_out +
                      (NCH >= 32 ? (long long)xo * nwo + half : (obit >> 5));
     const int osh = NCH >= 32 ? 0 : (int)(obit & 31);
+    // pooled whole-word stores (scatter_pool): the 4 lanes of a 2x2 window share its
+    // stores -- lane (wb, wc) = (lane & 1, lane >> 3 & 1) stores the steps s with
+    // s % 4 == 2 wc + wb (NS >= 4; NS == 2: steps wb, lanes wc == 0)
+    constexpr bool SCAT = NCH >= 32 && NS >= 2;
+    const int wb = (int)(lane & 1), wc = (int)((lane >> 3) & 1);
+    bool store_w = store_lane;
+    if (SCAT && pooled) {
+      optr += (long long)(NS >= 4 ? 2 * wc + wb : wb) * out_st;
+      store_w = valid && active_half && yo < p.Hq && xo < p.Wq && (NS >= 4 || wc == 0);
+    }
     float2 U[UT ? 1 : NCH / 2];
     const uint32_t ucol = tmem_base + lane_addr + (uint32_t)p.naccs * p.n_total + (uint32_t)co_base;
+    if (p.v_init) {
 #pragma unroll
-    for (int ch = 0; ch < NCHUNK; ++ch) {
-      uint32_t ub[8];
+      for (int ch = 0; ch < NCHUNK; ++ch) {
+        uint32_t ub[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int cc = ch * 8 + q;
-        // V_0 = v_init, or 0 (U_0 = -v_th 2^e, a kernel constant: no per-tile loads)
-        float u0 = p.nvth_s;
-        if (p.v_init) {
+        for (int q = 0; q < 8; ++q) {
+          const int cc = ch * 8 + q;
           float v0 = 0.f;
           if (valid && co_base + cc < Cout) v0 = __ldg(p.v_init + vbase + cc);
-          u0 = (v0 - vth) * ysc;
+          const float u0 = (v0 - vth) * ysc;
+          ub[q] = __float_as_uint(u0);
+          if (!UT) {
+            if (q & 1) U[UT ? 0 : cc / 2].y = u0; else U[UT ? 0 : cc / 2].x = u0;
+          }
         }
-        ub[q] = __float_as_uint(u0);
+        if (UT) ptx::tmem_st8(ucol + ch * 8, ub);
+      }
+    } else {
+      // V_0 = 0: U_0 = -v_th 2^e, a kernel constant (no per-tile loads, one register)
+      const float u0 = p.nvth_s;
+      uint32_t ub[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) ub[q] = __float_as_uint(u0);
+#pragma unroll
+      for (int ch = 0; ch < NCHUNK; ++ch) {
+        if (UT) ptx::tmem_st8(ucol + ch * 8, ub);
         if (!UT) {
-          if (q & 1) U[UT ? 0 : cc / 2].y = u0; else U[UT ? 0 : cc / 2].x = u0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) U[UT ? 0 : ch * 4 + q] = make_float2(u0, u0);
         }
       }
-      if (UT) ptx::tmem_st8(ucol + ch * 8, ub);
     }
     if (UT) ptx::tmem_wait_st();
     uint32_t planes[kPlanes];
 #pragma unroll
     for (int pl = 0; pl < kPlanes; ++pl) planes[pl] = 0u;
     int steps_acc = 0;
+    // spike words of one group -> per-lane bit-sliced counters (pre-pool, valid pixels
+    // only; skipped when the caller asked for no counts), flushed before they overflow
+    auto count_group = [&](const uint32_t (&spk)[NS], int k) {
+      if (!p.counts) {
+      } else if (NS == 1) {
+        uint32_t cy = spk[0];
+#pragma unroll
+        for (int pl = 0; pl < kPlanes; ++pl) {
+          const uint32_t t = planes[pl] & cy;
+          planes[pl] ^= cy;
+          cy = t;
+        }
+      } else if (NS == 2) {
+        planes_add3(planes, spk[0] ^ spk[NS - 1], spk[0] & spk[NS - 1], 0u);
+      } else {
+#pragma unroll
+        for (int j = 0; j + 3 < NS; j += 4) planes_add4(planes, spk[j], spk[j + 1], spk[j + 2], spk[j + 3]);
+      }
+      steps_acc += NS;
+      if (p.counts && (steps_acc + NS > (1 << kPlanes) - 1 || k == G - 1)) {
+        if (tok) {
+          uint32_t pw[kPlanes][1];
+#pragma unroll
+          for (int pl = 0; pl < kPlanes; ++pl) pw[pl][0] = planes[pl];
+          flush_counts<1>(p, pw, b, co_base, NCH, lane);
+        }
+#pragma unroll
+        for (int pl = 0; pl < kPlanes; ++pl) planes[pl] = 0u;
+        steps_acc = 0;
+      }
+    };
+    // in-warp 2x2 OR-pool (all shuffles first), then branch-free packed stores of the
+    // group's output steps
+    auto pool_store = [&](const uint32_t (&spk)[NS]) {
+      if constexpr (SCAT) if (pooled) {
+        // reduce-scatter OR over the window: xor-1 partner keeps the other step parity,
+        // xor-8 partner the other step pair -- NS/2 + NS/4 shuffles, NS/4 stores per lane
+        uint32_t a[NS / 2 > 0 ? NS / 2 : 1];
+#pragma unroll
+        for (int i = 0; i < NS / 2; ++i) {
+          const uint32_t send = wb ? spk[2 * i] : spk[2 * i + 1];
+          const uint32_t keep = wb ? spk[2 * i + 1] : spk[2 * i];
+          a[i] = keep | __shfl_xor_sync(0xFFFFFFFFu, send, 1);  // step 2 i + wb
+        }
+        if constexpr (NS == 2) {
+          ptx::st_global_pred(optr, a[0] | __shfl_xor_sync(0xFFFFFFFFu, a[0], 8), store_w);
+        } else {
+#pragma unroll
+          for (int i = 0; i < NS / 4; ++i) {
+            const uint32_t send = wc ? a[2 * i] : a[2 * i + 1];
+            const uint32_t keep = wc ? a[2 * i + 1] : a[2 * i];
+            ptx::st_global_pred(optr + (long long)(4 * i) * out_st,
+                                keep | __shfl_xor_sync(0xFFFFFFFFu, send, 8), store_w);  // step 4 i + 2 wc + wb
+          }
+        }
+        optr += (long long)NS * out_st;
+        return;
+      }
+      uint32_t pw[NS];
+#pragma unroll
+      for (int j = 0; j < NS; ++j) pw[j] = spk[j] | (pooled ? __shfl_xor_sync(0xFFFFFFFFu, spk[j], 1) : 0u);
+#pragma unroll
+      for (int j = 0; j < NS; ++j) pw[j] |= pooled ? __shfl_xor_sync(0xFFFFFFFFu, pw[j], 8) : 0u;
+#pragma unroll
+      for (int j = 0; j < NS; ++j) {  // one 64-bit pointer step per stored word
+        if (NCH >= 32) {
+          ptx::st_global_pred(optr, pw[j], store_lane);
+        } else if (store_lane && pw[j]) {
+          atomicOr(optr, pw[j] << osh);
+        }
+        optr += out_st;
+      }
+    };
     for (int k = 0; k < G; ++k, ++it) {
       const uint32_t acc = ar.i, aph = ar.ph;
       ar.next((uint32_t)p.naccs);
@@ -1639,51 +1760,8 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
       uint32_t spk[NS];
 #pragma unroll
       for (int j = 0; j < NS; ++j) TAC_LOP3(spk[j], nsp[j], vmask, vmask, 0x0C);  // ~nsp & vmask, one LOP3
-      // per-lane bit-sliced spike counters (pre-pool, valid pixels only; skipped when
-      // the caller asked for no counts)
-      if (!p.counts) {
-      } else if (NS == 1) {
-        uint32_t cy = spk[0];
-#pragma unroll
-        for (int pl = 0; pl < kPlanes; ++pl) {
-          const uint32_t t = planes[pl] & cy;
-          planes[pl] ^= cy;
-          cy = t;
-        }
-      } else if (NS == 2) {
-        planes_add3(planes, spk[0] ^ spk[NS - 1], spk[0] & spk[NS - 1], 0u);
-      } else {
-#pragma unroll
-        for (int j = 0; j + 3 < NS; j += 4) planes_add4(planes, spk[j], spk[j + 1], spk[j + 2], spk[j + 3]);
-      }
-      // in-warp 2x2 OR-pool (all shuffles first), then branch-free packed stores of
-      // output steps t = k NS + j
-      uint32_t pw[NS];
-#pragma unroll
-      for (int j = 0; j < NS; ++j) pw[j] = spk[j] | (pooled ? __shfl_xor_sync(0xFFFFFFFFu, spk[j], 1) : 0u);
-#pragma unroll
-      for (int j = 0; j < NS; ++j) pw[j] |= pooled ? __shfl_xor_sync(0xFFFFFFFFu, pw[j], 8) : 0u;
-#pragma unroll
-      for (int j = 0; j < NS; ++j) {  // one 64-bit pointer step per stored word
-        if (NCH >= 32) {
-          ptx::st_global_pred(optr, pw[j], store_lane);
-        } else if (store_lane && pw[j]) {
-          atomicOr(optr, pw[j] << osh);
-        }
-        optr += out_st;
-      }
-      steps_acc += NS;
-      if (p.counts && (steps_acc + NS > (1 << kPlanes) - 1 || k == G - 1)) {
-        if (tok) {
-          uint32_t pw[kPlanes][1];
-#pragma unroll
-          for (int pl = 0; pl < kPlanes; ++pl) pw[pl][0] = planes[pl];
-          flush_counts<1>(p, pw, b, co_base, NCH, lane);
-        }
-#pragma unroll
-        for (int pl = 0; pl < kPlanes; ++pl) planes[pl] = 0u;
-        steps_acc = 0;
-      }
+      pool_store(spk);  // output steps t = k NS + j
+      count_group(spk, k);
       if (e == 0 && lane == 0) trace_mark(p, it, TR_EPI_DONE);
     }
     if (p.v_final) {
@@ -1739,11 +1817,11 @@ __device__ __forceinline__ void epilogue_generic(const TcParams &p, uint8_t *sme
   const bool active_half = co_base < Cout;
   uint32_t it = 0;
   Ring ar;
-  for (int pair = cid; pair < p.num_pairs; pair += ncl) {
-    const int tile = 2 * pair + (int)rank;
-    int b, y0, x0;
-    bool tok;
-    tile_origin(p, tile, b, y0, x0, tok);
+  TileWalk tw(p, 2 * cid + (int)rank, 2 * ncl);
+  for (int pair = cid; pair < p.num_pairs; pair += ncl, tw.step(p)) {
+    const TileXY tile = tw.at(p, 2 * pair + (int)rank);
+    const int b = tile.b, y0 = tile.y0, x0 = tile.x0;
+    const bool tok = tile.ok;
     const int y = y0 + g, x = x0 + c;
     const bool valid = tok && y < p.Ho && x < p.Wo;
     const long long vbase = (((long long)b * p.Ho + y) * p.Wo + x) * Cout + co_base;
