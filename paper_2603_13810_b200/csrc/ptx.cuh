@@ -64,6 +64,24 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       : "memory");
 #endif
 }
+// wait for a phase the caller is usually far ahead of (producers waiting for a free A
+// stage, the MMA issuer waiting for a free accumulator): poll, then sleep `ns` between
+// polls.  A try_wait with a suspend hint (mbar_wait) wakes on every barrier event of the
+// CTA -- measured ~94 wake-ups per group on C5 L0, 4 % of all issued instructions,
+// taken from the epilogue warps on the same SM sub-partitions.
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, uint32_t ns) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra TAC_SDONE_%=;\n"
+      "TAC_SLEEP_%=:\n\t"
+      "nanosleep.u32 %2;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra TAC_SLEEP_%=;\n"
+      "TAC_SDONE_%=:\n}" ::"r"(bar),
+      "r"(parity), "r"(ns)
+      : "memory");
+}
 // arrive (release at CTA scope, like CUTLASS's ClusterBarrier::arrive(cta)) on the
 // barrier at this smem offset in CTA `cta`: no GPU-scope MEMBAR in the producer path
 __device__ __forceinline__ void mbar_arrive_cluster_cta(uint32_t bar, uint32_t cta) {

@@ -68,6 +68,8 @@ struct TcParams {
   int prod_refill;            // 1 (plane mode + warp_stage): the warp that consumed raw slot r refills it
   int occ;                    // CTA pairs per SM pair (1, or 2 for small first layers: OCC kernels)
   int c32w;                   // fp16 path, C_out 32: 4 epilogue warps x 32 channels (no atomic sub-word stores)
+  int sleep_ns;               // > 0: producers / MMA issuer poll their "free slot" barriers with
+                              // nanosleep backoff (mbar_wait_sleep) instead of suspend-hint waits
   int prod_step;              // halo-row stride of the pixel-wise producers: 96, or 32 with warp_stage
   uint32_t off_raw, raw_stage_bytes, raw_box_bytes;
   int B, H, W, Cin, Cout, Cout_pad, pad, Ho, Wo, pool;
@@ -399,6 +401,14 @@ struct TileWalk {
     b += db + cy;
   }
 };
+
+// wait used by roles that normally run ahead of the epilogue (see ptx::mbar_wait_sleep)
+__device__ __forceinline__ void wait_ahead(const TcParams &p, uint32_t bar, uint32_t parity) {
+  if (p.sleep_ns > 0)
+    ptx::mbar_wait_sleep(bar, parity, (uint32_t)p.sleep_ns);
+  else
+    ptx::mbar_wait(bar, parity);
+}
 
 // circular-buffer position (slot, phase parity) advanced by one per use: no integer
 // division by the runtime ring sizes in the role loops
@@ -1149,7 +1159,7 @@ struct RawLoader {
                                          uint32_t bar_raw_empty, uint32_t it, int ncl) {
     (void)it;  // refills come in consumption order: rel tracks it % nraw and its phase
     if (!more(p)) return;
-    ptx::mbar_wait(bar_raw_empty + 8 * rel.i, rel.ph);
+    wait_ahead(p, bar_raw_empty + 8 * rel.i, rel.ph);
     rel.next((uint32_t)p.nraw);
     issue(p, sbase, bar_raw, ncl);
   }
@@ -1204,9 +1214,9 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
       st.next(ns);
       rw.next(nr);
       if (ws && it % kProdWarps != pw) continue;  // another producer warp builds this stage
-      ptx::mbar_wait(bar_raw + 8 * r, rph);
+      wait_ahead(p, bar_raw + 8 * r, rph);
       if (wptid == 0) trace_mark(p, it, TR_PROD_RAW);
-      ptx::mbar_wait(bar_a_empty + 8 * s, ph ^ 1u);
+      wait_ahead(p, bar_a_empty + 8 * s, ph ^ 1u);
       if (wptid == 0) trace_mark(p, it, TR_PROD_START);
       const uint32_t *raw = reinterpret_cast<const uint32_t *>(smem + p.off_raw + r * p.raw_stage_bytes);
       const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
@@ -1290,7 +1300,7 @@ __device__ __forceinline__ void producer_role(const TcParams &p, uint32_t sbase,
       const uint32_t s = st.i, ph = st.ph;
       st.next(ns);
       if (ws && it % kProdWarps != pw) continue;
-      ptx::mbar_wait(bar_a_empty + 8 * s, ph ^ 1u);
+      wait_ahead(p, bar_a_empty + 8 * s, ph ^ 1u);
       const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
       if (PATH == PATH_SPLIT && p.real) {
         p.Cin == 1 ? produce_h16x<K, 1>(p, tile, k, a_stage, ptid) : produce_h16x<K, 2>(p, tile, k, a_stage, ptid);
@@ -1581,8 +1591,8 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
     // spike words of one group -> per-lane bit-sliced counters (pre-pool, valid pixels
     // only; skipped when the caller asked for no counts), flushed before they overflow
     auto count_group = [&](const uint32_t (&spk)[NS], int k) {
-      if (!p.counts) {
-      } else if (NS == 1) {
+      if (!p.counts) return;  // one uniform branch per group when no counts are asked for
+      if (NS == 1) {
         uint32_t cy = spk[0];
 #pragma unroll
         for (int pl = 0; pl < kPlanes; ++pl) {
@@ -1597,7 +1607,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
         for (int j = 0; j + 3 < NS; j += 4) planes_add4(planes, spk[j], spk[j + 1], spk[j + 2], spk[j + 3]);
       }
       steps_acc += NS;
-      if (p.counts && (steps_acc + NS > (1 << kPlanes) - 1 || k == G - 1)) {
+      if (steps_acc + NS > (1 << kPlanes) - 1 || k == G - 1) {
         if (tok) {
           uint32_t pw[kPlanes][1];
 #pragma unroll
@@ -2132,7 +2142,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
             __syncwarp();
             if (lane == 0) trace_mark(p, it, TR_MMA_REFILLED);
 #endif
-            ptx::mbar_wait(bar_t_empty + 8 * acc, aph ^ 1u);
+            wait_ahead(p, bar_t_empty + 8 * acc, aph ^ 1u);
             ptx::tc_fence_after();
             if (lane == 0) trace_mark(p, it, TR_MMA_READY);
             const uint64_t a_base = a_desc0 + (uint64_t)(s * stage16);
