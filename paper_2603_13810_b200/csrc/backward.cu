@@ -52,10 +52,10 @@ __device__ __forceinline__ float surrogate(int kind, float a, float u) {
   return 0.5f * a / fmaf(z, z, 1.f);
 }
 
-__device__ __forceinline__ float sat_spike(float u) {  // same instruction as the tcgen05 epilogue
-  float f;
-  asm("fma.rn.ftz.sat.f32 %0, %1, 0f7F000000, 0f3F800000;" : "=f"(f) : "f"(u));
-  return f;
+__device__ __forceinline__ float sat_nospike(float u) {  // same instruction as the tcgen05 epilogue
+  float g;
+  asm("mul.rn.ftz.sat.f32 %0, %1, 0fFF000000;" : "=f"(g) : "f"(u));
+  return g;
 }
 
 __global__ void __launch_bounds__(128) lif_bwd_kernel(const BwdParams p) {
@@ -68,14 +68,14 @@ __global__ void __launch_bounds__(128) lif_bwd_kernel(const BwdParams p) {
   float um[kMaxBwdSteps];  // V_t - v_th (unscaled) of every step
   // forward replay
   float st = p.v_init ? __ldg(p.v_init + n) : 0.f;
-  st = p.udomain ? (st - vth) * ysc : st * ysc;
+  st = st * ysc;
   for (int k = 0; k < G; ++k) {
     const float y = __ldg(p.y_seq + (long long)k * N + n);
     for (int j = 0; j < nsteps; ++j) {
       float pre;
-      if (p.udomain) {  // epilogue_sr: U <- d U + Y'; spike = sign(U); U <- U - v_th f
+      if (p.udomain) {  // epilogue_sr: U <- d V + Y''; spike = sign(U); V <- U + v_th [U < 0]
         pre = fmaf(d, st, y);
-        st = fmaf(-vths, sat_spike(pre), pre);
+        st = fmaf(sat_nospike(pre), vths, pre);
         um[k * nsteps + j] = pre * iysc;
       } else {  // epilogue_generic / SIMT: V <- d V + Y; spike = V >= v_th; V <- V - v_th
         const float v = fmaf(d, st, y);

@@ -36,18 +36,14 @@ const char *tc_unsupported_reason(const tac_conv_lif_desc *d) {
   return r ? r : "supported";
 }
 
-// The specialised subtract-reset epilogue (NS > 0) runs in U = V - v_th and needs
-// the drive Y' = Y + (decay - 1) v_th: the offset is folded into the prepared bias
-// (per-step decay = beta^K for TAC, beta otherwise, as abi.cu computes it).
+// The specialised subtract-reset epilogue (NS > 0) integrates U = decay V + Y'' with the
+// drive Y'' = Y - v_th: the offset is folded into the prepared bias.
 static bool lif_u_state(const tac_conv_lif_desc *d) {
   const int ns = d->mode == TAC_MODE_TACTP ? d->K : 1;
   return d->reset == TAC_RESET_SUBTRACT && (ns == 1 || ns == 2 || ns == 4 || ns == 8);
 }
 static double lif_bias_offset(const tac_conv_lif_desc *d) {
-  if (!lif_u_state(d)) return 0.0;
-  const int K = d->mode == TAC_MODE_DENSE ? 1 : d->K;
-  const float decay = (float)(d->mode == TAC_MODE_TAC ? std::pow((double)d->beta, (double)K) : d->beta);
-  return ((double)decay - 1.0) * (double)d->v_th;
+  return lif_u_state(d) ? -(double)d->v_th : 0.0;
 }
 
 // Image: [slice 0 | slice 1 | fp32 [s1/254 | bias | s1 | s2] x C_out_pad | fp32 yscale [4] |
@@ -339,7 +335,7 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   p.lut_g = reinterpret_cast<const uint32_t *>(tc_prep + lut_off(g));  // split: prepared tables
   p.ysc = (float)std::ldexp(1.0, g.path == PATH_HALO ? 0 : lp.yscale_exp);  // the plan's prescale
   p.iysc = (float)std::ldexp(1.0, g.path == PATH_HALO ? 0 : -lp.yscale_exp);
-  p.nvth_s = -lp.v_th * p.ysc;
+  p.vth_s = lp.v_th * p.ysc;
   p.wpr_in = lp.wpr_in; p.wpr_out = lp.wpr_out;
   p.nwo = lp.Cout % 32 == 0 ? lp.Cout / 32 : 1;
   static const bool no_c32w = [] { const char *e = std::getenv("TACSNN_NO_C32W"); return e && *e == '1'; }();

@@ -100,7 +100,7 @@ struct TcParams {
   const float *scale_bias;
   float ysc, iysc;            // fp16 paths: the Y prescale 2^e and 2^-e (tc_prepare; host-side
                               // from the plan); 1 on int8
-  float nvth_s;               // -v_th 2^e, precomputed so the reset FFMA2 reads it from the
+  float vth_s;                // v_th 2^e, precomputed so the reset FFMA2 reads it from the
                               // constant bank (no per-thread register, no FMUL)
   float *y_seq;               // training forward: per-group drive [G][B][Ho][Wo][Cout] (or NULL)
   long long yseq_plane;       // B * Ho * Wo * Cout
@@ -1458,29 +1458,38 @@ __device__ __forceinline__ void planes_add4(uint32_t *P, uint32_t s0, uint32_t s
 }
 
 // --- specialised subtract-reset epilogue (NS LIF steps per group) -------------
-// State U = V - v_th (drive Y' = Y + (decay - 1) v_th, folded into the bias):
-//   U <- decay U + Y'                      FFMA2 (two neurons)
+// State V (membrane after reset); the drive Y'' = Y - v_th is folded into the bias, so
+// one FFMA2 gives U = V_pre - v_th directly:
+//   U <- decay V + Y''                     FFMA2 (two neurons)
 //   no-spike bit = sign(U)  -> shift register  nsp = (nsp << 1) | (U >> 31)   SHF
-//   f = sat(U 2^127 + 1) = [U >= 0]        FFMA.SAT (exactly 0 or 1, ftz)
-//   U <- U - v_th f                        FFMA2 (exact for f in {0, 1})
+//   g = sat(-2^127 U) = [U < 0]            FMUL.SAT with an immediate: one register read
+//   V <- U + v_th g                        FFMA2 (no spike: V_pre; spike: V_pre - v_th)
 // Channels are visited from the highest to the lowest so that channel c of the
 // thread's word lands at bit c after NCH shifts: no per-bit masks, no folding.
-// (U = -0 would be a tie V == v_th read as "no spike" by the sign but reset by
-// f; U = V - v_th is never -0 in round-to-nearest unless both addends are -0.)
+// (U = -0 would be a tie V == v_th read as "no spike" by the sign but reset by g;
+// U = decay V + Y'' is never -0 in round-to-nearest unless both addends are -0, and
+// V = U + v_th g is -0 only for v_init = -0 while Y'' = Y - v_th is never -0.)
 __device__ __forceinline__ uint32_t shreg(uint32_t acc, float u) {
   return __funnelshift_l(__float_as_uint(u), acc, 1);  // (acc << 1) | sign(u)
 }
 
+// g = [u < 0] = sat(-2^127 u): exactly 0 or 1 for every u (ftz)
+__device__ __forceinline__ float sat_nospike(float u) {
+  float g;
+  asm("mul.rn.ftz.sat.f32 %0, %1, 0fFF000000;" : "=f"(g) : "f"(u));
+  return g;
+}
+
 template <int NS>
-__device__ __forceinline__ void lif_pair_sr(float2 &u, float2 y, float2 dec2, float2 nth2,
+__device__ __forceinline__ void lif_pair_sr(float2 &v, float2 y, float2 dec2, float2 th2,
                                             uint32_t (&nsp)[NS]) {
 #pragma unroll
   for (int j = 0; j < NS; ++j) {
-    u = __ffma2_rn(dec2, u, y);
+    const float2 u = __ffma2_rn(dec2, v, y);
     nsp[j] = shreg(nsp[j], u.y);
     nsp[j] = shreg(nsp[j], u.x);
-    const float2 f = make_float2(sat_spike(u.x), sat_spike(u.y));
-    u = __ffma2_rn(f, nth2, u);  // scalar -v_th in the operand slot that takes a constant
+    const float2 g = make_float2(sat_nospike(u.x), sat_nospike(u.y));
+    v = __ffma2_rn(g, th2, u);  // scalar v_th in the operand slot that takes a constant
   }
 }
 
@@ -1512,8 +1521,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
   // the scaled state U 2^e with threshold v_th 2^e -- power-of-two scaling commutes with
   // every fp32 rounding, so spikes and membranes are bitwise those of the unscaled update
   const float ysc = p.ysc, iysc = p.iysc;
-  const float vth = p.v_th;
-  const float2 dec2 = make_float2(p.decay, p.decay), nth2 = make_float2(p.nvth_s, p.nvth_s);
+  const float2 dec2 = make_float2(p.decay, p.decay), th2 = make_float2(p.vth_s, p.vth_s);
   const int G = p.G, Cout = p.Cout, nwo = p.nwo;
   const long long out_st = p.out_st;
   const uint32_t chmask = NCH >= 32 ? 0xFFFFFFFFu : ((1u << NCH) - 1u);
@@ -1560,7 +1568,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
           const int cc = ch * 8 + q;
           float v0 = 0.f;
           if (valid && co_base + cc < Cout) v0 = __ldg(p.v_init + vbase + cc);
-          const float u0 = (v0 - vth) * ysc;
+          const float u0 = v0 * ysc;
           ub[q] = __float_as_uint(u0);
           if (!UT) {
             if (q & 1) U[UT ? 0 : cc / 2].y = u0; else U[UT ? 0 : cc / 2].x = u0;
@@ -1569,8 +1577,8 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
         if (UT) ptx::tmem_st8(ucol + ch * 8, ub);
       }
     } else {
-      // V_0 = 0: U_0 = -v_th 2^e, a kernel constant (no per-tile loads, one register)
-      const float u0 = p.nvth_s;
+      // V_0 = 0 (no per-tile loads)
+      const float u0 = 0.f;
       uint32_t ub[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) ub[q] = __float_as_uint(u0);
@@ -1688,7 +1696,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
           for (int q = 3; q >= 0; --q) {
             float2 u = make_float2(__uint_as_float(du[cur][2 * q]), __uint_as_float(du[cur][2 * q + 1]));
             lif_pair_sr<NS>(u, make_float2(__uint_as_float(dy[cur][2 * q]), __uint_as_float(dy[cur][2 * q + 1])),
-                            dec2, nth2, nsp);
+                            dec2, th2, nsp);
             du[cur][2 * q] = __float_as_uint(u.x);
             du[cur][2 * q + 1] = __float_as_uint(u.y);
           }
@@ -1714,7 +1722,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
           for (int q = 3; q >= 0; --q) {
             float2 u = make_float2(__uint_as_float(du[2 * q]), __uint_as_float(du[2 * q + 1]));
             lif_pair_sr<NS>(u, make_float2(__uint_as_float(dy[2 * q]), __uint_as_float(dy[2 * q + 1])),
-                            dec2, nth2, nsp);
+                            dec2, th2, nsp);
             du[2 * q] = __float_as_uint(u.x);
             du[2 * q + 1] = __float_as_uint(u.y);
           }
@@ -1748,7 +1756,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
           }
 #pragma unroll
           for (int q = 3; q >= 0; --q)
-            lif_pair_sr<NS>(U[UT ? 0 : ch * 4 + q], make_float2(yv[2 * q], yv[2 * q + 1]), dec2, nth2, nsp);
+            lif_pair_sr<NS>(U[UT ? 0 : ch * 4 + q], make_float2(yv[2 * q], yv[2 * q + 1]), dec2, th2, nsp);
           if (TRAIN && valid && active_half) store_yseq8(p, k, vbase, ch * 8, Cout - co_base - ch * 8, yv);
           if (ch > 0) {
             if (NBUF == 1) {
@@ -1792,7 +1800,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
         if (valid) {
 #pragma unroll
           for (int q = 0; q < 8; ++q)
-            if (co_base + ch * 8 + q < Cout) p.v_final[vbase + ch * 8 + q] = __uint_as_float(du[q]) * iysc + vth;
+            if (co_base + ch * 8 + q < Cout) p.v_final[vbase + ch * 8 + q] = __uint_as_float(du[q]) * iysc;
         }
       }
     }

@@ -127,6 +127,18 @@ template <int C0> __device__ __forceinline__ void v10(float2 &u, float2 y, float
   u.x = fmaf(nth2.x, f0, u.x); u.y = fmaf(nth2.x, f1, u.y);
 }
 
+// variant 11: as v7, but the flag is g = [U < 0] = sat(-2^127 U) (FMUL.SAT, one register
+// read; the reset becomes P = U + th g with -th folded into the drive)
+__device__ __forceinline__ float sat_neg(float u) {
+  float g; asm("mul.rn.ftz.sat.f32 %0, %1, 0fFF000000;" : "=f"(g) : "f"(u)); return g;
+}
+template <int C0> __device__ __forceinline__ void v11(float2 &u, float2 y, float2 dec2, float2 nth2, uint32_t &acc) {
+  u = __ffma2_rn(dec2, u, y);
+  acc = shreg(acc, u.x); acc = shreg(acc, u.y);
+  const float2 g = make_float2(sat_neg(u.x), sat_neg(u.y));
+  u = __ffma2_rn(nth2, g, u);
+}
+
 template <int V>
 #ifndef NP
 #define NP 16  // neuron pairs per thread
@@ -202,6 +214,12 @@ __global__ void __launch_bounds__(THREADS, 1) bench(const float *ys, uint32_t *s
             CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15)
 #undef CASE
           }
+        } else if (V == 11) {
+          switch (c % 16) {
+#define CASE(k) case k: v11<(2 * k) % 32>(u[c], y, dec2, nth2, w[j]); break;
+            CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15)
+#undef CASE
+          }
         } else if (V == 10) {
           switch (c % 16) {
 #define CASE(k) case k: v10<(2 * k) % 32>(u[c], y, dec2, nth2, w[j]); break;
@@ -237,7 +255,7 @@ int main() {
   cudaMalloc(&ys, 32 * 32 * 4 * 8); cudaMalloc(&sink, blocks * threads * 4); cudaMalloc(&cyc, blocks * 8);
   static float h[8192]; for (int i = 0; i < 8192; ++i) h[i] = 0.05f + 0.3f * ((i * 37) % 101) / 101.f;
   cudaMemcpy(ys, h, sizeof h, cudaMemcpyHostToDevice);
-  for (int v = 0; v < 11; ++v) {
+  for (int v = 0; v < 12; ++v) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
       cudaEventRecord(a);
@@ -247,6 +265,7 @@ int main() {
       if (v == 3) bench<3><<<blocks, threads>>>(ys, sink, groups, cyc, 0.9f, 1.f);
       if (v == 4) bench<4><<<blocks, threads>>>(ys, sink, groups, cyc, 0.9f, 1.f);
       if (v == 6) bench<6><<<blocks, threads>>>(ys, sink, groups, cyc, 0.9f, 1.f);
+      if (v == 11) bench<11><<<blocks, threads>>>(ys, sink, groups, cyc, 0.9f, 1.f);
       if (v == 10) bench<10><<<blocks, threads>>>(ys, sink, groups, cyc, 0.9f, 1.f);
       if (v == 7) bench<7><<<blocks, threads>>>(ys, sink, groups, cyc, 0.9f, 1.f);
       if (v == 8) bench<8><<<blocks, threads>>>(ys, sink, groups, cyc, 0.9f, 1.f);
