@@ -149,7 +149,19 @@ constexpr int kUtUnroll = TACSNN_UT_UNROLL;
 // higher warp ids, so the warps feeding the tensor pipe (MMA, producers) win
 // issue slots over the 16 compute-heavy epilogue warps.
 constexpr int epi_warps(int npart) { return 4 * npart; }
-constexpr int kernel_threads(int npart) { return 32 * (1 + kProdWarps + epi_warps(npart)); }
+// OCC = 2 kernels with 4 epilogue warps (the rate-coded first layers, C_out 32) carry 2
+// more producer warps: their row producer builds a whole A stage in one warp and limits
+// the group period (scripts/trace_layer.py: 1.6 us per stage, 0.67 us per group), so 5
+// warps rotating the stages keep more of them in flight (C3 L1 TAC K=8 75.7 -> 72.4 us,
+// C2 L1 -3 %; 4 extra warps cap the registers at 80 and gain nothing).  The extra warps only
+// join the one-warp-per-stage (warp_stage) producers; the pixel-wise producers use 3.
+#ifndef TACSNN_EXTRA_PW
+#define TACSNN_EXTRA_PW 2
+#endif
+constexpr int extra_prod_warps(int npart, int occ) { return (npart == 1 && occ == 2) ? TACSNN_EXTRA_PW : 0; }
+constexpr int kernel_threads(int npart, int occ = 1) {
+  return 32 * (1 + kProdWarps + extra_prod_warps(npart, occ) + epi_warps(npart));
+}
 // A stages / TMEM accumulators: 3 / 2 (int8), 3 / 3 (fp16, C_out 128); the small first
 // layers (pixel-wise producers, C_out <= 64) run deeper rings -- their per-group work is
 // short, so the producer -> MMA -> epilogue round trip, not any role's busy time, sets
@@ -808,16 +820,40 @@ __device__ __forceinline__ void produce_h16s_rt(const TcParams &p, const uint32_
 // row is constant (h16_init_stages), so only chunk 0 is stored.
 __device__ __forceinline__ int halo_c0(const TcParams &p, int x0);
 // v[j]: frame j's bits of halo row `lane`, halo column 0 at bit 0 -> the row's 10 A rows
+// 8 x 8 bit-matrix transpose of a 64-bit word (bit 8 i + j <-> bit 8 j + i): three
+// delta swaps (Hacker's Delight 7-3) instead of 8 K shift / mask / or steps
+__device__ __forceinline__ uint64_t transpose8x8(uint64_t x) {
+  uint64_t t;
+  t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
+  x = x ^ t ^ (t << 7);
+  t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull;
+  x = x ^ t ^ (t << 14);
+  t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
+  return x ^ t ^ (t << 28);
+}
+
 template <int K, int CIN, bool SPLIT>
 __device__ __forceinline__ void emit_halo_row(const TcParams &p, const uint32_t *lut, uint32_t a_stage,
                                               int lane, const uint32_t (&v)[K]) {
-  uint32_t o[8];
+  // X[b]: byte j = byte b of frame j's row bits -> transposed: byte q = the K-bit frame
+  // index of row bit 8 b + q
+  constexpr int NB = (kHaloW * CIN + 7) / 8;
+  uint64_t X[NB];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    uint32_t t = 0;
-#pragma unroll
-    for (int j = 0; j < K; ++j) t |= ((v[j] >> q) & 0x01010101u) << j;
-    o[q] = t;
+  for (int bb = 0; bb < NB; ++bb) {
+    const uint32_t sel = (uint32_t)bb | ((uint32_t)(4 + bb) << 4);  // byte bb of x, byte bb of y
+    uint32_t lo = 0u, hi = 0u;
+    if (K >= 2) lo = __byte_perm(v[0], v[K >= 2 ? 1 : 0], sel);
+    else lo = (v[0] >> (8 * bb)) & 0xFFu;
+    if (K >= 4) lo = __byte_perm(lo, __byte_perm(v[K >= 4 ? 2 : 0], v[K >= 4 ? 3 : 0], sel), 0x5410u);
+    else if (K == 3) lo = __byte_perm(lo, (v[K == 3 ? 2 : 0] >> (8 * bb)) & 0xFFu, 0x5410u);
+    else lo &= 0xFFFFu;
+    if (K >= 6) hi = __byte_perm(v[K >= 6 ? 4 : 0], v[K >= 6 ? 5 : 0], sel);
+    else if (K == 5) hi = (v[K == 5 ? 4 : 0] >> (8 * bb)) & 0xFFu;
+    if (K == 8) hi = __byte_perm(hi, __byte_perm(v[K == 8 ? 6 : 0], v[K == 8 ? 7 : 0], sel), 0x5410u);
+    else if (K == 7) hi = __byte_perm(hi, (v[K == 7 ? 6 : 0] >> (8 * bb)) & 0xFFu, 0x5410u);
+    else if (K == 6) hi &= 0xFFFFu;
+    X[bb] = transpose8x8(((uint64_t)hi << 32) | lo);
   }
   uint32_t one_lo, one_hi, c8;
   h16_bias_slot(CIN, one_lo, one_hi, c8);
@@ -828,7 +864,7 @@ __device__ __forceinline__ void emit_halo_row(const TcParams &p, const uint32_t 
 #pragma unroll
     for (int ch = 0; ch < CIN; ++ch) {
       const int bp = c * CIN + ch;            // compile-time
-      idx[ch] = (o[bp & 7] >> (8 * (bp >> 3))) & 0xFFu;
+      idx[ch] = (uint32_t)(X[bp >> 3] >> (8 * (bp & 7))) & 0xFFu;
     }
     if constexpr (SPLIT) {
       const uint4 w = split_row_words<CIN>(lut[idx[0]], CIN == 2 ? lut[idx[CIN - 1]] : 0u, p.packed);
@@ -1193,13 +1229,15 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
                                                   const uint8_t *smem, uint32_t bar_a_full,
                                                   uint32_t bar_a_empty, uint32_t bar_raw,
                                                   uint32_t bar_raw_empty, int cid, int ncl,
-                                                  uint32_t rank, uint32_t lane, int ptid) {
+                                                  uint32_t rank, uint32_t lane, int ptid, int npw) {
   const uint32_t ns = (uint32_t)p.nstages, nr = (uint32_t)p.nraw;
-  if (PATH != PATH_HALO) h16_init_stages(p, sbase, ptid);  // fenced with the first stage
   const bool ws = p.warp_stage != 0;
+  if (!ws) npw = kProdWarps;
+  if (ptid >= 32 * npw) return;  // extra producer warps: warp_stage producers only
+  if (PATH != PATH_HALO && ptid < 32 * kProdWarps) h16_init_stages(p, sbase, ptid);  // fenced with the first stage
   if (ws) {  // every producer warp's init writes are visible before any warp's first stage
     ptx::fence_proxy_async_smem();
-    ptx::named_bar_sync(1, 32 * kProdWarps);
+    ptx::named_bar_sync(1, 32 * npw);
   }
   const uint32_t pw = (uint32_t)ptid >> 5;
   const int wptid = ws ? (int)lane : ptid;
@@ -1213,7 +1251,7 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
       const uint32_t s = st.i, ph = st.ph, r = rw.i, rph = rw.ph;
       st.next(ns);
       rw.next(nr);
-      if (ws && it % kProdWarps != pw) continue;  // another producer warp builds this stage
+      if (ws && it % (uint32_t)npw != pw) continue;  // another producer warp builds this stage
       wait_ahead(p, bar_raw + 8 * r, rph);
       if (wptid == 0) trace_mark(p, it, TR_PROD_RAW);
       wait_ahead(p, bar_a_empty + 8 * s, ph ^ 1u);
@@ -1285,10 +1323,12 @@ __device__ __forceinline__ void producer_role_tma(const TcParams &p, uint32_t sb
 template <int PATH, int K>
 __device__ __forceinline__ void producer_role(const TcParams &p, uint32_t sbase, const uint8_t *smem,
                                               uint32_t bar_a_full, uint32_t bar_a_empty, int cid,
-                                              int ncl, uint32_t rank, uint32_t lane, int ptid) {
+                                              int ncl, uint32_t rank, uint32_t lane, int ptid, int npw) {
   const uint32_t *lut = reinterpret_cast<const uint32_t *>(smem + p.off_lut);
   const uint32_t ns = (uint32_t)p.nstages;
   const bool ws = p.warp_stage != 0;
+  if (!ws) npw = kProdWarps;
+  if (ptid >= 32 * npw) return;  // extra producer warps: warp_stage producers only
   const uint32_t pw = (uint32_t)ptid >> 5;
   if (ws) ptid = (int)lane;  // each warp builds whole stages (stage it -> warp it % 3)
   uint32_t it = 0;
@@ -1299,7 +1339,7 @@ __device__ __forceinline__ void producer_role(const TcParams &p, uint32_t sbase,
     for (int k = 0; k < p.G; ++k, ++it) {
       const uint32_t s = st.i, ph = st.ph;
       st.next(ns);
-      if (ws && it % kProdWarps != pw) continue;
+      if (ws && it % (uint32_t)npw != pw) continue;
       wait_ahead(p, bar_a_empty + 8 * s, ph ^ 1u);
       const uint32_t a_stage = sbase + p.off_a + s * p.a_stage_bytes;
       if (PATH == PATH_SPLIT && p.real) {
@@ -2029,9 +2069,10 @@ __device__ __forceinline__ void mma_group_h16(uint32_t d_tmem, uint64_t a_base, 
 // latency-bound, so a second independent pipeline per SM fills the idle issue slots);
 // the register budget is then 64 K / (2 x threads) per thread and no setmaxnreg.
 template <int NCH, int PATH, int NPART, bool TRAIN, int OCC = 1>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART), OCC)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART, OCC), OCC)
     tc_conv_lif_kernel(const __grid_constant__ TcParams p) {
-  constexpr int kThreads = kernel_threads(NPART);
+  constexpr int kThreads = kernel_threads(NPART, OCC);
+  constexpr int kNpw = kProdWarps + extra_prod_warps(NPART, OCC);
   constexpr int kEpiWarps = epi_warps(NPART);
   extern __shared__ __align__(1024) uint8_t smem[];
   // warp index broadcast from lane 0: the compiler then knows it is warp-uniform and keeps
@@ -2204,21 +2245,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
       const int ptid = (int)(threadIdx.x - 32 * (kMmaWarp + 1));
       if (p.use_tma) {
         switch (p.K) {
-          case 1: producer_role_tma<PATH, 1>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
-          case 2: producer_role_tma<PATH, 2>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
-          case 3: producer_role_tma<PATH, 3>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
-          case 4: producer_role_tma<PATH, 4>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
-          case 8: producer_role_tma<PATH, 8>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
-          default: producer_role_tma<PATH, 0>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid); break;
+          case 1: producer_role_tma<PATH, 1>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid, kNpw); break;
+          case 2: producer_role_tma<PATH, 2>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid, kNpw); break;
+          case 3: producer_role_tma<PATH, 3>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid, kNpw); break;
+          case 4: producer_role_tma<PATH, 4>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid, kNpw); break;
+          case 8: producer_role_tma<PATH, 8>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid, kNpw); break;
+          default: producer_role_tma<PATH, 0>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid, kNpw); break;
         }
       } else {
         switch (p.K) {
-          case 1: producer_role<PATH, 1>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
-          case 2: producer_role<PATH, 2>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
-          case 3: producer_role<PATH, 3>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
-          case 4: producer_role<PATH, 4>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
-          case 8: producer_role<PATH, 8>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
-          default: producer_role<PATH, 0>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid); break;
+          case 1: producer_role<PATH, 1>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid, kNpw); break;
+          case 2: producer_role<PATH, 2>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid, kNpw); break;
+          case 3: producer_role<PATH, 3>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid, kNpw); break;
+          case 4: producer_role<PATH, 4>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid, kNpw); break;
+          case 8: producer_role<PATH, 8>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid, kNpw); break;
+          default: producer_role<PATH, 0>(p, sbase, smem, bar_a_full, bar_a_empty, cid, ncl, rank, lane, ptid, kNpw); break;
         }
       }
     }
@@ -2249,7 +2290,7 @@ cudaError_t launch_kernel(const TcParams &p, int nclusters, cudaStream_t stream)
   auto kern = tc_conv_lif_kernel<NCH, PATH, NPART, TRAIN, OCC>;
   cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void *>(kern), (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
-  kern<<<dim3(2 * nclusters), dim3(kernel_threads(NPART)), p.smem_bytes, stream>>>(p);
+  kern<<<dim3(2 * nclusters), dim3(kernel_threads(NPART, OCC)), p.smem_bytes, stream>>>(p);
   return cudaGetLastError();
 }
 

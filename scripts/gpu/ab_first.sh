@@ -1,9 +1,8 @@
-# A/B of variant libraries on the rate-coded first layers (and C5 L0), round robin x2:
-#   bash scripts/gpu/ab_first.sh libtacsnn.so libtacsnn_x.so ...
+# A/B of variant libraries ($LIBS) on the first layers, kernel time from graph replay
 for rep in 1 2; do
-  for c in "C3 0 tac 8 1024" "C2 0 tac 4 256" "C3 0 dense 1 1024" "C2 0 tac 8 256" "C1 0 tac 4 4"; do set -- $c
+  for c in "C3 0 tac 8 1024" "C3 1 tac 8 1024" "C2 0 tac 4 256" "C2 1 tac 4 256" "C3 0 dense 1 1024"; do set -- $c
     for v in $LIBS; do
-      t=$(TACSNN_LIB=paper_2603_13810_b200/$v python scripts/profile_layer.py --config $1 --layer $2 --mode $3 --K $4 --B $5 --iters 6 --no-counts 2>&1 | grep " ms " | tail -3 | awk '{print $1}' | tr '\n' ' ')
+      t=$(TACSNN_LIB=paper_2603_13810_b200/$v python scripts/graph_layer.py --config $1 --layer $2 --mode $3 --K $4 --B $5 2>&1 | grep "graph us" | sed 's/.*launch: //')
       echo "rep $rep $c $v: $t"
     done
   done
