@@ -126,7 +126,7 @@ constexpr int kProdWarps = 3;
 #define TACSNN_BDESC_OPAQUE 1
 #endif
 #ifndef TACSNN_UT_PREFETCH
-#define TACSNN_UT_PREFETCH 1
+#define TACSNN_UT_PREFETCH 0  // 1: double-buffered TMEM loads in the U-in-TMEM loop (round 2: C5 L0 +0.9 %)
 #endif
 #ifndef TACSNN_UT_MIN_NS
 #define TACSNN_UT_MIN_NS 4  // U in TMEM for the fp16 paths from this many LIF steps per group
@@ -1578,7 +1578,10 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
     const bool tok = tile < p.num_tiles;
     const int y = y0 + g, x = x0 + c;
     const bool valid = tok && y < p.Ho && x < p.Wo;
-    const long long vbase = (((long long)b * p.Ho + y) * p.Wo + x) * Cout + co_base;
+    // fp32 [B][H'][W'][C_out] offset of this lane's first channel: only the v_init /
+    // v_final / y_seq paths need it (skipped, with its 64-bit products, otherwise)
+    const long long vbase = (TRAIN || p.v_init || p.v_final)
+                                ? (((long long)b * p.Ho + y) * p.Wo + x) * Cout + co_base : 0;
     const int yo = pooled ? (y >> 1) : y, xo = pooled ? (x >> 1) : x;
     const bool store_lane = valid && active_half && (!pooled || (lane & 9) == 0) && yo < p.Hq && xo < p.Wq;
     const uint32_t vmask = (valid && active_half) ? chmask : 0u;
