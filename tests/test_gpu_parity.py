@@ -284,13 +284,17 @@ def test_reset_variants(T, O, mode, reset, engine):
 
 @pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("reset", ["subtract", "delayed", "hard"])
-def test_v_init_chaining(T, O, reset, engine):
-    """P12 on the device: forward(T) == forward(T1) -> forward(T-T1, v_init=v_final)."""
-    spec = T.LayerSpec(T=8, B=2, C_in=32, H=10, W=10, C_out=32, pad=1, K=2, mode="tactp",
+@pytest.mark.parametrize("shape", ["int8", "fp16_first"])
+def test_v_init_chaining(T, O, reset, engine, shape):
+    """P12 on the device: forward(T) == forward(T1) -> forward(T-T1, v_init=v_final),
+    bitwise on every path (int8 32->32, and the fp16 first-layer path 2->128 with TAC-TP
+    K=4 whose subtract-reset state lives in TMEM)."""
+    cin, cout, K, gain = (32, 32, 2, 1.2) if shape == "int8" else (2, 128, 4, 3.0)
+    spec = T.LayerSpec(T=8, B=2, C_in=cin, H=10, W=10, C_out=cout, pad=1, K=K, mode="tactp",
                        beta=0.5, reset=reset, out_pool=1)
     spec = _engine_or_skip(spec, engine)
-    S = _spikes(12, (8, 2, 32, 10, 10), 0.25)
-    w, b = _w(4, 32, 32, 1.2)
+    S = _spikes(12, (8, 2, cin, 10, 10), 0.25)
+    w, b = _w(4, cout, cin, gain)
     prep = T.prepare_weights(spec, w, b)
     x = T.pack(torch.from_numpy(S).cuda())
     full, vf, _ = T.conv_lif(spec, prep, x, want_v_final=True)
@@ -299,14 +303,9 @@ def test_v_init_chaining(T, O, reset, engine):
     c, vc, _ = T.conv_lif(h, prep, x[4:], v_init=va, want_v_final=True)
     torch.cuda.synchronize()
     assert torch.equal(torch.cat([a, c]), full)
-    # the subtract-reset tcgen05 path keeps U = V - v_th internally, so V crosses the
-    # call boundary with one extra fp32 rounding (U + v_th, then V - v_th): equal up
-    # to a few ulp of max(|V|, v_th); the other paths carry V itself (bit-exact)
-    exact = not (reset == "subtract" and spec.engine_used() == "tcgen05")
-    if exact:
-        assert torch.equal(vc, vf)
-    else:
-        assert torch.allclose(vc, vf, rtol=0, atol=4 * 2.0 ** -23 * max(1.0, vf.abs().max().item()))
+    # every path carries V itself across the call boundary (the tcgen05 subtract-reset
+    # epilogue keeps V scaled by the power of two 2^e, which is exact): bit-exact
+    assert torch.equal(vc, vf)
     # and the chained second half against the oracle with v_init
     P.check_layer(T, O, h, S[4:], w, b, v_init=va.cpu().numpy().transpose(0, 3, 1, 2),
                   label=f"chain/{reset}/{engine}")
