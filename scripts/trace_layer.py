@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--rows", type=int, default=24)
     ap.add_argument("--mode", default=None)
     ap.add_argument("--K", type=int, default=None)
+    ap.add_argument("--npw", type=int, default=3, help="warp-stage producer warps (5 on OCC=2 first layers)")
     a = ap.parse_args()
     cfg = configs.CONFIGS[a.config]
     spec = configs.layer_plan(cfg, mode=a.mode, K=a.K, B=a.B)[a.layer]
@@ -62,11 +63,12 @@ def main():
     print(f"median epi wait (prev done -> full): {np.median(tr[1:n, 4] - tr[:n-1, 6]) / 1e3:.2f} us; "
           f"MMA wait (prev issued -> ready): {np.median(tr[1:n, 2] - tr[:n-1, 3]) / 1e3:.2f} us; "
           f"producer wait (prev done -> start): {np.median(tr[1:n, 0] - tr[:n-1, 1]) / 1e3:.2f} us")
-    # warp-stage producers (first layers): stage it is built by the warp that built it - 3
-    if n > 4:
-        print(f"  per producer warp (stage it vs it-3): raw wait {np.median(tr[3:n, 7] - tr[:n-3, 1]) / 1e3:.2f} us, "
-              f"A-stage wait {np.median(tr[3:n, 0] - tr[3:n, 7]) / 1e3:.2f} us, "
-              f"stage-to-stage {np.median(tr[3:n, 1] - tr[:n-3, 1]) / 1e3:.2f} us")
+    # warp-stage producers (first layers): stage it is built by the warp that built it - npw
+    w = a.npw
+    if n > w + 1:
+        print(f"  per producer warp (stage it vs it-{w}): raw wait {np.median(tr[w:n, 7] - tr[:n-w, 1]) / 1e3:.2f} us, "
+              f"A-stage wait {np.median(tr[w:n, 0] - tr[w:n, 7]) / 1e3:.2f} us, "
+              f"stage-to-stage {np.median(tr[w:n, 1] - tr[:n-w, 1]) / 1e3:.2f} us")
     print(f"  of which prev done -> raw ready: {np.median(tr[1:n, 7] - tr[:n-1, 1]) / 1e3:.2f} us, "
           f"raw ready -> A stage free: {np.median(tr[1:n, 0] - tr[1:n, 7]) / 1e3:.2f} us")
 
