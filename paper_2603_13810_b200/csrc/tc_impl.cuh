@@ -120,7 +120,7 @@ constexpr int kProdWarps = 3;
 #define TACSNN_H16_PACK 1
 #endif
 #ifndef TACSNN_REFILL_EARLY
-#define TACSNN_REFILL_EARLY 1
+#define TACSNN_REFILL_EARLY 0  // 1: the MMA warp refills raw slots before issuing the group (round 2: 0 is -4..-5 % on the int8 layers with the nanosleep backoff, neutral elsewhere)
 #endif
 #ifndef TACSNN_BDESC_OPAQUE
 #define TACSNN_BDESC_OPAQUE 1
