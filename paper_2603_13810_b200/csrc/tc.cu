@@ -340,12 +340,18 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   p.nwo = lp.Cout % 32 == 0 ? lp.Cout / 32 : 1;
   static const bool no_c32w = [] { const char *e = std::getenv("TACSNN_NO_C32W"); return e && *e == '1'; }();
   p.c32w = (!no_c32w && g.path != PATH_HALO && g.cout_pad == 32) ? 1 : 0;
-  // int8 (halo-path) layers: producers, raw loader and MMA issuer back off with nanosleep
-  // while they wait for a free slot, instead of suspend-hint waits that wake on every
-  // barrier event (C5 L2 / L3 / L4 / L5 -6 / -4 / -3 / -3 %); the fp16 first layers keep
-  // the suspend-hint wait (C5 L1 +0.7 % with any backoff).  A/B: TACSNN_SLEEP_NS
+  // Waiting roles (measured per K on C5, scripts/gpu/ab_k.sh, A/B on one box): on the int8
+  // (halo-path) layers with <= 4 LIF steps per group the producers, raw loader and MMA
+  // issuer back off with nanosleep instead of suspend-hint waits that wake on every barrier
+  // event (K=4: C5 L2 -2..-6 %, L3..L5 -3..-4 %; K=2 neutral), and with 4 steps the MMA
+  // warp refills the raw slot after issuing (L3 / L4 -5 %).  With 8 steps per group both
+  // lose (L2 +11 % / +41 %), as does any backoff on the fp16 first layers (+0.6..5 %).
+  // A/B overrides: TACSNN_SLEEP_NS, TACSNN_REFILL_EARLY
+  const bool halo_short = g.path == PATH_HALO && p.nsteps <= 4;
   static const int sleep_env = [] { const char *e = std::getenv("TACSNN_SLEEP_NS"); return e ? std::atoi(e) : -1; }();
-  p.sleep_ns = sleep_env >= 0 ? sleep_env : (g.path == PATH_HALO ? 512 : 0);
+  p.sleep_ns = sleep_env >= 0 ? sleep_env : (halo_short ? 512 : 0);
+  static const int early_env = [] { const char *e = std::getenv("TACSNN_REFILL_EARLY"); return e ? std::atoi(e) : -1; }();
+  p.refill_early = early_env >= 0 ? early_env : ((g.path == PATH_HALO && p.nsteps == 4) ? 0 : 1);
   const bool out_atomic = g.cout_pad < 64 && !p.c32w;  // sub-word or shared-word output fields
   {  // exact s32 combine 254 D_hi + D_lo possible? |A| <= A_max, |q| <= 127, K_red terms
     double a_max = 0;

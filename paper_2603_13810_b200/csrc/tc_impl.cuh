@@ -68,6 +68,7 @@ struct TcParams {
   int prod_refill;            // 1 (plane mode + warp_stage): the warp that consumed raw slot r refills it
   int occ;                    // CTA pairs per SM pair (1, or 2 for small first layers: OCC kernels)
   int c32w;                   // fp16 path, C_out 32: 4 epilogue warps x 32 channels (no atomic sub-word stores)
+  int refill_early;           // 1: the MMA warp refills a consumed raw slot before issuing the group
   int sleep_ns;               // > 0: producers / MMA issuer poll their "free slot" barriers with
                               // nanosleep backoff (mbar_wait_sleep) instead of suspend-hint waits
   int prod_step;              // halo-row stride of the pixel-wise producers: 96, or 32 with warp_stage
@@ -118,9 +119,6 @@ constexpr int kProdWarps = 3;
 #endif
 #ifndef TACSNN_H16_PACK
 #define TACSNN_H16_PACK 1
-#endif
-#ifndef TACSNN_REFILL_EARLY
-#define TACSNN_REFILL_EARLY 0  // 1: the MMA warp refills raw slots before issuing the group (round 2: 0 is -4..-5 % on the int8 layers with the nanosleep backoff, neutral elsewhere)
 #endif
 #ifndef TACSNN_BDESC_OPAQUE
 #define TACSNN_BDESC_OPAQUE 1
@@ -2187,13 +2185,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
             ar.next((uint32_t)p.naccs);
             ptx::mbar_wait(bar_a_full + 8 * s, ph);
             if (lane == 0) trace_mark(p, it, TR_MMA_AFULL);
-#if TACSNN_REFILL_EARLY
             // A-full(it) implies every producer released raw slot it % nraw: refill it now,
-            // before the MMA issue below (which blocks while the tensor queue is full)
-            if (p.use_tma && !p.prod_refill && lane == 0) loader.refill(p, sbase, bar_raw, bar_raw_empty, it, ncl);
+            // before the MMA issue below (which blocks while the tensor queue is full), or
+            // after it (p.refill_early = 0, see tc.cu)
+            if (p.refill_early && p.use_tma && !p.prod_refill && lane == 0)
+              loader.refill(p, sbase, bar_raw, bar_raw_empty, it, ncl);
             __syncwarp();
             if (lane == 0) trace_mark(p, it, TR_MMA_REFILLED);
-#endif
             wait_ahead(p, bar_t_empty + 8 * acc, aph ^ 1u);
             ptx::tc_fence_after();
             if (lane == 0) trace_mark(p, it, TR_MMA_READY);
@@ -2235,10 +2233,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
             }
             __syncwarp();
             if (lane == 0) trace_mark(p, it, TR_MMA_ISSUED);
-#if !TACSNN_REFILL_EARLY
-            if (p.use_tma && !p.prod_refill && lane == 0) loader.refill(p, sbase, bar_raw, bar_raw_empty, it, ncl);
+            if (!p.refill_early && p.use_tma && !p.prod_refill && lane == 0)
+              loader.refill(p, sbase, bar_raw, bar_raw_empty, it, ncl);
             __syncwarp();
-#endif
           }
         }
       }
