@@ -38,9 +38,9 @@
  *   H' = (H+2 pad-R)/stride+1), contiguous.  v_final is V after the last step
  *   (post-reset for SUBTRACT / HARD; R5).  NULL v_init means V=0
  *   (Alg. 1 l.1); with SUBTRACT_DELAYED the pending reset at call start is
- *   [v_init >= v_th] (R4), so chained calls equal one long call (up
- *   to one fp32 rounding of V at the boundary: the tcgen05 subtract-reset path
- *   keeps U = V - v_th internally and converts at v_init / v_final).
+ *   [v_init >= v_th] (R4), so chained calls equal one long call
+ *   bit for bit (every engine carries V itself across the boundary, scaled by
+ *   a power of two at most).
  * counts: u32 [B][C_out] = sum over output steps and PRE-pool pixels of the
  *   spikes (the spike-count readout).
  *

@@ -60,8 +60,9 @@ struct BwdParams {
   int T, B, Cin, H, W, Cout, R, S, stride, pad, K, mode, G, nsteps, Ho, Wo, wpr_in;
   long long in_st, in_sb;  // packed words (spikes) or floats (real input)
   float decay, v_th, coef[kMaxK];
-  // replay of the forward integrator (backward LIF): U-domain (tcgen05 subtract epilogue:
-  // y = (Y + (decay - 1) v_th) s, state U s) or V-domain (y = Y s, state V s); s = 2^e
+  // replay of the forward integrator (backward LIF): the tcgen05 subtract epilogue's form
+  // (udomain: y = (Y - v_th) s, U = decay V + y, V <- U + v_th s [U < 0]) or the plain
+  // V-domain form (y = Y s, V = decay V + y, V <- V - v_th s on a spike); s = 2^e
   int udomain;
   const float *yscale;  // device [s, 1/s] or NULL (= 1)
   // surrogate

@@ -367,8 +367,8 @@ int tc_launch(const tac_conv_lif_desc *d, const LayerParams &lp, const unsigned 
   p.smem_bytes = g.smem_bytes; p.w_bytes_cta = g.w_bytes_cta;
   p.n_total = g.path == PATH_HALO ? 2u * g.cout_pad : (uint32_t)g.cout_pad;  // TMEM columns / acc
   uint32_t cols = 32;
-  const bool ut = g.path != PATH_HALO && g.cout_pad == 128;  // u_in_tmem(): U after the accumulators
-  // accumulators: 3 on the fp16 paths (n_total = C_out_pad; with U in TMEM 3 x 128 +
+  const bool ut = g.path != PATH_HALO && g.cout_pad == 128;  // u_in_tmem(): V after the accumulators
+  // accumulators: 3 on the fp16 paths (n_total = C_out_pad; with V in TMEM 3 x 128 +
   // 128 = 512 columns), 2 on the int8 path (n_total = 2 C_out_pad)
   p.naccs = g.path == PATH_HALO ? 2 : TACSNN_H16_ACCS;
   if (p.warp_stage && g.cout_pad <= 64) p.naccs = kAccs;  // small first layers: deeper TMEM ring

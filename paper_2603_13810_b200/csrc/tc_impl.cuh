@@ -127,7 +127,7 @@ constexpr int kProdWarps = 3;
 #define TACSNN_UT_PREFETCH 0  // 1: double-buffered TMEM loads in the U-in-TMEM loop (round 2: C5 L0 +0.9 %)
 #endif
 #ifndef TACSNN_UT_MIN_NS
-#define TACSNN_UT_MIN_NS 4  // U in TMEM for the fp16 paths from this many LIF steps per group
+#define TACSNN_UT_MIN_NS 4  // V in TMEM for the fp16 paths from this many LIF steps per group
 #endif
 #ifndef TACSNN_UT_UNROLL
 #define TACSNN_UT_UNROLL 4  // chunks per unrolled body of the U-in-TMEM LIF loop (instruction footprint)
@@ -1415,14 +1415,6 @@ __device__ __forceinline__ void lif_step(float &v, float y, float decay, float v
   if (RESET == 1) prev = (prev & ~bitmask) | (~(uint32_t)msk & bitmask);
 }
 
-// f = [U >= 0] = sat(U 2^127 + 1): exactly 0 or 1 for every U (ftz), used by the
-// subtract-reset epilogue (epilogue_sr) as U <- U - v_th f.
-__device__ __forceinline__ float sat_spike(float u) {
-  float f;
-  asm("fma.rn.ftz.sat.f32 %0, %1, 0f7F000000, 0f3F800000;" : "=f"(f) : "f"(u));
-  return f;
-}
-
 // training forward: the drive of one 8-channel chunk as the LIF consumes it -> y_seq
 __device__ __forceinline__ void store_yseq8(const TcParams &p, int k, long long vbase, int cc0, int nvalid,
                                             const float (&y)[8]) {
@@ -1531,8 +1523,8 @@ __device__ __forceinline__ void lif_pair_sr(float2 &v, float2 y, float2 dec2, fl
   }
 }
 
-// UT (fp16 first-layer path with C_out = 128): the membrane state U lives in TMEM
-// columns [2 n_total, 2 n_total + 128) (the accumulators use 2 x 128), and is
+// UT (fp16 first-layer path with C_out = 128): the membrane state V lives in TMEM
+// columns [naccs n_total, naccs n_total + 128) (after the accumulators), and is
 // streamed through registers 8 channels at a time -- 32 registers fewer per thread.
 template <int NCH, int PATH, int NPART>
 constexpr bool u_in_tmem() { return PATH != PATH_HALO && NPART == 4 && NCH == 32; }
@@ -1544,7 +1536,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
   static_assert(NCH <= 32, "one spike word per thread");
   constexpr int NCHUNK = NCH / 8;
   constexpr bool F16 = PATH != PATH_HALO;
-  // (U in TMEM only pays when the K LIF steps per group make registers scarce)
+  // (V in TMEM only pays when the K LIF steps per group make registers scarce)
   constexpr bool UT = u_in_tmem<NCH, PATH, NPART>() && NS >= TACSNN_UT_MIN_NS;
   constexpr int NBUF = (NPART == 2 || (F16 && NS <= 4)) ? 2 : 1;  // TMEM prefetch depth (registers)
   const float *sc = reinterpret_cast<const float *>(smem + p.off_scale);
@@ -1556,7 +1548,7 @@ __device__ __forceinline__ void epilogue_sr(const TcParams &p, uint8_t *smem, ui
   const int co_base = half * NCH;
   const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
   // fp16 paths: TMEM holds Y 2^e (the prescaled operands, tc_prepare); the LIF runs in
-  // the scaled state U 2^e with threshold v_th 2^e -- power-of-two scaling commutes with
+  // the scaled state V 2^e with threshold v_th 2^e -- power-of-two scaling commutes with
   // every fp32 rounding, so spikes and membranes are bitwise those of the unscaled update
   const float ysc = p.ysc, iysc = p.iysc;
   const float2 dec2 = make_float2(p.decay, p.decay), th2 = make_float2(p.vth_s, p.vth_s);
