@@ -126,6 +126,12 @@ constexpr int kProdWarps = 3;
 #ifndef TACSNN_UT_PREFETCH
 #define TACSNN_UT_PREFETCH 0  // 1: double-buffered TMEM loads in the U-in-TMEM loop (round 2: C5 L0 +0.9 %)
 #endif
+#ifndef TACSNN_REGS_LOW4
+#define TACSNN_REGS_LOW4 64    // setmaxnreg of the MMA / producer warps (16 epilogue warps)
+#endif
+#ifndef TACSNN_REGS_HIGH4
+#define TACSNN_REGS_HIGH4 104  // setmaxnreg of the 16 epilogue warps
+#endif
 #ifndef TACSNN_UT_MIN_NS
 #define TACSNN_UT_MIN_NS 4  // V in TMEM for the fp16 paths from this many LIF steps per group
 #endif
@@ -2136,7 +2142,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
   // (threads x kLaunchRegs), or the increase blocks forever.  Each setmaxnreg
   // sits at the top of its role branch so ptxas sees the register regions.
   constexpr uint32_t kLaunchRegs = NPART == 2 ? 168 : 96;  // ptxas allocation at launch
-  constexpr uint32_t kRegsLow = NPART == 2 ? 96 : 64, kRegsHigh = NPART == 2 ? 200 : 104;
+  constexpr uint32_t kRegsLow = NPART == 2 ? 96 : TACSNN_REGS_LOW4, kRegsHigh = NPART == 2 ? 200 : TACSNN_REGS_HIGH4;
   static_assert(32 * (1 + kProdWarps) * kRegsLow + 32 * epi_warps(NPART) * kRegsHigh <=
                     kernel_threads(NPART) * kLaunchRegs, "register budget");
   const uint32_t kMmaWarp = (uint32_t)kEpiWarps;
