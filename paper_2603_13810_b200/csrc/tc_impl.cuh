@@ -132,6 +132,9 @@ constexpr int kProdWarps = 3;
 #ifndef TACSNN_REGS_HIGH4
 #define TACSNN_REGS_HIGH4 104  // setmaxnreg of the 16 epilogue warps
 #endif
+#ifndef TACSNN_EPI_HIGH
+#define TACSNN_EPI_HIGH 1  // 16-epilogue-warp kernels put the epilogue warps on the high warp ids (C5 L1 -0.9 %, L2 -0.5 %)
+#endif
 #ifndef TACSNN_UT_MIN_NS
 #define TACSNN_UT_MIN_NS 4  // V in TMEM for the fp16 paths from this many LIF steps per group
 #endif
@@ -2145,8 +2148,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
   constexpr uint32_t kRegsLow = NPART == 2 ? 96 : TACSNN_REGS_LOW4, kRegsHigh = NPART == 2 ? 200 : TACSNN_REGS_HIGH4;
   static_assert(32 * (1 + kProdWarps) * kRegsLow + 32 * epi_warps(NPART) * kRegsHigh <=
                     kernel_threads(NPART) * kLaunchRegs, "register budget");
-  const uint32_t kMmaWarp = (uint32_t)kEpiWarps;
-  if (warp >= kMmaWarp) {
+  // Warp layout: epilogue warps first (the schedulers favour higher warp ids, so the MMA
+  // and producer warps win issue slots), or -- kEpiHigh, 16-epilogue-warp kernels -- MMA
+  // warp 0, producers 1..3 and the epilogue warps 4..19 on top (the epilogue-bound DVS
+  // first layer).  Either way an epilogue warp's TMEM lane quadrant is warp & 3.
+  constexpr bool kEpiHigh = NPART == 4 && TACSNN_EPI_HIGH;
+  constexpr uint32_t kEpiBase = kEpiHigh ? 1u + (uint32_t)kNpw : 0u;
+  static_assert(kEpiBase % 4 == 0, "epilogue warps must start on a TMEM lane-quadrant boundary");
+  const uint32_t kMmaWarp = kEpiHigh ? 0u : (uint32_t)kEpiWarps;
+  const bool role_warp = kEpiHigh ? warp < kEpiBase : warp >= kMmaWarp;
+  if (role_warp) {
     if constexpr (OCC == 1) ptx::setmaxnreg_dec<kRegsLow>();
     if (warp == kMmaWarp) {
       // ================================ MMA issuer (CTA 0 of the pair) =========
@@ -2240,7 +2251,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
       __syncwarp();
     } else {
       // ================================ producers ================================
-      const int ptid = (int)(threadIdx.x - 32 * (kMmaWarp + 1));
+      const int ptid = (int)(threadIdx.x - 32 * (kMmaWarp + 1));  // producers follow the MMA warp
       if (p.use_tma) {
         switch (p.K) {
           case 1: producer_role_tma<PATH, 1>(p, sbase, smem, bar_a_full, bar_a_empty, bar_raw, bar_raw_empty, cid, ncl, rank, lane, ptid, kNpw); break;
@@ -2266,11 +2277,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
     // ================================ epilogue =================================
     const int ns = p.reset == 0 ? p.nsteps : 0;
     switch (ns) {
-      case 1: epilogue_sr<NCH, PATH, NPART, 1, TRAIN>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      case 2: epilogue_sr<NCH, PATH, NPART, 2, TRAIN>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      case 4: epilogue_sr<NCH, PATH, NPART, 4, TRAIN>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      case 8: epilogue_sr<NCH, PATH, NPART, 8, TRAIN>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
-      default: epilogue_generic<NCH, PATH, NPART, TRAIN>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp, lane); break;
+      case 1: epilogue_sr<NCH, PATH, NPART, 1, TRAIN>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp - kEpiBase, lane); break;
+      case 2: epilogue_sr<NCH, PATH, NPART, 2, TRAIN>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp - kEpiBase, lane); break;
+      case 4: epilogue_sr<NCH, PATH, NPART, 4, TRAIN>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp - kEpiBase, lane); break;
+      case 8: epilogue_sr<NCH, PATH, NPART, 8, TRAIN>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp - kEpiBase, lane); break;
+      default: epilogue_generic<NCH, PATH, NPART, TRAIN>(p, smem, tmem_base, bar_t_full, bar_t_empty, cid, ncl, rank, warp - kEpiBase, lane); break;
     }
     }
 
