@@ -135,6 +135,9 @@ constexpr int kProdWarps = 3;
 #ifndef TACSNN_EPI_HIGH
 #define TACSNN_EPI_HIGH 1  // 16-epilogue-warp kernels put the epilogue warps on the high warp ids (C5 L1 -0.9 %, L2 -0.5 %)
 #endif
+#ifndef TACSNN_EPI_HIGH2
+#define TACSNN_EPI_HIGH2 0  // the same for the 8-epilogue-warp kernels (C3 L2 dense -3 %, TAC +1.5 %: off)
+#endif
 #ifndef TACSNN_UT_MIN_NS
 #define TACSNN_UT_MIN_NS 4  // V in TMEM for the fp16 paths from this many LIF steps per group
 #endif
@@ -2152,7 +2155,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kernel_threads(NPART
   // and producer warps win issue slots), or -- kEpiHigh, 16-epilogue-warp kernels -- MMA
   // warp 0, producers 1..3 and the epilogue warps 4..19 on top (the epilogue-bound DVS
   // first layer).  Either way an epilogue warp's TMEM lane quadrant is warp & 3.
-  constexpr bool kEpiHigh = NPART == 4 && TACSNN_EPI_HIGH;
+  constexpr bool kEpiHigh = (NPART == 4 || (NPART == 2 && TACSNN_EPI_HIGH2)) && kNpw == kProdWarps && TACSNN_EPI_HIGH;
   constexpr uint32_t kEpiBase = kEpiHigh ? 1u + (uint32_t)kNpw : 0u;
   static_assert(kEpiBase % 4 == 0, "epilogue warps must start on a TMEM lane-quadrant boundary");
   const uint32_t kMmaWarp = kEpiHigh ? 0u : (uint32_t)kEpiWarps;
